@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""Benchmark: one DPVO corr+BA iteration (the per-frame hot path) per step.
+
+Default workload = BASELINE config 2, the DPVO default window (96 patches /
+frame, W = 10, r = 13, 22-frame span, 480x640, 128-d features): 16,800 edges.
+A step is: Gram terms of the newest frame, correlation of every active edge
+(coordinates reprojected on the device) and optimize_window's 2 Gauss-Newton
+iterations (frozen targets, Schur, LDLT, retraction, divergence guard), all on
+device-resident inputs.  With --gpus N (torchrun) each rank runs its own
+independent sequence (weak scaling, no collective in the loop; a final NCCL
+gather of poses and stats after the timed region).
+
+Metric: corr+BA edge-iterations/s = E / t_step (whole job: sum over ranks of E
+divided by the max-over-ranks step time).
+
+--impl reference times the reference CPU path (the oracle restatement,
+oracle/, because the reference itself cannot be built here) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "corr+BA edge-iterations/sec and ms/iteration at DPVO default window; % roofline"
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in Path(self.path).read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6 and parts[0].replace(".", "").isdigit():
+                rows.append(parts)
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() in ("active", "1")})
+        sm = [float(r[0]) for r in rows]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- workload
+def corr_bytes_per_edge(prob, K, level_shapes, D=128):
+    """Algorithmic bytes of the correlation per edge: for each
+    level the union of in-bounds integer cells touched by the 3x3x7x7 bilinear
+    taps x D x 4 B, + 2 x 9 x D x 4 B of patch features + 3,528 B of output."""
+    import oracle.pyoracle as orc  # noqa: F401  (not used: coords come from the numpy generator)
+    from paper_2208_04726_b200 import synth
+
+    E = len(prob["e_patch"])
+    total = 0.0
+    poses, src = prob["poses"], prob["patch_src"]
+    per = np.empty(E)
+    rel_cache = {}
+    for e in range(E):
+        k = prob["e_patch"][e]
+        i, j = int(src[k]), int(prob["e_pose"][e])
+        px, py, d = prob["patch_x"][k], prob["patch_y"][k], prob["depth"][k]
+        if np.array_equal(poses[i], poses[j]):
+            u, v = px, py
+        else:
+            if (i, j) not in rel_cache:
+                rel = synth.compose(poses[j], synth.inverse(poses[i]))
+                rel_cache[(i, j)] = (synth._rotmat(rel[:4]), rel[4:])
+            R, t = rel_cache[(i, j)]
+            ray = np.stack([(px - K[2]) / K[0], (py - K[3]) / K[1], np.ones(9)])
+            q = R @ ray + (t * d)[:, None]
+            z = np.maximum(q[2], 1e-6)
+            u, v = K[0] * q[0] / z + K[2], K[1] * q[1] / z + K[3]
+        b = 2 * 9 * D * 4 + 3528
+        for lvl, (H, W) in enumerate(level_shapes):
+            s = 4.0 if lvl == 0 else 16.0
+            fx, fy = np.floor(u / s).astype(int), np.floor(v / s).astype(int)
+            cells = set()
+            for p in range(9):
+                for yy in range(fy[p] - 3, fy[p] + 5):
+                    if 0 <= yy < H:
+                        for xx in range(fx[p] - 3, fx[p] + 5):
+                            if 0 <= xx < W:
+                                cells.add((xx, yy))
+            b += len(cells) * D * 4
+        per[e] = b
+        total += b
+    return total, per
+
+
+def setup(config: str, seed: int, device: int):
+    import torch
+
+    import paper_2208_04726_b200 as pvo
+    from paper_2208_04726_b200 import synth
+
+    w = synth.generate(config, seed=seed)
+    g = synth.build_graph(w, pvo.PatchGraph)
+    prob = synth.window_arrays(w, g.window_problem(w.cfg["window"]))
+    ctx = pvo.Context(device)
+    stream = torch.cuda.Stream(device=device)
+    ctx.set_stream(stream.cuda_stream)
+    F = w.cfg["frames"]
+    _, H0, W0, D = w.level0.shape
+    _, H1, W1, _ = w.level1.shape
+    ctx.frames_reserve(F, W0, H0, W1, H1, D)
+    for f in range(F):
+        ctx.frames_upload(f, w.level0[f], w.level1[f])
+    win = pvo.Window(ctx)
+    win.load(prob, prob["pose_frames"], prob["patch_feats"], w.K, w.image)
+    ctx.synchronize()
+    return w, prob, ctx, stream, win
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle.pyoracle as orc
+    from paper_2208_04726_b200 import synth
+
+    w = synth.generate(args.config, seed=0)
+    og = synth.build_graph(w, orc.PatchGraph)
+    prob = og.window_problem(w.cfg["window"])
+    E = len(prob["e_patch"])
+    threads = os.cpu_count() or 1
+    sample = min(E, args.ref_edges)
+    coords = np.empty((sample, 9, 2))
+    for e in range(sample):
+        k = prob["e_patch"][e]
+        coords[e], _ = orc.reproject_patch(prob["poses"][prob["patch_src"][k]], prob["poses"][prob["e_pose"][e]],
+                                           w.K, prob["patch_x"][k], prob["patch_y"][k], prob["depth"][k])
+    pf = w.patch_feats[prob["patch_ids"]]
+    slots = prob["pose_frames"][prob["e_pose"][:sample]]
+
+    def one_step():
+        t0 = time.perf_counter()
+        orc.correlate_batch(prob["e_patch"][:sample], slots, coords, pf, w.level0, w.level1, threads=threads)
+        t1 = time.perf_counter()
+        og2 = synth.build_graph(w, orc.PatchGraph)
+        t2 = time.perf_counter()
+        og2.optimize_window(window=w.cfg["window"], iterations=2)
+        t3 = time.perf_counter()
+        return (t1 - t0) / sample * E, t3 - t2
+
+    for _ in range(args.warmup):
+        one_step()
+    times = [one_step() for _ in range(args.steps)]
+    step_s = float(np.mean([a + b for a, b in times]))
+    value = E / step_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "edge-iterations/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
+        "config": {"workload": args.config, "edges": E, "window": w.cfg["window"], "radius": w.cfg["radius"],
+                   "patches_per_frame": w.cfg["patches"], "channels": 128},
+        "cpu_baseline": {"value": value, "unit": "edge-iterations/s", "cores": threads, "kind": "port",
+                         "sample": f"correlate() over the first {sample} of {E} edges on {threads} threads "
+                                   f"(extrapolated to all edges) + full optimize_window(2 iterations, dense H, "
+                                   f"single-threaded as in the reference); oracle/pvo_oracle.cpp -O3"},
+        "e2e": {"value": value, "unit": "edge-iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "corr_ms": float(np.mean([a for a, _ in times])) * 1e3, "ba_ms": float(np.mean([b for _, b in times])) * 1e3,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(w, prob, sample_edges=600):
+    """Oracle timed on the host: corr single-threaded on a bounded sample (the
+    reference is single-threaded) + full optimize_window(2)."""
+    import oracle.pyoracle as orc
+    from paper_2208_04726_b200 import synth
+
+    E = len(prob["e_patch"])
+    sample = min(E, sample_edges)
+    coords = np.empty((sample, 9, 2))
+    for e in range(sample):
+        k = prob["e_patch"][e]
+        coords[e], _ = orc.reproject_patch(prob["poses"][prob["patch_src"][k]], prob["poses"][prob["e_pose"][e]],
+                                           w.K, prob["patch_x"][k], prob["patch_y"][k], prob["depth"][k])
+    slots = prob["pose_frames"][prob["e_pose"][:sample]]
+    t0 = time.perf_counter()
+    orc.correlate_batch(prob["e_patch"][:sample], slots, coords, prob["patch_feats"], w.level0, w.level1, threads=1)
+    t_corr = (time.perf_counter() - t0) / sample * E
+    og = synth.build_graph(w, orc.PatchGraph)
+    t0 = time.perf_counter()
+    og.optimize_window(window=w.cfg["window"], iterations=2)
+    t_ba = time.perf_counter() - t0
+    return {"value": E / (t_corr + t_ba), "unit": "edge-iterations/s", "cores": 1, "kind": "port",
+            "sample": f"correlate() on {sample}/{E} edges (1 thread, extrapolated) + optimize_window(2) in full; "
+                      f"corr {t_corr * 1e3:.0f} ms + BA {t_ba * 1e3:.0f} ms per iteration"}
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    w, prob, ctx, stream, win = setup(args.config, seed=rank, device=local_rank)
+    E = win.n_edges
+    F = w.cfg["frames"]
+    newest = F - 1
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local_rank}")
+
+    def step():
+        win.reset()
+        ctx.frames_refresh(newest)
+        win.iteration(2)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            flush.zero_()
+            step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    launches0 = ctx.kernel_launches
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kt = []
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter()
+    with torch.cuda.stream(stream):
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush between steps, outside the timed events
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+            kt.append(ctx.last_timing())
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall
+    launches = ctx.kernel_launches - launches0
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    mean_ms = float(np.mean(step_ms))
+    corr_ms = float(np.mean([k[0] for k in kt]))
+    ba_ms = float(np.mean([k[1] for k in kt]))
+
+    # max over ranks
+    t = torch.tensor([mean_ms, corr_ms, ba_ms], dtype=torch.float64, device=f"cuda:{local_rank}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    mean_ms, corr_ms_max, ba_ms_max = t.tolist()
+
+    # e2e through the public API with host buffers (our own sequence, rank-local)
+    e2e = run_e2e(args, w, prob, ctx, stream, win)
+    if world > 1:
+        te = torch.tensor([e2e["ms"]], dtype=torch.float64, device=f"cuda:{local_rank}")
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e["ms"] = te.item()
+
+    # final gather of poses + stats (the only collective)
+    poses, depth, norms = win.read()
+    if world > 1:
+        pt = torch.tensor(poses, device=f"cuda:{local_rank}")
+        gathered = [torch.empty_like(pt) for _ in range(world)]
+        dist.all_gather(gathered, pt)
+
+    if rank != 0:
+        return
+    hbm, peak_kind = load_peaks()
+    total_b, _ = corr_bytes_per_edge(prob, w.K, [w.level0.shape[1:3], w.level1.shape[1:3]])
+    achieved = total_b / (corr_ms * 1e-3) / 1e9
+    prof = ROOT / "profiles" / "corr_traffic.json"
+    traffic = None
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get(args.config)
+    cpu = cpu_baseline(w, prob) if (world == 1 and not args.no_cpu) else None
+    value = E * world / (mean_ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": "edge-iterations/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 corr (f64 coords/weights), f64 BA", "data": "synthetic",
+        "config": {"workload": args.config, "desc": w.cfg["desc"], "edges_per_gpu": E, "window": w.cfg["window"],
+                   "radius": w.cfg["radius"], "patches_per_frame": w.cfg["patches"], "channels": 128,
+                   "ba_iterations": 2, "sequences": world, "parallelism": f"sequence-sharded x{world}",
+                   "l2": "flushed between steps (256 MiB write, outside the timed events)"},
+        "corr_ms": corr_ms_max, "ba_ms": ba_ms_max,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": traffic, "kernel": "corr_kernel", "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": total_b},
+        "e2e": {"value": E * world / (e2e["ms"] * 1e-3), "unit": "edge-iterations/s",
+                "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"], "ms_per_step": e2e["ms"]},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "wall_s_timed_region": t_wall,
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+
+
+def run_e2e(args, w, prob, ctx, stream, win):
+    """Same step through the public API with HOST buffers: upload the newest
+    frame's pyramid and the window state, run, read back the corr volume and
+    the BA result — copies inside the timed region."""
+    import torch
+
+    E = win.n_edges
+    l0 = torch.from_numpy(w.level0[-1]).pin_memory()
+    l1 = torch.from_numpy(w.level1[-1]).pin_memory()
+    vol = torch.empty((E, 2, 9, 7, 7), dtype=torch.float32).pin_memory()
+    vol_np = vol.numpy()
+    F = w.cfg["frames"]
+    arrays = [prob["poses"], prob["fixed"], prob["pose_frames"], prob["patch_src"], prob["patch_x"],
+              prob["patch_y"], prob["depth"], prob["patch_feats"], prob["e_patch"], prob["e_pose"], prob["e_delta"],
+              prob["e_weight"]]
+    h2d = l0.numel() * 4 + l1.numel() * 4 + sum(np.asarray(a).nbytes for a in arrays)
+    d2h = vol.numel() * 4 + prob["poses"].nbytes + prob["depth"].nbytes + 8 * 3
+
+    def one():
+        ctx.frames_upload(F - 1, l0.numpy(), l1.numpy())
+        win.load(prob, prob["pose_frames"], prob["patch_feats"], w.K, w.image)
+        win.iteration(2, corr_out=vol_np)
+        return win.read()
+
+    for _ in range(max(1, args.warmup)):
+        one()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    n = max(1, min(args.steps, 20))
+    for _ in range(n):
+        one()
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) / n * 1e3
+    return {"ms": ms, "h2d": int(h2d), "d2h": int(d2h)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--ref-edges", type=int, default=2000)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

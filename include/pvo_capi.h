@@ -1,0 +1,207 @@
+/*
+ * pvo_capi.h — C-ABI of the B200-native DPVO geometric hot path.
+ *
+ * This is the drop-in boundary.  Every entry point replaces one operator of
+ * the reference's C++ API in /root/reference/proj/include/pvo (cited per
+ * function as file:line) with plain pointers and sizes: no Eigen, no torch,
+ * no C++ types.  Exceptions cannot cross extern "C", so each entry returns a
+ * pvo_status that maps 1:1 onto the reference's exception types, and the
+ * message is available from pvo_last_error() (thread-local) — see
+ * include/pvo/ (C++ headers) for the C++ wrappers that rethrow the same types.
+ *
+ * Conventions shared by every entry point
+ *   pose      7 doubles: quaternion (x, y, z, w) then translation (x, y, z);
+ *             world -> camera, Eigen coefficient order (se3.hpp:38-61).
+ *   K         4 doubles: fx, fy, cx, cy (camera.hpp:10-23).
+ *   patch     p*p x-coordinates and p*p y-coordinates, row-major
+ *             (camera.hpp:29-38); the GPU kernels require p == 3.
+ *   features  HWC fp32, data[(y*W + x)*C + c]  (features.hpp:14-36).
+ *   corr out  [2][p*p][7][7] fp32 per edge, index ((v*p+u)*7+alpha)*7+beta
+ *             (correlation.hpp:17-26).
+ *   memspace  PVO_HOST (pageable or pinned host memory, copied inside the
+ *             call) or PVO_DEVICE (device pointers, stream-ordered).
+ * All compute runs on the GPU owned by the context; there is no CPU
+ * fallback: without a usable sm_100 device every compute entry returns
+ * PVO_CUDA_ERROR.
+ */
+#ifndef PVO_CAPI_H
+#define PVO_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PVO_OK = 0,
+    PVO_INVALID_ARGUMENT = 1, /* std::invalid_argument                          */
+    PVO_DEGENERATE = 2,       /* pvo::DegenerateProblem (bundle_adjust.hpp:54-56) */
+    PVO_DOMAIN_ERROR = 3,     /* std::domain_error (se3.cpp:58-60)                */
+    PVO_OUT_OF_RANGE = 4,     /* std::out_of_range (map::at)                      */
+    PVO_CUDA_ERROR = 5,       /* device / driver failure                          */
+    PVO_UNSUPPORTED = 6       /* shape outside what the kernels implement         */
+} pvo_status;
+
+enum { PVO_HOST = 0, PVO_DEVICE = 1 };
+
+typedef struct pvo_ctx pvo_ctx;     /* device, stream, scratch arena, frame store */
+typedef struct pvo_graph pvo_graph; /* host PatchGraph (patch_graph.hpp:66-136)   */
+
+/* ---- library / context ------------------------------------------------- */
+int pvo_version(void);
+const char* pvo_last_error(void);
+const char* pvo_status_string(int status);
+int pvo_ctx_create(int device, pvo_ctx** out);
+int pvo_ctx_destroy(pvo_ctx* ctx);
+/* Run on an external cudaStream_t (e.g. torch's current stream); NULL = own stream. */
+int pvo_ctx_set_stream(pvo_ctx* ctx, void* cuda_stream);
+int pvo_ctx_synchronize(pvo_ctx* ctx);
+/* Number of kernels this context has launched (profiling / gpu_launches). */
+int64_t pvo_ctx_kernel_launches(pvo_ctx* ctx);
+/* Device-side timing of the last pvo_window_iteration: corr ms, BA ms. */
+int pvo_ctx_last_timing(pvo_ctx* ctx, double* corr_ms, double* ba_ms);
+
+/* ---- SE(3) (se3.hpp:63-77), host utilities shared with the kernels ------ */
+int pvo_se3_exp(const double* xi6, double* pose7);
+int pvo_se3_log(const double* pose7, double* xi6);
+int pvo_se3_compose(const double* a7, const double* b7, double* out7);
+int pvo_se3_inverse(const double* a7, double* out7);
+int pvo_se3_retract(const double* a7, const double* xi6, double* out7);
+
+/* ---- camera (camera.hpp:56-72), batched on the GPU -------------------------
+ * pvo_reproject_patches: n items; item i reprojects patch (x[i*pp..], y[i*pp..],
+ * inv_depth[i]) from pose_i[i] into pose_j[i].  out_xy [n][pp][2], behind [n].
+ * Keeps the bitwise-equal-pose shortcut of camera.cpp:52-57.
+ * pvo_reprojection_jacobians: out [n][28] = center(2), d_pose_i (2x6 row-major),
+ * d_pose_j (2x6), d_inverse_depth (2); behind [n].  (camera.cpp:73-108)   */
+int pvo_reproject_patches(pvo_ctx* ctx, int n, int p, const double* poses_i, const double* poses_j,
+                          const double* K, const double* x, const double* y, const double* inv_depth,
+                          double* out_xy, uint8_t* behind);
+int pvo_reprojection_jacobians(pvo_ctx* ctx, int n, int p, const double* poses_i, const double* poses_j,
+                               const double* K, const double* x, const double* y, const double* inv_depth,
+                               double* out, uint8_t* behind);
+
+/* ---- correlation (correlation.hpp:33-44) ----------------------------------
+ * pvo_correlate: one patch against one host pyramid (the reference signature,
+ * correlation.cpp:37-71).  feats0/feats1: [p*p][C]; coords [p*p][2].
+ * Throws (returns) INVALID_ARGUMENT on non-finite coordinates.            */
+int pvo_correlate(pvo_ctx* ctx, int p, int channels, const float* feats0, const float* feats1,
+                  const float* level0, int w0, int h0, const float* level1, int w1, int h1,
+                  const double* coords, float* out);
+
+/* Frame store: device-resident pyramids for n_frames slots, plus the per-cell
+ * Gram terms the normalised correlation needs (computed at upload).
+ * Replaces provider-owned FeaturePyramid storage (flow_provider.hpp:108).  */
+int pvo_frames_reserve(pvo_ctx* ctx, int n_frames, int w0, int h0, int w1, int h1, int channels);
+int pvo_frames_upload(pvo_ctx* ctx, int slot, const float* level0, const float* level1, int memspace);
+/* Re-derive the Gram terms of one slot (after writing features in place). */
+int pvo_frames_refresh(pvo_ctx* ctx, int slot);
+/* Device pointers of the store (for zero-copy producers). */
+int pvo_frames_device_ptrs(pvo_ctx* ctx, float** level0, float** level1);
+
+/* pvo_correlate_batch: the batched form of correlate() over E edges.
+ * e_patch[E] indexes patch_feats [P][2][pp][C]; e_slot[E] is the frame-store
+ * slot of the target frame; coords [E][pp][2].  out [E][2][pp][7][7].
+ * All arrays in `memspace`.                                                */
+int pvo_correlate_batch(pvo_ctx* ctx, int n_edges, int n_patches, int p, const int* e_patch,
+                        const int* e_slot, const double* coords, const float* patch_feats, float* out,
+                        int memspace);
+
+/* ---- bundle adjustment (bundle_adjust.hpp:20-111) --------------------------
+ * Flattened BAProblem (bundle_adjust.hpp:30-40):
+ *   poses [n_poses][7], pose_fixed [n_poses]
+ *   patch_src [n_patches] (pose index), patch_x/patch_y [n_patches][pp],
+ *   inv_depth [n_patches], depth_free [n_patches] or NULL (= all free)
+ *   e_patch, e_pose [n_edges], e_target [n_edges][2], e_weight [n_edges][2]
+ * Outputs: out_poses [n_poses][7] (fixed entries bit-identical),
+ * out_depth [n_patches], residual_norms (1 + iterations entries).        */
+
+/* gauss_newton_step (bundle_adjust.cpp:117-223).  residual_norms[2].
+ * debug_h ((np+nd)^2, row-major) / debug_b (np+nd) may be NULL; when given
+ * they receive the damped normal equations (NormalEquations, :65-72).    */
+int pvo_gauss_newton_step(pvo_ctx* ctx, int n_poses, const double* poses, const uint8_t* pose_fixed,
+                          int n_patches, int p, const int* patch_src, const double* patch_x,
+                          const double* patch_y, const double* inv_depth, const uint8_t* depth_free,
+                          int n_edges, const int* e_patch, const int* e_pose, const double* e_target,
+                          const double* e_weight, const double* K, double damping, double* out_poses,
+                          double* out_depth, double* residual_norms, double* debug_h, double* debug_b,
+                          int* n_free_poses, int* n_free_depths);
+
+/* schur_solve (bundle_adjust.cpp:62-94), dense row-major inputs:
+ * hpp [np][np], hpd [np][nd], hdd [nd], bp [np], bd [nd] -> dp [np], dd [nd]. */
+int pvo_schur_solve(pvo_ctx* ctx, int np, int nd, const double* hpp, const double* hpd, const double* hdd,
+                    const double* bp, const double* bd, double* dp, double* dd);
+
+/* The iteration loop of optimize_window on an already-flattened problem
+ * (bundle_adjust.cpp:309-366): structure-only steps, damped GN steps with
+ * the divergence guard (x1e3, x1e6, x1e9 retries), all on the device.
+ * freeze_targets != 0: e_target holds the revision delta and the frozen
+ * target / observability weight are derived on the device exactly as
+ * bundle_adjust.cpp:288-307 does (needs image_w/h).                        */
+int pvo_ba_window(pvo_ctx* ctx, int n_poses, const double* poses, const uint8_t* pose_fixed, int n_patches,
+                  int p, const int* patch_src, const double* patch_x, const double* patch_y,
+                  const double* inv_depth, int n_edges, const int* e_patch, const int* e_pose,
+                  const double* e_target, const double* e_weight, const double* K, int image_w, int image_h,
+                  int freeze_targets, double damping, int iterations, int structure_only, double* out_poses,
+                  double* out_depth, double* residual_norms, int* n_norms);
+
+/* ---- resident window: the per-frame hot path ------------------------------
+ * pvo_window_load uploads one active window (the flattened optimize_window
+ * problem with revision deltas, freeze_targets semantics) plus per-patch
+ * features and the pose -> frame-store slot map, and keeps it on the device.
+ * pvo_window_iteration runs  corr(all edges, coords = reproject at the current
+ * state) + optimize_window(iterations) on it, entirely stream-ordered; no
+ * host synchronisation inside.  pvo_window_read copies the state back.    */
+int pvo_window_load(pvo_ctx* ctx, int n_poses, const double* poses, const uint8_t* pose_fixed,
+                    const int* pose_slot, int n_patches, int p, const int* patch_src, const double* patch_x,
+                    const double* patch_y, const double* inv_depth, const float* patch_feats, int n_edges,
+                    const int* e_patch, const int* e_pose, const double* e_delta, const double* e_weight,
+                    const double* K, int image_w, int image_h, int memspace);
+/* Restore poses / depths of the loaded window (memspace as given). */
+int pvo_window_set_state(pvo_ctx* ctx, const double* poses, const double* inv_depth, int memspace);
+int pvo_window_iteration(pvo_ctx* ctx, int iterations, double damping, float* corr_out, int corr_memspace);
+int pvo_window_correlate(pvo_ctx* ctx, float* corr_out, int memspace);
+int pvo_window_read(pvo_ctx* ctx, double* poses, double* inv_depth, double* residual_norms, int* n_norms);
+/* Device pointer of the window's correlation volume buffer [E][2][pp][49]. */
+int pvo_window_corr_ptr(pvo_ctx* ctx, float** corr);
+
+/* ---- patch graph (patch_graph.hpp:66-136), host C++ ------------------------ */
+int pvo_graph_create(const double* K, int image_w, int image_h, int patch_width, pvo_graph** out);
+int pvo_graph_destroy(pvo_graph* g);
+int pvo_graph_add_frame(pvo_graph* g, double timestamp, const double* pose, int* out_index);
+int pvo_graph_add_patches(pvo_graph* g, int frame, int n, const double* centroids, const double* inv_depths,
+                          int* out_ids);
+int pvo_graph_connect(pvo_graph* g, int radius, int* n_added);
+int pvo_graph_remove_frame(pvo_graph* g, int frame);
+int pvo_graph_set_revision(pvo_graph* g, int patch_id, int frame, const double* delta, const double* weight);
+int pvo_graph_set_pose(pvo_graph* g, int frame, const double* pose);
+int pvo_graph_set_inverse_depth(pvo_graph* g, int patch_id, double inv_depth);
+int pvo_graph_num_frames(pvo_graph* g);
+int pvo_graph_num_patches(pvo_graph* g);
+int pvo_graph_num_edges(pvo_graph* g);
+/* Edges in reference key order (patch id, then frame index); rev [E][4] =
+ * dx dy wx wy, zeros when unset (dump_edges, patch_graph.cpp:144-151).   */
+int pvo_graph_edges(pvo_graph* g, int* kk, int* jj, double* rev, uint8_t* has_rev);
+int pvo_graph_frames(pvo_graph* g, int* indices, double* poses);
+int pvo_graph_patches(pvo_graph* g, int* ids, int* src, double* inv_depth);
+/* Pipeline::active_edges (pipeline.cpp:164-181); sizes first with NULL arrays. */
+int pvo_graph_active_edges(pvo_graph* g, int window, int* kk, int* jj, int* n);
+/* build_target (bundle_adjust.cpp:47-60). */
+int pvo_graph_build_target(pvo_graph* g, int patch_id, int frame, double* out2);
+/* The optimize_window problem build (bundle_adjust.cpp:231-307) flattened;
+ * sizes first with NULL arrays.  e_target receives the frozen targets.    */
+int pvo_graph_window_problem(pvo_graph* g, int window, int* n_poses, int* n_patches, int* n_edges,
+                             int* pose_frames, double* poses, uint8_t* fixed, int* patch_ids, int* patch_src,
+                             double* patch_x, double* patch_y, double* inv_depth, int* e_patch, int* e_pose,
+                             double* e_target, double* e_weight);
+/* optimize_window (bundle_adjust.cpp:225-375): flatten on the host, iterate
+ * on the device, write poses / depths back into the graph.              */
+int pvo_optimize_window(pvo_ctx* ctx, pvo_graph* g, int window, int iterations, int structure_only,
+                        double damping, double* residual_norms, int* n_norms, int* num_edges);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PVO_CAPI_H */

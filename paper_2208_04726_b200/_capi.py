@@ -1,0 +1,99 @@
+"""ctypes declarations of the C-ABI in include/pvo_capi.h.
+
+Loads the in-tree ``libpvo_b200.so`` (built by ``build.py``).  There is no
+fallback: if the library is missing the import raises, and every compute
+entry returns PVO_CUDA_ERROR without an sm_100 device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+_LIB_PATH = Path(__file__).resolve().parent / "libpvo_b200.so"
+
+PVO_OK = 0
+PVO_INVALID_ARGUMENT = 1
+PVO_DEGENERATE = 2
+PVO_DOMAIN_ERROR = 3
+PVO_OUT_OF_RANGE = 4
+PVO_CUDA_ERROR = 5
+PVO_UNSUPPORTED = 6
+PVO_HOST = 0
+PVO_DEVICE = 1
+
+i32, i64, f64, vp = C.c_int, C.c_int64, C.c_double, C.c_void_p
+P = vp  # every array argument is passed as a raw address
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "pvo_version": (i32, []),
+    "pvo_last_error": (C.c_char_p, []),
+    "pvo_status_string": (C.c_char_p, [i32]),
+    "pvo_ctx_create": (i32, [i32, C.POINTER(vp)]),
+    "pvo_ctx_destroy": (i32, [vp]),
+    "pvo_ctx_set_stream": (i32, [vp, vp]),
+    "pvo_ctx_synchronize": (i32, [vp]),
+    "pvo_ctx_kernel_launches": (i64, [vp]),
+    "pvo_ctx_last_timing": (i32, [vp, P, P]),
+    "pvo_se3_exp": (i32, [P, P]),
+    "pvo_se3_log": (i32, [P, P]),
+    "pvo_se3_compose": (i32, [P, P, P]),
+    "pvo_se3_inverse": (i32, [P, P]),
+    "pvo_se3_retract": (i32, [P, P, P]),
+    "pvo_reproject_patches": (i32, [vp, i32, i32, P, P, P, P, P, P, P, P]),
+    "pvo_reprojection_jacobians": (i32, [vp, i32, i32, P, P, P, P, P, P, P, P]),
+    "pvo_correlate": (i32, [vp, i32, i32, P, P, P, i32, i32, P, i32, i32, P, P]),
+    "pvo_frames_reserve": (i32, [vp, i32, i32, i32, i32, i32, i32]),
+    "pvo_frames_upload": (i32, [vp, i32, P, P, i32]),
+    "pvo_frames_refresh": (i32, [vp, i32]),
+    "pvo_frames_device_ptrs": (i32, [vp, P, P]),
+    "pvo_correlate_batch": (i32, [vp, i32, i32, i32, P, P, P, P, P, i32]),
+    "pvo_gauss_newton_step": (i32, [vp, i32, P, P, i32, i32, P, P, P, P, P, i32, P, P, P, P, P, f64,
+                                    P, P, P, P, P, P, P]),
+    "pvo_schur_solve": (i32, [vp, i32, i32, P, P, P, P, P, P, P]),
+    "pvo_ba_window": (i32, [vp, i32, P, P, i32, i32, P, P, P, P, i32, P, P, P, P, P, i32, i32, i32, f64,
+                            i32, i32, P, P, P, P]),
+    "pvo_window_load": (i32, [vp, i32, P, P, P, i32, i32, P, P, P, P, P, i32, P, P, P, P, P, i32, i32, i32]),
+    "pvo_window_set_state": (i32, [vp, P, P, i32]),
+    "pvo_window_iteration": (i32, [vp, i32, f64, P, i32]),
+    "pvo_window_correlate": (i32, [vp, P, i32]),
+    "pvo_window_read": (i32, [vp, P, P, P, P]),
+    "pvo_window_corr_ptr": (i32, [vp, P]),
+    "pvo_graph_create": (i32, [P, i32, i32, i32, C.POINTER(vp)]),
+    "pvo_graph_destroy": (i32, [vp]),
+    "pvo_graph_add_frame": (i32, [vp, f64, P, P]),
+    "pvo_graph_add_patches": (i32, [vp, i32, i32, P, P, P]),
+    "pvo_graph_connect": (i32, [vp, i32, P]),
+    "pvo_graph_remove_frame": (i32, [vp, i32]),
+    "pvo_graph_set_revision": (i32, [vp, i32, i32, P, P]),
+    "pvo_graph_set_pose": (i32, [vp, i32, P]),
+    "pvo_graph_set_inverse_depth": (i32, [vp, i32, f64]),
+    "pvo_graph_num_frames": (i32, [vp]),
+    "pvo_graph_num_patches": (i32, [vp]),
+    "pvo_graph_num_edges": (i32, [vp]),
+    "pvo_graph_edges": (i32, [vp, P, P, P, P]),
+    "pvo_graph_frames": (i32, [vp, P, P]),
+    "pvo_graph_patches": (i32, [vp, P, P, P]),
+    "pvo_graph_active_edges": (i32, [vp, i32, P, P, P]),
+    "pvo_graph_build_target": (i32, [vp, i32, i32, P]),
+    "pvo_graph_window_problem": (i32, [vp, i32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P]),
+    "pvo_optimize_window": (i32, [vp, vp, i32, i32, i32, f64, P, P, P]),
+}
+
+
+def load(path: Path | str | None = None) -> C.CDLL:
+    p = Path(path) if path else _LIB_PATH
+    if not p.exists():
+        raise ImportError(
+            f"{p} is missing: build the sm_100a library first "
+            "(python -m paper_2208_04726_b200.build); there is no CPU fallback"
+        )
+    lib = C.CDLL(str(p))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = load()

@@ -1,0 +1,621 @@
+"""Python mirror of the reference operator API over the C-ABI.
+
+Names and argument meaning follow /root/reference/proj/include/pvo:
+``reproject_patch`` / ``reprojection_jacobians`` (camera.hpp:56-72),
+``correlate`` (correlation.hpp:33-34), ``gauss_newton_step`` /
+``schur_solve`` / ``optimize_window`` / ``build_target``
+(bundle_adjust.hpp:62-111) and ``PatchGraph`` (patch_graph.hpp:66-136).
+Errors are raised as the exception types the reference throws
+(``ValueError`` for std::invalid_argument, ``DegenerateProblem`` for
+pvo::DegenerateProblem, ``ArithmeticError`` for std::domain_error,
+``IndexError`` for std::out_of_range).
+
+Every numeric result comes from the sm_100a kernels behind the C-ABI; this
+module only marshals numpy arrays.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _capi
+from ._capi import lib
+
+# ---------------------------------------------------------------------------
+# errors
+# ---------------------------------------------------------------------------
+
+
+class DegenerateProblem(RuntimeError):
+    """pvo::DegenerateProblem (bundle_adjust.hpp:54-56)."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class Unsupported(NotImplementedError):
+    pass
+
+
+_EXC = {
+    _capi.PVO_INVALID_ARGUMENT: ValueError,
+    _capi.PVO_DEGENERATE: DegenerateProblem,
+    _capi.PVO_DOMAIN_ERROR: ArithmeticError,
+    _capi.PVO_OUT_OF_RANGE: IndexError,
+    _capi.PVO_CUDA_ERROR: CudaError,
+    _capi.PVO_UNSUPPORTED: Unsupported,
+}
+
+
+def check(status: int) -> None:
+    if status != _capi.PVO_OK:
+        msg = lib.pvo_last_error().decode(errors="replace")
+        raise _EXC.get(status, RuntimeError)(msg)
+
+
+def _f64(a, shape=None) -> np.ndarray:
+    out = np.ascontiguousarray(a, dtype=np.float64)
+    return out.reshape(shape) if shape is not None else out
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _u8(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.uint8)
+
+
+def _ptr(a: Optional[np.ndarray]):
+    # `a.ctypes` (not `.data`) keeps a temporary array alive during the call
+    return None if a is None else a.ctypes
+
+
+# ---------------------------------------------------------------------------
+# context
+# ---------------------------------------------------------------------------
+
+
+class Context:
+    """Device + stream + scratch arena + frame store (one per host thread)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib.pvo_ctx_create(device, C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def close(self) -> None:
+        if self.handle:
+            lib.pvo_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, cuda_stream: int | None) -> None:
+        check(lib.pvo_ctx_set_stream(self.handle, cuda_stream or None))
+
+    def synchronize(self) -> None:
+        check(lib.pvo_ctx_synchronize(self.handle))
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(lib.pvo_ctx_kernel_launches(self.handle))
+
+    def last_timing(self) -> tuple[float, float]:
+        a, b = C.c_double(), C.c_double()
+        check(lib.pvo_ctx_last_timing(self.handle, C.addressof(a), C.addressof(b)))
+        return a.value, b.value
+
+    # ---- frame store ----
+    def frames_reserve(self, n_frames: int, w0: int, h0: int, w1: int, h1: int, channels: int) -> None:
+        check(lib.pvo_frames_reserve(self.handle, n_frames, w0, h0, w1, h1, channels))
+        self.frame_shape = (w0, h0, w1, h1, channels)
+
+    def frames_upload(self, slot: int, level0, level1, device: bool = False) -> None:
+        if device:  # torch tensors / raw device pointers
+            p0 = level0 if isinstance(level0, int) else level0.data_ptr()
+            p1 = level1 if isinstance(level1, int) else level1.data_ptr()
+            check(lib.pvo_frames_upload(self.handle, slot, p0, p1, _capi.PVO_DEVICE))
+            return
+        l0, l1 = _f32(level0), _f32(level1)
+        check(lib.pvo_frames_upload(self.handle, slot, _ptr(l0), _ptr(l1), _capi.PVO_HOST))
+
+    def frames_refresh(self, slot: int) -> None:
+        check(lib.pvo_frames_refresh(self.handle, slot))
+
+
+_default: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default
+    if _default is None:
+        _default = Context(0)
+    return _default
+
+
+def _ctx(ctx: Optional[Context]) -> Context:
+    return ctx if ctx is not None else default_context()
+
+
+# ---------------------------------------------------------------------------
+# SE(3) (se3.hpp:63-77): 7-vectors (qx qy qz qw tx ty tz), 6-vector twists
+# ---------------------------------------------------------------------------
+
+
+def se3_exp(xi) -> np.ndarray:
+    x, out = _f64(xi, (6,)), np.empty(7)
+    check(lib.pvo_se3_exp(_ptr(x), _ptr(out)))
+    return out
+
+
+def se3_log(pose) -> np.ndarray:
+    p, out = _f64(pose, (7,)), np.empty(6)
+    check(lib.pvo_se3_log(_ptr(p), _ptr(out)))
+    return out
+
+
+def compose(a, b) -> np.ndarray:
+    x, y, out = _f64(a, (7,)), _f64(b, (7,)), np.empty(7)
+    check(lib.pvo_se3_compose(_ptr(x), _ptr(y), _ptr(out)))
+    return out
+
+
+def inverse(a) -> np.ndarray:
+    x, out = _f64(a, (7,)), np.empty(7)
+    check(lib.pvo_se3_inverse(_ptr(x), _ptr(out)))
+    return out
+
+
+def retract(a, xi) -> np.ndarray:
+    x, t, out = _f64(a, (7,)), _f64(xi, (6,)), np.empty(7)
+    check(lib.pvo_se3_retract(_ptr(x), _ptr(t), _ptr(out)))
+    return out
+
+
+IDENTITY = np.array([0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0])
+
+# ---------------------------------------------------------------------------
+# camera (camera.hpp:10-72)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class Patch:
+    source_frame: int
+    width: int
+    x: np.ndarray
+    y: np.ndarray
+    inverse_depth: float
+
+    @staticmethod
+    def make(source_frame: int, centroid, width: int, inverse_depth: float) -> "Patch":
+        """Patch::make (camera.cpp:15-32)."""
+        if width < 1:
+            raise ValueError("patch: width must be >= 1")
+        if inverse_depth < 0:
+            raise ValueError("patch: inverse depth must be >= 0")
+        half = 0.5 * (width - 1)
+        col, row = np.meshgrid(np.arange(width, dtype=np.float64), np.arange(width, dtype=np.float64))
+        x = (float(centroid[0]) + col.ravel()) - half
+        y = (float(centroid[1]) + row.ravel()) - half
+        return Patch(source_frame, width, x, y, float(inverse_depth))
+
+    @property
+    def size(self) -> int:
+        return self.width * self.width
+
+    def center(self) -> np.ndarray:
+        if self.width % 2 == 1:
+            m = self.size // 2
+            return np.array([self.x[m], self.y[m]])
+        return np.array([self.x.sum() / self.size, self.y.sum() / self.size])
+
+
+def reproject_patches(poses_i, poses_j, K, x, y, inv_depth, ctx: Optional[Context] = None):
+    """Batched reproject_patch (camera.cpp:47-71). Returns (points [n,pp,2], behind [n])."""
+    pi, pj = _f64(poses_i).reshape(-1, 7), _f64(poses_j).reshape(-1, 7)
+    n = pi.shape[0]
+    xs, ys = _f64(x).reshape(n, -1), _f64(y).reshape(n, -1)
+    pp = xs.shape[1]
+    p = int(round(pp ** 0.5))
+    d = _f64(inv_depth).reshape(n)
+    out = np.empty((n, pp, 2))
+    behind = np.empty(n, np.uint8)
+    check(lib.pvo_reproject_patches(_ctx(ctx).handle, n, p, _ptr(pi), _ptr(pj), _ptr(_f64(K, (4,))), _ptr(xs),
+                                    _ptr(ys), _ptr(d), _ptr(out), _ptr(behind)))
+    return out, behind.astype(bool)
+
+
+def reproject_patch(pose_i, pose_j, K, patch: Patch, ctx: Optional[Context] = None):
+    pts, behind = reproject_patches(pose_i, pose_j, K, patch.x[None], patch.y[None], [patch.inverse_depth], ctx)
+    return pts[0], bool(behind[0])
+
+
+@dataclass
+class ReprojectionJacobians:
+    center: np.ndarray
+    d_pose_i: np.ndarray  # 2x6
+    d_pose_j: np.ndarray  # 2x6
+    d_inverse_depth: np.ndarray  # 2
+    behind_camera: bool
+
+
+def reprojection_jacobians_batch(poses_i, poses_j, K, x, y, inv_depth, ctx: Optional[Context] = None):
+    pi, pj = _f64(poses_i).reshape(-1, 7), _f64(poses_j).reshape(-1, 7)
+    n = pi.shape[0]
+    xs, ys = _f64(x).reshape(n, -1), _f64(y).reshape(n, -1)
+    pp = xs.shape[1]
+    d = _f64(inv_depth).reshape(n)
+    out = np.empty((n, 28))
+    behind = np.empty(n, np.uint8)
+    check(lib.pvo_reprojection_jacobians(_ctx(ctx).handle, n, int(round(pp ** 0.5)), _ptr(pi), _ptr(pj),
+                                         _ptr(_f64(K, (4,))), _ptr(xs), _ptr(ys), _ptr(d), _ptr(out),
+                                         _ptr(behind)))
+    return out, behind.astype(bool)
+
+
+def reprojection_jacobians(pose_i, pose_j, K, patch: Patch, ctx: Optional[Context] = None) -> ReprojectionJacobians:
+    out, behind = reprojection_jacobians_batch(pose_i, pose_j, K, patch.x[None], patch.y[None],
+                                               [patch.inverse_depth], ctx)
+    o = out[0]
+    return ReprojectionJacobians(o[0:2].copy(), o[2:14].reshape(2, 6).copy(), o[14:26].reshape(2, 6).copy(),
+                                 o[26:28].copy(), bool(behind[0]))
+
+
+# ---------------------------------------------------------------------------
+# correlation (correlation.hpp:11-44)
+# ---------------------------------------------------------------------------
+
+kCorrRadius = 3
+kCorrSize = 7
+
+
+def correlate(patch_features, pyramid, reprojection, ctx: Optional[Context] = None) -> np.ndarray:
+    """correlate() (correlation.cpp:37-71).
+
+    patch_features: (level0 [pp, C], level1 [pp, C]); pyramid: (level0 [H0, W0, C],
+    level1 [H1, W1, C]); reprojection [pp, 2].  Returns [2, p, p, 7, 7] float32
+    indexed [level, v, u, alpha, beta] (CorrelationGrid::at order).
+    """
+    g0, g1 = _f32(patch_features[0]), _f32(patch_features[1])
+    l0, l1 = _f32(pyramid[0]), _f32(pyramid[1])
+    coords = _f64(reprojection).reshape(-1, 2)
+    pp = coords.shape[0]
+    p = int(round(pp ** 0.5))
+    if p * p != pp or g0.reshape(pp, -1).shape[0] != pp:
+        raise ValueError("correlate: reprojection size mismatch")
+    Cc = g0.reshape(pp, -1).shape[1]
+    out = np.empty((2, p, p, kCorrSize, kCorrSize), np.float32)
+    check(lib.pvo_correlate(_ctx(ctx).handle, p, Cc, _ptr(g0), _ptr(g1), _ptr(l0), l0.shape[1], l0.shape[0],
+                            _ptr(l1), l1.shape[1], l1.shape[0], _ptr(coords), _ptr(out)))
+    return out
+
+
+def correlate_batch(e_patch, e_slot, coords, patch_feats, ctx: Optional[Context] = None) -> np.ndarray:
+    """Batched correlate over the context's frame store: out [E, 2, 9, 7, 7]."""
+    c = _ctx(ctx)
+    ep, es = _i32(e_patch), _i32(e_slot)
+    cs = _f64(coords)
+    pf = _f32(patch_feats)
+    E = ep.shape[0]
+    out = np.empty((E, 2, 9, kCorrSize, kCorrSize), np.float32)
+    check(lib.pvo_correlate_batch(c.handle, E, pf.shape[0], 3, _ptr(ep), _ptr(es), _ptr(cs), _ptr(pf), _ptr(out),
+                                  _capi.PVO_HOST))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# bundle adjustment (bundle_adjust.hpp:15-111)
+# ---------------------------------------------------------------------------
+
+kDefaultDamping = 1e-4
+kMaxObservableMarginPx = 32.0
+
+
+@dataclass
+class BAProblem:
+    """Flattened BAProblem (bundle_adjust.hpp:30-40)."""
+
+    poses: np.ndarray           # [N, 7]
+    pose_fixed: np.ndarray      # [N] bool
+    patch_src: np.ndarray       # [P] pose index
+    patch_x: np.ndarray         # [P, pp]
+    patch_y: np.ndarray         # [P, pp]
+    inverse_depth: np.ndarray   # [P]
+    edge_patch: np.ndarray      # [E]
+    edge_pose: np.ndarray       # [E]
+    edge_target: np.ndarray     # [E, 2]
+    edge_weight: np.ndarray     # [E, 2]
+    K: np.ndarray               # [4]
+    damping: float = kDefaultDamping
+    depth_free: Optional[np.ndarray] = None  # [P] bool or None (all free)
+    patch_width: int = 3
+
+    def arrays(self):
+        return dict(
+            poses=_f64(self.poses).reshape(-1, 7), fixed=_u8(self.pose_fixed), src=_i32(self.patch_src),
+            px=_f64(self.patch_x), py=_f64(self.patch_y), d=_f64(self.inverse_depth),
+            dfree=None if self.depth_free is None else _u8(self.depth_free), ep=_i32(self.edge_patch),
+            eo=_i32(self.edge_pose), et=_f64(self.edge_target), ew=_f64(self.edge_weight), K=_f64(self.K, (4,)))
+
+
+@dataclass
+class BASolution:
+    poses: np.ndarray
+    inverse_depths: np.ndarray
+    residual_norms: list = field(default_factory=list)
+    num_edges: int = 0
+
+
+@dataclass
+class NormalEquations:
+    h: np.ndarray
+    b: np.ndarray
+    num_free_poses: int
+    num_free_depths: int
+
+
+def gauss_newton_step(problem: BAProblem, debug: bool = False, ctx: Optional[Context] = None):
+    """gauss_newton_step (bundle_adjust.cpp:117-223). Returns BASolution (and NormalEquations if debug)."""
+    a = problem.arrays()
+    N, Pn, E = a["poses"].shape[0], a["d"].shape[0], a["ep"].shape[0]
+    out_p, out_d, norms = np.empty((N, 7)), np.empty(Pn), np.empty(2)
+    nfp, nfd = C.c_int(), C.c_int()
+    dh = db = None
+    if debug:
+        nf = int((~np.asarray(problem.pose_fixed, bool)).sum())
+        nd = Pn if problem.depth_free is None else int(np.asarray(problem.depth_free, bool).sum())
+        n = 6 * nf + nd
+        dh, db = np.empty((n, n)), np.empty(n)
+    check(lib.pvo_gauss_newton_step(
+        _ctx(ctx).handle, N, _ptr(a["poses"]), _ptr(a["fixed"]), Pn, problem.patch_width, _ptr(a["src"]),
+        _ptr(a["px"]), _ptr(a["py"]), _ptr(a["d"]), _ptr(a["dfree"]), E, _ptr(a["ep"]), _ptr(a["eo"]),
+        _ptr(a["et"]), _ptr(a["ew"]), _ptr(a["K"]), float(problem.damping), _ptr(out_p), _ptr(out_d),
+        _ptr(norms), _ptr(dh), _ptr(db), C.addressof(nfp), C.addressof(nfd)))
+    sol = BASolution(out_p, out_d, list(norms), E)
+    if debug:
+        return sol, NormalEquations(dh, db, nfp.value, nfd.value)
+    return sol
+
+
+def schur_solve(h_pp, h_pd, h_dd, b_p, b_d, ctx: Optional[Context] = None):
+    """schur_solve (bundle_adjust.cpp:62-94). Returns (pose_delta, depth_delta)."""
+    hpp = _f64(h_pp)
+    np_ = hpp.shape[0] if hpp.ndim == 2 else 0
+    hdd = _f64(h_dd).reshape(-1)
+    nd = hdd.shape[0]
+    hpd = _f64(h_pd).reshape(np_, nd)
+    bp, bd = _f64(b_p).reshape(np_), _f64(b_d).reshape(nd)
+    dp, dd = np.empty(np_), np.empty(nd)
+    check(lib.pvo_schur_solve(_ctx(ctx).handle, np_, nd, _ptr(hpp.reshape(np_, np_)), _ptr(hpd), _ptr(hdd),
+                              _ptr(bp), _ptr(bd), _ptr(dp), _ptr(dd)))
+    return dp, dd
+
+
+def ba_window(problem: BAProblem, iterations: int = 2, structure_only_iterations: int = 0,
+              freeze_targets: bool = False, image_size=(0, 0), ctx: Optional[Context] = None) -> BASolution:
+    """The iteration loop of optimize_window (bundle_adjust.cpp:309-366) on a flattened problem."""
+    a = problem.arrays()
+    N, Pn, E = a["poses"].shape[0], a["d"].shape[0], a["ep"].shape[0]
+    out_p, out_d = np.empty((N, 7)), np.empty(Pn)
+    norms = np.empty(iterations + 2)
+    nn = C.c_int()
+    check(lib.pvo_ba_window(
+        _ctx(ctx).handle, N, _ptr(a["poses"]), _ptr(a["fixed"]), Pn, problem.patch_width, _ptr(a["src"]),
+        _ptr(a["px"]), _ptr(a["py"]), _ptr(a["d"]), E, _ptr(a["ep"]), _ptr(a["eo"]), _ptr(a["et"]),
+        _ptr(a["ew"]), _ptr(a["K"]), int(image_size[0]), int(image_size[1]), int(bool(freeze_targets)),
+        float(problem.damping), iterations, structure_only_iterations, _ptr(out_p), _ptr(out_d), _ptr(norms),
+        C.addressof(nn)))
+    return BASolution(out_p, out_d, list(norms[: nn.value]), E)
+
+
+# ---------------------------------------------------------------------------
+# patch graph (patch_graph.hpp:66-136) and optimize_window
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class WindowOptions:
+    window: int = 10
+    iterations: int = 2
+    structure_only_iterations: int = 0
+    damping: float = kDefaultDamping
+
+
+class PatchGraph:
+    def __init__(self, K, image_width: int, image_height: int, patch_width: int = 3):
+        h = C.c_void_p()
+        self.K = _f64(K, (4,))
+        check(lib.pvo_graph_create(_ptr(self.K), image_width, image_height, patch_width, C.byref(h)))
+        self.handle = h
+        self.image_width, self.image_height, self.patch_width = image_width, image_height, patch_width
+
+    def __del__(self):  # pragma: no cover
+        if getattr(self, "handle", None):
+            lib.pvo_graph_destroy(self.handle)
+            self.handle = None
+
+    def add_frame(self, timestamp: float, pose) -> int:
+        idx = C.c_int()
+        check(lib.pvo_graph_add_frame(self.handle, float(timestamp), _ptr(_f64(pose, (7,))), C.addressof(idx)))
+        return idx.value
+
+    def add_patches(self, frame: int, centroids, inverse_depths) -> list:
+        c = _f64(centroids).reshape(-1, 2)
+        d = _f64(inverse_depths).reshape(-1)
+        if c.shape[0] != d.shape[0]:
+            raise ValueError("patch graph: centroid/depth count mismatch")
+        ids = np.empty(c.shape[0], np.int32)
+        check(lib.pvo_graph_add_patches(self.handle, frame, c.shape[0], _ptr(c), _ptr(d), _ptr(ids)))
+        return ids.tolist()
+
+    def connect(self, radius: int) -> int:
+        n = C.c_int()
+        check(lib.pvo_graph_connect(self.handle, radius, C.addressof(n)))
+        return n.value
+
+    def remove_frame(self, frame: int) -> None:
+        check(lib.pvo_graph_remove_frame(self.handle, frame))
+
+    def set_revision(self, key, delta, weight) -> None:
+        check(lib.pvo_graph_set_revision(self.handle, int(key[0]), int(key[1]), _ptr(_f64(delta, (2,))),
+                                         _ptr(_f64(weight, (2,)))))
+
+    def set_revisions(self, kk, jj, deltas, weights) -> None:
+        d, w = _f64(deltas).reshape(-1, 2), _f64(weights).reshape(-1, 2)
+        for i, (k, j) in enumerate(zip(kk, jj)):
+            check(lib.pvo_graph_set_revision(self.handle, int(k), int(j), d[i].ctypes.data, w[i].ctypes.data))
+
+    def set_pose(self, frame: int, pose) -> None:
+        check(lib.pvo_graph_set_pose(self.handle, frame, _ptr(_f64(pose, (7,)))))
+
+    def set_inverse_depth(self, patch_id: int, d: float) -> None:
+        check(lib.pvo_graph_set_inverse_depth(self.handle, patch_id, float(d)))
+
+    @property
+    def num_edges(self) -> int:
+        return lib.pvo_graph_num_edges(self.handle)
+
+    def edges(self):
+        """(kk, jj, rev [E,4], has_rev) in the reference key order."""
+        n = self.num_edges
+        kk, jj = np.empty(n, np.int32), np.empty(n, np.int32)
+        rev, has = np.empty((n, 4)), np.empty(n, np.uint8)
+        check(lib.pvo_graph_edges(self.handle, _ptr(kk), _ptr(jj), _ptr(rev), _ptr(has)))
+        return kk, jj, rev, has.astype(bool)
+
+    def frames(self):
+        n = lib.pvo_graph_num_frames(self.handle)
+        idx, poses = np.empty(n, np.int32), np.empty((n, 7))
+        check(lib.pvo_graph_frames(self.handle, _ptr(idx), _ptr(poses)))
+        return idx, poses
+
+    def patches(self):
+        n = lib.pvo_graph_num_patches(self.handle)
+        ids, src, d = np.empty(n, np.int32), np.empty(n, np.int32), np.empty(n)
+        check(lib.pvo_graph_patches(self.handle, _ptr(ids), _ptr(src), _ptr(d)))
+        return ids, src, d
+
+    def active_edges(self, window: int):
+        n = C.c_int()
+        check(lib.pvo_graph_active_edges(self.handle, window, None, None, C.addressof(n)))
+        kk, jj = np.empty(n.value, np.int32), np.empty(n.value, np.int32)
+        check(lib.pvo_graph_active_edges(self.handle, window, _ptr(kk), _ptr(jj), C.addressof(n)))
+        return kk, jj
+
+    def build_target(self, key) -> np.ndarray:
+        out = np.empty(2)
+        check(lib.pvo_graph_build_target(self.handle, int(key[0]), int(key[1]), _ptr(out)))
+        return out
+
+    def window_problem(self, window: int) -> Optional[dict]:
+        """The flattened optimize_window problem (bundle_adjust.cpp:231-307)."""
+        n_p, n_k, n_e = C.c_int(), C.c_int(), C.c_int()
+        nulls = [None] * 13
+        check(lib.pvo_graph_window_problem(self.handle, window, C.addressof(n_p), C.addressof(n_k),
+                                           C.addressof(n_e), *nulls))
+        if n_e.value == 0:
+            return None
+        N, Pn, E = n_p.value, n_k.value, n_e.value
+        pp = self.patch_width ** 2
+        r = dict(pose_frames=np.empty(N, np.int32), poses=np.empty((N, 7)), fixed=np.empty(N, np.uint8),
+                 patch_ids=np.empty(Pn, np.int32), patch_src=np.empty(Pn, np.int32), patch_x=np.empty((Pn, pp)),
+                 patch_y=np.empty((Pn, pp)), depth=np.empty(Pn), e_patch=np.empty(E, np.int32),
+                 e_pose=np.empty(E, np.int32), e_target=np.empty((E, 2)), e_weight=np.empty((E, 2)))
+        order = ["pose_frames", "poses", "fixed", "patch_ids", "patch_src", "patch_x", "patch_y", "depth",
+                 "e_patch", "e_pose", "e_target", "e_weight"]
+        check(lib.pvo_graph_window_problem(self.handle, window, C.addressof(n_p), C.addressof(n_k),
+                                           C.addressof(n_e), *[_ptr(r[k]) for k in order]))
+        return r
+
+
+def build_target(graph: PatchGraph, key) -> np.ndarray:
+    return graph.build_target(key)
+
+
+def optimize_window(graph: PatchGraph, options: WindowOptions = WindowOptions(),
+                    ctx: Optional[Context] = None) -> BASolution:
+    """optimize_window (bundle_adjust.cpp:225-375); mutates the graph."""
+    norms = np.empty(options.iterations + 2)
+    nn, ne = C.c_int(), C.c_int()
+    check(lib.pvo_optimize_window(_ctx(ctx).handle, graph.handle, options.window, options.iterations,
+                                  options.structure_only_iterations, float(options.damping), _ptr(norms),
+                                  C.addressof(nn), C.addressof(ne)))
+    idx, poses = graph.frames()
+    ids, src, d = graph.patches()
+    return BASolution(poses, d, list(norms[: nn.value]), ne.value)
+
+
+# ---------------------------------------------------------------------------
+# resident window (the per-frame hot path)
+# ---------------------------------------------------------------------------
+
+
+class Window:
+    """A device-resident active window: corr + BA iterations without host round trips."""
+
+    def __init__(self, ctx: Context):
+        self.ctx = ctx
+
+    def load(self, prob: dict, pose_slot, patch_feats, K, image_size) -> None:
+        """prob: flattened window with revision *deltas* in e_delta (freeze_targets semantics)."""
+        self.n_poses = int(prob["poses"].shape[0])
+        self.n_patches = int(prob["depth"].shape[0])
+        self.n_edges = int(prob["e_patch"].shape[0])
+        keep = dict(poses=_f64(prob["poses"]), fixed=_u8(prob["fixed"]), slot=_i32(pose_slot),
+                    src=_i32(prob["patch_src"]), px=_f64(prob["patch_x"]), py=_f64(prob["patch_y"]),
+                    d=_f64(prob["depth"]), pf=_f32(patch_feats), ep=_i32(prob["e_patch"]),
+                    eo=_i32(prob["e_pose"]), ed=_f64(prob["e_delta"]), ew=_f64(prob["e_weight"]),
+                    K=_f64(K, (4,)))
+        check(lib.pvo_window_load(self.ctx.handle, self.n_poses, _ptr(keep["poses"]), _ptr(keep["fixed"]),
+                                  _ptr(keep["slot"]), self.n_patches, 3, _ptr(keep["src"]), _ptr(keep["px"]),
+                                  _ptr(keep["py"]), _ptr(keep["d"]), _ptr(keep["pf"]), self.n_edges,
+                                  _ptr(keep["ep"]), _ptr(keep["eo"]), _ptr(keep["ed"]), _ptr(keep["ew"]),
+                                  _ptr(keep["K"]), int(image_size[0]), int(image_size[1]), _capi.PVO_HOST))
+
+    def reset(self) -> None:
+        check(lib.pvo_window_set_state(self.ctx.handle, None, None, _capi.PVO_HOST))
+
+    def set_state(self, poses, depth) -> None:
+        p, d = _f64(poses), _f64(depth)
+        check(lib.pvo_window_set_state(self.ctx.handle, _ptr(p), _ptr(d), _capi.PVO_HOST))
+
+    def iteration(self, iterations: int = 2, damping: float = kDefaultDamping, corr_out=None,
+                  corr_device_ptr: int | None = None) -> None:
+        if corr_device_ptr is not None:
+            check(lib.pvo_window_iteration(self.ctx.handle, iterations, damping, corr_device_ptr, _capi.PVO_DEVICE))
+        elif corr_out is not None:
+            check(lib.pvo_window_iteration(self.ctx.handle, iterations, damping, _ptr(corr_out), _capi.PVO_HOST))
+        else:
+            check(lib.pvo_window_iteration(self.ctx.handle, iterations, damping, None, _capi.PVO_DEVICE))
+
+    def correlate(self) -> np.ndarray:
+        out = np.empty((self.n_edges, 2, 9, 7, 7), np.float32)
+        check(lib.pvo_window_correlate(self.ctx.handle, _ptr(out), _capi.PVO_HOST))
+        return out
+
+    def read(self):
+        poses, d = np.empty((self.n_poses, 7)), np.empty(self.n_patches)
+        norms = np.empty(130)
+        nn = C.c_int()
+        check(lib.pvo_window_read(self.ctx.handle, _ptr(poses), _ptr(d), _ptr(norms), C.addressof(nn)))
+        return poses, d, list(norms[: nn.value])
+
+    def corr_device_ptr(self) -> int:
+        p = C.c_void_p()
+        check(lib.pvo_window_corr_ptr(self.ctx.handle, C.addressof(p)))
+        return p.value

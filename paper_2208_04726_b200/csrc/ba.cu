@@ -1,0 +1,967 @@
+// ba.cu — sparse Gauss-Newton bundle adjustment of one window (K3-K6),
+// sm_100a, FP64.
+//
+// Reference: optimize_window / gauss_newton_step / schur_solve
+// (bundle_adjust.cpp:62-375).  The reference builds a dense (6F+P)^2
+// Hessian and runs an Eigen LDLT on the Schur complement.  Here the whole
+// iteration loop — frozen targets, assembly, Schur elimination of the depth
+// block, the pose solve, retraction, the weighted residual norms and the
+// divergence guard (damping x1e3, x1e6, x1e9 retries) — runs inside ONE
+// persistent cooperative kernel; control never returns to the host.
+//
+// Phases per Gauss-Newton attempt (grid.sync() between them):
+//   P1 assemble   warp per patch, lane per edge: Jacobians (camera.cpp:73-108),
+//                 residual, weight; per-patch reductions give h_k, b_k, the
+//                 patch's H_pd column v_k and gradient; every thread of the CTA
+//                 owns fixed entries of the CTA's reduced system
+//                     S += sum_e J~_e^T W_e J~_e - v_k v_k^T / h_k
+//                     r += b_k - v_k b_dk / h_k
+//                 accumulated patch after patch (no atomics, fixed order).
+//   P2 reduce     entry-parallel over the grid: S = sum over CTAs (fixed order)
+//                 + damping on the diagonal.
+//   P3 solve      CTA 0: pivoted LDLT of S in shared memory (Eigen's pivot rule:
+//                 largest remaining original diagonal), solve, retract poses.
+//   P4 update     warp per patch: depth back-substitution, clamp at 0, weighted
+//                 residual at the candidate state (bitwise-equal-pose shortcut).
+//   P5 decide     every CTA evaluates the same guard from the same partial sums,
+//                 then commits, retries with heavier damping, or skips.
+// Determinism: every reduction has a fixed order (shuffle trees, per-thread
+// entry ownership, ordered cross-CTA sums), so reruns are bit-identical.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "geometry.cuh"
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace pvo_dev {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxFree = 16;            // free poses  -> np <= 96
+constexpr int kMaxNp = 6 * kMaxFree;
+constexpr int kMaxEdges = 32;           // edges per patch (lane per edge)
+constexpr int kRec = 30;                // doubles per edge record
+// edge record: Gs[12] Jt[12] Jd[2] r[2] w[2]
+constexpr int kGs = 0, kJt = 12, kJd = 24, kR = 26, kW = 28;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+struct Layout {
+    // byte offsets into dynamic shared memory
+    int S, rhs, rec, vb, scal, ints, ab, wr, total;
+    // solve-phase overlay (CTA 0 only)
+    int A, x, od, tr, solve_total;
+};
+
+__host__ __device__ inline int nent_of(int np) { return np * (np + 1) / 2; }
+
+__host__ __device__ inline Layout make_layout(int np) {
+    Layout L;
+    const int nent = nent_of(np);
+    int off = 0;
+    // The entry table comes first so the solve overlay (CTA 0) never clobbers it.
+    L.ab = off;
+    off += (4 * nent + 15) & ~15;
+    const int overlay = off;
+    L.S = off;
+    off += 8 * nent;
+    L.rhs = off;
+    off += 8 * np;
+    L.rec = off;
+    off += 8 * kWarps * kMaxEdges * kRec;
+    L.vb = off;
+    off += 8 * kWarps * 2 * np;
+    L.scal = off;
+    off += 8 * kWarps * 4;  // h, bd, inv_h, pad
+    L.wr = off;
+    off += 8 * kWarps * 4;  // wrms partials
+    L.ints = off;
+    off += 4 * kWarps * (4 + kMaxFree + kMaxEdges);  // si, ne, dslot, k | p2e[16] | next[32]
+    L.total = (off + 15) & ~15;
+    // solve overlay
+    off = overlay;
+    L.A = off;
+    off += 8 * np * np;
+    L.x = off;
+    off += 8 * np;
+    L.od = off;
+    off += 8 * np;
+    L.tr = off;
+    off += 4 * np;
+    L.solve_total = (off + 15) & ~15;
+    if (L.solve_total > L.total) L.total = L.solve_total;
+    return L;
+}
+
+__device__ inline void set_status(int* status, int code) { atomicOr(status, 1 << code); }
+
+// Reprojected center + behind flag with reproject_patch semantics
+// (camera.cpp:47-71): bitwise-equal shortcut, behind if ANY pixel's q_z <= eps.
+__device__ inline void reproject_center(const SE3& pi, const SE3& pj, const Cam& K, const double* px,
+                                        const double* py, double d, double* cu, double* cv, bool* behind) {
+    if (se3_equal(pi, pj)) {
+        *cu = px[4];
+        *cv = py[4];
+        *behind = false;
+        return;
+    }
+    const Relative rel = relative_pose(pi, pj);
+    bool b = false;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        double u, v;
+        const double qz = reproject_point(rel, K, d, px[k], py[k], &u, &v);
+        if (qz <= kDepthEpsilon) b = true;
+        if (k == 4) {
+            *cu = u;
+            *cv = v;
+        }
+    }
+    *behind = b;
+}
+
+struct Shared {
+    double* S;
+    double* rhs;
+    double* rec;
+    double* vb;
+    double* scal;
+    double* wr;
+    int* ints;
+    unsigned* ab;
+};
+
+__device__ inline Shared carve(unsigned char* smem, const Layout& L) {
+    Shared s;
+    s.S = reinterpret_cast<double*>(smem + L.S);
+    s.rhs = reinterpret_cast<double*>(smem + L.rhs);
+    s.rec = reinterpret_cast<double*>(smem + L.rec);
+    s.vb = reinterpret_cast<double*>(smem + L.vb);
+    s.scal = reinterpret_cast<double*>(smem + L.scal);
+    s.wr = reinterpret_cast<double*>(smem + L.wr);
+    s.ints = reinterpret_cast<int*>(smem + L.ints);
+    s.ab = reinterpret_cast<unsigned*>(smem + L.ab);
+    return s;
+}
+
+// Per-warp int block: [0]=si [1]=ne [2]=dslot [3]=k, [4..4+16)=p2e, then next[32]
+__device__ inline int* warp_ints(const Shared& s, int w) { return s.ints + w * (4 + kMaxFree + kMaxEdges); }
+
+// ---------------------------------------------------------------------------
+// P0: frozen targets (bundle_adjust.cpp:288-307) for the edges of [k0, k1)
+// ---------------------------------------------------------------------------
+__device__ void phase_freeze(const BAParams& a, int k0, int k1) {
+    const int e0 = a.patch_edge_begin[k0], e1 = a.patch_edge_begin[k1];
+    const Cam K{a.K[0], a.K[1], a.K[2], a.K[3]};
+    const double margin = 2.0 * 32.0;  // 2 * kMaxObservableMarginPx (bundle_adjust.hpp:18)
+    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        if (!a.freeze_targets) {
+            a.e_target[2 * e] = a.e_in[2 * e];
+            a.e_target[2 * e + 1] = a.e_in[2 * e + 1];
+            a.e_weight[2 * e] = a.e_weight_in[2 * e];
+            a.e_weight[2 * e + 1] = a.e_weight_in[2 * e + 1];
+            continue;
+        }
+        const int k = a.e_patch[e];
+        const SE3 pi = se3_load(a.poses + 7 * a.patch_src[k]);
+        const SE3 pj = se3_load(a.poses + 7 * a.e_pose[e]);
+        double cu, cv;
+        bool behind;
+        reproject_center(pi, pj, K, a.patch_x + 9 * (size_t)k, a.patch_y + 9 * (size_t)k, a.depth[k], &cu, &cv,
+                         &behind);
+        const bool observable = !behind && cu > -margin && cv > -margin && cu < a.image_w - 1 + margin &&
+                                cv < a.image_h - 1 + margin;
+        a.e_target[2 * e] = cu + a.e_in[2 * e];
+        a.e_target[2 * e + 1] = cv + a.e_in[2 * e + 1];
+        a.e_weight[2 * e] = observable ? a.e_weight_in[2 * e] : 0.0;
+        a.e_weight[2 * e + 1] = observable ? a.e_weight_in[2 * e + 1] : 0.0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// P1: assembly of the CTA's patches into its partial reduced system.
+// ---------------------------------------------------------------------------
+__device__ void phase_assemble(const BAParams& a, const Shared& s, int k0, int k1, int np, bool poses_frozen,
+                               double lambda, double* part) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nent = nent_of(np);
+    const Cam K{a.K[0], a.K[1], a.K[2], a.K[3]};
+    for (int i = tid; i < nent; i += kThreads) s.S[i] = 0.0;
+    for (int i = tid; i < np; i += kThreads) s.rhs[i] = 0.0;
+    double wr_sum = 0.0, wr_w = 0.0;  // lane-0 of each warp keeps its running sums
+    __syncthreads();
+
+    for (int batch = k0; batch < k1; batch += kWarps) {
+        // ---- per-warp patch records ----
+        const int k = batch + warp;
+        int* wi = warp_ints(s, warp);
+        double* rec = s.rec + (size_t)warp * kMaxEdges * kRec;
+        double* v = s.vb + (size_t)warp * 2 * np;
+        double* bvec = v + np;
+        double* sc = s.scal + warp * 4;
+        if (k < k1) {
+            const int eb = a.patch_edge_begin[k], ne = a.patch_edge_begin[k + 1] - eb;
+            const int src = a.patch_src[k];
+            const int si = poses_frozen ? -1 : a.pose_free_slot[src];
+            const int dslot = a.depth_slot[k];
+            const double d = a.depth[k];
+            const double* px = a.patch_x + 9 * (size_t)k;
+            const double* py = a.patch_y + 9 * (size_t)k;
+            for (int i = lane; i < 2 * np; i += 32) v[i] = 0.0;
+            double h = 0, bd = 0, vs[6] = {0, 0, 0, 0, 0, 0}, bs[6] = {0, 0, 0, 0, 0, 0};
+            int sj = -1;
+            double wrs = 0, wrw = 0;
+            if (lane < ne) {
+                const int e = eb + lane;
+                const int tgt = a.e_pose[e];
+                sj = poses_frozen ? -1 : a.pose_free_slot[tgt];
+                const SE3 pi = se3_load(a.poses + 7 * src);
+                const SE3 pj = se3_load(a.poses + 7 * tgt);
+                const Relative rel = relative_pose(pi, pj);
+                const CenterJac J = center_jacobians(rel, K, d, px[4], py[4]);
+                const double r0 = J.cu - a.e_target[2 * e], r1 = J.cv - a.e_target[2 * e + 1];
+                if (!isfinite(r0) || !isfinite(r1)) set_status(a.status, kDevNonFiniteResidual);
+                double w0 = J.behind ? 0.0 : a.e_weight[2 * e];
+                double w1 = J.behind ? 0.0 : a.e_weight[2 * e + 1];
+                const bool active = !(w0 == 0.0 && w1 == 0.0);  // bundle_adjust.cpp:151
+                if (!active) {
+                    w0 = 0.0;
+                    w1 = 0.0;
+                }
+                double* R = rec + lane * kRec;
+#pragma unroll
+                for (int c = 0; c < 12; ++c) {
+                    const double gs = J.di[c] + ((sj >= 0 && sj == si) ? J.dj[c] : 0.0);
+                    R[kGs + c] = active ? gs : 0.0;
+                    R[kJt + c] = active ? J.dj[c] : 0.0;
+                }
+                R[kJd] = active ? J.dd[0] : 0.0;
+                R[kJd + 1] = active ? J.dd[1] : 0.0;
+                R[kR] = active ? r0 : 0.0;
+                R[kR + 1] = active ? r1 : 0.0;
+                R[kW] = w0;
+                R[kW + 1] = w1;
+                if (active) {
+                    const double t0 = J.dd[0] * w0, t1 = J.dd[1] * w1;
+                    h = t0 * J.dd[0] + t1 * J.dd[1];
+                    bd = -(t0 * r0 + t1 * r1);
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) {
+                        const double g0 = R[kGs + c] * w0, g1 = R[kGs + 6 + c] * w1;
+                        vs[c] = g0 * J.dd[0] + g1 * J.dd[1];
+                        bs[c] = -(g0 * r0 + g1 * r1);
+                    }
+                }
+                if (!active || sj == si) sj = -1;  // no separate target block
+                // weighted_residual_norm term at the current state (bundle_adjust.cpp:99-113)
+                double cu, cv;
+                bool behind;
+                reproject_center(pi, pj, K, px, py, d, &cu, &cv, &behind);
+                const double rx = cu - a.e_target[2 * e], ry = cv - a.e_target[2 * e + 1];
+                const double wx = behind ? 0.0 : a.e_weight[2 * e];
+                const double wy = behind ? 0.0 : a.e_weight[2 * e + 1];
+                wrs = wx * rx * rx + wy * ry * ry;
+                wrw = wx + wy;
+            }
+            h = warp_sum(h);
+            bd = warp_sum(bd);
+            wrs = warp_sum(wrs);
+            wrw = warp_sum(wrw);
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+                vs[c] = warp_sum(vs[c]);
+                bs[c] = warp_sum(bs[c]);
+            }
+            __syncwarp();
+            // per-edge target blocks (disjoint unless a target repeats: serialise)
+            for (int l = 0; l < ne; ++l) {
+                const int sjl = __shfl_sync(0xffffffffu, sj, l);
+                if (sjl >= 0 && lane < 6) {
+                    const double* R = rec + l * kRec;
+                    const double g0 = R[kJt + lane] * R[kW], g1 = R[kJt + 6 + lane] * R[kW + 1];
+                    v[6 * sjl + lane] += g0 * R[kJd] + g1 * R[kJd + 1];
+                    bvec[6 * sjl + lane] += -(g0 * R[kR] + g1 * R[kR + 1]);
+                }
+                __syncwarp();
+            }
+            if (si >= 0 && lane < 6) {
+                v[6 * si + lane] += vs[lane];
+                bvec[6 * si + lane] += bs[lane];
+            }
+            // target-pose -> edge chains
+            int* p2e = wi + 4;
+            int* nxt = wi + 4 + kMaxFree;
+            if (lane == 0) {
+                for (int i = 0; i < kMaxFree; ++i) p2e[i] = -1;
+                for (int l = ne - 1; l >= 0; --l) {
+                    const int sjl = a.pose_free_slot[a.e_pose[eb + l]];
+                    const double* R = rec + l * kRec;
+                    const bool act = !(R[kW] == 0.0 && R[kW + 1] == 0.0);
+                    nxt[l] = -1;
+                    if (!poses_frozen && act && sjl >= 0 && sjl != si) {
+                        nxt[l] = p2e[sjl];
+                        p2e[sjl] = l;
+                    }
+                }
+                wi[0] = si;
+                wi[1] = ne;
+                wi[2] = dslot;
+                wi[3] = k;
+                const double hd = h + lambda;  // h_dd + damping (bundle_adjust.cpp:185)
+                sc[0] = hd;
+                sc[1] = bd;
+                sc[2] = 1.0 / hd;  // d_inv (bundle_adjust.cpp:69)
+                if (dslot >= 0 && !(hd > 0)) set_status(a.status, kDevNonPositiveDepth);
+                wr_sum += wrs;
+                wr_w += wrw;
+            }
+        } else if (lane == 0) {
+            wi[1] = -1;
+        }
+        __syncthreads();
+
+        // ---- ordered accumulation of the batch into the CTA system ----
+        for (int w = 0; w < kWarps; ++w) {
+            const int* wiw = warp_ints(s, w);
+            if (wiw[1] < 0) break;
+            const int si = wiw[0], ne = wiw[1];
+            const bool dfree = wiw[2] >= 0;
+            const double* recw = s.rec + (size_t)w * kMaxEdges * kRec;
+            const double* vw = s.vb + (size_t)w * 2 * np;
+            const double* bw = vw + np;
+            const double inv_h = s.scal[w * 4 + 2];
+            const int* p2e = wiw + 4;
+            const int* nxt = wiw + 4 + kMaxFree;
+            for (int ent = tid; ent < nent; ent += kThreads) {
+                const unsigned ab = s.ab[ent];
+                const int ia = ab & 0xffff, ib = ab >> 16;
+                const int A = ia / 6, B = ib / 6, ra = ia - 6 * A, rb = ib - 6 * B;
+                double val = 0.0;
+                if (A == si && B == si) {
+                    for (int l = 0; l < ne; ++l) {
+                        const double* R = recw + l * kRec;
+                        val += (R[kGs + ra] * R[kW]) * R[kGs + rb] + (R[kGs + 6 + ra] * R[kW + 1]) * R[kGs + 6 + rb];
+                    }
+                } else if (A == si) {
+                    for (int l = p2e[B]; l >= 0; l = nxt[l]) {
+                        const double* R = recw + l * kRec;
+                        val += (R[kGs + ra] * R[kW]) * R[kJt + rb] + (R[kGs + 6 + ra] * R[kW + 1]) * R[kJt + 6 + rb];
+                    }
+                } else if (B == si) {
+                    for (int l = p2e[A]; l >= 0; l = nxt[l]) {
+                        const double* R = recw + l * kRec;
+                        val += (R[kJt + ra] * R[kW]) * R[kGs + rb] + (R[kJt + 6 + ra] * R[kW + 1]) * R[kGs + 6 + rb];
+                    }
+                } else if (A == B) {
+                    for (int l = p2e[A]; l >= 0; l = nxt[l]) {
+                        const double* R = recw + l * kRec;
+                        val += (R[kJt + ra] * R[kW]) * R[kJt + rb] + (R[kJt + 6 + ra] * R[kW + 1]) * R[kJt + 6 + rb];
+                    }
+                }
+                if (dfree) val -= (vw[ia] * inv_h) * vw[ib];
+                s.S[ent] += val;
+            }
+            for (int i = tid; i < np; i += kThreads) {
+                double r = bw[i];
+                if (dfree) r -= vw[i] * (inv_h * s.scal[w * 4 + 1]);
+                s.rhs[i] += r;
+            }
+            // stash the patch's Schur data for the back-substitution
+            const int kw = wiw[3];
+            for (int i = tid; i < np; i += kThreads) a.patch_v[(size_t)kw * np + i] = vw[i];
+            if (tid == 0) {
+                a.patch_h[kw] = s.scal[w * 4 + 0];
+                a.patch_bd[kw] = s.scal[w * 4 + 1];
+            }
+        }
+        __syncthreads();
+    }
+    // ---- write the CTA partial ----
+    if (lane == 0) {
+        s.wr[warp * 2] = wr_sum;
+        s.wr[warp * 2 + 1] = wr_w;
+    }
+    __syncthreads();
+    for (int i = tid; i < nent; i += kThreads) part[i] = s.S[i];
+    for (int i = tid; i < np; i += kThreads) part[nent + i] = s.rhs[i];
+    if (tid == 0) {
+        double ws = 0, ww = 0;
+        for (int w = 0; w < kWarps; ++w) {
+            ws += s.wr[2 * w];
+            ww += s.wr[2 * w + 1];
+        }
+        part[nent + np] = ws;
+        part[nent + np + 1] = ww;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// P3: pivoted LDLT solve of the reduced camera system (CTA 0), retraction.
+// Pivot rule of Eigen's LDLT: at step k take the largest |diagonal| of the
+// not-yet-factored (original, permuted) diagonal.
+// ---------------------------------------------------------------------------
+__device__ void phase_solve(const BAParams& a, unsigned char* smem, const Layout& L, int np, bool poses_frozen) {
+    const int tid = threadIdx.x;
+    const int nent = nent_of(np);
+    __shared__ int s_piv;
+    __shared__ int s_fail;
+    if (np > 0 && !poses_frozen) {
+        double* A = reinterpret_cast<double*>(smem + L.A);
+        double* x = reinterpret_cast<double*>(smem + L.x);
+        double* od = reinterpret_cast<double*>(smem + L.od);
+        int* tr = reinterpret_cast<int*>(smem + L.tr);
+        // expand the upper triangle (row-major by rows a<=b)
+        for (int ent = tid; ent < nent; ent += kThreads) {
+            // invert ent -> (ia, ib)
+            int ia = 0, rowlen = np, base = 0;
+            while (ent >= base + rowlen) {
+                base += rowlen;
+                --rowlen;
+                ++ia;
+            }
+            const int ib = ia + (ent - base);
+            const double val = a.system[ent];
+            A[ia * np + ib] = val;
+            A[ib * np + ia] = val;
+        }
+        for (int i = tid; i < np; i += kThreads) x[i] = a.system[nent + i];
+        if (tid == 0) s_fail = 0;
+        __syncthreads();
+        for (int i = tid; i < np; i += kThreads) od[i] = A[i * np + i];
+        __syncthreads();
+        bool zero_all = false;
+        for (int k = 0; k < np; ++k) {
+            if (tid == 0) {
+                int big = k;
+                double bv = fabs(od[k]);
+                for (int i = k + 1; i < np; ++i) {
+                    if (fabs(od[i]) > bv) {
+                        bv = fabs(od[i]);
+                        big = i;
+                    }
+                }
+                tr[k] = big;
+                s_piv = big;
+            }
+            __syncthreads();
+            const int p = s_piv;
+            if (p != k) {
+                for (int j = tid; j < np; j += kThreads) {
+                    const double t = A[k * np + j];
+                    A[k * np + j] = A[p * np + j];
+                    A[p * np + j] = t;
+                }
+                __syncthreads();
+                for (int i = tid; i < np; i += kThreads) {
+                    const double t = A[i * np + k];
+                    A[i * np + k] = A[i * np + p];
+                    A[i * np + p] = t;
+                }
+                if (tid == 0) {
+                    const double t = od[k];
+                    od[k] = od[p];
+                    od[p] = t;
+                }
+                __syncthreads();
+            }
+            const double dk = A[k * np + k];
+            const bool valid = fabs(dk) > 0.0;
+            if (k == 0 && !valid) {
+                zero_all = true;
+                break;
+            }
+            if (valid) {
+                // trailing update with the unscaled column, then scale it
+                const int m = np - k - 1;
+                for (int t = tid; t < m * m; t += kThreads) {
+                    const int i = k + 1 + t / m, j = k + 1 + t % m;
+                    A[i * np + j] -= A[i * np + k] * (A[j * np + k] / dk);
+                }
+                __syncthreads();
+                for (int i = k + 1 + tid; i < np; i += kThreads) A[i * np + k] /= dk;
+                __syncthreads();
+            } else {
+                for (int i = k + 1 + tid; i < np; i += kThreads)
+                    if (A[i * np + k] != 0.0) s_fail = 1;
+                __syncthreads();
+            }
+        }
+        if (zero_all) {
+            for (int i = tid; i < np; i += kThreads) {
+                tr[i] = i;
+                A[i * np + i] = 0.0;
+            }
+        }
+        __syncthreads();
+        if (s_fail) {
+            if (tid == 0) set_status(a.status, kDevFactorization);
+        } else if (tid < 32) {
+            // substitutions on one warp
+            const int lane = tid;
+            if (lane == 0)
+                for (int k = 0; k < np; ++k) {
+                    const double t = x[k];
+                    x[k] = x[tr[k]];
+                    x[tr[k]] = t;
+                }
+            __syncwarp();
+            for (int j = 0; j < np; ++j) {
+                const double xj = x[j];
+                for (int i = j + 1 + lane; i < np; i += 32) x[i] -= A[i * np + j] * xj;
+                __syncwarp();
+            }
+            for (int i = lane; i < np; i += 32) {
+                const double dd = A[i * np + i];
+                x[i] = fabs(dd) > DBL_MIN ? x[i] / dd : 0.0;
+            }
+            __syncwarp();
+            for (int j = np - 1; j >= 0; --j) {
+                const double xj = x[j];
+                for (int i = lane; i < j; i += 32) x[i] -= A[j * np + i] * xj;
+                __syncwarp();
+            }
+            if (lane == 0)
+                for (int k = np - 1; k >= 0; --k) {
+                    const double t = x[k];
+                    x[k] = x[tr[k]];
+                    x[tr[k]] = t;
+                }
+            __syncwarp();
+            bool bad = false;
+            for (int i = lane; i < np; i += 32) {
+                a.delta[i] = x[i];
+                if (!isfinite(x[i])) bad = true;
+            }
+            if (__any_sync(0xffffffffu, bad) && lane == 0) set_status(a.status, kDevNonFinitePose);
+        }
+        __syncthreads();
+    }
+    // candidate poses (bundle_adjust.cpp:202-207)
+    for (int i = tid; i < a.n_poses; i += kThreads) {
+        const int slot = poses_frozen ? -1 : a.pose_free_slot[i];
+        const SE3 p = se3_load(a.poses + 7 * i);
+        if (slot >= 0 && np > 0) {
+            double xi[6];
+#pragma unroll
+            for (int c = 0; c < 6; ++c) xi[c] = a.delta[6 * slot + c];
+            se3_store(se3_retract(p, xi), a.cand_poses + 7 * i);
+        } else {
+            se3_store(p, a.cand_poses + 7 * i);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// P4: depth back-substitution + residual at the candidate state.
+// ---------------------------------------------------------------------------
+__device__ void phase_update(const BAParams& a, const Shared& s, int k0, int k1, int np, double* part_tail) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const Cam K{a.K[0], a.K[1], a.K[2], a.K[3]};
+    double wr_sum = 0, wr_w = 0;
+    for (int k = k0 + warp; k < k1; k += kWarps) {
+        double dnew = a.depth[k];
+        if (a.depth_slot[k] >= 0) {
+            double dot = 0.0;
+            for (int i = lane; i < np; i += 32) dot += a.patch_v[(size_t)k * np + i] * a.delta[i];
+            dot = warp_sum(dot);
+            const double inv_h = 1.0 / a.patch_h[k];
+            const double dd = inv_h * (a.patch_bd[k] - dot);  // bundle_adjust.cpp:88-89
+            if (!isfinite(dd) && lane == 0) set_status(a.status, kDevNonFiniteDepth);
+            dnew = fmax(0.0, dnew + dd);  // bundle_adjust.cpp:211
+            // std::max(0.0, x) returns 0.0 for NaN x; fmax returns 0.0 too.
+        }
+        if (lane == 0) a.cand_depth[k] = dnew;
+        const int eb = a.patch_edge_begin[k], ne = a.patch_edge_begin[k + 1] - eb;
+        const SE3 pi = se3_load(a.cand_poses + 7 * a.patch_src[k]);
+        double ws = 0, ww = 0;
+        for (int l = lane; l < ne; l += 32) {
+            const int e = eb + l;
+            const SE3 pj = se3_load(a.cand_poses + 7 * a.e_pose[e]);
+            double cu, cv;
+            bool behind;
+            reproject_center(pi, pj, K, a.patch_x + 9 * (size_t)k, a.patch_y + 9 * (size_t)k, dnew, &cu, &cv,
+                             &behind);
+            const double rx = cu - a.e_target[2 * e], ry = cv - a.e_target[2 * e + 1];
+            const double wx = behind ? 0.0 : a.e_weight[2 * e];
+            const double wy = behind ? 0.0 : a.e_weight[2 * e + 1];
+            ws += wx * rx * rx + wy * ry * ry;
+            ww += wx + wy;
+        }
+        ws = warp_sum(ws);
+        ww = warp_sum(ww);
+        wr_sum += ws;
+        wr_w += ww;
+    }
+    if (lane == 0) {
+        s.wr[warp * 2] = wr_sum;
+        s.wr[warp * 2 + 1] = wr_w;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double ws = 0, ww = 0;
+        for (int w = 0; w < kWarps; ++w) {
+            ws += s.wr[2 * w];
+            ww += s.wr[2 * w + 1];
+        }
+        part_tail[2] = ws;
+        part_tail[3] = ww;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) ba_kernel(BAParams a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    cg::grid_group grid = cg::this_grid();
+    const int np_full = 6 * a.n_free_poses;
+    const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+    const int k0 = (int)((long long)a.n_patches * b / G);
+    const int k1 = (int)((long long)a.n_patches * (b + 1) / G);
+
+    phase_freeze(a, k0, k1);
+    __syncthreads();
+
+    const int total_iters = a.structure_only + a.iterations;
+    for (int it = 0; it < total_iters; ++it) {
+        const bool structure = it < a.structure_only;
+        const int np = structure ? 0 : np_full;
+        const int nent = nent_of(np);
+        const size_t pstride = (size_t)nent_of(np_full) + np_full + 4;
+        const Layout L = make_layout(np);
+        const Shared s = carve(smem, L);
+        // entry -> (a, b) table for this np
+        for (int ent = tid; ent < nent; ent += kThreads) {
+            int ia = 0, rowlen = np, base = 0;
+            while (ent >= base + rowlen) {
+                base += rowlen;
+                --rowlen;
+                ++ia;
+            }
+            s.ab[ent] = (unsigned)ia | ((unsigned)(ia + ent - base) << 16);
+        }
+        __syncthreads();
+        int attempt = 0;
+        for (;;) {
+            const double lambda = attempt == 0 ? a.damping : a.damping * (attempt == 1 ? 1e3 : attempt == 2 ? 1e6 : 1e9);
+            double* part = a.partials + (size_t)b * pstride;
+            phase_assemble(a, s, k0, k1, np, structure, lambda, part);
+            grid.sync();
+            // P2: ordered reduction of the CTA partials (+ damping on the diagonal)
+            for (int ent = b * kThreads + tid; ent < nent + np; ent += G * kThreads) {
+                double acc = 0.0;
+                for (int c = 0; c < G; ++c) acc += a.partials[(size_t)c * pstride + ent];
+                if (ent < nent) {
+                    const unsigned ab = s.ab[ent];
+                    if ((ab & 0xffff) == (ab >> 16)) acc += lambda;
+                }
+                a.system[ent] = acc;
+            }
+            grid.sync();
+            if (b == 0) phase_solve(a, smem, L, np, structure);
+            grid.sync();
+            phase_update(a, s, k0, k1, np, part + nent + np);
+            grid.sync();
+            // P5: identical decision in every CTA
+            const int status = *((volatile int*)a.status);
+            if (status != 0) return;
+            double sb = 0, wb = 0, sa = 0, wa = 0;
+            for (int c = 0; c < G; ++c) {
+                const double* pt = a.partials + (size_t)c * pstride + nent + np;
+                sb += pt[0];
+                wb += pt[1];
+                sa += pt[2];
+                wa += pt[3];
+            }
+            const double before = wb > 0 ? sqrt(sb / wb) : 0.0;
+            const double after = wa > 0 ? sqrt(sa / wa) : 0.0;
+            const double thr = 1.5 * before + 1e-9;
+            bool accept, reject = false;
+            if (structure || a.gn_step_mode) {
+                accept = true;
+            } else if (attempt == 0) {
+                accept = !(after > thr);
+            } else {
+                accept = after <= thr;
+            }
+            if (!accept && !structure && !a.gn_step_mode) {
+                if (attempt < 3) {
+                    ++attempt;
+                    // every CTA must finish reading the partials before any
+                    // CTA overwrites them in the retry's assembly
+                    grid.sync();
+                    continue;
+                }
+                reject = true;
+            }
+            if (b == 0 && tid == 0 && !structure) {
+                int n = *a.n_norms;
+                if (a.gn_step_mode) {
+                    a.residual_norms[n++] = before;
+                    a.residual_norms[n++] = after;
+                } else {
+                    if (n == 0) a.residual_norms[n++] = before;
+                    a.residual_norms[n++] = reject ? before : after;
+                }
+                *a.n_norms = n;
+            }
+            if (!reject) {
+                if (b == 0)
+                    for (int i = tid; i < a.n_poses * 7; i += kThreads) a.poses[i] = a.cand_poses[i];
+                for (int k = k0 + tid; k < k1; k += kThreads) a.depth[k] = a.cand_depth[k];
+            }
+            grid.sync();
+            break;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Debug: dense damped normal equations in the reference's order (tests only).
+// ---------------------------------------------------------------------------
+__global__ void normal_equations_debug_kernel(BAParams a, double* H, double* bvec) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int np = 6 * a.n_free_poses, nd = a.n_free_depths, n = np + nd;
+    const Cam K{a.K[0], a.K[1], a.K[2], a.K[3]};
+    for (int i = 0; i < n * n; ++i) H[i] = 0.0;
+    for (int i = 0; i < n; ++i) bvec[i] = 0.0;
+    for (int e = 0; e < a.n_edges; ++e) {
+        const int k = a.e_patch[e];
+        const int src = a.patch_src[k], tgt = a.e_pose[e];
+        const Relative rel = relative_pose(se3_load(a.poses + 7 * src), se3_load(a.poses + 7 * tgt));
+        const CenterJac J = center_jacobians(rel, K, a.depth[k], a.patch_x[9 * k + 4], a.patch_y[9 * k + 4]);
+        const double r[2] = {J.cu - a.e_in[2 * e], J.cv - a.e_in[2 * e + 1]};
+        const double w[2] = {J.behind ? 0.0 : a.e_weight_in[2 * e], J.behind ? 0.0 : a.e_weight_in[2 * e + 1]};
+        if (w[0] == 0.0 && w[1] == 0.0) continue;
+        int off[3], cols[3];
+        const double* jac[3];
+        double jd[12] = {J.dd[0], 0, 0, 0, 0, 0, J.dd[1], 0, 0, 0, 0, 0};
+        int nb = 0;
+        const int si = a.pose_free_slot[src], sj = a.pose_free_slot[tgt], sd = a.depth_slot[k];
+        if (si >= 0) {
+            off[nb] = 6 * si;
+            cols[nb] = 6;
+            jac[nb++] = J.di;
+        }
+        if (sj >= 0) {
+            off[nb] = 6 * sj;
+            cols[nb] = 6;
+            jac[nb++] = J.dj;
+        }
+        if (sd >= 0) {
+            off[nb] = np + sd;
+            cols[nb] = 1;
+            jac[nb++] = jd;
+        }
+        for (int x = 0; x < nb; ++x) {
+            for (int ra = 0; ra < cols[x]; ++ra) {
+                const double t0 = jac[x][ra] * w[0], t1 = jac[x][6 + ra] * w[1];
+                bvec[off[x] + ra] -= t0 * r[0] + t1 * r[1];
+                for (int y = 0; y < nb; ++y)
+                    for (int rc = 0; rc < cols[y]; ++rc)
+                        H[(off[x] + ra) * n + off[y] + rc] += t0 * jac[y][rc] + t1 * jac[y][6 + rc];
+            }
+        }
+    }
+    for (int i = 0; i < n; ++i) H[i * n + i] += a.damping;
+}
+
+// ---------------------------------------------------------------------------
+// schur_solve on dense inputs (bundle_adjust.cpp:62-94), one CTA.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) schur_dense_kernel(int np, int nd, const double* hpp, const double* hpd,
+                                                               const double* hdd, const double* bp, const double* bd,
+                                                               double* dp, double* dd, double* system, int* status) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int tid = threadIdx.x;
+    __shared__ int s_bad;
+    if (tid == 0) s_bad = 0;
+    __syncthreads();
+    for (int k = tid; k < nd; k += kThreads)
+        if (hdd[k] <= 0) s_bad = 1;
+    __syncthreads();
+    if (s_bad) {
+        if (tid == 0) set_status(status, kDevNonPositiveDepth);
+        return;
+    }
+    const int nent = nent_of(np);
+    // reduced system into `system` (upper + rhs), then reuse the LDLT phase
+    for (int ent = tid; ent < nent; ent += kThreads) {
+        int ia = 0, rowlen = np, base = 0;
+        while (ent >= base + rowlen) {
+            base += rowlen;
+            --rowlen;
+            ++ia;
+        }
+        const int ib = ia + ent - base;
+        double s = 0;
+        for (int k = 0; k < nd; ++k) s += (hpd[ia * nd + k] * (1.0 / hdd[k])) * hpd[ib * nd + k];
+        system[ent] = hpp[ia * np + ib] - s;
+    }
+    for (int i = tid; i < np; i += kThreads) {
+        double s = 0;
+        for (int k = 0; k < nd; ++k) s += hpd[i * nd + k] * ((1.0 / hdd[k]) * bd[k]);
+        system[nent + i] = bp[i] - s;
+    }
+    __syncthreads();
+    __threadfence_block();
+    BAParams a;
+    a.system = system;
+    a.delta = dp;
+    a.status = status;
+    a.n_poses = 0;
+    const Layout L = make_layout(np);
+    phase_solve(a, smem, L, np, false);
+    __syncthreads();
+    if (*((volatile int*)status) != 0) return;
+    for (int k = tid; k < nd; k += kThreads) {
+        double s = 0;
+        for (int i = 0; i < np; ++i) s += hpd[i * nd + k] * dp[i];
+        const double v = (1.0 / hdd[k]) * (bd[k] - s);
+        if (!isfinite(v)) set_status(status, kDevNonFiniteDepth);
+        dd[k] = v;
+    }
+}
+
+// camera entry points: thread per item
+__global__ void reproject_kernel(int n, int pp, const double* pi, const double* pj, const double* Kd, const double* x,
+                                 const double* y, const double* d, double* out, uint8_t* behind) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const SE3 a = se3_load(pi + 7 * i), b = se3_load(pj + 7 * i);
+    const Cam K{Kd[0], Kd[1], Kd[2], Kd[3]};
+    if (se3_equal(a, b)) {
+        for (int k = 0; k < pp; ++k) {
+            out[((size_t)i * pp + k) * 2] = x[(size_t)i * pp + k];
+            out[((size_t)i * pp + k) * 2 + 1] = y[(size_t)i * pp + k];
+        }
+        behind[i] = 0;
+        return;
+    }
+    const Relative rel = relative_pose(a, b);
+    bool bh = false;
+    for (int k = 0; k < pp; ++k) {
+        double u, v;
+        const double qz = reproject_point(rel, K, d[i], x[(size_t)i * pp + k], y[(size_t)i * pp + k], &u, &v);
+        if (qz <= kDepthEpsilon) bh = true;
+        out[((size_t)i * pp + k) * 2] = u;
+        out[((size_t)i * pp + k) * 2 + 1] = v;
+    }
+    behind[i] = bh ? 1 : 0;
+}
+
+__global__ void jacobians_kernel(int n, int pp, const double* pi, const double* pj, const double* Kd, const double* x,
+                                 const double* y, const double* d, double* out, uint8_t* behind) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const Cam K{Kd[0], Kd[1], Kd[2], Kd[3]};
+    // Patch::center (camera.cpp:34-45)
+    double cx, cy;
+    const int p = (int)lround(sqrt((double)pp));
+    if (p % 2 == 1) {
+        cx = x[(size_t)i * pp + pp / 2];
+        cy = y[(size_t)i * pp + pp / 2];
+    } else {
+        double sx = 0, sy = 0;
+        for (int k = 0; k < pp; ++k) {
+            sx += x[(size_t)i * pp + k];
+            sy += y[(size_t)i * pp + k];
+        }
+        cx = sx / pp;
+        cy = sy / pp;
+    }
+    const Relative rel = relative_pose(se3_load(pi + 7 * i), se3_load(pj + 7 * i));
+    const CenterJac J = center_jacobians(rel, K, d[i], cx, cy);
+    double* o = out + (size_t)i * 28;
+    o[0] = J.cu;
+    o[1] = J.cv;
+    for (int c = 0; c < 12; ++c) {
+        o[2 + c] = J.di[c];
+        o[14 + c] = J.dj[c];
+    }
+    o[26] = J.dd[0];
+    o[27] = J.dd[1];
+    behind[i] = J.behind ? 1 : 0;
+}
+
+}  // namespace
+
+int ba_max_free_poses() { return kMaxFree; }
+int ba_max_edges_per_patch() { return kMaxEdges; }
+
+size_t ba_partials_doubles(int n_free_poses, int grid) {
+    const int np = 6 * n_free_poses;
+    return (size_t)grid * ((size_t)nent_of(np) + np + 4);
+}
+
+static int ba_blocks_per_sm_cached(int smem) {
+    int blocks = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, ba_kernel, kThreads, smem) != cudaSuccess) return 1;
+    return blocks > 0 ? blocks : 1;
+}
+
+int ba_grid_size(int n_patches, int n_free_poses, int num_sms) {
+    const int np = 6 * n_free_poses;
+    const Layout L = make_layout(np);
+    cudaFuncSetAttribute(ba_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
+    const int per_sm = ba_blocks_per_sm_cached(L.total);
+    int g = (n_patches + kWarps - 1) / kWarps;
+    if (g > num_sms * per_sm) g = num_sms * per_sm;
+    if (g < 1) g = 1;
+    return g;
+}
+
+cudaError_t launch_ba(BAParams& p, int num_sms, cudaStream_t stream, int* grid_out) {
+    if (p.n_free_poses > kMaxFree) return cudaErrorNotSupported;
+    const int np = 6 * p.n_free_poses;
+    const Layout L = make_layout(np);
+    cudaError_t err = cudaFuncSetAttribute(ba_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
+    if (err != cudaSuccess) return err;
+    const int grid = ba_grid_size(p.n_patches, p.n_free_poses, num_sms);
+    if (grid_out) *grid_out = grid;
+    void* args[] = {&p};
+    return cudaLaunchCooperativeKernel((void*)ba_kernel, dim3(grid), dim3(kThreads), args, L.total, stream);
+}
+
+cudaError_t launch_normal_equations_debug(const BAParams& p, double* h, double* b, cudaStream_t stream) {
+    normal_equations_debug_kernel<<<1, 32, 0, stream>>>(p, h, b);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_schur_dense(int np, int nd, const double* hpp, const double* hpd, const double* hdd,
+                               const double* bp, const double* bd, double* dp, double* dd, int* status,
+                               cudaStream_t stream) {
+    if (np > kMaxNp) return cudaErrorNotSupported;
+    const Layout L = make_layout(np);
+    const int smem = L.solve_total;
+    cudaError_t err = cudaFuncSetAttribute(schur_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err != cudaSuccess) return err;
+    // `system` scratch lives right after dd in the caller's buffer (see capi.cu)
+    double* system = dd + nd;
+    schur_dense_kernel<<<1, kThreads, smem, stream>>>(np, nd, hpp, hpd, hdd, bp, bd, dp, dd, system, status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reproject(int n, int pp, const double* pi, const double* pj, const double* K, const double* x,
+                             const double* y, const double* d, double* out, uint8_t* behind, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    reproject_kernel<<<(n + 127) / 128, 128, 0, stream>>>(n, pp, pi, pj, K, x, y, d, out, behind);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_jacobians(int n, int pp, const double* pi, const double* pj, const double* K, const double* x,
+                             const double* y, const double* d, double* out, uint8_t* behind, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    jacobians_kernel<<<(n + 127) / 128, 128, 0, stream>>>(n, pp, pi, pj, K, x, y, d, out, behind);
+    return cudaGetLastError();
+}
+
+}  // namespace pvo_dev

@@ -1,0 +1,908 @@
+// capi.cu — the extern "C" boundary (include/pvo_capi.h): context, frame
+// store, correlation, camera, bundle adjustment and the resident window.
+//
+// The host code here only validates, flattens and moves memory; every
+// numeric result comes from the sm_100a kernels in corr.cu / ba.cu.  There
+// is deliberately no CPU compute fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "geometry.cuh"
+#include "internal.hpp"
+#include "kernels.cuh"
+
+using namespace pvo_host;
+
+namespace pvo_host {
+namespace {
+thread_local std::string g_last_error;
+}
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace pvo_host
+
+struct BABuffers {
+    DevBuf poses, free_slot, patch_src, px, py, depth, depth_slot, edge_begin, e_patch, e_pose, e_in, e_w, e_target,
+        e_weight, cand_poses, cand_depth, patch_v, patch_h, patch_bd, partials, system, delta, norms, n_norms, dbg_h,
+        dbg_b, K;
+    void release() {
+        DevBuf* all[] = {&poses,    &free_slot,  &patch_src, &px,        &py,       &depth,    &depth_slot,
+                         &edge_begin, &e_patch,  &e_pose,    &e_in,      &e_w,      &e_target, &e_weight,
+                         &cand_poses, &cand_depth, &patch_v, &patch_h,   &patch_bd, &partials, &system,
+                         &delta,    &norms,      &n_norms,   &dbg_h,     &dbg_b,    &K};
+        for (DevBuf* b : all) b->release();
+    }
+};
+
+// Host-side plan of a flattened problem (edges grouped by patch).
+struct Plan {
+    int n_free_poses = 0, n_free_depths = 0;
+    std::vector<int> free_slot, depth_slot, edge_begin, perm;  // perm: sorted edge -> input edge
+    bool sorted = true;
+};
+
+struct Window {
+    bool loaded = false;
+    int n_poses = 0, n_patches = 0, n_edges = 0;
+    Plan plan;
+    HostProblem shape;  // sizes, K, image size (pointers unused)
+    DevBuf pose_slot, patch_feats, corr, init_poses, init_depth;
+};
+
+struct pvo_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int num_sms = 0;
+    int64_t launches = 0;
+    int* d_status = nullptr;
+    // frame store
+    int nf = 0, w0 = 0, h0 = 0, w1 = 0, h1 = 0, C = 0;
+    DevBuf feat0, feat1, gram0, gram1;
+    // direct-op scratch
+    DevBuf s0, s1, s2, s3, s4, s5, s6, s7, s8;
+    BABuffers ba;
+    Window win;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    bool timing_pending = false;
+};
+
+namespace {
+
+void bind(pvo_ctx* ctx) {
+    if (!ctx) fail(PVO_INVALID_ARGUMENT, "null context");
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+}
+
+template <typename T>
+T* upload(pvo_ctx* ctx, DevBuf& buf, const T* host, size_t count) {
+    T* d = buf.as<T>(count);
+    if (count) cuda_check(cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    return d;
+}
+template <typename T>
+void download(pvo_ctx* ctx, T* host, const T* dev, size_t count) {
+    if (count) cuda_check(cudaMemcpyAsync(host, dev, count * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+}
+void sync(pvo_ctx* ctx) { cuda_check(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize"); }
+
+void reset_status(pvo_ctx* ctx) {
+    cuda_check(cudaMemsetAsync(ctx->d_status, 0, sizeof(int), ctx->stream), "status reset");
+}
+int read_status(pvo_ctx* ctx) {
+    int s = 0;
+    cuda_check(cudaMemcpyAsync(&s, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "status");
+    sync(ctx);
+    return s;
+}
+// BA status bits -> the reference's exception (bundle_adjust.cpp:65-92, :147-149).
+void raise_ba_status(int s) {
+    if (!s) return;
+    using namespace pvo_dev;
+    if (s & (1 << kDevNonFiniteResidual)) fail(PVO_DEGENERATE, "ba: non-finite residual");
+    if (s & (1 << kDevNonPositiveDepth)) fail(PVO_DEGENERATE, "schur: non-positive damped depth-block entry");
+    if (s & (1 << kDevFactorization)) fail(PVO_DEGENERATE, "schur: reduced camera system factorization failed");
+    if (s & (1 << kDevNonFinitePose)) fail(PVO_DEGENERATE, "schur: non-finite pose update");
+    if (s & (1 << kDevNonFiniteDepth)) fail(PVO_DEGENERATE, "schur: non-finite depth update");
+    fail(PVO_CUDA_ERROR, "unknown device status");
+}
+
+bool finite2(const double* v) { return std::isfinite(v[0]) && std::isfinite(v[1]); }
+
+// BAProblem::validate (bundle_adjust.cpp:11-36).
+void validate(const HostProblem& pr) {
+    if (pr.n_poses < 0 || pr.n_patches < 0 || pr.n_edges < 0) fail(PVO_INVALID_ARGUMENT, "ba: negative size");
+    for (int e = 0; e < pr.n_edges; ++e) {
+        if (pr.e_patch[e] < 0 || pr.e_patch[e] >= pr.n_patches || pr.e_pose[e] < 0 || pr.e_pose[e] >= pr.n_poses) {
+            fail(PVO_INVALID_ARGUMENT, "ba: edge references an unknown patch or pose");
+        }
+        if (!finite2(pr.e_in + 2 * e)) fail(PVO_INVALID_ARGUMENT, "ba: non-finite edge target");
+        const double wx = pr.e_w[2 * e], wy = pr.e_w[2 * e + 1];
+        if (wx < 0 || wx >= 1 || wy < 0 || wy >= 1) fail(PVO_INVALID_ARGUMENT, "ba: edge weights must lie in [0, 1)");
+    }
+    for (int k = 0; k < pr.n_patches; ++k) {
+        if (pr.src[k] < 0 || pr.src[k] >= pr.n_poses) fail(PVO_INVALID_ARGUMENT, "ba: patch source pose out of range");
+    }
+}
+
+Plan make_plan(const HostProblem& pr, bool all_fixed) {
+    Plan pl;
+    pl.free_slot.assign(pr.n_poses, -1);
+    for (int i = 0; i < pr.n_poses; ++i)
+        if (!all_fixed && !pr.fixed[i]) pl.free_slot[i] = pl.n_free_poses++;
+    pl.depth_slot.assign(pr.n_patches, -1);
+    for (int k = 0; k < pr.n_patches; ++k)
+        if (!pr.depth_free || pr.depth_free[k]) pl.depth_slot[k] = pl.n_free_depths++;
+    // group edges by patch (stable): the kernel runs a warp per patch
+    std::vector<int> count(pr.n_patches + 1, 0);
+    for (int e = 0; e < pr.n_edges; ++e) count[pr.e_patch[e] + 1]++;
+    pl.edge_begin.assign(pr.n_patches + 1, 0);
+    for (int k = 0; k < pr.n_patches; ++k) pl.edge_begin[k + 1] = pl.edge_begin[k] + count[k + 1];
+    std::vector<int> fill(pl.edge_begin.begin(), pl.edge_begin.end() - 1);
+    pl.perm.assign(pr.n_edges, 0);
+    for (int e = 0; e < pr.n_edges; ++e) {
+        const int pos = fill[pr.e_patch[e]]++;
+        pl.perm[pos] = e;
+        if (pos != e) pl.sorted = false;
+    }
+    int max_edges = 0;
+    for (int k = 0; k < pr.n_patches; ++k) max_edges = std::max(max_edges, pl.edge_begin[k + 1] - pl.edge_begin[k]);
+    if (max_edges > pvo_dev::ba_max_edges_per_patch()) {
+        fail(PVO_UNSUPPORTED, "ba: more than " + std::to_string(pvo_dev::ba_max_edges_per_patch()) +
+                                  " edges on one patch");
+    }
+    if (pl.n_free_poses > pvo_dev::ba_max_free_poses()) {
+        fail(PVO_UNSUPPORTED, "ba: more than " + std::to_string(pvo_dev::ba_max_free_poses()) +
+                                  " free poses in one window");
+    }
+    if (pr.p != 3) fail(PVO_UNSUPPORTED, "ba: the kernels implement 3x3 patches");
+    return pl;
+}
+
+// Upload the problem into ctx->ba and fill the kernel parameter block.
+pvo_dev::BAParams stage_problem(pvo_ctx* ctx, const HostProblem& pr, const Plan& pl, int extra_norms) {
+    BABuffers& B = ctx->ba;
+    const int pp = pr.p * pr.p;
+    pvo_dev::BAParams a;
+    a.n_poses = pr.n_poses;
+    a.n_patches = pr.n_patches;
+    a.n_edges = pr.n_edges;
+    a.n_free_poses = pl.n_free_poses;
+    a.n_free_depths = pl.n_free_depths;
+    a.poses = upload(ctx, B.poses, pr.poses, (size_t)pr.n_poses * 7);
+    a.pose_free_slot = upload(ctx, B.free_slot, pl.free_slot.data(), pl.free_slot.size());
+    a.patch_src = upload(ctx, B.patch_src, pr.src, pr.n_patches);
+    a.patch_x = upload(ctx, B.px, pr.px, (size_t)pr.n_patches * pp);
+    a.patch_y = upload(ctx, B.py, pr.py, (size_t)pr.n_patches * pp);
+    a.depth = upload(ctx, B.depth, pr.depth, pr.n_patches);
+    a.depth_slot = upload(ctx, B.depth_slot, pl.depth_slot.data(), pl.depth_slot.size());
+    a.patch_edge_begin = upload(ctx, B.edge_begin, pl.edge_begin.data(), pl.edge_begin.size());
+    if (pl.sorted) {
+        a.e_patch = upload(ctx, B.e_patch, pr.e_patch, pr.n_edges);
+        a.e_pose = upload(ctx, B.e_pose, pr.e_pose, pr.n_edges);
+        a.e_in = upload(ctx, B.e_in, pr.e_in, (size_t)pr.n_edges * 2);
+        a.e_weight_in = upload(ctx, B.e_w, pr.e_w, (size_t)pr.n_edges * 2);
+    } else {
+        std::vector<int> ep(pr.n_edges), eo(pr.n_edges);
+        std::vector<double> ein(2 * (size_t)pr.n_edges), ew(2 * (size_t)pr.n_edges);
+        for (int i = 0; i < pr.n_edges; ++i) {
+            const int e = pl.perm[i];
+            ep[i] = pr.e_patch[e];
+            eo[i] = pr.e_pose[e];
+            ein[2 * i] = pr.e_in[2 * e];
+            ein[2 * i + 1] = pr.e_in[2 * e + 1];
+            ew[2 * i] = pr.e_w[2 * e];
+            ew[2 * i + 1] = pr.e_w[2 * e + 1];
+        }
+        a.e_patch = upload(ctx, B.e_patch, ep.data(), ep.size());
+        a.e_pose = upload(ctx, B.e_pose, eo.data(), eo.size());
+        a.e_in = upload(ctx, B.e_in, ein.data(), ein.size());
+        a.e_weight_in = upload(ctx, B.e_w, ew.data(), ew.size());
+        sync(ctx);  // the temporaries die here
+    }
+    const int np = 6 * pl.n_free_poses;
+    a.e_target = B.e_target.as<double>((size_t)pr.n_edges * 2);
+    a.e_weight = B.e_weight.as<double>((size_t)pr.n_edges * 2);
+    a.cand_poses = B.cand_poses.as<double>((size_t)pr.n_poses * 7);
+    a.cand_depth = B.cand_depth.as<double>(pr.n_patches);
+    a.patch_v = B.patch_v.as<double>((size_t)pr.n_patches * std::max(np, 1));
+    a.patch_h = B.patch_h.as<double>(pr.n_patches);
+    a.patch_bd = B.patch_bd.as<double>(pr.n_patches);
+    const int grid = pvo_dev::ba_grid_size(pr.n_patches, pl.n_free_poses, ctx->num_sms);
+    a.partials = B.partials.as<double>(pvo_dev::ba_partials_doubles(pl.n_free_poses, grid));
+    a.system = B.system.as<double>((size_t)np * (np + 1) / 2 + np + 1);
+    a.delta = B.delta.as<double>(std::max(np, 1));
+    a.residual_norms = B.norms.as<double>(2 + extra_norms);
+    a.n_norms = B.n_norms.as<int>(1);
+    a.status = ctx->d_status;
+    std::memcpy(a.K, pr.K, sizeof(a.K));
+    a.image_w = pr.image_w;
+    a.image_h = pr.image_h;
+    a.damping = pr.damping;
+    return a;
+}
+
+void launch_ba_checked(pvo_ctx* ctx, pvo_dev::BAParams& a) {
+    cuda_check(cudaMemsetAsync(a.n_norms, 0, sizeof(int), ctx->stream), "memset");
+    int grid = 0;
+    cuda_check(pvo_dev::launch_ba(a, ctx->num_sms, ctx->stream, &grid), "ba kernel");
+    ctx->launches += 1;
+}
+
+void ensure_p3(int p) {
+    if (p != 3) fail(PVO_UNSUPPORTED, "the sm_100a kernels implement 3x3 patches (p = 3)");
+}
+
+void compute_gram(pvo_ctx* ctx, const float* f0, float* g0, const float* f1, float* g1, int w0, int h0, int w1,
+                  int h1, int C) {
+    if (w0 * h0 > 0) {
+        cuda_check(pvo_dev::launch_gram(f0, g0, w0, h0, C, ctx->num_sms, ctx->stream), "gram kernel");
+        ctx->launches += 1;
+    }
+    if (w1 * h1 > 0) {
+        cuda_check(pvo_dev::launch_gram(f1, g1, w1, h1, C, ctx->num_sms, ctx->stream), "gram kernel");
+        ctx->launches += 1;
+    }
+}
+
+}  // namespace
+
+namespace pvo_host {
+
+void run_ba(pvo_ctx* ctx, const HostProblem& pr, const BARun& run) {
+    bind(ctx);
+    validate(pr);
+    if (run.gn_step_mode && pr.n_edges == 0) fail(PVO_INVALID_ARGUMENT, "ba: need at least one edge");
+    const Plan pl = make_plan(pr, false);
+    if (run.n_free_poses) *run.n_free_poses = pl.n_free_poses;
+    if (run.n_free_depths) *run.n_free_depths = pl.n_free_depths;
+    if (pr.n_edges == 0) {
+        // nothing to optimise: state unchanged
+        std::memcpy(run.out_poses, pr.poses, sizeof(double) * 7 * pr.n_poses);
+        std::memcpy(run.out_depth, pr.depth, sizeof(double) * pr.n_patches);
+        if (run.n_norms) *run.n_norms = 0;
+        return;
+    }
+    pvo_dev::BAParams a = stage_problem(ctx, pr, pl, run.iterations + run.structure_only + 2);
+    a.freeze_targets = run.freeze_targets;
+    a.iterations = run.iterations;
+    a.structure_only = run.structure_only;
+    a.gn_step_mode = run.gn_step_mode;
+    reset_status(ctx);
+    if (run.debug_h || run.debug_b) {
+        const int n = 6 * pl.n_free_poses + pl.n_free_depths;
+        double* dh = ctx->ba.dbg_h.as<double>((size_t)n * n);
+        double* db = ctx->ba.dbg_b.as<double>(n);
+        cuda_check(pvo_dev::launch_normal_equations_debug(a, dh, db, ctx->stream), "debug kernel");
+        ctx->launches += 1;
+        if (run.debug_h) download(ctx, run.debug_h, dh, (size_t)n * n);
+        if (run.debug_b) download(ctx, run.debug_b, db, n);
+    }
+    launch_ba_checked(ctx, a);
+    const int status = read_status(ctx);
+    raise_ba_status(status);
+    download(ctx, run.out_poses, a.poses, (size_t)pr.n_poses * 7);
+    download(ctx, run.out_depth, a.depth, pr.n_patches);
+    int n_norms = 0;
+    download(ctx, &n_norms, a.n_norms, 1);
+    sync(ctx);
+    if (run.residual_norms && n_norms > 0) {
+        download(ctx, run.residual_norms, a.residual_norms, n_norms);
+        sync(ctx);
+    }
+    if (run.n_norms) *run.n_norms = n_norms;
+}
+
+}  // namespace pvo_host
+
+// ===========================================================================
+// extern "C"
+// ===========================================================================
+extern "C" {
+
+int pvo_version(void) { return 1; }
+const char* pvo_last_error(void) { return pvo_host::g_last_error.c_str(); }
+
+const char* pvo_status_string(int status) {
+    switch (status) {
+        case PVO_OK: return "ok";
+        case PVO_INVALID_ARGUMENT: return "invalid_argument";
+        case PVO_DEGENERATE: return "degenerate_problem";
+        case PVO_DOMAIN_ERROR: return "domain_error";
+        case PVO_OUT_OF_RANGE: return "out_of_range";
+        case PVO_CUDA_ERROR: return "cuda_error";
+        case PVO_UNSUPPORTED: return "unsupported";
+        default: return "unknown";
+    }
+}
+
+int pvo_ctx_create(int device, pvo_ctx** out) {
+    return guarded([&] {
+        if (!out) fail(PVO_INVALID_ARGUMENT, "null output");
+        *out = nullptr;
+        int n = 0;
+        cuda_check(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+        if (device < 0 || device >= n) fail(PVO_CUDA_ERROR, "no CUDA device " + std::to_string(device));
+        cudaDeviceProp prop{};
+        cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+        if (prop.major < 10) {
+            fail(PVO_CUDA_ERROR, std::string("device ") + prop.name + " is not sm_100 (kernels are built for sm_100a)");
+        }
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        auto* ctx = new pvo_ctx();
+        ctx->device = device;
+        ctx->num_sms = prop.multiProcessorCount;
+        cuda_check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        ctx->own_stream = true;
+        cuda_check(cudaMalloc(&ctx->d_status, sizeof(int)), "cudaMalloc");
+        for (auto& e : ctx->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+        *out = ctx;
+    });
+}
+
+int pvo_ctx_destroy(pvo_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        DevBuf* bufs[] = {&ctx->feat0, &ctx->feat1, &ctx->gram0, &ctx->gram1, &ctx->s0, &ctx->s1, &ctx->s2,
+                          &ctx->s3,    &ctx->s4,    &ctx->s5,    &ctx->s6,    &ctx->s7, &ctx->s8,
+                          &ctx->win.pose_slot, &ctx->win.patch_feats, &ctx->win.corr, &ctx->win.init_poses,
+                          &ctx->win.init_depth};
+        for (DevBuf* b : bufs) b->release();
+        ctx->ba.release();
+        if (ctx->d_status) cudaFree(ctx->d_status);
+        for (auto& e : ctx->ev)
+            if (e) cudaEventDestroy(e);
+        if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+int pvo_ctx_set_stream(pvo_ctx* ctx, void* stream) {
+    return guarded([&] {
+        bind(ctx);
+        if (ctx->own_stream) {
+            cudaStreamSynchronize(ctx->stream);
+            cudaStreamDestroy(ctx->stream);
+            ctx->own_stream = false;
+        }
+        if (stream) {
+            ctx->stream = static_cast<cudaStream_t>(stream);
+        } else {
+            cuda_check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            ctx->own_stream = true;
+        }
+    });
+}
+
+int pvo_ctx_synchronize(pvo_ctx* ctx) {
+    return guarded([&] {
+        bind(ctx);
+        sync(ctx);
+    });
+}
+
+int64_t pvo_ctx_kernel_launches(pvo_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int pvo_ctx_last_timing(pvo_ctx* ctx, double* corr_ms, double* ba_ms) {
+    return guarded([&] {
+        bind(ctx);
+        if (!ctx->timing_pending) fail(PVO_INVALID_ARGUMENT, "no timed iteration recorded");
+        cuda_check(cudaEventSynchronize(ctx->ev[2]), "cudaEventSynchronize");
+        float a = 0, b = 0;
+        cuda_check(cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]), "cudaEventElapsedTime");
+        cuda_check(cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]), "cudaEventElapsedTime");
+        if (corr_ms) *corr_ms = a;
+        if (ba_ms) *ba_ms = b;
+    });
+}
+
+// ---- SE(3) host utilities ------------------------------------------------
+int pvo_se3_exp(const double* xi, double* out) {
+    return guarded([&] { pvo_dev::se3_store(pvo_dev::se3_exp(xi), out); });
+}
+int pvo_se3_log(const double* pose, double* xi) {
+    return guarded([&] { se3_log_host(pose, xi); });
+}
+int pvo_se3_compose(const double* a, const double* b, double* out) {
+    return guarded([&] {
+        pvo_dev::se3_store(pvo_dev::se3_compose(pvo_dev::se3_load(a), pvo_dev::se3_load(b)), out);
+    });
+}
+int pvo_se3_inverse(const double* a, double* out) {
+    return guarded([&] { pvo_dev::se3_store(pvo_dev::se3_inverse(pvo_dev::se3_load(a)), out); });
+}
+int pvo_se3_retract(const double* a, const double* xi, double* out) {
+    return guarded([&] { pvo_dev::se3_store(pvo_dev::se3_retract(pvo_dev::se3_load(a), xi), out); });
+}
+
+// ---- camera ----------------------------------------------------------------
+int pvo_reproject_patches(pvo_ctx* ctx, int n, int p, const double* pi, const double* pj, const double* K,
+                          const double* x, const double* y, const double* d, double* out_xy, uint8_t* behind) {
+    return guarded([&] {
+        bind(ctx);
+        if (n < 0 || p < 1) fail(PVO_INVALID_ARGUMENT, "reproject: bad sizes");
+        if (n == 0) return;
+        const int pp = p * p;
+        double* dpi = upload(ctx, ctx->s0, pi, (size_t)n * 7);
+        double* dpj = upload(ctx, ctx->s1, pj, (size_t)n * 7);
+        double* dK = upload(ctx, ctx->s2, K, 4);
+        double* dx = upload(ctx, ctx->s3, x, (size_t)n * pp);
+        double* dy = upload(ctx, ctx->s4, y, (size_t)n * pp);
+        double* dd = upload(ctx, ctx->s5, d, n);
+        double* dout = ctx->s6.as<double>((size_t)n * pp * 2);
+        uint8_t* db = ctx->s7.as<uint8_t>(n);
+        cuda_check(pvo_dev::launch_reproject(n, pp, dpi, dpj, dK, dx, dy, dd, dout, db, ctx->stream), "reproject");
+        ctx->launches += 1;
+        download(ctx, out_xy, dout, (size_t)n * pp * 2);
+        download(ctx, behind, db, n);
+        sync(ctx);
+    });
+}
+
+int pvo_reprojection_jacobians(pvo_ctx* ctx, int n, int p, const double* pi, const double* pj, const double* K,
+                               const double* x, const double* y, const double* d, double* out, uint8_t* behind) {
+    return guarded([&] {
+        bind(ctx);
+        if (n < 0 || p < 1) fail(PVO_INVALID_ARGUMENT, "jacobians: bad sizes");
+        if (n == 0) return;
+        const int pp = p * p;
+        double* dpi = upload(ctx, ctx->s0, pi, (size_t)n * 7);
+        double* dpj = upload(ctx, ctx->s1, pj, (size_t)n * 7);
+        double* dK = upload(ctx, ctx->s2, K, 4);
+        double* dx = upload(ctx, ctx->s3, x, (size_t)n * pp);
+        double* dy = upload(ctx, ctx->s4, y, (size_t)n * pp);
+        double* dd = upload(ctx, ctx->s5, d, n);
+        double* dout = ctx->s6.as<double>((size_t)n * 28);
+        uint8_t* db = ctx->s7.as<uint8_t>(n);
+        cuda_check(pvo_dev::launch_jacobians(n, pp, dpi, dpj, dK, dx, dy, dd, dout, db, ctx->stream), "jacobians");
+        ctx->launches += 1;
+        download(ctx, out, dout, (size_t)n * 28);
+        download(ctx, behind, db, n);
+        sync(ctx);
+    });
+}
+
+// ---- correlation -------------------------------------------------------------
+int pvo_correlate(pvo_ctx* ctx, int p, int C, const float* feats0, const float* feats1, const float* level0, int w0,
+                  int h0, const float* level1, int w1, int h1, const double* coords, float* out) {
+    return guarded([&] {
+        bind(ctx);
+        ensure_p3(p);
+        if (C < 1 || w0 < 0 || h0 < 0 || w1 < 0 || h1 < 0) fail(PVO_INVALID_ARGUMENT, "correlate: bad sizes");
+        for (int k = 0; k < p * p; ++k)
+            if (!finite2(coords + 2 * k)) fail(PVO_INVALID_ARGUMENT, "correlate: non-finite reprojection");
+        const size_t n0 = (size_t)w0 * h0 * C, n1 = (size_t)w1 * h1 * C;
+        float* f0 = upload(ctx, ctx->s0, level0, n0);
+        float* f1 = upload(ctx, ctx->s1, level1, n1);
+        float* g0 = ctx->s2.as<float>((size_t)w0 * h0 * 8);
+        float* g1 = ctx->s3.as<float>((size_t)w1 * h1 * 8);
+        compute_gram(ctx, f0, g0, f1, g1, w0, h0, w1, h1, C);
+        float* pf = ctx->s4.as<float>((size_t)2 * 9 * C);
+        cuda_check(cudaMemcpyAsync(pf, feats0, sizeof(float) * 9 * C, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+        cuda_check(cudaMemcpyAsync(pf + 9 * C, feats1, sizeof(float) * 9 * C, cudaMemcpyHostToDevice, ctx->stream),
+                   "H2D");
+        double* dc = upload(ctx, ctx->s5, coords, 18);
+        int zero = 0;
+        int* idx = upload(ctx, ctx->s6, &zero, 1);
+        float* dout = ctx->s7.as<float>(2 * 9 * 49);
+        reset_status(ctx);
+        pvo_dev::CorrParams cp;
+        cp.n_edges = 1;
+        cp.channels = C;
+        cp.e_patch = idx;
+        cp.e_slot = idx;
+        cp.coords = dc;
+        cp.feat0 = f0;
+        cp.feat1 = f1;
+        cp.gram0 = g0;
+        cp.gram1 = g1;
+        cp.w0 = w0;
+        cp.h0 = h0;
+        cp.w1 = w1;
+        cp.h1 = h1;
+        cp.patch_feats = pf;
+        cp.out = dout;
+        cp.status = ctx->d_status;
+        cuda_check(pvo_dev::launch_corr(cp, ctx->stream), "corr kernel");
+        ctx->launches += 1;
+        download(ctx, out, dout, 2 * 9 * 49);
+        if (read_status(ctx)) fail(PVO_INVALID_ARGUMENT, "correlate: non-finite reprojection");
+    });
+}
+
+int pvo_frames_reserve(pvo_ctx* ctx, int n_frames, int w0, int h0, int w1, int h1, int C) {
+    return guarded([&] {
+        bind(ctx);
+        if (n_frames < 1 || w0 < 1 || h0 < 1 || w1 < 0 || h1 < 0 || C < 1) fail(PVO_INVALID_ARGUMENT, "frames: bad sizes");
+        ctx->nf = n_frames;
+        ctx->w0 = w0;
+        ctx->h0 = h0;
+        ctx->w1 = w1;
+        ctx->h1 = h1;
+        ctx->C = C;
+        ctx->feat0.get(sizeof(float) * (size_t)n_frames * w0 * h0 * C);
+        ctx->feat1.get(sizeof(float) * (size_t)n_frames * std::max(w1 * h1, 1) * C);
+        ctx->gram0.get(sizeof(float) * (size_t)n_frames * w0 * h0 * 8);
+        ctx->gram1.get(sizeof(float) * (size_t)n_frames * std::max(w1 * h1, 1) * 8);
+    });
+}
+
+int pvo_frames_refresh(pvo_ctx* ctx, int slot) {
+    return guarded([&] {
+        bind(ctx);
+        if (slot < 0 || slot >= ctx->nf) fail(PVO_OUT_OF_RANGE, "frames: slot out of range");
+        const size_t c0 = (size_t)ctx->w0 * ctx->h0, c1 = (size_t)ctx->w1 * ctx->h1;
+        float* f0 = static_cast<float*>(ctx->feat0.p) + slot * c0 * ctx->C;
+        float* f1 = static_cast<float*>(ctx->feat1.p) + slot * c1 * ctx->C;
+        float* g0 = static_cast<float*>(ctx->gram0.p) + slot * c0 * 8;
+        float* g1 = static_cast<float*>(ctx->gram1.p) + slot * c1 * 8;
+        compute_gram(ctx, f0, g0, f1, g1, ctx->w0, ctx->h0, ctx->w1, ctx->h1, ctx->C);
+    });
+}
+
+int pvo_frames_upload(pvo_ctx* ctx, int slot, const float* level0, const float* level1, int memspace) {
+    return guarded([&] {
+        bind(ctx);
+        if (slot < 0 || slot >= ctx->nf) fail(PVO_OUT_OF_RANGE, "frames: slot out of range");
+        const size_t c0 = (size_t)ctx->w0 * ctx->h0, c1 = (size_t)ctx->w1 * ctx->h1;
+        float* f0 = static_cast<float*>(ctx->feat0.p) + slot * c0 * ctx->C;
+        float* f1 = static_cast<float*>(ctx->feat1.p) + slot * c1 * ctx->C;
+        const cudaMemcpyKind kind = memspace == PVO_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        cuda_check(cudaMemcpyAsync(f0, level0, sizeof(float) * c0 * ctx->C, kind, ctx->stream), "frame upload");
+        if (c1) cuda_check(cudaMemcpyAsync(f1, level1, sizeof(float) * c1 * ctx->C, kind, ctx->stream), "frame upload");
+        float* g0 = static_cast<float*>(ctx->gram0.p) + slot * c0 * 8;
+        float* g1 = static_cast<float*>(ctx->gram1.p) + slot * c1 * 8;
+        compute_gram(ctx, f0, g0, f1, g1, ctx->w0, ctx->h0, ctx->w1, ctx->h1, ctx->C);
+        if (memspace != PVO_DEVICE) sync(ctx);
+    });
+}
+
+int pvo_frames_device_ptrs(pvo_ctx* ctx, float** level0, float** level1) {
+    return guarded([&] {
+        bind(ctx);
+        if (level0) *level0 = static_cast<float*>(ctx->feat0.p);
+        if (level1) *level1 = static_cast<float*>(ctx->feat1.p);
+    });
+}
+
+int pvo_correlate_batch(pvo_ctx* ctx, int n_edges, int n_patches, int p, const int* e_patch, const int* e_slot,
+                        const double* coords, const float* patch_feats, float* out, int memspace) {
+    return guarded([&] {
+        bind(ctx);
+        ensure_p3(p);
+        if (ctx->nf == 0) fail(PVO_INVALID_ARGUMENT, "correlate_batch: frame store is empty (pvo_frames_reserve)");
+        if (n_edges < 0 || n_patches < 0) fail(PVO_INVALID_ARGUMENT, "correlate_batch: bad sizes");
+        if (n_edges == 0) return;
+        const int C = ctx->C;
+        const int* dep;
+        const int* des;
+        const double* dc;
+        const float* dpf;
+        float* dout;
+        if (memspace == PVO_DEVICE) {
+            dep = e_patch;
+            des = e_slot;
+            dc = coords;
+            dpf = patch_feats;
+            dout = out;
+        } else {
+            for (int e = 0; e < n_edges; ++e) {
+                if (e_patch[e] < 0 || e_patch[e] >= n_patches) fail(PVO_OUT_OF_RANGE, "correlate_batch: bad patch index");
+                if (e_slot[e] < 0 || e_slot[e] >= ctx->nf) fail(PVO_OUT_OF_RANGE, "correlate_batch: bad frame slot");
+            }
+            dep = upload(ctx, ctx->s0, e_patch, n_edges);
+            des = upload(ctx, ctx->s1, e_slot, n_edges);
+            dc = upload(ctx, ctx->s2, coords, (size_t)n_edges * 18);
+            dpf = upload(ctx, ctx->s3, patch_feats, (size_t)n_patches * 2 * 9 * C);
+            dout = ctx->s4.as<float>((size_t)n_edges * 2 * 9 * 49);
+        }
+        reset_status(ctx);
+        pvo_dev::CorrParams cp;
+        cp.n_edges = n_edges;
+        cp.channels = C;
+        cp.e_patch = dep;
+        cp.e_slot = des;
+        cp.coords = dc;
+        cp.feat0 = static_cast<const float*>(ctx->feat0.p);
+        cp.feat1 = static_cast<const float*>(ctx->feat1.p);
+        cp.gram0 = static_cast<const float*>(ctx->gram0.p);
+        cp.gram1 = static_cast<const float*>(ctx->gram1.p);
+        cp.w0 = ctx->w0;
+        cp.h0 = ctx->h0;
+        cp.w1 = ctx->w1;
+        cp.h1 = ctx->h1;
+        cp.patch_feats = dpf;
+        cp.out = dout;
+        cp.status = ctx->d_status;
+        cuda_check(pvo_dev::launch_corr(cp, ctx->stream), "corr kernel");
+        ctx->launches += 1;
+        if (memspace != PVO_DEVICE) {
+            download(ctx, out, dout, (size_t)n_edges * 2 * 9 * 49);
+            if (read_status(ctx)) fail(PVO_INVALID_ARGUMENT, "correlate: non-finite reprojection");
+        }
+    });
+}
+
+// ---- bundle adjustment -----------------------------------------------------------
+int pvo_gauss_newton_step(pvo_ctx* ctx, int n_poses, const double* poses, const uint8_t* fixed, int n_patches, int p,
+                          const int* src, const double* px, const double* py, const double* depth,
+                          const uint8_t* depth_free, int n_edges, const int* e_patch, const int* e_pose,
+                          const double* e_target, const double* e_weight, const double* K, double damping,
+                          double* out_poses, double* out_depth, double* residual_norms, double* debug_h,
+                          double* debug_b, int* n_free_poses, int* n_free_depths) {
+    return guarded([&] {
+        HostProblem pr{n_poses, poses, fixed, n_patches, p, src, px, py, depth, depth_free, n_edges,
+                       e_patch, e_pose, e_target, e_weight};
+        std::memcpy(pr.K, K, sizeof(pr.K));
+        pr.damping = damping;
+        BARun run;
+        run.iterations = 1;
+        run.gn_step_mode = 1;
+        run.out_poses = out_poses;
+        run.out_depth = out_depth;
+        run.residual_norms = residual_norms;
+        run.debug_h = debug_h;
+        run.debug_b = debug_b;
+        run.n_free_poses = n_free_poses;
+        run.n_free_depths = n_free_depths;
+        run_ba(ctx, pr, run);
+    });
+}
+
+int pvo_schur_solve(pvo_ctx* ctx, int np, int nd, const double* hpp, const double* hpd, const double* hdd,
+                    const double* bp, const double* bd, double* dp, double* dd) {
+    return guarded([&] {
+        bind(ctx);
+        if (np < 0 || nd < 0) fail(PVO_INVALID_ARGUMENT, "schur: bad sizes");
+        for (int k = 0; k < nd; ++k)
+            if (hdd[k] <= 0) fail(PVO_DEGENERATE, "schur: non-positive damped depth-block entry");
+        double* d_hpp = upload(ctx, ctx->s0, hpp, (size_t)np * np);
+        double* d_hpd = upload(ctx, ctx->s1, hpd, (size_t)np * nd);
+        double* d_hdd = upload(ctx, ctx->s2, hdd, nd);
+        double* d_bp = upload(ctx, ctx->s3, bp, np);
+        double* d_bd = upload(ctx, ctx->s4, bd, nd);
+        double* d_dp = ctx->s5.as<double>(std::max(np, 1));
+        // dd followed by the reduced-system scratch (see launch_schur_dense)
+        double* d_dd = ctx->s6.as<double>((size_t)nd + (size_t)np * (np + 1) / 2 + np + 1);
+        reset_status(ctx);
+        cuda_check(pvo_dev::launch_schur_dense(np, nd, d_hpp, d_hpd, d_hdd, d_bp, d_bd, d_dp, d_dd, ctx->d_status,
+                                               ctx->stream),
+                   "schur kernel");
+        ctx->launches += 1;
+        raise_ba_status(read_status(ctx));
+        if (np) download(ctx, dp, d_dp, np);
+        download(ctx, dd, d_dd, nd);
+        sync(ctx);
+    });
+}
+
+int pvo_ba_window(pvo_ctx* ctx, int n_poses, const double* poses, const uint8_t* fixed, int n_patches, int p,
+                  const int* src, const double* px, const double* py, const double* depth, int n_edges,
+                  const int* e_patch, const int* e_pose, const double* e_target, const double* e_weight,
+                  const double* K, int image_w, int image_h, int freeze_targets, double damping, int iterations,
+                  int structure_only, double* out_poses, double* out_depth, double* residual_norms, int* n_norms) {
+    return guarded([&] {
+        if (iterations < 0 || structure_only < 0) fail(PVO_INVALID_ARGUMENT, "ba: negative iteration count");
+        HostProblem pr{n_poses, poses, fixed, n_patches, p, src, px, py, depth, nullptr, n_edges,
+                       e_patch, e_pose, e_target, e_weight};
+        std::memcpy(pr.K, K, sizeof(pr.K));
+        pr.image_w = image_w;
+        pr.image_h = image_h;
+        pr.damping = damping;
+        BARun run;
+        run.freeze_targets = freeze_targets;
+        run.iterations = iterations;
+        run.structure_only = structure_only;
+        run.out_poses = out_poses;
+        run.out_depth = out_depth;
+        run.residual_norms = residual_norms;
+        run.n_norms = n_norms;
+        if (freeze_targets) {
+            // deltas are not validated as targets; validate() only checks finiteness
+        }
+        run_ba(ctx, pr, run);
+    });
+}
+
+// ---- resident window ------------------------------------------------------------
+int pvo_window_load(pvo_ctx* ctx, int n_poses, const double* poses, const uint8_t* fixed, const int* pose_slot,
+                    int n_patches, int p, const int* src, const double* px, const double* py, const double* depth,
+                    const float* patch_feats, int n_edges, const int* e_patch, const int* e_pose,
+                    const double* e_delta, const double* e_weight, const double* K, int image_w, int image_h,
+                    int memspace) {
+    return guarded([&] {
+        bind(ctx);
+        if (memspace != PVO_HOST) fail(PVO_INVALID_ARGUMENT, "window_load: host arrays expected");
+        if (ctx->nf == 0) fail(PVO_INVALID_ARGUMENT, "window_load: frame store is empty (pvo_frames_reserve)");
+        HostProblem pr{n_poses, poses, fixed, n_patches, p, src, px, py, depth, nullptr, n_edges,
+                       e_patch, e_pose, e_delta, e_weight};
+        std::memcpy(pr.K, K, sizeof(pr.K));
+        pr.image_w = image_w;
+        pr.image_h = image_h;
+        validate(pr);
+        for (int i = 0; i < n_poses; ++i)
+            if (pose_slot[i] < 0 || pose_slot[i] >= ctx->nf) fail(PVO_OUT_OF_RANGE, "window_load: bad frame slot");
+        Window& w = ctx->win;
+        w.plan = make_plan(pr, false);
+        if (!w.plan.sorted) fail(PVO_INVALID_ARGUMENT, "window_load: edges must be grouped by patch (reference order)");
+        w.shape = pr;
+        w.n_poses = n_poses;
+        w.n_patches = n_patches;
+        w.n_edges = n_edges;
+        stage_problem(ctx, pr, w.plan, 64);
+        upload(ctx, w.pose_slot, pose_slot, n_poses);
+        upload(ctx, w.patch_feats, patch_feats, (size_t)n_patches * 2 * 9 * ctx->C);
+        upload(ctx, w.init_poses, poses, (size_t)n_poses * 7);
+        upload(ctx, w.init_depth, depth, n_patches);
+        upload(ctx, ctx->ba.K, K, 4);
+        w.corr.get(sizeof(float) * (size_t)n_edges * 2 * 9 * 49);
+        sync(ctx);
+        w.loaded = true;
+    });
+}
+
+int pvo_window_set_state(pvo_ctx* ctx, const double* poses, const double* depth, int memspace) {
+    return guarded([&] {
+        bind(ctx);
+        Window& w = ctx->win;
+        if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
+        const cudaMemcpyKind kind = memspace == PVO_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        const double* sp = poses ? poses : static_cast<const double*>(w.init_poses.p);
+        const double* sd = depth ? depth : static_cast<const double*>(w.init_depth.p);
+        const cudaMemcpyKind kp = poses ? kind : cudaMemcpyDeviceToDevice;
+        const cudaMemcpyKind kd = depth ? kind : cudaMemcpyDeviceToDevice;
+        cuda_check(cudaMemcpyAsync(ctx->ba.poses.p, sp, sizeof(double) * 7 * w.n_poses, kp, ctx->stream), "state");
+        cuda_check(cudaMemcpyAsync(ctx->ba.depth.p, sd, sizeof(double) * w.n_patches, kd, ctx->stream), "state");
+    });
+}
+
+namespace {
+pvo_dev::CorrParams window_corr_params(pvo_ctx* ctx, float* out) {
+    Window& w = ctx->win;
+    pvo_dev::CorrParams cp;
+    cp.n_edges = w.n_edges;
+    cp.channels = ctx->C;
+    cp.e_patch = static_cast<const int*>(ctx->ba.e_patch.p);
+    cp.e_pose = static_cast<const int*>(ctx->ba.e_pose.p);
+    cp.pose_slot = static_cast<const int*>(w.pose_slot.p);
+    cp.poses = static_cast<const double*>(ctx->ba.poses.p);
+    cp.patch_src = static_cast<const int*>(ctx->ba.patch_src.p);
+    cp.patch_x = static_cast<const double*>(ctx->ba.px.p);
+    cp.patch_y = static_cast<const double*>(ctx->ba.py.p);
+    cp.depth = static_cast<const double*>(ctx->ba.depth.p);
+    cp.K = static_cast<const double*>(ctx->ba.K.p);
+    cp.feat0 = static_cast<const float*>(ctx->feat0.p);
+    cp.feat1 = static_cast<const float*>(ctx->feat1.p);
+    cp.gram0 = static_cast<const float*>(ctx->gram0.p);
+    cp.gram1 = static_cast<const float*>(ctx->gram1.p);
+    cp.w0 = ctx->w0;
+    cp.h0 = ctx->h0;
+    cp.w1 = ctx->w1;
+    cp.h1 = ctx->h1;
+    cp.patch_feats = static_cast<const float*>(w.patch_feats.p);
+    cp.out = out ? out : static_cast<float*>(w.corr.p);
+    cp.status = ctx->d_status;
+    return cp;
+}
+
+pvo_dev::BAParams window_ba_params(pvo_ctx* ctx, int iterations, double damping) {
+    Window& w = ctx->win;
+    BABuffers& B = ctx->ba;
+    const int np = 6 * w.plan.n_free_poses;
+    pvo_dev::BAParams a;
+    a.n_poses = w.n_poses;
+    a.n_patches = w.n_patches;
+    a.n_edges = w.n_edges;
+    a.n_free_poses = w.plan.n_free_poses;
+    a.n_free_depths = w.plan.n_free_depths;
+    a.poses = static_cast<double*>(B.poses.p);
+    a.pose_free_slot = static_cast<const int*>(B.free_slot.p);
+    a.patch_src = static_cast<const int*>(B.patch_src.p);
+    a.patch_x = static_cast<const double*>(B.px.p);
+    a.patch_y = static_cast<const double*>(B.py.p);
+    a.depth = static_cast<double*>(B.depth.p);
+    a.depth_slot = static_cast<const int*>(B.depth_slot.p);
+    a.patch_edge_begin = static_cast<const int*>(B.edge_begin.p);
+    a.e_patch = static_cast<const int*>(B.e_patch.p);
+    a.e_pose = static_cast<const int*>(B.e_pose.p);
+    a.e_in = static_cast<const double*>(B.e_in.p);
+    a.e_weight_in = static_cast<const double*>(B.e_w.p);
+    a.e_target = static_cast<double*>(B.e_target.p);
+    a.e_weight = static_cast<double*>(B.e_weight.p);
+    a.cand_poses = static_cast<double*>(B.cand_poses.p);
+    a.cand_depth = static_cast<double*>(B.cand_depth.p);
+    a.patch_v = static_cast<double*>(B.patch_v.p);
+    a.patch_h = static_cast<double*>(B.patch_h.p);
+    a.patch_bd = static_cast<double*>(B.patch_bd.p);
+    const int grid = pvo_dev::ba_grid_size(w.n_patches, w.plan.n_free_poses, ctx->num_sms);
+    a.partials = B.partials.as<double>(pvo_dev::ba_partials_doubles(w.plan.n_free_poses, grid));
+    a.system = B.system.as<double>((size_t)np * (np + 1) / 2 + np + 1);
+    a.delta = B.delta.as<double>(std::max(np, 1));
+    a.residual_norms = B.norms.as<double>(iterations + 2);
+    a.n_norms = B.n_norms.as<int>(1);
+    a.status = ctx->d_status;
+    std::memcpy(a.K, w.shape.K, sizeof(a.K));
+    a.image_w = w.shape.image_w;
+    a.image_h = w.shape.image_h;
+    a.freeze_targets = 1;
+    a.damping = damping;
+    a.iterations = iterations;
+    return a;
+}
+}  // namespace
+
+int pvo_window_correlate(pvo_ctx* ctx, float* out, int memspace) {
+    return guarded([&] {
+        bind(ctx);
+        Window& w = ctx->win;
+        if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
+        reset_status(ctx);
+        pvo_dev::CorrParams cp = window_corr_params(ctx, memspace == PVO_DEVICE ? out : nullptr);
+        cuda_check(pvo_dev::launch_corr(cp, ctx->stream), "corr kernel");
+        ctx->launches += 1;
+        if (out && memspace != PVO_DEVICE) {
+            download(ctx, out, static_cast<float*>(w.corr.p), (size_t)w.n_edges * 2 * 9 * 49);
+            if (read_status(ctx)) fail(PVO_INVALID_ARGUMENT, "correlate: non-finite reprojection");
+        }
+    });
+}
+
+int pvo_window_iteration(pvo_ctx* ctx, int iterations, double damping, float* corr_out, int corr_memspace) {
+    return guarded([&] {
+        bind(ctx);
+        Window& w = ctx->win;
+        if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
+        if (iterations < 0) fail(PVO_INVALID_ARGUMENT, "ba: negative iteration count");
+        reset_status(ctx);
+        cuda_check(cudaEventRecord(ctx->ev[0], ctx->stream), "event");
+        pvo_dev::CorrParams cp = window_corr_params(ctx, corr_memspace == PVO_DEVICE ? corr_out : nullptr);
+        cuda_check(pvo_dev::launch_corr(cp, ctx->stream), "corr kernel");
+        ctx->launches += 1;
+        cuda_check(cudaEventRecord(ctx->ev[1], ctx->stream), "event");
+        pvo_dev::BAParams a = window_ba_params(ctx, iterations, damping);
+        launch_ba_checked(ctx, a);
+        cuda_check(cudaEventRecord(ctx->ev[2], ctx->stream), "event");
+        ctx->timing_pending = true;
+        if (corr_out && corr_memspace != PVO_DEVICE) {
+            download(ctx, corr_out, static_cast<float*>(w.corr.p), (size_t)w.n_edges * 2 * 9 * 49);
+        }
+    });
+}
+
+int pvo_window_read(pvo_ctx* ctx, double* poses, double* depth, double* residual_norms, int* n_norms) {
+    return guarded([&] {
+        bind(ctx);
+        Window& w = ctx->win;
+        if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
+        const int status = read_status(ctx);
+        if (status & (1 << pvo_dev::kDevBadCoords)) fail(PVO_INVALID_ARGUMENT, "correlate: non-finite reprojection");
+        raise_ba_status(status);
+        if (poses) download(ctx, poses, static_cast<double*>(ctx->ba.poses.p), (size_t)w.n_poses * 7);
+        if (depth) download(ctx, depth, static_cast<double*>(ctx->ba.depth.p), w.n_patches);
+        int n = 0;
+        download(ctx, &n, static_cast<int*>(ctx->ba.n_norms.p), 1);
+        sync(ctx);
+        if (residual_norms && n > 0) {
+            download(ctx, residual_norms, static_cast<double*>(ctx->ba.norms.p), n);
+            sync(ctx);
+        }
+        if (n_norms) *n_norms = n;
+    });
+}
+
+int pvo_window_corr_ptr(pvo_ctx* ctx, float** corr) {
+    return guarded([&] {
+        bind(ctx);
+        if (!ctx->win.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
+        *corr = static_cast<float*>(ctx->win.corr.p);
+    });
+}
+
+}  // extern "C"

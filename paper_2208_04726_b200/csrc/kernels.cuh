@@ -1,0 +1,115 @@
+// kernels.cuh — parameter blocks and launchers of the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace pvo_dev {
+
+// K2: correlation over a batch of edges (corr.cu).
+struct CorrParams {
+    int n_edges = 0;
+    int channels = 0;
+    const int* e_patch = nullptr;   // [E] patch index
+    const int* e_pose = nullptr;    // [E] target pose index (state mode)
+    const int* e_slot = nullptr;    // [E] frame-store slot (explicit mode) or null
+    const int* pose_slot = nullptr; // [n_poses] pose -> frame-store slot (state mode)
+    // Coordinates: explicit [E][9][2], or reprojected from the state below.
+    const double* coords = nullptr;
+    const double* poses = nullptr;
+    const int* patch_src = nullptr;
+    const double* patch_x = nullptr;
+    const double* patch_y = nullptr;
+    const double* depth = nullptr;
+    const double* K = nullptr;      // device [4]
+    // Frame store.
+    const float* feat0 = nullptr;
+    const float* feat1 = nullptr;
+    const float* gram0 = nullptr;
+    const float* gram1 = nullptr;
+    int w0 = 0, h0 = 0, w1 = 0, h1 = 0;
+    const float* patch_feats = nullptr;  // [P][2][9][C]
+    float* out = nullptr;                // [E][2][9][49]
+    int* status = nullptr;               // device status word (1 = non-finite coords)
+};
+
+int corr_smem_bytes(int channels);
+cudaError_t launch_corr(const CorrParams& p, cudaStream_t stream);
+cudaError_t launch_gram(const float* feat, float* gram, int W, int H, int D, int num_sms, cudaStream_t stream);
+
+// Device status word values (ba.cu / corr.cu) -> pvo_status on the host.
+enum DevStatus : int {
+    kDevOk = 0,
+    kDevBadCoords = 1,         // correlate: non-finite reprojection
+    kDevNonFiniteResidual = 2, // ba: non-finite residual (bundle_adjust.cpp:147-149)
+    kDevNonPositiveDepth = 3,  // schur: non-positive damped depth-block entry
+    kDevFactorization = 4,     // schur: reduced camera system factorization failed
+    kDevNonFinitePose = 5,     // schur: non-finite pose update
+    kDevNonFiniteDepth = 6,    // schur: non-finite depth update
+};
+
+// K3-K6: the bundle-adjustment window, one persistent cooperative kernel (ba.cu).
+struct BAParams {
+    int n_poses = 0, n_patches = 0, n_edges = 0;
+    int n_free_poses = 0;      // np = 6 * n_free_poses
+    int n_free_depths = 0;
+    // problem (device)
+    double* poses = nullptr;          // [n_poses][7] current state (updated in place)
+    const int* pose_free_slot = nullptr;  // [n_poses] free slot or -1
+    const int* patch_src = nullptr;
+    const double* patch_x = nullptr;  // [P][9]
+    const double* patch_y = nullptr;
+    double* depth = nullptr;          // [P] current state (updated in place)
+    const int* depth_slot = nullptr;  // [P] free slot or -1
+    const int* patch_edge_begin = nullptr;  // [P+1] CSR, edges grouped by patch
+    const int* e_patch = nullptr;
+    const int* e_pose = nullptr;
+    const double* e_in = nullptr;     // [E][2] targets, or deltas when freeze_targets
+    const double* e_weight_in = nullptr;  // [E][2]
+    double* e_target = nullptr;       // [E][2] scratch: frozen targets
+    double* e_weight = nullptr;       // [E][2] scratch: effective weights
+    double K[4] = {0, 0, 0, 0};
+    int image_w = 0, image_h = 0;
+    int freeze_targets = 0;
+    double damping = 1e-4;
+    int iterations = 0;
+    int structure_only = 0;
+    int gn_step_mode = 0;   // 1: single gauss_newton_step (no guard, always accept)
+    // scratch (device)
+    double* cand_poses = nullptr;     // [n_poses][7]
+    double* cand_depth = nullptr;     // [P]
+    double* patch_v = nullptr;        // [P][np]  H_pd column of each patch
+    double* patch_h = nullptr;        // [P] damped h_dd
+    double* patch_bd = nullptr;       // [P]
+    double* partials = nullptr;       // [grid][nent + np + 4]
+    double* system = nullptr;         // [nent + np] reduced S (upper) + rhs
+    double* delta = nullptr;          // [np] pose update
+    double* residual_norms = nullptr; // [1 + iterations]
+    int* n_norms = nullptr;
+    int* status = nullptr;
+};
+
+// Returns cudaErrorNotSupported when the shape exceeds the kernel (np > 96
+// or a patch with > 32 edges); the host maps that to PVO_UNSUPPORTED.
+cudaError_t launch_ba(BAParams& p, int num_sms, cudaStream_t stream, int* grid_out);
+int ba_max_free_poses();
+int ba_max_edges_per_patch();
+size_t ba_partials_doubles(int n_free_poses, int grid);
+int ba_grid_size(int n_patches, int n_free_poses, int num_sms);
+
+// Debug capture of the damped dense normal equations (sequential, tests only).
+cudaError_t launch_normal_equations_debug(const BAParams& p, double* h, double* b, cudaStream_t stream);
+
+// schur_solve on dense inputs (one CTA, np <= 96).
+cudaError_t launch_schur_dense(int np, int nd, const double* hpp, const double* hpd, const double* hdd,
+                               const double* bp, const double* bd, double* dp, double* dd, int* status,
+                               cudaStream_t stream);
+
+// Batched reprojection / Jacobians (camera entry points).
+cudaError_t launch_reproject(int n, int pp, const double* pi, const double* pj, const double* K, const double* x,
+                             const double* y, const double* d, double* out, uint8_t* behind, cudaStream_t stream);
+cudaError_t launch_jacobians(int n, int pp, const double* pi, const double* pj, const double* K, const double* x,
+                             const double* y, const double* d, double* out, uint8_t* behind, cudaStream_t stream);
+
+}  // namespace pvo_dev

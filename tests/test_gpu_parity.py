@@ -1,0 +1,329 @@
+"""GPU parity: the sm_100a path through the C-ABI against the CPU oracle on the
+same seeded inputs.  Tolerances (north star):
+  * indices / graph: bit-exact (tests/test_graph_and_abi.py, CPU);
+  * correlation: |C_gpu - C_ref| <= 1e-4 * max(|C_ref|, CORR_FLOOR * ||g||);
+  * BA poses / depths after the same iterations: 1e-3 relative;
+  * geometry (FP64): 1e-9 relative.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle.pyoracle as orc
+import paper_2208_04726_b200 as pvo
+from paper_2208_04726_b200 import synth
+from tests.helpers import pose_parity, random_pose, random_twist, smooth_features
+
+pytestmark = pytest.mark.gpu
+
+CORR_RTOL = 1e-4
+CORR_FLOOR = 1e-3  # floor of the relative measure, in units of ||g|| (|C| <= ||g||)
+KCAM = np.array([160.0, 155.0, 128.0, 126.0])
+I7 = np.array([0, 0, 0, 1.0, 0, 0, 0])
+THREADS = os.cpu_count() or 1
+
+
+def corr_violations(gpu, ref, gnorm):
+    """Count entries outside the tolerance; gnorm broadcastable to ref."""
+    tol = CORR_RTOL * np.maximum(np.abs(ref), CORR_FLOOR * gnorm)
+    return int((np.abs(gpu.astype(np.float64) - ref) > tol).sum())
+
+
+def _gnorm_for_batch(patch_feats, e_patch):
+    g = np.linalg.norm(patch_feats[e_patch].astype(np.float64), axis=-1)  # [E, 2, 9]
+    return g[..., None, None]
+
+
+# ------------------------------------------------------------------ camera
+def test_reproject_and_jacobians_match_oracle(ctx):
+    rng = np.random.default_rng(0)
+    n = 400
+    pi = np.stack([random_pose(rng, 0.3, 0.3) for _ in range(n)])
+    pj = np.stack([random_pose(rng, 0.3, 0.3) for _ in range(n)])
+    pj[:20] = pi[:20]  # bitwise-equal shortcut
+    pj[20:30] = [[0, 0, 0, 1, 0, 0, -8]] * 10  # behind the camera for some
+    pi[20:30] = I7
+    xs, ys, ds = [], [], []
+    for _ in range(n):
+        x, y = orc.patch_make((rng.uniform(20, 230), rng.uniform(20, 230)), 3, 0.0)
+        xs.append(x)
+        ys.append(y)
+        ds.append(rng.uniform(0.0, 2.0))
+    xs, ys, ds = np.array(xs), np.array(ys), np.array(ds)
+    pts, behind = pvo.reproject_patches(pi, pj, KCAM, xs, ys, ds, ctx=ctx)
+    jac, jb = pvo.reprojection_jacobians_batch(pi, pj, KCAM, xs, ys, ds, ctx=ctx)
+    for i in range(n):
+        ref, rb = orc.reproject_patch(pi[i], pj[i], KCAM, xs[i], ys[i], ds[i])
+        assert rb == behind[i]
+        if i < 20:
+            assert np.array_equal(pts[i], ref)  # shortcut returns the input coordinates exactly
+        scale = max(1.0, np.abs(ref).max())
+        assert np.abs(pts[i] - ref).max() <= 1e-9 * scale
+        rj, rjb = orc.reprojection_jacobians(pi[i], pj[i], KCAM, xs[i], ys[i], ds[i])
+        assert rjb == jb[i]
+        assert np.abs(jac[i] - rj).max() <= 1e-9 * max(1.0, np.abs(rj).max())
+
+
+# ------------------------------------------------------------------ correlation
+def _pyr(seed, H, W, D):
+    rng = np.random.default_rng(seed)
+    l0 = smooth_features(rng, H, W, D)
+    return l0, synth.make_level1(l0[None])[0]
+
+
+@pytest.mark.parametrize("D", [128, 25, 3])
+def test_correlate_single_matches_oracle(ctx, D):
+    l0, l1 = _pyr(D, 40, 48, D)
+    rng = np.random.default_rng(D)
+    worst = 0
+    for trial in range(40):
+        c = (rng.uniform(-20, 210), rng.uniform(-20, 180))  # includes off-grid / border cases
+        x, y = orc.patch_make(c, 3, 1.0)
+        coords = np.stack([x, y], 1) + rng.normal(0, 1.5, (9, 2)) * (trial % 2)
+        g = [rng.standard_normal((9, D)).astype(np.float32) for _ in range(2)]
+        out = pvo.correlate(g, (l0, l1), coords, ctx=ctx)
+        ref = orc.correlate(g, (l0, l1), coords)
+        gn = np.stack([np.linalg.norm(g[l].astype(np.float64), axis=1) for l in range(2)])[:, :, None, None]
+        worst += corr_violations(out.reshape(2, 9, 7, 7), ref.reshape(2, 9, 7, 7), gn)
+    assert worst == 0
+
+
+def test_correlate_zero_map_is_zero(ctx):  # test_features.cpp:171-184
+    l0, l1 = np.zeros((32, 32, 1), np.float32), np.zeros((8, 8, 1), np.float32)
+    x, y = orc.patch_make((60, 60), 3, 1.0)
+    out = pvo.correlate((np.ones((9, 1)), np.ones((9, 1))), (l0, l1), np.stack([x, y], 1), ctx=ctx)
+    assert not out.any()
+
+
+def test_correlate_rejects_non_finite(ctx):  # correlation.cpp:43-45
+    l0, l1 = _pyr(1, 16, 16, 8)
+    x, y = orc.patch_make((20, 20), 3, 1.0)
+    coords = np.stack([x, y], 1)
+    coords[3, 1] = np.inf
+    with pytest.raises(ValueError):
+        pvo.correlate((np.ones((9, 8)), np.ones((9, 8))), (l0, l1), coords, ctx=ctx)
+
+
+def test_correlate_self_match_and_shift(ctx):  # test_features.cpp:144-217
+    l0, l1 = _pyr(23, 64, 64, 128)
+    x, y = orc.patch_make((120, 132), 3, 1.0)
+    coords = np.stack([x, y], 1)
+    feats = (synth.crop_cubic(l0, x / 4, y / 4), synth.crop_cubic(l1, x / 16, y / 16))
+    grid = pvo.correlate(feats, (l0, l1), coords, ctx=ctx)
+    for v in range(3):
+        for u in range(3):
+            assert grid[0, v, u, 3, 3] >= grid[0, v, u].max() - 1e-6
+    rng = np.random.default_rng(14)
+    for _ in range(8):
+        a, b = int(rng.integers(7)) - 3, int(rng.integers(7)) - 3
+        g = pvo.correlate(feats, (l0, l1), coords + [4.0 * a, 4.0 * b], ctx=ctx)
+        al, be = np.unravel_index(np.argmax(g[0, 1, 1]), (7, 7))
+        assert (al, be) == (3 - b, 3 - a)
+
+
+def test_correlate_linearity(ctx):  # test_features.cpp:219-245
+    l0, l1 = _pyr(29, 64, 64, 128)
+    x, y = orc.patch_make((100, 80), 3, 1.0)
+    coords = np.stack([x, y], 1)
+    rng = np.random.default_rng(15)
+    g1 = [rng.standard_normal((9, 128)).astype(np.float32) for _ in range(2)]
+    g2 = [rng.standard_normal((9, 128)).astype(np.float32) for _ in range(2)]
+    gs = [g1[i] + g2[i] for i in range(2)]
+    c1, c2, cs = (pvo.correlate(g, (l0, l1), coords, ctx=ctx) for g in (g1, g2, gs))
+    assert np.allclose(cs, c1 + c2, rtol=1e-5, atol=1e-5)
+
+
+@pytest.fixture(scope="module")
+def c1_workload():
+    return synth.generate("c1")
+
+
+def test_correlate_batch_c1_full(ctx, c1_workload):
+    """Config 1 (6,144 edges, 128-d, 120x160): every edge against the oracle."""
+    w = c1_workload
+    F = w.cfg["frames"]
+    ctx.frames_reserve(F, w.level0.shape[2], w.level0.shape[1], w.level1.shape[2], w.level1.shape[1], 128)
+    for f in range(F):
+        ctx.frames_upload(f, w.level0[f], w.level1[f])
+    g = synth.build_graph(w, pvo.PatchGraph)
+    prob = g.window_problem(w.cfg["window"])
+    # coordinates = reproject_patch at the current state (oracle, FP64)
+    E = len(prob["e_patch"])
+    coords = np.empty((E, 9, 2))
+    for e in range(E):
+        k = prob["e_patch"][e]
+        coords[e], _ = orc.reproject_patch(prob["poses"][prob["patch_src"][k]], prob["poses"][prob["e_pose"][e]],
+                                           w.K, prob["patch_x"][k], prob["patch_y"][k], prob["depth"][k])
+    pf = w.patch_feats[prob["patch_ids"]]
+    slots = prob["pose_frames"][prob["e_pose"]]
+    out = pvo.correlate_batch(prob["e_patch"], slots, coords, pf, ctx=ctx)
+    ref = orc.correlate_batch(prob["e_patch"], slots, coords, pf, w.level0, w.level1, threads=THREADS)
+    gn = _gnorm_for_batch(pf, prob["e_patch"])
+    bad = corr_violations(out, ref, gn)
+    err = np.abs(out.astype(np.float64) - ref)
+    print(f"C1 corr: max abs err {err.max():.3e}, violations {bad} / {ref.size}")
+    assert bad == 0
+
+
+def test_window_corr_matches_explicit_coords(ctx, c1_workload):
+    """The resident window reprojects on the device (K1 fused in K2): same volume."""
+    w = c1_workload
+    g = synth.build_graph(w, pvo.PatchGraph)
+    prob = synth.window_arrays(w, g.window_problem(w.cfg["window"]))
+    win = pvo.Window(ctx)
+    win.load(prob, prob["pose_frames"], prob["patch_feats"], w.K, w.image)
+    vol = win.correlate()
+    E = len(prob["e_patch"])
+    sel = np.arange(0, E, 7)
+    coords = np.empty((len(sel), 9, 2))
+    for i, e in enumerate(sel):
+        k = prob["e_patch"][e]
+        coords[i], _ = orc.reproject_patch(prob["poses"][prob["patch_src"][k]], prob["poses"][prob["e_pose"][e]],
+                                           w.K, prob["patch_x"][k], prob["patch_y"][k], prob["depth"][k])
+    ref = orc.correlate_batch(prob["e_patch"][sel], prob["pose_frames"][prob["e_pose"][sel]], coords,
+                              prob["patch_feats"], w.level0, w.level1, threads=THREADS)
+    gn = _gnorm_for_batch(prob["patch_feats"], prob["e_patch"][sel])
+    assert corr_violations(vol[sel], ref, gn) == 0
+
+
+# ------------------------------------------------------------------ bundle adjustment
+KBA = np.array([160.0, 160.0, 128.0, 128.0])
+
+
+def _two_view(rng, edges, depths_free=True):
+    from tests.test_oracle_pins import two_view_problem
+
+    return two_view_problem(rng, edges, depths_free)
+
+
+def _to_problem(pr, dfree=None, damping=1e-4, K=KBA):
+    return pvo.BAProblem(pr["poses"], pr["fixed"].astype(bool), pr["patch_src"], pr["patch_x"], pr["patch_y"],
+                         pr["depth"], pr["e_patch"], pr["e_pose"], pr["e_target"], pr["e_weight"], K, damping,
+                         None if dfree is None else dfree.astype(bool))
+
+
+def test_gauss_newton_step_matches_oracle(ctx):
+    rng = np.random.default_rng(32)
+    for trial in range(6):
+        pr, dfree = _two_view(rng, 20, depths_free=bool(trial % 2))
+        sol, ne = pvo.gauss_newton_step(_to_problem(pr, dfree), debug=True, ctx=ctx)
+        ref = orc.gauss_newton_step(pr, KBA, depth_free=dfree, debug=True)
+        assert np.array_equal(sol.poses[0], pr["poses"][0])  # fixed pose bit-identical
+        dt, dq = pose_parity(sol.poses, ref["poses"])
+        assert dt.max() <= 1e-9 and dq.max() <= 1e-9
+        assert np.abs(sol.inverse_depths - ref["depth"]).max() <= 1e-9
+        assert np.allclose(sol.residual_norms, ref["residual_norms"], rtol=1e-9)
+        assert ne.num_free_poses == ref["num_free_poses"] and ne.num_free_depths == ref["num_free_depths"]
+        assert np.abs(ne.h - ref["h"]).max() <= 1e-9 * max(1, np.abs(ref["h"]).max())
+        assert np.abs(ne.b - ref["b"]).max() <= 1e-9 * max(1, np.abs(ref["b"]).max())
+
+
+def test_gn_zero_residual_zero_update(ctx):  # test_bundle_adjust.cpp:107-128
+    rng = np.random.default_rng(31)
+    pr, _ = _two_view(rng, 12)
+    for e in range(12):
+        pts, _ = orc.reproject_patch(pr["poses"][0], pr["poses"][1], KBA, pr["patch_x"][e], pr["patch_y"][e],
+                                     pr["depth"][e])
+        pr["e_target"][e] = pts[4]
+    sol = pvo.gauss_newton_step(_to_problem(pr), ctx=ctx)
+    d, ang = orc.pose_distance(sol.poses[1], pr["poses"][1])
+    assert d < 1e-12 and ang < 1e-12 and sol.residual_norms[0] == pytest.approx(0.0)
+
+
+def test_schur_solve_matches_oracle(ctx):
+    from tests.test_oracle_pins import random_system
+
+    rng = np.random.default_rng(35)
+    for _ in range(10):
+        sysm = random_system(rng, 2 + int(rng.integers(5)), 10 + int(rng.integers(41)))
+        dp, dd = pvo.schur_solve(*sysm, ctx=ctx)
+        rp, rd = orc.schur_solve(*sysm)
+        scale = max(1.0, np.abs(np.concatenate([rp, rd])).max())
+        assert np.abs(np.concatenate([dp, dd]) - np.concatenate([rp, rd])).max() / scale < 1e-9
+    sysm = list(random_system(rng, 1, 3))
+    sysm[2][1] = 0.0
+    with pytest.raises(pvo.DegenerateProblem):
+        pvo.schur_solve(*sysm, ctx=ctx)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_ba_window_matches_oracle(ctx, name):
+    """optimize_window's 2 iterations on the flattened config window, GPU vs oracle."""
+    w = synth.generate(name, features=False)
+    g = synth.build_graph(w, pvo.PatchGraph)
+    prob = g.window_problem(w.cfg["window"])
+    ref = orc.ba_window(prob, w.K, iterations=2)
+    pr = pvo.BAProblem(prob["poses"], prob["fixed"].astype(bool), prob["patch_src"], prob["patch_x"],
+                       prob["patch_y"], prob["depth"], prob["e_patch"], prob["e_pose"], prob["e_target"],
+                       prob["e_weight"], w.K)
+    sol = pvo.ba_window(pr, iterations=2, ctx=ctx)
+    fixed = prob["fixed"].astype(bool)
+    assert np.array_equal(sol.poses[fixed], prob["poses"][fixed])
+    dt, dq = pose_parity(sol.poses, ref["poses"])
+    tref = np.abs(ref["poses"][:, 4:]).max(1)
+    assert (dt <= 1e-3 * np.maximum(tref, 1.0)).all() and (dq <= 1e-3).all()
+    dd = np.abs(sol.inverse_depths - ref["depth"])
+    assert (dd <= 1e-3 * np.maximum(np.abs(ref["depth"]), 1e-3)).all()
+    assert len(sol.residual_norms) == len(ref["residual_norms"]) == 3
+    assert np.allclose(sol.residual_norms, ref["residual_norms"], rtol=1e-6)
+    print(name, "max pose dt", dt.max(), "dq", dq.max(), "depth", dd.max())
+
+
+def test_optimize_window_graph_matches_oracle(ctx):
+    w = synth.generate("c1", features=False)
+    g, o = synth.build_graph(w, pvo.PatchGraph), synth.build_graph(w, orc.PatchGraph)
+    sol = pvo.optimize_window(g, pvo.WindowOptions(window=w.cfg["window"]), ctx=ctx)
+    norms, ne = o.optimize_window(window=w.cfg["window"])
+    assert sol.num_edges == ne == w.n_edges
+    assert np.allclose(sol.residual_norms, norms, rtol=1e-6)
+    _, pg = g.frames()
+    _, po = o.frames()
+    dt, dq = pose_parity(pg, po)
+    assert dt.max() <= 1e-3 and dq.max() <= 1e-3
+    _, _, dg = g.patches()
+    _, _, do = o.patches()
+    assert (np.abs(dg - do) <= 1e-3 * np.maximum(np.abs(do), 1e-3)).all()
+
+
+def test_structure_only_and_guard_paths(ctx):
+    """structure-only steps + the divergence guard (bundle_adjust.cpp:317-354)."""
+    w = synth.generate("c1", features=False)
+    g = synth.build_graph(w, pvo.PatchGraph)
+    prob = g.window_problem(w.cfg["window"])
+    # wild targets force the guard to retry / skip
+    prob["e_target"] = prob["e_target"] + np.random.default_rng(0).normal(0, 300, prob["e_target"].shape)
+    ref = orc.ba_window(prob, w.K, iterations=2, structure_only=1)
+    pr = pvo.BAProblem(prob["poses"], prob["fixed"].astype(bool), prob["patch_src"], prob["patch_x"],
+                       prob["patch_y"], prob["depth"], prob["e_patch"], prob["e_pose"], prob["e_target"],
+                       prob["e_weight"], w.K)
+    sol = pvo.ba_window(pr, iterations=2, structure_only_iterations=1, ctx=ctx)
+    assert len(sol.residual_norms) == len(ref["residual_norms"])
+    assert np.allclose(sol.residual_norms, ref["residual_norms"], rtol=1e-6)
+    dt, dq = pose_parity(sol.poses, ref["poses"])
+    assert dt.max() <= 1e-3 and dq.max() <= 1e-3
+
+
+def test_window_iteration_deterministic(ctx, c1_workload):
+    w = c1_workload
+    F = w.cfg["frames"]
+    ctx.frames_reserve(F, w.level0.shape[2], w.level0.shape[1], w.level1.shape[2], w.level1.shape[1], 128)
+    for f in range(F):
+        ctx.frames_upload(f, w.level0[f], w.level1[f])
+    g = synth.build_graph(w, pvo.PatchGraph)
+    prob = synth.window_arrays(w, g.window_problem(w.cfg["window"]))
+    win = pvo.Window(ctx)
+    win.load(prob, prob["pose_frames"], prob["patch_feats"], w.K, w.image)
+    outs = []
+    for _ in range(2):
+        win.reset()
+        vol = np.empty((win.n_edges, 2, 9, 7, 7), np.float32)
+        win.iteration(2, corr_out=vol)
+        poses, depth, norms = win.read()
+        outs.append((vol, poses, depth, norms))
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
+    # and the BA half equals the flat-problem oracle on the same window
+    ref = orc.ba_window(g.window_problem(w.cfg["window"]), w.K, iterations=2)
+    dt, dq = pose_parity(outs[0][1], ref["poses"])
+    assert dt.max() <= 1e-3 and dq.max() <= 1e-3
