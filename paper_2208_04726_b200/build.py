@@ -34,7 +34,7 @@ NVCC_FLAGS = [
     "-I",
     str(ROOT / "include"),
 ]
-SOURCES = ["corr.cu", "ba.cu", "capi.cu", "graph.cpp"]
+SOURCES = ["corr.cu", "corr_tma.cu", "ba.cu", "capi.cu", "graph.cpp"]
 
 
 def nvcc() -> str:

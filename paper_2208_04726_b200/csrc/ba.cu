@@ -9,7 +9,7 @@
 // divergence guard (damping x1e3, x1e6, x1e9 retries) — runs inside ONE
 // persistent cooperative kernel; control never returns to the host.
 //
-// Phases per Gauss-Newton attempt (grid.sync() between them):
+// Phases per Gauss-Newton attempt (3 grid-wide barriers):
 //   P1 assemble   warp per patch, lane per edge: Jacobians (camera.cpp:73-108),
 //                 residual, weight; per-patch reductions give h_k, b_k, the
 //                 patch's H_pd column v_k and gradient; every thread of the CTA
@@ -17,14 +17,24 @@
 //                     S += sum_e J~_e^T W_e J~_e - v_k v_k^T / h_k
 //                     r += b_k - v_k b_dk / h_k
 //                 accumulated patch after patch (no atomics, fixed order).
+//   --- grid sync
 //   P2 reduce     entry-parallel over the grid: S = sum over CTAs (fixed order)
 //                 + damping on the diagonal.
-//   P3 solve      CTA 0: pivoted LDLT of S in shared memory (Eigen's pivot rule:
-//                 largest remaining original diagonal), solve, retract poses.
+//   --- grid sync
+//   P3 solve      EVERY CTA solves the small pose system redundantly (identical
+//                 inputs and code -> bit-identical results, no broadcast):
+//                 Eigen's LDLT pivot sequence (largest remaining original
+//                 diagonal, bundle_adjust.cpp:76) is simulated first, then an
+//                 unpivoted right-looking LDL^T of the permuted system runs in
+//                 shared memory; retraction of the free poses into the CTA's
+//                 own copy of the candidate state.
 //   P4 update     warp per patch: depth back-substitution, clamp at 0, weighted
 //                 residual at the candidate state (bitwise-equal-pose shortcut).
+//   --- grid sync
 //   P5 decide     every CTA evaluates the same guard from the same partial sums,
-//                 then commits, retries with heavier damping, or skips.
+//                 then commits (its pose copy, its depths), retries with heavier
+//                 damping, or skips.  Partials and status words are double
+//                 buffered by attempt parity, so no barrier is needed here.
 // Determinism: every reduction has a fixed order (shuffle trees, per-thread
 // entry ownership, ordered cross-CTA sums), so reruns are bit-identical.
 #include <cooperative_groups.h>
@@ -47,6 +57,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kMaxFree = 16;            // free poses  -> np <= 96
 constexpr int kMaxNp = 6 * kMaxFree;
 constexpr int kMaxEdges = 32;           // edges per patch (lane per edge)
+constexpr int kMaxPoses = 128;          // poses held per CTA in shared memory
 constexpr int kRec = 30;                // doubles per edge record
 // edge record: Gs[12] Jt[12] Jd[2] r[2] w[2]
 constexpr int kGs = 0, kJt = 12, kJd = 24, kR = 26, kW = 28;
@@ -57,51 +68,67 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+__host__ __device__ inline int nent_of(int np) { return np * (np + 1) / 2; }
+__host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
+
+// Shared-memory plan (bytes).  Fixed part: entry table, pose copies, delta.
+// Union part: assembly scratch | solve workspace.
 struct Layout {
-    // byte offsets into dynamic shared memory
-    int S, rhs, rec, vb, scal, ints, ab, wr, total;
-    // solve-phase overlay (CTA 0 only)
-    int A, x, od, tr, solve_total;
+    int ab, pose, cand, delta, flags, uni;
+    int S, rhs, rec, vb, scal, wr, ints;  // assembly
+    int A, x, od, perm, c, l;             // solve
+    int total;
 };
 
-__host__ __device__ inline int nent_of(int np) { return np * (np + 1) / 2; }
-
-__host__ __device__ inline Layout make_layout(int np) {
+__host__ __device__ inline Layout make_layout(int np_full, int n_poses) {
     Layout L;
-    const int nent = nent_of(np);
     int off = 0;
-    // The entry table comes first so the solve overlay (CTA 0) never clobbers it.
     L.ab = off;
-    off += (4 * nent + 15) & ~15;
-    const int overlay = off;
-    L.S = off;
-    off += 8 * nent;
-    L.rhs = off;
-    off += 8 * np;
-    L.rec = off;
-    off += 8 * kWarps * kMaxEdges * kRec;
-    L.vb = off;
-    off += 8 * kWarps * 2 * np;
-    L.scal = off;
-    off += 8 * kWarps * 4;  // h, bd, inv_h, pad
-    L.wr = off;
-    off += 8 * kWarps * 4;  // wrms partials
-    L.ints = off;
-    off += 4 * kWarps * (4 + kMaxFree + kMaxEdges);  // si, ne, dslot, k | p2e[16] | next[32]
-    L.total = (off + 15) & ~15;
-    // solve overlay
-    off = overlay;
-    L.A = off;
-    off += 8 * np * np;
-    L.x = off;
-    off += 8 * np;
-    L.od = off;
-    off += 8 * np;
-    L.tr = off;
-    off += 4 * np;
-    L.solve_total = (off + 15) & ~15;
-    if (L.solve_total > L.total) L.total = L.solve_total;
+    off += align16(4 * nent_of(np_full));
+    L.pose = off;
+    off += align16(8 * 7 * n_poses);
+    L.cand = off;
+    off += align16(8 * 7 * n_poses);
+    L.delta = off;
+    off += align16(8 * (np_full > 0 ? np_full : 1));
+    L.flags = off;
+    off += 16;
+    L.uni = off;
+    int a = off;
+    L.S = a;
+    a += 8 * nent_of(np_full);
+    L.rhs = a;
+    a += 8 * np_full;
+    L.rec = a;
+    a += 8 * kWarps * kMaxEdges * kRec;
+    L.vb = a;
+    a += 8 * kWarps * 2 * np_full;
+    L.scal = a;
+    a += 8 * kWarps * 4;
+    L.wr = a;
+    a += 8 * kWarps * 4;
+    L.ints = a;
+    a += 4 * kWarps * (4 + kMaxFree + kMaxEdges);
+    int s = off;
+    L.A = s;
+    s += 8 * np_full * np_full;
+    L.x = s;
+    s += 8 * np_full;
+    L.od = s;
+    s += 8 * np_full;
+    L.c = s;
+    s += 8 * np_full;
+    L.l = s;
+    s += 8 * np_full;
+    L.perm = s;
+    s += 4 * np_full;
+    L.total = align16(a > s ? a : s);
     return L;
+}
+
+template <typename T>
+__device__ __forceinline__ T* at(unsigned char* smem, int off) {
+    return reinterpret_cast<T*>(smem + off);
 }
 
 __device__ inline void set_status(int* status, int code) { atomicOr(status, 1 << code); }
@@ -131,37 +158,125 @@ __device__ inline void reproject_center(const SE3& pi, const SE3& pj, const Cam&
     *behind = b;
 }
 
-struct Shared {
-    double* S;
-    double* rhs;
-    double* rec;
-    double* vb;
-    double* scal;
-    double* wr;
-    int* ints;
-    unsigned* ab;
-};
-
-__device__ inline Shared carve(unsigned char* smem, const Layout& L) {
-    Shared s;
-    s.S = reinterpret_cast<double*>(smem + L.S);
-    s.rhs = reinterpret_cast<double*>(smem + L.rhs);
-    s.rec = reinterpret_cast<double*>(smem + L.rec);
-    s.vb = reinterpret_cast<double*>(smem + L.vb);
-    s.scal = reinterpret_cast<double*>(smem + L.scal);
-    s.wr = reinterpret_cast<double*>(smem + L.wr);
-    s.ints = reinterpret_cast<int*>(smem + L.ints);
-    s.ab = reinterpret_cast<unsigned*>(smem + L.ab);
-    return s;
+// ---------------------------------------------------------------------------
+// Pivoted LDLT solve of an np x np SPD system held as (upper triangle, rhs),
+// Eigen's pivot rule; all threads of the CTA.  x_out may be
+// shared or global memory.  Returns false (all threads) on a factorization
+// failure (zero pivot with a non-zero column below, LDLT::info()).
+// ---------------------------------------------------------------------------
+__device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, const Layout& L, double* x_out) {
+    const int tid = threadIdx.x;
+    double* A = at<double>(smem, L.A);
+    double* x = at<double>(smem, L.x);
+    double* od = at<double>(smem, L.od);
+    double* c = at<double>(smem, L.c);
+    double* l = at<double>(smem, L.l);
+    int* perm = at<int>(smem, L.perm);
+    __shared__ int s_fail, s_zero;
+    // Eigen's transposition sequence depends only on the original diagonal:
+    // simulate it (first largest |d| among the remaining entries).
+    if (tid == 0) {
+        s_fail = 0;
+        s_zero = 0;
+        for (int i = 0; i < np; ++i) {
+            perm[i] = i;
+            // diagonal entry (i, i) of the upper-triangle row-major layout
+            od[i] = sys[i * np - i * (i - 1) / 2];
+        }
+        for (int k = 0; k < np; ++k) {
+            int big = k;
+            double bv = fabs(od[k]);
+            for (int i = k + 1; i < np; ++i)
+                if (fabs(od[i]) > bv) {
+                    bv = fabs(od[i]);
+                    big = i;
+                }
+            const double td = od[k];
+            od[k] = od[big];
+            od[big] = td;
+            const int tp = perm[k];
+            perm[k] = perm[big];
+            perm[big] = tp;
+        }
+    }
+    __syncthreads();
+    // A = P S P^T (lower triangle), x = P rhs
+    for (int t = tid; t < np * np; t += kThreads) {
+        const int i = t / np, j = t - i * np;
+        if (j > i) continue;
+        int a = perm[i], b = perm[j];
+        if (a > b) {
+            const int s = a;
+            a = b;
+            b = s;
+        }
+        A[i * np + j] = sys[a * np - a * (a - 1) / 2 + (b - a)];
+    }
+    const int nent = nent_of(np);
+    for (int i = tid; i < np; i += kThreads) x[i] = sys[nent + perm[i]];
+    __syncthreads();
+    // right-looking LDL^T
+    for (int k = 0; k < np; ++k) {
+        const double dk = A[k * np + k];
+        const bool valid = fabs(dk) > 0.0;
+        if (k == 0 && !valid) {
+            // Eigen: all-zero diagonal -> D = 0, identity transpositions
+            if (tid == 0) s_zero = 1;
+            break;
+        }
+        for (int i = k + 1 + tid; i < np; i += kThreads) {
+            const double ci = A[i * np + k];
+            c[i] = ci;
+            if (valid) {
+                l[i] = ci / dk;
+            } else {
+                l[i] = 0.0;
+                if (ci != 0.0) s_fail = 1;
+            }
+        }
+        __syncthreads();
+        const int m = np - k - 1;
+        for (int t = tid; t < m * m; t += kThreads) {
+            const int i = k + 1 + t / m, j = k + 1 + t % m;
+            if (j <= i) A[i * np + j] -= c[i] * l[j];
+        }
+        for (int i = k + 1 + tid; i < np; i += kThreads) A[i * np + k] = valid ? l[i] : c[i];
+        __syncthreads();
+    }
+    __syncthreads();
+    if (s_fail) return false;
+    if (s_zero) {
+        for (int i = tid; i < np; i += kThreads) x_out[i] = 0.0;
+        __syncthreads();
+        return true;
+    }
+    if (tid < 32) {
+        const int lane = tid;
+        for (int j = 0; j < np; ++j) {
+            const double xj = x[j];
+            for (int i = j + 1 + lane; i < np; i += 32) x[i] -= A[i * np + j] * xj;
+            __syncwarp();
+        }
+        for (int i = lane; i < np; i += 32) {
+            const double dd = A[i * np + i];
+            x[i] = fabs(dd) > DBL_MIN ? x[i] / dd : 0.0;  // pseudo-inverse of D (LDLT::_solve_impl)
+        }
+        __syncwarp();
+        for (int j = np - 1; j >= 0; --j) {
+            const double xj = x[j];
+            for (int i = lane; i < j; i += 32) x[i] -= A[j * np + i] * xj;
+            __syncwarp();
+        }
+        for (int i = lane; i < np; i += 32) x_out[perm[i]] = x[i];
+    }
+    __syncthreads();
+    return true;
 }
-
-// Per-warp int block: [0]=si [1]=ne [2]=dslot [3]=k, [4..4+16)=p2e, then next[32]
-__device__ inline int* warp_ints(const Shared& s, int w) { return s.ints + w * (4 + kMaxFree + kMaxEdges); }
 
 // ---------------------------------------------------------------------------
 // P0: frozen targets (bundle_adjust.cpp:288-307) for the edges of [k0, k1)
 // ---------------------------------------------------------------------------
-__device__ void phase_freeze(const BAParams& a, int k0, int k1) {
+__device__ void phase_freeze(const BAParams& a, const double* poses, int k0, int k1) {
     const int e0 = a.patch_edge_begin[k0], e1 = a.patch_edge_begin[k1];
     const Cam K{a.K[0], a.K[1], a.K[2], a.K[3]};
     const double margin = 2.0 * 32.0;  // 2 * kMaxObservableMarginPx (bundle_adjust.hpp:18)
@@ -174,8 +289,8 @@ __device__ void phase_freeze(const BAParams& a, int k0, int k1) {
             continue;
         }
         const int k = a.e_patch[e];
-        const SE3 pi = se3_load(a.poses + 7 * a.patch_src[k]);
-        const SE3 pj = se3_load(a.poses + 7 * a.e_pose[e]);
+        const SE3 pi = se3_load(poses + 7 * a.patch_src[k]);
+        const SE3 pj = se3_load(poses + 7 * a.e_pose[e]);
         double cu, cv;
         bool behind;
         reproject_center(pi, pj, K, a.patch_x + 9 * (size_t)k, a.patch_y + 9 * (size_t)k, a.depth[k], &cu, &cv,
@@ -189,27 +304,34 @@ __device__ void phase_freeze(const BAParams& a, int k0, int k1) {
     }
 }
 
+// Per-warp int block: [0]=si [1]=ne [2]=dslot [3]=k, [4..4+16)=p2e, then next[32]
+__device__ inline int* warp_ints(unsigned char* smem, const Layout& L, int w) {
+    return at<int>(smem, L.ints) + w * (4 + kMaxFree + kMaxEdges);
+}
+
 // ---------------------------------------------------------------------------
 // P1: assembly of the CTA's patches into its partial reduced system.
 // ---------------------------------------------------------------------------
-__device__ void phase_assemble(const BAParams& a, const Shared& s, int k0, int k1, int np, bool poses_frozen,
-                               double lambda, double* part) {
+__device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Layout& L, const double* poses, int k0,
+                               int k1, int np, bool poses_frozen, double lambda, double* part, int* status) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nent = nent_of(np);
     const Cam K{a.K[0], a.K[1], a.K[2], a.K[3]};
-    for (int i = tid; i < nent; i += kThreads) s.S[i] = 0.0;
-    for (int i = tid; i < np; i += kThreads) s.rhs[i] = 0.0;
-    double wr_sum = 0.0, wr_w = 0.0;  // lane-0 of each warp keeps its running sums
+    double* S = at<double>(smem, L.S);
+    double* rhs = at<double>(smem, L.rhs);
+    const unsigned* abt = at<unsigned>(smem, L.ab);
+    for (int i = tid; i < nent; i += kThreads) S[i] = 0.0;
+    for (int i = tid; i < np; i += kThreads) rhs[i] = 0.0;
+    double wr_sum = 0.0, wr_w = 0.0;  // lane 0 of each warp keeps its running sums
     __syncthreads();
 
     for (int batch = k0; batch < k1; batch += kWarps) {
-        // ---- per-warp patch records ----
         const int k = batch + warp;
-        int* wi = warp_ints(s, warp);
-        double* rec = s.rec + (size_t)warp * kMaxEdges * kRec;
-        double* v = s.vb + (size_t)warp * 2 * np;
+        int* wi = warp_ints(smem, L, warp);
+        double* rec = at<double>(smem, L.rec) + (size_t)warp * kMaxEdges * kRec;
+        double* v = at<double>(smem, L.vb) + (size_t)warp * 2 * np;
         double* bvec = v + np;
-        double* sc = s.scal + warp * 4;
+        double* sc = at<double>(smem, L.scal) + warp * 4;
         if (k < k1) {
             const int eb = a.patch_edge_begin[k], ne = a.patch_edge_begin[k + 1] - eb;
             const int src = a.patch_src[k];
@@ -226,12 +348,12 @@ __device__ void phase_assemble(const BAParams& a, const Shared& s, int k0, int k
                 const int e = eb + lane;
                 const int tgt = a.e_pose[e];
                 sj = poses_frozen ? -1 : a.pose_free_slot[tgt];
-                const SE3 pi = se3_load(a.poses + 7 * src);
-                const SE3 pj = se3_load(a.poses + 7 * tgt);
+                const SE3 pi = se3_load(poses + 7 * src);
+                const SE3 pj = se3_load(poses + 7 * tgt);
                 const Relative rel = relative_pose(pi, pj);
                 const CenterJac J = center_jacobians(rel, K, d, px[4], py[4]);
                 const double r0 = J.cu - a.e_target[2 * e], r1 = J.cv - a.e_target[2 * e + 1];
-                if (!isfinite(r0) || !isfinite(r1)) set_status(a.status, kDevNonFiniteResidual);
+                if (!isfinite(r0) || !isfinite(r1)) set_status(status, kDevNonFiniteResidual);
                 double w0 = J.behind ? 0.0 : a.e_weight[2 * e];
                 double w1 = J.behind ? 0.0 : a.e_weight[2 * e + 1];
                 const bool active = !(w0 == 0.0 && w1 == 0.0);  // bundle_adjust.cpp:151
@@ -322,7 +444,7 @@ __device__ void phase_assemble(const BAParams& a, const Shared& s, int k0, int k
                 sc[0] = hd;
                 sc[1] = bd;
                 sc[2] = 1.0 / hd;  // d_inv (bundle_adjust.cpp:69)
-                if (dslot >= 0 && !(hd > 0)) set_status(a.status, kDevNonPositiveDepth);
+                if (dslot >= 0 && !(hd > 0)) set_status(status, kDevNonPositiveDepth);
                 wr_sum += wrs;
                 wr_w += wrw;
             }
@@ -333,18 +455,19 @@ __device__ void phase_assemble(const BAParams& a, const Shared& s, int k0, int k
 
         // ---- ordered accumulation of the batch into the CTA system ----
         for (int w = 0; w < kWarps; ++w) {
-            const int* wiw = warp_ints(s, w);
+            const int* wiw = warp_ints(smem, L, w);
             if (wiw[1] < 0) break;
             const int si = wiw[0], ne = wiw[1];
             const bool dfree = wiw[2] >= 0;
-            const double* recw = s.rec + (size_t)w * kMaxEdges * kRec;
-            const double* vw = s.vb + (size_t)w * 2 * np;
+            const double* recw = at<double>(smem, L.rec) + (size_t)w * kMaxEdges * kRec;
+            const double* vw = at<double>(smem, L.vb) + (size_t)w * 2 * np;
             const double* bw = vw + np;
-            const double inv_h = s.scal[w * 4 + 2];
+            const double* scw = at<double>(smem, L.scal) + w * 4;
+            const double inv_h = scw[2];
             const int* p2e = wiw + 4;
             const int* nxt = wiw + 4 + kMaxFree;
             for (int ent = tid; ent < nent; ent += kThreads) {
-                const unsigned ab = s.ab[ent];
+                const unsigned ab = abt[ent];
                 const int ia = ab & 0xffff, ib = ab >> 16;
                 const int A = ia / 6, B = ib / 6, ra = ia - 6 * A, rb = ib - 6 * B;
                 double val = 0.0;
@@ -370,36 +493,37 @@ __device__ void phase_assemble(const BAParams& a, const Shared& s, int k0, int k
                     }
                 }
                 if (dfree) val -= (vw[ia] * inv_h) * vw[ib];
-                s.S[ent] += val;
+                S[ent] += val;
             }
             for (int i = tid; i < np; i += kThreads) {
                 double r = bw[i];
-                if (dfree) r -= vw[i] * (inv_h * s.scal[w * 4 + 1]);
-                s.rhs[i] += r;
+                if (dfree) r -= vw[i] * (inv_h * scw[1]);
+                rhs[i] += r;
             }
             // stash the patch's Schur data for the back-substitution
             const int kw = wiw[3];
             for (int i = tid; i < np; i += kThreads) a.patch_v[(size_t)kw * np + i] = vw[i];
             if (tid == 0) {
-                a.patch_h[kw] = s.scal[w * 4 + 0];
-                a.patch_bd[kw] = s.scal[w * 4 + 1];
+                a.patch_h[kw] = scw[0];
+                a.patch_bd[kw] = scw[1];
             }
         }
         __syncthreads();
     }
     // ---- write the CTA partial ----
+    double* wr = at<double>(smem, L.wr);
     if (lane == 0) {
-        s.wr[warp * 2] = wr_sum;
-        s.wr[warp * 2 + 1] = wr_w;
+        wr[warp * 2] = wr_sum;
+        wr[warp * 2 + 1] = wr_w;
     }
     __syncthreads();
-    for (int i = tid; i < nent; i += kThreads) part[i] = s.S[i];
-    for (int i = tid; i < np; i += kThreads) part[nent + i] = s.rhs[i];
+    for (int i = tid; i < nent; i += kThreads) part[i] = S[i];
+    for (int i = tid; i < np; i += kThreads) part[nent + i] = rhs[i];
     if (tid == 0) {
         double ws = 0, ww = 0;
         for (int w = 0; w < kWarps; ++w) {
-            ws += s.wr[2 * w];
-            ww += s.wr[2 * w + 1];
+            ws += wr[2 * w];
+            ww += wr[2 * w + 1];
         }
         part[nent + np] = ws;
         part[nent + np + 1] = ww;
@@ -407,187 +531,32 @@ __device__ void phase_assemble(const BAParams& a, const Shared& s, int k0, int k
 }
 
 // ---------------------------------------------------------------------------
-// P3: pivoted LDLT solve of the reduced camera system (CTA 0), retraction.
-// Pivot rule of Eigen's LDLT: at step k take the largest |diagonal| of the
-// not-yet-factored (original, permuted) diagonal.
-// ---------------------------------------------------------------------------
-__device__ void phase_solve(const BAParams& a, unsigned char* smem, const Layout& L, int np, bool poses_frozen) {
-    const int tid = threadIdx.x;
-    const int nent = nent_of(np);
-    __shared__ int s_piv;
-    __shared__ int s_fail;
-    if (np > 0 && !poses_frozen) {
-        double* A = reinterpret_cast<double*>(smem + L.A);
-        double* x = reinterpret_cast<double*>(smem + L.x);
-        double* od = reinterpret_cast<double*>(smem + L.od);
-        int* tr = reinterpret_cast<int*>(smem + L.tr);
-        // expand the upper triangle (row-major by rows a<=b)
-        for (int ent = tid; ent < nent; ent += kThreads) {
-            // invert ent -> (ia, ib)
-            int ia = 0, rowlen = np, base = 0;
-            while (ent >= base + rowlen) {
-                base += rowlen;
-                --rowlen;
-                ++ia;
-            }
-            const int ib = ia + (ent - base);
-            const double val = a.system[ent];
-            A[ia * np + ib] = val;
-            A[ib * np + ia] = val;
-        }
-        for (int i = tid; i < np; i += kThreads) x[i] = a.system[nent + i];
-        if (tid == 0) s_fail = 0;
-        __syncthreads();
-        for (int i = tid; i < np; i += kThreads) od[i] = A[i * np + i];
-        __syncthreads();
-        bool zero_all = false;
-        for (int k = 0; k < np; ++k) {
-            if (tid == 0) {
-                int big = k;
-                double bv = fabs(od[k]);
-                for (int i = k + 1; i < np; ++i) {
-                    if (fabs(od[i]) > bv) {
-                        bv = fabs(od[i]);
-                        big = i;
-                    }
-                }
-                tr[k] = big;
-                s_piv = big;
-            }
-            __syncthreads();
-            const int p = s_piv;
-            if (p != k) {
-                for (int j = tid; j < np; j += kThreads) {
-                    const double t = A[k * np + j];
-                    A[k * np + j] = A[p * np + j];
-                    A[p * np + j] = t;
-                }
-                __syncthreads();
-                for (int i = tid; i < np; i += kThreads) {
-                    const double t = A[i * np + k];
-                    A[i * np + k] = A[i * np + p];
-                    A[i * np + p] = t;
-                }
-                if (tid == 0) {
-                    const double t = od[k];
-                    od[k] = od[p];
-                    od[p] = t;
-                }
-                __syncthreads();
-            }
-            const double dk = A[k * np + k];
-            const bool valid = fabs(dk) > 0.0;
-            if (k == 0 && !valid) {
-                zero_all = true;
-                break;
-            }
-            if (valid) {
-                // trailing update with the unscaled column, then scale it
-                const int m = np - k - 1;
-                for (int t = tid; t < m * m; t += kThreads) {
-                    const int i = k + 1 + t / m, j = k + 1 + t % m;
-                    A[i * np + j] -= A[i * np + k] * (A[j * np + k] / dk);
-                }
-                __syncthreads();
-                for (int i = k + 1 + tid; i < np; i += kThreads) A[i * np + k] /= dk;
-                __syncthreads();
-            } else {
-                for (int i = k + 1 + tid; i < np; i += kThreads)
-                    if (A[i * np + k] != 0.0) s_fail = 1;
-                __syncthreads();
-            }
-        }
-        if (zero_all) {
-            for (int i = tid; i < np; i += kThreads) {
-                tr[i] = i;
-                A[i * np + i] = 0.0;
-            }
-        }
-        __syncthreads();
-        if (s_fail) {
-            if (tid == 0) set_status(a.status, kDevFactorization);
-        } else if (tid < 32) {
-            // substitutions on one warp
-            const int lane = tid;
-            if (lane == 0)
-                for (int k = 0; k < np; ++k) {
-                    const double t = x[k];
-                    x[k] = x[tr[k]];
-                    x[tr[k]] = t;
-                }
-            __syncwarp();
-            for (int j = 0; j < np; ++j) {
-                const double xj = x[j];
-                for (int i = j + 1 + lane; i < np; i += 32) x[i] -= A[i * np + j] * xj;
-                __syncwarp();
-            }
-            for (int i = lane; i < np; i += 32) {
-                const double dd = A[i * np + i];
-                x[i] = fabs(dd) > DBL_MIN ? x[i] / dd : 0.0;
-            }
-            __syncwarp();
-            for (int j = np - 1; j >= 0; --j) {
-                const double xj = x[j];
-                for (int i = lane; i < j; i += 32) x[i] -= A[j * np + i] * xj;
-                __syncwarp();
-            }
-            if (lane == 0)
-                for (int k = np - 1; k >= 0; --k) {
-                    const double t = x[k];
-                    x[k] = x[tr[k]];
-                    x[tr[k]] = t;
-                }
-            __syncwarp();
-            bool bad = false;
-            for (int i = lane; i < np; i += 32) {
-                a.delta[i] = x[i];
-                if (!isfinite(x[i])) bad = true;
-            }
-            if (__any_sync(0xffffffffu, bad) && lane == 0) set_status(a.status, kDevNonFinitePose);
-        }
-        __syncthreads();
-    }
-    // candidate poses (bundle_adjust.cpp:202-207)
-    for (int i = tid; i < a.n_poses; i += kThreads) {
-        const int slot = poses_frozen ? -1 : a.pose_free_slot[i];
-        const SE3 p = se3_load(a.poses + 7 * i);
-        if (slot >= 0 && np > 0) {
-            double xi[6];
-#pragma unroll
-            for (int c = 0; c < 6; ++c) xi[c] = a.delta[6 * slot + c];
-            se3_store(se3_retract(p, xi), a.cand_poses + 7 * i);
-        } else {
-            se3_store(p, a.cand_poses + 7 * i);
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
 // P4: depth back-substitution + residual at the candidate state.
 // ---------------------------------------------------------------------------
-__device__ void phase_update(const BAParams& a, const Shared& s, int k0, int k1, int np, double* part_tail) {
+__device__ void phase_update(const BAParams& a, unsigned char* smem, const Layout& L, const double* cand, int k0,
+                             int k1, int np, const double* delta, double* part_tail, int* status) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const Cam K{a.K[0], a.K[1], a.K[2], a.K[3]};
+    double* wr = at<double>(smem, L.wr);
     double wr_sum = 0, wr_w = 0;
     for (int k = k0 + warp; k < k1; k += kWarps) {
         double dnew = a.depth[k];
         if (a.depth_slot[k] >= 0) {
             double dot = 0.0;
-            for (int i = lane; i < np; i += 32) dot += a.patch_v[(size_t)k * np + i] * a.delta[i];
+            for (int i = lane; i < np; i += 32) dot += a.patch_v[(size_t)k * np + i] * delta[i];
             dot = warp_sum(dot);
             const double inv_h = 1.0 / a.patch_h[k];
             const double dd = inv_h * (a.patch_bd[k] - dot);  // bundle_adjust.cpp:88-89
-            if (!isfinite(dd) && lane == 0) set_status(a.status, kDevNonFiniteDepth);
+            if (!isfinite(dd) && lane == 0) set_status(status, kDevNonFiniteDepth);
             dnew = fmax(0.0, dnew + dd);  // bundle_adjust.cpp:211
-            // std::max(0.0, x) returns 0.0 for NaN x; fmax returns 0.0 too.
         }
         if (lane == 0) a.cand_depth[k] = dnew;
         const int eb = a.patch_edge_begin[k], ne = a.patch_edge_begin[k + 1] - eb;
-        const SE3 pi = se3_load(a.cand_poses + 7 * a.patch_src[k]);
+        const SE3 pi = se3_load(cand + 7 * a.patch_src[k]);
         double ws = 0, ww = 0;
         for (int l = lane; l < ne; l += 32) {
             const int e = eb + l;
-            const SE3 pj = se3_load(a.cand_poses + 7 * a.e_pose[e]);
+            const SE3 pj = se3_load(cand + 7 * a.e_pose[e]);
             double cu, cv;
             bool behind;
             reproject_center(pi, pj, K, a.patch_x + 9 * (size_t)k, a.patch_y + 9 * (size_t)k, dnew, &cu, &cv,
@@ -604,15 +573,15 @@ __device__ void phase_update(const BAParams& a, const Shared& s, int k0, int k1,
         wr_w += ww;
     }
     if (lane == 0) {
-        s.wr[warp * 2] = wr_sum;
-        s.wr[warp * 2 + 1] = wr_w;
+        wr[warp * 2] = wr_sum;
+        wr[warp * 2 + 1] = wr_w;
     }
     __syncthreads();
     if (tid == 0) {
         double ws = 0, ww = 0;
         for (int w = 0; w < kWarps; ++w) {
-            ws += s.wr[2 * w];
-            ww += s.wr[2 * w + 1];
+            ws += wr[2 * w];
+            ww += wr[2 * w + 1];
         }
         part_tail[2] = ws;
         part_tail[3] = ww;
@@ -626,56 +595,95 @@ __global__ void __launch_bounds__(kThreads, 1) ba_kernel(BAParams a) {
     const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
     const int k0 = (int)((long long)a.n_patches * b / G);
     const int k1 = (int)((long long)a.n_patches * (b + 1) / G);
+    const Layout L = make_layout(np_full, a.n_poses);
+    double* pose = at<double>(smem, L.pose);
+    double* cand = at<double>(smem, L.cand);
+    double* delta = at<double>(smem, L.delta);
+    const size_t pstride = (size_t)nent_of(np_full) + np_full + 4;
 
-    phase_freeze(a, k0, k1);
-    __syncthreads();
-
-    const int total_iters = a.structure_only + a.iterations;
-    for (int it = 0; it < total_iters; ++it) {
-        const bool structure = it < a.structure_only;
-        const int np = structure ? 0 : np_full;
-        const int nent = nent_of(np);
-        const size_t pstride = (size_t)nent_of(np_full) + np_full + 4;
-        const Layout L = make_layout(np);
-        const Shared s = carve(smem, L);
-        // entry -> (a, b) table for this np
+    // entry -> (a, b) table of the joint system; CTA copy of the pose state
+    {
+        unsigned* abt = at<unsigned>(smem, L.ab);
+        const int nent = nent_of(np_full);
         for (int ent = tid; ent < nent; ent += kThreads) {
-            int ia = 0, rowlen = np, base = 0;
+            int ia = 0, rowlen = np_full, base = 0;
             while (ent >= base + rowlen) {
                 base += rowlen;
                 --rowlen;
                 ++ia;
             }
-            s.ab[ent] = (unsigned)ia | ((unsigned)(ia + ent - base) << 16);
+            abt[ent] = (unsigned)ia | ((unsigned)(ia + ent - base) << 16);
         }
-        __syncthreads();
+        for (int i = tid; i < 7 * a.n_poses; i += kThreads) pose[i] = a.poses[i];
+    }
+    __syncthreads();
+    phase_freeze(a, pose, k0, k1);
+    __syncthreads();
+
+    int attempt_no = 0;  // global attempt counter -> buffer parity
+    const int total_iters = a.structure_only + a.iterations;
+    for (int it = 0; it < total_iters; ++it) {
+        const bool structure = it < a.structure_only;
+        const int np = structure ? 0 : np_full;
+        const int nent = nent_of(np);
         int attempt = 0;
         for (;;) {
-            const double lambda = attempt == 0 ? a.damping : a.damping * (attempt == 1 ? 1e3 : attempt == 2 ? 1e6 : 1e9);
-            double* part = a.partials + (size_t)b * pstride;
-            phase_assemble(a, s, k0, k1, np, structure, lambda, part);
+            const int buf = attempt_no & 1;
+            int* status = a.status2 + buf;
+            double* partials = a.partials + (size_t)buf * G * pstride;
+            const double lambda =
+                attempt == 0 ? a.damping : a.damping * (attempt == 1 ? 1e3 : attempt == 2 ? 1e6 : 1e9);
+            double* part = partials + (size_t)b * pstride;
+            phase_assemble(a, smem, L, pose, k0, k1, np, structure, lambda, part, status);
             grid.sync();
             // P2: ordered reduction of the CTA partials (+ damping on the diagonal)
-            for (int ent = b * kThreads + tid; ent < nent + np; ent += G * kThreads) {
-                double acc = 0.0;
-                for (int c = 0; c < G; ++c) acc += a.partials[(size_t)c * pstride + ent];
-                if (ent < nent) {
-                    const unsigned ab = s.ab[ent];
-                    if ((ab & 0xffff) == (ab >> 16)) acc += lambda;
+            {
+                const unsigned* abt = at<unsigned>(smem, L.ab);
+                for (int ent = b * kThreads + tid; ent < nent + np; ent += G * kThreads) {
+                    double acc = 0.0;
+                    for (int c = 0; c < G; ++c) acc += partials[(size_t)c * pstride + ent];
+                    if (ent < nent) {
+                        const unsigned ab = abt[ent];
+                        if ((ab & 0xffff) == (ab >> 16)) acc += lambda;
+                    }
+                    a.system[ent] = acc;
                 }
-                a.system[ent] = acc;
             }
             grid.sync();
-            if (b == 0) phase_solve(a, smem, L, np, structure);
-            grid.sync();
-            phase_update(a, s, k0, k1, np, part + nent + np);
+            // P3: every CTA solves the pose system and retracts its pose copy
+            if (np > 0) {
+                if (!ldlt_solve_cta(a.system, np, smem, L, delta)) {
+                    if (tid == 0) set_status(status, kDevFactorization);
+                } else {
+                    bool bad = false;
+                    for (int i = tid; i < np; i += kThreads) bad = bad || !isfinite(delta[i]);
+                    if (__syncthreads_or(bad) && tid == 0) set_status(status, kDevNonFinitePose);
+                }
+            }
+            for (int i = tid; i < a.n_poses; i += kThreads) {
+                const int slot = structure ? -1 : a.pose_free_slot[i];
+                const SE3 p = se3_load(pose + 7 * i);
+                if (slot >= 0 && np > 0) {
+                    double xi[6];
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) xi[c] = delta[6 * slot + c];
+                    se3_store(se3_retract(p, xi), cand + 7 * i);  // bundle_adjust.cpp:202-207
+                } else {
+                    se3_store(p, cand + 7 * i);
+                }
+            }
+            __syncthreads();
+            phase_update(a, smem, L, cand, k0, k1, np, delta, part + nent + np, status);
             grid.sync();
             // P5: identical decision in every CTA
-            const int status = *((volatile int*)a.status);
-            if (status != 0) return;
+            const int st = *((volatile int*)status);
+            if (st != 0) {
+                if (b == 0 && tid == 0) atomicOr(a.status, st);
+                return;
+            }
             double sb = 0, wb = 0, sa = 0, wa = 0;
             for (int c = 0; c < G; ++c) {
-                const double* pt = a.partials + (size_t)c * pstride + nent + np;
+                const double* pt = partials + (size_t)c * pstride + nent + np;
                 sb += pt[0];
                 wb += pt[1];
                 sa += pt[2];
@@ -684,23 +692,21 @@ __global__ void __launch_bounds__(kThreads, 1) ba_kernel(BAParams a) {
             const double before = wb > 0 ? sqrt(sb / wb) : 0.0;
             const double after = wa > 0 ? sqrt(sa / wa) : 0.0;
             const double thr = 1.5 * before + 1e-9;
+            ++attempt_no;
             bool accept, reject = false;
             if (structure || a.gn_step_mode) {
                 accept = true;
             } else if (attempt == 0) {
-                accept = !(after > thr);
+                accept = !(after > thr);  // bundle_adjust.cpp:330
             } else {
-                accept = after <= thr;
+                accept = after <= thr;  // bundle_adjust.cpp:339-340
             }
             if (!accept && !structure && !a.gn_step_mode) {
                 if (attempt < 3) {
                     ++attempt;
-                    // every CTA must finish reading the partials before any
-                    // CTA overwrites them in the retry's assembly
-                    grid.sync();
                     continue;
                 }
-                reject = true;
+                reject = true;  // keep the state put (bundle_adjust.cpp:347-353)
             }
             if (b == 0 && tid == 0 && !structure) {
                 int n = *a.n_norms;
@@ -714,11 +720,13 @@ __global__ void __launch_bounds__(kThreads, 1) ba_kernel(BAParams a) {
                 *a.n_norms = n;
             }
             if (!reject) {
-                if (b == 0)
-                    for (int i = tid; i < a.n_poses * 7; i += kThreads) a.poses[i] = a.cand_poses[i];
+                __syncthreads();
+                for (int i = tid; i < 7 * a.n_poses; i += kThreads) pose[i] = cand[i];
                 for (int k = k0 + tid; k < k1; k += kThreads) a.depth[k] = a.cand_depth[k];
+                if (b == 0)
+                    for (int i = tid; i < 7 * a.n_poses; i += kThreads) a.poses[i] = cand[i];
+                __syncthreads();
             }
-            grid.sync();
             break;
         }
     }
@@ -793,7 +801,7 @@ __global__ void __launch_bounds__(kThreads) schur_dense_kernel(int np, int nd, c
         return;
     }
     const int nent = nent_of(np);
-    // reduced system into `system` (upper + rhs), then reuse the LDLT phase
+    // reduced camera system S = H_pp - H_pd diag(1/h_dd) H_pd^T and its rhs
     for (int ent = tid; ent < nent; ent += kThreads) {
         int ia = 0, rowlen = np, base = 0;
         while (ent >= base + rowlen) {
@@ -812,16 +820,19 @@ __global__ void __launch_bounds__(kThreads) schur_dense_kernel(int np, int nd, c
         system[nent + i] = bp[i] - s;
     }
     __syncthreads();
-    __threadfence_block();
-    BAParams a;
-    a.system = system;
-    a.delta = dp;
-    a.status = status;
-    a.n_poses = 0;
-    const Layout L = make_layout(np);
-    phase_solve(a, smem, L, np, false);
-    __syncthreads();
-    if (*((volatile int*)status) != 0) return;
+    if (np > 0) {
+        const Layout L = make_layout(np, 0);
+        if (!ldlt_solve_cta(system, np, smem, L, dp)) {
+            if (tid == 0) set_status(status, kDevFactorization);
+            return;
+        }
+        bool bad = false;
+        for (int i = tid; i < np; i += kThreads) bad = bad || !isfinite(dp[i]);
+        if (__syncthreads_or(bad)) {
+            if (tid == 0) set_status(status, kDevNonFinitePose);
+            return;
+        }
+    }
     for (int k = tid; k < nd; k += kThreads) {
         double s = 0;
         for (int i = 0; i < np; ++i) s += hpd[i * nd + k] * dp[i];
@@ -896,23 +907,20 @@ __global__ void jacobians_kernel(int n, int pp, const double* pi, const double* 
 
 int ba_max_free_poses() { return kMaxFree; }
 int ba_max_edges_per_patch() { return kMaxEdges; }
+int ba_max_poses() { return kMaxPoses; }
 
 size_t ba_partials_doubles(int n_free_poses, int grid) {
     const int np = 6 * n_free_poses;
-    return (size_t)grid * ((size_t)nent_of(np) + np + 4);
+    return 2 * (size_t)grid * ((size_t)nent_of(np) + np + 4);  // double-buffered by attempt parity
 }
 
-static int ba_blocks_per_sm_cached(int smem) {
-    int blocks = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, ba_kernel, kThreads, smem) != cudaSuccess) return 1;
-    return blocks > 0 ? blocks : 1;
-}
-
-int ba_grid_size(int n_patches, int n_free_poses, int num_sms) {
-    const int np = 6 * n_free_poses;
-    const Layout L = make_layout(np);
+int ba_grid_size(int n_patches, int n_free_poses, int n_poses, int num_sms) {
+    const Layout L = make_layout(6 * n_free_poses, n_poses);
     cudaFuncSetAttribute(ba_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
-    const int per_sm = ba_blocks_per_sm_cached(L.total);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ba_kernel, kThreads, L.total) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
     int g = (n_patches + kWarps - 1) / kWarps;
     if (g > num_sms * per_sm) g = num_sms * per_sm;
     if (g < 1) g = 1;
@@ -920,13 +928,14 @@ int ba_grid_size(int n_patches, int n_free_poses, int num_sms) {
 }
 
 cudaError_t launch_ba(BAParams& p, int num_sms, cudaStream_t stream, int* grid_out) {
-    if (p.n_free_poses > kMaxFree) return cudaErrorNotSupported;
-    const int np = 6 * p.n_free_poses;
-    const Layout L = make_layout(np);
+    if (p.n_free_poses > kMaxFree || p.n_poses > kMaxPoses) return cudaErrorNotSupported;
+    const Layout L = make_layout(6 * p.n_free_poses, p.n_poses);
     cudaError_t err = cudaFuncSetAttribute(ba_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
     if (err != cudaSuccess) return err;
-    const int grid = ba_grid_size(p.n_patches, p.n_free_poses, num_sms);
+    const int grid = ba_grid_size(p.n_patches, p.n_free_poses, p.n_poses, num_sms);
     if (grid_out) *grid_out = grid;
+    err = cudaMemsetAsync(p.status2, 0, 2 * sizeof(int), stream);
+    if (err != cudaSuccess) return err;
     void* args[] = {&p};
     return cudaLaunchCooperativeKernel((void*)ba_kernel, dim3(grid), dim3(kThreads), args, L.total, stream);
 }
@@ -940,13 +949,12 @@ cudaError_t launch_schur_dense(int np, int nd, const double* hpp, const double* 
                                const double* bp, const double* bd, double* dp, double* dd, int* status,
                                cudaStream_t stream) {
     if (np > kMaxNp) return cudaErrorNotSupported;
-    const Layout L = make_layout(np);
-    const int smem = L.solve_total;
-    cudaError_t err = cudaFuncSetAttribute(schur_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const Layout L = make_layout(np, 0);
+    cudaError_t err = cudaFuncSetAttribute(schur_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
     if (err != cudaSuccess) return err;
     // `system` scratch lives right after dd in the caller's buffer (see capi.cu)
     double* system = dd + nd;
-    schur_dense_kernel<<<1, kThreads, smem, stream>>>(np, nd, hpp, hpd, hdd, bp, bd, dp, dd, system, status);
+    schur_dense_kernel<<<1, kThreads, L.total, stream>>>(np, nd, hpp, hpd, hdd, bp, bd, dp, dd, system, status);
     return cudaGetLastError();
 }
 

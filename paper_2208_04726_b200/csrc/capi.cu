@@ -4,6 +4,8 @@
 // The host code here only validates, flattens and moves memory; every
 // numeric result comes from the sm_100a kernels in corr.cu / ba.cu.  There
 // is deliberately no CPU compute fallback.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -29,12 +31,12 @@ void set_last_error(const std::string& msg) { g_last_error = msg; }
 struct BABuffers {
     DevBuf poses, free_slot, patch_src, px, py, depth, depth_slot, edge_begin, e_patch, e_pose, e_in, e_w, e_target,
         e_weight, cand_poses, cand_depth, patch_v, patch_h, patch_bd, partials, system, delta, norms, n_norms, dbg_h,
-        dbg_b, K;
+        dbg_b, K, status2;
     void release() {
         DevBuf* all[] = {&poses,    &free_slot,  &patch_src, &px,        &py,       &depth,    &depth_slot,
                          &edge_begin, &e_patch,  &e_pose,    &e_in,      &e_w,      &e_target, &e_weight,
                          &cand_poses, &cand_depth, &patch_v, &patch_h,   &patch_bd, &partials, &system,
-                         &delta,    &norms,      &n_norms,   &dbg_h,     &dbg_b,    &K};
+                         &delta,    &norms,      &n_norms,   &dbg_h,     &dbg_b,    &K,        &status2};
         for (DevBuf* b : all) b->release();
     }
 };
@@ -51,7 +53,7 @@ struct Window {
     int n_poses = 0, n_patches = 0, n_edges = 0;
     Plan plan;
     HostProblem shape;  // sizes, K, image size (pointers unused)
-    DevBuf pose_slot, patch_feats, corr, init_poses, init_depth;
+    DevBuf pose_slot, patch_feats, corr, init_poses, init_depth, order;
 };
 
 struct pvo_ctx {
@@ -66,6 +68,11 @@ struct pvo_ctx {
     DevBuf feat0, feat1, gram0, gram1;
     // direct-op scratch
     DevBuf s0, s1, s2, s3, s4, s5, s6, s7, s8;
+    // TMA descriptors of the frame store (feat0, feat1, gram0, gram1) and the
+    // production correlation kernel's scratch
+    CUtensorMap maps[4];
+    bool maps_ok = false;
+    DevBuf c_coords, c_meta, c_over, c_count, c_order;
     BABuffers ba;
     Window win;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -213,7 +220,11 @@ pvo_dev::BAParams stage_problem(pvo_ctx* ctx, const HostProblem& pr, const Plan&
     a.patch_v = B.patch_v.as<double>((size_t)pr.n_patches * std::max(np, 1));
     a.patch_h = B.patch_h.as<double>(pr.n_patches);
     a.patch_bd = B.patch_bd.as<double>(pr.n_patches);
-    const int grid = pvo_dev::ba_grid_size(pr.n_patches, pl.n_free_poses, ctx->num_sms);
+    if (pr.n_poses > pvo_dev::ba_max_poses()) {
+        fail(PVO_UNSUPPORTED, "ba: more than " + std::to_string(pvo_dev::ba_max_poses()) + " poses in one problem");
+    }
+    a.status2 = B.status2.as<int>(2);
+    const int grid = pvo_dev::ba_grid_size(pr.n_patches, pl.n_free_poses, pr.n_poses, ctx->num_sms);
     a.partials = B.partials.as<double>(pvo_dev::ba_partials_doubles(pl.n_free_poses, grid));
     a.system = B.system.as<double>((size_t)np * (np + 1) / 2 + np + 1);
     a.delta = B.delta.as<double>(std::max(np, 1));
@@ -248,6 +259,126 @@ void compute_gram(pvo_ctx* ctx, const float* f0, float* g0, const float* f1, flo
         cuda_check(pvo_dev::launch_gram(f1, g1, w1, h1, C, ctx->num_sms, ctx->stream), "gram kernel");
         ctx->launches += 1;
     }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cuda_check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q),
+                   "cudaGetDriverEntryPoint");
+        if (q != cudaDriverEntryPointSuccess || !p) fail(PVO_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+void encode_4d(CUtensorMap* map, void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3, uint32_t box0,
+               uint32_t box1, uint32_t box2) {
+    const cuuint64_t dims[4] = {d0, d1, d2, d3};
+    const cuuint64_t strides[3] = {d0 * 4, d0 * d1 * 4, d0 * d1 * d2 * 4};
+    const cuuint32_t box[4] = {box0, box1, box2, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = tensor_map_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims, strides, box, estr,
+                                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(PVO_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+}
+
+// (Re)build the frame-store TMA descriptors: the feature tile box is
+// 132 channels x 9 x 9 cells (channels 128..131 are out of bounds -> zero
+// pad), the Gram box 8 x 9 x 9.
+void encode_frame_maps(pvo_ctx* ctx) {
+    ctx->maps_ok = false;
+    if (ctx->C != 128 || ctx->w1 < 1 || ctx->h1 < 1) return;  // generic kernel only
+    encode_4d(&ctx->maps[0], ctx->feat0.p, 128, ctx->w0, ctx->h0, ctx->nf, 132, 9, 9);
+    encode_4d(&ctx->maps[1], ctx->feat1.p, 128, ctx->w1, ctx->h1, ctx->nf, 132, 9, 9);
+    encode_4d(&ctx->maps[2], ctx->gram0.p, 8, ctx->w0, ctx->h0, ctx->nf, 8, 9, 9);
+    encode_4d(&ctx->maps[3], ctx->gram1.p, 8, ctx->w1, ctx->h1, ctx->nf, 8, 9, 9);
+    ctx->maps_ok = true;
+}
+
+// Correlation of a batch of edges against the frame store: the TMA kernel for
+// D = 128 followed by the generic kernel on its overflow items, or the generic
+// kernel alone.  `t` carries the inputs; scratch is filled in here.
+void run_corr(pvo_ctx* ctx, pvo_dev::CorrTmaParams t) {
+    if (t.n_edges <= 0) return;
+    if (ctx->maps_ok) {
+        t.w0 = ctx->w0;
+        t.h0 = ctx->h0;
+        t.w1 = ctx->w1;
+        t.h1 = ctx->h1;
+        t.coords = ctx->c_coords.as<double>((size_t)t.n_edges * 18);
+        t.meta = ctx->c_meta.as<int>((size_t)t.n_edges * 8);
+        t.overflow = ctx->c_over.as<int>((size_t)t.n_edges * 2);
+        t.overflow_count = ctx->c_count.as<int>(1);
+        t.status = ctx->d_status;
+        cuda_check(cudaMemsetAsync(t.overflow_count, 0, sizeof(int), ctx->stream), "memset");
+        cuda_check(pvo_dev::launch_corr_tma(t, ctx->maps, ctx->num_sms, ctx->stream), "corr_tma kernel");
+        ctx->launches += 1;
+        pvo_dev::CorrParams cp;
+        cp.n_edges = t.n_edges;
+        cp.channels = ctx->C;
+        cp.e_patch = t.e_patch;
+        cp.e_pose = t.e_pose;
+        cp.e_slot = t.e_slot;
+        cp.pose_slot = t.pose_slot;
+        cp.coords = t.coords;
+        cp.feat0 = static_cast<const float*>(ctx->feat0.p);
+        cp.feat1 = static_cast<const float*>(ctx->feat1.p);
+        cp.gram0 = static_cast<const float*>(ctx->gram0.p);
+        cp.gram1 = static_cast<const float*>(ctx->gram1.p);
+        cp.w0 = ctx->w0;
+        cp.h0 = ctx->h0;
+        cp.w1 = ctx->w1;
+        cp.h1 = ctx->h1;
+        cp.patch_feats = t.patch_feats;
+        cp.out = t.out;
+        cp.status = ctx->d_status;
+        cp.items = t.overflow;
+        cp.items_count = t.overflow_count;
+        cuda_check(pvo_dev::launch_corr_items(cp, ctx->num_sms, ctx->stream), "corr overflow kernel");
+        ctx->launches += 1;
+        return;
+    }
+    pvo_dev::CorrParams cp;
+    cp.n_edges = t.n_edges;
+    cp.channels = ctx->C;
+    cp.e_patch = t.e_patch;
+    cp.e_pose = t.e_pose;
+    cp.e_slot = t.e_slot;
+    cp.pose_slot = t.pose_slot;
+    cp.coords = t.coords_in;
+    cp.poses = t.poses;
+    cp.patch_src = t.patch_src;
+    cp.patch_x = t.patch_x;
+    cp.patch_y = t.patch_y;
+    cp.depth = t.depth;
+    cp.K = t.K;
+    cp.feat0 = static_cast<const float*>(ctx->feat0.p);
+    cp.feat1 = static_cast<const float*>(ctx->feat1.p);
+    cp.gram0 = static_cast<const float*>(ctx->gram0.p);
+    cp.gram1 = static_cast<const float*>(ctx->gram1.p);
+    cp.w0 = ctx->w0;
+    cp.h0 = ctx->h0;
+    cp.w1 = ctx->w1;
+    cp.h1 = ctx->h1;
+    cp.patch_feats = t.patch_feats;
+    cp.out = t.out;
+    cp.status = ctx->d_status;
+    cuda_check(pvo_dev::launch_corr(cp, ctx->stream), "corr kernel");
+    ctx->launches += 1;
+}
+
+// Stable order of edges by frame-store slot (L2 locality of the TMA kernel).
+std::vector<int> slot_order(int n, const int* slot_of_edge) {
+    std::vector<int> order(n);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return slot_of_edge[a] < slot_of_edge[b]; });
+    return order;
 }
 
 }  // namespace
@@ -531,6 +662,7 @@ int pvo_frames_reserve(pvo_ctx* ctx, int n_frames, int w0, int h0, int w1, int h
         ctx->feat1.get(sizeof(float) * (size_t)n_frames * std::max(w1 * h1, 1) * C);
         ctx->gram0.get(sizeof(float) * (size_t)n_frames * w0 * h0 * 8);
         ctx->gram1.get(sizeof(float) * (size_t)n_frames * std::max(w1 * h1, 1) * 8);
+        encode_frame_maps(ctx);
     });
 }
 
@@ -603,26 +735,22 @@ int pvo_correlate_batch(pvo_ctx* ctx, int n_edges, int n_patches, int p, const i
             dpf = upload(ctx, ctx->s3, patch_feats, (size_t)n_patches * 2 * 9 * C);
             dout = ctx->s4.as<float>((size_t)n_edges * 2 * 9 * 49);
         }
+        const int* dorder = nullptr;
+        if (memspace != PVO_DEVICE) {
+            const std::vector<int> order = slot_order(n_edges, e_slot);
+            dorder = upload(ctx, ctx->c_order, order.data(), order.size());
+            sync(ctx);
+        }
         reset_status(ctx);
-        pvo_dev::CorrParams cp;
-        cp.n_edges = n_edges;
-        cp.channels = C;
-        cp.e_patch = dep;
-        cp.e_slot = des;
-        cp.coords = dc;
-        cp.feat0 = static_cast<const float*>(ctx->feat0.p);
-        cp.feat1 = static_cast<const float*>(ctx->feat1.p);
-        cp.gram0 = static_cast<const float*>(ctx->gram0.p);
-        cp.gram1 = static_cast<const float*>(ctx->gram1.p);
-        cp.w0 = ctx->w0;
-        cp.h0 = ctx->h0;
-        cp.w1 = ctx->w1;
-        cp.h1 = ctx->h1;
-        cp.patch_feats = dpf;
-        cp.out = dout;
-        cp.status = ctx->d_status;
-        cuda_check(pvo_dev::launch_corr(cp, ctx->stream), "corr kernel");
-        ctx->launches += 1;
+        pvo_dev::CorrTmaParams t;
+        t.n_edges = n_edges;
+        t.order = dorder;
+        t.e_patch = dep;
+        t.e_slot = des;
+        t.coords_in = dc;
+        t.patch_feats = dpf;
+        t.out = dout;
+        run_corr(ctx, t);
         if (memspace != PVO_DEVICE) {
             download(ctx, out, dout, (size_t)n_edges * 2 * 9 * 49);
             if (read_status(ctx)) fail(PVO_INVALID_ARGUMENT, "correlate: non-finite reprojection");
@@ -738,6 +866,13 @@ int pvo_window_load(pvo_ctx* ctx, int n_poses, const double* poses, const uint8_
         w.n_edges = n_edges;
         stage_problem(ctx, pr, w.plan, 64);
         upload(ctx, w.pose_slot, pose_slot, n_poses);
+        {
+            std::vector<int> eslot(n_edges);
+            for (int e = 0; e < n_edges; ++e) eslot[e] = pose_slot[e_pose[e]];
+            const std::vector<int> order = slot_order(n_edges, eslot.data());
+            upload(ctx, w.order, order.data(), order.size());
+            sync(ctx);
+        }
         upload(ctx, w.patch_feats, patch_feats, (size_t)n_patches * 2 * 9 * ctx->C);
         upload(ctx, w.init_poses, poses, (size_t)n_poses * 7);
         upload(ctx, w.init_depth, depth, n_patches);
@@ -764,11 +899,11 @@ int pvo_window_set_state(pvo_ctx* ctx, const double* poses, const double* depth,
 }
 
 namespace {
-pvo_dev::CorrParams window_corr_params(pvo_ctx* ctx, float* out) {
+pvo_dev::CorrTmaParams window_corr_params(pvo_ctx* ctx, float* out) {
     Window& w = ctx->win;
-    pvo_dev::CorrParams cp;
+    pvo_dev::CorrTmaParams cp;
     cp.n_edges = w.n_edges;
-    cp.channels = ctx->C;
+    cp.order = static_cast<const int*>(w.order.p);
     cp.e_patch = static_cast<const int*>(ctx->ba.e_patch.p);
     cp.e_pose = static_cast<const int*>(ctx->ba.e_pose.p);
     cp.pose_slot = static_cast<const int*>(w.pose_slot.p);
@@ -778,17 +913,8 @@ pvo_dev::CorrParams window_corr_params(pvo_ctx* ctx, float* out) {
     cp.patch_y = static_cast<const double*>(ctx->ba.py.p);
     cp.depth = static_cast<const double*>(ctx->ba.depth.p);
     cp.K = static_cast<const double*>(ctx->ba.K.p);
-    cp.feat0 = static_cast<const float*>(ctx->feat0.p);
-    cp.feat1 = static_cast<const float*>(ctx->feat1.p);
-    cp.gram0 = static_cast<const float*>(ctx->gram0.p);
-    cp.gram1 = static_cast<const float*>(ctx->gram1.p);
-    cp.w0 = ctx->w0;
-    cp.h0 = ctx->h0;
-    cp.w1 = ctx->w1;
-    cp.h1 = ctx->h1;
     cp.patch_feats = static_cast<const float*>(w.patch_feats.p);
     cp.out = out ? out : static_cast<float*>(w.corr.p);
-    cp.status = ctx->d_status;
     return cp;
 }
 
@@ -821,7 +947,8 @@ pvo_dev::BAParams window_ba_params(pvo_ctx* ctx, int iterations, double damping)
     a.patch_v = static_cast<double*>(B.patch_v.p);
     a.patch_h = static_cast<double*>(B.patch_h.p);
     a.patch_bd = static_cast<double*>(B.patch_bd.p);
-    const int grid = pvo_dev::ba_grid_size(w.n_patches, w.plan.n_free_poses, ctx->num_sms);
+    a.status2 = B.status2.as<int>(2);
+    const int grid = pvo_dev::ba_grid_size(w.n_patches, w.plan.n_free_poses, w.n_poses, ctx->num_sms);
     a.partials = B.partials.as<double>(pvo_dev::ba_partials_doubles(w.plan.n_free_poses, grid));
     a.system = B.system.as<double>((size_t)np * (np + 1) / 2 + np + 1);
     a.delta = B.delta.as<double>(std::max(np, 1));
@@ -844,9 +971,7 @@ int pvo_window_correlate(pvo_ctx* ctx, float* out, int memspace) {
         Window& w = ctx->win;
         if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
         reset_status(ctx);
-        pvo_dev::CorrParams cp = window_corr_params(ctx, memspace == PVO_DEVICE ? out : nullptr);
-        cuda_check(pvo_dev::launch_corr(cp, ctx->stream), "corr kernel");
-        ctx->launches += 1;
+        run_corr(ctx, window_corr_params(ctx, memspace == PVO_DEVICE ? out : nullptr));
         if (out && memspace != PVO_DEVICE) {
             download(ctx, out, static_cast<float*>(w.corr.p), (size_t)w.n_edges * 2 * 9 * 49);
             if (read_status(ctx)) fail(PVO_INVALID_ARGUMENT, "correlate: non-finite reprojection");
@@ -862,9 +987,7 @@ int pvo_window_iteration(pvo_ctx* ctx, int iterations, double damping, float* co
         if (iterations < 0) fail(PVO_INVALID_ARGUMENT, "ba: negative iteration count");
         reset_status(ctx);
         cuda_check(cudaEventRecord(ctx->ev[0], ctx->stream), "event");
-        pvo_dev::CorrParams cp = window_corr_params(ctx, corr_memspace == PVO_DEVICE ? corr_out : nullptr);
-        cuda_check(pvo_dev::launch_corr(cp, ctx->stream), "corr kernel");
-        ctx->launches += 1;
+        run_corr(ctx, window_corr_params(ctx, corr_memspace == PVO_DEVICE ? corr_out : nullptr));
         cuda_check(cudaEventRecord(ctx->ev[1], ctx->stream), "event");
         pvo_dev::BAParams a = window_ba_params(ctx, iterations, damping);
         launch_ba_checked(ctx, a);

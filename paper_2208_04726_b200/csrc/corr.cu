@@ -92,8 +92,14 @@ __global__ void __launch_bounds__(kThreads) corr_kernel(CorrParams a) {
     __shared__ double s_xy[2 * kPix];
     __shared__ int s_bad;
 
-    const int e = blockIdx.x;
-    if (e >= a.n_edges) return;
+    // Work items: one edge (both levels) per CTA, or — overflow mode — a
+    // device-side list of (edge, level) items left over by corr_tma.cu.
+    const int n_items = a.items ? *a.items_count : a.n_edges;
+    const int item_stride = a.items ? gridDim.x : a.n_edges;
+    for (int item = blockIdx.x; item < n_items; item += item_stride) {
+    const int e = a.items ? (a.items[item] >> 1) : item;
+    const int lv_begin = a.items ? (a.items[item] & 1) : 0;
+    const int lv_end = a.items ? lv_begin + 1 : 2;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int D = a.channels;
@@ -117,13 +123,14 @@ __global__ void __launch_bounds__(kThreads) corr_kernel(CorrParams a) {
     __syncthreads();
     if (s_bad) {
         if (tid == 0) atomicOr(a.status, 1 << kDevBadCoords);  // correlation.cpp:43-45
-        return;
+        __syncthreads();
+        continue;
     }
 
     const int k = a.e_patch[e];
     const int slot = a.e_slot ? a.e_slot[e] : a.pose_slot[a.e_pose[e]];
 
-    for (int level = 0; level < 2; ++level) {
+    for (int level = lv_begin; level < lv_end; ++level) {
         const int W = level ? a.w1 : a.w0;
         const int H = level ? a.h1 : a.h0;
         const float* fbase = (level ? a.feat1 : a.feat0) + (size_t)slot * W * H * D;
@@ -295,6 +302,7 @@ __global__ void __launch_bounds__(kThreads) corr_kernel(CorrParams a) {
             __syncthreads();
         }
     }
+    }  // item loop
 }
 
 // Gram terms of one pyramid level of one frame.  One warp per cell.
@@ -354,6 +362,14 @@ cudaError_t launch_corr(const CorrParams& p, cudaStream_t stream) {
     cudaError_t err = cudaFuncSetAttribute(corr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
     corr_kernel<<<p.n_edges, kThreads, smem, stream>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_corr_items(const CorrParams& p, int num_sms, cudaStream_t stream) {
+    const int smem = corr_smem_bytes(p.channels);
+    cudaError_t err = cudaFuncSetAttribute(corr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err != cudaSuccess) return err;
+    corr_kernel<<<num_sms * 2, kThreads, smem, stream>>>(p);
     return cudaGetLastError();
 }
 

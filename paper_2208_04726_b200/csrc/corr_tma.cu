@@ -1,0 +1,345 @@
+// corr_tma.cu — the production correlation kernel (K2) for D = 128, sm_100a.
+//
+// Same arithmetic as corr.cu (see its header: dots at integer cells + per-frame
+// Gram terms, regrouped by linearity from correlation.cpp:8-71), organised for
+// the B200 memory system:
+//   * persistent CTAs (one per SM), each walking its share of the edges in
+//     target-frame order, so the frames being read stay resident in L2;
+//   * a 3-stage TMA pipeline: for every (edge, level) one elected thread issues
+//       - a 4-D tensor copy of the 9x9-cell tile [9][9][132] fp32 whose channel
+//         box (132) overhangs the 128 stored channels, so TMA zero-fills 4 pad
+//         channels per cell — the padded, bank-conflict-free layout the FMA loop
+//         wants — and zero-fills out-of-image cells, which IS the reference's
+//         zero padding (features.cpp:15-17);
+//       - a 4-D tensor copy of the tile's Gram records [9][9][8];
+//       - a 1-D bulk copy of the patch's 9 x 128 descriptors;
+//     all completing on one mbarrier (complete_tx bytes);
+//   * FP32 FMA dot products, register-blocked 3 cells x 9 pixels per lane, warps
+//     split the channel chunks; fixed-order cross-warp sum (deterministic);
+//   * output recombination in FP32 with the bilinear weights' fractional parts
+//     taken exactly in FP64 (x - floor(x)), as the reference does.
+// (edge, level) tiles whose 9 pixel windows do not fit one 9x9 tile (extreme
+// zoom, pixels far outside the image) are diverted to an overflow list that the
+// generic kernel (corr.cu) finishes.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "geometry.cuh"
+#include "kernels.cuh"
+
+namespace pvo_dev {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kD = 128;
+constexpr int kDP = 132;  // padded cell stride (floats)
+constexpr int kBox = 9;
+constexpr int kCells = kBox * kBox;
+constexpr int kPix = 9;
+constexpr int kStages = 3;
+constexpr int kTileBytes = kCells * kDP * 4;                  // 42768
+constexpr int kTileRegion = (kTileBytes + 127) / 128 * 128;   // 42880
+constexpr int kGramBytes = kCells * 8 * 4;                    // 2592
+constexpr int kGramRegion = (kGramBytes + 127) / 128 * 128;   // 2688
+constexpr int kGBytes = kPix * kD * 4;                        // 4608
+constexpr int kStageBytes = kTileRegion + kGramRegion + kGBytes;  // 50176
+constexpr int kTxBytes = kTileBytes + kGramBytes + kGBytes;
+// after the stages
+constexpr int kPartOff = kStages * kStageBytes;                    // [8][9][81] f32
+constexpr int kDotsOff = kPartOff + kWarps * kPix * kCells * 4;    // [9][81] f32
+constexpr int kGramSOff = kDotsOff + kPix * kCells * 4;            // [81][5] f32
+constexpr int kSmemBytes = kGramSOff + kCells * 5 * 4 + 1024;      // + alignment slack
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        "@!P bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+        "%5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+struct TileMeta {
+    int x0, y0, tw, th;  // union origin (cells) and extent; tw <= 0: not on this path
+};
+
+// reproject_patch of pixel `pix` of edge e (camera.cpp:47-71)
+__device__ inline void edge_pixel(const CorrTmaParams& a, int e, int pix, double* xy) {
+    if (a.coords_in) {
+        xy[0] = a.coords_in[(size_t)e * 18 + 2 * pix];
+        xy[1] = a.coords_in[(size_t)e * 18 + 2 * pix + 1];
+        return;
+    }
+    const int k = a.e_patch[e];
+    const SE3 pi = se3_load(a.poses + 7 * a.patch_src[k]);
+    const SE3 pj = se3_load(a.poses + 7 * a.e_pose[e]);
+    const double px = a.patch_x[(size_t)k * 9 + pix], py = a.patch_y[(size_t)k * 9 + pix];
+    if (se3_equal(pi, pj)) {
+        xy[0] = px;
+        xy[1] = py;
+        return;
+    }
+    const Relative rel = relative_pose(pi, pj);
+    const Cam K{a.K[0], a.K[1], a.K[2], a.K[3]};
+    reproject_point(rel, K, a.depth[k], px, py, &xy[0], &xy[1]);
+}
+
+__device__ __forceinline__ int clamp_floor(double b, int extent) {
+    return (int)floor(fmin(fmax(b, -16.0), (double)extent + 16.0));
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    corr_tma_kernel(const __grid_constant__ CUtensorMap feat0, const __grid_constant__ CUtensorMap feat1,
+                    const __grid_constant__ CUtensorMap gram0, const __grid_constant__ CUtensorMap gram1,
+                    CorrTmaParams a) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t full[kStages];
+    __shared__ double s_bx[kPix], s_by[kPix];
+    __shared__ int s_fx[kPix], s_fy[kPix];
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int G = gridDim.x, b = blockIdx.x;
+    const int my_edges = a.n_edges > b ? (a.n_edges - 1 - b) / G + 1 : 0;
+    const int n_tiles = 2 * my_edges;
+
+    float* s_part = reinterpret_cast<float*>(smem + kPartOff);
+    float* s_dots = reinterpret_cast<float*>(smem + kDotsOff);
+    float* s_gram = reinterpret_cast<float*>(smem + kGramSOff);
+
+    // ---- phase 0: coordinates and tile geometry of this CTA's edges ----
+    for (int i = tid; i < my_edges * kPix; i += kThreads) {
+        const int e = a.order ? a.order[b + (i / kPix) * G] : b + (i / kPix) * G;
+        const int pix = i % kPix;
+        double xy[2];
+        edge_pixel(a, e, pix, xy);
+        a.coords[(size_t)e * 18 + 2 * pix] = xy[0];
+        a.coords[(size_t)e * 18 + 2 * pix + 1] = xy[1];
+    }
+    __syncthreads();
+    for (int i = tid; i < my_edges * 2; i += kThreads) {
+        const int e = a.order ? a.order[b + (i >> 1) * G] : b + (i >> 1) * G;
+        const int level = i & 1;
+        const double scale = level ? 16.0 : 4.0;
+        const int W = level ? a.w1 : a.w0, H = level ? a.h1 : a.h0;
+        int xmin = 1 << 30, xmax = -(1 << 30), ymin = 1 << 30, ymax = -(1 << 30);
+        bool finite = true;
+        for (int p = 0; p < kPix; ++p) {
+            const double x = a.coords[(size_t)e * 18 + 2 * p], y = a.coords[(size_t)e * 18 + 2 * p + 1];
+            finite = finite && isfinite(x) && isfinite(y);
+            const int fx = clamp_floor(x / scale, W), fy = clamp_floor(y / scale, H);
+            xmin = min(xmin, fx);
+            xmax = max(xmax, fx);
+            ymin = min(ymin, fy);
+            ymax = max(ymax, fy);
+        }
+        TileMeta m{xmin - 3, ymin - 3, xmax - xmin + 8, ymax - ymin + 8};
+        if (!finite) {
+            atomicOr(a.status, 1 << kDevBadCoords);  // correlation.cpp:43-45
+            m.tw = -1;
+        } else if (m.tw > kBox || m.th > kBox) {
+            const int slot = atomicAdd(a.overflow_count, 1);
+            a.overflow[slot] = 2 * e + level;
+            m.tw = 0;
+        }
+        reinterpret_cast<int4*>(a.meta)[2 * e + level] = make_int4(m.x0, m.y0, m.tw, m.th);
+    }
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    auto tile_edge = [&](int t) { return a.order ? a.order[b + (t >> 1) * G] : b + (t >> 1) * G; };
+    auto issue = [&](int t) {
+        const int s = t % kStages;
+        const int e = tile_edge(t), level = t & 1;
+        const int4 m = reinterpret_cast<const int4*>(a.meta)[2 * e + level];
+        if (m.z <= 0) {  // not on this path: complete the phase without data
+            mbar_arrive(&full[s]);
+            return;
+        }
+        unsigned char* st = smem + s * kStageBytes;
+        const int slot = a.e_slot ? a.e_slot[e] : a.pose_slot[a.e_pose[e]];
+        mbar_expect_tx(&full[s], kTxBytes);
+        tma_load_4d(st, level ? &feat1 : &feat0, 0, m.x, m.y, slot, &full[s]);
+        tma_load_4d(st + kTileRegion, level ? &gram1 : &gram0, 0, m.x, m.y, slot, &full[s]);
+        const float* g = a.patch_feats + ((size_t)a.e_patch[e] * 2 + level) * kPix * kD;
+        bulk_load(st + kTileRegion + kGramRegion, g, kGBytes, &full[s]);
+    };
+    if (tid == 0) {
+        for (int t = 0; t < kStages && t < n_tiles; ++t) issue(t);
+    }
+
+    for (int t = 0; t < n_tiles; ++t) {
+        const int s = t % kStages;
+        const int e = tile_edge(t), level = t & 1;
+        const int4 m = reinterpret_cast<const int4*>(a.meta)[2 * e + level];
+        mbar_wait(&full[s], (uint32_t)((t / kStages) & 1));
+        const unsigned char* st = smem + s * kStageBytes;
+        const bool active = m.z > 0;
+        const int TW = m.z, TH = m.w, NC = active ? TW * TH : 0;
+
+        // ---- dot products: lane owns up to 3 union cells x 9 pixels; warp owns 4 chunks ----
+        if (active) {
+            const float* tile = reinterpret_cast<const float*>(st);
+            const float* g = reinterpret_cast<const float*>(st + kTileRegion + kGramRegion);
+            int off[3];
+#pragma unroll
+            for (int ci = 0; ci < 3; ++ci) {
+                const int c = lane + 32 * ci;
+                const int cy = c / TW, cx = c - cy * TW;
+                off[ci] = c < NC ? (cy * kBox + cx) * kDP : -1;
+            }
+            float acc[3][kPix];
+#pragma unroll
+            for (int ci = 0; ci < 3; ++ci)
+#pragma unroll
+                for (int p = 0; p < kPix; ++p) acc[ci][p] = 0.f;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int ch = warp + kWarps * j;
+                float4 gv[kPix];
+#pragma unroll
+                for (int p = 0; p < kPix; ++p) gv[p] = *reinterpret_cast<const float4*>(g + p * kD + 4 * ch);
+#pragma unroll
+                for (int ci = 0; ci < 3; ++ci) {
+                    if (off[ci] >= 0) {
+                        const float4 v = *reinterpret_cast<const float4*>(tile + off[ci] + 4 * ch);
+#pragma unroll
+                        for (int p = 0; p < kPix; ++p) {
+                            float x = acc[ci][p];
+                            x = fmaf(v.x, gv[p].x, x);
+                            x = fmaf(v.y, gv[p].y, x);
+                            x = fmaf(v.z, gv[p].z, x);
+                            x = fmaf(v.w, gv[p].w, x);
+                            acc[ci][p] = x;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int ci = 0; ci < 3; ++ci) {
+                const int c = lane + 32 * ci;
+                if (c < NC) {
+#pragma unroll
+                    for (int p = 0; p < kPix; ++p) s_part[(warp * kPix + p) * kCells + c] = acc[ci][p];
+                }
+            }
+        }
+        __syncthreads();  // (A) partials complete; stage s no longer read below except gram
+        if (active) {
+            for (int i = tid; i < kPix * NC; i += kThreads) {
+                const int p = i / NC, c = i - p * NC;
+                float sum = 0.f;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) sum += s_part[(w * kPix + p) * kCells + c];
+                s_dots[p * kCells + c] = sum;
+            }
+            const float* gr = reinterpret_cast<const float*>(st + kTileRegion);
+            for (int i = tid; i < NC * 5; i += kThreads) {
+                const int c = i / 5, r = i - 5 * c;
+                const int cy = c / TW, cx = c - cy * TW;
+                s_gram[i] = gr[(cy * kBox + cx) * 8 + r];
+            }
+            if (tid < kPix) {
+                const double scale = level ? 16.0 : 4.0;
+                const int W = level ? a.w1 : a.w0, H = level ? a.h1 : a.h0;
+                const double bx = a.coords[(size_t)e * 18 + 2 * tid] / scale;
+                const double by = a.coords[(size_t)e * 18 + 2 * tid + 1] / scale;
+                s_bx[tid] = bx;
+                s_by[tid] = by;
+                s_fx[tid] = clamp_floor(bx, W);
+                s_fy[tid] = clamp_floor(by, H);
+            }
+        }
+        __syncthreads();  // (B) stage s free: refill it
+        if (tid == 0 && t + kStages < n_tiles) issue(t + kStages);
+        if (active) {
+            float* out = a.out + ((size_t)e * 2 + level) * kPix * 49;
+            for (int o = tid; o < kPix * 49; o += kThreads) {
+                const int p = o / 49, ab = o - 49 * p;
+                const int alpha = ab / 7, beta = ab - 7 * alpha;
+                // x = base + (beta - 3) and its floor exactly as features.cpp:10-13
+                const int x0 = s_fx[p] + beta - 3, y0 = s_fy[p] + alpha - 3;
+                const float ax = (float)((s_bx[p] + (double)(beta - 3)) - (double)x0);
+                const float ay = (float)((s_by[p] + (double)(alpha - 3)) - (double)y0);
+                const int c00 = (y0 - m.y) * TW + (x0 - m.x);
+                const float* d = s_dots + p * kCells;
+                const float w00 = (1.f - ax) * (1.f - ay), w10 = ax * (1.f - ay);
+                const float w01 = (1.f - ax) * ay, w11 = ax * ay;
+                float dot = w00 * d[c00];
+                dot = fmaf(w10, d[c00 + 1], dot);
+                dot = fmaf(w01, d[c00 + TW], dot);
+                dot = fmaf(w11, d[c00 + TW + 1], dot);
+                const float* g00 = s_gram + 5 * c00;
+                const float* g10 = g00 + 5;
+                const float* g01 = g00 + 5 * TW;
+                const float* g11 = g01 + 5;
+                // |f(x)|^2 = sum_t sum_t' w_t w_t' <f_t, f_t'> (Gram record: |f|^2, right, down, diag, anti)
+                float n2 = w00 * w00 * g00[0];
+                n2 = fmaf(w10 * w10, g10[0], n2);
+                n2 = fmaf(w01 * w01, g01[0], n2);
+                n2 = fmaf(w11 * w11, g11[0], n2);
+                float cross = w00 * w10 * g00[1];
+                cross = fmaf(w01 * w11, g01[1], cross);
+                cross = fmaf(w00 * w01, g00[2], cross);
+                cross = fmaf(w10 * w11, g10[2], cross);
+                cross = fmaf(w00 * w11, g00[3], cross);
+                cross = fmaf(w10 * w01, g00[4], cross);
+                n2 = fmaf(2.f, cross, n2);
+                out[o] = n2 > 1e-12f ? dot / sqrtf(n2) : 0.f;  // correlation.cpp:22
+            }
+        }
+    }
+}
+
+}  // namespace
+
+int corr_tma_smem_bytes() { return kSmemBytes; }
+
+cudaError_t launch_corr_tma(const CorrTmaParams& p, const CUtensorMap* maps, int num_sms, cudaStream_t stream) {
+    if (p.n_edges <= 0) return cudaSuccess;
+    cudaError_t err = cudaFuncSetAttribute(corr_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (err != cudaSuccess) return err;
+    int grid = num_sms;
+    if (grid > p.n_edges) grid = p.n_edges;
+    corr_tma_kernel<<<grid, kThreads, kSmemBytes, stream>>>(maps[0], maps[1], maps[2], maps[3], p);
+    return cudaGetLastError();
+}
+
+}  // namespace pvo_dev

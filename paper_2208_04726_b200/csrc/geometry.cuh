@@ -20,7 +20,11 @@
 
 #if defined(__CUDACC__)
 #define PVO_HD __host__ __device__ __forceinline__
+#if defined(__CUDA_ARCH__)
 #define PVO_UNROLL _Pragma("unroll")
+#else
+#define PVO_UNROLL
+#endif
 #else
 #define PVO_HD inline
 #define PVO_UNROLL

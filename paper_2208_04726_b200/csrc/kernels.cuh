@@ -1,6 +1,7 @@
 // kernels.cuh — parameter blocks and launchers of the sm_100a kernels.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -32,10 +33,42 @@ struct CorrParams {
     const float* patch_feats = nullptr;  // [P][2][9][C]
     float* out = nullptr;                // [E][2][9][49]
     int* status = nullptr;               // device status word (1 = non-finite coords)
+    // overflow mode: (edge << 1 | level) items, count on the device
+    const int* items = nullptr;
+    const int* items_count = nullptr;
 };
 
 int corr_smem_bytes(int channels);
 cudaError_t launch_corr(const CorrParams& p, cudaStream_t stream);
+cudaError_t launch_corr_items(const CorrParams& p, int num_sms, cudaStream_t stream);
+
+// K2 production path (corr_tma.cu): D = 128, TMA pipeline, persistent CTAs.
+struct CorrTmaParams {
+    int n_edges = 0;
+    const int* order = nullptr;     // edge processing order (target-frame sorted) or null
+    const int* e_patch = nullptr;
+    const int* e_pose = nullptr;
+    const int* e_slot = nullptr;    // explicit frame slot per edge, or null (pose_slot[e_pose])
+    const int* pose_slot = nullptr;
+    const double* coords_in = nullptr;  // explicit [E][9][2] or null (reproject the state)
+    const double* poses = nullptr;
+    const int* patch_src = nullptr;
+    const double* patch_x = nullptr;
+    const double* patch_y = nullptr;
+    const double* depth = nullptr;
+    const double* K = nullptr;
+    int w0 = 0, h0 = 0, w1 = 0, h1 = 0;
+    const float* patch_feats = nullptr;  // [P][2][9][128]
+    float* out = nullptr;
+    double* coords = nullptr;     // scratch [E][9][2]
+    int* meta = nullptr;          // scratch [E][2][4]
+    int* overflow = nullptr;      // scratch [2E]
+    int* overflow_count = nullptr;
+    int* status = nullptr;
+};
+int corr_tma_smem_bytes();
+// maps: feat0, feat1, gram0, gram1
+cudaError_t launch_corr_tma(const CorrTmaParams& p, const CUtensorMap* maps, int num_sms, cudaStream_t stream);
 cudaError_t launch_gram(const float* feat, float* gram, int W, int H, int D, int num_sms, cudaStream_t stream);
 
 // Device status word values (ba.cu / corr.cu) -> pvo_status on the host.
@@ -88,6 +121,7 @@ struct BAParams {
     double* residual_norms = nullptr; // [1 + iterations]
     int* n_norms = nullptr;
     int* status = nullptr;
+    int* status2 = nullptr;           // [2] per-attempt-parity status words (scratch)
 };
 
 // Returns cudaErrorNotSupported when the shape exceeds the kernel (np > 96
@@ -96,7 +130,8 @@ cudaError_t launch_ba(BAParams& p, int num_sms, cudaStream_t stream, int* grid_o
 int ba_max_free_poses();
 int ba_max_edges_per_patch();
 size_t ba_partials_doubles(int n_free_poses, int grid);
-int ba_grid_size(int n_patches, int n_free_poses, int num_sms);
+int ba_grid_size(int n_patches, int n_free_poses, int n_poses, int num_sms);
+int ba_max_poses();
 
 // Debug capture of the damped dense normal equations (sequential, tests only).
 cudaError_t launch_normal_equations_debug(const BAParams& p, double* h, double* b, cudaStream_t stream);
