@@ -86,7 +86,7 @@ def load(path: Path | str | None = None) -> C.CDLL:
     if not p.exists():
         raise ImportError(
             f"{p} is missing: build the sm_100a library first "
-            "(python -m paper_2208_04726_b200.build); there is no CPU fallback"
+            "(python paper_2208_04726_b200/build.py); there is no CPU fallback"
         )
     lib = C.CDLL(str(p))
     for name, (res, args) in SIGNATURES.items():

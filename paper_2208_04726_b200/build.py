@@ -1,6 +1,6 @@
 """Build the sm_100a shared library ``libpvo_b200.so`` in-tree.
 
-``python -m paper_2208_04726_b200.build`` (or ``__graft_entry__.build()``)
+``python paper_2208_04726_b200/build.py`` (or ``__graft_entry__.build()``)
 compiles every CUDA/C++ source under ``csrc/`` with nvcc for
 ``-gencode arch=compute_100a,code=sm_100a`` and links the C-ABI library next
 to this file, where the ctypes loader finds it.  nvcc cross-compiles, so this

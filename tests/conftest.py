@@ -13,14 +13,12 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) device")
     # Build the checker and the product library if a fresh checkout lacks them
     # (nvcc cross-compiles; no GPU needed).
-    from oracle import build as obuild
+    import __graft_entry__
 
-    obuild.build()
+    __graft_entry__._load_by_path("oracle_build", ROOT / "oracle" / "build.py").build()
     lib = ROOT / "paper_2208_04726_b200" / "libpvo_b200.so"
     if not lib.exists():
-        from paper_2208_04726_b200 import build as pbuild
-
-        pbuild.build()
+        __graft_entry__._load_by_path("pvo_build", ROOT / "paper_2208_04726_b200" / "build.py").build()
 
 
 @pytest.fixture(scope="session")
