@@ -174,30 +174,77 @@ __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, c
     int* perm = at<int>(smem, L.perm);
     __shared__ int s_fail, s_zero;
     // Eigen's transposition sequence depends only on the original diagonal:
-    // simulate it (first largest |d| among the remaining entries).
-    if (tid == 0) {
-        s_fail = 0;
-        s_zero = 0;
-        for (int i = 0; i < np; ++i) {
-            perm[i] = i;
-            // diagonal entry (i, i) of the upper-triangle row-major layout
-            od[i] = sys[i * np - i * (i - 1) / 2];
+    // simulate it (first largest |d| among the remaining entries) on warp 0,
+    // positions p = lane + 32 r held in registers (np <= 96).
+    if (tid < 32) {
+        const int lane = tid;
+        double v[3];
+        int id[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            const int i = lane + 32 * r;
+            id[r] = i;
+            v[r] = i < np ? fabs(sys[i * np - i * (i - 1) / 2]) : -1.0;  // diagonal (i, i) of the upper layout
+        }
+        if (lane == 0) {
+            s_fail = 0;
+            s_zero = 0;
         }
         for (int k = 0; k < np; ++k) {
-            int big = k;
-            double bv = fabs(od[k]);
-            for (int i = k + 1; i < np; ++i)
-                if (fabs(od[i]) > bv) {
-                    bv = fabs(od[i]);
-                    big = i;
+            // first maximum over positions >= k: compare (value desc, position asc)
+            double bv = -1.0;
+            int bp = 1 << 30;
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                const int p = lane + 32 * r;
+                if (p >= k && p < np && (v[r] > bv || (v[r] == bv && p < bp))) {
+                    bv = v[r];
+                    bp = p;
                 }
-            const double td = od[k];
-            od[k] = od[big];
-            od[big] = td;
-            const int tp = perm[k];
-            perm[k] = perm[big];
-            perm[big] = tp;
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+                const int op = __shfl_xor_sync(0xffffffffu, bp, off);
+                if (ov > bv || (ov == bv && op < bp)) {
+                    bv = ov;
+                    bp = op;
+                }
+            }
+            // swap positions k and bp
+            const int ownk = k & 31, rk = k >> 5, ownp = bp & 31, rp = bp >> 5;
+            double vk = 0, vp = 0;
+            int ik = 0, ip = 0;
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                if (r == rk) {
+                    vk = v[r];
+                    ik = id[r];
+                }
+                if (r == rp) {
+                    vp = v[r];
+                    ip = id[r];
+                }
+            }
+            vk = __shfl_sync(0xffffffffu, vk, ownk);
+            ik = __shfl_sync(0xffffffffu, ik, ownk);
+            vp = __shfl_sync(0xffffffffu, vp, ownp);
+            ip = __shfl_sync(0xffffffffu, ip, ownp);
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                if (lane == ownk && r == rk) {
+                    v[r] = vp;
+                    id[r] = ip;
+                }
+                if (lane == ownp && r == rp) {
+                    v[r] = vk;
+                    id[r] = ik;
+                }
+            }
         }
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+            if (lane + 32 * r < np) perm[lane + 32 * r] = id[r];
     }
     __syncthreads();
     // A = P S P^T (lower triangle), x = P rhs
@@ -235,10 +282,14 @@ __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, c
             }
         }
         __syncthreads();
-        const int m = np - k - 1;
-        for (int t = tid; t < m * m; t += kThreads) {
-            const int i = k + 1 + t / m, j = k + 1 + t % m;
-            if (j <= i) A[i * np + j] -= c[i] * l[j];
+        // lower-triangle trailing update: warp w takes rows i = k+1+w (mod 8),
+        // lanes stride the columns j in (k, i]
+        {
+            const int w = tid >> 5, lane = tid & 31;
+            for (int i = k + 1 + w; i < np; i += kWarps) {
+                const double ci = c[i];
+                for (int j = k + 1 + lane; j <= i; j += 32) A[i * np + j] -= ci * l[j];
+            }
         }
         for (int i = k + 1 + tid; i < np; i += kThreads) A[i * np + k] = valid ? l[i] : c[i];
         __syncthreads();

@@ -33,8 +33,10 @@ namespace pvo_dev {
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
+constexpr int kConsumerWarps = 8;              // two groups of 4 warps (ping-pong)
+constexpr int kGroupWarps = 4;
+constexpr int kGroupThreads = 32 * kGroupWarps;
+constexpr int kThreads = 32 * (kConsumerWarps + 1);  // + one producer warp
 constexpr int kD = 128;
 constexpr int kDP = 132;  // padded cell stride (floats)
 constexpr int kBox = 9;
@@ -48,11 +50,14 @@ constexpr int kGramRegion = (kGramBytes + 127) / 128 * 128;   // 2688
 constexpr int kGBytes = kPix * kD * 4;                        // 4608
 constexpr int kStageBytes = kTileRegion + kGramRegion + kGBytes;  // 50176
 constexpr int kTxBytes = kTileBytes + kGramBytes + kGBytes;
-// after the stages
-constexpr int kPartOff = kStages * kStageBytes;                    // [8][9][81] f32
-constexpr int kDotsOff = kPartOff + kWarps * kPix * kCells * 4;    // [9][81] f32
-constexpr int kGramSOff = kDotsOff + kPix * kCells * 4;            // [81][5] f32
-constexpr int kSmemBytes = kGramSOff + kCells * 5 * 4 + 1024;      // + alignment slack
+// per consumer group scratch (after the stages); dots / gram / pixel data are
+// double-buffered by the group's tile parity
+constexpr int kPartBytes = kGroupWarps * kPix * kCells * 4;   // [4][9][81] f32
+constexpr int kDotsBytes = kPix * kCells * 4;                  // [9][81] f32
+constexpr int kGramSBytes = kCells * 5 * 4;                    // [81][5] f32
+constexpr int kGroupBytes = kPartBytes + 2 * (kDotsBytes + kGramSBytes) + 2 * 640;
+constexpr int kScratchOff = kStages * kStageBytes;
+constexpr int kSmemBytes = kScratchOff + 2 * kGroupBytes + 1024;  // + alignment slack
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -66,6 +71,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void named_barrier(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
@@ -122,26 +130,34 @@ __device__ __forceinline__ int clamp_floor(double b, int extent) {
     return (int)floor(fmin(fmax(b, -16.0), (double)extent + 16.0));
 }
 
+
+// Per-pixel data of one tile: fractional bilinear weights per offset (exact
+// x - floor(x) in FP64, stored FP32) and the pixel's window origin in the
+// union tile.
+struct PixData {
+    float ax[kPix][7];
+    float ay[kPix][7];
+    int cx0[kPix];
+    int cy0[kPix];
+};
+static_assert(sizeof(PixData) <= 640, "PixData");
+
 __global__ void __launch_bounds__(kThreads, 1)
     corr_tma_kernel(const __grid_constant__ CUtensorMap feat0, const __grid_constant__ CUtensorMap feat1,
                     const __grid_constant__ CUtensorMap gram0, const __grid_constant__ CUtensorMap gram1,
                     CorrTmaParams a) {
     extern __shared__ unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* smem =
+        reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ __align__(8) uint64_t full[kStages];
-    __shared__ double s_bx[kPix], s_by[kPix];
-    __shared__ int s_fx[kPix], s_fy[kPix];
+    __shared__ __align__(8) uint64_t empty[kStages];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int G = gridDim.x, b = blockIdx.x;
     const int my_edges = a.n_edges > b ? (a.n_edges - 1 - b) / G + 1 : 0;
     const int n_tiles = 2 * my_edges;
 
-    float* s_part = reinterpret_cast<float*>(smem + kPartOff);
-    float* s_dots = reinterpret_cast<float*>(smem + kDotsOff);
-    float* s_gram = reinterpret_cast<float*>(smem + kGramSOff);
-
-    // ---- phase 0: coordinates and tile geometry of this CTA's edges ----
+    // ---- phase 0 (all warps): coordinates and tile geometry of this CTA's edges ----
     for (int i = tid; i < my_edges * kPix; i += kThreads) {
         const int e = a.order ? a.order[b + (i / kPix) * G] : b + (i / kPix) * G;
         const int pix = i % kPix;
@@ -179,43 +195,63 @@ __global__ void __launch_bounds__(kThreads, 1)
         reinterpret_cast<int4*>(a.meta)[2 * e + level] = make_int4(m.x0, m.y0, m.tw, m.th);
     }
     if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kGroupWarps);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
     auto tile_edge = [&](int t) { return a.order ? a.order[b + (t >> 1) * G] : b + (t >> 1) * G; };
-    auto issue = [&](int t) {
-        const int s = t % kStages;
-        const int e = tile_edge(t), level = t & 1;
-        const int4 m = reinterpret_cast<const int4*>(a.meta)[2 * e + level];
-        if (m.z <= 0) {  // not on this path: complete the phase without data
-            mbar_arrive(&full[s]);
-            return;
+
+    if (warp == kConsumerWarps) {
+        // ================= producer warp =================
+        if (lane == 0) {
+            for (int t = 0; t < n_tiles; ++t) {
+                const int s = t % kStages;
+                if (t >= kStages) mbar_wait(&empty[s], (uint32_t)(((t / kStages) - 1) & 1));
+                const int e = tile_edge(t), level = t & 1;
+                const int4 m = reinterpret_cast<const int4*>(a.meta)[2 * e + level];
+                if (m.z <= 0) {  // not on this path: complete the phase without data
+                    mbar_arrive(&full[s]);
+                    continue;
+                }
+                unsigned char* st = smem + s * kStageBytes;
+                const int slot = a.e_slot ? a.e_slot[e] : a.pose_slot[a.e_pose[e]];
+                mbar_expect_tx(&full[s], kTxBytes);
+                tma_load_4d(st, level ? &feat1 : &feat0, 0, m.x, m.y, slot, &full[s]);
+                tma_load_4d(st + kTileRegion, level ? &gram1 : &gram0, 0, m.x, m.y, slot, &full[s]);
+                const float* g = a.patch_feats + ((size_t)a.e_patch[e] * 2 + level) * kPix * kD;
+                bulk_load(st + kTileRegion + kGramRegion, g, kGBytes, &full[s]);
+            }
         }
-        unsigned char* st = smem + s * kStageBytes;
-        const int slot = a.e_slot ? a.e_slot[e] : a.pose_slot[a.e_pose[e]];
-        mbar_expect_tx(&full[s], kTxBytes);
-        tma_load_4d(st, level ? &feat1 : &feat0, 0, m.x, m.y, slot, &full[s]);
-        tma_load_4d(st + kTileRegion, level ? &gram1 : &gram0, 0, m.x, m.y, slot, &full[s]);
-        const float* g = a.patch_feats + ((size_t)a.e_patch[e] * 2 + level) * kPix * kD;
-        bulk_load(st + kTileRegion + kGramRegion, g, kGBytes, &full[s]);
-    };
-    if (tid == 0) {
-        for (int t = 0; t < kStages && t < n_tiles; ++t) issue(t);
+        return;
     }
 
-    for (int t = 0; t < n_tiles; ++t) {
+    // ================= consumer groups =================
+    const int grp = warp / kGroupWarps;           // 0 or 1
+    const int gw = warp - grp * kGroupWarps;       // warp within the group
+    const int gtid = tid - grp * kGroupThreads;    // thread within the group
+    unsigned char* gscr = smem + kScratchOff + grp * kGroupBytes;
+    float* s_part = reinterpret_cast<float*>(gscr);
+    const int bar_id = 1 + grp;
+
+    int parity = 0;  // this group's tile parity (double buffers)
+    for (int t = grp; t < n_tiles; t += 2, parity ^= 1) {
         const int s = t % kStages;
         const int e = tile_edge(t), level = t & 1;
         const int4 m = reinterpret_cast<const int4*>(a.meta)[2 * e + level];
+        float* s_dots = reinterpret_cast<float*>(gscr + kPartBytes + parity * (kDotsBytes + kGramSBytes));
+        float* s_gram = s_dots + kPix * kCells;
+        PixData* pd = reinterpret_cast<PixData*>(gscr + kPartBytes + 2 * (kDotsBytes + kGramSBytes) + parity * 640);
         mbar_wait(&full[s], (uint32_t)((t / kStages) & 1));
         const unsigned char* st = smem + s * kStageBytes;
         const bool active = m.z > 0;
         const int TW = m.z, TH = m.w, NC = active ? TW * TH : 0;
 
-        // ---- dot products: lane owns up to 3 union cells x 9 pixels; warp owns 4 chunks ----
         if (active) {
+            // ---- dot products: lane owns up to 3 union cells x 9 pixels; warp owns 8 chunks ----
             const float* tile = reinterpret_cast<const float*>(st);
             const float* g = reinterpret_cast<const float*>(st + kTileRegion + kGramRegion);
             int off[3];
@@ -230,9 +266,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int ci = 0; ci < 3; ++ci)
 #pragma unroll
                 for (int p = 0; p < kPix; ++p) acc[ci][p] = 0.f;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int ch = warp + kWarps * j;
+#pragma unroll 2
+            for (int j = 0; j < 8; ++j) {
+                const int ch = gw + kGroupWarps * j;
                 float4 gv[kPix];
 #pragma unroll
                 for (int p = 0; p < kPix; ++p) gv[p] = *reinterpret_cast<const float4*>(g + p * kD + 4 * ch);
@@ -257,48 +293,54 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int c = lane + 32 * ci;
                 if (c < NC) {
 #pragma unroll
-                    for (int p = 0; p < kPix; ++p) s_part[(warp * kPix + p) * kCells + c] = acc[ci][p];
+                    for (int p = 0; p < kPix; ++p) s_part[(gw * kPix + p) * kCells + c] = acc[ci][p];
                 }
             }
-        }
-        __syncthreads();  // (A) partials complete; stage s no longer read below except gram
-        if (active) {
-            for (int i = tid; i < kPix * NC; i += kThreads) {
-                const int p = i / NC, c = i - p * NC;
-                float sum = 0.f;
-#pragma unroll
-                for (int w = 0; w < kWarps; ++w) sum += s_part[(w * kPix + p) * kCells + c];
-                s_dots[p * kCells + c] = sum;
-            }
+            // Gram records of the union cells (this group's copy)
             const float* gr = reinterpret_cast<const float*>(st + kTileRegion);
-            for (int i = tid; i < NC * 5; i += kThreads) {
+            for (int i = gtid; i < NC * 5; i += kGroupThreads) {
                 const int c = i / 5, r = i - 5 * c;
                 const int cy = c / TW, cx = c - cy * TW;
                 s_gram[i] = gr[(cy * kBox + cx) * 8 + r];
             }
-            if (tid < kPix) {
+            // per-pixel bilinear data (features.cpp:10-13 arithmetic)
+            if (gtid < kPix) {
+                const int p = gtid;
                 const double scale = level ? 16.0 : 4.0;
                 const int W = level ? a.w1 : a.w0, H = level ? a.h1 : a.h0;
-                const double bx = a.coords[(size_t)e * 18 + 2 * tid] / scale;
-                const double by = a.coords[(size_t)e * 18 + 2 * tid + 1] / scale;
-                s_bx[tid] = bx;
-                s_by[tid] = by;
-                s_fx[tid] = clamp_floor(bx, W);
-                s_fy[tid] = clamp_floor(by, H);
+                const double bx = a.coords[(size_t)e * 18 + 2 * p] / scale;
+                const double by = a.coords[(size_t)e * 18 + 2 * p + 1] / scale;
+                const int fx = clamp_floor(bx, W), fy = clamp_floor(by, H);
+#pragma unroll
+                for (int o = 0; o < 7; ++o) {
+                    pd->ax[p][o] = (float)((bx + (double)(o - 3)) - (double)(fx + o - 3));
+                    pd->ay[p][o] = (float)((by + (double)(o - 3)) - (double)(fy + o - 3));
+                }
+                pd->cx0[p] = fx - 3 - m.x;
+                pd->cy0[p] = fy - 3 - m.y;
             }
         }
-        __syncthreads();  // (B) stage s free: refill it
-        if (tid == 0 && t + kStages < n_tiles) issue(t + kStages);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
+        named_barrier(bar_id, kGroupThreads);   // partials, gram copy and pixel data complete
+        if (active) {
+            for (int i = gtid; i < kPix * NC; i += kGroupThreads) {
+                const int p = i / NC, c = i - p * NC;
+                float sum = s_part[(0 * kPix + p) * kCells + c];
+                sum += s_part[(1 * kPix + p) * kCells + c];
+                sum += s_part[(2 * kPix + p) * kCells + c];
+                sum += s_part[(3 * kPix + p) * kCells + c];
+                s_dots[p * kCells + c] = sum;
+            }
+        }
+        named_barrier(bar_id, kGroupThreads);  // dots complete; s_part free for the next tile
         if (active) {
             float* out = a.out + ((size_t)e * 2 + level) * kPix * 49;
-            for (int o = tid; o < kPix * 49; o += kThreads) {
+            for (int o = gtid; o < kPix * 49; o += kGroupThreads) {
                 const int p = o / 49, ab = o - 49 * p;
                 const int alpha = ab / 7, beta = ab - 7 * alpha;
-                // x = base + (beta - 3) and its floor exactly as features.cpp:10-13
-                const int x0 = s_fx[p] + beta - 3, y0 = s_fy[p] + alpha - 3;
-                const float ax = (float)((s_bx[p] + (double)(beta - 3)) - (double)x0);
-                const float ay = (float)((s_by[p] + (double)(alpha - 3)) - (double)y0);
-                const int c00 = (y0 - m.y) * TW + (x0 - m.x);
+                const float ax = pd->ax[p][beta], ay = pd->ay[p][alpha];
+                const int c00 = (pd->cy0[p] + alpha) * TW + (pd->cx0[p] + beta);
                 const float* d = s_dots + p * kCells;
                 const float w00 = (1.f - ax) * (1.f - ay), w10 = ax * (1.f - ay);
                 const float w01 = (1.f - ax) * ay, w11 = ax * ay;
