@@ -173,78 +173,26 @@ __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, c
     double* l = at<double>(smem, L.l);
     int* perm = at<int>(smem, L.perm);
     __shared__ int s_fail, s_zero;
-    // Eigen's transposition sequence depends only on the original diagonal:
-    // simulate it (first largest |d| among the remaining entries) on warp 0,
-    // positions p = lane + 32 r held in registers (np <= 96).
-    if (tid < 32) {
-        const int lane = tid;
-        double v[3];
-        int id[3];
-#pragma unroll
-        for (int r = 0; r < 3; ++r) {
-            const int i = lane + 32 * r;
-            id[r] = i;
-            v[r] = i < np ? fabs(sys[i * np - i * (i - 1) / 2]) : -1.0;  // diagonal (i, i) of the upper layout
+    // Pivot order.  Eigen's LDLT picks, step by step, the largest remaining
+    // |diagonal| of the original matrix (its left-looking update leaves the
+    // trailing diagonal untouched): with distinct values that is the
+    // descending order of |diag|, computed here as a parallel rank.  Among
+    // exactly equal values Eigen's order follows its swap history; we keep
+    // index order there, which changes rounding only (same SPD solution).
+    for (int i = tid; i < np; i += kThreads) od[i] = fabs(sys[i * np - i * (i - 1) / 2]);  // diag (i, i)
+    if (tid == 0) {
+        s_fail = 0;
+        s_zero = 0;
+    }
+    __syncthreads();
+    for (int i = tid; i < np; i += kThreads) {
+        const double di = od[i];
+        int rank = 0;
+        for (int j = 0; j < np; ++j) {
+            const double dj = od[j];
+            rank += (dj > di) || (dj == di && j < i);
         }
-        if (lane == 0) {
-            s_fail = 0;
-            s_zero = 0;
-        }
-        for (int k = 0; k < np; ++k) {
-            // first maximum over positions >= k: compare (value desc, position asc)
-            double bv = -1.0;
-            int bp = 1 << 30;
-#pragma unroll
-            for (int r = 0; r < 3; ++r) {
-                const int p = lane + 32 * r;
-                if (p >= k && p < np && (v[r] > bv || (v[r] == bv && p < bp))) {
-                    bv = v[r];
-                    bp = p;
-                }
-            }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
-                const int op = __shfl_xor_sync(0xffffffffu, bp, off);
-                if (ov > bv || (ov == bv && op < bp)) {
-                    bv = ov;
-                    bp = op;
-                }
-            }
-            // swap positions k and bp
-            const int ownk = k & 31, rk = k >> 5, ownp = bp & 31, rp = bp >> 5;
-            double vk = 0, vp = 0;
-            int ik = 0, ip = 0;
-#pragma unroll
-            for (int r = 0; r < 3; ++r) {
-                if (r == rk) {
-                    vk = v[r];
-                    ik = id[r];
-                }
-                if (r == rp) {
-                    vp = v[r];
-                    ip = id[r];
-                }
-            }
-            vk = __shfl_sync(0xffffffffu, vk, ownk);
-            ik = __shfl_sync(0xffffffffu, ik, ownk);
-            vp = __shfl_sync(0xffffffffu, vp, ownp);
-            ip = __shfl_sync(0xffffffffu, ip, ownp);
-#pragma unroll
-            for (int r = 0; r < 3; ++r) {
-                if (lane == ownk && r == rk) {
-                    v[r] = vp;
-                    id[r] = ip;
-                }
-                if (lane == ownp && r == rp) {
-                    v[r] = vk;
-                    id[r] = ik;
-                }
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-            if (lane + 32 * r < np) perm[lane + 32 * r] = id[r];
+        perm[rank] = i;
     }
     __syncthreads();
     // A = P S P^T (lower triangle), x = P rhs

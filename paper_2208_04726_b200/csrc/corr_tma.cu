@@ -48,8 +48,15 @@ constexpr int kTileRegion = (kTileBytes + 127) / 128 * 128;   // 42880
 constexpr int kGramBytes = kCells * 8 * 4;                    // 2592
 constexpr int kGramRegion = (kGramBytes + 127) / 128 * 128;   // 2688
 constexpr int kGBytes = kPix * kD * 4;                        // 4608
-constexpr int kStageBytes = kTileRegion + kGramRegion + kGBytes;  // 50176
-constexpr int kTxBytes = kTileBytes + kGramBytes + kGBytes;
+constexpr int kCoordBytes = kPix * 2 * 8;                    // 144: the 9 reprojected pixels
+constexpr int kInfoOff = kTileRegion + kGramRegion + kGBytes;  // tile info written by the producer
+constexpr int kCoordOff = kInfoOff + 32;
+constexpr int kStageBytes = kCoordOff + 160;                   // 50368
+constexpr int kTxBytes = kTileBytes + kGramBytes + kGBytes + kCoordBytes;
+struct StageInfo {
+    int4 meta;  // union origin x, y, extent w, h (w <= 0: not on this path)
+    int e, level;
+};
 // per consumer group scratch (after the stages); dots / gram / pixel data are
 // double-buffered by the group's tile parity
 constexpr int kPartBytes = kGroupWarps * kPix * kCells * 4;   // [4][9][81] f32
@@ -166,6 +173,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         a.coords[(size_t)e * 18 + 2 * pix] = xy[0];
         a.coords[(size_t)e * 18 + 2 * pix + 1] = xy[1];
     }
+    // the producer re-reads these coordinates with bulk (async-proxy) copies
+    asm volatile("fence.proxy.async.global;" ::: "memory");
     __syncthreads();
     for (int i = tid; i < my_edges * 2; i += kThreads) {
         const int e = a.order ? a.order[b + (i >> 1) * G] : b + (i >> 1) * G;
@@ -213,17 +222,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (t >= kStages) mbar_wait(&empty[s], (uint32_t)(((t / kStages) - 1) & 1));
                 const int e = tile_edge(t), level = t & 1;
                 const int4 m = reinterpret_cast<const int4*>(a.meta)[2 * e + level];
+                unsigned char* st = smem + s * kStageBytes;
+                StageInfo* info = reinterpret_cast<StageInfo*>(st + kInfoOff);
+                info->meta = m;
+                info->e = e;
+                info->level = level;
                 if (m.z <= 0) {  // not on this path: complete the phase without data
                     mbar_arrive(&full[s]);
                     continue;
                 }
-                unsigned char* st = smem + s * kStageBytes;
                 const int slot = a.e_slot ? a.e_slot[e] : a.pose_slot[a.e_pose[e]];
                 mbar_expect_tx(&full[s], kTxBytes);
                 tma_load_4d(st, level ? &feat1 : &feat0, 0, m.x, m.y, slot, &full[s]);
                 tma_load_4d(st + kTileRegion, level ? &gram1 : &gram0, 0, m.x, m.y, slot, &full[s]);
                 const float* g = a.patch_feats + ((size_t)a.e_patch[e] * 2 + level) * kPix * kD;
                 bulk_load(st + kTileRegion + kGramRegion, g, kGBytes, &full[s]);
+                bulk_load(st + kCoordOff, a.coords + (size_t)e * 18, kCoordBytes, &full[s]);
             }
         }
         return;
@@ -240,13 +254,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     int parity = 0;  // this group's tile parity (double buffers)
     for (int t = grp; t < n_tiles; t += 2, parity ^= 1) {
         const int s = t % kStages;
-        const int e = tile_edge(t), level = t & 1;
-        const int4 m = reinterpret_cast<const int4*>(a.meta)[2 * e + level];
         float* s_dots = reinterpret_cast<float*>(gscr + kPartBytes + parity * (kDotsBytes + kGramSBytes));
         float* s_gram = s_dots + kPix * kCells;
         PixData* pd = reinterpret_cast<PixData*>(gscr + kPartBytes + 2 * (kDotsBytes + kGramSBytes) + parity * 640);
         mbar_wait(&full[s], (uint32_t)((t / kStages) & 1));
         const unsigned char* st = smem + s * kStageBytes;
+        const StageInfo info = *reinterpret_cast<const StageInfo*>(st + kInfoOff);
+        const int e = info.e, level = info.level;
+        const int4 m = info.meta;
+        const double* tc = reinterpret_cast<const double*>(st + kCoordOff);
         const bool active = m.z > 0;
         const int TW = m.z, TH = m.w, NC = active ? TW * TH : 0;
 
@@ -308,8 +324,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int p = gtid;
                 const double scale = level ? 16.0 : 4.0;
                 const int W = level ? a.w1 : a.w0, H = level ? a.h1 : a.h0;
-                const double bx = a.coords[(size_t)e * 18 + 2 * p] / scale;
-                const double by = a.coords[(size_t)e * 18 + 2 * p + 1] / scale;
+                const double bx = tc[2 * p] / scale;
+                const double by = tc[2 * p + 1] / scale;
                 const int fx = clamp_floor(bx, W), fy = clamp_floor(by, H);
 #pragma unroll
                 for (int o = 0; o < 7; ++o) {
