@@ -51,7 +51,7 @@ constexpr int kGBytes = kPix * kD * 4;                        // 4608
 constexpr int kCoordBytes = kPix * 2 * 8;                    // 144: the 9 reprojected pixels
 constexpr int kInfoOff = kTileRegion + kGramRegion + kGBytes;  // tile info written by the producer
 constexpr int kCoordOff = kInfoOff + 32;
-constexpr int kStageBytes = kCoordOff + 160;                   // 50368
+constexpr int kStageBytes = (kCoordOff + 160 + 1023) / 1024 * 1024;  // 51200: TMA dst needs 128 B alignment
 constexpr int kTxBytes = kTileBytes + kGramBytes + kGBytes + kCoordBytes;
 struct StageInfo {
     int4 meta;  // union origin x, y, extent w, h (w <= 0: not on this path)
