@@ -92,7 +92,7 @@ __host__ __device__ inline Layout make_layout(int np_full, int n_poses) {
     L.delta = off;
     off += align16(8 * (np_full > 0 ? np_full : 1));
     L.flags = off;
-    off += 16;
+    off += 32;
     L.uni = off;
     int a = off;
     L.S = a;
@@ -195,53 +195,71 @@ __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, c
         perm[rank] = i;
     }
     __syncthreads();
-    // A = P S P^T (lower triangle), x = P rhs
-    for (int t = tid; t < np * np; t += kThreads) {
-        const int i = t / np, j = t - i * np;
-        if (j > i) continue;
-        int a = perm[i], b = perm[j];
-        if (a > b) {
-            const int s = a;
-            a = b;
-            b = s;
+    // A = P S P^T: every thread owns fixed lower-triangle entries (i, j) of the
+    // permuted matrix in registers (row-major index q = i(i+1)/2 + j, q = tid + 256 r)
+    constexpr int kOwn = (kMaxNp * (kMaxNp + 1) / 2 + kThreads - 1) / kThreads;  // 19
+    const int nlow = nent_of(np);
+    double av[kOwn];
+    int ai[kOwn], aj[kOwn];
+#pragma unroll
+    for (int r = 0; r < kOwn; ++r) {
+        const int q = tid + kThreads * r;
+        int i = (int)((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
+        while ((i + 1) * (i + 2) / 2 <= q) ++i;
+        while (i * (i + 1) / 2 > q) --i;
+        const int j = q - i * (i + 1) / 2;
+        ai[r] = q < nlow ? i : -1;
+        aj[r] = j;
+        av[r] = 0.0;
+        if (q < nlow) {
+            int a = perm[i], b = perm[j];
+            if (a > b) {
+                const int s = a;
+                a = b;
+                b = s;
+            }
+            av[r] = sys[a * np - a * (a - 1) / 2 + (b - a)];
         }
-        A[i * np + j] = sys[a * np - a * (a - 1) / 2 + (b - a)];
     }
     const int nent = nent_of(np);
     for (int i = tid; i < np; i += kThreads) x[i] = sys[nent + perm[i]];
-    __syncthreads();
-    // right-looking LDL^T
+    // right-looking LDL^T, one barrier per step: column k is published into a
+    // double-buffered vector, every owner updates its entries in registers
+    bool fail = false;
     for (int k = 0; k < np; ++k) {
-        const double dk = A[k * np + k];
+        double* cb = (k & 1) ? l : c;
+#pragma unroll
+        for (int r = 0; r < kOwn; ++r)
+            if (aj[r] == k && ai[r] >= k) cb[ai[r]] = av[r];
+        __syncthreads();
+        const double dk = cb[k];
         const bool valid = fabs(dk) > 0.0;
         if (k == 0 && !valid) {
             // Eigen: all-zero diagonal -> D = 0, identity transpositions
             if (tid == 0) s_zero = 1;
             break;
         }
-        for (int i = k + 1 + tid; i < np; i += kThreads) {
-            const double ci = A[i * np + k];
-            c[i] = ci;
-            if (valid) {
-                l[i] = ci / dk;
-            } else {
-                l[i] = 0.0;
-                if (ci != 0.0) s_fail = 1;
+        const double inv = valid ? 1.0 / dk : 0.0;
+#pragma unroll
+        for (int r = 0; r < kOwn; ++r) {
+            const int i = ai[r], j = aj[r];
+            if (i < 0) continue;
+            if (j > k) {
+                av[r] -= cb[i] * (cb[j] * inv);
+            } else if (j == k && i > k) {
+                if (valid) {
+                    av[r] *= inv;  // L column k
+                } else if (av[r] != 0.0) {
+                    fail = true;  // zero pivot with a non-zero column (LDLT::info())
+                }
             }
         }
-        __syncthreads();
-        // lower-triangle trailing update: warp w takes rows i = k+1+w (mod 8),
-        // lanes stride the columns j in (k, i]
-        {
-            const int w = tid >> 5, lane = tid & 31;
-            for (int i = k + 1 + w; i < np; i += kWarps) {
-                const double ci = c[i];
-                for (int j = k + 1 + lane; j <= i; j += 32) A[i * np + j] -= ci * l[j];
-            }
-        }
-        for (int i = k + 1 + tid; i < np; i += kThreads) A[i * np + k] = valid ? l[i] : c[i];
-        __syncthreads();
     }
+    if (fail) s_fail = 1;
+    // publish L (strict lower) and D (diagonal)
+#pragma unroll
+    for (int r = 0; r < kOwn; ++r)
+        if (ai[r] >= 0) A[ai[r] * np + aj[r]] = av[r];
     __syncthreads();
     if (s_fail) return false;
     if (s_zero) {
@@ -250,23 +268,46 @@ __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, c
         return true;
     }
     if (tid < 32) {
+        // substitutions on one warp, x in registers (x[lane + 32 r])
         const int lane = tid;
-        for (int j = 0; j < np; ++j) {
-            const double xj = x[j];
-            for (int i = j + 1 + lane; i < np; i += 32) x[i] -= A[i * np + j] * xj;
-            __syncwarp();
+        double xr[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) xr[r] = lane + 32 * r < np ? x[lane + 32 * r] : 0.0;
+        for (int j = 0; j < np; ++j) {  // L y = P b
+            double xj = 0.0;
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+                if ((j >> 5) == r) xj = xr[r];
+            xj = __shfl_sync(0xffffffffu, xj, j & 31);
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                const int i = lane + 32 * r;
+                if (i > j && i < np) xr[r] -= A[i * np + j] * xj;
+            }
         }
-        for (int i = lane; i < np; i += 32) {
-            const double dd = A[i * np + i];
-            x[i] = fabs(dd) > DBL_MIN ? x[i] / dd : 0.0;  // pseudo-inverse of D (LDLT::_solve_impl)
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {  // pseudo-inverse of D (LDLT::_solve_impl)
+            const int i = lane + 32 * r;
+            if (i < np) {
+                const double dd = A[i * np + i];
+                xr[r] = fabs(dd) > DBL_MIN ? xr[r] / dd : 0.0;
+            }
         }
-        __syncwarp();
-        for (int j = np - 1; j >= 0; --j) {
-            const double xj = x[j];
-            for (int i = lane; i < j; i += 32) x[i] -= A[j * np + i] * xj;
-            __syncwarp();
+        for (int j = np - 1; j >= 0; --j) {  // L^T x = z
+            double xj = 0.0;
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+                if ((j >> 5) == r) xj = xr[r];
+            xj = __shfl_sync(0xffffffffu, xj, j & 31);
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                const int i = lane + 32 * r;
+                if (i < j) xr[r] -= A[j * np + i] * xj;
+            }
         }
-        for (int i = lane; i < np; i += 32) x_out[perm[i]] = x[i];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+            if (lane + 32 * r < np) x_out[perm[lane + 32 * r]] = xr[r];
     }
     __syncthreads();
     return true;
@@ -640,6 +681,7 @@ __global__ void __launch_bounds__(kThreads, 1) ba_kernel(BAParams a) {
                 const unsigned* abt = at<unsigned>(smem, L.ab);
                 for (int ent = b * kThreads + tid; ent < nent + np; ent += G * kThreads) {
                     double acc = 0.0;
+#pragma unroll 8
                     for (int c = 0; c < G; ++c) acc += partials[(size_t)c * pstride + ent];
                     if (ent < nent) {
                         const unsigned ab = abt[ent];
@@ -680,14 +722,23 @@ __global__ void __launch_bounds__(kThreads, 1) ba_kernel(BAParams a) {
                 if (b == 0 && tid == 0) atomicOr(a.status, st);
                 return;
             }
-            double sb = 0, wb = 0, sa = 0, wa = 0;
-            for (int c = 0; c < G; ++c) {
-                const double* pt = partials + (size_t)c * pstride + nent + np;
-                sb += pt[0];
-                wb += pt[1];
-                sa += pt[2];
-                wa += pt[3];
+            // residual sums over the CTA partials: warp 0, fixed lane order + shuffle tree
+            double* s_res = at<double>(smem, L.flags);
+            if (tid < 32) {
+                double q[4] = {0, 0, 0, 0};
+                for (int c = tid; c < G; c += 32) {
+                    const double* pt = partials + (size_t)c * pstride + nent + np;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) q[u] += pt[u];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) q[u] = warp_sum(q[u]);
+                if (tid == 0)
+                    for (int u = 0; u < 4; ++u) s_res[u] = q[u];
             }
+            __syncthreads();
+            const double sb = s_res[0], wb = s_res[1], sa = s_res[2], wa = s_res[3];
+            __syncthreads();
             const double before = wb > 0 ? sqrt(sb / wb) : 0.0;
             const double after = wa > 0 ? sqrt(sa / wa) : 0.0;
             const double thr = 1.5 * before + 1e-9;

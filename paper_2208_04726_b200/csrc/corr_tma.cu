@@ -282,27 +282,35 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int ci = 0; ci < 3; ++ci)
 #pragma unroll
                 for (int p = 0; p < kPix; ++p) acc[ci][p] = 0.f;
+            // cells past NC read cell 0 (valid memory); their sums are never stored
+            int roff[3];
+#pragma unroll
+            for (int ci = 0; ci < 3; ++ci) roff[ci] = off[ci] >= 0 ? off[ci] : 0;
 #pragma unroll 2
             for (int j = 0; j < 8; ++j) {
                 const int ch = gw + kGroupWarps * j;
-                float4 gv[kPix];
+                float4 gv[kPix], v[3];
 #pragma unroll
                 for (int p = 0; p < kPix; ++p) gv[p] = *reinterpret_cast<const float4*>(g + p * kD + 4 * ch);
 #pragma unroll
-                for (int ci = 0; ci < 3; ++ci) {
-                    if (off[ci] >= 0) {
-                        const float4 v = *reinterpret_cast<const float4*>(tile + off[ci] + 4 * ch);
+                for (int ci = 0; ci < 3; ++ci) v[ci] = *reinterpret_cast<const float4*>(tile + roff[ci] + 4 * ch);
+                // component-major: 27 independent FMAs between dependent ones
 #pragma unroll
-                        for (int p = 0; p < kPix; ++p) {
-                            float x = acc[ci][p];
-                            x = fmaf(v.x, gv[p].x, x);
-                            x = fmaf(v.y, gv[p].y, x);
-                            x = fmaf(v.z, gv[p].z, x);
-                            x = fmaf(v.w, gv[p].w, x);
-                            acc[ci][p] = x;
-                        }
-                    }
-                }
+                for (int ci = 0; ci < 3; ++ci)
+#pragma unroll
+                    for (int p = 0; p < kPix; ++p) acc[ci][p] = fmaf(v[ci].x, gv[p].x, acc[ci][p]);
+#pragma unroll
+                for (int ci = 0; ci < 3; ++ci)
+#pragma unroll
+                    for (int p = 0; p < kPix; ++p) acc[ci][p] = fmaf(v[ci].y, gv[p].y, acc[ci][p]);
+#pragma unroll
+                for (int ci = 0; ci < 3; ++ci)
+#pragma unroll
+                    for (int p = 0; p < kPix; ++p) acc[ci][p] = fmaf(v[ci].z, gv[p].z, acc[ci][p]);
+#pragma unroll
+                for (int ci = 0; ci < 3; ++ci)
+#pragma unroll
+                    for (int p = 0; p < kPix; ++p) acc[ci][p] = fmaf(v[ci].w, gv[p].w, acc[ci][p]);
             }
 #pragma unroll
             for (int ci = 0; ci < 3; ++ci) {
