@@ -60,6 +60,8 @@ int pvo_ctx_set_stream(pvo_ctx* ctx, void* cuda_stream);
 int pvo_ctx_synchronize(pvo_ctx* ctx);
 /* Number of kernels this context has launched (profiling / gpu_launches). */
 int64_t pvo_ctx_kernel_launches(pvo_ctx* ctx);
+/* Gauss-Newton attempts of the last BA run (divergence-guard retries included). */
+int pvo_ctx_ba_attempts(pvo_ctx* ctx, int* attempts);
 /* Device-side timing of the last pvo_window_iteration: corr ms, BA ms. */
 int pvo_ctx_last_timing(pvo_ctx* ctx, double* corr_ms, double* ba_ms);
 

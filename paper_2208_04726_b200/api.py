@@ -114,6 +114,12 @@ class Context:
     def kernel_launches(self) -> int:
         return int(lib.pvo_ctx_kernel_launches(self.handle))
 
+    @property
+    def ba_attempts(self) -> int:
+        n = C.c_int()
+        check(lib.pvo_ctx_ba_attempts(self.handle, C.addressof(n)))
+        return n.value
+
     def last_timing(self) -> tuple[float, float]:
         a, b = C.c_double(), C.c_double()
         check(lib.pvo_ctx_last_timing(self.handle, C.addressof(a), C.addressof(b)))

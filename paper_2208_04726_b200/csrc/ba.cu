@@ -164,7 +164,8 @@ __device__ inline void reproject_center(const SE3& pi, const SE3& pj, const Cam&
 // shared or global memory.  Returns false (all threads) on a factorization
 // failure (zero pivot with a non-zero column below, LDLT::info()).
 // ---------------------------------------------------------------------------
-__device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, const Layout& L, double* x_out) {
+template <int kOwn>  // lower-triangle entries owned per thread: ceil(np(np+1)/2 / 256)
+__device__ bool ldlt_solve_cta_t(const double* sys, int np, unsigned char* smem, const Layout& L, double* x_out) {
     const int tid = threadIdx.x;
     double* A = at<double>(smem, L.A);
     double* x = at<double>(smem, L.x);
@@ -197,7 +198,6 @@ __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, c
     __syncthreads();
     // A = P S P^T: every thread owns fixed lower-triangle entries (i, j) of the
     // permuted matrix in registers (row-major index q = i(i+1)/2 + j, q = tid + 256 r)
-    constexpr int kOwn = (kMaxNp * (kMaxNp + 1) / 2 + kThreads - 1) / kThreads;  // 19
     const int nlow = nent_of(np);
     double av[kOwn];
     int ai[kOwn], aj[kOwn];
@@ -311,6 +311,16 @@ __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, c
     }
     __syncthreads();
     return true;
+}
+
+__device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, const Layout& L, double* x_out) {
+    const int nlow = nent_of(np);
+    if (nlow <= 1 * kThreads) return ldlt_solve_cta_t<1>(sys, np, smem, L, x_out);
+    if (nlow <= 2 * kThreads) return ldlt_solve_cta_t<2>(sys, np, smem, L, x_out);
+    if (nlow <= 4 * kThreads) return ldlt_solve_cta_t<4>(sys, np, smem, L, x_out);
+    if (nlow <= 8 * kThreads) return ldlt_solve_cta_t<8>(sys, np, smem, L, x_out);
+    if (nlow <= 12 * kThreads) return ldlt_solve_cta_t<12>(sys, np, smem, L, x_out);
+    return ldlt_solve_cta_t<(kMaxNp * (kMaxNp + 1) / 2 + kThreads - 1) / kThreads>(sys, np, smem, L, x_out);
 }
 
 // ---------------------------------------------------------------------------
@@ -743,6 +753,7 @@ __global__ void __launch_bounds__(kThreads, 1) ba_kernel(BAParams a) {
             const double after = wa > 0 ? sqrt(sa / wa) : 0.0;
             const double thr = 1.5 * before + 1e-9;
             ++attempt_no;
+            if (b == 0 && tid == 0 && a.attempts) *a.attempts = attempt_no;
             bool accept, reject = false;
             if (structure || a.gn_step_mode) {
                 accept = true;

@@ -31,12 +31,13 @@ void set_last_error(const std::string& msg) { g_last_error = msg; }
 struct BABuffers {
     DevBuf poses, free_slot, patch_src, px, py, depth, depth_slot, edge_begin, e_patch, e_pose, e_in, e_w, e_target,
         e_weight, cand_poses, cand_depth, patch_v, patch_h, patch_bd, partials, system, delta, norms, n_norms, dbg_h,
-        dbg_b, K, status2;
+        dbg_b, K, status2, attempts;
     void release() {
         DevBuf* all[] = {&poses,    &free_slot,  &patch_src, &px,        &py,       &depth,    &depth_slot,
                          &edge_begin, &e_patch,  &e_pose,    &e_in,      &e_w,      &e_target, &e_weight,
                          &cand_poses, &cand_depth, &patch_v, &patch_h,   &patch_bd, &partials, &system,
-                         &delta,    &norms,      &n_norms,   &dbg_h,     &dbg_b,    &K,        &status2};
+                         &delta,    &norms,      &n_norms,   &dbg_h,     &dbg_b,    &K,        &status2,
+                         &attempts};
         for (DevBuf* b : all) b->release();
     }
 };
@@ -224,6 +225,7 @@ pvo_dev::BAParams stage_problem(pvo_ctx* ctx, const HostProblem& pr, const Plan&
         fail(PVO_UNSUPPORTED, "ba: more than " + std::to_string(pvo_dev::ba_max_poses()) + " poses in one problem");
     }
     a.status2 = B.status2.as<int>(2);
+    a.attempts = B.attempts.as<int>(1);
     const int grid = pvo_dev::ba_grid_size(pr.n_patches, pl.n_free_poses, pr.n_poses, ctx->num_sms);
     a.partials = B.partials.as<double>(pvo_dev::ba_partials_doubles(pl.n_free_poses, grid));
     a.system = B.system.as<double>((size_t)np * (np + 1) / 2 + np + 1);
@@ -520,6 +522,17 @@ int pvo_ctx_synchronize(pvo_ctx* ctx) {
 }
 
 int64_t pvo_ctx_kernel_launches(pvo_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int pvo_ctx_ba_attempts(pvo_ctx* ctx, int* attempts) {
+    return guarded([&] {
+        bind(ctx);
+        *attempts = 0;
+        if (ctx->ba.attempts.p) {
+            download(ctx, attempts, static_cast<const int*>(ctx->ba.attempts.p), 1);
+            sync(ctx);
+        }
+    });
+}
 
 int pvo_ctx_last_timing(pvo_ctx* ctx, double* corr_ms, double* ba_ms) {
     return guarded([&] {
@@ -948,6 +961,7 @@ pvo_dev::BAParams window_ba_params(pvo_ctx* ctx, int iterations, double damping)
     a.patch_h = static_cast<double*>(B.patch_h.p);
     a.patch_bd = static_cast<double*>(B.patch_bd.p);
     a.status2 = B.status2.as<int>(2);
+    a.attempts = B.attempts.as<int>(1);
     const int grid = pvo_dev::ba_grid_size(w.n_patches, w.plan.n_free_poses, w.n_poses, ctx->num_sms);
     a.partials = B.partials.as<double>(pvo_dev::ba_partials_doubles(w.plan.n_free_poses, grid));
     a.system = B.system.as<double>((size_t)np * (np + 1) / 2 + np + 1);

@@ -122,6 +122,7 @@ struct BAParams {
     int* n_norms = nullptr;
     int* status = nullptr;
     int* status2 = nullptr;           // [2] per-attempt-parity status words (scratch)
+    int* attempts = nullptr;          // [1] Gauss-Newton attempts made (guard retries included)
 };
 
 // Returns cudaErrorNotSupported when the shape exceeds the kernel (np > 96

@@ -17,3 +17,4 @@ with torch.cuda.stream(stream):
         win.iteration(2)
 torch.cuda.synchronize()
 print("corr/ba ms", ctx.last_timing())
+print("attempts", ctx.ba_attempts)
