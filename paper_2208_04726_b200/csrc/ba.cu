@@ -76,7 +76,7 @@ __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 struct Layout {
     int ab, pose, cand, delta, flags, uni;
     int S, rhs, rec, vb, scal, wr, ints;  // assembly
-    int A, x, od, perm, c, l;             // solve
+    int A, x, od, perm, c, l, pw;         // solve
     int total;
 };
 
@@ -120,6 +120,8 @@ __host__ __device__ inline Layout make_layout(int np_full, int n_poses) {
     s += 8 * np_full;
     L.l = s;
     s += 8 * np_full;
+    L.pw = s;
+    s += 8 * 16 * np_full;  // blocked LDL^T panel buffers (L^T panel, L D panel)
     L.perm = s;
     s += 4 * np_full;
     L.total = align16(a > s ? a : s);
@@ -163,15 +165,22 @@ __device__ inline void reproject_center(const SE3& pi, const SE3& pj, const Cam&
 // Eigen's pivot rule; all threads of the CTA.  x_out may be
 // shared or global memory.  Returns false (all threads) on a factorization
 // failure (zero pivot with a non-zero column below, LDLT::info()).
+//
+// Blocked right-looking LDL^T (block 8) on the permuted matrix:
+//   (1) warp 0 factors the 8x8 diagonal block (pivot chain in registers/shuffles),
+//   (2) one thread per panel row eliminates its 8 entries in registers,
+//   (3) all threads apply the rank-8 trailing update A -= (L D) L^T.
 // ---------------------------------------------------------------------------
-template <int kOwn>  // lower-triangle entries owned per thread: ceil(np(np+1)/2 / 256)
-__device__ bool ldlt_solve_cta_t(const double* sys, int np, unsigned char* smem, const Layout& L, double* x_out) {
-    const int tid = threadIdx.x;
+constexpr int kBlk = 8;
+
+__device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, const Layout& L, double* x_out) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     double* A = at<double>(smem, L.A);
     double* x = at<double>(smem, L.x);
     double* od = at<double>(smem, L.od);
-    double* c = at<double>(smem, L.c);
-    double* l = at<double>(smem, L.l);
+    double* dinv = at<double>(smem, L.c);     // reciprocal pivots
+    double* LT = at<double>(smem, L.pw);      // [kBlk][np]: L panel, transposed
+    double* WD = LT + kBlk * np;              // [np][kBlk]: L panel scaled by D
     int* perm = at<int>(smem, L.perm);
     __shared__ int s_fail, s_zero;
     // Pivot order.  Eigen's LDLT picks, step by step, the largest remaining
@@ -196,71 +205,101 @@ __device__ bool ldlt_solve_cta_t(const double* sys, int np, unsigned char* smem,
         perm[rank] = i;
     }
     __syncthreads();
-    // A = P S P^T: every thread owns fixed lower-triangle entries (i, j) of the
-    // permuted matrix in registers (row-major index q = i(i+1)/2 + j, q = tid + 256 r)
-    const int nlow = nent_of(np);
-    double av[kOwn];
-    int ai[kOwn], aj[kOwn];
-#pragma unroll
-    for (int r = 0; r < kOwn; ++r) {
-        const int q = tid + kThreads * r;
-        int i = (int)((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
-        while ((i + 1) * (i + 2) / 2 <= q) ++i;
-        while (i * (i + 1) / 2 > q) --i;
-        const int j = q - i * (i + 1) / 2;
-        ai[r] = q < nlow ? i : -1;
-        aj[r] = j;
-        av[r] = 0.0;
-        if (q < nlow) {
-            int a = perm[i], b = perm[j];
-            if (a > b) {
-                const int s = a;
-                a = b;
-                b = s;
+    // A = P S P^T (lower triangle, row-major rows), x = P rhs
+    for (int i = warp; i < np; i += kWarps) {
+        const int a = perm[i];
+        for (int j = lane; j <= i; j += 32) {
+            int r = a, s = perm[j];
+            if (r > s) {
+                const int t = r;
+                r = s;
+                s = t;
             }
-            av[r] = sys[a * np - a * (a - 1) / 2 + (b - a)];
+            A[i * np + j] = sys[r * np - r * (r - 1) / 2 + (s - r)];
         }
     }
     const int nent = nent_of(np);
     for (int i = tid; i < np; i += kThreads) x[i] = sys[nent + perm[i]];
-    // right-looking LDL^T, one barrier per step: column k is published into a
-    // double-buffered vector, every owner updates its entries in registers
-    bool fail = false;
-    for (int k = 0; k < np; ++k) {
-        double* cb = (k & 1) ? l : c;
+    __syncthreads();
+
+    for (int K0 = 0; K0 < np; K0 += kBlk) {
+        const int bsz = min(kBlk, np - K0);
+        // (1) diagonal block on warp 0: lane i < bsz holds row K0+i of the block
+        if (warp == 0) {
+            double row[kBlk];
 #pragma unroll
-        for (int r = 0; r < kOwn; ++r)
-            if (aj[r] == k && ai[r] >= k) cb[ai[r]] = av[r];
-        __syncthreads();
-        const double dk = cb[k];
-        const bool valid = fabs(dk) > 0.0;
-        if (k == 0 && !valid) {
-            // Eigen: all-zero diagonal -> D = 0, identity transpositions
-            if (tid == 0) s_zero = 1;
-            break;
-        }
-        const double inv = valid ? 1.0 / dk : 0.0;
+            for (int j = 0; j < kBlk; ++j) row[j] = (lane < bsz && j <= lane) ? A[(K0 + lane) * np + K0 + j] : 0.0;
+            bool fail = false, zero = false;
 #pragma unroll
-        for (int r = 0; r < kOwn; ++r) {
-            const int i = ai[r], j = aj[r];
-            if (i < 0) continue;
-            if (j > k) {
-                av[r] -= cb[i] * (cb[j] * inv);
-            } else if (j == k && i > k) {
-                if (valid) {
-                    av[r] *= inv;  // L column k
-                } else if (av[r] != 0.0) {
-                    fail = true;  // zero pivot with a non-zero column (LDLT::info())
+            for (int kk = 0; kk < kBlk; ++kk) {
+                if (kk < bsz) {
+                    const double dk = __shfl_sync(0xffffffffu, row[kk], kk);
+                    const bool valid = fabs(dk) > 0.0;
+                    if (K0 + kk == 0 && !valid) zero = true;  // Eigen: all-zero diagonal
+                    const double inv = valid ? 1.0 / dk : 0.0;
+                    if (lane == 0) dinv[K0 + kk] = inv;
+                    const double ci = row[kk];  // unscaled column entry of this lane's row
+                    const bool below = lane > kk && lane < bsz;
+                    if (below && !valid && ci != 0.0) fail = true;
+                    const double li = below ? (valid ? ci * inv : ci) : row[kk];
+#pragma unroll
+                    for (int j = kk + 1; j < kBlk; ++j) {
+                        const double cj = __shfl_sync(0xffffffffu, ci, j);  // column entry of row K0+j
+                        if (below && j <= lane && valid) row[j] -= ci * (cj * inv);
+                    }
+                    row[kk] = li;
                 }
             }
-        }
-    }
-    if (fail) s_fail = 1;
-    // publish L (strict lower) and D (diagonal)
+            if (lane < bsz) {
 #pragma unroll
-    for (int r = 0; r < kOwn; ++r)
-        if (ai[r] >= 0) A[ai[r] * np + aj[r]] = av[r];
-    __syncthreads();
+                for (int j = 0; j < kBlk; ++j)
+                    if (j <= lane) A[(K0 + lane) * np + K0 + j] = row[j];
+            }
+            if (__any_sync(0xffffffffu, fail) && lane == 0) s_fail = 1;
+            if (zero && lane == 0) s_zero = 1;
+        }
+        __syncthreads();
+        if (s_zero) break;
+        // (2) panel rows i >= K0+bsz: forward elimination of the row's block segment
+        for (int i = K0 + bsz + tid; i < np; i += kThreads) {
+            double seg[kBlk];
+#pragma unroll
+            for (int j = 0; j < kBlk; ++j) seg[j] = j < bsz ? A[i * np + K0 + j] : 0.0;
+#pragma unroll
+            for (int kk = 0; kk < kBlk; ++kk) {
+                if (kk < bsz) {
+                    const double c = seg[kk];
+                    const double inv = dinv[K0 + kk];
+#pragma unroll
+                    for (int j = kk + 1; j < kBlk; ++j)
+                        if (j < bsz) seg[j] -= c * A[(K0 + j) * np + K0 + kk];  // L of the diagonal block
+                    const double lv = inv != 0.0 ? c * inv : c;
+                    if (inv == 0.0 && c != 0.0) s_fail = 1;
+                    seg[kk] = lv;
+                    LT[kk * np + i] = lv;
+                    WD[i * kBlk + kk] = c;  // = l * d (the unscaled column entry)
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kBlk; ++j)
+                if (j < bsz) A[i * np + K0 + j] = seg[j];
+        }
+        __syncthreads();
+        // (3) trailing update A[i][j] -= sum_kk (L_i D)_kk L_j,kk for K0+bsz <= j <= i
+        for (int i = K0 + bsz + warp; i < np; i += kWarps) {
+            double w[kBlk];
+#pragma unroll
+            for (int kk = 0; kk < kBlk; ++kk) w[kk] = kk < bsz ? WD[i * kBlk + kk] : 0.0;
+            for (int j = K0 + bsz + lane; j <= i; j += 32) {
+                double acc = A[i * np + j];
+#pragma unroll
+                for (int kk = 0; kk < kBlk; ++kk)
+                    if (kk < bsz) acc -= w[kk] * LT[kk * np + j];
+                A[i * np + j] = acc;
+            }
+        }
+        __syncthreads();
+    }
     if (s_fail) return false;
     if (s_zero) {
         for (int i = tid; i < np; i += kThreads) x_out[i] = 0.0;
@@ -269,20 +308,22 @@ __device__ bool ldlt_solve_cta_t(const double* sys, int np, unsigned char* smem,
     }
     if (tid < 32) {
         // substitutions on one warp, x in registers (x[lane + 32 r])
-        const int lane = tid;
         double xr[3];
 #pragma unroll
         for (int r = 0; r < 3; ++r) xr[r] = lane + 32 * r < np ? x[lane + 32 * r] : 0.0;
-        for (int j = 0; j < np; ++j) {  // L y = P b
-            double xj = 0.0;
+        // the owner register of x[j] is static within each 32-wide segment
 #pragma unroll
-            for (int r = 0; r < 3; ++r)
-                if ((j >> 5) == r) xj = xr[r];
-            xj = __shfl_sync(0xffffffffu, xj, j & 31);
+        for (int seg = 0; seg < 3; ++seg) {  // L y = P b
+            for (int jj = 0; jj < 32; ++jj) {
+                const int j = 32 * seg + jj;
+                if (j >= np) break;
+                const double xj = __shfl_sync(0xffffffffu, xr[seg], jj);
 #pragma unroll
-            for (int r = 0; r < 3; ++r) {
-                const int i = lane + 32 * r;
-                if (i > j && i < np) xr[r] -= A[i * np + j] * xj;
+                for (int r = seg; r < 3; ++r) {
+                    const int i = lane + 32 * r;
+                    const double lij = (i > j && i < np) ? A[i * np + j] : 0.0;
+                    xr[r] -= lij * xj;
+                }
             }
         }
 #pragma unroll
@@ -293,16 +334,18 @@ __device__ bool ldlt_solve_cta_t(const double* sys, int np, unsigned char* smem,
                 xr[r] = fabs(dd) > DBL_MIN ? xr[r] / dd : 0.0;
             }
         }
-        for (int j = np - 1; j >= 0; --j) {  // L^T x = z
-            double xj = 0.0;
 #pragma unroll
-            for (int r = 0; r < 3; ++r)
-                if ((j >> 5) == r) xj = xr[r];
-            xj = __shfl_sync(0xffffffffu, xj, j & 31);
+        for (int seg = 2; seg >= 0; --seg) {  // L^T x = z
+            for (int jj = 31; jj >= 0; --jj) {
+                const int j = 32 * seg + jj;
+                if (j >= np) continue;
+                const double xj = __shfl_sync(0xffffffffu, xr[seg], jj);
 #pragma unroll
-            for (int r = 0; r < 3; ++r) {
-                const int i = lane + 32 * r;
-                if (i < j) xr[r] -= A[j * np + i] * xj;
+                for (int r = 0; r <= seg; ++r) {
+                    const int i = lane + 32 * r;
+                    const double lji = i < j ? A[j * np + i] : 0.0;
+                    xr[r] -= lji * xj;
+                }
             }
         }
 #pragma unroll
@@ -311,16 +354,6 @@ __device__ bool ldlt_solve_cta_t(const double* sys, int np, unsigned char* smem,
     }
     __syncthreads();
     return true;
-}
-
-__device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, const Layout& L, double* x_out) {
-    const int nlow = nent_of(np);
-    if (nlow <= 1 * kThreads) return ldlt_solve_cta_t<1>(sys, np, smem, L, x_out);
-    if (nlow <= 2 * kThreads) return ldlt_solve_cta_t<2>(sys, np, smem, L, x_out);
-    if (nlow <= 4 * kThreads) return ldlt_solve_cta_t<4>(sys, np, smem, L, x_out);
-    if (nlow <= 8 * kThreads) return ldlt_solve_cta_t<8>(sys, np, smem, L, x_out);
-    if (nlow <= 12 * kThreads) return ldlt_solve_cta_t<12>(sys, np, smem, L, x_out);
-    return ldlt_solve_cta_t<(kMaxNp * (kMaxNp + 1) / 2 + kThreads - 1) / kThreads>(sys, np, smem, L, x_out);
 }
 
 // ---------------------------------------------------------------------------

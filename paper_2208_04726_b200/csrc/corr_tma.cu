@@ -138,6 +138,59 @@ __device__ __forceinline__ int clamp_floor(double b, int extent) {
 }
 
 
+// Dot products of one tile for this warp's 8 channel chunks: lane owns NCS
+// union cells (lane, lane+32, ...) x 9 pixels.  Component-major FMA order
+// (9 * NCS independent FMAs between dependent ones).  Writes the partials.
+template <int NCS>
+__device__ __forceinline__ void dot_phase(const float* tile, const float* g, float* s_part, int TW, int NC, int lane,
+                                          int gw) {
+    int roff[NCS];
+#pragma unroll
+    for (int ci = 0; ci < NCS; ++ci) {
+        const int c = lane + 32 * ci;
+        const int cy = TW == 8 ? c >> 3 : (c * 57) >> 9, cx = c - cy * TW;  // c / TW, TW in {8, 9}
+        roff[ci] = c < NC ? (cy * kBox + cx) * kDP : 0;  // cells past NC read cell 0; never stored
+    }
+    float acc[NCS][kPix];
+#pragma unroll
+    for (int ci = 0; ci < NCS; ++ci)
+#pragma unroll
+        for (int p = 0; p < kPix; ++p) acc[ci][p] = 0.f;
+#pragma unroll 2
+    for (int j = 0; j < 8; ++j) {
+        const int ch = gw + kGroupWarps * j;
+        float4 gv[kPix], v[NCS];
+#pragma unroll
+        for (int p = 0; p < kPix; ++p) gv[p] = *reinterpret_cast<const float4*>(g + p * kD + 4 * ch);
+#pragma unroll
+        for (int ci = 0; ci < NCS; ++ci) v[ci] = *reinterpret_cast<const float4*>(tile + roff[ci] + 4 * ch);
+#pragma unroll
+        for (int ci = 0; ci < NCS; ++ci)
+#pragma unroll
+            for (int p = 0; p < kPix; ++p) acc[ci][p] = fmaf(v[ci].x, gv[p].x, acc[ci][p]);
+#pragma unroll
+        for (int ci = 0; ci < NCS; ++ci)
+#pragma unroll
+            for (int p = 0; p < kPix; ++p) acc[ci][p] = fmaf(v[ci].y, gv[p].y, acc[ci][p]);
+#pragma unroll
+        for (int ci = 0; ci < NCS; ++ci)
+#pragma unroll
+            for (int p = 0; p < kPix; ++p) acc[ci][p] = fmaf(v[ci].z, gv[p].z, acc[ci][p]);
+#pragma unroll
+        for (int ci = 0; ci < NCS; ++ci)
+#pragma unroll
+            for (int p = 0; p < kPix; ++p) acc[ci][p] = fmaf(v[ci].w, gv[p].w, acc[ci][p]);
+    }
+#pragma unroll
+    for (int ci = 0; ci < NCS; ++ci) {
+        const int c = lane + 32 * ci;
+        if (c < NC) {
+#pragma unroll
+            for (int p = 0; p < kPix; ++p) s_part[(gw * kPix + p) * kCells + c] = acc[ci][p];
+        }
+    }
+}
+
 // Per-pixel data of one tile: fractional bilinear weights per offset (exact
 // x - floor(x) in FP64, stored FP32) and the pixel's window origin in the
 // union tile.
@@ -267,69 +320,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int TW = m.z, TH = m.w, NC = active ? TW * TH : 0;
 
         if (active) {
-            // ---- dot products: lane owns up to 3 union cells x 9 pixels; warp owns 8 chunks ----
             const float* tile = reinterpret_cast<const float*>(st);
             const float* g = reinterpret_cast<const float*>(st + kTileRegion + kGramRegion);
-            int off[3];
-#pragma unroll
-            for (int ci = 0; ci < 3; ++ci) {
-                const int c = lane + 32 * ci;
-                const int cy = c / TW, cx = c - cy * TW;
-                off[ci] = c < NC ? (cy * kBox + cx) * kDP : -1;
+            // ---- dot products: lane owns 2 or 3 union cells x 9 pixels; warp owns 8 chunks ----
+            if (NC <= 64) {
+                dot_phase<2>(tile, g, s_part, TW, NC, lane, gw);
+            } else {
+                dot_phase<3>(tile, g, s_part, TW, NC, lane, gw);
             }
-            float acc[3][kPix];
-#pragma unroll
-            for (int ci = 0; ci < 3; ++ci)
-#pragma unroll
-                for (int p = 0; p < kPix; ++p) acc[ci][p] = 0.f;
-            // cells past NC read cell 0 (valid memory); their sums are never stored
-            int roff[3];
-#pragma unroll
-            for (int ci = 0; ci < 3; ++ci) roff[ci] = off[ci] >= 0 ? off[ci] : 0;
-#pragma unroll 2
-            for (int j = 0; j < 8; ++j) {
-                const int ch = gw + kGroupWarps * j;
-                float4 gv[kPix], v[3];
-#pragma unroll
-                for (int p = 0; p < kPix; ++p) gv[p] = *reinterpret_cast<const float4*>(g + p * kD + 4 * ch);
-#pragma unroll
-                for (int ci = 0; ci < 3; ++ci) v[ci] = *reinterpret_cast<const float4*>(tile + roff[ci] + 4 * ch);
-                // component-major: 27 independent FMAs between dependent ones
-#pragma unroll
-                for (int ci = 0; ci < 3; ++ci)
-#pragma unroll
-                    for (int p = 0; p < kPix; ++p) acc[ci][p] = fmaf(v[ci].x, gv[p].x, acc[ci][p]);
-#pragma unroll
-                for (int ci = 0; ci < 3; ++ci)
-#pragma unroll
-                    for (int p = 0; p < kPix; ++p) acc[ci][p] = fmaf(v[ci].y, gv[p].y, acc[ci][p]);
-#pragma unroll
-                for (int ci = 0; ci < 3; ++ci)
-#pragma unroll
-                    for (int p = 0; p < kPix; ++p) acc[ci][p] = fmaf(v[ci].z, gv[p].z, acc[ci][p]);
-#pragma unroll
-                for (int ci = 0; ci < 3; ++ci)
-#pragma unroll
-                    for (int p = 0; p < kPix; ++p) acc[ci][p] = fmaf(v[ci].w, gv[p].w, acc[ci][p]);
-            }
-#pragma unroll
-            for (int ci = 0; ci < 3; ++ci) {
-                const int c = lane + 32 * ci;
-                if (c < NC) {
-#pragma unroll
-                    for (int p = 0; p < kPix; ++p) s_part[(gw * kPix + p) * kCells + c] = acc[ci][p];
-                }
-            }
-            // Gram records of the union cells (this group's copy)
+            // Gram records of the union cells (this group's copy); TW is 8 or 9
             const float* gr = reinterpret_cast<const float*>(st + kTileRegion);
-            for (int i = gtid; i < NC * 5; i += kGroupThreads) {
-                const int c = i / 5, r = i - 5 * c;
-                const int cy = c / TW, cx = c - cy * TW;
-                s_gram[i] = gr[(cy * kBox + cx) * 8 + r];
+            if (gtid < NC) {
+                const int c = gtid;
+                const int cy = TW == 8 ? c >> 3 : (c * 57) >> 9, cx = c - cy * TW;
+                const float* src = gr + (cy * kBox + cx) * 8;
+#pragma unroll
+                for (int r = 0; r < 5; ++r) s_gram[5 * c + r] = src[r];
             }
             // per-pixel bilinear data (features.cpp:10-13 arithmetic)
-            if (gtid < kPix) {
-                const int p = gtid;
+            if (gtid >= kGroupThreads - kPix) {
+                const int p = gtid - (kGroupThreads - kPix);
                 const double scale = level ? 16.0 : 4.0;
                 const int W = level ? a.w1 : a.w0, H = level ? a.h1 : a.h0;
                 const double bx = tc[2 * p] / scale;
@@ -347,9 +357,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
         named_barrier(bar_id, kGroupThreads);   // partials, gram copy and pixel data complete
-        if (active) {
-            for (int i = gtid; i < kPix * NC; i += kGroupThreads) {
-                const int p = i / NC, c = i - p * NC;
+        if (active && gtid < NC) {
+            const int c = gtid;
+#pragma unroll
+            for (int p = 0; p < kPix; ++p) {
                 float sum = s_part[(0 * kPix + p) * kCells + c];
                 sum += s_part[(1 * kPix + p) * kCells + c];
                 sum += s_part[(2 * kPix + p) * kCells + c];
@@ -358,14 +369,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         named_barrier(bar_id, kGroupThreads);  // dots complete; s_part free for the next tile
-        if (active) {
-            float* out = a.out + ((size_t)e * 2 + level) * kPix * 49;
-            for (int o = gtid; o < kPix * 49; o += kGroupThreads) {
-                const int p = o / 49, ab = o - 49 * p;
-                const int alpha = ab / 7, beta = ab - 7 * alpha;
-                const float ax = pd->ax[p][beta], ay = pd->ay[p][alpha];
-                const int c00 = (pd->cy0[p] + alpha) * TW + (pd->cx0[p] + beta);
-                const float* d = s_dots + p * kCells;
+        if (active && gtid < 2 * kPix * 7) {
+            // thread -> (pixel p, row alpha, half of the 7 beta offsets)
+            const int pair = gtid >> 1, half = gtid & 1;
+            const int p = (pair * 37) >> 8, alpha = pair - 7 * p;  // pair / 7 for pair < 63
+            const float ay = pd->ay[p][alpha];
+            const int row = (pd->cy0[p] + alpha) * TW + pd->cx0[p];
+            const float* d = s_dots + p * kCells;
+            float* out = a.out + ((size_t)e * 2 + level) * kPix * 49 + p * 49 + alpha * 7;
+            const int b0 = half ? 4 : 0, b1 = half ? 7 : 4;
+            for (int beta = b0; beta < b1; ++beta) {
+                const float ax = pd->ax[p][beta];
+                const int c00 = row + beta;
                 const float w00 = (1.f - ax) * (1.f - ay), w10 = ax * (1.f - ay);
                 const float w01 = (1.f - ax) * ay, w11 = ax * ay;
                 float dot = w00 * d[c00];
@@ -388,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 cross = fmaf(w00 * w11, g00[3], cross);
                 cross = fmaf(w10 * w01, g00[4], cross);
                 n2 = fmaf(2.f, cross, n2);
-                out[o] = n2 > 1e-12f ? dot / sqrtf(n2) : 0.f;  // correlation.cpp:22
+                out[beta] = n2 > 1e-12f ? dot / sqrtf(n2) : 0.f;  // correlation.cpp:22
             }
         }
     }
