@@ -60,6 +60,11 @@ int pvo_ctx_set_stream(pvo_ctx* ctx, void* cuda_stream);
 int pvo_ctx_synchronize(pvo_ctx* ctx);
 /* Number of kernels this context has launched (profiling / gpu_launches). */
 int64_t pvo_ctx_kernel_launches(pvo_ctx* ctx);
+/* Tracing: when on, the BA kernel records clock64() at its phase boundaries
+ * (per attempt, up to 16 attempts x 8 stamps: assemble start/end, reduce
+ * start/end, solve start, update start/end, after the last barrier). */
+int pvo_ctx_set_tracing(pvo_ctx* ctx, int on);
+int pvo_ctx_ba_phase_cycles(pvo_ctx* ctx, long long* out128);
 /* Gauss-Newton attempts of the last BA run (divergence-guard retries included). */
 int pvo_ctx_ba_attempts(pvo_ctx* ctx, int* attempts);
 /* Device-side timing of the last pvo_window_iteration: corr ms, BA ms. */

@@ -36,6 +36,8 @@ SIGNATURES = {
     "pvo_ctx_kernel_launches": (i64, [vp]),
     "pvo_ctx_last_timing": (i32, [vp, P, P]),
     "pvo_ctx_ba_attempts": (i32, [vp, P]),
+    "pvo_ctx_set_tracing": (i32, [vp, i32]),
+    "pvo_ctx_ba_phase_cycles": (i32, [vp, P]),
     "pvo_se3_exp": (i32, [P, P]),
     "pvo_se3_log": (i32, [P, P]),
     "pvo_se3_compose": (i32, [P, P, P]),

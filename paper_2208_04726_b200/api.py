@@ -120,6 +120,15 @@ class Context:
         check(lib.pvo_ctx_ba_attempts(self.handle, C.addressof(n)))
         return n.value
 
+    def set_tracing(self, on: bool = True) -> None:
+        check(lib.pvo_ctx_set_tracing(self.handle, int(bool(on))))
+
+    def ba_phase_cycles(self) -> np.ndarray:
+        """[16 attempts][8] clock64 stamps of the last BA run (tracing on)."""
+        out = np.zeros(128, np.int64)
+        check(lib.pvo_ctx_ba_phase_cycles(self.handle, _ptr(out)))
+        return out.reshape(16, 8)
+
     def last_timing(self) -> tuple[float, float]:
         a, b = C.c_double(), C.c_double()
         check(lib.pvo_ctx_last_timing(self.handle, C.addressof(a), C.addressof(b)))

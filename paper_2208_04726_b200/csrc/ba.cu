@@ -74,11 +74,14 @@ __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 // Shared-memory plan (bytes).  Fixed part: entry table, pose copies, delta.
 // Union part: assembly scratch | solve workspace.
 struct Layout {
-    int ab, pose, cand, delta, flags, uni;
+    int ab, pose, cand, rmat, rmatc, delta, flags, uni;
     int S, rhs, rec, vb, scal, wr, ints;  // assembly
     int A, x, od, perm, c, l, pw;         // solve
     int total;
 };
+
+constexpr int kBlkL = 8;  // LDL^T block size (see ldlt_solve_cta)
+constexpr int kScal = 40;  // per-warp scalars: h, bd, inv_h, pad, then the 6x6 source block
 
 __host__ __device__ inline Layout make_layout(int np_full, int n_poses) {
     Layout L;
@@ -89,6 +92,10 @@ __host__ __device__ inline Layout make_layout(int np_full, int n_poses) {
     off += align16(8 * 7 * n_poses);
     L.cand = off;
     off += align16(8 * 7 * n_poses);
+    L.rmat = off;  // rotation matrix + translation of every pose (current state)
+    off += align16(8 * 12 * n_poses);
+    L.rmatc = off;  // ... of the candidate state
+    off += align16(8 * 12 * n_poses);
     L.delta = off;
     off += align16(8 * (np_full > 0 ? np_full : 1));
     L.flags = off;
@@ -104,24 +111,24 @@ __host__ __device__ inline Layout make_layout(int np_full, int n_poses) {
     L.vb = a;
     a += 8 * kWarps * 2 * np_full;
     L.scal = a;
-    a += 8 * kWarps * 4;
+    a += 8 * kWarps * kScal;
     L.wr = a;
     a += 8 * kWarps * 4;
     L.ints = a;
     a += 4 * kWarps * (4 + kMaxFree + kMaxEdges);
     int s = off;
     L.A = s;
-    s += 8 * np_full * np_full;
+    s += 8 * (np_full + 1) * (np_full + 1);  // + the rhs row
     L.x = s;
-    s += 8 * np_full;
+    s += 8 * (nent_of(np_full) + np_full);   // staged system, then x
     L.od = s;
-    s += 8 * np_full;
+    s += 8 * (np_full > kBlkL ? np_full : kBlkL);
     L.c = s;
     s += 8 * np_full;
     L.l = s;
     s += 8 * np_full;
     L.pw = s;
-    s += 8 * 16 * np_full;  // blocked LDL^T panel buffers (L^T panel, L D panel)
+    s += 8 * 16 * (np_full + 1);  // blocked LDL^T panel buffers (L^T panel, L D panel)
     L.perm = s;
     s += 4 * np_full;
     L.total = align16(a > s ? a : s);
@@ -160,6 +167,60 @@ __device__ inline void reproject_center(const SE3& pi, const SE3& pj, const Cam&
     *behind = b;
 }
 
+// Per-pose rotation matrix + translation, so that a relative pose is a 3x3
+// product instead of two quaternion normalisations per edge:
+//   T_j T_i^-1 = (R_j R_i^T, t_j - R_j R_i^T t_i)   (camera.cpp:59-61)
+__device__ void pose_mats(const double* poses, double* mats, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const SE3 p = se3_load(poses + 7 * i);
+        q_matrix(p.q, mats + 12 * i);
+        mats[12 * i + 9] = p.t.x;
+        mats[12 * i + 10] = p.t.y;
+        mats[12 * i + 11] = p.t.z;
+    }
+}
+__device__ __forceinline__ Relative rel_from_mats(const double* Mi, const double* Mj) {
+    Relative r;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+            r.r[3 * a + b] = Mj[3 * a] * Mi[3 * b] + Mj[3 * a + 1] * Mi[3 * b + 1] + Mj[3 * a + 2] * Mi[3 * b + 2];
+    const double ti0 = Mi[9], ti1 = Mi[10], ti2 = Mi[11];
+    r.t.x = Mj[9] - (r.r[0] * ti0 + r.r[1] * ti1 + r.r[2] * ti2);
+    r.t.y = Mj[10] - (r.r[3] * ti0 + r.r[4] * ti1 + r.r[5] * ti2);
+    r.t.z = Mj[11] - (r.r[6] * ti0 + r.r[7] * ti1 + r.r[8] * ti2);
+    return r;
+}
+// reproject_patch center + behind flag (camera.cpp:47-71) from a relative
+// pose: the shortcut when the two poses are bitwise equal, otherwise behind
+// if ANY of the 9 pixels has q_z <= eps (no division except the centre's).
+__device__ __forceinline__ void center_behind(bool equal, const Relative& rel, const Cam& K, const double* px,
+                                              const double* py, double d, double* cu, double* cv, bool* behind) {
+    if (equal) {
+        *cu = px[4];
+        *cv = py[4];
+        *behind = false;
+        return;
+    }
+    bool b = false;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        if (k == 4) {
+            double u, v;
+            const double qz = reproject_point(rel, K, d, px[k], py[k], &u, &v);
+            *cu = u;
+            *cv = v;
+            b = b || qz <= kDepthEpsilon;
+        } else {
+            const double rx = (px[k] - K.cx) / K.fx, ry = (py[k] - K.cy) / K.fy;
+            const double qz = rel.r[6] * rx + rel.r[7] * ry + rel.r[8] + rel.t.z * d;
+            b = b || qz <= kDepthEpsilon;
+        }
+    }
+    *behind = b;
+}
+
 // ---------------------------------------------------------------------------
 // Pivoted LDLT solve of an np x np SPD system held as (upper triangle, rhs),
 // Eigen's pivot rule; all threads of the CTA.  x_out may be
@@ -175,25 +236,30 @@ constexpr int kBlk = 8;
 
 __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, const Layout& L, double* x_out) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    double* A = at<double>(smem, L.A);
-    double* x = at<double>(smem, L.x);
+    const int ld = np + 1;                    // row stride: row np carries the right-hand side
+    double* A = at<double>(smem, L.A);        // [(np+1)][(np+1)] lower triangle (+ rhs row)
+    double* x = at<double>(smem, L.x);        // staged system (upper triangle + rhs), then x
     double* od = at<double>(smem, L.od);
     double* dinv = at<double>(smem, L.c);     // reciprocal pivots
-    double* LT = at<double>(smem, L.pw);      // [kBlk][np]: L panel, transposed
-    double* WD = LT + kBlk * np;              // [np][kBlk]: L panel scaled by D
+    double* LT = at<double>(smem, L.pw);      // [kBlk][np+1]: L panel, transposed
+    double* WD = LT + kBlk * ld;              // [np+1][kBlk]: unscaled panel (= L D)
     int* perm = at<int>(smem, L.perm);
     __shared__ int s_fail, s_zero;
+    const int nent = nent_of(np);
+    // stage the reduced system with coalesced loads
+    for (int i = tid; i < nent + np; i += kThreads) x[i] = sys[i];
+    if (tid == 0) {
+        s_fail = 0;
+        s_zero = 0;
+    }
+    __syncthreads();
     // Pivot order.  Eigen's LDLT picks, step by step, the largest remaining
     // |diagonal| of the original matrix (its left-looking update leaves the
     // trailing diagonal untouched): with distinct values that is the
     // descending order of |diag|, computed here as a parallel rank.  Among
     // exactly equal values Eigen's order follows its swap history; we keep
     // index order there, which changes rounding only (same SPD solution).
-    for (int i = tid; i < np; i += kThreads) od[i] = fabs(sys[i * np - i * (i - 1) / 2]);  // diag (i, i)
-    if (tid == 0) {
-        s_fail = 0;
-        s_zero = 0;
-    }
+    for (int i = tid; i < np; i += kThreads) od[i] = fabs(x[i * np - i * (i - 1) / 2]);  // diag (i, i)
     __syncthreads();
     for (int i = tid; i < np; i += kThreads) {
         const double di = od[i];
@@ -205,21 +271,26 @@ __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, c
         perm[rank] = i;
     }
     __syncthreads();
-    // A = P S P^T (lower triangle, row-major rows), x = P rhs
-    for (int i = warp; i < np; i += kWarps) {
-        const int a = perm[i];
-        for (int j = lane; j <= i; j += 32) {
-            int r = a, s = perm[j];
-            if (r > s) {
-                const int t = r;
-                r = s;
-                s = t;
+    // A = P S P^T (lower triangle), and row np = (P rhs)^T: eliminating it with
+    // the factorization yields z = D^-1 L^-1 P rhs (forward substitution for free)
+    for (int i = warp; i <= np; i += kWarps) {
+        const int a = i < np ? perm[i] : -1;
+        for (int j = lane; j <= i && j < np; j += 32) {
+            double v;
+            if (a < 0) {
+                v = x[nent + perm[j]];
+            } else {
+                int r = a, s = perm[j];
+                if (r > s) {
+                    const int t = r;
+                    r = s;
+                    s = t;
+                }
+                v = x[r * np - r * (r - 1) / 2 + (s - r)];
             }
-            A[i * np + j] = sys[r * np - r * (r - 1) / 2 + (s - r)];
+            A[i * ld + j] = v;
         }
     }
-    const int nent = nent_of(np);
-    for (int i = tid; i < np; i += kThreads) x[i] = sys[nent + perm[i]];
     __syncthreads();
 
     for (int K0 = 0; K0 < np; K0 += kBlk) {
@@ -228,7 +299,7 @@ __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, c
         if (warp == 0) {
             double row[kBlk];
 #pragma unroll
-            for (int j = 0; j < kBlk; ++j) row[j] = (lane < bsz && j <= lane) ? A[(K0 + lane) * np + K0 + j] : 0.0;
+            for (int j = 0; j < kBlk; ++j) row[j] = (lane < bsz && j <= lane) ? A[(K0 + lane) * ld + K0 + j] : 0.0;
             bool fail = false, zero = false;
 #pragma unroll
             for (int kk = 0; kk < kBlk; ++kk) {
@@ -253,18 +324,18 @@ __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, c
             if (lane < bsz) {
 #pragma unroll
                 for (int j = 0; j < kBlk; ++j)
-                    if (j <= lane) A[(K0 + lane) * np + K0 + j] = row[j];
+                    if (j <= lane) A[(K0 + lane) * ld + K0 + j] = row[j];
             }
             if (__any_sync(0xffffffffu, fail) && lane == 0) s_fail = 1;
             if (zero && lane == 0) s_zero = 1;
         }
         __syncthreads();
         if (s_zero) break;
-        // (2) panel rows i >= K0+bsz: forward elimination of the row's block segment
-        for (int i = K0 + bsz + tid; i < np; i += kThreads) {
+        // (2) panel rows i >= K0+bsz (the rhs row np included): forward elimination
+        for (int i = K0 + bsz + tid; i <= np; i += kThreads) {
             double seg[kBlk];
 #pragma unroll
-            for (int j = 0; j < kBlk; ++j) seg[j] = j < bsz ? A[i * np + K0 + j] : 0.0;
+            for (int j = 0; j < kBlk; ++j) seg[j] = j < bsz ? A[i * ld + K0 + j] : 0.0;
 #pragma unroll
             for (int kk = 0; kk < kBlk; ++kk) {
                 if (kk < bsz) {
@@ -272,30 +343,30 @@ __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, c
                     const double inv = dinv[K0 + kk];
 #pragma unroll
                     for (int j = kk + 1; j < kBlk; ++j)
-                        if (j < bsz) seg[j] -= c * A[(K0 + j) * np + K0 + kk];  // L of the diagonal block
+                        if (j < bsz) seg[j] -= c * A[(K0 + j) * ld + K0 + kk];  // L of the diagonal block
                     const double lv = inv != 0.0 ? c * inv : c;
-                    if (inv == 0.0 && c != 0.0) s_fail = 1;
+                    if (inv == 0.0 && c != 0.0 && i < np) s_fail = 1;
                     seg[kk] = lv;
-                    LT[kk * np + i] = lv;
+                    LT[kk * ld + i] = lv;
                     WD[i * kBlk + kk] = c;  // = l * d (the unscaled column entry)
                 }
             }
 #pragma unroll
             for (int j = 0; j < kBlk; ++j)
-                if (j < bsz) A[i * np + K0 + j] = seg[j];
+                if (j < bsz) A[i * ld + K0 + j] = seg[j];
         }
         __syncthreads();
-        // (3) trailing update A[i][j] -= sum_kk (L_i D)_kk L_j,kk for K0+bsz <= j <= i
-        for (int i = K0 + bsz + warp; i < np; i += kWarps) {
+        // (3) trailing update A[i][j] -= sum_kk (L D)_i,kk L_j,kk for K0+bsz <= j <= i (j < np)
+        for (int i = K0 + bsz + warp; i <= np; i += kWarps) {
             double w[kBlk];
 #pragma unroll
             for (int kk = 0; kk < kBlk; ++kk) w[kk] = kk < bsz ? WD[i * kBlk + kk] : 0.0;
-            for (int j = K0 + bsz + lane; j <= i; j += 32) {
-                double acc = A[i * np + j];
+            for (int j = K0 + bsz + lane; j <= i && j < np; j += 32) {
+                double acc = A[i * ld + j];
 #pragma unroll
                 for (int kk = 0; kk < kBlk; ++kk)
-                    if (kk < bsz) acc -= w[kk] * LT[kk * np + j];
-                A[i * np + j] = acc;
+                    if (kk < bsz) acc -= w[kk] * LT[kk * ld + j];
+                A[i * ld + j] = acc;
             }
         }
         __syncthreads();
@@ -306,52 +377,33 @@ __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, c
         __syncthreads();
         return true;
     }
-    if (tid < 32) {
-        // substitutions on one warp, x in registers (x[lane + 32 r])
-        double xr[3];
-#pragma unroll
-        for (int r = 0; r < 3; ++r) xr[r] = lane + 32 * r < np ? x[lane + 32 * r] : 0.0;
-        // the owner register of x[j] is static within each 32-wide segment
-#pragma unroll
-        for (int seg = 0; seg < 3; ++seg) {  // L y = P b
-            for (int jj = 0; jj < 32; ++jj) {
-                const int j = 32 * seg + jj;
-                if (j >= np) break;
-                const double xj = __shfl_sync(0xffffffffu, xr[seg], jj);
-#pragma unroll
-                for (int r = seg; r < 3; ++r) {
-                    const int i = lane + 32 * r;
-                    const double lij = (i > j && i < np) ? A[i * np + j] : 0.0;
-                    xr[r] -= lij * xj;
-                }
-            }
+    // z = D^-1 L^-1 P b sits in row np (pseudo-inverse of D: |d| <= DBL_MIN -> 0)
+    for (int i = tid; i < np; i += kThreads) x[i] = fabs(A[i * ld + i]) > DBL_MIN ? A[np * ld + i] : 0.0;
+    __syncthreads();
+    // blocked backward substitution L^T x = z, last block first
+    for (int K0 = ((np - 1) / kBlk) * kBlk; K0 >= 0; K0 -= kBlk) {
+        const int bsz = min(kBlk, np - K0);
+        // x_K -= L_{J,K}^T x_J over the solved rows J below the block: warp c owns column K0+c
+        if (warp < bsz) {
+            const int c = K0 + warp;
+            double s = 0.0;
+            for (int j = K0 + bsz + lane; j < np; j += 32) s += A[j * ld + c] * x[j];
+            s = warp_sum(s);
+            if (lane == 0) od[warp] = x[c] - s;
         }
-#pragma unroll
-        for (int r = 0; r < 3; ++r) {  // pseudo-inverse of D (LDLT::_solve_impl)
-            const int i = lane + 32 * r;
-            if (i < np) {
-                const double dd = A[i * np + i];
-                xr[r] = fabs(dd) > DBL_MIN ? xr[r] / dd : 0.0;
+        __syncthreads();
+        // unit upper-triangular solve inside the block (warp 0, lane c holds x_c)
+        if (warp == 0) {
+            double xc = lane < bsz ? od[lane] : 0.0;
+            for (int cc = bsz - 1; cc >= 0; --cc) {
+                const double xv = __shfl_sync(0xffffffffu, xc, cc);
+                if (lane < cc) xc -= A[(K0 + cc) * ld + K0 + lane] * xv;
             }
+            if (lane < bsz) x[K0 + lane] = xc;
         }
-#pragma unroll
-        for (int seg = 2; seg >= 0; --seg) {  // L^T x = z
-            for (int jj = 31; jj >= 0; --jj) {
-                const int j = 32 * seg + jj;
-                if (j >= np) continue;
-                const double xj = __shfl_sync(0xffffffffu, xr[seg], jj);
-#pragma unroll
-                for (int r = 0; r <= seg; ++r) {
-                    const int i = lane + 32 * r;
-                    const double lji = i < j ? A[j * np + i] : 0.0;
-                    xr[r] -= lji * xj;
-                }
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-            if (lane + 32 * r < np) x_out[perm[lane + 32 * r]] = xr[r];
+        __syncthreads();
     }
+    for (int i = tid; i < np; i += kThreads) x_out[perm[i]] = x[i];
     __syncthreads();
     return true;
 }
@@ -395,8 +447,9 @@ __device__ inline int* warp_ints(unsigned char* smem, const Layout& L, int w) {
 // ---------------------------------------------------------------------------
 // P1: assembly of the CTA's patches into its partial reduced system.
 // ---------------------------------------------------------------------------
-__device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Layout& L, const double* poses, int k0,
-                               int k1, int np, bool poses_frozen, double lambda, double* part, int* status) {
+__device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Layout& L, const double* poses,
+                               const double* mats, int k0, int k1, int np, bool poses_frozen, double lambda,
+                               double* part, int* status) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nent = nent_of(np);
     const Cam K{a.K[0], a.K[1], a.K[2], a.K[3]};
@@ -414,7 +467,7 @@ __device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Lay
         double* rec = at<double>(smem, L.rec) + (size_t)warp * kMaxEdges * kRec;
         double* v = at<double>(smem, L.vb) + (size_t)warp * 2 * np;
         double* bvec = v + np;
-        double* sc = at<double>(smem, L.scal) + warp * 4;
+        double* sc = at<double>(smem, L.scal) + warp * kScal;
         if (k < k1) {
             const int eb = a.patch_edge_begin[k], ne = a.patch_edge_begin[k + 1] - eb;
             const int src = a.patch_src[k];
@@ -433,7 +486,7 @@ __device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Lay
                 sj = poses_frozen ? -1 : a.pose_free_slot[tgt];
                 const SE3 pi = se3_load(poses + 7 * src);
                 const SE3 pj = se3_load(poses + 7 * tgt);
-                const Relative rel = relative_pose(pi, pj);
+                const Relative rel = rel_from_mats(mats + 12 * src, mats + 12 * tgt);
                 const CenterJac J = center_jacobians(rel, K, d, px[4], py[4]);
                 const double r0 = J.cu - a.e_target[2 * e], r1 = J.cv - a.e_target[2 * e + 1];
                 if (!isfinite(r0) || !isfinite(r1)) set_status(status, kDevNonFiniteResidual);
@@ -472,12 +525,30 @@ __device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Lay
                 // weighted_residual_norm term at the current state (bundle_adjust.cpp:99-113)
                 double cu, cv;
                 bool behind;
-                reproject_center(pi, pj, K, px, py, d, &cu, &cv, &behind);
+                center_behind(se3_equal(pi, pj), rel, K, px, py, d, &cu, &cv, &behind);
                 const double rx = cu - a.e_target[2 * e], ry = cv - a.e_target[2 * e + 1];
                 const double wx = behind ? 0.0 : a.e_weight[2 * e];
                 const double wy = behind ? 0.0 : a.e_weight[2 * e + 1];
                 wrs = wx * rx * rx + wy * ry * ry;
                 wrw = wx + wy;
+            }
+            __syncwarp();
+            // 6x6 source-pose block sum_e Gs^T W Gs of this patch (upper triangle on
+            // lanes 0..20, mirrored), so the CTA accumulation below is O(1) per entry
+            if (si >= 0 && lane < 21) {
+                int ra = 0, rem = lane;
+                while (rem >= 6 - ra) {
+                    rem -= 6 - ra;
+                    ++ra;
+                }
+                const int rb = ra + rem;
+                double val = 0.0;
+                for (int l = 0; l < ne; ++l) {
+                    const double* R = rec + l * kRec;
+                    val += (R[kGs + ra] * R[kW]) * R[kGs + rb] + (R[kGs + 6 + ra] * R[kW + 1]) * R[kGs + 6 + rb];
+                }
+                sc[4 + 6 * ra + rb] = val;
+                sc[4 + 6 * rb + ra] = val;
             }
             h = warp_sum(h);
             bd = warp_sum(bd);
@@ -535,6 +606,7 @@ __device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Lay
             wi[1] = -1;
         }
         __syncthreads();
+        if (a.phase_clocks && blockIdx.x == 0 && tid == 0 && batch == k0) a.phase_clocks[15 * 8 + 0] = clock64();
 
         // ---- ordered accumulation of the batch into the CTA system ----
         for (int w = 0; w < kWarps; ++w) {
@@ -545,20 +617,18 @@ __device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Lay
             const double* recw = at<double>(smem, L.rec) + (size_t)w * kMaxEdges * kRec;
             const double* vw = at<double>(smem, L.vb) + (size_t)w * 2 * np;
             const double* bw = vw + np;
-            const double* scw = at<double>(smem, L.scal) + w * 4;
+            const double* scw = at<double>(smem, L.scal) + w * kScal;
             const double inv_h = scw[2];
             const int* p2e = wiw + 4;
             const int* nxt = wiw + 4 + kMaxFree;
+            (void)ne;
             for (int ent = tid; ent < nent; ent += kThreads) {
-                const unsigned ab = abt[ent];
-                const int ia = ab & 0xffff, ib = ab >> 16;
-                const int A = ia / 6, B = ib / 6, ra = ia - 6 * A, rb = ib - 6 * B;
+                const unsigned ab = abt[ent];  // ia | ib << 8 | A << 16 | B << 24
+                const int ia = ab & 0xff, ib = (ab >> 8) & 0xff, A = (ab >> 16) & 0xff, B = ab >> 24;
+                const int ra = ia - 6 * A, rb = ib - 6 * B;
                 double val = 0.0;
                 if (A == si && B == si) {
-                    for (int l = 0; l < ne; ++l) {
-                        const double* R = recw + l * kRec;
-                        val += (R[kGs + ra] * R[kW]) * R[kGs + rb] + (R[kGs + 6 + ra] * R[kW + 1]) * R[kGs + 6 + rb];
-                    }
+                    val = scw[4 + 6 * ra + rb];
                 } else if (A == si) {
                     for (int l = p2e[B]; l >= 0; l = nxt[l]) {
                         const double* R = recw + l * kRec;
@@ -593,6 +663,7 @@ __device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Lay
         }
         __syncthreads();
     }
+    if (a.phase_clocks && blockIdx.x == 0 && tid == 0) a.phase_clocks[15 * 8 + 1] = clock64();
     // ---- write the CTA partial ----
     double* wr = at<double>(smem, L.wr);
     if (lane == 0) {
@@ -616,8 +687,9 @@ __device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Lay
 // ---------------------------------------------------------------------------
 // P4: depth back-substitution + residual at the candidate state.
 // ---------------------------------------------------------------------------
-__device__ void phase_update(const BAParams& a, unsigned char* smem, const Layout& L, const double* cand, int k0,
-                             int k1, int np, const double* delta, double* part_tail, int* status) {
+__device__ void phase_update(const BAParams& a, unsigned char* smem, const Layout& L, const double* cand,
+                             const double* cmats, int k0, int k1, int np, const double* delta, double* part_tail,
+                             int* status) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const Cam K{a.K[0], a.K[1], a.K[2], a.K[3]};
     double* wr = at<double>(smem, L.wr);
@@ -635,15 +707,18 @@ __device__ void phase_update(const BAParams& a, unsigned char* smem, const Layou
         }
         if (lane == 0) a.cand_depth[k] = dnew;
         const int eb = a.patch_edge_begin[k], ne = a.patch_edge_begin[k + 1] - eb;
-        const SE3 pi = se3_load(cand + 7 * a.patch_src[k]);
+        const int src = a.patch_src[k];
+        const SE3 pi = se3_load(cand + 7 * src);
         double ws = 0, ww = 0;
         for (int l = lane; l < ne; l += 32) {
             const int e = eb + l;
-            const SE3 pj = se3_load(cand + 7 * a.e_pose[e]);
+            const int tgt = a.e_pose[e];
+            const SE3 pj = se3_load(cand + 7 * tgt);
             double cu, cv;
             bool behind;
-            reproject_center(pi, pj, K, a.patch_x + 9 * (size_t)k, a.patch_y + 9 * (size_t)k, dnew, &cu, &cv,
-                             &behind);
+            const Relative rel = rel_from_mats(cmats + 12 * src, cmats + 12 * tgt);
+            center_behind(se3_equal(pi, pj), rel, K, a.patch_x + 9 * (size_t)k, a.patch_y + 9 * (size_t)k, dnew, &cu,
+                          &cv, &behind);
             const double rx = cu - a.e_target[2 * e], ry = cv - a.e_target[2 * e + 1];
             const double wx = behind ? 0.0 : a.e_weight[2 * e];
             const double wy = behind ? 0.0 : a.e_weight[2 * e + 1];
@@ -682,9 +757,12 @@ __global__ void __launch_bounds__(kThreads, 1) ba_kernel(BAParams a) {
     double* pose = at<double>(smem, L.pose);
     double* cand = at<double>(smem, L.cand);
     double* delta = at<double>(smem, L.delta);
+    double* rmat = at<double>(smem, L.rmat);
+    double* rmatc = at<double>(smem, L.rmatc);
     const size_t pstride = (size_t)nent_of(np_full) + np_full + 4;
 
-    // entry -> (a, b) table of the joint system; CTA copy of the pose state
+    // entry -> (row, col, row pose block, col pose block) table of the joint
+    // system; CTA copy of the pose state and its rotation matrices
     {
         unsigned* abt = at<unsigned>(smem, L.ab);
         const int nent = nent_of(np_full);
@@ -695,10 +773,13 @@ __global__ void __launch_bounds__(kThreads, 1) ba_kernel(BAParams a) {
                 --rowlen;
                 ++ia;
             }
-            abt[ent] = (unsigned)ia | ((unsigned)(ia + ent - base) << 16);
+            const int ib = ia + ent - base;
+            abt[ent] = (unsigned)ia | ((unsigned)ib << 8) | ((unsigned)(ia / 6) << 16) | ((unsigned)(ib / 6) << 24);
         }
         for (int i = tid; i < 7 * a.n_poses; i += kThreads) pose[i] = a.poses[i];
     }
+    __syncthreads();
+    pose_mats(pose, rmat, a.n_poses);
     __syncthreads();
     phase_freeze(a, pose, k0, k1);
     __syncthreads();
@@ -717,23 +798,34 @@ __global__ void __launch_bounds__(kThreads, 1) ba_kernel(BAParams a) {
             const double lambda =
                 attempt == 0 ? a.damping : a.damping * (attempt == 1 ? 1e3 : attempt == 2 ? 1e6 : 1e9);
             double* part = partials + (size_t)b * pstride;
-            phase_assemble(a, smem, L, pose, k0, k1, np, structure, lambda, part, status);
+            const bool clk = a.phase_clocks && b == 0 && tid == 0;
+            long long* pc = a.phase_clocks ? a.phase_clocks + 8 * (attempt_no < 15 ? attempt_no : 15) : nullptr;
+            if (clk) pc[0] = clock64();
+            phase_assemble(a, smem, L, pose, rmat, k0, k1, np, structure, lambda, part, status);
+            if (clk) pc[1] = clock64();
             grid.sync();
-            // P2: ordered reduction of the CTA partials (+ damping on the diagonal)
+            if (clk) pc[2] = clock64();
+            // P2: ordered reduction of the CTA partials (+ damping on the diagonal):
+            // one warp per entry, lanes over CTAs in fixed order, shuffle tree
             {
                 const unsigned* abt = at<unsigned>(smem, L.ab);
-                for (int ent = b * kThreads + tid; ent < nent + np; ent += G * kThreads) {
+                const int lane = tid & 31;
+                for (int ent = (b * kThreads + tid) >> 5; ent < nent + np; ent += (G * kThreads) >> 5) {
                     double acc = 0.0;
-#pragma unroll 8
-                    for (int c = 0; c < G; ++c) acc += partials[(size_t)c * pstride + ent];
-                    if (ent < nent) {
-                        const unsigned ab = abt[ent];
-                        if ((ab & 0xffff) == (ab >> 16)) acc += lambda;
+                    for (int c = lane; c < G; c += 32) acc += partials[(size_t)c * pstride + ent];
+                    acc = warp_sum(acc);
+                    if (lane == 0) {
+                        if (ent < nent) {
+                            const unsigned ab = abt[ent];
+                            if ((ab & 0xff) == ((ab >> 8) & 0xff)) acc += lambda;
+                        }
+                        a.system[ent] = acc;
                     }
-                    a.system[ent] = acc;
                 }
             }
+            if (clk) pc[3] = clock64();
             grid.sync();
+            if (clk) pc[4] = clock64();
             // P3: every CTA solves the pose system and retracts its pose copy
             if (np > 0) {
                 if (!ldlt_solve_cta(a.system, np, smem, L, delta)) {
@@ -757,8 +849,13 @@ __global__ void __launch_bounds__(kThreads, 1) ba_kernel(BAParams a) {
                 }
             }
             __syncthreads();
-            phase_update(a, smem, L, cand, k0, k1, np, delta, part + nent + np, status);
+            pose_mats(cand, rmatc, a.n_poses);
+            __syncthreads();
+            if (clk) pc[5] = clock64();
+            phase_update(a, smem, L, cand, rmatc, k0, k1, np, delta, part + nent + np, status);
+            if (clk) pc[6] = clock64();
             grid.sync();
+            if (clk) pc[7] = clock64();
             // P5: identical decision in every CTA
             const int st = *((volatile int*)status);
             if (st != 0) {
@@ -816,6 +913,7 @@ __global__ void __launch_bounds__(kThreads, 1) ba_kernel(BAParams a) {
             if (!reject) {
                 __syncthreads();
                 for (int i = tid; i < 7 * a.n_poses; i += kThreads) pose[i] = cand[i];
+                for (int i = tid; i < 12 * a.n_poses; i += kThreads) rmat[i] = rmatc[i];
                 for (int k = k0 + tid; k < k1; k += kThreads) a.depth[k] = a.cand_depth[k];
                 if (b == 0)
                     for (int i = tid; i < 7 * a.n_poses; i += kThreads) a.poses[i] = cand[i];

@@ -31,13 +31,13 @@ void set_last_error(const std::string& msg) { g_last_error = msg; }
 struct BABuffers {
     DevBuf poses, free_slot, patch_src, px, py, depth, depth_slot, edge_begin, e_patch, e_pose, e_in, e_w, e_target,
         e_weight, cand_poses, cand_depth, patch_v, patch_h, patch_bd, partials, system, delta, norms, n_norms, dbg_h,
-        dbg_b, K, status2, attempts;
+        dbg_b, K, status2, attempts, clocks;
     void release() {
         DevBuf* all[] = {&poses,    &free_slot,  &patch_src, &px,        &py,       &depth,    &depth_slot,
                          &edge_begin, &e_patch,  &e_pose,    &e_in,      &e_w,      &e_target, &e_weight,
                          &cand_poses, &cand_depth, &patch_v, &patch_h,   &patch_bd, &partials, &system,
                          &delta,    &norms,      &n_norms,   &dbg_h,     &dbg_b,    &K,        &status2,
-                         &attempts};
+                         &attempts, &clocks};
         for (DevBuf* b : all) b->release();
     }
 };
@@ -78,6 +78,7 @@ struct pvo_ctx {
     Window win;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     bool timing_pending = false;
+    bool tracing = false;  // record BA phase clocks (pvo_ctx_set_tracing)
 };
 
 namespace {
@@ -226,6 +227,7 @@ pvo_dev::BAParams stage_problem(pvo_ctx* ctx, const HostProblem& pr, const Plan&
     }
     a.status2 = B.status2.as<int>(2);
     a.attempts = B.attempts.as<int>(1);
+    a.phase_clocks = ctx->tracing ? B.clocks.as<long long>(128) : nullptr;
     const int grid = pvo_dev::ba_grid_size(pr.n_patches, pl.n_free_poses, pr.n_poses, ctx->num_sms);
     a.partials = B.partials.as<double>(pvo_dev::ba_partials_doubles(pl.n_free_poses, grid));
     a.system = B.system.as<double>((size_t)np * (np + 1) / 2 + np + 1);
@@ -522,6 +524,26 @@ int pvo_ctx_synchronize(pvo_ctx* ctx) {
 }
 
 int64_t pvo_ctx_kernel_launches(pvo_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int pvo_ctx_set_tracing(pvo_ctx* ctx, int on) {
+    return guarded([&] {
+        bind(ctx);
+        ctx->tracing = on != 0;
+        if (ctx->tracing) {
+            long long* c = ctx->ba.clocks.as<long long>(128);
+            cuda_check(cudaMemsetAsync(c, 0, 128 * sizeof(long long), ctx->stream), "memset");
+        }
+    });
+}
+
+int pvo_ctx_ba_phase_cycles(pvo_ctx* ctx, long long* out128) {
+    return guarded([&] {
+        bind(ctx);
+        if (!ctx->tracing) fail(PVO_INVALID_ARGUMENT, "tracing is off (pvo_ctx_set_tracing)");
+        download(ctx, out128, static_cast<const long long*>(ctx->ba.clocks.p), 128);
+        sync(ctx);
+    });
+}
 
 int pvo_ctx_ba_attempts(pvo_ctx* ctx, int* attempts) {
     return guarded([&] {
@@ -962,6 +984,7 @@ pvo_dev::BAParams window_ba_params(pvo_ctx* ctx, int iterations, double damping)
     a.patch_bd = static_cast<double*>(B.patch_bd.p);
     a.status2 = B.status2.as<int>(2);
     a.attempts = B.attempts.as<int>(1);
+    a.phase_clocks = ctx->tracing ? B.clocks.as<long long>(128) : nullptr;
     const int grid = pvo_dev::ba_grid_size(w.n_patches, w.plan.n_free_poses, w.n_poses, ctx->num_sms);
     a.partials = B.partials.as<double>(pvo_dev::ba_partials_doubles(w.plan.n_free_poses, grid));
     a.system = B.system.as<double>((size_t)np * (np + 1) / 2 + np + 1);

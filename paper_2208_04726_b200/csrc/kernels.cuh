@@ -123,6 +123,7 @@ struct BAParams {
     int* status = nullptr;
     int* status2 = nullptr;           // [2] per-attempt-parity status words (scratch)
     int* attempts = nullptr;          // [1] Gauss-Newton attempts made (guard retries included)
+    long long* phase_clocks = nullptr;  // [16][8] optional: CTA 0 clock64 at phase boundaries
 };
 
 // Returns cudaErrorNotSupported when the shape exceeds the kernel (np > 96

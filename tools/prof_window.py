@@ -18,3 +18,16 @@ with torch.cuda.stream(stream):
 torch.cuda.synchronize()
 print("corr/ba ms", ctx.last_timing())
 print("attempts", ctx.ba_attempts)
+ctx.set_tracing(True)
+with torch.cuda.stream(stream):
+    win.reset()
+    win.iteration(1)
+torch.cuda.synchronize()
+c = ctx.ba_phase_cycles()
+names = ["assemble", "sync1", "reduce", "sync2", "solve+retract", "update", "sync3"]
+for att in range(4):
+    row = c[att]
+    if row[0] == 0:
+        break
+    print("attempt", att, {n: int(row[i + 1] - row[i]) for i, n in enumerate(names)})
+print("assemble: records", int(c[15][0] - c[0][0]), "accumulate", int(c[15][1] - c[15][0]), "(last attempt's records vs first start; rerun with 1 iteration for exact)")
