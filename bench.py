@@ -281,25 +281,20 @@ def run_ours(args, rank, world, local_rank):
     corr_ms = float(np.mean([k[0] for k in kt]))
     ba_ms = float(np.mean([k[1] for k in kt]))
 
-    # max over ranks
-    t = torch.tensor([mean_ms, corr_ms, ba_ms], dtype=torch.float64, device=f"cuda:{local_rank}")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    mean_ms, corr_ms_max, ba_ms_max = t.tolist()
+    # max over ranks (the job's clock)
+    from paper_2208_04726_b200.dist import gather_poses, max_over_ranks
+
+    dev = f"cuda:{local_rank}"
+    mean_ms, corr_ms_max, ba_ms_max = max_over_ranks([mean_ms, corr_ms, ba_ms], device=dev).tolist()
 
     # e2e through the public API with host buffers (our own sequence, rank-local)
     e2e = run_e2e(args, w, prob, ctx, stream, win)
-    if world > 1:
-        te = torch.tensor([e2e["ms"]], dtype=torch.float64, device=f"cuda:{local_rank}")
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e["ms"] = te.item()
+    e2e["ms"] = float(max_over_ranks([e2e["ms"]], device=dev)[0])
 
-    # final gather of poses + stats (the only collective)
+    # final gather of poses (the only data collective, after the timed region)
     poses, depth, norms = win.read()
-    if world > 1:
-        pt = torch.tensor(poses, device=f"cuda:{local_rank}")
-        gathered = [torch.empty_like(pt) for _ in range(world)]
-        dist.all_gather(gathered, pt)
+    gathered = gather_poses(poses, device=dev)
+    assert len(gathered) == world
 
     if rank != 0:
         return
