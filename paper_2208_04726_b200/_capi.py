@@ -7,6 +7,7 @@ entry returns PVO_CUDA_ERROR without an sm_100 device.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 _LIB_PATH = Path(__file__).resolve().parent / "libpvo_b200.so"
@@ -85,7 +86,8 @@ SIGNATURES = {
 
 
 def load(path: Path | str | None = None) -> C.CDLL:
-    p = Path(path) if path else _LIB_PATH
+    # PVO_LIB: an alternative build of the same library (A/B kernel variants)
+    p = Path(path or os.environ.get("PVO_LIB") or _LIB_PATH)
     if not p.exists():
         raise ImportError(
             f"{p} is missing: build the sm_100a library first "

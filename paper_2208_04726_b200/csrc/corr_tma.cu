@@ -33,6 +33,10 @@ namespace pvo_dev {
 
 namespace {
 
+#ifndef PVO_CORR_UNROLL
+#define PVO_CORR_UNROLL 2
+#endif
+constexpr int kCorrUnroll = PVO_CORR_UNROLL;  // channel-chunk unroll of the FMA loop
 constexpr int kConsumerWarps = 8;              // two groups of 4 warps (ping-pong)
 constexpr int kGroupWarps = 4;
 constexpr int kGroupThreads = 32 * kGroupWarps;
@@ -156,7 +160,7 @@ __device__ __forceinline__ void dot_phase(const float* tile, const float* g, flo
     for (int ci = 0; ci < NCS; ++ci)
 #pragma unroll
         for (int p = 0; p < kPix; ++p) acc[ci][p] = 0.f;
-#pragma unroll 2
+#pragma unroll kCorrUnroll
     for (int j = 0; j < 8; ++j) {
         const int ch = gw + kGroupWarps * j;
         float4 gv[kPix], v[NCS];
@@ -236,10 +240,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int W = level ? a.w1 : a.w0, H = level ? a.h1 : a.h0;
         int xmin = 1 << 30, xmax = -(1 << 30), ymin = 1 << 30, ymax = -(1 << 30);
         bool finite = true;
+        int far = 0;  // pixels whose whole 8x8 tap window lies outside the grid: all 49 outputs are 0
         for (int p = 0; p < kPix; ++p) {
             const double x = a.coords[(size_t)e * 18 + 2 * p], y = a.coords[(size_t)e * 18 + 2 * p + 1];
             finite = finite && isfinite(x) && isfinite(y);
             const int fx = clamp_floor(x / scale, W), fy = clamp_floor(y / scale, H);
+            if (fx + 4 < 0 || fx - 3 >= W || fy + 4 < 0 || fy - 3 >= H) {
+                far |= 1 << p;
+                continue;
+            }
             xmin = min(xmin, fx);
             xmax = max(xmax, fx);
             ymin = min(ymin, fy);
@@ -249,12 +258,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!finite) {
             atomicOr(a.status, 1 << kDevBadCoords);  // correlation.cpp:43-45
             m.tw = -1;
+        } else if (far == (1 << kPix) - 1) {
+            m = TileMeta{0, 0, -2, 0};  // every tap of every pixel is zero padding
         } else if (m.tw > kBox || m.th > kBox) {
             const int slot = atomicAdd(a.overflow_count, 1);
             a.overflow[slot] = 2 * e + level;
             m.tw = 0;
         }
-        reinterpret_cast<int4*>(a.meta)[2 * e + level] = make_int4(m.x0, m.y0, m.tw, m.th);
+        reinterpret_cast<int4*>(a.meta)[2 * e + level] = make_int4(m.x0, m.y0, m.tw, m.th | (far << 8));
     }
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -317,7 +328,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int4 m = info.meta;
         const double* tc = reinterpret_cast<const double*>(st + kCoordOff);
         const bool active = m.z > 0;
-        const int TW = m.z, TH = m.w, NC = active ? TW * TH : 0;
+        const int TW = m.z, TH = m.w & 0xff, far = m.w >> 8, NC = active ? TW * TH : 0;
+        if (m.z == -2) {  // all taps outside the grid: the reference's zero padding gives 0 everywhere
+            float* out = a.out + ((size_t)e * 2 + level) * kPix * 49;
+            for (int o = gtid; o < kPix * 49; o += kGroupThreads) out[o] = 0.f;
+        }
 
         if (active) {
             const float* tile = reinterpret_cast<const float*>(st);
@@ -378,7 +393,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float* d = s_dots + p * kCells;
             float* out = a.out + ((size_t)e * 2 + level) * kPix * 49 + p * 49 + alpha * 7;
             const int b0 = half ? 4 : 0, b1 = half ? 7 : 4;
+            const bool far_p = (far >> p) & 1;  // window entirely outside the grid
             for (int beta = b0; beta < b1; ++beta) {
+                if (far_p) {
+                    out[beta] = 0.f;
+                    continue;
+                }
                 const float ax = pd->ax[p][beta];
                 const int c00 = row + beta;
                 const float w00 = (1.f - ax) * (1.f - ay), w10 = ax * (1.f - ay);
@@ -403,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 cross = fmaf(w00 * w11, g00[3], cross);
                 cross = fmaf(w10 * w01, g00[4], cross);
                 n2 = fmaf(2.f, cross, n2);
-                out[beta] = n2 > 1e-12f ? dot / sqrtf(n2) : 0.f;  // correlation.cpp:22
+                out[beta] = n2 > 1e-12f ? dot * rsqrtf(n2) : 0.f;  // correlation.cpp:22
             }
         }
     }
