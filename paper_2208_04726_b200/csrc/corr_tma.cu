@@ -60,6 +60,7 @@ constexpr int kTxBytes = kTileBytes + kGramBytes + kGBytes + kCoordBytes;
 struct StageInfo {
     int4 meta;  // union origin x, y, extent w, h (w <= 0: not on this path)
     int e, level;
+    int seq;  // tile index the stage currently holds (written by the producer)
 };
 // per consumer group scratch (after the stages); dots / gram / pixel data are
 // double-buffered by the group's tile parity
@@ -271,6 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kGroupWarps);
+            reinterpret_cast<StageInfo*>(smem + s * kStageBytes + kInfoOff)->seq = -1;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -291,6 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 info->meta = m;
                 info->e = e;
                 info->level = level;
+                *reinterpret_cast<volatile int*>(&info->seq) = t;
                 if (m.z <= 0) {  // not on this path: complete the phase without data
                     mbar_arrive(&full[s]);
                     continue;
@@ -321,8 +324,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* s_dots = reinterpret_cast<float*>(gscr + kPartBytes + parity * (kDotsBytes + kGramSBytes));
         float* s_gram = s_dots + kPix * kCells;
         PixData* pd = reinterpret_cast<PixData*>(gscr + kPartBytes + 2 * (kDotsBytes + kGramSBytes) + parity * 640);
-        mbar_wait(&full[s], (uint32_t)((t / kStages) & 1));
         const unsigned char* st = smem + s * kStageBytes;
+        // Stages alternate between the two groups (kStages is odd), so a group
+        // can reach stage s while it still holds an older phase: the parity
+        // wait alone would then pass on the stale phase.  Wait for the producer
+        // to claim the stage for tile t first; from then on the parity is exact.
+        while (reinterpret_cast<const volatile StageInfo*>(st + kInfoOff)->seq != t) {
+        }
+        mbar_wait(&full[s], (uint32_t)((t / kStages) & 1));
         const StageInfo info = *reinterpret_cast<const StageInfo*>(st + kInfoOff);
         const int e = info.e, level = info.level;
         const int4 m = info.meta;

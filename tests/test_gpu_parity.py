@@ -324,7 +324,9 @@ def test_window_iteration_deterministic(ctx, c1_workload):
         poses, depth, norms = win.read()
         outs.append((vol, poses, depth, norms))
     for a, b in zip(outs[0], outs[1]):
-        assert np.array_equal(np.asarray(a), np.asarray(b))
+        a, b = np.asarray(a), np.asarray(b)
+        diff = np.argwhere(a != b)
+        assert len(diff) == 0, (len(diff), diff[:4].tolist(), a[tuple(diff[0])], b[tuple(diff[0])])
     # and the BA half equals the flat-problem oracle on the same window
     ref = orc.ba_window(g.window_problem(w.cfg["window"]), w.K, iterations=2)
     dt, dq = pose_parity(outs[0][1], ref["poses"])
