@@ -71,8 +71,10 @@ struct pvo_ctx {
     DevBuf s0, s1, s2, s3, s4, s5, s6, s7, s8;
     // TMA descriptors of the frame store (feat0, feat1, gram0, gram1) and the
     // production correlation kernel's scratch
-    CUtensorMap maps[4];
+    CUtensorMap maps[5];  // feat0, feat1, gram0, gram1, patch descriptors (per call)
     bool maps_ok = false;
+    const void* patch_map_base = nullptr;
+    int patch_map_rows = 0;
     DevBuf c_coords, c_meta, c_over, c_count, c_order;
     BABuffers ba;
     Window win;
@@ -279,29 +281,54 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
-void encode_4d(CUtensorMap* map, void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3, uint32_t box0,
-               uint32_t box1, uint32_t box2) {
-    const cuuint64_t dims[4] = {d0, d1, d2, d3};
-    const cuuint64_t strides[3] = {d0 * 4, d0 * d1 * 4, d0 * d1 * d2 * 4};
-    const cuuint32_t box[4] = {box0, box1, box2, 1};
-    const cuuint32_t estr[4] = {1, 1, 1, 1};
-    const CUresult r = tensor_map_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims, strides, box, estr,
-                                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+bool encode_map(CUtensorMap* map, int rank, void* base, const uint64_t* dims, const uint32_t* box,
+                CUtensorMapSwizzle swizzle) {
+    cuuint64_t d[4], strides[3];
+    cuuint32_t bx[4], estr[4];
+    uint64_t stride = 4;
+    for (int i = 0; i < rank; ++i) {
+        d[i] = dims[i];
+        bx[i] = box[i];
+        estr[i] = 1;
+        if (i > 0) strides[i - 1] = stride;
+        stride *= dims[i];
+    }
+    const CUresult r = tensor_map_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, base, d, strides, bx, estr,
+                                            CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) fail(PVO_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return r == CUDA_SUCCESS;
 }
 
-// (Re)build the frame-store TMA descriptors: the feature tile box is
-// 132 channels x 9 x 9 cells (channels 128..131 are out of bounds -> zero
-// pad), the Gram box 8 x 9 x 9.
+// (Re)build the frame-store TMA descriptors (layouts in kernels.cuh): feature
+// tiles in 16-channel chunks with the 64B swizzle, planar Gram records with a
+// 12 x 9 x 5 box.  Shapes TMA cannot describe (C != 128, widths that are not a
+// multiple of 4 cells) leave the generic kernel in charge.
 void encode_frame_maps(pvo_ctx* ctx) {
     ctx->maps_ok = false;
-    if (ctx->C != 128 || ctx->w1 < 1 || ctx->h1 < 1) return;  // generic kernel only
-    encode_4d(&ctx->maps[0], ctx->feat0.p, 128, ctx->w0, ctx->h0, ctx->nf, 132, 9, 9);
-    encode_4d(&ctx->maps[1], ctx->feat1.p, 128, ctx->w1, ctx->h1, ctx->nf, 132, 9, 9);
-    encode_4d(&ctx->maps[2], ctx->gram0.p, 8, ctx->w0, ctx->h0, ctx->nf, 8, 9, 9);
-    encode_4d(&ctx->maps[3], ctx->gram1.p, 8, ctx->w1, ctx->h1, ctx->nf, 8, 9, 9);
-    ctx->maps_ok = true;
+    ctx->patch_map_base = nullptr;
+    if (ctx->C != 128 || ctx->w1 < 1 || ctx->h1 < 1 || ctx->w0 % 4 || ctx->w1 % 4) return;
+    const uint64_t f0[4] = {128, (uint64_t)ctx->w0, (uint64_t)ctx->h0, (uint64_t)ctx->nf};
+    const uint64_t f1[4] = {128, (uint64_t)ctx->w1, (uint64_t)ctx->h1, (uint64_t)ctx->nf};
+    const uint64_t g0[4] = {(uint64_t)ctx->w0, (uint64_t)ctx->h0, 8, (uint64_t)ctx->nf};
+    const uint64_t g1[4] = {(uint64_t)ctx->w1, (uint64_t)ctx->h1, 8, (uint64_t)ctx->nf};
+    const uint32_t fbox[4] = {16, 9, 9, 1}, gbox[4] = {12, 9, 5, 1};
+    ctx->maps_ok = encode_map(&ctx->maps[0], 4, ctx->feat0.p, f0, fbox, CU_TENSOR_MAP_SWIZZLE_64B) &&
+                   encode_map(&ctx->maps[1], 4, ctx->feat1.p, f1, fbox, CU_TENSOR_MAP_SWIZZLE_64B) &&
+                   encode_map(&ctx->maps[2], 4, ctx->gram0.p, g0, gbox, CU_TENSOR_MAP_SWIZZLE_NONE) &&
+                   encode_map(&ctx->maps[3], 4, ctx->gram1.p, g1, gbox, CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+// Descriptor of the patch-descriptor array [P * 2 * 9][128] (cached per base).
+bool encode_patch_map(pvo_ctx* ctx, const float* base, int n_patches) {
+    if (ctx->patch_map_base == base && ctx->patch_map_rows == n_patches * 18) return true;
+    ctx->patch_map_base = nullptr;
+    if (n_patches < 1 || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+    const uint64_t dims[2] = {128, (uint64_t)n_patches * 18};
+    const uint32_t box[2] = {16, 9};
+    if (!encode_map(&ctx->maps[4], 2, const_cast<float*>(base), dims, box, CU_TENSOR_MAP_SWIZZLE_NONE)) return false;
+    ctx->patch_map_base = base;
+    ctx->patch_map_rows = n_patches * 18;
+    return true;
 }
 
 // Correlation of a batch of edges against the frame store: the TMA kernel for
@@ -309,13 +336,13 @@ void encode_frame_maps(pvo_ctx* ctx) {
 // kernel alone.  `t` carries the inputs; scratch is filled in here.
 void run_corr(pvo_ctx* ctx, pvo_dev::CorrTmaParams t) {
     if (t.n_edges <= 0) return;
-    if (ctx->maps_ok) {
+    if (ctx->maps_ok && encode_patch_map(ctx, t.patch_feats, t.n_patches)) {
         t.w0 = ctx->w0;
         t.h0 = ctx->h0;
         t.w1 = ctx->w1;
         t.h1 = ctx->h1;
         t.coords = ctx->c_coords.as<double>((size_t)t.n_edges * 18);
-        t.meta = ctx->c_meta.as<int>((size_t)t.n_edges * 8);
+        t.meta = ctx->c_meta.as<int>((size_t)t.n_edges * 2 * pvo_dev::kCorrMetaInts);
         t.overflow = ctx->c_over.as<int>((size_t)t.n_edges * 2);
         t.overflow_count = ctx->c_count.as<int>(1);
         t.status = ctx->d_status;
@@ -784,6 +811,7 @@ int pvo_correlate_batch(pvo_ctx* ctx, int n_edges, int n_patches, int p, const i
         t.e_slot = des;
         t.coords_in = dc;
         t.patch_feats = dpf;
+        t.n_patches = n_patches;
         t.out = dout;
         run_corr(ctx, t);
         if (memspace != PVO_DEVICE) {
@@ -949,6 +977,7 @@ pvo_dev::CorrTmaParams window_corr_params(pvo_ctx* ctx, float* out) {
     cp.depth = static_cast<const double*>(ctx->ba.depth.p);
     cp.K = static_cast<const double*>(ctx->ba.K.p);
     cp.patch_feats = static_cast<const float*>(w.patch_feats.p);
+    cp.n_patches = w.n_patches;
     cp.out = out ? out : static_cast<float*>(w.corr.p);
     return cp;
 }

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(kThreads) corr_kernel(CorrParams a) {
                 const int cy = Y0 + cell / TW;
                 const int cx = X0 + cell % TW;
                 float v = 0.f;
-                if (cx >= 0 && cy >= 0 && cx < W && cy < H) v = __ldg(gbase + ((size_t)cy * W + cx) * 8 + t);
+                if (cx >= 0 && cy >= 0 && cx < W && cy < H) v = __ldg(gbase + (size_t)t * W * H + (size_t)cy * W + cx);
                 s_gram[i] = v;
             }
             for (int i = tid; i < npx * dp; i += kThreads) {
@@ -338,16 +338,13 @@ __global__ void gram_kernel(const float* __restrict__ feat, float* __restrict__ 
             s3 += __shfl_xor_sync(0xffffffffu, s3, off);
             s4 += __shfl_xor_sync(0xffffffffu, s4, off);
         }
-        if (lane == 0) {
-            float* g = gram + (size_t)cell * 8;
-            g[0] = s0;
-            g[1] = s1;
-            g[2] = s2;
-            g[3] = s3;
-            g[4] = s4;
-            g[5] = 0.f;
-            g[6] = 0.f;
-            g[7] = 0.f;
+        if (lane == 0) {  // planar records: plane k at gram + k * W * H (8 planes reserved, 5 used)
+            float* g = gram + cell;
+            g[0 * (size_t)ncell] = s0;
+            g[1 * (size_t)ncell] = s1;
+            g[2 * (size_t)ncell] = s2;
+            g[3 * (size_t)ncell] = s3;
+            g[4 * (size_t)ncell] = s4;
         }
     }
 }

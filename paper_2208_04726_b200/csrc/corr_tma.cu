@@ -2,25 +2,28 @@
 //
 // Same arithmetic as corr.cu (see its header: dots at integer cells + per-frame
 // Gram terms, regrouped by linearity from correlation.cpp:8-71), organised for
-// the B200 memory system:
-//   * persistent CTAs (one per SM), each walking its share of the edges in
-//     target-frame order, so the frames being read stay resident in L2;
-//   * a 3-stage TMA pipeline: for every (edge, level) one elected thread issues
-//       - a 4-D tensor copy of the 9x9-cell tile [9][9][132] fp32 whose channel
-//         box (132) overhangs the 128 stored channels, so TMA zero-fills 4 pad
-//         channels per cell — the padded, bank-conflict-free layout the FMA loop
-//         wants — and zero-fills out-of-image cells, which IS the reference's
-//         zero padding (features.cpp:15-17);
-//       - a 4-D tensor copy of the tile's Gram records [9][9][8];
-//       - a 1-D bulk copy of the patch's 9 x 128 descriptors;
-//     all completing on one mbarrier (complete_tx bytes);
-//   * FP32 FMA dot products, register-blocked 3 cells x 9 pixels per lane, warps
-//     split the channel chunks; fixed-order cross-warp sum (deterministic);
-//   * output recombination in FP32 with the bilinear weights' fractional parts
-//     taken exactly in FP64 (x - floor(x)), as the reference does.
-// (edge, level) tiles whose 9 pixel windows do not fit one 9x9 tile (extreme
-// zoom, pixels far outside the image) are diverted to an overflow list that the
-// generic kernel (corr.cu) finishes.
+// the B200 memory system and issue rate:
+//   * one (edge, level) tile = the 9x9-cell union window of the patch's 9
+//     pixels; the 729 dots <g_p, f_cell> of a tile are owned by ONE warp (lane
+//     owns 3 cells x 9 pixels, lanes 27..31 idle), so a tile needs no block
+//     barrier and no cross-warp reduction;
+//   * persistent CTAs (one per SM, 8 warps), each walking its share of the
+//     edges in target-frame order so the frames being read stay in L2; warps
+//     grab tiles dynamically from a CTA counter;
+//   * every warp runs its own 3-stage TMA ring over 16-channel chunks: per
+//     chunk a 4-D tensor copy of the tile [81 cells][16 ch] (64B-swizzled, so
+//     the 8-lane phases of a 128-bit shared load hit 8 distinct bank groups;
+//     out-of-image cells are zero-filled by TMA, which IS the reference's zero
+//     padding, features.cpp:15-17) and a 2-D copy of the patch descriptors
+//     [9 px][16 ch]; the first chunk of a tile also brings the tile's planar
+//     Gram records [5][9][12] and its 9 reprojected pixels.  The warp's elected
+//     lane refills a stage as soon as the warp has consumed it;
+//   * FP32 FMA dot products in fixed channel order (deterministic); output
+//     recombination in FP32 with the bilinear weights' fractional parts taken
+//     exactly in FP64 (x - floor(x)) as the reference does; coalesced stores.
+// (edge, level) tiles whose pixel windows do not fit one 9x9 tile (extreme
+// zoom) are diverted to an overflow list that the generic kernel (corr.cu)
+// finishes; tiles whose every tap is zero padding are zero-filled directly.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -33,43 +36,45 @@ namespace pvo_dev {
 
 namespace {
 
-#ifndef PVO_CORR_UNROLL
-#define PVO_CORR_UNROLL 2
-#endif
-constexpr int kCorrUnroll = PVO_CORR_UNROLL;  // channel-chunk unroll of the FMA loop
-constexpr int kConsumerWarps = 8;              // two groups of 4 warps (ping-pong)
-constexpr int kGroupWarps = 4;
-constexpr int kGroupThreads = 32 * kGroupWarps;
-constexpr int kThreads = 32 * (kConsumerWarps + 1);  // + one producer warp
+constexpr int kWarps = 8;
+constexpr int kThreads = 32 * kWarps;
 constexpr int kD = 128;
-constexpr int kDP = 132;  // padded cell stride (floats)
 constexpr int kBox = 9;
 constexpr int kCells = kBox * kBox;
 constexpr int kPix = 9;
-constexpr int kStages = 3;
-constexpr int kTileBytes = kCells * kDP * 4;                  // 42768
-constexpr int kTileRegion = (kTileBytes + 127) / 128 * 128;   // 42880
-constexpr int kGramBytes = kCells * 8 * 4;                    // 2592
-constexpr int kGramRegion = (kGramBytes + 127) / 128 * 128;   // 2688
-constexpr int kGBytes = kPix * kD * 4;                        // 4608
-constexpr int kCoordBytes = kPix * 2 * 8;                    // 144: the 9 reprojected pixels
-constexpr int kInfoOff = kTileRegion + kGramRegion + kGBytes;  // tile info written by the producer
-constexpr int kCoordOff = kInfoOff + 32;
-constexpr int kStageBytes = (kCoordOff + 160 + 1023) / 1024 * 1024;  // 51200: TMA dst needs 128 B alignment
-constexpr int kTxBytes = kTileBytes + kGramBytes + kGBytes + kCoordBytes;
-struct StageInfo {
-    int4 meta;  // union origin x, y, extent w, h (w <= 0: not on this path)
-    int e, level;
-    int seq;  // tile index the stage currently holds (written by the producer)
+constexpr int kOut = kPix * 49;
+constexpr int kChunkCh = 16;                           // channels per pipeline chunk (64 B rows)
+constexpr int kChunks = kD / kChunkCh;                 // 8
+constexpr int kStages = 3;                             // per-warp ring depth
+constexpr int kChunkTileBytes = kCells * kChunkCh * 4;  // 5184: [81][16] f32, 64B swizzle
+constexpr int kChunkGOff = 5248;                        // 128-aligned
+constexpr int kChunkGBytes = kPix * kChunkCh * 4;       // 576: [9][16] f32
+constexpr int kStageBytes = 6144;                       // 1024-aligned stages
+constexpr int kGramW = 12;                              // Gram box x extent (48 B rows)
+constexpr int kGramPlane = kBox * kGramW;               // 108
+constexpr int kGramBytes = 5 * kGramPlane * 4;          // 2160: [5][9][12]
+constexpr int kCoordBytes = kPix * 2 * 8;               // 144
+constexpr int kHeaderBytes = 2304;
+constexpr uint32_t kChunkTx = kChunkTileBytes + kChunkGBytes;
+constexpr uint32_t kHeaderTx = kGramBytes + kCoordBytes;
+constexpr int kHeaderOff = kStages * kStageBytes;        // 18432, 2 tile headers
+constexpr int kDotsOff = kHeaderOff + 2 * kHeaderBytes;  // 23040: [9][81] f32
+constexpr int kPixOff = kDotsOff + 2944;                 // 25984: PixData
+constexpr int kMetaOff = kPixOff + 640;                  // 26624: 2 tile records
+constexpr int kWarpBytes = 27648;
+constexpr int kSmemBytes = kWarps * kWarpBytes + 1024;   // + alignment slack
+static_assert(kChunkGOff >= kChunkTileBytes && kChunkGOff + kChunkGBytes <= kStageBytes, "stage");
+static_assert(kGramBytes + kCoordBytes <= kHeaderBytes, "header");
+static_assert(kMetaOff + 64 <= kWarpBytes && kWarpBytes % 1024 == 0, "warp region");
+static_assert(kCorrMetaInts == 8, "tile record");
+
+// tile record kinds (TileRec.code bits 0..1); bits 8..16: far-pixel mask
+constexpr int kKindTma = 0, kKindOverflow = 1, kKindZero = 2, kKindBad = 3;
+
+struct TileRec {
+    int x0, y0, code, slot;  // window origin (cells), kind | far << 8, frame-store slot
+    int grow, e, level, pad;  // patch-descriptor row ((patch * 2 + level) * 9), edge, level
 };
-// per consumer group scratch (after the stages); dots / gram / pixel data are
-// double-buffered by the group's tile parity
-constexpr int kPartBytes = kGroupWarps * kPix * kCells * 4;   // [4][9][81] f32
-constexpr int kDotsBytes = kPix * kCells * 4;                  // [9][81] f32
-constexpr int kGramSBytes = kCells * 5 * 4;                    // [81][5] f32
-constexpr int kGroupBytes = kPartBytes + 2 * (kDotsBytes + kGramSBytes) + 2 * 640;
-constexpr int kScratchOff = kStages * kStageBytes;
-constexpr int kSmemBytes = kScratchOff + 2 * kGroupBytes + 1024;  // + alignment slack
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -80,12 +85,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void named_barrier(int id, int threads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
@@ -106,16 +105,19 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(dst)),
                  "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
-
-struct TileMeta {
-    int x0, y0, tw, th;  // union origin (cells) and extent; tw <= 0: not on this path
-};
 
 // reproject_patch of pixel `pix` of edge e (camera.cpp:47-71)
 __device__ inline void edge_pixel(const CorrTmaParams& a, int e, int pix, double* xy) {
@@ -142,63 +144,8 @@ __device__ __forceinline__ int clamp_floor(double b, int extent) {
     return (int)floor(fmin(fmax(b, -16.0), (double)extent + 16.0));
 }
 
-
-// Dot products of one tile for this warp's 8 channel chunks: lane owns NCS
-// union cells (lane, lane+32, ...) x 9 pixels.  Component-major FMA order
-// (9 * NCS independent FMAs between dependent ones).  Writes the partials.
-template <int NCS>
-__device__ __forceinline__ void dot_phase(const float* tile, const float* g, float* s_part, int TW, int NC, int lane,
-                                          int gw) {
-    int roff[NCS];
-#pragma unroll
-    for (int ci = 0; ci < NCS; ++ci) {
-        const int c = lane + 32 * ci;
-        const int cy = TW == 8 ? c >> 3 : (c * 57) >> 9, cx = c - cy * TW;  // c / TW, TW in {8, 9}
-        roff[ci] = c < NC ? (cy * kBox + cx) * kDP : 0;  // cells past NC read cell 0; never stored
-    }
-    float acc[NCS][kPix];
-#pragma unroll
-    for (int ci = 0; ci < NCS; ++ci)
-#pragma unroll
-        for (int p = 0; p < kPix; ++p) acc[ci][p] = 0.f;
-#pragma unroll kCorrUnroll
-    for (int j = 0; j < 8; ++j) {
-        const int ch = gw + kGroupWarps * j;
-        float4 gv[kPix], v[NCS];
-#pragma unroll
-        for (int p = 0; p < kPix; ++p) gv[p] = *reinterpret_cast<const float4*>(g + p * kD + 4 * ch);
-#pragma unroll
-        for (int ci = 0; ci < NCS; ++ci) v[ci] = *reinterpret_cast<const float4*>(tile + roff[ci] + 4 * ch);
-#pragma unroll
-        for (int ci = 0; ci < NCS; ++ci)
-#pragma unroll
-            for (int p = 0; p < kPix; ++p) acc[ci][p] = fmaf(v[ci].x, gv[p].x, acc[ci][p]);
-#pragma unroll
-        for (int ci = 0; ci < NCS; ++ci)
-#pragma unroll
-            for (int p = 0; p < kPix; ++p) acc[ci][p] = fmaf(v[ci].y, gv[p].y, acc[ci][p]);
-#pragma unroll
-        for (int ci = 0; ci < NCS; ++ci)
-#pragma unroll
-            for (int p = 0; p < kPix; ++p) acc[ci][p] = fmaf(v[ci].z, gv[p].z, acc[ci][p]);
-#pragma unroll
-        for (int ci = 0; ci < NCS; ++ci)
-#pragma unroll
-            for (int p = 0; p < kPix; ++p) acc[ci][p] = fmaf(v[ci].w, gv[p].w, acc[ci][p]);
-    }
-#pragma unroll
-    for (int ci = 0; ci < NCS; ++ci) {
-        const int c = lane + 32 * ci;
-        if (c < NC) {
-#pragma unroll
-            for (int p = 0; p < kPix; ++p) s_part[(gw * kPix + p) * kCells + c] = acc[ci][p];
-        }
-    }
-}
-
 // Per-pixel data of one tile: fractional bilinear weights per offset (exact
-// x - floor(x) in FP64, stored FP32) and the pixel's window origin in the
-// union tile.
+// x - floor(x) in FP64, stored FP32) and the pixel's window origin in the tile.
 struct PixData {
     float ax[kPix][7];
     float ay[kPix][7];
@@ -210,34 +157,36 @@ static_assert(sizeof(PixData) <= 640, "PixData");
 __global__ void __launch_bounds__(kThreads, 1)
     corr_tma_kernel(const __grid_constant__ CUtensorMap feat0, const __grid_constant__ CUtensorMap feat1,
                     const __grid_constant__ CUtensorMap gram0, const __grid_constant__ CUtensorMap gram1,
-                    CorrTmaParams a) {
+                    const __grid_constant__ CUtensorMap patch, CorrTmaParams a) {
     extern __shared__ unsigned char smem_raw[];
-    unsigned char* smem =
-        reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ __align__(8) uint64_t full[kStages];
-    __shared__ __align__(8) uint64_t empty[kStages];
+    // 1024-aligned base, derived by offset so the compiler keeps the shared address space
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    __shared__ __align__(8) uint64_t full[kWarps * kStages];
+    __shared__ int s_next;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int G = gridDim.x, b = blockIdx.x;
     const int my_edges = a.n_edges > b ? (a.n_edges - 1 - b) / G + 1 : 0;
     const int n_tiles = 2 * my_edges;
 
-    // ---- phase 0 (all warps): coordinates and tile geometry of this CTA's edges ----
+    // ---- prologue (all warps): coordinates and tile records of this CTA's edges ----
     for (int i = tid; i < my_edges * kPix; i += kThreads) {
-        const int e = a.order ? a.order[b + (i / kPix) * G] : b + (i / kPix) * G;
+        const int pos = b + (i / kPix) * G;
+        const int e = a.order ? a.order[pos] : pos;
         const int pix = i % kPix;
         double xy[2];
         edge_pixel(a, e, pix, xy);
         a.coords[(size_t)e * 18 + 2 * pix] = xy[0];
         a.coords[(size_t)e * 18 + 2 * pix + 1] = xy[1];
     }
-    // the producer re-reads these coordinates with bulk (async-proxy) copies
+    // the tile headers re-read these coordinates with bulk (async-proxy) copies
     asm volatile("fence.proxy.async.global;" ::: "memory");
     __syncthreads();
-    for (int i = tid; i < my_edges * 2; i += kThreads) {
-        const int e = a.order ? a.order[b + (i >> 1) * G] : b + (i >> 1) * G;
+    for (int i = tid; i < n_tiles; i += kThreads) {
+        const int pos = b + (i >> 1) * G;
+        const int e = a.order ? a.order[pos] : pos;
         const int level = i & 1;
-        const double scale = level ? 16.0 : 4.0;
+        const double scale = level ? 16.0 : 4.0;  // kFeatureStride (features.hpp:46)
         const int W = level ? a.w1 : a.w0, H = level ? a.h1 : a.h0;
         int xmin = 1 << 30, xmax = -(1 << 30), ymin = 1 << 30, ymax = -(1 << 30);
         bool finite = true;
@@ -255,186 +204,227 @@ __global__ void __launch_bounds__(kThreads, 1)
             ymin = min(ymin, fy);
             ymax = max(ymax, fy);
         }
-        TileMeta m{xmin - 3, ymin - 3, xmax - xmin + 8, ymax - ymin + 8};
+        int kind = kKindTma;
         if (!finite) {
             atomicOr(a.status, 1 << kDevBadCoords);  // correlation.cpp:43-45
-            m.tw = -1;
+            kind = kKindBad;
         } else if (far == (1 << kPix) - 1) {
-            m = TileMeta{0, 0, -2, 0};  // every tap of every pixel is zero padding
-        } else if (m.tw > kBox || m.th > kBox) {
+            kind = kKindZero;  // every tap of every pixel is zero padding
+        } else if (xmax - xmin + 8 > kBox || ymax - ymin + 8 > kBox) {
             const int slot = atomicAdd(a.overflow_count, 1);
             a.overflow[slot] = 2 * e + level;
-            m.tw = 0;
+            kind = kKindOverflow;
         }
-        reinterpret_cast<int4*>(a.meta)[2 * e + level] = make_int4(m.x0, m.y0, m.tw, m.th | (far << 8));
+        const int fslot = a.e_slot ? a.e_slot[e] : a.pose_slot[a.e_pose[e]];
+        int4* rec = reinterpret_cast<int4*>(a.meta) + 2 * ((size_t)2 * pos + level);
+        rec[0] = make_int4(xmin - 3, ymin - 3, kind | (far << 8), fslot);
+        rec[1] = make_int4((a.e_patch[e] * 2 + level) * kPix, e, level, 0);
     }
-    if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kGroupWarps);
-            reinterpret_cast<StageInfo*>(smem + s * kStageBytes + kInfoOff)->seq = -1;
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
+    if (tid < kWarps * kStages) mbar_init(&full[tid], 1);
+    if (tid == 0) s_next = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
 
-    auto tile_edge = [&](int t) { return a.order ? a.order[b + (t >> 1) * G] : b + (t >> 1) * G; };
+    // ================= per-warp pipeline =================
+    unsigned char* wb = smem + warp * kWarpBytes;
+    uint64_t* bars = full + warp * kStages;
 
-    if (warp == kConsumerWarps) {
-        // ================= producer warp =================
+    // issue cursor (warp-uniform): pending tile + its record, current tile, chunk
+    int pend = 0;
+    int4 pr0 = make_int4(0, 0, 0, 0), pr1 = make_int4(0, 0, 0, 0);
+    auto grab = [&]() {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(&s_next, 1);
+        pend = __shfl_sync(0xffffffffu, t, 0);
+        if (pend < n_tiles) {
+            const int4* src = reinterpret_cast<const int4*>(a.meta) + 2 * ((size_t)2 * (b + (pend >> 1) * G) + (pend & 1));
+            pr0 = __ldcg(src);
+            pr1 = __ldcg(src + 1);
+        }
+    };
+    grab();
+    int4 ir0 = make_int4(0, 0, 0, 0), ir1 = make_int4(0, 0, 0, 0);
+    int ichunk = kChunks;  // chunks of the current issue tile already issued
+    bool idone = false;
+    int qi = 0, hi = 0;    // chunks issued, tiles issued
+    auto issue_one = [&]() {
+        if (idone) return;
+        while (ichunk == kChunks) {  // advance to the next tile that needs the pipeline
+            if (pend >= n_tiles) {
+                idone = true;
+                return;
+            }
+            const int4 r0 = pr0, r1 = pr1;
+            grab();
+            const int kind = r0.z & 3;
+            if (kind == kKindTma) {
+                ir0 = r0;
+                ir1 = r1;
+                ichunk = 0;
+            } else if (kind == kKindZero) {
+                float* out = a.out + ((size_t)r1.y * 2 + r1.z) * kOut;
+                for (int o = lane; o < kOut; o += 32) out[o] = 0.f;
+            }
+        }
+        const int s = qi % kStages;
+        unsigned char* st = wb + s * kStageBytes;
         if (lane == 0) {
-            for (int t = 0; t < n_tiles; ++t) {
-                const int s = t % kStages;
-                if (t >= kStages) mbar_wait(&empty[s], (uint32_t)(((t / kStages) - 1) & 1));
-                const int e = tile_edge(t), level = t & 1;
-                const int4 m = reinterpret_cast<const int4*>(a.meta)[2 * e + level];
-                unsigned char* st = smem + s * kStageBytes;
-                StageInfo* info = reinterpret_cast<StageInfo*>(st + kInfoOff);
-                info->meta = m;
-                info->e = e;
-                info->level = level;
-                *reinterpret_cast<volatile int*>(&info->seq) = t;
-                if (m.z <= 0) {  // not on this path: complete the phase without data
-                    mbar_arrive(&full[s]);
-                    continue;
-                }
-                const int slot = a.e_slot ? a.e_slot[e] : a.pose_slot[a.e_pose[e]];
-                mbar_expect_tx(&full[s], kTxBytes);
-                tma_load_4d(st, level ? &feat1 : &feat0, 0, m.x, m.y, slot, &full[s]);
-                tma_load_4d(st + kTileRegion, level ? &gram1 : &gram0, 0, m.x, m.y, slot, &full[s]);
-                const float* g = a.patch_feats + ((size_t)a.e_patch[e] * 2 + level) * kPix * kD;
-                bulk_load(st + kTileRegion + kGramRegion, g, kGBytes, &full[s]);
-                bulk_load(st + kCoordOff, a.coords + (size_t)e * 18, kCoordBytes, &full[s]);
-            }
-        }
-        return;
-    }
-
-    // ================= consumer groups =================
-    const int grp = warp / kGroupWarps;           // 0 or 1
-    const int gw = warp - grp * kGroupWarps;       // warp within the group
-    const int gtid = tid - grp * kGroupThreads;    // thread within the group
-    unsigned char* gscr = smem + kScratchOff + grp * kGroupBytes;
-    float* s_part = reinterpret_cast<float*>(gscr);
-    const int bar_id = 1 + grp;
-
-    int parity = 0;  // this group's tile parity (double buffers)
-    for (int t = grp; t < n_tiles; t += 2, parity ^= 1) {
-        const int s = t % kStages;
-        float* s_dots = reinterpret_cast<float*>(gscr + kPartBytes + parity * (kDotsBytes + kGramSBytes));
-        float* s_gram = s_dots + kPix * kCells;
-        PixData* pd = reinterpret_cast<PixData*>(gscr + kPartBytes + 2 * (kDotsBytes + kGramSBytes) + parity * 640);
-        const unsigned char* st = smem + s * kStageBytes;
-        // Stages alternate between the two groups (kStages is odd), so a group
-        // can reach stage s while it still holds an older phase: the parity
-        // wait alone would then pass on the stale phase.  Wait for the producer
-        // to claim the stage for tile t first; from then on the parity is exact.
-        while (reinterpret_cast<const volatile StageInfo*>(st + kInfoOff)->seq != t) {
-        }
-        mbar_wait(&full[s], (uint32_t)((t / kStages) & 1));
-        const StageInfo info = *reinterpret_cast<const StageInfo*>(st + kInfoOff);
-        const int e = info.e, level = info.level;
-        const int4 m = info.meta;
-        const double* tc = reinterpret_cast<const double*>(st + kCoordOff);
-        const bool active = m.z > 0;
-        const int TW = m.z, TH = m.w & 0xff, far = m.w >> 8, NC = active ? TW * TH : 0;
-        if (m.z == -2) {  // all taps outside the grid: the reference's zero padding gives 0 everywhere
-            float* out = a.out + ((size_t)e * 2 + level) * kPix * 49;
-            for (int o = gtid; o < kPix * 49; o += kGroupThreads) out[o] = 0.f;
-        }
-
-        if (active) {
-            const float* tile = reinterpret_cast<const float*>(st);
-            const float* g = reinterpret_cast<const float*>(st + kTileRegion + kGramRegion);
-            // ---- dot products: lane owns 2 or 3 union cells x 9 pixels; warp owns 8 chunks ----
-            if (NC <= 64) {
-                dot_phase<2>(tile, g, s_part, TW, NC, lane, gw);
+            const int level = ir1.z;
+            if (ichunk == 0) {
+                const int hb = hi & 1;
+                int4* rec = reinterpret_cast<int4*>(wb + kMetaOff + 32 * hb);
+                rec[0] = ir0;
+                rec[1] = ir1;
+                unsigned char* hd = wb + kHeaderOff + hb * kHeaderBytes;
+                mbar_expect_tx(&bars[s], kChunkTx + kHeaderTx);
+                // TMA needs a 16-byte aligned start in the innermost (x) dimension: start at
+                // floor4(x0); the 12-wide box still covers x0 .. x0 + 8
+                tma_load_4d(hd, level ? &gram1 : &gram0, ir0.x & ~3, ir0.y, 0, ir0.w, &bars[s]);
+                bulk_load(hd + kGramBytes, a.coords + (size_t)ir1.y * 18, kCoordBytes, &bars[s]);
             } else {
-                dot_phase<3>(tile, g, s_part, TW, NC, lane, gw);
+                mbar_expect_tx(&bars[s], kChunkTx);
             }
-            // Gram records of the union cells (this group's copy); TW is 8 or 9
-            const float* gr = reinterpret_cast<const float*>(st + kTileRegion);
-            if (gtid < NC) {
-                const int c = gtid;
-                const int cy = TW == 8 ? c >> 3 : (c * 57) >> 9, cx = c - cy * TW;
-                const float* src = gr + (cy * kBox + cx) * 8;
+            tma_load_4d(st, level ? &feat1 : &feat0, ichunk * kChunkCh, ir0.x, ir0.y, ir0.w, &bars[s]);
+            tma_load_2d(st + kChunkGOff, &patch, ichunk * kChunkCh, ir1.x, &bars[s]);
+        }
+        if (ichunk == 0) ++hi;
+        ++ichunk;
+        ++qi;
+    };
+    for (int k = 0; k < kStages; ++k) issue_one();
+    __syncwarp();
+
+    // lane -> its 3 cells (rows of the 9x9 box); lanes 27..31 compute throwaway rows
+    int roff[3];
 #pragma unroll
-                for (int r = 0; r < 5; ++r) s_gram[5 * c + r] = src[r];
-            }
-            // per-pixel bilinear data (features.cpp:10-13 arithmetic)
-            if (gtid >= kGroupThreads - kPix) {
-                const int p = gtid - (kGroupThreads - kPix);
-                const double scale = level ? 16.0 : 4.0;
-                const int W = level ? a.w1 : a.w0, H = level ? a.h1 : a.h0;
-                const double bx = tc[2 * p] / scale;
-                const double by = tc[2 * p + 1] / scale;
-                const int fx = clamp_floor(bx, W), fy = clamp_floor(by, H);
+    for (int k = 0; k < 3; ++k) {
+        const int r = lane + 27 * k;
+        roff[k] = r * 64;
+    }
+    float* dots = reinterpret_cast<float*>(wb + kDotsOff);
+    PixData* pd = reinterpret_cast<PixData*>(wb + kPixOff);
+    int qc = 0;
+    for (int hc = 0; hc < hi; ++hc) {
+        float acc[3][kPix];
 #pragma unroll
-                for (int o = 0; o < 7; ++o) {
-                    pd->ax[p][o] = (float)((bx + (double)(o - 3)) - (double)(fx + o - 3));
-                    pd->ay[p][o] = (float)((by + (double)(o - 3)) - (double)(fy + o - 3));
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int p = 0; p < kPix; ++p) acc[k][p] = 0.f;
+        for (int c = 0; c < kChunks; ++c, ++qc) {
+            const int s = qc % kStages;
+            mbar_wait(&bars[s], (uint32_t)((qc / kStages) & 1));
+            const unsigned char* st = wb + s * kStageBytes;
+            const float* g = reinterpret_cast<const float*>(st + kChunkGOff);
+            // per-chunk partial sums, then one add into the tile total: 16 + 8 term
+            // chains instead of one 128-term chain (FP32 error well inside 1e-4)
+            float part[3][kPix];
+#pragma unroll
+            for (int u = 0; u < kChunkCh / 4; ++u) {
+                float4 v[3], gv[kPix];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    // 64B swizzle: 16-byte unit u of row r lives at unit u ^ ((r >> 1) & 3)
+                    const int sw = (roff[k] >> 7) & 3;
+                    v[k] = *reinterpret_cast<const float4*>(st + roff[k] + ((u ^ sw) << 4));
                 }
-                pd->cx0[p] = fx - 3 - m.x;
-                pd->cy0[p] = fy - 3 - m.y;
+#pragma unroll
+                for (int p = 0; p < kPix; ++p) gv[p] = *reinterpret_cast<const float4*>(g + p * kChunkCh + 4 * u);
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+#pragma unroll
+                    for (int p = 0; p < kPix; ++p)
+                        part[k][p] = u == 0 ? v[k].x * gv[p].x : fmaf(v[k].x, gv[p].x, part[k][p]);
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+#pragma unroll
+                    for (int p = 0; p < kPix; ++p) part[k][p] = fmaf(v[k].y, gv[p].y, part[k][p]);
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+#pragma unroll
+                    for (int p = 0; p < kPix; ++p) part[k][p] = fmaf(v[k].z, gv[p].z, part[k][p]);
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+#pragma unroll
+                    for (int p = 0; p < kPix; ++p) part[k][p] = fmaf(v[k].w, gv[p].w, part[k][p]);
             }
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                for (int p = 0; p < kPix; ++p) acc[k][p] += part[k][p];
+            __syncwarp();  // every lane is done with stage s
+            issue_one();
+        }
+
+        // ---- epilogue: dots -> shared, per-pixel bilinear data, 441 outputs ----
+        const int hb = hc & 1;
+        const int4 r0 = *reinterpret_cast<const int4*>(wb + kMetaOff + 32 * hb);
+        const int4 r1 = *reinterpret_cast<const int4*>(wb + kMetaOff + 32 * hb + 16);
+        const unsigned char* hd = wb + kHeaderOff + hb * kHeaderBytes;
+        const float* gram = reinterpret_cast<const float*>(hd);
+        const double* tc = reinterpret_cast<const double*>(hd + kGramBytes);
+        const int e = r1.y, level = r1.z, far = r0.z >> 8;
+        if (lane < 27) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                for (int p = 0; p < kPix; ++p) dots[p * kCells + lane + 27 * k] = acc[k][p];
+        }
+        // per-pixel bilinear data (features.cpp:10-13 arithmetic): lanes 27..31 take
+        // pixels 0..4, lanes 0..3 pixels 5..8
+        const int p_pix = lane >= 27 ? lane - 27 : (lane < 4 ? 5 + lane : -1);
+        if (p_pix >= 0) {
+            const int p = p_pix;
+            const double scale = level ? 16.0 : 4.0;
+            const int W = level ? a.w1 : a.w0, H = level ? a.h1 : a.h0;
+            const double bx = tc[2 * p] / scale;
+            const double by = tc[2 * p + 1] / scale;
+            const int fx = clamp_floor(bx, W), fy = clamp_floor(by, H);
+#pragma unroll
+            for (int o = 0; o < 7; ++o) {
+                pd->ax[p][o] = (float)((bx + (double)(o - 3)) - (double)(fx + o - 3));
+                pd->ay[p][o] = (float)((by + (double)(o - 3)) - (double)(fy + o - 3));
+            }
+            pd->cx0[p] = fx - 3 - r0.x;
+            pd->cy0[p] = fy - 3 - r0.y;
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
-        named_barrier(bar_id, kGroupThreads);   // partials, gram copy and pixel data complete
-        if (active && gtid < NC) {
-            const int c = gtid;
-#pragma unroll
-            for (int p = 0; p < kPix; ++p) {
-                float sum = s_part[(0 * kPix + p) * kCells + c];
-                sum += s_part[(1 * kPix + p) * kCells + c];
-                sum += s_part[(2 * kPix + p) * kCells + c];
-                sum += s_part[(3 * kPix + p) * kCells + c];
-                s_dots[p * kCells + c] = sum;
-            }
-        }
-        named_barrier(bar_id, kGroupThreads);  // dots complete; s_part free for the next tile
-        if (active && gtid < 2 * kPix * 7) {
-            // thread -> (pixel p, row alpha, half of the 7 beta offsets)
-            const int pair = gtid >> 1, half = gtid & 1;
-            const int p = (pair * 37) >> 8, alpha = pair - 7 * p;  // pair / 7 for pair < 63
-            const float ay = pd->ay[p][alpha];
-            const int row = (pd->cy0[p] + alpha) * TW + pd->cx0[p];
-            const float* d = s_dots + p * kCells;
-            float* out = a.out + ((size_t)e * 2 + level) * kPix * 49 + p * 49 + alpha * 7;
-            const int b0 = half ? 4 : 0, b1 = half ? 7 : 4;
-            const bool far_p = (far >> p) & 1;  // window entirely outside the grid
-            for (int beta = b0; beta < b1; ++beta) {
-                if (far_p) {
-                    out[beta] = 0.f;
-                    continue;
-                }
-                const float ax = pd->ax[p][beta];
-                const int c00 = row + beta;
+        float* out = a.out + ((size_t)e * 2 + level) * kOut;
+        for (int o = lane; o < kOut; o += 32) {
+            const int p = o / 49, rem = o - 49 * p;
+            const int alpha = rem / 7, beta = rem - 7 * alpha;
+            float res = 0.f;
+            if (!((far >> p) & 1)) {  // far pixels: every tap is zero padding
+                const float ax = pd->ax[p][beta], ay = pd->ay[p][alpha];
+                const int gy = pd->cy0[p] + alpha, gx = pd->cx0[p] + beta;
+                const float* d = dots + p * kCells + gy * kBox + gx;
+                const float* g0 = gram + gy * kGramW + gx + (r0.x & 3);  // planes: |f|^2, right, down, diag, anti
+                const float* g1 = g0 + kGramPlane;
+                const float* g2 = g1 + kGramPlane;
+                const float* g3 = g2 + kGramPlane;
+                const float* g4 = g3 + kGramPlane;
                 const float w00 = (1.f - ax) * (1.f - ay), w10 = ax * (1.f - ay);
                 const float w01 = (1.f - ax) * ay, w11 = ax * ay;
-                float dot = w00 * d[c00];
-                dot = fmaf(w10, d[c00 + 1], dot);
-                dot = fmaf(w01, d[c00 + TW], dot);
-                dot = fmaf(w11, d[c00 + TW + 1], dot);
-                const float* g00 = s_gram + 5 * c00;
-                const float* g10 = g00 + 5;
-                const float* g01 = g00 + 5 * TW;
-                const float* g11 = g01 + 5;
-                // |f(x)|^2 = sum_t sum_t' w_t w_t' <f_t, f_t'> (Gram record: |f|^2, right, down, diag, anti)
-                float n2 = w00 * w00 * g00[0];
-                n2 = fmaf(w10 * w10, g10[0], n2);
-                n2 = fmaf(w01 * w01, g01[0], n2);
-                n2 = fmaf(w11 * w11, g11[0], n2);
-                float cross = w00 * w10 * g00[1];
-                cross = fmaf(w01 * w11, g01[1], cross);
-                cross = fmaf(w00 * w01, g00[2], cross);
-                cross = fmaf(w10 * w11, g10[2], cross);
-                cross = fmaf(w00 * w11, g00[3], cross);
-                cross = fmaf(w10 * w01, g00[4], cross);
+                float dot = w00 * d[0];
+                dot = fmaf(w10, d[1], dot);
+                dot = fmaf(w01, d[kBox], dot);
+                dot = fmaf(w11, d[kBox + 1], dot);
+                // |f(x)|^2 = sum_t sum_t' w_t w_t' <f_t, f_t'>
+                float n2 = w00 * w00 * g0[0];
+                n2 = fmaf(w10 * w10, g0[1], n2);
+                n2 = fmaf(w01 * w01, g0[kGramW], n2);
+                n2 = fmaf(w11 * w11, g0[kGramW + 1], n2);
+                float cross = w00 * w10 * g1[0];
+                cross = fmaf(w01 * w11, g1[kGramW], cross);
+                cross = fmaf(w00 * w01, g2[0], cross);
+                cross = fmaf(w10 * w11, g2[1], cross);
+                cross = fmaf(w00 * w11, g3[0], cross);
+                cross = fmaf(w10 * w01, g4[0], cross);
                 n2 = fmaf(2.f, cross, n2);
-                out[beta] = n2 > 1e-12f ? dot * rsqrtf(n2) : 0.f;  // correlation.cpp:22
+                res = n2 > 1e-12f ? dot * rsqrtf(n2) : 0.f;  // correlation.cpp:22
             }
+            out[o] = res;
         }
+        __syncwarp();  // dots / pixel data are rewritten by the next tile
     }
 }
 
@@ -448,7 +438,7 @@ cudaError_t launch_corr_tma(const CorrTmaParams& p, const CUtensorMap* maps, int
     if (err != cudaSuccess) return err;
     int grid = num_sms;
     if (grid > p.n_edges) grid = p.n_edges;
-    corr_tma_kernel<<<grid, kThreads, kSmemBytes, stream>>>(maps[0], maps[1], maps[2], maps[3], p);
+    corr_tma_kernel<<<grid, kThreads, kSmemBytes, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], p);
     return cudaGetLastError();
 }
 

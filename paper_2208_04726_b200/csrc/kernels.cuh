@@ -59,15 +59,21 @@ struct CorrTmaParams {
     const double* K = nullptr;
     int w0 = 0, h0 = 0, w1 = 0, h1 = 0;
     const float* patch_feats = nullptr;  // [P][2][9][128]
+    int n_patches = 0;
     float* out = nullptr;
     double* coords = nullptr;     // scratch [E][9][2]
-    int* meta = nullptr;          // scratch [E][2][4]
+    int* meta = nullptr;          // scratch [E][2][8] tile records, in processing-position order
     int* overflow = nullptr;      // scratch [2E]
     int* overflow_count = nullptr;
     int* status = nullptr;
 };
 int corr_tma_smem_bytes();
-// maps: feat0, feat1, gram0, gram1
+// Frame-store layouts the TMA kernel reads (encoded by the host):
+//   feat{0,1}: [slot][H][W][128] f32, box {16 ch, 9, 9, 1}, 64B swizzle
+//   gram{0,1}: [slot][8 planes][H][W] f32 (planes 0..4 used), box {12, 9, 5, 1}
+//   patch:     [P * 2 * 9][128] f32, box {16 ch, 9 rows}
+constexpr int kCorrMetaInts = 8;
+// maps: feat0, feat1, gram0, gram1, patch
 cudaError_t launch_corr_tma(const CorrTmaParams& p, const CUtensorMap* maps, int num_sms, cudaStream_t stream);
 cudaError_t launch_gram(const float* feat, float* gram, int W, int H, int D, int num_sms, cudaStream_t stream);
 
