@@ -82,41 +82,44 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n"
         ".reg .pred P;\n"
         "WAIT_%=:\n"
         "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
         "@!P bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
+        "}\n" ::"r"(bar),
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
-                                            uint64_t* bar) {
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint32_t bar) {
     asm volatile(
         "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
-        "%5}], [%6];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        "%5}], [%6];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
         : "memory");
 }
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-        "[%4];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        "[%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
         : "memory");
 }
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
                  : "memory");
+}
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
 }
 
 // reproject_patch of pixel `pix` of edge e (camera.cpp:47-71)
@@ -143,16 +146,6 @@ __device__ inline void edge_pixel(const CorrTmaParams& a, int e, int pix, double
 __device__ __forceinline__ int clamp_floor(double b, int extent) {
     return (int)floor(fmin(fmax(b, -16.0), (double)extent + 16.0));
 }
-
-// Per-pixel data of one tile: fractional bilinear weights per offset (exact
-// x - floor(x) in FP64, stored FP32) and the pixel's window origin in the tile.
-struct PixData {
-    float ax[kPix][7];
-    float ay[kPix][7];
-    int cx0[kPix];
-    int cy0[kPix];
-};
-static_assert(sizeof(PixData) <= 640, "PixData");
 
 __global__ void __launch_bounds__(kThreads, 1)
     corr_tma_kernel(const __grid_constant__ CUtensorMap feat0, const __grid_constant__ CUtensorMap feat1,
@@ -227,7 +220,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     // ================= per-warp pipeline =================
     unsigned char* wb = smem + warp * kWarpBytes;
-    uint64_t* bars = full + warp * kStages;
+    const uint32_t wbu = smem_u32(wb);                    // shared-window addresses, computed once
+    const uint32_t baru = smem_u32(full + warp * kStages);  // stage s barrier: baru + 8 * s
 
     // issue cursor (warp-uniform): pending tile + its record, current tile, chunk
     int pend = 0;
@@ -246,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int4 ir0 = make_int4(0, 0, 0, 0), ir1 = make_int4(0, 0, 0, 0);
     int ichunk = kChunks;  // chunks of the current issue tile already issued
     bool idone = false;
-    int qi = 0, hi = 0;    // chunks issued, tiles issued
+    int is = 0, hi = 0;    // next stage to fill, tiles issued
     auto issue_one = [&]() {
         if (idone) return;
         while (ichunk == kChunks) {  // advance to the next tile that needs the pipeline
@@ -266,30 +260,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int o = lane; o < kOut; o += 32) out[o] = 0.f;
             }
         }
-        const int s = qi % kStages;
-        unsigned char* st = wb + s * kStageBytes;
         if (lane == 0) {
             const int level = ir1.z;
+            const uint32_t bar = baru + 8 * is;
+            const uint32_t st = wbu + is * kStageBytes;
             if (ichunk == 0) {
                 const int hb = hi & 1;
                 int4* rec = reinterpret_cast<int4*>(wb + kMetaOff + 32 * hb);
                 rec[0] = ir0;
                 rec[1] = ir1;
-                unsigned char* hd = wb + kHeaderOff + hb * kHeaderBytes;
-                mbar_expect_tx(&bars[s], kChunkTx + kHeaderTx);
+                const uint32_t hd = wbu + kHeaderOff + hb * kHeaderBytes;
+                mbar_expect_tx(bar, kChunkTx + kHeaderTx);
                 // TMA needs a 16-byte aligned start in the innermost (x) dimension: start at
                 // floor4(x0); the 12-wide box still covers x0 .. x0 + 8
-                tma_load_4d(hd, level ? &gram1 : &gram0, ir0.x & ~3, ir0.y, 0, ir0.w, &bars[s]);
-                bulk_load(hd + kGramBytes, a.coords + (size_t)ir1.y * 18, kCoordBytes, &bars[s]);
+                tma_load_4d(hd, level ? &gram1 : &gram0, ir0.x & ~3, ir0.y, 0, ir0.w, bar);
+                bulk_load(hd + kGramBytes, a.coords + (size_t)ir1.y * 18, kCoordBytes, bar);
             } else {
-                mbar_expect_tx(&bars[s], kChunkTx);
+                mbar_expect_tx(bar, kChunkTx);
             }
-            tma_load_4d(st, level ? &feat1 : &feat0, ichunk * kChunkCh, ir0.x, ir0.y, ir0.w, &bars[s]);
-            tma_load_2d(st + kChunkGOff, &patch, ichunk * kChunkCh, ir1.x, &bars[s]);
+            tma_load_4d(st, level ? &feat1 : &feat0, ichunk * kChunkCh, ir0.x, ir0.y, ir0.w, bar);
+            tma_load_2d(st + kChunkGOff, &patch, ichunk * kChunkCh, ir1.x, bar);
         }
         if (ichunk == 0) ++hi;
         ++ichunk;
-        ++qi;
+        is = is == kStages - 1 ? 0 : is + 1;
     };
     for (int k = 0; k < kStages; ++k) issue_one();
     __syncwarp();
@@ -302,22 +296,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         roff[k] = r * 64;
     }
     float* dots = reinterpret_cast<float*>(wb + kDotsOff);
-    PixData* pd = reinterpret_cast<PixData*>(wb + kPixOff);
-    int qc = 0;
+    int cs = 0;          // stage being consumed
+    uint32_t cph = 0;    // its barrier phase parity
     for (int hc = 0; hc < hi; ++hc) {
-        float acc[3][kPix];
+        // (even, odd)-channel sums per (cell, pixel): packed FP32x2 FMAs (FFMA2)
+        float2 acc[3][kPix];
 #pragma unroll
         for (int k = 0; k < 3; ++k)
 #pragma unroll
-            for (int p = 0; p < kPix; ++p) acc[k][p] = 0.f;
-        for (int c = 0; c < kChunks; ++c, ++qc) {
-            const int s = qc % kStages;
-            mbar_wait(&bars[s], (uint32_t)((qc / kStages) & 1));
-            const unsigned char* st = wb + s * kStageBytes;
+            for (int p = 0; p < kPix; ++p) acc[k][p] = make_float2(0.f, 0.f);
+        for (int c = 0; c < kChunks; ++c) {
+            mbar_wait(baru + 8 * cs, cph);
+            const unsigned char* st = wb + cs * kStageBytes;
             const float* g = reinterpret_cast<const float*>(st + kChunkGOff);
-            // per-chunk partial sums, then one add into the tile total: 16 + 8 term
-            // chains instead of one 128-term chain (FP32 error well inside 1e-4)
-            float part[3][kPix];
+            // per-chunk partial sums, then one add into the tile total: short chains
+            // (8 + 8 terms per component) keep the FP32 error far inside 1e-4
+            float2 part[3][kPix];
 #pragma unroll
             for (int u = 0; u < kChunkCh / 4; ++u) {
                 float4 v[3], gv[kPix];
@@ -332,99 +326,94 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int k = 0; k < 3; ++k)
 #pragma unroll
+                    for (int p = 0; p < kPix; ++p) {
+                        const float2 va = make_float2(v[k].x, v[k].y), ga = make_float2(gv[p].x, gv[p].y);
+                        part[k][p] = u == 0 ? __fmul2_rn(va, ga) : __ffma2_rn(va, ga, part[k][p]);
+                    }
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+#pragma unroll
                     for (int p = 0; p < kPix; ++p)
-                        part[k][p] = u == 0 ? v[k].x * gv[p].x : fmaf(v[k].x, gv[p].x, part[k][p]);
-#pragma unroll
-                for (int k = 0; k < 3; ++k)
-#pragma unroll
-                    for (int p = 0; p < kPix; ++p) part[k][p] = fmaf(v[k].y, gv[p].y, part[k][p]);
-#pragma unroll
-                for (int k = 0; k < 3; ++k)
-#pragma unroll
-                    for (int p = 0; p < kPix; ++p) part[k][p] = fmaf(v[k].z, gv[p].z, part[k][p]);
-#pragma unroll
-                for (int k = 0; k < 3; ++k)
-#pragma unroll
-                    for (int p = 0; p < kPix; ++p) part[k][p] = fmaf(v[k].w, gv[p].w, part[k][p]);
+                        part[k][p] = __ffma2_rn(make_float2(v[k].z, v[k].w), make_float2(gv[p].z, gv[p].w), part[k][p]);
             }
 #pragma unroll
             for (int k = 0; k < 3; ++k)
 #pragma unroll
-                for (int p = 0; p < kPix; ++p) acc[k][p] += part[k][p];
-            __syncwarp();  // every lane is done with stage s
+                for (int p = 0; p < kPix; ++p) acc[k][p] = __fadd2_rn(acc[k][p], part[k][p]);
+            __syncwarp();  // every lane is done with this stage: refill it
+            if (++cs == kStages) {
+                cs = 0;
+                cph ^= 1;
+            }
             issue_one();
         }
 
-        // ---- epilogue: dots -> shared, per-pixel bilinear data, 441 outputs ----
+        // ---- epilogue ----
         const int hb = hc & 1;
         const int4 r0 = *reinterpret_cast<const int4*>(wb + kMetaOff + 32 * hb);
         const int4 r1 = *reinterpret_cast<const int4*>(wb + kMetaOff + 32 * hb + 16);
         const unsigned char* hd = wb + kHeaderOff + hb * kHeaderBytes;
-        const float* gram = reinterpret_cast<const float*>(hd);
+        const float* gram = reinterpret_cast<const float*>(hd) + (r0.x & 3);  // box starts at floor4(x0)
         const double* tc = reinterpret_cast<const double*>(hd + kGramBytes);
         const int e = r1.y, level = r1.z, far = r0.z >> 8;
         if (lane < 27) {
 #pragma unroll
             for (int k = 0; k < 3; ++k)
 #pragma unroll
-                for (int p = 0; p < kPix; ++p) dots[p * kCells + lane + 27 * k] = acc[k][p];
-        }
-        // per-pixel bilinear data (features.cpp:10-13 arithmetic): lanes 27..31 take
-        // pixels 0..4, lanes 0..3 pixels 5..8
-        const int p_pix = lane >= 27 ? lane - 27 : (lane < 4 ? 5 + lane : -1);
-        if (p_pix >= 0) {
-            const int p = p_pix;
-            const double scale = level ? 16.0 : 4.0;
-            const int W = level ? a.w1 : a.w0, H = level ? a.h1 : a.h0;
-            const double bx = tc[2 * p] / scale;
-            const double by = tc[2 * p + 1] / scale;
-            const int fx = clamp_floor(bx, W), fy = clamp_floor(by, H);
-#pragma unroll
-            for (int o = 0; o < 7; ++o) {
-                pd->ax[p][o] = (float)((bx + (double)(o - 3)) - (double)(fx + o - 3));
-                pd->ay[p][o] = (float)((by + (double)(o - 3)) - (double)(fy + o - 3));
-            }
-            pd->cx0[p] = fx - 3 - r0.x;
-            pd->cy0[p] = fy - 3 - r0.y;
+                for (int p = 0; p < kPix; ++p) dots[p * kCells + lane + 27 * k] = acc[k][p].x + acc[k][p].y;
         }
         __syncwarp();
+        // Separable bilinear recombination (correlation.cpp:8-23 regrouped): lane owns
+        // the output column (pixel p, offset beta) and walks alpha = 0..6, carrying the
+        // x-interpolated row terms of row alpha + 1 into the next step:
+        //   fx(y)   = (1-ax) f[y][x] + ax f[y][x+1]
+        //   dot     = (1-ay) <g, fx(y)> + ay <g, fx(y+1)>
+        //   |f(x)|^2 = (1-ay)^2 |fx(y)|^2 + ay^2 |fx(y+1)|^2 + 2 ay (1-ay) <fx(y), fx(y+1)>
+        // with |fx|^2 and <fx(y), fx(y+1)> from the Gram records (|f|^2, right, down,
+        // diag, anti).  ax / ay are the reference's per-offset fractional parts (FP64).
+        const double scale = level ? 16.0 : 4.0;  // kFeatureStride (features.hpp:46)
+        const int W = level ? a.w1 : a.w0, H = level ? a.h1 : a.h0;
         float* out = a.out + ((size_t)e * 2 + level) * kOut;
-        for (int o = lane; o < kOut; o += 32) {
-            const int p = o / 49, rem = o - 49 * p;
-            const int alpha = rem / 7, beta = rem - 7 * alpha;
-            float res = 0.f;
-            if (!((far >> p) & 1)) {  // far pixels: every tap is zero padding
-                const float ax = pd->ax[p][beta], ay = pd->ay[p][alpha];
-                const int gy = pd->cy0[p] + alpha, gx = pd->cx0[p] + beta;
-                const float* d = dots + p * kCells + gy * kBox + gx;
-                const float* g0 = gram + gy * kGramW + gx + (r0.x & 3);  // planes: |f|^2, right, down, diag, anti
-                const float* g1 = g0 + kGramPlane;
-                const float* g2 = g1 + kGramPlane;
-                const float* g3 = g2 + kGramPlane;
-                const float* g4 = g3 + kGramPlane;
-                const float w00 = (1.f - ax) * (1.f - ay), w10 = ax * (1.f - ay);
-                const float w01 = (1.f - ax) * ay, w11 = ax * ay;
-                float dot = w00 * d[0];
-                dot = fmaf(w10, d[1], dot);
-                dot = fmaf(w01, d[kBox], dot);
-                dot = fmaf(w11, d[kBox + 1], dot);
-                // |f(x)|^2 = sum_t sum_t' w_t w_t' <f_t, f_t'>
-                float n2 = w00 * w00 * g0[0];
-                n2 = fmaf(w10 * w10, g0[1], n2);
-                n2 = fmaf(w01 * w01, g0[kGramW], n2);
-                n2 = fmaf(w11 * w11, g0[kGramW + 1], n2);
-                float cross = w00 * w10 * g1[0];
-                cross = fmaf(w01 * w11, g1[kGramW], cross);
-                cross = fmaf(w00 * w01, g2[0], cross);
-                cross = fmaf(w10 * w11, g2[1], cross);
-                cross = fmaf(w00 * w11, g3[0], cross);
-                cross = fmaf(w10 * w01, g4[0], cross);
-                n2 = fmaf(2.f, cross, n2);
-                res = n2 > 1e-12f ? dot * rsqrtf(n2) : 0.f;  // correlation.cpp:22
+#pragma unroll 1
+        for (int col = lane; col < kPix * 7; col += 32) {
+            const int p = (col * 37) >> 8, beta = col - 7 * p;  // col / 7 for col < 63
+            float* o = out + p * 49 + beta;
+            if ((far >> p) & 1) {  // every tap of this pixel is zero padding
+#pragma unroll
+                for (int alpha = 0; alpha < 7; ++alpha) o[alpha * 7] = 0.f;
+                continue;
             }
-            out[o] = res;
+            const double bx = tc[2 * p] / scale, by = tc[2 * p + 1] / scale;
+            const int fx = clamp_floor(bx, W), fy = clamp_floor(by, H);
+            const float ax = (float)((bx + (double)(beta - 3)) - (double)(fx + beta - 3));
+            const float bx0 = 1.f - ax;
+            const int cx = fx - 3 - r0.x + beta, cy = fy - 3 - r0.y;
+            const float* d = dots + p * kCells + cy * kBox + cx;
+            const float* G = gram + cy * kGramW + cx;
+            const float qa = bx0 * bx0, qb = ax * ax, qc = 2.f * ax * bx0, qd = ax * bx0;
+            // row terms of row y: <g, fx(y)>, |fx(y)|^2
+            float dA = fmaf(ax, d[1], bx0 * d[0]);
+            float nA = fmaf(qc, G[kGramPlane], fmaf(qb, G[1], qa * G[0]));
+#pragma unroll
+            for (int alpha = 0; alpha < 7; ++alpha) {
+                const float* dn = d + (alpha + 1) * kBox;
+                const float* Gn = G + (alpha + 1) * kGramW;
+                const float* Gc = G + alpha * kGramW;
+                const float dB = fmaf(ax, dn[1], bx0 * dn[0]);
+                const float nB = fmaf(qc, Gn[kGramPlane], fmaf(qb, Gn[1], qa * Gn[0]));
+                // <fx(y), fx(y+1)> = (1-ax)^2 down[x] + ax^2 down[x+1] + ax(1-ax) (diag[x] + anti[x])
+                const float cr = fmaf(qd, Gc[3 * kGramPlane] + Gc[4 * kGramPlane],
+                                      fmaf(qb, Gc[2 * kGramPlane + 1], qa * Gc[2 * kGramPlane]));
+                const float ay = (float)((by + (double)(alpha - 3)) - (double)(fy + alpha - 3));
+                const float by0 = 1.f - ay;
+                const float dot = fmaf(ay, dB, by0 * dA);
+                const float n2 = fmaf(2.f * ay * by0, cr, fmaf(ay * ay, nB, by0 * by0 * nA));
+                o[alpha * 7] = n2 > 1e-12f ? dot * rsqrt_approx(n2) : 0.f;  // correlation.cpp:22
+                dA = dB;
+                nA = nB;
+            }
         }
-        __syncwarp();  // dots / pixel data are rewritten by the next tile
+        __syncwarp();  // dots are rewritten by the next tile
     }
 }
 
