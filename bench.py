@@ -47,25 +47,63 @@ def load_peaks():
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons sampled every 5 ms (NVML) during the timed
+    region; nvidia-smi -lms 50 when NVML is unavailable."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
 
     def __init__(self, device: int):
         self.device = device
+        self.rows = []
+        self.stop_ev = threading.Event()
+        self.thread = None
         self.proc = None
         self.path = None
 
+    def _nvml_loop(self, nv, h):
+        while not self.stop_ev.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((float(sm), int(r)))
+            except Exception:
+                pass
+            self.stop_ev.wait(0.005)
+
     def start(self):
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.device]) if vis else self.device
+            h = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.thread = None
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
+        fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={fields}", "--format=csv,noheader,nounits",
                  "-lms", "50"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.proc = None
 
     def stop(self):
+        if self.thread is not None:
+            self.stop_ev.set()
+            self.thread.join()
+            if not self.rows:
+                return None
+            reasons = sorted({n for _, r in self.rows for n, bit in self.REASONS.items() if r & bit})
+            return {"sm_mhz": statistics.median(sm for sm, _ in self.rows), "sm_max_mhz": self.max_mhz,
+                    "reasons": reasons, "samples": len(self.rows), "source": "nvml 5 ms"}
         if self.proc is None:
             return None
         self.proc.terminate()
@@ -84,7 +122,7 @@ class ClockSampler:
         reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() in ("active", "1")})
         sm = [float(r[0]) for r in rows]
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
-                "samples": len(rows)}
+                "samples": len(rows), "source": "nvidia-smi 50 ms"}
 
 
 # ---------------------------------------------------------------- workload
@@ -317,7 +355,7 @@ def run_ours(args, rank, world, local_rank):
                    "l2": "flushed between steps (256 MiB write, outside the timed events)"},
         "corr_ms": corr_ms_max, "ba_ms": ba_ms_max,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": traffic, "kernel": "corr_kernel", "peak_kind": peak_kind,
+                     "traffic": traffic, "kernel": "corr_tma_kernel", "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": total_b},
         "e2e": {"value": E * world / (e2e["ms"] * 1e-3), "unit": "edge-iterations/s",
                 "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"], "ms_per_step": e2e["ms"]},
@@ -369,7 +407,7 @@ def run_e2e(args, w, prob, ctx, stream, win):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])

@@ -75,7 +75,7 @@ struct pvo_ctx {
     bool maps_ok = false;
     const void* patch_map_base = nullptr;
     int patch_map_rows = 0;
-    DevBuf c_coords, c_meta, c_over, c_count, c_order;
+    DevBuf c_coords, c_meta, c_over, c_order;
     BABuffers ba;
     Window win;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -332,8 +332,8 @@ bool encode_patch_map(pvo_ctx* ctx, const float* base, int n_patches) {
 }
 
 // Correlation of a batch of edges against the frame store: the TMA kernel for
-// D = 128 followed by the generic kernel on its overflow items, or the generic
-// kernel alone.  `t` carries the inputs; scratch is filled in here.
+// D = 128 (it splits wide tiles into sub-tiles itself), or the generic kernel
+// for other channel counts.  `t` carries the inputs; scratch is filled in here.
 void run_corr(pvo_ctx* ctx, pvo_dev::CorrTmaParams t) {
     if (t.n_edges <= 0) return;
     if (ctx->maps_ok && encode_patch_map(ctx, t.patch_feats, t.n_patches)) {
@@ -343,34 +343,11 @@ void run_corr(pvo_ctx* ctx, pvo_dev::CorrTmaParams t) {
         t.h1 = ctx->h1;
         t.coords = ctx->c_coords.as<double>((size_t)t.n_edges * 18);
         t.meta = ctx->c_meta.as<int>((size_t)t.n_edges * 2 * pvo_dev::kCorrMetaInts);
-        t.overflow = ctx->c_over.as<int>((size_t)t.n_edges * 2);
-        t.overflow_count = ctx->c_count.as<int>(1);
+        const int grid = pvo_dev::corr_tma_grid(t.n_edges, ctx->num_sms);
+        t.extra_cap = pvo_dev::corr_tma_extra_cap(t.n_edges, grid);
+        t.extra = ctx->c_over.as<int>((size_t)grid * t.extra_cap * pvo_dev::kCorrMetaInts);
         t.status = ctx->d_status;
-        cuda_check(cudaMemsetAsync(t.overflow_count, 0, sizeof(int), ctx->stream), "memset");
         cuda_check(pvo_dev::launch_corr_tma(t, ctx->maps, ctx->num_sms, ctx->stream), "corr_tma kernel");
-        ctx->launches += 1;
-        pvo_dev::CorrParams cp;
-        cp.n_edges = t.n_edges;
-        cp.channels = ctx->C;
-        cp.e_patch = t.e_patch;
-        cp.e_pose = t.e_pose;
-        cp.e_slot = t.e_slot;
-        cp.pose_slot = t.pose_slot;
-        cp.coords = t.coords;
-        cp.feat0 = static_cast<const float*>(ctx->feat0.p);
-        cp.feat1 = static_cast<const float*>(ctx->feat1.p);
-        cp.gram0 = static_cast<const float*>(ctx->gram0.p);
-        cp.gram1 = static_cast<const float*>(ctx->gram1.p);
-        cp.w0 = ctx->w0;
-        cp.h0 = ctx->h0;
-        cp.w1 = ctx->w1;
-        cp.h1 = ctx->h1;
-        cp.patch_feats = t.patch_feats;
-        cp.out = t.out;
-        cp.status = ctx->d_status;
-        cp.items = t.overflow;
-        cp.items_count = t.overflow_count;
-        cuda_check(pvo_dev::launch_corr_items(cp, ctx->num_sms, ctx->stream), "corr overflow kernel");
         ctx->launches += 1;
         return;
     }

@@ -92,14 +92,10 @@ __global__ void __launch_bounds__(kThreads) corr_kernel(CorrParams a) {
     __shared__ double s_xy[2 * kPix];
     __shared__ int s_bad;
 
-    // Work items: one edge (both levels) per CTA, or — overflow mode — a
-    // device-side list of (edge, level) items left over by corr_tma.cu.
-    const int n_items = a.items ? *a.items_count : a.n_edges;
-    const int item_stride = a.items ? gridDim.x : a.n_edges;
-    for (int item = blockIdx.x; item < n_items; item += item_stride) {
-    const int e = a.items ? (a.items[item] >> 1) : item;
-    const int lv_begin = a.items ? (a.items[item] & 1) : 0;
-    const int lv_end = a.items ? lv_begin + 1 : 2;
+    // one edge (both levels) per CTA
+    for (int item = blockIdx.x; item < a.n_edges; item += gridDim.x) {
+    const int e = item;
+    const int lv_begin = 0, lv_end = 2;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int D = a.channels;
@@ -359,14 +355,6 @@ cudaError_t launch_corr(const CorrParams& p, cudaStream_t stream) {
     cudaError_t err = cudaFuncSetAttribute(corr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
     corr_kernel<<<p.n_edges, kThreads, smem, stream>>>(p);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_corr_items(const CorrParams& p, int num_sms, cudaStream_t stream) {
-    const int smem = corr_smem_bytes(p.channels);
-    cudaError_t err = cudaFuncSetAttribute(corr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (err != cudaSuccess) return err;
-    corr_kernel<<<num_sms * 2, kThreads, smem, stream>>>(p);
     return cudaGetLastError();
 }
 

@@ -21,13 +21,20 @@
 //   * FP32 FMA dot products in fixed channel order (deterministic); output
 //     recombination in FP32 with the bilinear weights' fractional parts taken
 //     exactly in FP64 (x - floor(x)) as the reference does; coalesced stores.
-// (edge, level) tiles whose pixel windows do not fit one 9x9 tile (extreme
-// zoom) are diverted to an overflow list that the generic kernel (corr.cu)
-// finishes; tiles whose every tap is zero padding are zero-filled directly.
+//   * tiles whose 9 pixel windows share one 8x8 cell window ("narrow": ~half
+//     of all tiles, most level-1 tiles) run a 2-cells-per-lane variant (64
+//     cells over 32 lanes) instead of 3 cells over 27 lanes: 1/3 fewer FMAs.
+// (edge, level) tiles whose pixel windows do not fit one 9x9 box (strong
+// zoom / wide spread) are split into pixel groups that each fit a box: the
+// first group takes the tile's slot, the others are appended to a per-CTA
+// extra list that the CTA's warps drain after their regular tiles (each
+// sub-tile writes only its member pixels).  Tiles whose every tap is zero
+// padding are zero-filled directly.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "geometry.cuh"
 #include "kernels.cuh"
@@ -68,8 +75,12 @@ static_assert(kGramBytes + kCoordBytes <= kHeaderBytes, "header");
 static_assert(kMetaOff + 64 <= kWarpBytes && kWarpBytes % 1024 == 0, "warp region");
 static_assert(kCorrMetaInts == 8, "tile record");
 
-// tile record kinds (TileRec.code bits 0..1); bits 8..16: far-pixel mask
-constexpr int kKindTma = 0, kKindOverflow = 1, kKindZero = 2, kKindBad = 3;
+// tile record kinds (TileRec.code bits 0..1); bit 2: narrow (8x8 window);
+// bits 8..16: far-pixel mask (zero-filled by this record); bits 17..25: member
+// pixels (outputs written by this record)
+constexpr int kKindTma = 0, kKindZero = 2, kKindBad = 3;
+constexpr int kNarrow = 4;
+constexpr int kPixMask = (1 << kPix) - 1;
 
 struct TileRec {
     int x0, y0, code, slot;  // window origin (cells), kind | far << 8, frame-store slot
@@ -155,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // 1024-aligned base, derived by offset so the compiler keeps the shared address space
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     __shared__ __align__(8) uint64_t full[kWarps * kStages];
-    __shared__ int s_next;
+    __shared__ int s_next, s_nextra;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int G = gridDim.x, b = blockIdx.x;
@@ -163,6 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int n_tiles = 2 * my_edges;
 
     // ---- prologue (all warps): coordinates and tile records of this CTA's edges ----
+    if (tid == 0) s_nextra = 0;
     for (int i = tid; i < my_edges * kPix; i += kThreads) {
         const int pos = b + (i / kPix) * G;
         const int e = a.order ? a.order[pos] : pos;
@@ -181,42 +193,90 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int level = i & 1;
         const double scale = level ? 16.0 : 4.0;  // kFeatureStride (features.hpp:46)
         const int W = level ? a.w1 : a.w0, H = level ? a.h1 : a.h0;
-        int xmin = 1 << 30, xmax = -(1 << 30), ymin = 1 << 30, ymax = -(1 << 30);
+        int fxs[kPix], fys[kPix];
         bool finite = true;
         int far = 0;  // pixels whose whole 8x8 tap window lies outside the grid: all 49 outputs are 0
+#pragma unroll
         for (int p = 0; p < kPix; ++p) {
             const double x = a.coords[(size_t)e * 18 + 2 * p], y = a.coords[(size_t)e * 18 + 2 * p + 1];
             finite = finite && isfinite(x) && isfinite(y);
-            const int fx = clamp_floor(x / scale, W), fy = clamp_floor(y / scale, H);
-            if (fx + 4 < 0 || fx - 3 >= W || fy + 4 < 0 || fy - 3 >= H) {
-                far |= 1 << p;
-                continue;
-            }
-            xmin = min(xmin, fx);
-            xmax = max(xmax, fx);
-            ymin = min(ymin, fy);
-            ymax = max(ymax, fy);
-        }
-        int kind = kKindTma;
-        if (!finite) {
-            atomicOr(a.status, 1 << kDevBadCoords);  // correlation.cpp:43-45
-            kind = kKindBad;
-        } else if (far == (1 << kPix) - 1) {
-            kind = kKindZero;  // every tap of every pixel is zero padding
-        } else if (xmax - xmin + 8 > kBox || ymax - ymin + 8 > kBox) {
-            const int slot = atomicAdd(a.overflow_count, 1);
-            a.overflow[slot] = 2 * e + level;
-            kind = kKindOverflow;
+            fxs[p] = clamp_floor(x / scale, W);
+            fys[p] = clamp_floor(y / scale, H);
+            if (fxs[p] + 4 < 0 || fxs[p] - 3 >= W || fys[p] + 4 < 0 || fys[p] - 3 >= H) far |= 1 << p;
         }
         const int fslot = a.e_slot ? a.e_slot[e] : a.pose_slot[a.e_pose[e]];
+        const int grow = (a.e_patch[e] * 2 + level) * kPix;
         int4* rec = reinterpret_cast<int4*>(a.meta) + 2 * ((size_t)2 * pos + level);
-        rec[0] = make_int4(xmin - 3, ymin - 3, kind | (far << 8), fslot);
-        rec[1] = make_int4((a.e_patch[e] * 2 + level) * kPix, e, level, 0);
+        if (!finite) {
+            atomicOr(a.status, 1 << kDevBadCoords);  // correlation.cpp:43-45
+            rec[0] = make_int4(0, 0, kKindBad, fslot);
+            rec[1] = make_int4(grow, e, level, 0);
+            continue;
+        }
+        if (far == kPixMask) {  // every tap of every pixel is zero padding
+            rec[0] = make_int4(0, 0, kKindZero | (far << 8), fslot);
+            rec[1] = make_int4(grow, e, level, 0);
+            continue;
+        }
+        // Pixel groups that each fit one 9x9 box: a box at origin (X0, Y0) holds the
+        // 8x8 window of pixel q iff fx_q - 3 in {X0, X0+1} and fy_q - 3 in {Y0, Y0+1}.
+        // Greedy: seed = lowest remaining pixel; of the 4 boxes containing its window
+        // take the one covering most remaining pixels.  Group 0 (usually the whole
+        // tile) takes the tile's slot and also zero-fills the far pixels.
+        int rest = kPixMask & ~far;
+        bool first = true;
+        while (rest) {
+            const int p0 = __ffs(rest) - 1;
+            int best = 0, bx = 0, by = 0;
+#pragma unroll
+            for (int cand = 0; cand < 4; ++cand) {
+                const int X0 = fxs[p0] - 3 - (cand & 1), Y0 = fys[p0] - 3 - (cand >> 1);
+                int m = 0;
+#pragma unroll
+                for (int q = 0; q < kPix; ++q) {
+                    const int dx = fxs[q] - 3 - X0, dy = fys[q] - 3 - Y0;
+                    if (((rest >> q) & 1) && (unsigned)dx <= 1u && (unsigned)dy <= 1u) m |= 1 << q;
+                }
+                if (__popc(m) > __popc(best)) {
+                    best = m;
+                    bx = X0;
+                    by = Y0;
+                }
+            }
+            // narrow: every member's window is the same 8x8 block -> origin = that block
+            int xl = 1 << 30, xh = -(1 << 30), yl = 1 << 30, yh = -(1 << 30);
+#pragma unroll
+            for (int q = 0; q < kPix; ++q)
+                if ((best >> q) & 1) {
+                    xl = min(xl, fxs[q]);
+                    xh = max(xh, fxs[q]);
+                    yl = min(yl, fys[q]);
+                    yh = max(yh, fys[q]);
+                }
+            int code = kKindTma | (best << 17);
+            if (xl == xh && yl == yh) {
+                code |= kNarrow;
+                bx = xl - 3;
+                by = yl - 3;
+            }
+            if (first) {
+                rec[0] = make_int4(bx, by, code | (far << 8), fslot);
+                rec[1] = make_int4(grow, e, level, 0);
+                first = false;
+            } else {
+                const int x = atomicAdd(&s_nextra, 1);
+                int4* xr = reinterpret_cast<int4*>(a.extra) + 2 * ((size_t)b * a.extra_cap + x);
+                xr[0] = make_int4(bx, by, code, fslot);
+                xr[1] = make_int4(grow, e, level, 0);
+            }
+            rest &= ~best;
+        }
     }
     if (tid < kWarps * kStages) mbar_init(&full[tid], 1);
     if (tid == 0) s_next = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
+    const int n_all = n_tiles + s_nextra;  // regular tiles, then this CTA's extra sub-tiles
 
     // ================= per-warp pipeline =================
     unsigned char* wb = smem + warp * kWarpBytes;
@@ -230,8 +290,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         int t = 0;
         if (lane == 0) t = atomicAdd(&s_next, 1);
         pend = __shfl_sync(0xffffffffu, t, 0);
-        if (pend < n_tiles) {
-            const int4* src = reinterpret_cast<const int4*>(a.meta) + 2 * ((size_t)2 * (b + (pend >> 1) * G) + (pend & 1));
+        if (pend < n_all) {
+            const int4* src = pend < n_tiles
+                                  ? reinterpret_cast<const int4*>(a.meta) + 2 * ((size_t)2 * (b + (pend >> 1) * G) + (pend & 1))
+                                  : reinterpret_cast<const int4*>(a.extra) + 2 * ((size_t)b * a.extra_cap + (pend - n_tiles));
             pr0 = __ldcg(src);
             pr1 = __ldcg(src + 1);
         }
@@ -244,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto issue_one = [&]() {
         if (idone) return;
         while (ichunk == kChunks) {  // advance to the next tile that needs the pipeline
-            if (pend >= n_tiles) {
+            if (pend >= n_all) {
                 idone = true;
                 return;
             }
@@ -288,21 +350,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int k = 0; k < kStages; ++k) issue_one();
     __syncwarp();
 
-    // lane -> its 3 cells (rows of the 9x9 box); lanes 27..31 compute throwaway rows
-    int roff[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const int r = lane + 27 * k;
-        roff[k] = r * 64;
-    }
     float* dots = reinterpret_cast<float*>(wb + kDotsOff);
     int cs = 0;          // stage being consumed
     uint32_t cph = 0;    // its barrier phase parity
-    for (int hc = 0; hc < hi; ++hc) {
-        // (even, odd)-channel sums per (cell, pixel): packed FP32x2 FMAs (FFMA2)
-        float2 acc[3][kPix];
+    // Dots <g_p, f_cell> of one tile, NC cells per lane: NC = 3 -> lanes 0..26 own
+    // rows lane, lane+27, lane+54 of the 9x9 box (lanes 27..31 compute throwaway rows);
+    // NC = 2 (narrow tile) -> lane owns cells (lane&7, lane>>3) and (lane&7, 4+(lane>>3))
+    // of the 8x8 window at the box origin.  Results go to dots[p][box row].
+    auto tile_dots = [&](auto nc_tag) {
+        constexpr int NC = decltype(nc_tag)::value;
+        int roff[NC];
 #pragma unroll
-        for (int k = 0; k < 3; ++k)
+        for (int k = 0; k < NC; ++k) {
+            const int r = NC == 3 ? lane + 27 * k : ((lane >> 3) + 4 * k) * kBox + (lane & 7);
+            roff[k] = r * 64;
+        }
+        // (even, odd)-channel sums per (cell, pixel): packed FP32x2 FMAs (FFMA2)
+        float2 acc[NC][kPix];
+#pragma unroll
+        for (int k = 0; k < NC; ++k)
 #pragma unroll
             for (int p = 0; p < kPix; ++p) acc[k][p] = make_float2(0.f, 0.f);
         for (int c = 0; c < kChunks; ++c) {
@@ -311,12 +377,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float* g = reinterpret_cast<const float*>(st + kChunkGOff);
             // per-chunk partial sums, then one add into the tile total: short chains
             // (8 + 8 terms per component) keep the FP32 error far inside 1e-4
-            float2 part[3][kPix];
+            float2 part[NC][kPix];
 #pragma unroll
             for (int u = 0; u < kChunkCh / 4; ++u) {
-                float4 v[3], gv[kPix];
+                float4 v[NC], gv[kPix];
 #pragma unroll
-                for (int k = 0; k < 3; ++k) {
+                for (int k = 0; k < NC; ++k) {
                     // 64B swizzle: 16-byte unit u of row r lives at unit u ^ ((r >> 1) & 3)
                     const int sw = (roff[k] >> 7) & 3;
                     v[k] = *reinterpret_cast<const float4*>(st + roff[k] + ((u ^ sw) << 4));
@@ -324,20 +390,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int p = 0; p < kPix; ++p) gv[p] = *reinterpret_cast<const float4*>(g + p * kChunkCh + 4 * u);
 #pragma unroll
-                for (int k = 0; k < 3; ++k)
+                for (int k = 0; k < NC; ++k)
 #pragma unroll
                     for (int p = 0; p < kPix; ++p) {
                         const float2 va = make_float2(v[k].x, v[k].y), ga = make_float2(gv[p].x, gv[p].y);
                         part[k][p] = u == 0 ? __fmul2_rn(va, ga) : __ffma2_rn(va, ga, part[k][p]);
                     }
 #pragma unroll
-                for (int k = 0; k < 3; ++k)
+                for (int k = 0; k < NC; ++k)
 #pragma unroll
                     for (int p = 0; p < kPix; ++p)
                         part[k][p] = __ffma2_rn(make_float2(v[k].z, v[k].w), make_float2(gv[p].z, gv[p].w), part[k][p]);
             }
 #pragma unroll
-            for (int k = 0; k < 3; ++k)
+            for (int k = 0; k < NC; ++k)
 #pragma unroll
                 for (int p = 0; p < kPix; ++p) acc[k][p] = __fadd2_rn(acc[k][p], part[k][p]);
             __syncwarp();  // every lane is done with this stage: refill it
@@ -347,21 +413,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             issue_one();
         }
-
-        // ---- epilogue ----
+        if (NC == 2 || lane < 27) {
+#pragma unroll
+            for (int k = 0; k < NC; ++k)
+#pragma unroll
+                for (int p = 0; p < kPix; ++p) dots[p * kCells + (roff[k] >> 6)] = acc[k][p].x + acc[k][p].y;
+        }
+    };
+    for (int hc = 0; hc < hi; ++hc) {
         const int hb = hc & 1;
         const int4 r0 = *reinterpret_cast<const int4*>(wb + kMetaOff + 32 * hb);
         const int4 r1 = *reinterpret_cast<const int4*>(wb + kMetaOff + 32 * hb + 16);
+        if (r0.z & kNarrow)
+            tile_dots(std::integral_constant<int, 2>{});
+        else
+            tile_dots(std::integral_constant<int, 3>{});
+
+        // ---- epilogue ----
         const unsigned char* hd = wb + kHeaderOff + hb * kHeaderBytes;
         const float* gram = reinterpret_cast<const float*>(hd) + (r0.x & 3);  // box starts at floor4(x0)
         const double* tc = reinterpret_cast<const double*>(hd + kGramBytes);
-        const int e = r1.y, level = r1.z, far = r0.z >> 8;
-        if (lane < 27) {
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-#pragma unroll
-                for (int p = 0; p < kPix; ++p) dots[p * kCells + lane + 27 * k] = acc[k][p].x + acc[k][p].y;
-        }
+        const int e = r1.y, level = r1.z, far = (r0.z >> 8) & kPixMask, member = (r0.z >> 17) & kPixMask;
         __syncwarp();
         // Separable bilinear recombination (correlation.cpp:8-23 regrouped): lane owns
         // the output column (pixel p, offset beta) and walks alpha = 0..6, carrying the
@@ -378,10 +450,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int col = lane; col < kPix * 7; col += 32) {
             const int p = (col * 37) >> 8, beta = col - 7 * p;  // col / 7 for col < 63
             float* o = out + p * 49 + beta;
-            if ((far >> p) & 1) {  // every tap of this pixel is zero padding
+            if (!((member >> p) & 1)) {
+                if ((far >> p) & 1) {  // every tap of this pixel is zero padding
 #pragma unroll
-                for (int alpha = 0; alpha < 7; ++alpha) o[alpha * 7] = 0.f;
-                continue;
+                    for (int alpha = 0; alpha < 7; ++alpha) o[alpha * 7] = 0.f;
+                }
+                continue;  // else: another sub-tile of this (edge, level) writes it
             }
             const double bx = tc[2 * p] / scale, by = tc[2 * p + 1] / scale;
             const int fx = clamp_floor(bx, W), fy = clamp_floor(by, H);
@@ -420,13 +494,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace
 
 int corr_tma_smem_bytes() { return kSmemBytes; }
+int corr_tma_grid(int n_edges, int num_sms) { return n_edges < num_sms ? n_edges : num_sms; }
+// worst case: every pixel of every tile in its own box -> 8 extra sub-tiles per tile
+int corr_tma_extra_cap(int n_edges, int grid) { return grid > 0 ? 2 * (kPix - 1) * ((n_edges + grid - 1) / grid) : 0; }
 
 cudaError_t launch_corr_tma(const CorrTmaParams& p, const CUtensorMap* maps, int num_sms, cudaStream_t stream) {
     if (p.n_edges <= 0) return cudaSuccess;
     cudaError_t err = cudaFuncSetAttribute(corr_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     if (err != cudaSuccess) return err;
-    int grid = num_sms;
-    if (grid > p.n_edges) grid = p.n_edges;
+    const int grid = corr_tma_grid(p.n_edges, num_sms);
+    if (p.extra_cap < corr_tma_extra_cap(p.n_edges, grid)) return cudaErrorInvalidValue;
     corr_tma_kernel<<<grid, kThreads, kSmemBytes, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], p);
     return cudaGetLastError();
 }

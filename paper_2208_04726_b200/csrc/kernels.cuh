@@ -33,14 +33,10 @@ struct CorrParams {
     const float* patch_feats = nullptr;  // [P][2][9][C]
     float* out = nullptr;                // [E][2][9][49]
     int* status = nullptr;               // device status word (1 = non-finite coords)
-    // overflow mode: (edge << 1 | level) items, count on the device
-    const int* items = nullptr;
-    const int* items_count = nullptr;
 };
 
 int corr_smem_bytes(int channels);
 cudaError_t launch_corr(const CorrParams& p, cudaStream_t stream);
-cudaError_t launch_corr_items(const CorrParams& p, int num_sms, cudaStream_t stream);
 
 // K2 production path (corr_tma.cu): D = 128, TMA pipeline, persistent CTAs.
 struct CorrTmaParams {
@@ -63,8 +59,8 @@ struct CorrTmaParams {
     float* out = nullptr;
     double* coords = nullptr;     // scratch [E][9][2]
     int* meta = nullptr;          // scratch [E][2][8] tile records, in processing-position order
-    int* overflow = nullptr;      // scratch [2E]
-    int* overflow_count = nullptr;
+    int* extra = nullptr;         // scratch [grid][extra_cap][8]: extra sub-tile records per CTA
+    int extra_cap = 0;            // records per CTA (>= 8 per regular tile of the CTA)
     int* status = nullptr;
 };
 int corr_tma_smem_bytes();
@@ -74,6 +70,8 @@ int corr_tma_smem_bytes();
 //   patch:     [P * 2 * 9][128] f32, box {16 ch, 9 rows}
 constexpr int kCorrMetaInts = 8;
 // maps: feat0, feat1, gram0, gram1, patch
+int corr_tma_grid(int n_edges, int num_sms);
+int corr_tma_extra_cap(int n_edges, int grid);
 cudaError_t launch_corr_tma(const CorrTmaParams& p, const CUtensorMap* maps, int num_sms, cudaStream_t stream);
 cudaError_t launch_gram(const float* feat, float* gram, int W, int H, int D, int num_sms, cudaStream_t stream);
 

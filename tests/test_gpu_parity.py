@@ -166,6 +166,41 @@ def test_correlate_batch_c1_full(ctx, c1_workload):
     assert bad == 0
 
 
+def test_correlate_batch_wide_and_border_tiles(ctx, c1_workload):
+    """Tiles that do not fit one 9x9 box (split into pixel-group sub-tiles),
+    narrow 8x8 tiles, pixels partly / wholly outside the grid, and mixed far +
+    near pixels in one patch — every entry against the oracle."""
+    w = c1_workload
+    F = w.cfg["frames"]
+    H0, W0 = w.level0.shape[1:3]
+    ctx.frames_reserve(F, W0, H0, w.level1.shape[2], w.level1.shape[1], 128)
+    for f in range(F):
+        ctx.frames_upload(f, w.level0[f], w.level1[f])
+    rng = np.random.default_rng(11)
+    n = 600
+    cx = rng.uniform(-40, 4 * W0 + 40, n)
+    cy = rng.uniform(-40, 4 * H0 + 40, n)
+    spread = rng.choice([0.0, 1.0, 6.0, 30.0, 90.0, 400.0], n)  # pixel scatter (px, level-0 image coords)
+    coords = np.empty((n, 9, 2))
+    gx, gy = np.meshgrid(np.arange(3) - 1.0, np.arange(3) - 1.0)
+    for e in range(n):
+        if spread[e] == 0.0:  # an exact 3x3 grid (narrow at both levels mostly)
+            coords[e, :, 0] = cx[e] + gx.ravel()
+            coords[e, :, 1] = cy[e] + gy.ravel()
+        else:
+            coords[e, :, 0] = cx[e] + rng.uniform(-1, 1, 9) * spread[e]
+            coords[e, :, 1] = cy[e] + rng.uniform(-1, 1, 9) * spread[e]
+    P = 50
+    pf = w.patch_feats[:P]
+    e_patch = rng.integers(0, P, n).astype(np.int32)
+    slots = rng.integers(0, F, n).astype(np.int32)
+    out = pvo.correlate_batch(e_patch, slots, coords, pf, ctx=ctx)
+    ref = orc.correlate_batch(e_patch, slots, coords, pf, w.level0, w.level1, threads=THREADS)
+    bad = corr_violations(out, ref, _gnorm_for_batch(pf, e_patch))
+    print(f"wide/border corr: max abs err {np.abs(out.astype(np.float64) - ref).max():.3e}, violations {bad}")
+    assert bad == 0
+
+
 def test_window_corr_matches_explicit_coords(ctx, c1_workload):
     """The resident window reprojects on the device (K1 fused in K2): same volume."""
     w = c1_workload
