@@ -34,7 +34,7 @@ NVCC_FLAGS = [
     "-I",
     str(ROOT / "include"),
 ]
-SOURCES = ["corr.cu", "corr_tma.cu", "ba.cu", "capi.cu", "graph.cpp"]
+SOURCES = ["corr.cu", "corr_tma.cu", "ba.cu", "ba_large.cu", "capi.cu", "graph.cpp"]
 
 
 def nvcc() -> str:

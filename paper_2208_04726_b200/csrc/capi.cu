@@ -10,6 +10,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -32,12 +34,15 @@ struct BABuffers {
     DevBuf poses, free_slot, patch_src, px, py, depth, depth_slot, edge_begin, e_patch, e_pose, e_in, e_w, e_target,
         e_weight, cand_poses, cand_depth, patch_v, patch_h, patch_bd, partials, system, delta, norms, n_norms, dbg_h,
         dbg_b, K, status2, attempts, clocks;
+    // large-window path (ba_large.cu)
+    DevBuf g_begin, g_lo, g_nl, g_off, patch_group, g_part, g_res, A, A2, mats, cmats, u_res, ctrl;
     void release() {
         DevBuf* all[] = {&poses,    &free_slot,  &patch_src, &px,        &py,       &depth,    &depth_slot,
                          &edge_begin, &e_patch,  &e_pose,    &e_in,      &e_w,      &e_target, &e_weight,
                          &cand_poses, &cand_depth, &patch_v, &patch_h,   &patch_bd, &partials, &system,
                          &delta,    &norms,      &n_norms,   &dbg_h,     &dbg_b,    &K,        &status2,
-                         &attempts, &clocks};
+                         &attempts, &clocks,     &g_begin,   &g_lo,      &g_nl,     &g_off,    &patch_group,
+                         &g_part,   &g_res,      &A,  &A2,       &mats,      &cmats,    &u_res,    &ctrl};
         for (DevBuf* b : all) b->release();
     }
 };
@@ -47,7 +52,59 @@ struct Plan {
     int n_free_poses = 0, n_free_depths = 0;
     std::vector<int> free_slot, depth_slot, edge_begin, perm;  // perm: sorted edge -> input edge
     bool sorted = true;
+    // large pose systems (> 16 free poses or > 128 poses): multi-kernel path (ba_large.cu)
+    bool large = false;
+    std::vector<int> g_begin, g_lo, g_nl, patch_group;
+    std::vector<long long> g_off;
+    long long g_part_doubles = 0;
+    int max_nl = 0, bw = 0;
 };
+
+// Patch groups of the large path: runs of consecutive patches with one source
+// pose, cut to <= 64 patches; the window of a run = the free pose slots its
+// patches touch (source + edge targets).  The reduced system's half-bandwidth
+// is the widest window - 1 (patch_graph.cpp:79 keeps edges within the radius).
+void plan_groups(const HostProblem& pr, Plan& pl) {
+    constexpr int kGroupPatches = 64;
+    pl.g_begin.assign(1, 0);
+    pl.patch_group.assign(pr.n_patches, 0);
+    int k = 0;
+    while (k < pr.n_patches) {
+        int r1 = k;
+        while (r1 < pr.n_patches && pr.src[r1] == pr.src[k]) ++r1;
+        int lo = 1 << 30, hi = -1;
+        auto touch = [&](int pose) {
+            const int f = pl.free_slot[pose];
+            if (f >= 0) {
+                lo = std::min(lo, f);
+                hi = std::max(hi, f);
+            }
+        };
+        for (int q = k; q < r1; ++q) {
+            touch(pr.src[q]);
+            for (int i = pl.edge_begin[q]; i < pl.edge_begin[q + 1]; ++i) touch(pr.e_pose[pl.perm[i]]);
+        }
+        const int nposes = hi >= lo ? hi - lo + 1 : 0;
+        if (nposes > pvo_dev::kMaxLocalPoses) {
+            fail(PVO_UNSUPPORTED, "ba: a patch run touches " + std::to_string(nposes) + " free poses (max " +
+                                      std::to_string(pvo_dev::kMaxLocalPoses) + ")");
+        }
+        for (int c = k; c < r1; c += kGroupPatches) {
+            const int c1 = std::min(r1, c + kGroupPatches);
+            const int g = (int)pl.g_lo.size();
+            for (int q = c; q < c1; ++q) pl.patch_group[q] = g;
+            pl.g_begin.push_back(c1);
+            pl.g_lo.push_back(nposes ? lo : 0);
+            pl.g_nl.push_back(6 * nposes);
+            pl.g_off.push_back(pl.g_part_doubles);
+            const long long nl = 6 * nposes;
+            pl.g_part_doubles += nl * (nl + 1) / 2 + nl;
+            pl.max_nl = std::max(pl.max_nl, (int)nl);
+        }
+        k = r1;
+    }
+    pl.bw = pl.max_nl > 0 ? pl.max_nl - 1 : 0;
+}
 
 struct Window {
     bool loaded = false;
@@ -167,11 +224,10 @@ Plan make_plan(const HostProblem& pr, bool all_fixed) {
         fail(PVO_UNSUPPORTED, "ba: more than " + std::to_string(pvo_dev::ba_max_edges_per_patch()) +
                                   " edges on one patch");
     }
-    if (pl.n_free_poses > pvo_dev::ba_max_free_poses()) {
-        fail(PVO_UNSUPPORTED, "ba: more than " + std::to_string(pvo_dev::ba_max_free_poses()) +
-                                  " free poses in one window");
-    }
     if (pr.p != 3) fail(PVO_UNSUPPORTED, "ba: the kernels implement 3x3 patches");
+    pl.large = pl.n_free_poses > pvo_dev::ba_max_free_poses() || pr.n_poses > pvo_dev::ba_max_poses();
+    if (std::getenv("PVO_BA_LARGE")) pl.large = true;  // testing: force the multi-kernel path
+    if (pl.large) plan_groups(pr, pl);
     return pl;
 }
 
@@ -224,15 +280,21 @@ pvo_dev::BAParams stage_problem(pvo_ctx* ctx, const HostProblem& pr, const Plan&
     a.patch_v = B.patch_v.as<double>((size_t)pr.n_patches * std::max(np, 1));
     a.patch_h = B.patch_h.as<double>(pr.n_patches);
     a.patch_bd = B.patch_bd.as<double>(pr.n_patches);
-    if (pr.n_poses > pvo_dev::ba_max_poses()) {
-        fail(PVO_UNSUPPORTED, "ba: more than " + std::to_string(pvo_dev::ba_max_poses()) + " poses in one problem");
+    if (pl.large) {
+        upload(ctx, B.g_begin, pl.g_begin.data(), pl.g_begin.size());
+        upload(ctx, B.g_lo, pl.g_lo.data(), pl.g_lo.size());
+        upload(ctx, B.g_nl, pl.g_nl.data(), pl.g_nl.size());
+        upload(ctx, B.g_off, pl.g_off.data(), pl.g_off.size());
+        upload(ctx, B.patch_group, pl.patch_group.data(), pl.patch_group.size());
     }
     a.status2 = B.status2.as<int>(2);
     a.attempts = B.attempts.as<int>(1);
     a.phase_clocks = ctx->tracing ? B.clocks.as<long long>(128) : nullptr;
-    const int grid = pvo_dev::ba_grid_size(pr.n_patches, pl.n_free_poses, pr.n_poses, ctx->num_sms);
-    a.partials = B.partials.as<double>(pvo_dev::ba_partials_doubles(pl.n_free_poses, grid));
-    a.system = B.system.as<double>((size_t)np * (np + 1) / 2 + np + 1);
+    if (!pl.large) {
+        const int grid = pvo_dev::ba_grid_size(pr.n_patches, pl.n_free_poses, pr.n_poses, ctx->num_sms);
+        a.partials = B.partials.as<double>(pvo_dev::ba_partials_doubles(pl.n_free_poses, grid));
+        a.system = B.system.as<double>((size_t)np * (np + 1) / 2 + np + 1);
+    }
     a.delta = B.delta.as<double>(std::max(np, 1));
     a.residual_norms = B.norms.as<double>(2 + extra_norms);
     a.n_norms = B.n_norms.as<int>(1);
@@ -244,8 +306,58 @@ pvo_dev::BAParams stage_problem(pvo_ctx* ctx, const HostProblem& pr, const Plan&
     return a;
 }
 
-void launch_ba_checked(pvo_ctx* ctx, pvo_dev::BAParams& a) {
+// Large-window parameter block over the context's buffers (groups uploaded by stage_problem).
+pvo_dev::BALargeParams large_params(pvo_ctx* ctx, const pvo_dev::BAParams& a, const Plan& pl) {
+    BABuffers& B = ctx->ba;
+    pvo_dev::BALargeParams p;
+    p.a = a;
+    const int np = 6 * pl.n_free_poses;
+    p.a.patch_v = nullptr;
+    p.n_groups = (int)pl.g_lo.size();
+    p.g_begin = static_cast<const int*>(B.g_begin.p);
+    p.g_lo = static_cast<const int*>(B.g_lo.p);
+    p.g_nl = static_cast<const int*>(B.g_nl.p);
+    p.g_off = static_cast<const long long*>(B.g_off.p);
+    p.patch_group = static_cast<const int*>(B.patch_group.p);
+    p.max_nl = pl.max_nl;
+    p.bw = pl.bw;
+    p.g_part = B.g_part.as<double>((size_t)std::max<long long>(1, pl.g_part_doubles));
+    p.g_res = B.g_res.as<double>(2 * (size_t)std::max(1, p.n_groups));
+    p.patch_vl = B.patch_v.as<double>((size_t)a.n_patches * std::max(1, pl.max_nl));
+    p.A = B.A.as<double>((size_t)(np + 1) * (np + 1));
+    p.A2 = B.A2.as<double>((size_t)(np + 1) * (np + 1));
+    p.mats = B.mats.as<double>(12 * (size_t)a.n_poses);
+    p.cmats = B.cmats.as<double>(12 * (size_t)a.n_poses);
+    p.n_update_ctas = std::max(1, std::min(2 * ctx->num_sms, (a.n_patches + 7) / 8));
+    p.u_res = B.u_res.as<double>(2 * (size_t)p.n_update_ctas);
+    p.ctrl = B.ctrl.as<int>(4);
+    return p;
+}
+
+void launch_ba_checked(pvo_ctx* ctx, pvo_dev::BAParams& a, const Plan& pl) {
     cuda_check(cudaMemsetAsync(a.n_norms, 0, sizeof(int), ctx->stream), "memset");
+    if (pl.large) {
+        if (a.gn_step_mode) fail(PVO_UNSUPPORTED, "gauss_newton_step: pose systems beyond 16 free poses");
+        cuda_check(cudaMemsetAsync(a.attempts, 0, sizeof(int), ctx->stream), "memset");
+        pvo_dev::BALargeParams p = large_params(ctx, a, pl);
+        const char* dump = std::getenv("PVO_BA_LARGE_DUMP");
+        const int np = 6 * pl.n_free_poses;
+        if (dump) p.dbg_A = ctx->ba.dbg_h.as<double>((size_t)(np + 1) * (np + 1));
+        int n = 0;
+        cuda_check(pvo_dev::launch_ba_large(p, ctx->num_sms, ctx->stream, &n), "ba large kernels");
+        ctx->launches += n;
+        if (dump) {
+            std::vector<double> h((size_t)(np + 1) * (np + 1)), dl(np);
+            download(ctx, h.data(), p.dbg_A, h.size());
+            download(ctx, dl.data(), a.delta, dl.size());
+            sync(ctx);
+            FILE* f = std::fopen(dump, "wb");
+            std::fwrite(h.data(), 8, h.size(), f);
+            std::fwrite(dl.data(), 8, dl.size(), f);
+            std::fclose(f);
+        }
+        return;
+    }
     int grid = 0;
     cuda_check(pvo_dev::launch_ba(a, ctx->num_sms, ctx->stream, &grid), "ba kernel");
     ctx->launches += 1;
@@ -413,6 +525,7 @@ void run_ba(pvo_ctx* ctx, const HostProblem& pr, const BARun& run) {
     a.structure_only = run.structure_only;
     a.gn_step_mode = run.gn_step_mode;
     reset_status(ctx);
+    if ((run.debug_h || run.debug_b) && pl.large) fail(PVO_UNSUPPORTED, "normal-equation capture: pose systems beyond 16 free poses");
     if (run.debug_h || run.debug_b) {
         const int n = 6 * pl.n_free_poses + pl.n_free_depths;
         double* dh = ctx->ba.dbg_h.as<double>((size_t)n * n);
@@ -422,7 +535,7 @@ void run_ba(pvo_ctx* ctx, const HostProblem& pr, const BARun& run) {
         if (run.debug_h) download(ctx, run.debug_h, dh, (size_t)n * n);
         if (run.debug_b) download(ctx, run.debug_b, db, n);
     }
-    launch_ba_checked(ctx, a);
+    launch_ba_checked(ctx, a, pl);
     const int status = read_status(ctx);
     raise_ba_status(status);
     download(ctx, run.out_poses, a.poses, (size_t)pr.n_poses * 7);
@@ -991,9 +1104,11 @@ pvo_dev::BAParams window_ba_params(pvo_ctx* ctx, int iterations, double damping)
     a.status2 = B.status2.as<int>(2);
     a.attempts = B.attempts.as<int>(1);
     a.phase_clocks = ctx->tracing ? B.clocks.as<long long>(128) : nullptr;
-    const int grid = pvo_dev::ba_grid_size(w.n_patches, w.plan.n_free_poses, w.n_poses, ctx->num_sms);
-    a.partials = B.partials.as<double>(pvo_dev::ba_partials_doubles(w.plan.n_free_poses, grid));
-    a.system = B.system.as<double>((size_t)np * (np + 1) / 2 + np + 1);
+    if (!w.plan.large) {
+        const int grid = pvo_dev::ba_grid_size(w.n_patches, w.plan.n_free_poses, w.n_poses, ctx->num_sms);
+        a.partials = B.partials.as<double>(pvo_dev::ba_partials_doubles(w.plan.n_free_poses, grid));
+        a.system = B.system.as<double>((size_t)np * (np + 1) / 2 + np + 1);
+    }
     a.delta = B.delta.as<double>(std::max(np, 1));
     a.residual_norms = B.norms.as<double>(iterations + 2);
     a.n_norms = B.n_norms.as<int>(1);
@@ -1033,7 +1148,7 @@ int pvo_window_iteration(pvo_ctx* ctx, int iterations, double damping, float* co
         run_corr(ctx, window_corr_params(ctx, corr_memspace == PVO_DEVICE ? corr_out : nullptr));
         cuda_check(cudaEventRecord(ctx->ev[1], ctx->stream), "event");
         pvo_dev::BAParams a = window_ba_params(ctx, iterations, damping);
-        launch_ba_checked(ctx, a);
+        launch_ba_checked(ctx, a, w.plan);
         cuda_check(cudaEventRecord(ctx->ev[2], ctx->stream), "event");
         ctx->timing_pending = true;
         if (corr_out && corr_memspace != PVO_DEVICE) {

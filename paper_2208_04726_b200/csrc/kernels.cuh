@@ -130,6 +130,35 @@ struct BAParams {
     long long* phase_clocks = nullptr;  // [16][8] optional: CTA 0 clock64 at phase boundaries
 };
 
+// Large-window BA (ba_large.cu): pose systems beyond the single-kernel path.
+constexpr int kMaxLocalPoses = 25;  // free poses one patch group may touch (150 local dims)
+struct BALargeParams {
+    BAParams a;                     // problem + the shared scratch of BAParams
+    int structure = 0;              // current iteration is structure-only (set per launch)
+    int n_groups = 0;               // patch groups (runs of one source pose, <= 64 patches)
+    const int* g_begin = nullptr;   // [G+1] patch ranges
+    const int* g_lo = nullptr;      // [G] first free pose slot of the group window
+    const int* g_nl = nullptr;      // [G] window dims (6 x poses)
+    const long long* g_off = nullptr;  // [G] offset of the group block in g_part (doubles)
+    const int* patch_group = nullptr;  // [P]
+    int max_nl = 0;                 // widest window (dims)
+    int bw = 0;                     // half-bandwidth of the reduced system (scalars): reduce skips the rest
+    double* g_part = nullptr;       // group blocks: local upper triangle + local rhs
+    double* g_res = nullptr;        // [G][2] weighted residual sums at the current state
+    double* patch_vl = nullptr;     // [P][max_nl] local H_pd column of each patch
+    double* A = nullptr;            // [(np+1)][(np+1)] reduced system, natural order (row np = rhs)
+    double* A2 = nullptr;           // [(np+1)][(np+1)] permuted copy, factorised in place
+    double* mats = nullptr;         // [N][12] rotation + translation, current state
+    double* cmats = nullptr;        // [N][12] ... candidate state
+    double* u_res = nullptr;        // [n_update_ctas][2] residual sums at the candidate
+    int n_update_ctas = 0;
+    int* ctrl = nullptr;            // [4] settled, attempt, failed, pad
+    double* dbg_A = nullptr;        // debug: copy of the first reduced system
+};
+cudaError_t launch_ba_large(BALargeParams& p, int num_sms, cudaStream_t stream, int* launches);
+size_t ba_large_solver_smem(int n_free_poses);
+int ba_large_assemble_smem(int nl);
+
 // Returns cudaErrorNotSupported when the shape exceeds the kernel (np > 96
 // or a patch with > 32 edges); the host maps that to PVO_UNSUPPORTED.
 cudaError_t launch_ba(BAParams& p, int num_sms, cudaStream_t stream, int* grid_out);

@@ -56,3 +56,40 @@ int main() {
     int v; cudaDeviceGetAttribute(&v, cudaDevAttrSingleToDoublePrecisionPerfRatio, 0);
     printf("single/double perf ratio attribute: %d\n", v);
 }
+// dependent DFMA chain latency + block barrier cost
+__global__ void dfma_lat(double* out, long long* t, int n) {
+    double a = 1.0 + threadIdx.x;
+    long long t0 = clock64();
+    for (int it = 0; it < n; ++it) a = fma(a, 1.0000001, 1e-9);
+    long long t1 = clock64();
+    out[threadIdx.x] = a;
+    if (threadIdx.x == 0) t[0] = t1 - t0;
+}
+__global__ void bar_cost(long long* t, int n) {
+    long long t0 = clock64();
+    for (int it = 0; it < n; ++it) __syncthreads();
+    long long t1 = clock64();
+    if (threadIdx.x == 0) t[0] = t1 - t0;
+}
+__global__ void lds_lat(double* out, long long* t, int n) {
+    __shared__ double s[64];
+    if (threadIdx.x < 64) s[threadIdx.x] = 0.0;
+    __syncthreads();
+    int i = 0;
+    double acc = 0;
+    long long t0 = clock64();
+    for (int it = 0; it < n; ++it) { double v = s[i]; acc += v; i = (int)v; }
+    long long t1 = clock64();
+    out[threadIdx.x] = acc;
+    if (threadIdx.x == 0) t[0] = t1 - t0;
+}
+struct Extra { Extra() {
+    double* o; long long* t; long long h;
+    cudaMalloc(&o, 8192); cudaMalloc(&t, 8);
+    dfma_lat<<<1, 32>>>(o, t, 1000); cudaMemcpy(&h, t, 8, cudaMemcpyDeviceToHost);
+    printf("DFMA dependent latency: %.1f cycles\n", h / 1000.0);
+    for (int th : {32, 256, 1024}) { bar_cost<<<1, th>>>(t, 1000); cudaMemcpy(&h, t, 8, cudaMemcpyDeviceToHost);
+        printf("__syncthreads x%d threads: %.1f cycles\n", th, h / 1000.0); }
+    lds_lat<<<1, 32>>>(o, t, 1000); cudaMemcpy(&h, t, 8, cudaMemcpyDeviceToHost);
+    printf("LDS.64 + DADD dependent: %.1f cycles\n", h / 1000.0);
+} } g_extra;
