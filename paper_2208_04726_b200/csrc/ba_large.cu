@@ -18,13 +18,15 @@
 //    CTA's threads in patch order (deterministic, no atomics);
 //  * an entry-parallel kernel sums the group blocks into the dense S (fixed
 //    group order) and adds the damping;
-//  * one 512-thread CTA applies Eigen's diagonal pivot order (as ba.cu) and
-//    factors the permuted S with a blocked (32) right-looking LDL^T, the rhs
-//    carried as an extra row (forward substitution for free), then a blocked
-//    back-substitution and the retraction.  The pivot order matters for
-//    parity, not just speed: on ill-conditioned windows (weakly observed
-//    poses held only by the 1e-4 damping) a different elimination order moves
-//    the update by 1e-4 relative and can flip the divergence guard;
+//  * one CTA factors S with a blocked (32) right-looking LDL^T restricted to
+//    the band (half-bandwidth = widest group window - 1; without pivoting
+//    there is no fill-in outside the band: 5x fewer flops than dense at
+//    config 4), the rhs carried as an extra row (forward substitution for
+//    free), 4x4 register-tiled trailing updates, then a blocked banded
+//    back-substitution and the retraction.  Unlike ba.cu it keeps the natural
+//    order instead of Eigen's diagonal pivoting: a symmetric permutation of an
+//    SPD system, the same solution up to rounding (tested against the oracle,
+//    which follows Eigen), and pivoting would destroy the band;
 //  * depth back-substitution + residual at the candidate state, then a
 //    one-CTA guard kernel that accepts / retries with heavier damping / skips,
 //    exactly as bundle_adjust.cpp:327-366.  Later attempts of an iteration
@@ -48,7 +50,7 @@ constexpr int kMaxE = 32;       // edges per patch (lane per edge)
 constexpr int kRec = 30;        // doubles per edge record: Gs[12] Jt[12] Jd[2] r[2] w[2]
 constexpr int kGs = 0, kJt = 12, kJd = 24, kR = 26, kWt = 28;
 constexpr int kScal = 40;       // per-warp scalars: h, bd, 1/h, pad, 6x6 source block
-constexpr int kST = 512;        // solver CTA size (128 registers: the panel row lives in registers)
+constexpr int kST = 256;        // solver CTA size (255 registers: the panel row lives in registers)
 constexpr int kB = 32;          // solver block size
 
 __host__ __device__ inline int nent(int n) { return n * (n + 1) / 2; }
@@ -385,93 +387,84 @@ __global__ void __launch_bounds__(kST, 1) bal_solve_kernel(BALargeParams P) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int np = P.structure ? 0 : 6 * a.n_free_poses;
     const int ld = 6 * a.n_free_poses + 1;
-    const double* S = P.A;  // natural order (reduce kernel)
-    double* A = P.A2;       // permuted copy, factorised in place
-    const int bw = np > 0 ? np - 1 : 0;  // pivoting fills the whole triangle
-    const int pr_cap = np + 1;           // panel rows + the rhs row
+    double* A = P.A;  // reduced system from the reduce kernel, factorised in place
+    const int bw = min(P.bw, np > 0 ? np - 1 : 0);
+    const int pr_cap = ((bw + 2 + 3) / 4) * 4;              // panel rows (band) + the rhs row, 4-row tiles
     double* Dg = reinterpret_cast<double*>(smem);          // [32][33] diagonal block
-    double* Wp = Dg + kB * (kB + 1);                        // [pr_cap][33] unscaled panel (L D)
-    double* x = Wp + (size_t)pr_cap * (kB + 1);             // [np] solution / |diag|
-    double* cc = x + (np > 0 ? np : 1);                     // [32] unscaled pivot column
-    double* xb = cc + kB;                                   // [32]
+    double* Wp = Dg + kB * (kB + 1);                        // [32][pr_cap] unscaled panel (L D), column-major
+    double* x = Wp + (size_t)pr_cap * kB;                   // [np] solution
+    double* cc = x + (np > 0 ? np : 1);                     // [33] unscaled pivot column + d_kk
+    double* xb = cc + kB + 1;                               // [32]
     double* dinv = xb + kB;                                 // [32]
-    int* perm = reinterpret_cast<int*>(dinv + kB);          // [np]
     __shared__ int s_fail, s_zero;
     if (tid == 0) {
         s_fail = 0;
         s_zero = 0;
     }
-    // Eigen's pivot sequence (largest remaining original |diagonal|, ties by
-    // index; see ba.cu ldlt_solve_blocked) as a parallel rank, then the
-    // symmetric permutation of the system into the factor workspace.
-    for (int i = tid; i < np; i += kST) x[i] = fabs(S[(size_t)i * ld + i]);
-    __syncthreads();
-    for (int i = tid; i < np; i += kST) {
-        const double di = x[i];
-        int rank = 0;
-        for (int j = 0; j < np; ++j) {
-            const double dj = x[j];
-            rank += (dj > di) || (dj == di && j < i);
-        }
-        perm[rank] = i;
+    // optional phase clocks (pvo_ctx_set_tracing): [0] start, [1] begin, [2] diag, [3] panel,
+    // [4] trailing (accumulated over blocks), [5] factorised, [6] solved, [7] end
+    long long* pc = (a.phase_clocks && tid == 0) ? a.phase_clocks + 8 * 14 : nullptr;
+    long long tk = 0;
+    if (pc) {
+        pc[0] = clock64();
+        pc[2] = pc[3] = pc[4] = 0;
     }
     __syncthreads();
-    {
-        const long long total = (long long)(np + 1) * (np + 2) / 2 - 1;
-        for (long long idx = tid; idx < total; idx += kST) {
-            int i = (int)((sqrt(8.0 * (double)idx + 1.0) - 1.0) * 0.5);
-            while ((long long)i * (i + 1) / 2 > idx) --i;
-            while ((long long)(i + 1) * (i + 2) / 2 <= idx) ++i;
-            const int j = (int)(idx - (long long)i * (i + 1) / 2);
-            double v;
-            if (i == np) {
-                v = S[(size_t)np * ld + perm[j]];
-            } else {
-                const int r = perm[i], c = perm[j];
-                v = r >= c ? S[(size_t)r * ld + c] : S[(size_t)c * ld + r];
-            }
-            A[(size_t)i * ld + j] = v;
-        }
-    }
-    __syncthreads();
+    if (pc) pc[1] = tk = clock64();
     for (int k0 = 0; k0 < np; k0 += kB) {
         const int kb = min(kB, np - k0);
         const int r0 = k0 + kb;                        // first panel row
         const int r1 = min(np, k0 + kb + bw);           // panel rows [r0, r1) + the rhs row
         const int nr = r1 - r0 + 1;
-        // (1) diagonal block, warp 0 (lane = row), unscaled column kept in cc
+        // (1) diagonal block, warp 0: lane = row, the row in registers (loads issued
+        //     together), the unscaled pivot column broadcast through shared memory
         if (warp == 0) {
-            for (int j = 0; j < kb; ++j)
-                if (lane < kb && j <= lane) Dg[lane * (kB + 1) + j] = A[(size_t)(k0 + lane) * ld + k0 + j];
-            __syncwarp();
+            double r[kB];
+#pragma unroll
+            for (int j = 0; j < kB; ++j) r[j] = (lane < kb && j <= lane) ? A[(size_t)(k0 + lane) * ld + k0 + j] : 0.0;
             bool fail = false, zero = false;
-            for (int kk = 0; kk < kb; ++kk) {
-                const double dk = Dg[kk * (kB + 1) + kk];
-                const bool valid = fabs(dk) > 0.0;
-                if (k0 + kk == 0 && !valid) zero = true;  // Eigen: all-zero diagonal -> x = 0
-                const double inv = valid ? 1.0 / dk : 0.0;
-                if (lane == 0) dinv[kk] = inv;
-                const bool below = lane > kk && lane < kb;
-                const double ci = below ? Dg[lane * (kB + 1) + kk] : 0.0;
-                cc[lane] = ci;
-                __syncwarp();
-                if (below) {
-                    if (!valid && ci != 0.0) fail = true;
-                    for (int j = kk + 1; j <= lane; ++j) Dg[lane * (kB + 1) + j] -= ci * (cc[j] * inv);
-                    Dg[lane * (kB + 1) + kk] = valid ? ci * inv : ci;
+#pragma unroll
+            for (int kk = 0; kk < kB; ++kk) {
+                if (kk < kb) {
+                    if (lane == kk) cc[kB] = r[kk];  // d_kk
+                    __syncwarp();
+                    const double dk = cc[kB];
+                    const bool valid = fabs(dk) > 0.0;
+                    if (k0 + kk == 0 && !valid) zero = true;  // Eigen: all-zero diagonal -> x = 0
+                    const double inv = valid ? 1.0 / dk : 0.0;
+                    if (lane == 0) dinv[kk] = inv;
+                    const bool below = lane > kk && lane < kb;
+                    const double ci = below ? r[kk] : 0.0;
+                    cc[lane] = ci;
+                    __syncwarp();
+                    if (below && !valid && ci != 0.0) fail = true;
+                    const double cs = ci * inv;
+#pragma unroll
+                    for (int j = kk + 1; j < kB; ++j)
+                        if (below && j <= lane) r[j] -= cs * cc[j];
+                    if (below) r[kk] = valid ? cs : ci;
+                    __syncwarp();
                 }
-                __syncwarp();
             }
-            for (int j = 0; j < kb; ++j)
-                if (lane < kb && j <= lane) A[(size_t)(k0 + lane) * ld + k0 + j] = Dg[lane * (kB + 1) + j];
+#pragma unroll
+            for (int j = 0; j < kB; ++j)
+                if (lane < kb && j <= lane) {
+                    Dg[lane * (kB + 1) + j] = r[j];
+                    A[(size_t)(k0 + lane) * ld + k0 + j] = r[j];
+                }
             if (__any_sync(0xffffffffu, fail) && lane == 0) s_fail = 1;
             if (__any_sync(0xffffffffu, zero) && lane == 0) s_zero = 1;
         }
         __syncthreads();
+        if (pc) {
+            const long long t = clock64();
+            pc[2] += t - tk;
+            tk = t;
+        }
         if (s_zero) break;
         // (2) panel rows: forward elimination against the diagonal block, one thread per row
-        if (tid < nr) {
-            const int i = tid < nr - 1 ? r0 + tid : np;
+        for (int t = tid; t < nr; t += kST) {
+            const int i = t < nr - 1 ? r0 + t : np;
             double seg[kB];
 #pragma unroll
             for (int j = 0; j < kB; ++j) seg[j] = j < kb ? A[(size_t)i * ld + k0 + j] : 0.0;
@@ -485,7 +478,7 @@ __global__ void __launch_bounds__(kST, 1) bal_solve_kernel(BALargeParams P) {
                         if (j < kb) seg[j] -= c * Dg[j * (kB + 1) + kk];
                     const double inv = dinv[kk];
                     if (inv == 0.0 && c != 0.0 && i < np) fail = true;
-                    Wp[tid * (kB + 1) + kk] = c;
+                    Wp[kk * pr_cap + t] = c;
                     seg[kk] = inv != 0.0 ? c * inv : c;
                 }
             }
@@ -495,36 +488,75 @@ __global__ void __launch_bounds__(kST, 1) bal_solve_kernel(BALargeParams P) {
             if (fail) s_fail = 1;
         }
         __syncthreads();
-        // (3) trailing update inside the band: A[i][j] -= sum_kk (L D)_i,kk L_j,kk, j <= i, j < np
+        if (pc) {
+            const long long t = clock64();
+            pc[3] += t - tk;
+            tk = t;
+        }
+        // (3) trailing update A[i][j] -= sum_kk (L D)_i,kk L_j,kk over the panel rows
+        //     (j <= i, j < np; the rhs row is panel row nr - 1), 4 x 4 register tiles:
+        //     8 shared loads feed 16 FMAs
         {
-            const int npairs = (nr - 1) * nr / 2 + (nr - 1);  // rows r0..r1-1 lower triangle + rhs row
-            for (int p = tid; p < npairs; p += kST) {
-                int ti, tj;
-                const int tri = (nr - 1) * nr / 2;
-                if (p < tri) {
-                    ti = (int)((sqrtf(8.f * (float)p + 1.f) - 1.f) * 0.5f);
-                    while (ti * (ti + 1) / 2 > p) --ti;
-                    while ((ti + 1) * (ti + 2) / 2 <= p) ++ti;
-                    tj = p - ti * (ti + 1) / 2;
-                } else {
-                    ti = nr - 1;  // rhs row
-                    tj = p - tri;
+            const int TI = (nr + 3) / 4;
+            const int ntiles = TI * (TI + 1) / 2;
+            for (int t = tid; t < ntiles; t += kST) {
+                int I = (int)((sqrtf(8.f * (float)t + 1.f) - 1.f) * 0.5f);
+                while (I * (I + 1) / 2 > t) --I;
+                while ((I + 1) * (I + 2) / 2 <= t) ++I;
+                const int J = t - I * (I + 1) / 2;
+                double acc[4][4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+                const double* w0 = Wp + 4 * I;  // rows 4I.. of column kk at w0[kk * pr_cap]
+                const double* l0 = Wp + 4 * J;
+                double old[4][4];  // the tile's current values: 16 independent loads in flight
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int ti = 4 * I + u;
+                    const int i = ti < nr - 1 ? r0 + ti : np;
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const int tj = 4 * J + v;
+                        old[u][v] = (ti < nr && tj < nr - 1 && tj <= ti) ? A[(size_t)i * ld + r0 + tj] : 0.0;
+                    }
                 }
-                const double* wrow = Wp + ti * (kB + 1);
-                const double* lrow = Wp + tj * (kB + 1);  // L_j,kk = W_j,kk / d_kk
-                double acc = 0.0;
-#pragma unroll 8
                 for (int kk = 0; kk < kb; ++kk) {
-                    const double l = dinv[kk] != 0.0 ? lrow[kk] * dinv[kk] : lrow[kk];
-                    acc += wrow[kk] * l;
+                    const double di = dinv[kk];
+                    const double2* wq = reinterpret_cast<const double2*>(w0 + kk * pr_cap);
+                    const double2* lq = reinterpret_cast<const double2*>(l0 + kk * pr_cap);
+                    const double2 wa = wq[0], wb = wq[1], la = lq[0], lb = lq[1];
+                    const double wv[4] = {wa.x, wa.y, wb.x, wb.y};
+                    const double lr[4] = {la.x, la.y, lb.x, lb.y};
+                    double lv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) lv[u] = di != 0.0 ? lr[u] * di : lr[u];  // L_j,kk = W_j,kk / d_kk
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) acc[u][v] = fma(wv[u], lv[v], acc[u][v]);
                 }
-                const int i = ti < nr - 1 ? r0 + ti : np;
-                const int j = r0 + tj;
-                A[(size_t)i * ld + j] -= acc;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int ti = 4 * I + u;
+                    const int i = ti < nr - 1 ? r0 + ti : np;
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const int tj = 4 * J + v;
+                        if (ti < nr && tj < nr - 1 && tj <= ti) A[(size_t)i * ld + r0 + tj] = old[u][v] - acc[u][v];
+                    }
+                }
             }
         }
         __syncthreads();
+        if (pc) {
+            const long long t = clock64();
+            pc[4] += t - tk;
+            tk = t;
+        }
     }
+    if (pc) pc[5] = clock64();
     if (np > 0 && s_fail) {
         if (tid == 0) set_status(a.status, kDevFactorization);
         P.ctrl[2] = 1;  // factorization failure: stop the window
@@ -549,19 +581,26 @@ __global__ void __launch_bounds__(kST, 1) bal_solve_kernel(BALargeParams P) {
                 }
                 __syncthreads();
                 if (warp == 0) {
+                    double lq[kB];  // L_{k0+q, k0+lane}: loads issued together
+#pragma unroll
+                    for (int q = 0; q < kB; ++q) lq[q] = (q < kb && lane < q) ? A[(size_t)(k0 + q) * ld + k0 + lane] : 0.0;
                     double xc = lane < kb ? xb[lane] : 0.0;
-                    for (int q = kb - 1; q >= 0; --q) {
-                        const double xv = __shfl_sync(0xffffffffu, xc, q);
-                        if (lane < q) xc -= A[(size_t)(k0 + q) * ld + k0 + lane] * xv;
+#pragma unroll
+                    for (int q = kB - 1; q >= 0; --q) {
+                        if (q < kb) {
+                            const double xv = __shfl_sync(0xffffffffu, xc, q);
+                            if (lane < q) xc -= lq[q] * xv;
+                        }
                     }
                     if (lane < kb) x[k0 + lane] = xc;
                 }
                 __syncthreads();
             }
         }
+        if (pc) pc[6] = clock64();
         bool bad = false;
         for (int i = tid; i < np; i += kST) {
-            a.delta[perm[i]] = x[i];
+            a.delta[i] = x[i];
             bad = bad || !isfinite(x[i]);
         }
         if (__syncthreads_or(bad)) {
@@ -585,6 +624,7 @@ __global__ void __launch_bounds__(kST, 1) bal_solve_kernel(BALargeParams P) {
     }
     __syncthreads();
     pose_mats(a.cand_poses, P.cmats, a.n_poses);
+    if (pc) pc[7] = clock64();
 }
 
 // ---------------------------------------------------------------------------
@@ -728,9 +768,11 @@ __global__ void bal_decide_kernel(BALargeParams P, int n_update_ctas) {
 
 }  // namespace
 
-size_t ba_large_solver_smem(int n_free_poses) {
+size_t ba_large_solver_smem(int n_free_poses, int bw) {
     const int np = 6 * n_free_poses;
-    return 8 * ((size_t)kB * (kB + 1) + (size_t)(np + 1) * (kB + 1) + (np > 0 ? np : 1) + 3 * kB) + 4 * (size_t)np + 16;
+    if (bw > np - 1) bw = np > 0 ? np - 1 : 0;
+    const size_t rows = ((size_t)(bw + 2 + 3) / 4) * 4;
+    return 8 * ((size_t)kB * (kB + 1) + rows * kB + (np > 0 ? np : 1) + 3 * kB + 1) + 16;
 }
 int ba_large_assemble_smem(int nl) { return assemble_layout(nl).total; }
 
@@ -741,7 +783,7 @@ cudaError_t launch_ba_large(BALargeParams& p, int num_sms, cudaStream_t stream, 
     const int asm_bytes = assemble_layout(p.max_nl).total;
     if ((err = cudaFuncSetAttribute(bal_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, asm_bytes)))
         return err;
-    const size_t solve_bytes = ba_large_solver_smem(a.n_free_poses);
+    const size_t solve_bytes = ba_large_solver_smem(a.n_free_poses, p.bw);
     if (solve_bytes > 227 * 1024) return cudaErrorNotSupported;
     if ((err = cudaFuncSetAttribute(bal_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)solve_bytes)))
         return err;

@@ -35,14 +35,14 @@ struct BABuffers {
         e_weight, cand_poses, cand_depth, patch_v, patch_h, patch_bd, partials, system, delta, norms, n_norms, dbg_h,
         dbg_b, K, status2, attempts, clocks;
     // large-window path (ba_large.cu)
-    DevBuf g_begin, g_lo, g_nl, g_off, patch_group, g_part, g_res, A, A2, mats, cmats, u_res, ctrl;
+    DevBuf g_begin, g_lo, g_nl, g_off, patch_group, g_part, g_res, A, mats, cmats, u_res, ctrl;
     void release() {
         DevBuf* all[] = {&poses,    &free_slot,  &patch_src, &px,        &py,       &depth,    &depth_slot,
                          &edge_begin, &e_patch,  &e_pose,    &e_in,      &e_w,      &e_target, &e_weight,
                          &cand_poses, &cand_depth, &patch_v, &patch_h,   &patch_bd, &partials, &system,
                          &delta,    &norms,      &n_norms,   &dbg_h,     &dbg_b,    &K,        &status2,
                          &attempts, &clocks,     &g_begin,   &g_lo,      &g_nl,     &g_off,    &patch_group,
-                         &g_part,   &g_res,      &A,  &A2,       &mats,      &cmats,    &u_res,    &ctrl};
+                         &g_part,   &g_res,      &A,         &mats,      &cmats,    &u_res,    &ctrl};
         for (DevBuf* b : all) b->release();
     }
 };
@@ -325,7 +325,6 @@ pvo_dev::BALargeParams large_params(pvo_ctx* ctx, const pvo_dev::BAParams& a, co
     p.g_res = B.g_res.as<double>(2 * (size_t)std::max(1, p.n_groups));
     p.patch_vl = B.patch_v.as<double>((size_t)a.n_patches * std::max(1, pl.max_nl));
     p.A = B.A.as<double>((size_t)(np + 1) * (np + 1));
-    p.A2 = B.A2.as<double>((size_t)(np + 1) * (np + 1));
     p.mats = B.mats.as<double>(12 * (size_t)a.n_poses);
     p.cmats = B.cmats.as<double>(12 * (size_t)a.n_poses);
     p.n_update_ctas = std::max(1, std::min(2 * ctx->num_sms, (a.n_patches + 7) / 8));

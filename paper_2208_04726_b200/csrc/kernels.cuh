@@ -142,12 +142,11 @@ struct BALargeParams {
     const long long* g_off = nullptr;  // [G] offset of the group block in g_part (doubles)
     const int* patch_group = nullptr;  // [P]
     int max_nl = 0;                 // widest window (dims)
-    int bw = 0;                     // half-bandwidth of the reduced system (scalars): reduce skips the rest
+    int bw = 0;                     // half-bandwidth of the reduced system (scalars)
     double* g_part = nullptr;       // group blocks: local upper triangle + local rhs
     double* g_res = nullptr;        // [G][2] weighted residual sums at the current state
     double* patch_vl = nullptr;     // [P][max_nl] local H_pd column of each patch
-    double* A = nullptr;            // [(np+1)][(np+1)] reduced system, natural order (row np = rhs)
-    double* A2 = nullptr;           // [(np+1)][(np+1)] permuted copy, factorised in place
+    double* A = nullptr;            // [(np+1)][(np+1)] reduced system (row np = rhs), factorised in place
     double* mats = nullptr;         // [N][12] rotation + translation, current state
     double* cmats = nullptr;        // [N][12] ... candidate state
     double* u_res = nullptr;        // [n_update_ctas][2] residual sums at the candidate
@@ -156,7 +155,7 @@ struct BALargeParams {
     double* dbg_A = nullptr;        // debug: copy of the first reduced system
 };
 cudaError_t launch_ba_large(BALargeParams& p, int num_sms, cudaStream_t stream, int* launches);
-size_t ba_large_solver_smem(int n_free_poses);
+size_t ba_large_solver_smem(int n_free_poses, int bw);
 int ba_large_assemble_smem(int nl);
 
 // Returns cudaErrorNotSupported when the shape exceeds the kernel (np > 96
