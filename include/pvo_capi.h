@@ -174,6 +174,23 @@ int pvo_window_read(pvo_ctx* ctx, double* poses, double* inv_depth, double* resi
 /* Device pointer of the window's correlation volume buffer [E][2][pp][49]. */
 int pvo_window_corr_ptr(pvo_ctx* ctx, float** corr);
 
+/* ---- batch of independent windows (config 5: sequences sharded per device) -
+ * Windows are concatenated: pose/patch/edge offsets [n_windows + 1] (starting
+ * at 0); inside a window every index is window-local (as pvo_window_load);
+ * pose_slot is the frame-store slot of every pose (global).  One correlation
+ * launch covers all edges, one BA launch runs a CTA per window; each window
+ * keeps its own divergence guard (bundle_adjust.cpp:327-366).  Each window
+ * has <= 16 free poses.  residual_norms: [n_windows][pvo_batch_norm_stride()]. */
+int pvo_batch_load(pvo_ctx* ctx, int n_windows, const int* pose_off, const int* patch_off, const int* edge_off,
+                   const double* poses, const uint8_t* pose_fixed, const int* pose_slot, int p,
+                   const int* patch_src, const double* patch_x, const double* patch_y, const double* inv_depth,
+                   const float* patch_feats, const int* e_patch, const int* e_pose, const double* e_delta,
+                   const double* e_weight, const double* K, int image_w, int image_h);
+int pvo_batch_reset(pvo_ctx* ctx);
+int pvo_batch_iteration(pvo_ctx* ctx, int iterations, double damping, float* corr_out, int corr_memspace);
+int pvo_batch_read(pvo_ctx* ctx, double* poses, double* inv_depth, double* residual_norms, int* n_norms);
+int pvo_batch_norm_stride(void);
+
 /* ---- patch graph (patch_graph.hpp:66-136), host C++ ------------------------ */
 int pvo_graph_create(const double* K, int image_w, int image_h, int patch_width, pvo_graph** out);
 int pvo_graph_destroy(pvo_graph* g);

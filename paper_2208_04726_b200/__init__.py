@@ -8,6 +8,7 @@ library has not been built (there is no CPU fallback).
 from .api import (  # noqa: F401
     IDENTITY,
     BAProblem,
+    Batch,
     BASolution,
     Context,
     CudaError,

@@ -63,6 +63,11 @@ SIGNATURES = {
     "pvo_window_correlate": (i32, [vp, P, i32]),
     "pvo_window_read": (i32, [vp, P, P, P, P]),
     "pvo_window_corr_ptr": (i32, [vp, P]),
+    "pvo_batch_load": (i32, [vp, i32, P, P, P, P, P, P, i32, P, P, P, P, P, P, P, P, P, P, i32, i32]),
+    "pvo_batch_reset": (i32, [vp]),
+    "pvo_batch_iteration": (i32, [vp, i32, f64, P, i32]),
+    "pvo_batch_read": (i32, [vp, P, P, P, P]),
+    "pvo_batch_norm_stride": (i32, []),
     "pvo_graph_create": (i32, [P, i32, i32, i32, C.POINTER(vp)]),
     "pvo_graph_destroy": (i32, [vp]),
     "pvo_graph_add_frame": (i32, [vp, f64, P, P]),

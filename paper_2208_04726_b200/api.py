@@ -634,3 +634,53 @@ class Window:
         p = C.c_void_p()
         check(lib.pvo_window_corr_ptr(self.ctx.handle, C.addressof(p)))
         return p.value
+
+
+class Batch:
+    """Many independent windows on one device (config 5): one correlation launch
+    over every edge, one BA launch with a CTA per window (pvo_batch_*)."""
+
+    def __init__(self, ctx: Context):
+        self.ctx = ctx
+
+    def load(self, probs: list, pose_slots: list, patch_feats: list, K, image_size) -> None:
+        """probs: flattened windows (window-local indices, revision deltas in e_delta);
+        pose_slots: frame-store slot of every pose of each window."""
+        self.n_windows = len(probs)
+        self.pose_off = np.concatenate([[0], np.cumsum([len(p["poses"]) for p in probs])]).astype(np.int32)
+        self.patch_off = np.concatenate([[0], np.cumsum([len(p["depth"]) for p in probs])]).astype(np.int32)
+        self.edge_off = np.concatenate([[0], np.cumsum([len(p["e_patch"]) for p in probs])]).astype(np.int32)
+        cat = lambda key, conv: conv(np.concatenate([p[key] for p in probs]))  # noqa: E731
+        keep = dict(poses=cat("poses", _f64), fixed=cat("fixed", _u8), slot=_i32(np.concatenate(pose_slots)),
+                    src=cat("patch_src", _i32), px=cat("patch_x", _f64), py=cat("patch_y", _f64),
+                    d=cat("depth", _f64), pf=_f32(np.concatenate(patch_feats)), ep=cat("e_patch", _i32),
+                    eo=cat("e_pose", _i32), ed=cat("e_delta", _f64), ew=cat("e_weight", _f64), K=_f64(K, (4,)),
+                    po=self.pose_off, ko=self.patch_off, eo_=self.edge_off)
+        self.n_poses, self.n_patches, self.n_edges = int(self.pose_off[-1]), int(self.patch_off[-1]), int(self.edge_off[-1])
+        check(lib.pvo_batch_load(self.ctx.handle, self.n_windows, _ptr(keep["po"]), _ptr(keep["ko"]),
+                                 _ptr(keep["eo_"]), _ptr(keep["poses"]), _ptr(keep["fixed"]), _ptr(keep["slot"]), 3,
+                                 _ptr(keep["src"]), _ptr(keep["px"]), _ptr(keep["py"]), _ptr(keep["d"]),
+                                 _ptr(keep["pf"]), _ptr(keep["ep"]), _ptr(keep["eo"]), _ptr(keep["ed"]),
+                                 _ptr(keep["ew"]), _ptr(keep["K"]), int(image_size[0]), int(image_size[1])))
+
+    def reset(self) -> None:
+        check(lib.pvo_batch_reset(self.ctx.handle))
+
+    def iteration(self, iterations: int = 2, damping: float = kDefaultDamping, corr_out=None) -> None:
+        if corr_out is not None:
+            check(lib.pvo_batch_iteration(self.ctx.handle, iterations, damping, _ptr(corr_out), _capi.PVO_HOST))
+        else:
+            check(lib.pvo_batch_iteration(self.ctx.handle, iterations, damping, None, _capi.PVO_DEVICE))
+
+    def read(self):
+        """-> per-window lists of (poses [N_w, 7], depths [P_w], residual_norms)."""
+        stride = lib.pvo_batch_norm_stride()
+        poses, d = np.empty((self.n_poses, 7)), np.empty(self.n_patches)
+        norms = np.empty((self.n_windows, stride))
+        nn = np.empty(self.n_windows, np.int32)
+        check(lib.pvo_batch_read(self.ctx.handle, _ptr(poses), _ptr(d), _ptr(norms), _ptr(nn)))
+        out = []
+        for w in range(self.n_windows):
+            out.append((poses[self.pose_off[w]:self.pose_off[w + 1]], d[self.patch_off[w]:self.patch_off[w + 1]],
+                        list(norms[w, : nn[w]])))
+        return out

@@ -497,7 +497,7 @@ __device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Lay
             wi[1] = -1;
         }
         __syncthreads();
-        if (a.phase_clocks && blockIdx.x == 0 && tid == 0 && batch == k0) a.phase_clocks[15 * 8 + 0] = clock64();
+        if (a.phase_clocks && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0 && batch == k0) a.phase_clocks[15 * 8 + 0] = clock64();
 
         // ---- ordered accumulation of the batch into the CTA system ----
         for (int w = 0; w < kWarps; ++w) {
@@ -554,7 +554,7 @@ __device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Lay
         }
         __syncthreads();
     }
-    if (a.phase_clocks && blockIdx.x == 0 && tid == 0) a.phase_clocks[15 * 8 + 1] = clock64();
+    if (a.phase_clocks && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) a.phase_clocks[15 * 8 + 1] = clock64();
     // ---- write the CTA partial ----
     double* wr = at<double>(smem, L.wr);
     if (lane == 0) {
@@ -637,11 +637,21 @@ __device__ void phase_update(const BAParams& a, unsigned char* smem, const Layou
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) ba_kernel(BAParams a) {
+// The window loop.  Single window: a cooperative grid of G CTAs (grid-wide
+// barriers).  Batch of independent windows (pvo_batch_*): one CTA per window
+// (blockIdx.y), so every barrier is a CTA barrier and windows never wait for
+// each other (each keeps its own guard / attempt sequence).
+__device__ __forceinline__ void window_sync(bool batched) {
+    if (batched)
+        __syncthreads();
+    else
+        cg::this_grid().sync();
+}
+
+__device__ void ba_window_body(const BAParams& a, bool batched) {
     extern __shared__ __align__(16) unsigned char smem[];
-    cg::grid_group grid = cg::this_grid();
     const int np_full = 6 * a.n_free_poses;
-    const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+    const int G = batched ? 1 : gridDim.x, b = batched ? 0 : blockIdx.x, tid = threadIdx.x;
     const int k0 = (int)((long long)a.n_patches * b / G);
     const int k1 = (int)((long long)a.n_patches * (b + 1) / G);
     const Layout L = make_layout(np_full, a.n_poses);
@@ -689,12 +699,12 @@ __global__ void __launch_bounds__(kThreads, 1) ba_kernel(BAParams a) {
             const double lambda =
                 attempt == 0 ? a.damping : a.damping * (attempt == 1 ? 1e3 : attempt == 2 ? 1e6 : 1e9);
             double* part = partials + (size_t)b * pstride;
-            const bool clk = a.phase_clocks && b == 0 && tid == 0;
+            const bool clk = a.phase_clocks && b == 0 && tid == 0 && blockIdx.y == 0;
             long long* pc = a.phase_clocks ? a.phase_clocks + 8 * (attempt_no < 15 ? attempt_no : 15) : nullptr;
             if (clk) pc[0] = clock64();
             phase_assemble(a, smem, L, pose, rmat, k0, k1, np, structure, lambda, part, status);
             if (clk) pc[1] = clock64();
-            grid.sync();
+            window_sync(batched);
             if (clk) pc[2] = clock64();
             // P2: ordered reduction of the CTA partials (+ damping on the diagonal):
             // one warp per entry, lanes over CTAs in fixed order, shuffle tree
@@ -715,7 +725,7 @@ __global__ void __launch_bounds__(kThreads, 1) ba_kernel(BAParams a) {
                 }
             }
             if (clk) pc[3] = clock64();
-            grid.sync();
+            window_sync(batched);
             if (clk) pc[4] = clock64();
             // P3: every CTA solves the pose system and retracts its pose copy
             if (np > 0) {
@@ -745,7 +755,7 @@ __global__ void __launch_bounds__(kThreads, 1) ba_kernel(BAParams a) {
             if (clk) pc[5] = clock64();
             phase_update(a, smem, L, cand, rmatc, k0, k1, np, delta, part + nent + np, status);
             if (clk) pc[6] = clock64();
-            grid.sync();
+            window_sync(batched);
             if (clk) pc[7] = clock64();
             // P5: identical decision in every CTA
             const int st = *((volatile int*)status);
@@ -813,6 +823,15 @@ __global__ void __launch_bounds__(kThreads, 1) ba_kernel(BAParams a) {
             break;
         }
     }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) ba_kernel(const __grid_constant__ BAParams a) { ba_window_body(a, false); }
+
+__global__ void __launch_bounds__(kThreads, 1) ba_batch_kernel(const BAParams* __restrict__ windows) {
+    __shared__ BAParams sa;  // this CTA's window
+    if (threadIdx.x == 0) sa = windows[blockIdx.y];
+    __syncthreads();
+    ba_window_body(sa, true);
 }
 
 // ---------------------------------------------------------------------------
@@ -1021,6 +1040,19 @@ cudaError_t launch_ba(BAParams& p, int num_sms, cudaStream_t stream, int* grid_o
     if (err != cudaSuccess) return err;
     void* args[] = {&p};
     return cudaLaunchCooperativeKernel((void*)ba_kernel, dim3(grid), dim3(kThreads), args, L.total, stream);
+}
+
+size_t ba_batch_smem(int n_free_poses, int n_poses) { return make_layout(6 * n_free_poses, n_poses).total; }
+
+cudaError_t launch_ba_batch(const BAParams* windows_dev, int n_windows, int max_free_poses, int max_poses,
+                            cudaStream_t stream) {
+    if (n_windows <= 0) return cudaSuccess;
+    if (max_free_poses > kMaxFree || max_poses > kMaxPoses) return cudaErrorNotSupported;
+    const int smem = (int)ba_batch_smem(max_free_poses, max_poses);
+    cudaError_t err = cudaFuncSetAttribute(ba_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err != cudaSuccess) return err;
+    ba_batch_kernel<<<dim3(1, n_windows), kThreads, smem, stream>>>(windows_dev);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_normal_equations_debug(const BAParams& p, double* h, double* b, cudaStream_t stream) {

@@ -166,6 +166,11 @@ int ba_max_edges_per_patch();
 size_t ba_partials_doubles(int n_free_poses, int grid);
 int ba_grid_size(int n_patches, int n_free_poses, int n_poses, int num_sms);
 int ba_max_poses();
+// Batch of independent windows: one CTA per window (params array on the device);
+// each window's status word is its own (BAParams::status).
+cudaError_t launch_ba_batch(const BAParams* windows_dev, int n_windows, int max_free_poses, int max_poses,
+                            cudaStream_t stream);
+size_t ba_batch_smem(int n_free_poses, int n_poses);
 
 // Debug capture of the damped dense normal equations (sequential, tests only).
 cudaError_t launch_normal_equations_debug(const BAParams& p, double* h, double* b, cudaStream_t stream);

@@ -424,3 +424,47 @@ def test_window_iteration_deterministic(ctx, c1_workload):
     ref = orc.ba_window(g.window_problem(w.cfg["window"]), w.K, iterations=2)
     dt, dq = pose_parity(outs[0][1], ref["poses"])
     assert dt.max() <= 1e-3 and dq.max() <= 1e-3
+
+
+def test_batch_of_windows_matches_single_windows_and_oracle(ctx):
+    """Config-5 path (pvo_batch_*): several independent windows in one
+    correlation launch + one BA launch (CTA per window).  Correlation is
+    bit-identical to the single-window path; BA matches the oracle per window."""
+    ws = [synth.generate("c1", seed=s, frames=6, patches=24) for s in (11, 12, 13)]
+    F = ws[0].cfg["frames"]
+    _, H0, W0, D = ws[0].level0.shape
+    _, H1, W1, _ = ws[0].level1.shape
+    ctx.frames_reserve(F * len(ws), W0, H0, W1, H1, D)
+    probs, slots, feats = [], [], []
+    for i, w in enumerate(ws):
+        for f in range(F):
+            ctx.frames_upload(i * F + f, w.level0[f], w.level1[f])
+        g = synth.build_graph(w, pvo.PatchGraph)
+        prob = synth.window_arrays(w, g.window_problem(w.cfg["window"]))
+        probs.append(prob)
+        slots.append(prob["pose_frames"] + i * F)
+        feats.append(prob["patch_feats"])
+    bat = pvo.Batch(ctx)
+    bat.load(probs, slots, feats, ws[0].K, ws[0].image)
+    vol = np.empty((bat.n_edges, 2, 9, 7, 7), np.float32)
+    bat.iteration(2, corr_out=vol)
+    res = bat.read()
+    for i, (w, prob) in enumerate(zip(ws, probs)):
+        win = pvo.Window(ctx)
+        win.load(prob, slots[i], prob["patch_feats"], w.K, w.image)
+        v1 = np.empty((win.n_edges, 2, 9, 7, 7), np.float32)
+        win.iteration(2, corr_out=v1)
+        assert np.array_equal(vol[bat.edge_off[i]:bat.edge_off[i + 1]], v1)
+        poses, depth, norms = res[i]
+        g = synth.build_graph(w, orc.PatchGraph)
+        rb = orc.ba_window(g.window_problem(w.cfg["window"]), w.K, iterations=2)
+        dt, dq = pose_parity(poses, rb["poses"])
+        assert dt.max() <= 1e-3 and dq.max() <= 1e-3
+        assert (np.abs(depth - rb["depth"]) <= 1e-3 * np.maximum(np.abs(rb["depth"]), 1e-3)).all()
+        assert len(norms) == len(rb["residual_norms"]) and np.allclose(norms, rb["residual_norms"], rtol=1e-6)
+    # reset restores the initial state: a rerun is bit-identical
+    bat.reset()
+    bat.iteration(2)
+    res2 = bat.read()
+    for (p1, d1, n1), (p2, d2, n2) in zip(res, res2):
+        assert np.array_equal(p1, p2) and np.array_equal(d1, d2) and n1 == n2
