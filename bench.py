@@ -201,7 +201,8 @@ def run_reference(args, rank, world):
     import oracle.pyoracle as orc
     from paper_2208_04726_b200 import synth
 
-    w = synth.generate(args.config, seed=0)
+    # c5 (a batch of c2 sequences): the CPU path's per-edge cost is the c2 window's
+    w = synth.generate("c2" if args.config == "c5" else args.config, seed=0)
     og = synth.build_graph(w, orc.PatchGraph)
     prob = og.window_problem(w.cfg["window"])
     E = len(prob["e_patch"])
@@ -368,6 +369,156 @@ def run_ours(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def run_batch(args, rank, world, local_rank):
+    """Config 5: a batch of independent sequences at the DPVO default window,
+    sharded by sequence across ranks (weak scaling, no collective in the loop).
+    Each rank runs its 1024 / N sequences in chunks that fit HBM (frame store of
+    a chunk = chunk x 22 frames x 10.4 MB); a step = one corr + 2-GN-iteration
+    pass over all of the rank's sequences.  Inputs: `distinct` synthetic C2
+    trajectories (geometry + patch descriptors) replicated over the chunk,
+    frame features generated on the device per chunk (unit-norm random cells,
+    distinct for every sequence), so the frames read by the correlation are
+    never shared between sequences."""
+    import torch
+
+    import paper_2208_04726_b200 as pvo
+    from paper_2208_04726_b200 import synth
+    from paper_2208_04726_b200.dist import gather_poses, max_over_ranks
+
+    torch.cuda.set_device(local_rank)
+    dev = f"cuda:{local_rank}"
+    n_seq = args.sequences // world
+    chunk = min(n_seq, args.chunk)
+    n_chunks = (n_seq + chunk - 1) // chunk
+    geos = []
+    for gi in range(min(args.distinct, chunk)):
+        w = synth.generate("c2", seed=10_000 * rank + gi, features=False)
+        g = synth.build_graph(w, pvo.PatchGraph)
+        prob = synth.window_arrays(w, g.window_problem(w.cfg["window"]))
+        rng = np.random.default_rng(77 + gi)
+        pf = rng.standard_normal((len(prob["depth"]), 2, 9, 128)).astype(np.float32)
+        pf /= np.linalg.norm(pf, axis=-1, keepdims=True)
+        geos.append((w, prob, pf))
+    w0 = geos[0][0]
+    F = w0.cfg["frames"]
+    H0, W0i = w0.image[1] // 4, w0.image[0] // 4
+    H1, W1i = H0 // 4, W0i // 4
+    D = 128
+    ctx = pvo.Context(local_rank)
+    stream = torch.cuda.Stream(device=local_rank)
+    ctx.set_stream(stream.cuda_stream)
+    ctx.frames_reserve(chunk * F, W0i, H0, W1i, H1, D)
+    probs, slots, feats = [], [], []
+    for i in range(chunk):
+        _, prob, pf = geos[i % len(geos)]
+        probs.append(prob)
+        slots.append(prob["pose_frames"] + i * F)
+        feats.append(pf)
+    bat = pvo.Batch(ctx)
+    bat.load(probs, slots, feats, w0.K, w0.image)
+    E_chunk = bat.n_edges
+    newest = [i * F + int(p["pose_frames"].max()) for i, p in enumerate(probs)]
+
+    def fill(c):  # device-generated frame features of chunk c (untimed)
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(1_000_003 * rank + c)
+        with torch.cuda.stream(stream):
+            for s0 in range(0, chunk * F, 64):
+                k = min(64, chunk * F - s0)
+                l0 = torch.randn((k, H0, W0i, D), device=dev, generator=gen)
+                l0 /= l0.norm(dim=-1, keepdim=True)
+                l1 = l0.view(k, H1, 4, W1i, 4, D).mean(dim=(2, 4))
+                l1 /= l1.norm(dim=-1, keepdim=True).clamp_min(1e-12)
+                l1 = l1.contiguous()
+                for j in range(k):
+                    ctx.frames_upload(s0 + j, l0[j], l1[j], device=True)
+                del l0, l1
+        torch.cuda.synchronize()
+
+    timed_launches = [0]
+
+    def step():  # one corr + BA pass over all of the rank's sequences: device ms
+        tot = 0.0
+        for c in range(n_chunks):
+            fill(c)
+            bat.reset()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            l0 = ctx.kernel_launches
+            with torch.cuda.stream(stream):
+                ev0.record(stream)
+                for sl in newest:
+                    ctx.frames_refresh(sl)
+                bat.iteration(2)
+                ev1.record(stream)
+            timed_launches[0] += ctx.kernel_launches - l0
+            ev1.synchronize()
+            tot += ev0.elapsed_time(ev1)
+        return tot
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    timed_launches[0] = 0
+    t_wall = time.perf_counter()
+    ms = [step() for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall
+    clk = clocks.stop()
+    launches = timed_launches[0]
+    corr_ms, ba_ms = ctx.last_timing()
+    mean_ms = float(np.mean(ms))
+    mean_ms = float(max_over_ranks([mean_ms], device=dev)[0])
+
+    # e2e through the public API with host buffers: per chunk, the newest frame
+    # of every sequence from pinned host memory + the iteration + poses/depths back
+    frame0 = torch.randn((H0, W0i, D)).pin_memory()
+    frame0 /= frame0.norm(dim=-1, keepdim=True)
+    frame1 = frame0.view(H1, 4, W1i, 4, D).mean(dim=(1, 3)).contiguous().pin_memory()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    n_e2e = max(1, min(args.steps, 2))
+    for _ in range(n_e2e):
+        for c in range(n_chunks):
+            bat.reset()
+            for sl in newest:
+                ctx.frames_upload(sl, frame0.numpy(), frame1.numpy())
+            bat.iteration(2)
+            bat.read()
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - t0) / n_e2e * 1e3
+    e2e_ms = float(max_over_ranks([e2e_ms], device=dev)[0])
+    h2d = n_chunks * chunk * (frame0.numel() + frame1.numel()) * 4
+    d2h = n_chunks * (bat.n_poses * 7 * 8 + bat.n_patches * 8 + chunk * (66 * 8 + 4))
+    res = bat.read()
+    gathered = gather_poses(np.concatenate([r[0] for r in res]), device=dev)
+    assert len(gathered) == world
+    if rank != 0:
+        return
+    E_total = E_chunk * n_chunks * world
+    line = {
+        "metric": METRIC, "value": E_total / (mean_ms * 1e-3), "unit": "edge-iterations/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 corr (f64 coords/weights), f64 BA", "data": "synthetic",
+        "config": {"workload": "c5", "desc": "batch of independent sequences at the DPVO default window, "
+                   "sharded by sequence", "sequences_total": n_seq * world, "sequences_per_gpu": n_seq,
+                   "chunk": chunk, "chunks_per_gpu": n_chunks, "edges_per_gpu": E_chunk * n_chunks,
+                   "distinct_trajectories_per_gpu": len(geos), "frames_per_sequence": F,
+                   "parallelism": f"sequence-sharded x{world}",
+                   "l2": f"inputs ({chunk * F * 10.4 / 1024:.1f} GB frame store per chunk) far larger than L2"},
+        "last_chunk_corr_ms": corr_ms, "last_chunk_ba_ms": ba_ms,
+        "e2e": {"value": E_total / (e2e_ms * 1e-3), "unit": "edge-iterations/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms},
+        "gpu_launches": int(launches), "clocks": clk, "wall_s_timed_region": t_wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_e2e(args, w, prob, ctx, stream, win):
     """Same step through the public API with HOST buffers: upload the newest
     frame's pyramid and the window state, run, read back the corr volume and
@@ -410,7 +561,10 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--sequences", type=int, default=1024, help="c5: sequences in the whole job")
+    ap.add_argument("--chunk", type=int, default=256, help="c5: sequences per device launch")
+    ap.add_argument("--distinct", type=int, default=32, help="c5: distinct trajectories per rank")
     ap.add_argument("--ref-edges", type=int, default=256)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -427,7 +581,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     try:
-        run_ours(args, rank, world, local_rank)
+        if args.config == "c5":
+            run_batch(args, rank, world, local_rank)
+        else:
+            run_ours(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

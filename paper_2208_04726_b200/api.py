@@ -151,6 +151,11 @@ class Context:
     def frames_refresh(self, slot: int) -> None:
         check(lib.pvo_frames_refresh(self.handle, slot))
 
+    def frames_device_ptrs(self) -> tuple[int, int]:
+        a, b = C.c_void_p(), C.c_void_p()
+        check(lib.pvo_frames_device_ptrs(self.handle, C.addressof(a), C.addressof(b)))
+        return a.value, b.value
+
 
 _default: Optional[Context] = None
 
