@@ -537,9 +537,17 @@ def run_e2e(args, w, prob, ctx, stream, win):
     h2d = l0.numel() * 4 + l1.numel() * 4 + sum(np.asarray(a).nbytes for a in arrays)
     d2h = vol.numel() * 4 + prob["poses"].nbytes + prob["depth"].nbytes + 8 * 3
 
+    def pinned(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+
+    hp = dict(prob)  # the step's host inputs live in pinned memory (DMA straight from the caller's arrays)
+    for k in ("poses", "fixed", "pose_frames", "patch_src", "patch_x", "patch_y", "depth", "patch_feats",
+              "e_patch", "e_pose", "e_delta", "e_weight"):
+        hp[k] = pinned(prob[k])
+
     def one():
         ctx.frames_upload(F - 1, l0.numpy(), l1.numpy())
-        win.load(prob, prob["pose_frames"], prob["patch_feats"], w.K, w.image)
+        win.load(hp, hp["pose_frames"], hp["patch_feats"], w.K, w.image)
         win.iteration(2, corr_out=vol_np)
         return win.read()
 

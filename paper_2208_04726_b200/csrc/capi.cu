@@ -164,6 +164,9 @@ struct pvo_ctx {
     Window win;
     Batch bat;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    // copy stream: device->host read-back of the correlation volume overlaps the BA kernels
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_corr = nullptr, ev_copy = nullptr;
     bool timing_pending = false;
     bool tracing = false;  // record BA phase clocks (pvo_ctx_set_tracing)
 };
@@ -620,6 +623,9 @@ int pvo_ctx_create(int device, pvo_ctx** out) {
         ctx->own_stream = true;
         cuda_check(cudaMalloc(&ctx->d_status, sizeof(int)), "cudaMalloc");
         for (auto& e : ctx->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+        cuda_check(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        cuda_check(cudaEventCreateWithFlags(&ctx->ev_corr, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming), "cudaEventCreate");
         *out = ctx;
     });
 }
@@ -639,6 +645,12 @@ int pvo_ctx_destroy(pvo_ctx* ctx) {
         if (ctx->d_status) cudaFree(ctx->d_status);
         for (auto& e : ctx->ev)
             if (e) cudaEventDestroy(e);
+        if (ctx->copy_stream) {
+            cudaStreamSynchronize(ctx->copy_stream);
+            cudaStreamDestroy(ctx->copy_stream);
+        }
+        if (ctx->ev_corr) cudaEventDestroy(ctx->ev_corr);
+        if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
         if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
         delete ctx;
     });
@@ -1051,8 +1063,7 @@ int pvo_window_load(pvo_ctx* ctx, int n_poses, const double* poses, const uint8_
             std::vector<int> eslot(n_edges);
             for (int e = 0; e < n_edges; ++e) eslot[e] = pose_slot[e_pose[e]];
             const std::vector<int> order = slot_order(n_edges, eslot.data());
-            upload(ctx, w.order, order.data(), order.size());
-            sync(ctx);
+            upload(ctx, w.order, order.data(), order.size());  // pageable source: staged before return
         }
         upload(ctx, w.patch_feats, patch_feats, (size_t)n_patches * 2 * 9 * ctx->C);
         upload(ctx, w.init_poses, poses, (size_t)n_poses * 7);
@@ -1175,13 +1186,20 @@ int pvo_window_iteration(pvo_ctx* ctx, int iterations, double damping, float* co
         cuda_check(cudaEventRecord(ctx->ev[0], ctx->stream), "event");
         run_corr(ctx, window_corr_params(ctx, corr_memspace == PVO_DEVICE ? corr_out : nullptr));
         cuda_check(cudaEventRecord(ctx->ev[1], ctx->stream), "event");
+        const bool readback = corr_out && corr_memspace != PVO_DEVICE;
+        if (readback) {  // the volume's D2H runs on the copy stream, under the BA kernels
+            cuda_check(cudaEventRecord(ctx->ev_corr, ctx->stream), "event");
+            cuda_check(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_corr, 0), "stream wait");
+            cuda_check(cudaMemcpyAsync(corr_out, w.corr.p, sizeof(float) * (size_t)w.n_edges * 2 * 9 * 49,
+                                       cudaMemcpyDeviceToHost, ctx->copy_stream),
+                       "D2H");
+            cuda_check(cudaEventRecord(ctx->ev_copy, ctx->copy_stream), "event");
+        }
         pvo_dev::BAParams a = window_ba_params(ctx, iterations, damping);
         launch_ba_checked(ctx, a, w.plan);
         cuda_check(cudaEventRecord(ctx->ev[2], ctx->stream), "event");
         ctx->timing_pending = true;
-        if (corr_out && corr_memspace != PVO_DEVICE) {
-            download(ctx, corr_out, static_cast<float*>(w.corr.p), (size_t)w.n_edges * 2 * 9 * 49);
-        }
+        if (readback) cuda_check(cudaStreamWaitEvent(ctx->stream, ctx->ev_copy, 0), "stream wait");
     });
 }
 

@@ -33,7 +33,8 @@ for k, v, u in own:
 
 
 def raw(rep, names):
-    txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv", "--print-units", "base"], capture_output=True,
+                         text=True).stdout
     r = list(csv.reader(txt.splitlines()))
     hh, vv = r[0], r[2]
     return {n: vv[hh.index(n)] for n in names if n in hh}
@@ -50,14 +51,16 @@ tot = sum(sum(v) for v in per.values())
 for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
     lines.append(f"| {k} | {len(v)} | {sum(v) / len(v) / 1000:.1f} | {100 * sum(v) / tot:.1f}% |")
 traffic = None
-for name in ("corr_full", "ba_full"):
+names = sorted(f.name[len(tag) + 1:-len(".ncu-rep")] for f in src.glob(f"{tag}_*_full.ncu-rep"))
+traffic_by_cfg = {}
+for name in names:
     rep = src / f"{tag}_{name}.ncu-rep"
     if not rep.exists():
         continue
     d = raw(rep, M)
     lines += ["", f"## `--set full` capture: {name}", "", "| metric | value |", "|---|---|"]
     lines += [f"| {k} | {v} |" for k, v in d.items()]
-    if name == "corr_full":
+    if name.startswith("corr"):
         def mb(x):
             x = x.replace(",", "")
             return float(x)
@@ -68,8 +71,11 @@ for name in ("corr_full", "ba_full"):
         r = list(csv.reader(txt.splitlines()))
         hh, vv = r[0], r[2]
         traffic = mb(vv[hh.index("dram__bytes_read.sum")]) + mb(vv[hh.index("dram__bytes_write.sum")])
+        cfg = name.split("_")[1] if name.count("_") >= 2 else "c2"
+        traffic_by_cfg[cfg] = traffic
 (out_dir / f"{tag}_ncu_summary.md").write_text("\n".join(lines) + "\n")
-if traffic is not None:
-    (out_dir / "corr_traffic.json").write_text(json.dumps({"c2": traffic, "source": f"{tag}_corr_full.ncu-rep"}) + "\n")
+if traffic_by_cfg:
+    traffic_by_cfg["source"] = f"{tag}_corr*_full.ncu-rep (dram__bytes_read.sum + dram__bytes_write.sum, one launch)"
+    (out_dir / "corr_traffic.json").write_text(json.dumps(traffic_by_cfg) + "\n")
 print("\n".join(lines))
 print("traffic", traffic)
