@@ -1,0 +1,63 @@
+// Micro-benchmark of the in-CTA pose solve (ldlt_solve_cta) on one CTA, clock64.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include -DPVO_LDLT_BLOCK=8 \
+//      -o tools/micro_solve tools/micro_solve.cu
+__device__ long long g_ph[8];
+#define SOLVE_PROBE_BEGIN long long _pt = clock64(); if (threadIdx.x == 0) for (int _i = 0; _i < 8; ++_i) g_ph[_i] = 0;
+#define SOLVE_PROBE(i) if (threadIdx.x == 0) { const long long _t = clock64(); g_ph[i] += _t - _pt; _pt = _t; }
+#include "../paper_2208_04726_b200/csrc/ba.cu"
+#include <cstdio>
+#include <vector>
+namespace pvo_dev {
+namespace {
+__global__ void micro(const double* sys, int np, double* x, long long* t) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Layout L = make_layout(np, 0);
+    __syncthreads();
+    const long long t0 = clock64();
+    const bool ok = ldlt_solve_cta(sys, np, smem, L, x);
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) {
+        t[0] = t1 - t0;
+        t[1] = ok;
+        printf("  stage+perm %lld diag %lld panel %lld trailing %lld backsub %lld\n", g_ph[0], g_ph[1], g_ph[2], g_ph[3], g_ph[4]);
+    }
+}
+}  // namespace
+}  // namespace pvo_dev
+int main() {
+    for (int np : {42, 60, 96}) {
+        const int nent = np * (np + 1) / 2;
+        std::vector<double> h(nent + np), A((size_t)np * np), b(np);
+        int e = 0;
+        for (int i = 0; i < np; ++i)
+            for (int j = i; j < np; ++j) {
+                const double v = (i == j) ? np + 1.0 + i : 0.5 / (1 + i + j);
+                h[e++] = v;
+                A[i * np + j] = A[j * np + i] = v;
+            }
+        for (int i = 0; i < np; ++i) h[nent + i] = b[i] = 1.0 + i;
+        double *dsys, *dx;
+        long long* dt;
+        cudaMalloc(&dsys, sizeof(double) * h.size());
+        cudaMalloc(&dx, sizeof(double) * np);
+        cudaMalloc(&dt, 2 * sizeof(long long));
+        cudaMemcpy(dsys, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice);
+        const pvo_dev::Layout L = pvo_dev::make_layout(np, 0);
+        cudaFuncSetAttribute(pvo_dev::micro, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
+        long long t[2];
+        for (int rep = 0; rep < 3; ++rep) {
+            pvo_dev::micro<<<1, 256, L.total>>>(dsys, np, dx, dt);
+            cudaMemcpy(t, dt, sizeof(t), cudaMemcpyDeviceToHost);
+        }
+        std::vector<double> x(np);
+        cudaMemcpy(x.data(), dx, sizeof(double) * np, cudaMemcpyDeviceToHost);
+        double res = 0;  // residual |A x - b|
+        for (int i = 0; i < np; ++i) {
+            double s = -b[i];
+            for (int j = 0; j < np; ++j) s += A[i * np + j] * x[j];
+            res = fmax(res, fabs(s));
+        }
+        printf("np=%d cycles=%lld ok=%lld residual=%.2e (%s)\n", np, t[0], t[1], res,
+               cudaGetErrorString(cudaGetLastError()));
+    }
+}
