@@ -174,6 +174,21 @@ int pvo_window_read(pvo_ctx* ctx, double* poses, double* inv_depth, double* resi
 /* Device pointer of the window's correlation volume buffer [E][2][pp][49]. */
 int pvo_window_corr_ptr(pvo_ctx* ctx, float** corr);
 
+/* ---- correlation flow provider (flow_provider.cpp:150-312) --
+ * pvo_measure_batch: CorrelationFlowProvider::measure per edge against the
+ * frame store: centers [E][2] = reproject_patch(...).points[centre], behind
+ * [E] (may be NULL), patch_feats [P][2][9][C] (C <= 128).  Out: delta [E][2],
+ * weight [E][2] (FP64), flags [E] (1 flat, 2 out of range, 4 behind camera;
+ * may be NULL).  pvo_window_propose: the same over the resident window at its
+ * current state (propose, flow_provider.cpp:289-314); the revisions replace
+ * the window's edge deltas / weights for the next pvo_window_iteration
+ * (pipeline.cpp: propose -> set_revision -> optimize_window).  Outputs may
+ * be NULL (no read-back).                                                   */
+int pvo_measure_batch(pvo_ctx* ctx, int n_edges, int n_patches, int p, const int* e_patch, const int* e_slot,
+                      const double* centers, const uint8_t* behind, const float* patch_feats, double* delta,
+                      double* weight, uint8_t* flags);
+int pvo_window_propose(pvo_ctx* ctx, double* delta, double* weight, uint8_t* flags);
+
 /* ---- batch of independent windows (config 5: sequences sharded per device) -
  * Windows are concatenated: pose/patch/edge offsets [n_windows + 1] (starting
  * at 0); inside a window every index is window-local (as pvo_window_load);

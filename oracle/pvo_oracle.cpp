@@ -13,6 +13,8 @@
 //   camera.cpp:15-108         Patch::make, reproject_patch, reprojection_jacobians
 //   features.cpp:9-52         FeatureGrid::sample_zero_padded / sample_cubic
 //   correlation.cpp:8-71      correlate_at, correlate
+//   flow_provider.cpp:150-287 CorrelationFlowProvider::measure (parabola_refine,
+//                             subpixel_peak) and propose's per-edge part (:289-314)
 //   patch_graph.cpp:27-173    PatchGraph (std::map keyed, same iteration order)
 //   pipeline.cpp:164-181      Pipeline::active_edges
 //   bundle_adjust.cpp:11-375  validate, build_target, schur_solve (Eigen LDLT
@@ -494,6 +496,123 @@ void correlate(int p, int channels, const float* feats0, const float* feats1, co
             }
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// CorrelationFlowProvider::measure (flow_provider.cpp:150-287)
+// ---------------------------------------------------------------------------
+struct Measurement {
+    V2 delta{0, 0};
+    V2 weight{0.01, 0.01};
+    bool flat = false, out_of_range = false;
+};
+
+// flow_provider.cpp:152-162
+double parabola_refine(const float* feature, int channels, const GridView& grid, double x, double y, bool along_x,
+                       double h) {
+    const double f0 = correlate_at_cubic(feature, channels, grid, x - (along_x ? h : 0), y - (along_x ? 0 : h));
+    const double f1 = correlate_at_cubic(feature, channels, grid, x, y);
+    const double f2 = correlate_at_cubic(feature, channels, grid, x + (along_x ? h : 0), y + (along_x ? 0 : h));
+    const double denom = f0 - 2 * f1 + f2;
+    if (std::abs(denom) < 1e-12 || denom > 0) return 0.0;  // not a local max
+    return std::clamp(0.5 * h * (f0 - f2) / denom, -h, h);
+}
+
+// flow_provider.cpp:167-205
+V2 subpixel_peak(const float* feature, int channels, const GridView& grid, V2 base, bool* on_border) {
+    int best_a = kCorrRadius, best_b = kCorrRadius;
+    double best = -std::numeric_limits<double>::infinity();
+    for (int alpha = 0; alpha < kCorrSize; ++alpha) {
+        for (int beta = 0; beta < kCorrSize; ++beta) {
+            const double v =
+                correlate_at(feature, channels, grid, base.x + beta - kCorrRadius, base.y + alpha - kCorrRadius);
+            if (v > best) {
+                best = v;
+                best_a = alpha;
+                best_b = beta;
+            }
+        }
+    }
+    if (on_border) *on_border = best_a == 0 || best_a == kCorrSize - 1 || best_b == 0 || best_b == kCorrSize - 1;
+    double dx = best_b - kCorrRadius, dy = best_a - kCorrRadius;
+    double current = correlate_at_cubic(feature, channels, grid, base.x + dx, base.y + dy);
+    for (const double h : {0.5, 0.25, 0.125, 0.0625, 0.03125, 0.015625}) {
+        for (const bool along_x : {true, false}) {
+            const double step = parabola_refine(feature, channels, grid, base.x + dx, base.y + dy, along_x, h);
+            if (step == 0.0) continue;
+            const double nx = dx + (along_x ? step : 0);
+            const double ny = dy + (along_x ? 0 : step);
+            const double value = correlate_at_cubic(feature, channels, grid, base.x + nx, base.y + ny);
+            if (value >= current) {  // hill climb only
+                dx = nx;
+                dy = ny;
+                current = value;
+            }
+        }
+    }
+    return {dx, dy};
+}
+
+// flow_provider.cpp:209-287; g0 / g1 = the centre pixel's level-0 / level-1 descriptors
+Measurement measure(const float* g0, const float* g1, int channels, const GridView& l0, const GridView& l1,
+                    V2 center) {
+    Measurement m;
+    const V2 base0{center.x / kFeatureStride, center.y / kFeatureStride};
+    double values[kCorrSize * kCorrSize];
+    double peak = -std::numeric_limits<double>::infinity();
+    double minimum = std::numeric_limits<double>::infinity();
+    double mean = 0;
+    int peak_a = 0, peak_b = 0;
+    for (int alpha = 0; alpha < kCorrSize; ++alpha) {
+        for (int beta = 0; beta < kCorrSize; ++beta) {
+            const double v = correlate_at(g0, channels, l0, base0.x + beta - kCorrRadius, base0.y + alpha - kCorrRadius);
+            values[alpha * kCorrSize + beta] = v;
+            mean += v;
+            minimum = std::min(minimum, v);
+            if (v > peak) {
+                peak = v;
+                peak_a = alpha;
+                peak_b = beta;
+            }
+        }
+    }
+    mean /= kCorrSize * kCorrSize;
+    const double peak_to_mean = (peak - minimum) / (mean - minimum + 1e-9);
+    if (!(peak_to_mean >= 1.05)) {
+        m.flat = true;
+        return m;
+    }
+    double second = -std::numeric_limits<double>::infinity();
+    for (int alpha = 0; alpha < kCorrSize; ++alpha) {
+        for (int beta = 0; beta < kCorrSize; ++beta) {
+            if (std::max(std::abs(alpha - peak_a), std::abs(beta - peak_b)) <= 1) continue;
+            second = std::max(second, values[alpha * kCorrSize + beta]);
+        }
+    }
+    const double score = 2.0 * (peak - 0.75) + (peak - second - 0.08);
+    double confidence = std::clamp(1.0 / (1.0 + std::exp(-12.0 * score)), 0.01, 0.99);
+    bool border0 = false, border1 = false;
+    const V2 peak0 = subpixel_peak(g0, channels, l0, base0, &border0);
+    const double s1 = kFeatureStride * kFeatureStride;
+    const V2 peak1 = subpixel_peak(g1, channels, l1, {center.x / s1, center.y / s1}, &border1);
+    const V2 e0{kFeatureStride * peak0.x, kFeatureStride * peak0.y};
+    const V2 e1{s1 * peak1.x, s1 * peak1.y};
+    if (border0 && border1) {
+        m.out_of_range = true;
+        return m;
+    }
+    if (border0) {
+        m.delta = e1;
+        confidence = std::min(confidence, 0.25);
+    } else {
+        m.delta = e0;
+        const double dx = e1.x - e0.x, dy = e1.y - e0.y;
+        if (!border1 && std::sqrt(dx * dx + dy * dy) > 2.0 * kFeatureStride * kFeatureStride) {
+            confidence = std::min(confidence, 0.25);
+        }
+    }
+    m.weight = {confidence, confidence};
+    return m;
 }
 
 // ---------------------------------------------------------------------------
@@ -1332,6 +1451,48 @@ int orc_correlate_batch(int n_edges, const int* e_patch, const int* e_frame, con
         for (auto& th : pool) th.join();
         for (auto& s : errs)
             if (!s.empty()) throw std::invalid_argument(s);
+    });
+}
+
+// CorrelationFlowProvider::propose's per-edge part (flow_provider.cpp:297-312)
+// on flattened inputs: centers [E][2] = reproject_patch(...).points[centre],
+// behind [E]; patch_feats [P][2][p*p][C]; frames [F][H][W][C].
+// Out: delta [E][2], weight [E][2], flags [E] (bit 0 flat, bit 1 out_of_range,
+// bit 2 behind the camera).
+int orc_measure_batch(int n_edges, const int* e_patch, const int* e_frame, const double* centers,
+                      const uint8_t* behind, int p, int channels, const float* patch_feats, const float* frames0,
+                      int w0, int h0, const float* frames1, int w1, int h1, double* delta, double* weight,
+                      uint8_t* flags, int threads) {
+    return guard([&] {
+        const size_t pp = static_cast<size_t>(p) * p;
+        const size_t f0 = static_cast<size_t>(w0) * h0 * channels, f1 = static_cast<size_t>(w1) * h1 * channels;
+        const int nt = threads > 0 ? threads : 1;
+        auto work = [&](int t) {
+            for (int e = t; e < n_edges; e += nt) {
+                Measurement m;
+                uint8_t fl = 0;
+                if (behind && behind[e]) {
+                    fl = 4;  // weight (0.01, 0.01), delta 0 (flow_provider.cpp:301-302)
+                } else {
+                    const float* g = patch_feats + static_cast<size_t>(e_patch[e]) * 2 * pp * channels;
+                    const size_t cp = pp / 2;  // centre pixel (patch.size() / 2)
+                    m = measure(g + cp * channels, g + (pp + cp) * channels, channels,
+                                GridView{frames0 + e_frame[e] * f0, w0, h0, channels},
+                                GridView{frames1 + e_frame[e] * f1, w1, h1, channels},
+                                {centers[2 * e], centers[2 * e + 1]});
+                    fl = (m.flat ? 1 : 0) | (m.out_of_range ? 2 : 0);
+                }
+                delta[2 * e] = m.delta.x;
+                delta[2 * e + 1] = m.delta.y;
+                weight[2 * e] = m.weight.x;
+                weight[2 * e + 1] = m.weight.y;
+                flags[e] = fl;
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+        work(0);
+        for (auto& th : pool) th.join();
     });
 }
 

@@ -168,6 +168,24 @@ def correlate_batch(e_patch, e_frame, coords, patch_feats, frames0, frames1, thr
     return out
 
 
+def measure_batch(e_patch, e_frame, centers, behind, patch_feats, frames0, frames1, threads=1):
+    """CorrelationFlowProvider::measure per edge (flow_provider.cpp:209-312):
+    -> delta [E, 2], weight [E, 2], flags [E] (1 flat, 2 out of range, 4 behind)."""
+    ep = np.ascontiguousarray(e_patch, np.int32)
+    ef = np.ascontiguousarray(e_frame, np.int32)
+    cs = _f64(centers)
+    bh = None if behind is None else np.ascontiguousarray(behind, np.uint8)
+    pf = np.ascontiguousarray(patch_feats, np.float32)
+    f0 = np.ascontiguousarray(frames0, np.float32)
+    f1 = np.ascontiguousarray(frames1, np.float32)
+    E = ep.shape[0]
+    d, w, fl = np.empty((E, 2)), np.empty((E, 2)), np.empty(E, np.uint8)
+    check(lib.orc_measure_batch(I(E), _p(ep), _p(ef), _p(cs), _p(bh), I(3), I(pf.shape[-1]), _p(pf), _p(f0),
+                                I(f0.shape[2]), I(f0.shape[1]), _p(f1), I(f1.shape[2]), I(f1.shape[1]), _p(d), _p(w),
+                                _p(fl), I(threads)))
+    return d, w, fl
+
+
 def correlate_at(feature, grid, x, y):
     f = np.ascontiguousarray(feature, np.float32)
     g = np.ascontiguousarray(grid, np.float32)

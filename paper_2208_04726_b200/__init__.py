@@ -28,6 +28,7 @@ from .api import (  # noqa: F401
     default_context,
     gauss_newton_step,
     inverse,
+    measure_batch,
     optimize_window,
     reproject_patch,
     reproject_patches,

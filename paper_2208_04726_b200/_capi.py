@@ -63,6 +63,8 @@ SIGNATURES = {
     "pvo_window_correlate": (i32, [vp, P, i32]),
     "pvo_window_read": (i32, [vp, P, P, P, P]),
     "pvo_window_corr_ptr": (i32, [vp, P]),
+    "pvo_measure_batch": (i32, [vp, i32, i32, i32, P, P, P, P, P, P, P, P]),
+    "pvo_window_propose": (i32, [vp, P, P, P]),
     "pvo_batch_load": (i32, [vp, i32, P, P, P, P, P, P, i32, P, P, P, P, P, P, P, P, P, P, i32, i32]),
     "pvo_batch_reset": (i32, [vp]),
     "pvo_batch_iteration": (i32, [vp, i32, f64, P, i32]),

@@ -338,6 +338,22 @@ def correlate_batch(e_patch, e_slot, coords, patch_feats, ctx: Optional[Context]
     return out
 
 
+def measure_batch(e_patch, e_slot, centers, patch_feats, behind=None, ctx: Optional[Context] = None):
+    """CorrelationFlowProvider::measure per edge (flow_provider.cpp:209-312) against the
+    context's frame store -> (delta [E, 2], weight [E, 2], flags [E]: 1 flat,
+    2 out of range, 4 behind the camera)."""
+    c = _ctx(ctx)
+    ep, es = _i32(e_patch), _i32(e_slot)
+    cs = _f64(centers).reshape(-1, 2)
+    bh = None if behind is None else _u8(behind)
+    pf = _f32(patch_feats)
+    E = ep.shape[0]
+    d, w, fl = np.empty((E, 2)), np.empty((E, 2)), np.empty(E, np.uint8)
+    check(lib.pvo_measure_batch(c.handle, E, pf.shape[0], 3, _ptr(ep), _ptr(es), _ptr(cs),
+                                None if bh is None else _ptr(bh), _ptr(pf), _ptr(d), _ptr(w), _ptr(fl)))
+    return d, w, fl
+
+
 # ---------------------------------------------------------------------------
 # bundle adjustment (bundle_adjust.hpp:15-111)
 # ---------------------------------------------------------------------------
@@ -634,6 +650,16 @@ class Window:
         nn = C.c_int()
         check(lib.pvo_window_read(self.ctx.handle, _ptr(poses), _ptr(d), _ptr(norms), C.addressof(nn)))
         return poses, d, list(norms[: nn.value])
+
+    def propose(self, read_back: bool = True):
+        """CorrelationFlowProvider::propose at the current state; the revisions become
+        the window's edge deltas / weights for the next iteration."""
+        if not read_back:
+            check(lib.pvo_window_propose(self.ctx.handle, None, None, None))
+            return None
+        d, w, fl = np.empty((self.n_edges, 2)), np.empty((self.n_edges, 2)), np.empty(self.n_edges, np.uint8)
+        check(lib.pvo_window_propose(self.ctx.handle, _ptr(d), _ptr(w), _ptr(fl)))
+        return d, w, fl
 
     def corr_device_ptr(self) -> int:
         p = C.c_void_p()

@@ -34,7 +34,10 @@ NVCC_FLAGS = [
     "-I",
     str(ROOT / "include"),
 ]
-SOURCES = ["corr.cu", "corr_tma.cu", "ba.cu", "ba_large.cu", "capi.cu", "graph.cpp"]
+SOURCES = ["corr.cu", "corr_tma.cu", "ba.cu", "ba_large.cu", "measure.cu", "capi.cu", "graph.cpp"]
+# per-file extra flags: the provider measurement rounds every product / sum like the
+# x86-64 reference build (no FMA contraction), so its discrete decisions agree
+EXTRA = {"measure.cu": ["--fmad=false"]}
 
 
 def nvcc() -> str:
@@ -58,7 +61,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         objs.append(o)
         if not force and o.exists() and o.stat().st_mtime >= max(s.stat().st_mtime, newest_header):
             continue
-        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", str(s), "-o", str(o)]
+        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *EXTRA.get(src, []), "-c", str(s), "-o", str(o)]
         if src.endswith(".cu"):
             cmd[1:1] = ["-Xptxas", "-v"] if verbose else []
         if verbose:

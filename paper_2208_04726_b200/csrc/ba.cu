@@ -737,6 +737,7 @@ __device__ void ba_window_body(const BAParams& a, bool batched) {
                     if (__syncthreads_or(bad) && tid == 0) set_status(status, kDevNonFinitePose);
                 }
             }
+            if (clk && attempt_no == 0) a.phase_clocks[15 * 8 + 2] = clock64();  // solve done (first attempt)
             for (int i = tid; i < a.n_poses; i += kThreads) {
                 const int slot = structure ? -1 : a.pose_free_slot[i];
                 const SE3 p = se3_load(pose + 7 * i);

@@ -111,7 +111,7 @@ struct Window {
     int n_poses = 0, n_patches = 0, n_edges = 0;
     Plan plan;
     HostProblem shape;  // sizes, K, image size (pointers unused)
-    DevBuf pose_slot, patch_feats, corr, init_poses, init_depth, order;
+    DevBuf pose_slot, patch_feats, corr, init_poses, init_depth, order, flags;
 };
 
 // Batch of independent windows (config 5: many sequences per device).  All
@@ -638,7 +638,7 @@ int pvo_ctx_destroy(pvo_ctx* ctx) {
         DevBuf* bufs[] = {&ctx->feat0, &ctx->feat1, &ctx->gram0, &ctx->gram1, &ctx->s0, &ctx->s1, &ctx->s2,
                           &ctx->s3,    &ctx->s4,    &ctx->s5,    &ctx->s6,    &ctx->s7, &ctx->s8,
                           &ctx->win.pose_slot, &ctx->win.patch_feats, &ctx->win.corr, &ctx->win.init_poses,
-                          &ctx->win.init_depth};
+                          &ctx->win.init_depth, &ctx->win.order, &ctx->win.flags};
         for (DevBuf* b : bufs) b->release();
         ctx->ba.release();
         ctx->bat.release();
@@ -1221,6 +1221,93 @@ int pvo_window_read(pvo_ctx* ctx, double* poses, double* depth, double* residual
             sync(ctx);
         }
         if (n_norms) *n_norms = n;
+    });
+}
+
+// ---- flow-provider measurement (flow_provider.cpp:150-312) -------------------
+int pvo_measure_batch(pvo_ctx* ctx, int n_edges, int n_patches, int p, const int* e_patch, const int* e_slot,
+                      const double* centers, const uint8_t* behind, const float* patch_feats, double* delta,
+                      double* weight, uint8_t* flags) {
+    return guarded([&] {
+        bind(ctx);
+        ensure_p3(p);
+        if (ctx->nf == 0) fail(PVO_INVALID_ARGUMENT, "measure_batch: frame store is empty (pvo_frames_reserve)");
+        if (n_edges < 0 || n_patches < 0) fail(PVO_INVALID_ARGUMENT, "measure_batch: bad sizes");
+        if (n_edges == 0) return;
+        if (ctx->C > 128) fail(PVO_UNSUPPORTED, "measure_batch: more than 128 channels");
+        for (int e = 0; e < n_edges; ++e) {
+            if (e_patch[e] < 0 || e_patch[e] >= n_patches) fail(PVO_OUT_OF_RANGE, "measure_batch: bad patch index");
+            if (e_slot[e] < 0 || e_slot[e] >= ctx->nf) fail(PVO_OUT_OF_RANGE, "measure_batch: bad frame slot");
+        }
+        pvo_dev::MeasureParams m;
+        m.n_edges = n_edges;
+        m.channels = ctx->C;
+        m.e_patch = upload(ctx, ctx->s0, e_patch, n_edges);
+        m.e_slot = upload(ctx, ctx->s1, e_slot, n_edges);
+        m.centers = upload(ctx, ctx->s2, centers, (size_t)n_edges * 2);
+        m.behind = behind ? upload(ctx, ctx->s5, behind, n_edges) : nullptr;
+        m.patch_feats = upload(ctx, ctx->s3, patch_feats, (size_t)n_patches * 2 * 9 * ctx->C);
+        m.feat0 = static_cast<const float*>(ctx->feat0.p);
+        m.feat1 = static_cast<const float*>(ctx->feat1.p);
+        m.w0 = ctx->w0;
+        m.h0 = ctx->h0;
+        m.w1 = ctx->w1;
+        m.h1 = ctx->h1;
+        double* dd = ctx->s4.as<double>((size_t)n_edges * 4);
+        m.delta = dd;
+        m.weight = dd + (size_t)n_edges * 2;
+        m.flags = ctx->s6.as<uint8_t>(n_edges);
+        m.status = ctx->d_status;
+        reset_status(ctx);
+        cuda_check(pvo_dev::launch_measure(m, ctx->stream), "measure kernel");
+        ctx->launches += 1;
+        download(ctx, delta, m.delta, (size_t)n_edges * 2);
+        download(ctx, weight, m.weight, (size_t)n_edges * 2);
+        if (flags) download(ctx, flags, m.flags, n_edges);
+        if (read_status(ctx) & (1 << pvo_dev::kDevBadCoords)) fail(PVO_INVALID_ARGUMENT, "measure: non-finite centre");
+    });
+}
+
+// CorrelationFlowProvider::propose over the resident window's edges: measure at
+// the current state and store the revisions (delta, weight) as the window's
+// edge revisions, which the next pvo_window_iteration freezes into targets
+// (pipeline.cpp:183-198: propose -> set_revision -> optimize_window).
+int pvo_window_propose(pvo_ctx* ctx, double* delta_out, double* weight_out, uint8_t* flags_out) {
+    return guarded([&] {
+        bind(ctx);
+        Window& w = ctx->win;
+        if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
+        if (ctx->C > 128) fail(PVO_UNSUPPORTED, "window_propose: more than 128 channels");
+        BABuffers& B = ctx->ba;
+        pvo_dev::MeasureParams m;
+        m.n_edges = w.n_edges;
+        m.channels = ctx->C;
+        m.e_patch = static_cast<const int*>(B.e_patch.p);
+        m.e_pose = static_cast<const int*>(B.e_pose.p);
+        m.pose_slot = static_cast<const int*>(w.pose_slot.p);
+        m.poses = static_cast<const double*>(B.poses.p);
+        m.patch_src = static_cast<const int*>(B.patch_src.p);
+        m.patch_x = static_cast<const double*>(B.px.p);
+        m.patch_y = static_cast<const double*>(B.py.p);
+        m.depth = static_cast<const double*>(B.depth.p);
+        m.K = static_cast<const double*>(B.K.p);
+        m.patch_feats = static_cast<const float*>(w.patch_feats.p);
+        m.feat0 = static_cast<const float*>(ctx->feat0.p);
+        m.feat1 = static_cast<const float*>(ctx->feat1.p);
+        m.w0 = ctx->w0;
+        m.h0 = ctx->h0;
+        m.w1 = ctx->w1;
+        m.h1 = ctx->h1;
+        m.delta = static_cast<double*>(B.e_in.p);  // the window's revisions, edge order = load order
+        m.weight = static_cast<double*>(B.e_w.p);
+        m.flags = w.flags.as<uint8_t>(w.n_edges);
+        m.status = ctx->d_status;
+        cuda_check(pvo_dev::launch_measure(m, ctx->stream), "measure kernel");
+        ctx->launches += 1;
+        if (delta_out) download(ctx, delta_out, m.delta, (size_t)w.n_edges * 2);
+        if (weight_out) download(ctx, weight_out, m.weight, (size_t)w.n_edges * 2);
+        if (flags_out) download(ctx, flags_out, m.flags, w.n_edges);
+        if (delta_out || weight_out || flags_out) sync(ctx);
     });
 }
 

@@ -75,6 +75,35 @@ int corr_tma_extra_cap(int n_edges, int grid);
 cudaError_t launch_corr_tma(const CorrTmaParams& p, const CUtensorMap* maps, int num_sms, cudaStream_t stream);
 cudaError_t launch_gram(const float* feat, float* gram, int W, int H, int D, int num_sms, cudaStream_t stream);
 
+// Flow-provider measurement per edge (measure.cu): CorrelationFlowProvider::
+// measure + propose's per-edge part (flow_provider.cpp:150-312), FP64.
+struct MeasureParams {
+    int n_edges = 0;
+    int channels = 0;                   // <= 128
+    const int* e_patch = nullptr;       // [E]
+    const int* e_slot = nullptr;        // [E] frame-store slot, or null (pose_slot[e_pose])
+    const int* e_pose = nullptr;
+    const int* pose_slot = nullptr;
+    // explicit centres [E][2] + behind flags, or null: reproject the state below
+    const double* centers = nullptr;
+    const uint8_t* behind = nullptr;
+    const double* poses = nullptr;
+    const int* patch_src = nullptr;
+    const double* patch_x = nullptr;
+    const double* patch_y = nullptr;
+    const double* depth = nullptr;
+    const double* K = nullptr;          // device [4]
+    const float* patch_feats = nullptr; // [P][2][9][C]
+    const float* feat0 = nullptr;       // frame store [slot][H][W][C]
+    const float* feat1 = nullptr;
+    int w0 = 0, h0 = 0, w1 = 0, h1 = 0;
+    double* delta = nullptr;            // [E][2]
+    double* weight = nullptr;           // [E][2]
+    uint8_t* flags = nullptr;           // [E] 1 flat, 2 out of range, 4 behind, 8 non-finite (optional)
+    int* status = nullptr;
+};
+cudaError_t launch_measure(const MeasureParams& p, cudaStream_t stream);
+
 // Device status word values (ba.cu / corr.cu) -> pvo_status on the host.
 enum DevStatus : int {
     kDevOk = 0,

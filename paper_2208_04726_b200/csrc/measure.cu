@@ -1,0 +1,286 @@
+// measure.cu — the correlation flow provider's per-edge measurement (§8f row 1),
+// sm_100a, FP64 like the reference.
+//
+// Reference: CorrelationFlowProvider::measure / subpixel_peak / parabola_refine
+// (flow_provider.cpp:150-287) and propose's per-edge part (:297-312), over
+// correlate_at / correlate_at_cubic (correlation.cpp:8-35) and the
+// zero-padded bilinear / Catmull-Rom samplers (features.cpp:9-52).
+//
+// One warp per edge, lanes over channels (C <= 128: four channels per lane,
+// the centre pixel's descriptors of both levels held in registers).  Every
+// correlation sample is the reference's per-channel FP64 formula with the
+// reference's operation order (this file is compiled with --fmad=false, so
+// every product and sum rounds like the x86-64 reference build); only the
+// channel sum is a warp tree instead of a sequential loop (a difference of a
+// few ulp).  Work per edge: the 7x7 level-0 slice (shared by the flatness /
+// sharpness scores and the level-0 subpixel peak, which the reference
+// evaluates twice with identical arguments), the 7x7 level-1 slice, then two
+// hill climbs of at most 1 + 6 x 2 x 3 Catmull-Rom samples each (the centre
+// value f1 of every parabola step IS the current value: reused).
+#include <cuda_runtime.h>
+
+#include <math_constants.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "ba_common.cuh"
+#include "kernels.cuh"
+
+namespace pvo_dev {
+
+namespace {
+
+constexpr int kR = 3, kS = 7;  // kCorrRadius, kCorrSize (correlation.hpp:11-12)
+constexpr double kStride = 4.0;  // kFeatureStride (features.hpp:46)
+constexpr int kCh = 4;           // channels per lane (C <= 128)
+
+struct Level {
+    const float* f;  // [H][W][C] of this edge's target frame
+    int W, H;
+};
+
+// correlate_at (correlation.cpp:8-23) with sample_zero_padded (features.cpp:9-21)
+__device__ double corr_bilinear(const Level& L, int C, const float (&g)[kCh], double x, double y) {
+    const int lane = threadIdx.x & 31;
+    const double fx = floor(x), fy = floor(y);
+    const int x0 = (int)fx, y0 = (int)fy;
+    const double ax = x - x0, ay = y - y0;
+    const double w00 = (1 - ax) * (1 - ay), w10 = ax * (1 - ay), w01 = (1 - ax) * ay, w11 = ax * ay;
+    const bool in00 = x0 >= 0 && y0 >= 0 && x0 < L.W && y0 < L.H;
+    const bool in10 = x0 + 1 >= 0 && y0 >= 0 && x0 + 1 < L.W && y0 < L.H;
+    const bool in01 = x0 >= 0 && y0 + 1 >= 0 && x0 < L.W && y0 + 1 < L.H;
+    const bool in11 = x0 + 1 >= 0 && y0 + 1 >= 0 && x0 + 1 < L.W && y0 + 1 < L.H;
+    const float* p00 = L.f + ((size_t)y0 * L.W + x0) * C;
+    const float* p10 = p00 + C;
+    const float* p01 = p00 + (size_t)L.W * C;
+    const float* p11 = p01 + C;
+    double dot = 0, nrm = 0;
+#pragma unroll
+    for (int k = 0; k < kCh; ++k) {
+        const int c = lane + 32 * k;
+        if (c < C) {
+            const double v00 = in00 ? (double)__ldg(p00 + c) : 0.0;
+            const double v10 = in10 ? (double)__ldg(p10 + c) : 0.0;
+            const double v01 = in01 ? (double)__ldg(p01 + c) : 0.0;
+            const double v11 = in11 ? (double)__ldg(p11 + c) : 0.0;
+            const double v = w00 * v00 + w10 * v10 + w01 * v01 + w11 * v11;
+            dot += (double)g[k] * v;
+            nrm += v * v;
+        }
+    }
+    dot = warp_sum(dot);
+    nrm = warp_sum(nrm);
+    return nrm > 1e-12 ? dot / sqrt(nrm) : 0.0;
+}
+
+__device__ __forceinline__ void cubic_weights(double t, double w[4]) {  // features.cpp:29-34
+    w[0] = ((-0.5 * t + 1.0) * t - 0.5) * t;
+    w[1] = (1.5 * t - 2.5) * t * t + 1.0;
+    w[2] = ((-1.5 * t + 2.0) * t + 0.5) * t;
+    w[3] = (0.5 * t - 0.5) * t * t;
+}
+
+// correlate_at_cubic (correlation.cpp:25-35) with sample_cubic (features.cpp:23-52)
+__device__ double corr_cubic(const Level& L, int C, const float (&g)[kCh], double x, double y) {
+    const int lane = threadIdx.x & 31;
+    const int x0 = (int)floor(x), y0 = (int)floor(y);
+    double wx[4], wy[4];
+    cubic_weights(x - x0, wx);
+    cubic_weights(y - y0, wy);
+    double dot = 0, nrm = 0;
+#pragma unroll
+    for (int k = 0; k < kCh; ++k) {
+        const int c = lane + 32 * k;
+        if (c < C) {
+            double v = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int yi = y0 - 1 + j;
+                if (yi < 0 || yi >= L.H) continue;
+                double row = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int xi = x0 - 1 + i;
+                    if (xi < 0 || xi >= L.W) continue;
+                    row += wx[i] * (double)__ldg(L.f + ((size_t)yi * L.W + xi) * C + c);
+                }
+                v += wy[j] * row;
+            }
+            dot += (double)g[k] * v;
+            nrm += v * v;
+        }
+    }
+    dot = warp_sum(dot);
+    nrm = warp_sum(nrm);
+    return nrm > 1e-12 ? dot / sqrt(nrm) : 0.0;
+}
+
+// subpixel_peak (flow_provider.cpp:167-205) from the 7x7 slice `vals` (already
+// evaluated at base + (beta - 3, alpha - 3)); returns the offset in cells
+__device__ void subpixel_peak(const Level& L, int C, const float (&g)[kCh], double bx, double by,
+                              const double* vals, double* ox, double* oy, bool* on_border) {
+    int best_a = kR, best_b = kR;
+    double best = -CUDART_INF;
+    for (int alpha = 0; alpha < kS; ++alpha)
+        for (int beta = 0; beta < kS; ++beta) {
+            const double v = vals[alpha * kS + beta];
+            if (v > best) {
+                best = v;
+                best_a = alpha;
+                best_b = beta;
+            }
+        }
+    *on_border = best_a == 0 || best_a == kS - 1 || best_b == 0 || best_b == kS - 1;
+    double dx = best_b - kR, dy = best_a - kR;
+    double current = corr_cubic(L, C, g, bx + dx, by + dy);
+    double h = 0.5;
+    for (int hs = 0; hs < 6; ++hs, h *= 0.5) {
+        for (int ax = 0; ax < 2; ++ax) {
+            const bool along_x = ax == 0;
+            // parabola_refine (flow_provider.cpp:152-162); f1 = the current value
+            const double x = bx + dx, y = by + dy;
+            const double f0 = corr_cubic(L, C, g, x - (along_x ? h : 0), y - (along_x ? 0 : h));
+            const double f1 = current;
+            const double f2 = corr_cubic(L, C, g, x + (along_x ? h : 0), y + (along_x ? 0 : h));
+            const double denom = f0 - 2 * f1 + f2;
+            double step = 0.0;
+            if (!(fabs(denom) < 1e-12 || denom > 0)) step = fmin(fmax(0.5 * h * (f0 - f2) / denom, -h), h);
+            if (step == 0.0) continue;
+            const double nx = dx + (along_x ? step : 0);
+            const double ny = dy + (along_x ? 0 : step);
+            const double value = corr_cubic(L, C, g, bx + nx, by + ny);
+            if (value >= current) {  // hill climb only
+                dx = nx;
+                dy = ny;
+                current = value;
+            }
+        }
+    }
+    *ox = dx;
+    *oy = dy;
+}
+
+__global__ void __launch_bounds__(256) measure_kernel(MeasureParams a) {
+    __shared__ double s_vals[8][2][kS * kS];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int e = blockIdx.x * 8 + warp;
+    if (e >= a.n_edges) return;
+    double cx, cy;
+    bool behind;
+    if (a.centers) {
+        cx = a.centers[2 * e];
+        cy = a.centers[2 * e + 1];
+        behind = a.behind && a.behind[e];
+    } else {  // window mode: reproject_patch of the current state (camera.cpp:47-71)
+        const int k = a.e_patch[e];
+        const SE3 pi = se3_load(a.poses + 7 * a.patch_src[k]);
+        const SE3 pj = se3_load(a.poses + 7 * a.e_pose[e]);
+        const Cam K{a.K[0], a.K[1], a.K[2], a.K[3]};
+        reproject_center(pi, pj, K, a.patch_x + 9 * (size_t)k, a.patch_y + 9 * (size_t)k, a.depth[k], &cx, &cy,
+                         &behind);
+    }
+    double dxo = 0, dyo = 0, wgt = 0.01;
+    int flags = 0;
+    if (behind) {
+        flags = 4;  // flow_provider.cpp:301-302
+    } else if (!isfinite(cx) || !isfinite(cy)) {
+        flags = 8;
+        if (lane == 0) atomicOr(a.status, 1 << kDevBadCoords);
+    } else {
+        const int slot = a.e_slot ? a.e_slot[e] : a.pose_slot[a.e_pose[e]];
+        const Level L0{a.feat0 + (size_t)slot * a.h0 * a.w0 * a.channels, a.w0, a.h0};
+        const Level L1{a.feat1 + (size_t)slot * a.h1 * a.w1 * a.channels, a.w1, a.h1};
+        const float* gp = a.patch_feats + (size_t)a.e_patch[e] * 2 * 9 * a.channels;
+        float g0[kCh], g1[kCh];
+#pragma unroll
+        for (int k = 0; k < kCh; ++k) {
+            const int c = lane + 32 * k;
+            g0[k] = c < a.channels ? gp[4 * a.channels + c] : 0.f;        // centre pixel, level 0
+            g1[k] = c < a.channels ? gp[(9 + 4) * a.channels + c] : 0.f;  // centre pixel, level 1
+        }
+        double* v0 = s_vals[warp][0];
+        double* v1 = s_vals[warp][1];
+        const double b0x = cx / kStride, b0y = cy / kStride;
+        const double b1x = cx / (kStride * kStride), b1y = cy / (kStride * kStride);
+        for (int i = 0; i < kS * kS; ++i) {
+            const int alpha = i / kS, beta = i % kS;
+            const double va = corr_bilinear(L0, a.channels, g0, b0x + beta - kR, b0y + alpha - kR);
+            if (lane == 0) v0[i] = va;
+        }
+        __syncwarp();
+        // flatness / sharpness scores on the level-0 slice (flow_provider.cpp:217-250)
+        double peak = -CUDART_INF, minimum = CUDART_INF, mean = 0;
+        int peak_a = 0, peak_b = 0;
+        for (int i = 0; i < kS * kS; ++i) {
+            const double v = v0[i];
+            mean += v;
+            minimum = fmin(minimum, v);
+            if (v > peak) {
+                peak = v;
+                peak_a = i / kS;
+                peak_b = i % kS;
+            }
+        }
+        mean /= kS * kS;
+        const double peak_to_mean = (peak - minimum) / (mean - minimum + 1e-9);
+        if (!(peak_to_mean >= 1.05)) {
+            flags = 1;  // flat: delta 0, weight 0.01
+        } else {
+            double second = -CUDART_INF;
+            for (int i = 0; i < kS * kS; ++i) {
+                const int alpha = i / kS, beta = i % kS;
+                if (max(abs(alpha - peak_a), abs(beta - peak_b)) <= 1) continue;
+                second = fmax(second, v0[i]);
+            }
+            const double score = 2.0 * (peak - 0.75) + (peak - second - 0.08);
+            double confidence = fmin(fmax(1.0 / (1.0 + exp(-12.0 * score)), 0.01), 0.99);
+            for (int i = 0; i < kS * kS; ++i) {
+                const int alpha = i / kS, beta = i % kS;
+                const double vb = corr_bilinear(L1, a.channels, g1, b1x + beta - kR, b1y + alpha - kR);
+                if (lane == 0) v1[i] = vb;
+            }
+            __syncwarp();
+            bool border0 = false, border1 = false;
+            double p0x, p0y, p1x, p1y;
+            subpixel_peak(L0, a.channels, g0, b0x, b0y, v0, &p0x, &p0y, &border0);
+            subpixel_peak(L1, a.channels, g1, b1x, b1y, v1, &p1x, &p1y, &border1);
+            const double e0x = kStride * p0x, e0y = kStride * p0y;
+            const double e1x = kStride * kStride * p1x, e1y = kStride * kStride * p1y;
+            if (border0 && border1) {
+                flags = 2;  // out of range: delta 0, weight 0.01
+            } else {
+                if (border0) {
+                    dxo = e1x;
+                    dyo = e1y;
+                    confidence = fmin(confidence, 0.25);
+                } else {
+                    dxo = e0x;
+                    dyo = e0y;
+                    const double ddx = e1x - e0x, ddy = e1y - e0y;
+                    if (!border1 && sqrt(ddx * ddx + ddy * ddy) > 2.0 * kStride * kStride)
+                        confidence = fmin(confidence, 0.25);
+                }
+                wgt = confidence;
+            }
+        }
+    }
+    if (lane == 0) {
+        a.delta[2 * e] = dxo;
+        a.delta[2 * e + 1] = dyo;
+        a.weight[2 * e] = wgt;
+        a.weight[2 * e + 1] = wgt;
+        if (a.flags) a.flags[e] = (uint8_t)flags;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_measure(const MeasureParams& p, cudaStream_t stream) {
+    if (p.n_edges <= 0) return cudaSuccess;
+    if (p.channels > 32 * kCh) return cudaErrorNotSupported;
+    measure_kernel<<<(p.n_edges + 7) / 8, 256, 0, stream>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace pvo_dev

@@ -468,3 +468,84 @@ def test_batch_of_windows_matches_single_windows_and_oracle(ctx):
     res2 = bat.read()
     for (p1, d1, n1), (p2, d2, n2) in zip(res, res2):
         assert np.array_equal(p1, p2) and np.array_equal(d1, d2) and n1 == n2
+
+
+def _measure_report(name, d, w, fl, rd, rw, rfl):
+    dd = np.abs(d - rd).max(1)
+    dw = np.abs(w - rw).max(1)
+    flips = int((fl != rfl).sum())
+    off = int(((dd > 1e-6) | (dw > 1e-9)).sum())
+    print(f"{name}: {len(fl)} edges, flag mismatches {flips}, delta/weight outside 1e-6 px / 1e-9: {off}, "
+          f"max |d| err {dd.max():.2e}, max |w| err {dw.max():.2e}, flat {int((rfl & 1).sum())}, "
+          f"out-of-range {int((rfl & 2).sum())}, behind {int((rfl & 4).sum())}")
+    return flips, off
+
+
+def test_measure_batch_matches_oracle(ctx, c1_workload):
+    """CorrelationFlowProvider::measure (flow_provider.cpp:209-312) per edge on the
+    C1 window (6,144 edges), GPU vs the oracle on identical inputs."""
+    w = c1_workload
+    F = w.cfg["frames"]
+    ctx.frames_reserve(F, w.level0.shape[2], w.level0.shape[1], w.level1.shape[2], w.level1.shape[1], 128)
+    for f in range(F):
+        ctx.frames_upload(f, w.level0[f], w.level1[f])
+    g = synth.build_graph(w, pvo.PatchGraph)
+    prob = g.window_problem(w.cfg["window"])
+    E = len(prob["e_patch"])
+    centers, behind = np.empty((E, 2)), np.zeros(E, np.uint8)
+    for e in range(E):
+        k = prob["e_patch"][e]
+        c, b = orc.reproject_patch(prob["poses"][prob["patch_src"][k]], prob["poses"][prob["e_pose"][e]], w.K,
+                                   prob["patch_x"][k], prob["patch_y"][k], prob["depth"][k])
+        centers[e], behind[e] = c[4], b
+    pf = w.patch_feats[prob["patch_ids"]]
+    slots = prob["pose_frames"][prob["e_pose"]]
+    d, wt, fl = pvo.measure_batch(prob["e_patch"], slots, centers, pf, behind=behind, ctx=ctx)
+    rd, rw, rfl = orc.measure_batch(prob["e_patch"], slots, centers, behind, pf, w.level0, w.level1, threads=THREADS)
+    flips, off = _measure_report("C1 measure", d, wt, fl, rd, rw, rfl)
+    assert flips == 0
+    assert off <= max(1, E // 1000)  # a few-ulp channel-sum order difference may move a hill-climb tie
+    # a synthetic self-match sanity check: every edge of a frame onto itself measures ~0
+    self_e = np.nonzero(slots == prob["pose_frames"][prob["patch_src"][prob["e_patch"]]])[0]
+    assert np.abs(d[self_e]).max() < 0.05
+
+
+def test_window_propose_matches_oracle(ctx, c1_workload):
+    """propose() over the resident window at its current state: revisions equal the
+    oracle's, and the next iteration uses them (BA on the proposed revisions)."""
+    w = c1_workload
+    F = w.cfg["frames"]
+    ctx.frames_reserve(F, w.level0.shape[2], w.level0.shape[1], w.level1.shape[2], w.level1.shape[1], 128)
+    for f in range(F):
+        ctx.frames_upload(f, w.level0[f], w.level1[f])
+    g = synth.build_graph(w, pvo.PatchGraph)
+    prob = synth.window_arrays(w, g.window_problem(w.cfg["window"]))
+    win = pvo.Window(ctx)
+    win.load(prob, prob["pose_frames"], prob["patch_feats"], w.K, w.image)
+    d, wt, fl = win.propose()
+    E = win.n_edges
+    centers, behind = np.empty((E, 2)), np.zeros(E, np.uint8)
+    for e in range(E):
+        k = prob["e_patch"][e]
+        c, b = orc.reproject_patch(prob["poses"][prob["patch_src"][k]], prob["poses"][prob["e_pose"][e]], w.K,
+                                   prob["patch_x"][k], prob["patch_y"][k], prob["depth"][k])
+        centers[e], behind[e] = c[4], b
+    slots = prob["pose_frames"][prob["e_pose"]]
+    rd, rw, rfl = orc.measure_batch(prob["e_patch"], slots, centers, behind, prob["patch_feats"], w.level0, w.level1,
+                                    threads=THREADS)
+    flips, off = _measure_report("C1 propose", d, wt, fl, rd, rw, rfl)
+    assert flips == 0 and off <= max(1, E // 1000)
+    # the proposed revisions drive the next BA: compare with the oracle BA on them
+    win.iteration(2)
+    poses, depth, norms = win.read()
+    p2 = dict(prob)
+    p2["e_delta"], p2["e_weight"] = d, wt
+    og = synth.build_graph(w, orc.PatchGraph, with_revisions=False)
+    for e in range(E):
+        og.set_revision((int(prob["patch_ids"][prob["e_patch"][e]]), int(prob["pose_frames"][prob["e_pose"][e]])),
+                        d[e], wt[e])
+    rb = og.window_problem(w.cfg["window"])
+    ref = orc.ba_window(rb, w.K, iterations=2)
+    dt, dq = pose_parity(poses, ref["poses"])
+    assert dt.max() <= 1e-3 and dq.max() <= 1e-3
+    assert np.allclose(norms, ref["residual_norms"], rtol=1e-6)

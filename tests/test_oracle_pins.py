@@ -501,3 +501,102 @@ def test_residual_non_increasing():  # test_bundle_adjust.cpp:310-334 (reduced s
         if norms[-1] > norms[0] + 1e-12:
             failures += 1
     assert failures <= 1
+
+
+# ---------------------------------------------------------------- provider measure()
+# CorrelationFlowProvider::measure (flow_provider.cpp:209-287), the "next" row of
+# SURVEY.md §8f.  The reference's own tests (test_features.cpp:246-340) use its
+# image feature extractor (out of scope); these ports keep their properties on
+# the synthetic 128-d feature grids the rest of the suite uses.
+def _measure_one(g_patch, lvl0, lvl1, center):
+    pf = np.asarray(g_patch, np.float32)[None]
+    d, w, fl = orc.measure_batch([0], [0], np.array([center], float), None, pf, lvl0[None], lvl1[None])
+    return d[0], w[0], int(fl[0])
+
+
+def _crop_patch(lvl0, lvl1, centroid):
+    from paper_2208_04726_b200 import synth
+
+    px, py = _patch_grid(centroid)  # Patch::make grid (camera.cpp:15-38)
+    g0 = synth.crop_cubic(lvl0, px / 4.0, py / 4.0)
+    g1 = synth.crop_cubic(lvl1, px / 16.0, py / 16.0)
+    return np.stack([g0, g1])  # [2][9][C]
+
+
+def _patch_grid(centroid):
+    gx, gy = np.meshgrid(np.arange(3) - 1.0, np.arange(3) - 1.0)
+    return centroid[0] + gx.ravel(), centroid[1] + gy.ravel()
+
+
+def _smooth_grid(rng, H, W, D, passes=3):
+    from paper_2208_04726_b200 import synth
+
+    g = synth.make_level0(rng, 1, H, W, D)[0]
+    for _ in range(passes - 1):  # extra blur passes: a smoother field for subpixel accuracy
+        pad = np.pad(g, ((1, 1), (1, 1), (0, 0)))
+        g = (pad[:-2, 1:-1] + 2 * pad[1:-1, 1:-1] + pad[2:, 1:-1]) / 4
+        pad = np.pad(g, ((1, 1), (1, 1), (0, 0)))
+        g = (pad[1:-1, :-2] + 2 * pad[1:-1, 1:-1] + pad[1:-1, 2:]) / 4
+        g /= np.linalg.norm(g, axis=-1, keepdims=True) + 1e-12
+    return np.ascontiguousarray(g, np.float32)
+
+
+def _level1(g):
+    from paper_2208_04726_b200 import synth
+
+    return synth.make_level1(g[None])[0]
+
+
+def test_measure_self_match_zero_and_confident():  # test_features.cpp:246-263
+    rng = np.random.default_rng(16)
+    l0 = _smooth_grid(rng, 64, 64, 32)
+    l1 = _level1(l0)
+    confident = 0
+    for _ in range(50):
+        c = rng.uniform(20.0, 235.0, 2)
+        d, w, fl = _measure_one(_crop_patch(l0, l1, c), l0, l1, c)
+        assert np.linalg.norm(d) < 0.05 and fl == 0
+        confident += w[0] > 0.5
+    assert confident > 45
+
+
+def test_measure_equivariant_at_whole_cell_shifts():  # test_features.cpp:265-300 (4 px = 1 cell)
+    rng = np.random.default_rng(18)
+    worst = 0.0
+    for _ in range(12):
+        l0 = _smooth_grid(rng, 64, 64, 32)
+        a, b = rng.integers(-2, 3, 2)
+        t0 = np.zeros_like(l0)  # target = source moved by (a, b) cells (zero fill)
+        ys, xs = slice(max(b, 0), 64 + min(b, 0)), slice(max(a, 0), 64 + min(a, 0))
+        ys2, xs2 = slice(max(-b, 0), 64 + min(-b, 0)), slice(max(-a, 0), 64 + min(-a, 0))
+        t0[ys, xs] = l0[ys2, xs2]
+        c = rng.uniform(60.0, 190.0, 2)
+        d, _, _ = _measure_one(_crop_patch(l0, _level1(l0), c), t0, _level1(t0), c)
+        worst = max(worst, np.linalg.norm(d - 4.0 * np.array([a, b])))
+    assert worst < 0.25
+
+
+def test_measure_half_cell_shift_in_bands():  # test_features.cpp:302-322 (2 px pure-x shift)
+    rng = np.random.default_rng(19)
+    for _ in range(8):
+        l0 = _smooth_grid(rng, 64, 64, 32)
+        t0 = np.zeros_like(l0)  # target(x) = source(x - 0.5 cell): linear half-cell resample
+        t0[:, 1:] = 0.5 * (l0[:, 1:] + l0[:, :-1])
+        t0 /= np.linalg.norm(t0, axis=-1, keepdims=True) + 1e-12
+        c = rng.uniform(60.0, 190.0, 2)
+        d, _, _ = _measure_one(_crop_patch(l0, _level1(l0), c), t0, _level1(t0), c)
+        assert 1.5 <= d[0] <= 2.5 and -0.5 <= d[1] <= 0.5
+
+
+def test_measure_flat_region():  # test_features.cpp:324-340
+    l0 = np.full((64, 64, 8), 0.5, np.float32)
+    l1 = _level1(l0)
+    d, w, fl = _measure_one(np.zeros((2, 9, 8), np.float32), l0, l1, (128.0, 128.0))
+    assert fl & 1 and np.allclose(d, 0.0) and np.allclose(w, 0.01)
+
+
+def test_measure_behind_camera_default_revision():  # flow_provider.cpp:301-302
+    l0 = np.ones((8, 8, 4), np.float32)
+    d, w, fl = orc.measure_batch([0], [0], np.zeros((1, 2)), np.array([1], np.uint8),
+                                 np.ones((1, 2, 9, 4), np.float32), l0[None], _level1(l0)[None])
+    assert fl[0] == 4 and np.allclose(d, 0) and np.allclose(w, 0.01)

@@ -31,3 +31,4 @@ for att in range(4):
         break
     print("attempt", att, {n: int(row[i + 1] - row[i]) for i, n in enumerate(names)})
 print("assemble: records", int(c[15][0] - c[0][0]), "accumulate", int(c[15][1] - c[15][0]), "(last attempt's records vs first start; rerun with 1 iteration for exact)")
+print("first attempt: solve", int(c[15][2] - c[0][4]), "retract+mats", int(c[0][5] - c[15][2]))
