@@ -40,38 +40,44 @@ struct Level {
     int W, H;
 };
 
-// correlate_at (correlation.cpp:8-23) with sample_zero_padded (features.cpp:9-21)
-__device__ double corr_bilinear(const Level& L, int C, const float (&g)[kCh], double x, double y) {
-    const int lane = threadIdx.x & 31;
-    const double fx = floor(x), fy = floor(y);
-    const int x0 = (int)fx, y0 = (int)fy;
-    const double ax = x - x0, ay = y - y0;
-    const double w00 = (1 - ax) * (1 - ay), w10 = ax * (1 - ay), w01 = (1 - ax) * ay, w11 = ax * ay;
-    const bool in00 = x0 >= 0 && y0 >= 0 && x0 < L.W && y0 < L.H;
-    const bool in10 = x0 + 1 >= 0 && y0 >= 0 && x0 + 1 < L.W && y0 < L.H;
-    const bool in01 = x0 >= 0 && y0 + 1 >= 0 && x0 < L.W && y0 + 1 < L.H;
-    const bool in11 = x0 + 1 >= 0 && y0 + 1 >= 0 && x0 + 1 < L.W && y0 + 1 < L.H;
-    const float* p00 = L.f + ((size_t)y0 * L.W + x0) * C;
-    const float* p10 = p00 + C;
-    const float* p01 = p00 + (size_t)L.W * C;
-    const float* p11 = p01 + C;
-    double dot = 0, nrm = 0;
-#pragma unroll
-    for (int k = 0; k < kCh; ++k) {
-        const int c = lane + 32 * k;
-        if (c < C) {
-            const double v00 = in00 ? (double)__ldg(p00 + c) : 0.0;
-            const double v10 = in10 ? (double)__ldg(p10 + c) : 0.0;
-            const double v01 = in01 ? (double)__ldg(p01 + c) : 0.0;
-            const double v11 = in11 ? (double)__ldg(p11 + c) : 0.0;
-            const double v = w00 * v00 + w10 * v10 + w01 * v01 + w11 * v11;
-            dot += (double)g[k] * v;
-            nrm += v * v;
-        }
-    }
+// The lane's 4 channels c = lane + 32 k of the centre pixel's descriptor.
+struct G4 {
+    float v[kCh];
+};
+
+// Channel-sum epilogue of correlate_at / correlate_at_cubic (correlation.cpp:16-22)
+__device__ __forceinline__ double finish(double dot, double nrm) {
     dot = warp_sum(dot);
     nrm = warp_sum(nrm);
     return nrm > 1e-12 ? dot / sqrt(nrm) : 0.0;
+}
+
+// correlate_at (correlation.cpp:8-23) with sample_zero_padded (features.cpp:9-21).
+// Not inlined: one copy of the sampler keeps the kernel inside the instruction cache.
+__device__ __noinline__ double corr_bilinear(const float* f, int W, int H, int C, G4 g, double x, double y) {
+    const int lane = threadIdx.x & 31;
+    const int x0 = (int)floor(x), y0 = (int)floor(y);
+    const double ax = x - x0, ay = y - y0;
+    const double w[4] = {(1 - ax) * (1 - ay), ax * (1 - ay), (1 - ax) * ay, ax * ay};
+    double v[kCh] = {0, 0, 0, 0};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {  // taps in the reference's order: (x0,y0) (x0+1,y0) (x0,y0+1) (x0+1,y0+1)
+        const int xi = x0 + (t & 1), yi = y0 + (t >> 1);
+        const bool in = xi >= 0 && yi >= 0 && xi < W && yi < H;
+        const float* p = f + ((size_t)(in ? yi : 0) * W + (in ? xi : 0)) * C + lane;
+#pragma unroll
+        for (int k = 0; k < kCh; ++k) {
+            const double val = (in && lane + 32 * k < C) ? (double)__ldg(p + 32 * k) : 0.0;
+            v[k] = t == 0 ? w[0] * val : v[k] + w[t] * val;
+        }
+    }
+    double dot = 0, nrm = 0;
+#pragma unroll
+    for (int k = 0; k < kCh; ++k) {
+        dot += (double)g.v[k] * v[k];
+        nrm += v[k] * v[k];
+    }
+    return finish(dot, nrm);
 }
 
 __device__ __forceinline__ void cubic_weights(double t, double w[4]) {  // features.cpp:29-34
@@ -81,44 +87,45 @@ __device__ __forceinline__ void cubic_weights(double t, double w[4]) {  // featu
     w[3] = (0.5 * t - 0.5) * t * t;
 }
 
-// correlate_at_cubic (correlation.cpp:25-35) with sample_cubic (features.cpp:23-52)
-__device__ double corr_cubic(const Level& L, int C, const float (&g)[kCh], double x, double y) {
+// correlate_at_cubic (correlation.cpp:25-35) with sample_cubic (features.cpp:23-52):
+// taps outer (one address per tap, four channel loads at immediate offsets),
+// the per-channel operation order unchanged.
+__device__ __noinline__ double corr_cubic(const float* f, int W, int H, int C, G4 g, double x, double y) {
     const int lane = threadIdx.x & 31;
     const int x0 = (int)floor(x), y0 = (int)floor(y);
     double wx[4], wy[4];
     cubic_weights(x - x0, wx);
     cubic_weights(y - y0, wy);
+    double v[kCh] = {0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int yi = y0 - 1 + j;
+        if (yi < 0 || yi >= H) continue;
+        double row[kCh] = {0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int xi = x0 - 1 + i;
+            if (xi < 0 || xi >= W) continue;
+            const float* p = f + ((size_t)yi * W + xi) * C + lane;
+#pragma unroll
+            for (int k = 0; k < kCh; ++k)
+                if (lane + 32 * k < C) row[k] += wx[i] * (double)__ldg(p + 32 * k);
+        }
+#pragma unroll
+        for (int k = 0; k < kCh; ++k) v[k] += wy[j] * row[k];
+    }
     double dot = 0, nrm = 0;
 #pragma unroll
     for (int k = 0; k < kCh; ++k) {
-        const int c = lane + 32 * k;
-        if (c < C) {
-            double v = 0;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int yi = y0 - 1 + j;
-                if (yi < 0 || yi >= L.H) continue;
-                double row = 0;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int xi = x0 - 1 + i;
-                    if (xi < 0 || xi >= L.W) continue;
-                    row += wx[i] * (double)__ldg(L.f + ((size_t)yi * L.W + xi) * C + c);
-                }
-                v += wy[j] * row;
-            }
-            dot += (double)g[k] * v;
-            nrm += v * v;
-        }
+        dot += (double)g.v[k] * v[k];
+        nrm += v[k] * v[k];
     }
-    dot = warp_sum(dot);
-    nrm = warp_sum(nrm);
-    return nrm > 1e-12 ? dot / sqrt(nrm) : 0.0;
+    return finish(dot, nrm);
 }
 
 // subpixel_peak (flow_provider.cpp:167-205) from the 7x7 slice `vals` (already
 // evaluated at base + (beta - 3, alpha - 3)); returns the offset in cells
-__device__ void subpixel_peak(const Level& L, int C, const float (&g)[kCh], double bx, double by,
+__device__ void subpixel_peak(const Level& L, int C, G4 g, double bx, double by,
                               const double* vals, double* ox, double* oy, bool* on_border) {
     int best_a = kR, best_b = kR;
     double best = -CUDART_INF;
@@ -133,23 +140,23 @@ __device__ void subpixel_peak(const Level& L, int C, const float (&g)[kCh], doub
         }
     *on_border = best_a == 0 || best_a == kS - 1 || best_b == 0 || best_b == kS - 1;
     double dx = best_b - kR, dy = best_a - kR;
-    double current = corr_cubic(L, C, g, bx + dx, by + dy);
+    double current = corr_cubic(L.f, L.W, L.H, C, g, bx + dx, by + dy);
     double h = 0.5;
     for (int hs = 0; hs < 6; ++hs, h *= 0.5) {
         for (int ax = 0; ax < 2; ++ax) {
             const bool along_x = ax == 0;
             // parabola_refine (flow_provider.cpp:152-162); f1 = the current value
             const double x = bx + dx, y = by + dy;
-            const double f0 = corr_cubic(L, C, g, x - (along_x ? h : 0), y - (along_x ? 0 : h));
+            const double f0 = corr_cubic(L.f, L.W, L.H, C, g, x - (along_x ? h : 0), y - (along_x ? 0 : h));
             const double f1 = current;
-            const double f2 = corr_cubic(L, C, g, x + (along_x ? h : 0), y + (along_x ? 0 : h));
+            const double f2 = corr_cubic(L.f, L.W, L.H, C, g, x + (along_x ? h : 0), y + (along_x ? 0 : h));
             const double denom = f0 - 2 * f1 + f2;
             double step = 0.0;
             if (!(fabs(denom) < 1e-12 || denom > 0)) step = fmin(fmax(0.5 * h * (f0 - f2) / denom, -h), h);
             if (step == 0.0) continue;
             const double nx = dx + (along_x ? step : 0);
             const double ny = dy + (along_x ? 0 : step);
-            const double value = corr_cubic(L, C, g, bx + nx, by + ny);
+            const double value = corr_cubic(L.f, L.W, L.H, C, g, bx + nx, by + ny);
             if (value >= current) {  // hill climb only
                 dx = nx;
                 dy = ny;
@@ -192,12 +199,12 @@ __global__ void __launch_bounds__(256) measure_kernel(MeasureParams a) {
         const Level L0{a.feat0 + (size_t)slot * a.h0 * a.w0 * a.channels, a.w0, a.h0};
         const Level L1{a.feat1 + (size_t)slot * a.h1 * a.w1 * a.channels, a.w1, a.h1};
         const float* gp = a.patch_feats + (size_t)a.e_patch[e] * 2 * 9 * a.channels;
-        float g0[kCh], g1[kCh];
+        G4 g0, g1;
 #pragma unroll
         for (int k = 0; k < kCh; ++k) {
             const int c = lane + 32 * k;
-            g0[k] = c < a.channels ? gp[4 * a.channels + c] : 0.f;        // centre pixel, level 0
-            g1[k] = c < a.channels ? gp[(9 + 4) * a.channels + c] : 0.f;  // centre pixel, level 1
+            g0.v[k] = c < a.channels ? gp[4 * a.channels + c] : 0.f;        // centre pixel, level 0
+            g1.v[k] = c < a.channels ? gp[(9 + 4) * a.channels + c] : 0.f;  // centre pixel, level 1
         }
         double* v0 = s_vals[warp][0];
         double* v1 = s_vals[warp][1];
@@ -205,7 +212,7 @@ __global__ void __launch_bounds__(256) measure_kernel(MeasureParams a) {
         const double b1x = cx / (kStride * kStride), b1y = cy / (kStride * kStride);
         for (int i = 0; i < kS * kS; ++i) {
             const int alpha = i / kS, beta = i % kS;
-            const double va = corr_bilinear(L0, a.channels, g0, b0x + beta - kR, b0y + alpha - kR);
+            const double va = corr_bilinear(L0.f, L0.W, L0.H, a.channels, g0, b0x + beta - kR, b0y + alpha - kR);
             if (lane == 0) v0[i] = va;
         }
         __syncwarp();
@@ -237,7 +244,7 @@ __global__ void __launch_bounds__(256) measure_kernel(MeasureParams a) {
             double confidence = fmin(fmax(1.0 / (1.0 + exp(-12.0 * score)), 0.01), 0.99);
             for (int i = 0; i < kS * kS; ++i) {
                 const int alpha = i / kS, beta = i % kS;
-                const double vb = corr_bilinear(L1, a.channels, g1, b1x + beta - kR, b1y + alpha - kR);
+                const double vb = corr_bilinear(L1.f, L1.W, L1.H, a.channels, g1, b1x + beta - kR, b1y + alpha - kR);
                 if (lane == 0) v1[i] = vb;
             }
             __syncwarp();
