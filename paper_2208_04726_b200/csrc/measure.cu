@@ -168,7 +168,10 @@ __device__ void subpixel_peak(const Level& L, int C, G4 g, double bx, double by,
     *oy = dy;
 }
 
-__global__ void __launch_bounds__(256) measure_kernel(MeasureParams a) {
+#ifndef PVO_MEASURE_MINB
+#define PVO_MEASURE_MINB 1
+#endif
+__global__ void __launch_bounds__(256, PVO_MEASURE_MINB) measure_kernel(MeasureParams a) {
     __shared__ double s_vals[8][2][kS * kS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int e = blockIdx.x * 8 + warp;
