@@ -443,16 +443,16 @@ bool encode_map(CUtensorMap* map, int rank, void* base, const uint64_t* dims, co
 
 // (Re)build the frame-store TMA descriptors (layouts in kernels.cuh): feature
 // tiles in 16-channel chunks with the 64B swizzle, planar Gram records with a
-// 12 x 9 x 5 box.  Shapes TMA cannot describe (C != 128, widths that are not a
-// multiple of 4 cells) leave the generic kernel in charge.
+// 12 x 9 x 5 box (Gram rows padded to 4 cells).  C != 128 leaves the generic
+// kernel in charge.
 void encode_frame_maps(pvo_ctx* ctx) {
     ctx->maps_ok = false;
     ctx->patch_map_base = nullptr;
-    if (ctx->C != 128 || ctx->w1 < 1 || ctx->h1 < 1 || ctx->w0 % 4 || ctx->w1 % 4) return;
+    if (ctx->C != 128 || ctx->w1 < 1 || ctx->h1 < 1) return;
     const uint64_t f0[4] = {128, (uint64_t)ctx->w0, (uint64_t)ctx->h0, (uint64_t)ctx->nf};
     const uint64_t f1[4] = {128, (uint64_t)ctx->w1, (uint64_t)ctx->h1, (uint64_t)ctx->nf};
-    const uint64_t g0[4] = {(uint64_t)ctx->w0, (uint64_t)ctx->h0, 8, (uint64_t)ctx->nf};
-    const uint64_t g1[4] = {(uint64_t)ctx->w1, (uint64_t)ctx->h1, 8, (uint64_t)ctx->nf};
+    const uint64_t g0[4] = {(uint64_t)pvo_dev::gram_stride(ctx->w0), (uint64_t)ctx->h0, 8, (uint64_t)ctx->nf};
+    const uint64_t g1[4] = {(uint64_t)pvo_dev::gram_stride(ctx->w1), (uint64_t)ctx->h1, 8, (uint64_t)ctx->nf};
     const uint32_t fbox[4] = {16, 9, 9, 1}, gbox[4] = {12, 9, 5, 1};
     ctx->maps_ok = encode_map(&ctx->maps[0], 4, ctx->feat0.p, f0, fbox, CU_TENSOR_MAP_SWIZZLE_64B) &&
                    encode_map(&ctx->maps[1], 4, ctx->feat1.p, f1, fbox, CU_TENSOR_MAP_SWIZZLE_64B) &&
@@ -804,8 +804,8 @@ int pvo_correlate(pvo_ctx* ctx, int p, int C, const float* feats0, const float* 
         const size_t n0 = (size_t)w0 * h0 * C, n1 = (size_t)w1 * h1 * C;
         float* f0 = upload(ctx, ctx->s0, level0, n0);
         float* f1 = upload(ctx, ctx->s1, level1, n1);
-        float* g0 = ctx->s2.as<float>((size_t)w0 * h0 * 8);
-        float* g1 = ctx->s3.as<float>((size_t)w1 * h1 * 8);
+        float* g0 = ctx->s2.as<float>((size_t)pvo_dev::gram_stride(w0) * h0 * 8);
+        float* g1 = ctx->s3.as<float>((size_t)std::max(pvo_dev::gram_stride(w1) * h1, 1) * 8);
         compute_gram(ctx, f0, g0, f1, g1, w0, h0, w1, h1, C);
         float* pf = ctx->s4.as<float>((size_t)2 * 9 * C);
         cuda_check(cudaMemcpyAsync(pf, feats0, sizeof(float) * 9 * C, cudaMemcpyHostToDevice, ctx->stream), "H2D");
@@ -852,8 +852,13 @@ int pvo_frames_reserve(pvo_ctx* ctx, int n_frames, int w0, int h0, int w1, int h
         ctx->C = C;
         ctx->feat0.get(sizeof(float) * (size_t)n_frames * w0 * h0 * C);
         ctx->feat1.get(sizeof(float) * (size_t)n_frames * std::max(w1 * h1, 1) * C);
-        ctx->gram0.get(sizeof(float) * (size_t)n_frames * w0 * h0 * 8);
-        ctx->gram1.get(sizeof(float) * (size_t)n_frames * std::max(w1 * h1, 1) * 8);
+        const size_t gb0 = sizeof(float) * (size_t)n_frames * pvo_dev::gram_stride(w0) * h0 * 8;
+        const size_t gb1 = sizeof(float) * (size_t)n_frames * std::max(pvo_dev::gram_stride(w1) * h1, 1) * 8;
+        ctx->gram0.get(gb0);
+        ctx->gram1.get(gb1);
+        // row-pad cells of the Gram planes must read as zero (out of the image)
+        cuda_check(cudaMemsetAsync(ctx->gram0.p, 0, gb0, ctx->stream), "memset");
+        cuda_check(cudaMemsetAsync(ctx->gram1.p, 0, gb1, ctx->stream), "memset");
         encode_frame_maps(ctx);
     });
 }
@@ -865,8 +870,8 @@ int pvo_frames_refresh(pvo_ctx* ctx, int slot) {
         const size_t c0 = (size_t)ctx->w0 * ctx->h0, c1 = (size_t)ctx->w1 * ctx->h1;
         float* f0 = static_cast<float*>(ctx->feat0.p) + slot * c0 * ctx->C;
         float* f1 = static_cast<float*>(ctx->feat1.p) + slot * c1 * ctx->C;
-        float* g0 = static_cast<float*>(ctx->gram0.p) + slot * c0 * 8;
-        float* g1 = static_cast<float*>(ctx->gram1.p) + slot * c1 * 8;
+        float* g0 = static_cast<float*>(ctx->gram0.p) + (size_t)slot * pvo_dev::gram_stride(ctx->w0) * ctx->h0 * 8;
+        float* g1 = static_cast<float*>(ctx->gram1.p) + (size_t)slot * pvo_dev::gram_stride(ctx->w1) * ctx->h1 * 8;
         compute_gram(ctx, f0, g0, f1, g1, ctx->w0, ctx->h0, ctx->w1, ctx->h1, ctx->C);
     });
 }
@@ -881,8 +886,8 @@ int pvo_frames_upload(pvo_ctx* ctx, int slot, const float* level0, const float* 
         const cudaMemcpyKind kind = memspace == PVO_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
         cuda_check(cudaMemcpyAsync(f0, level0, sizeof(float) * c0 * ctx->C, kind, ctx->stream), "frame upload");
         if (c1) cuda_check(cudaMemcpyAsync(f1, level1, sizeof(float) * c1 * ctx->C, kind, ctx->stream), "frame upload");
-        float* g0 = static_cast<float*>(ctx->gram0.p) + slot * c0 * 8;
-        float* g1 = static_cast<float*>(ctx->gram1.p) + slot * c1 * 8;
+        float* g0 = static_cast<float*>(ctx->gram0.p) + (size_t)slot * pvo_dev::gram_stride(ctx->w0) * ctx->h0 * 8;
+        float* g1 = static_cast<float*>(ctx->gram1.p) + (size_t)slot * pvo_dev::gram_stride(ctx->w1) * ctx->h1 * 8;
         compute_gram(ctx, f0, g0, f1, g1, ctx->w0, ctx->h0, ctx->w1, ctx->h1, ctx->C);
         if (memspace != PVO_DEVICE) sync(ctx);
     });

@@ -130,7 +130,8 @@ __global__ void __launch_bounds__(kThreads) corr_kernel(CorrParams a) {
         const int W = level ? a.w1 : a.w0;
         const int H = level ? a.h1 : a.h0;
         const float* fbase = (level ? a.feat1 : a.feat0) + (size_t)slot * W * H * D;
-        const float* gbase = (level ? a.gram1 : a.gram0) + (size_t)slot * W * H * 8;
+        const int Wg = gram_stride(W);
+        const float* gbase = (level ? a.gram1 : a.gram0) + (size_t)slot * Wg * H * 8;
         const float* pfeat = a.patch_feats + ((size_t)k * 2 + level) * kPix * D;
         const double scale = level ? 16.0 : 4.0;  // kFeatureStride (features.hpp:46)
 
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(kThreads) corr_kernel(CorrParams a) {
                 const int cy = Y0 + cell / TW;
                 const int cx = X0 + cell % TW;
                 float v = 0.f;
-                if (cx >= 0 && cy >= 0 && cx < W && cy < H) v = __ldg(gbase + (size_t)t * W * H + (size_t)cy * W + cx);
+                if (cx >= 0 && cy >= 0 && cx < W && cy < H) v = __ldg(gbase + (size_t)t * Wg * H + (size_t)cy * Wg + cx);
                 s_gram[i] = v;
             }
             for (int i = tid; i < npx * dp; i += kThreads) {
@@ -303,6 +304,7 @@ __global__ void __launch_bounds__(kThreads) corr_kernel(CorrParams a) {
 
 // Gram terms of one pyramid level of one frame.  One warp per cell.
 __global__ void gram_kernel(const float* __restrict__ feat, float* __restrict__ gram, int W, int H, int D) {
+    const int Wp = gram_stride(W);
     const int warps_per_block = blockDim.x >> 5;
     const int lane = threadIdx.x & 31;
     const int ncell = W * H;
@@ -334,13 +336,14 @@ __global__ void gram_kernel(const float* __restrict__ feat, float* __restrict__ 
             s3 += __shfl_xor_sync(0xffffffffu, s3, off);
             s4 += __shfl_xor_sync(0xffffffffu, s4, off);
         }
-        if (lane == 0) {  // planar records: plane k at gram + k * W * H (8 planes reserved, 5 used)
-            float* g = gram + cell;
-            g[0 * (size_t)ncell] = s0;
-            g[1 * (size_t)ncell] = s1;
-            g[2 * (size_t)ncell] = s2;
-            g[3 * (size_t)ncell] = s3;
-            g[4 * (size_t)ncell] = s4;
+        if (lane == 0) {  // planar records: plane k at gram + k * H * Wp (8 planes reserved, 5 used)
+            const size_t plane = (size_t)H * Wp;
+            float* g = gram + (size_t)y * Wp + x;
+            g[0 * plane] = s0;
+            g[1 * plane] = s1;
+            g[2 * plane] = s2;
+            g[3 * plane] = s3;
+            g[4 * plane] = s4;
         }
     }
 }

@@ -66,7 +66,7 @@ constexpr uint32_t kChunkTx = kChunkTileBytes + kChunkGBytes;
 constexpr uint32_t kHeaderTx = kGramBytes + kCoordBytes;
 constexpr int kHeaderOff = kStages * kStageBytes;        // 18432, 2 tile headers
 constexpr int kDotsOff = kHeaderOff + 2 * kHeaderBytes;  // 23040: [9][81] f32
-constexpr int kPixOff = kDotsOff + 2944;                 // 25984: PixData
+constexpr int kPixOff = kDotsOff + 2944;                 // 25984: per-tile pixel table (ax, ay, floors)
 constexpr int kMetaOff = kPixOff + 640;                  // 26624: 2 tile records
 constexpr int kWarpBytes = 27648;
 constexpr int kSmemBytes = kWarps * kWarpBytes + 1024;   // + alignment slack
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int pos = b + (i >> 1) * G;
         const int e = a.order ? a.order[pos] : pos;
         const int level = i & 1;
-        const double scale = level ? 16.0 : 4.0;  // kFeatureStride (features.hpp:46)
+        const double inv_scale = level ? 1.0 / 16.0 : 1.0 / 4.0;  // 1 / kFeatureStride^(level+1) (features.hpp:46)
         const int W = level ? a.w1 : a.w0, H = level ? a.h1 : a.h0;
         int fxs[kPix], fys[kPix];
         bool finite = true;
@@ -200,8 +200,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int p = 0; p < kPix; ++p) {
             const double x = a.coords[(size_t)e * 18 + 2 * p], y = a.coords[(size_t)e * 18 + 2 * p + 1];
             finite = finite && isfinite(x) && isfinite(y);
-            fxs[p] = clamp_floor(x / scale, W);
-            fys[p] = clamp_floor(y / scale, H);
+            fxs[p] = clamp_floor(x * inv_scale, W);  // x / 4 or x / 16, exact
+            fys[p] = clamp_floor(y * inv_scale, H);
             if (fxs[p] + 4 < 0 || fxs[p] - 3 >= W || fys[p] + 4 < 0 || fys[p] - 3 >= H) far |= 1 << p;
         }
         const int fslot = a.e_slot ? a.e_slot[e] : a.pose_slot[a.e_pose[e]];
@@ -443,8 +443,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         //   |f(x)|^2 = (1-ay)^2 |fx(y)|^2 + ay^2 |fx(y+1)|^2 + 2 ay (1-ay) <fx(y), fx(y+1)>
         // with |fx|^2 and <fx(y), fx(y+1)> from the Gram records (|f|^2, right, down,
         // diag, anti).  ax / ay are the reference's per-offset fractional parts (FP64).
-        const double scale = level ? 16.0 : 4.0;  // kFeatureStride (features.hpp:46)
+        // per-pixel fractional offsets, computed once per tile (not per column):
+        // ax[p][beta] = (bx + (beta-3)) - floor(...), ay[p][alpha] likewise, in FP64
+        // exactly as the reference (features.cpp:10-13); 1/4 and 1/16 are exact
+        const double inv_scale = level ? 1.0 / 16.0 : 1.0 / 4.0;  // kFeatureStride (features.hpp:46)
         const int W = level ? a.w1 : a.w0, H = level ? a.h1 : a.h0;
+        float* s_ax = reinterpret_cast<float*>(wb + kPixOff);  // [9][7]
+        float* s_ay = s_ax + kPix * 7;                          // [9][7]
+        int* s_f = reinterpret_cast<int*>(s_ay + kPix * 7);     // [9][2] floor(bx), floor(by)
+        for (int t = lane; t < kPix * 7; t += 32) {
+            const int p = (t * 37) >> 8, q = t - 7 * p;
+            const double bx = tc[2 * p] * inv_scale, by = tc[2 * p + 1] * inv_scale;
+            const int fx = clamp_floor(bx, W), fy = clamp_floor(by, H);
+            s_ax[t] = (float)((bx + (double)(q - 3)) - (double)(fx + q - 3));
+            s_ay[t] = (float)((by + (double)(q - 3)) - (double)(fy + q - 3));
+            if (q == 0) {
+                s_f[2 * p] = fx;
+                s_f[2 * p + 1] = fy;
+            }
+        }
+        __syncwarp();
         float* out = a.out + ((size_t)e * 2 + level) * kOut;
 #pragma unroll 1
         for (int col = lane; col < kPix * 7; col += 32) {
@@ -457,9 +475,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 continue;  // else: another sub-tile of this (edge, level) writes it
             }
-            const double bx = tc[2 * p] / scale, by = tc[2 * p + 1] / scale;
-            const int fx = clamp_floor(bx, W), fy = clamp_floor(by, H);
-            const float ax = (float)((bx + (double)(beta - 3)) - (double)(fx + beta - 3));
+            const int fx = s_f[2 * p], fy = s_f[2 * p + 1];
+            const float ax = s_ax[col];
             const float bx0 = 1.f - ax;
             const int cx = fx - 3 - r0.x + beta, cy = fy - 3 - r0.y;
             const float* d = dots + p * kCells + cy * kBox + cx;
@@ -478,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // <fx(y), fx(y+1)> = (1-ax)^2 down[x] + ax^2 down[x+1] + ax(1-ax) (diag[x] + anti[x])
                 const float cr = fmaf(qd, Gc[3 * kGramPlane] + Gc[4 * kGramPlane],
                                       fmaf(qb, Gc[2 * kGramPlane + 1], qa * Gc[2 * kGramPlane]));
-                const float ay = (float)((by + (double)(alpha - 3)) - (double)(fy + alpha - 3));
+                const float ay = s_ay[p * 7 + alpha];
                 const float by0 = 1.f - ay;
                 const float dot = fmaf(ay, dB, by0 * dA);
                 const float n2 = fmaf(2.f * ay * by0, cr, fmaf(ay * ay, nB, by0 * by0 * nA));

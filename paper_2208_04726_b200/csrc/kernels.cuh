@@ -66,13 +66,16 @@ struct CorrTmaParams {
 int corr_tma_smem_bytes();
 // Frame-store layouts the TMA kernel reads (encoded by the host):
 //   feat{0,1}: [slot][H][W][128] f32, box {16 ch, 9, 9, 1}, 64B swizzle
-//   gram{0,1}: [slot][8 planes][H][W] f32 (planes 0..4 used), box {12, 9, 5, 1}
+//   gram{0,1}: [slot][8 planes][H][gram_stride(W)] f32 (planes 0..4 used), box {12, 9, 5, 1}
 //   patch:     [P * 2 * 9][128] f32, box {16 ch, 9 rows}
 constexpr int kCorrMetaInts = 8;
 // maps: feat0, feat1, gram0, gram1, patch
 int corr_tma_grid(int n_edges, int num_sms);
 int corr_tma_extra_cap(int n_edges, int grid);
 cudaError_t launch_corr_tma(const CorrTmaParams& p, const CUtensorMap* maps, int num_sms, cudaStream_t stream);
+// Gram records of a level: planes [8][H][gram_stride(W)], rows padded to a 16-byte
+// multiple (TMA global strides must be 16-byte multiples); pad cells stay zero.
+__host__ __device__ inline int gram_stride(int W) { return (W + 3) & ~3; }
 cudaError_t launch_gram(const float* feat, float* gram, int W, int H, int D, int num_sms, cudaStream_t stream);
 
 // Flow-provider measurement per edge (measure.cu): CorrelationFlowProvider::

@@ -166,6 +166,31 @@ def test_correlate_batch_c1_full(ctx, c1_workload):
     assert bad == 0
 
 
+def test_correlate_batch_euroc_shape(ctx):
+    """Config 3 camera (752x480: level-0 188 x 120, level-1 47 x 30 cells): widths
+    that are not a multiple of 4 cells (padded Gram rows under the TMA path)."""
+    w = synth.generate("c3", seed=5, frames=8)
+    F = w.cfg["frames"]
+    ctx.frames_reserve(F, w.level0.shape[2], w.level0.shape[1], w.level1.shape[2], w.level1.shape[1], 128)
+    for f in range(F):
+        ctx.frames_upload(f, w.level0[f], w.level1[f])
+    g = synth.build_graph(w, pvo.PatchGraph)
+    prob = g.window_problem(w.cfg["window"])
+    E = len(prob["e_patch"])
+    coords = np.empty((E, 9, 2))
+    for e in range(E):
+        k = prob["e_patch"][e]
+        coords[e], _ = orc.reproject_patch(prob["poses"][prob["patch_src"][k]], prob["poses"][prob["e_pose"][e]],
+                                           w.K, prob["patch_x"][k], prob["patch_y"][k], prob["depth"][k])
+    pf = w.patch_feats[prob["patch_ids"]]
+    slots = prob["pose_frames"][prob["e_pose"]]
+    out = pvo.correlate_batch(prob["e_patch"], slots, coords, pf, ctx=ctx)
+    ref = orc.correlate_batch(prob["e_patch"], slots, coords, pf, w.level0, w.level1, threads=THREADS)
+    bad = corr_violations(out, ref, _gnorm_for_batch(pf, prob["e_patch"]))
+    print(f"C3-shape corr: {E} edges, max abs err {np.abs(out.astype(np.float64) - ref).max():.3e}, violations {bad}")
+    assert bad == 0
+
+
 def test_correlate_batch_wide_and_border_tiles(ctx, c1_workload):
     """Tiles that do not fit one 9x9 box (split into pixel-group sub-tiles),
     narrow 8x8 tiles, pixels partly / wholly outside the grid, and mixed far +
