@@ -500,23 +500,25 @@ __device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Lay
         if (a.phase_clocks && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0 && batch == k0) a.phase_clocks[15 * 8 + 0] = clock64();
 
         // ---- ordered accumulation of the batch into the CTA system ----
-        for (int w = 0; w < kWarps; ++w) {
-            const int* wiw = warp_ints(smem, L, w);
-            if (wiw[1] < 0) break;
-            const int si = wiw[0], ne = wiw[1];
-            const bool dfree = wiw[2] >= 0;
-            const double* recw = at<double>(smem, L.rec) + (size_t)w * kMaxEdges * kRec;
-            const double* vw = at<double>(smem, L.vb) + (size_t)w * 2 * np;
-            const double* bw = vw + np;
-            const double* scw = at<double>(smem, L.scal) + w * kScal;
-            const double inv_h = scw[2];
-            const int* p2e = wiw + 4;
-            const int* nxt = wiw + 4 + kMaxFree;
-            (void)ne;
-            for (int ent = tid; ent < nent; ent += kThreads) {
-                const unsigned ab = abt[ent];  // ia | ib << 8 | A << 16 | B << 24
-                const int ia = ab & 0xff, ib = (ab >> 8) & 0xff, A = (ab >> 16) & 0xff, B = ab >> 24;
-                const int ra = ia - 6 * A, rb = ib - 6 * B;
+        // entry-major: each thread keeps its entry in a register across the batch's
+        // patches (decoded once; the patches' independent lookups overlap), adding
+        // them in patch order exactly as a patch-major loop would
+        int nw = 0;
+        while (nw < kWarps && warp_ints(smem, L, nw)[1] >= 0) ++nw;
+        for (int ent = tid; ent < nent; ent += kThreads) {
+            const unsigned ab = abt[ent];  // ia | ib << 8 | A << 16 | B << 24
+            const int ia = ab & 0xff, ib = (ab >> 8) & 0xff, A = (ab >> 16) & 0xff, B = ab >> 24;
+            const int ra = ia - 6 * A, rb = ib - 6 * B;
+            double sacc = S[ent];
+            for (int w = 0; w < nw; ++w) {
+                const int* wiw = warp_ints(smem, L, w);
+                const int si = wiw[0];
+                const bool dfree = wiw[2] >= 0;
+                const double* recw = at<double>(smem, L.rec) + (size_t)w * kMaxEdges * kRec;
+                const double* vw = at<double>(smem, L.vb) + (size_t)w * 2 * np;
+                const double* scw = at<double>(smem, L.scal) + w * kScal;
+                const int* p2e = wiw + 4;
+                const int* nxt = wiw + 4 + kMaxFree;
                 double val = 0.0;
                 if (A == si && B == si) {
                     val = scw[4 + 6 * ra + rb];
@@ -536,16 +538,28 @@ __device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Lay
                         val += (R[kJt + ra] * R[kW]) * R[kJt + rb] + (R[kJt + 6 + ra] * R[kW + 1]) * R[kJt + 6 + rb];
                     }
                 }
-                if (dfree) val -= (vw[ia] * inv_h) * vw[ib];
-                S[ent] += val;
+                if (dfree) val -= (vw[ia] * scw[2]) * vw[ib];
+                sacc += val;
             }
-            for (int i = tid; i < np; i += kThreads) {
-                double r = bw[i];
-                if (dfree) r -= vw[i] * (inv_h * scw[1]);
-                rhs[i] += r;
+            S[ent] = sacc;
+        }
+        for (int i = tid; i < np; i += kThreads) {
+            double racc = rhs[i];
+            for (int w = 0; w < nw; ++w) {
+                const bool dfree = warp_ints(smem, L, w)[2] >= 0;
+                const double* vw = at<double>(smem, L.vb) + (size_t)w * 2 * np;
+                const double* scw = at<double>(smem, L.scal) + w * kScal;
+                double r = vw[np + i];
+                if (dfree) r -= vw[i] * (scw[2] * scw[1]);
+                racc += r;
             }
-            // stash the patch's Schur data for the back-substitution
-            const int kw = wiw[3];
+            rhs[i] = racc;
+        }
+        // stash the patches' Schur data for the back-substitution
+        for (int w = 0; w < nw; ++w) {
+            const int kw = warp_ints(smem, L, w)[3];
+            const double* vw = at<double>(smem, L.vb) + (size_t)w * 2 * np;
+            const double* scw = at<double>(smem, L.scal) + w * kScal;
             for (int i = tid; i < np; i += kThreads) a.patch_v[(size_t)kw * np + i] = vw[i];
             if (tid == 0) {
                 a.patch_h[kw] = scw[0];
