@@ -188,5 +188,50 @@ inline WindowResult optimize_window(Context& ctx, PatchGraph& graph, int window 
     return r;
 }
 
+// CorrelationFlowProvider::measure (flow_provider.cpp:209-287) per edge against the
+// context's frame store.  flags: 1 flat, 2 out of range, 4 behind the camera.
+struct Measurements {
+    std::vector<double> delta, weight;  // [E][2]
+    std::vector<uint8_t> flags;         // [E]
+};
+inline Measurements measure_batch(Context& ctx, const std::vector<int>& e_patch, const std::vector<int>& e_slot,
+                                  const std::vector<double>& centers, const std::vector<uint8_t>& behind,
+                                  int n_patches, const std::vector<float>& patch_feats) {
+    const int E = static_cast<int>(e_patch.size());
+    Measurements m;
+    m.delta.resize(2 * (size_t)E);
+    m.weight.resize(2 * (size_t)E);
+    m.flags.resize(E);
+    check(pvo_measure_batch(ctx.get(), E, n_patches, 3, e_patch.data(), e_slot.data(), centers.data(),
+                            behind.empty() ? nullptr : behind.data(), patch_feats.data(), m.delta.data(),
+                            m.weight.data(), m.flags.data()));
+    return m;
+}
+
+// A batch of independent windows on one device (config 5): concatenated arrays
+// with pose / patch / edge offsets, window-local indices (pvo_batch_load).
+class Batch {
+  public:
+    explicit Batch(Context& ctx) : ctx_(ctx) {}
+    void load(int n_windows, const int* pose_off, const int* patch_off, const int* edge_off, const double* poses,
+              const uint8_t* fixed, const int* pose_slot, const int* src, const double* px, const double* py,
+              const double* depth, const float* patch_feats, const int* e_patch, const int* e_pose,
+              const double* e_delta, const double* e_weight, const double K[4], int image_w, int image_h) {
+        check(pvo_batch_load(ctx_.get(), n_windows, pose_off, patch_off, edge_off, poses, fixed, pose_slot, 3, src, px,
+                             py, depth, patch_feats, e_patch, e_pose, e_delta, e_weight, K, image_w, image_h));
+    }
+    void reset() { check(pvo_batch_reset(ctx_.get())); }
+    void iteration(int iterations = 2, double damping = 1e-4) {
+        check(pvo_batch_iteration(ctx_.get(), iterations, damping, nullptr, PVO_DEVICE));
+    }
+    // poses [N][7], depths [P], residual norms [n_windows][pvo_batch_norm_stride()], counts [n_windows]
+    void read(double* poses, double* depth, double* norms, int* n_norms) {
+        check(pvo_batch_read(ctx_.get(), poses, depth, norms, n_norms));
+    }
+
+  private:
+    Context& ctx_;
+};
+
 }  // namespace b200
 }  // namespace pvo
