@@ -516,6 +516,15 @@ def run_batch(args, rank, world, local_rank):
     if rank != 0:
         return
     E_total = E_chunk * n_chunks * world
+    # roofline of the correlation launch of the last chunk: algorithmic bytes of every
+    # distinct trajectory's edges (the chunk replicates them) over the launch time
+    hbm, peak_kind = load_peaks()
+    level_shapes = [(H0, W0i), (H1, W1i)]
+    sampled = geos[: min(4, len(geos))]  # exact per-edge bytes of 4 trajectories, scaled to the chunk
+    per_edge = sum(corr_bytes_per_edge(p, w0.K, level_shapes)[0] for _, p, _ in sampled) / sum(
+        len(p["e_patch"]) for _, p, _ in sampled)
+    chunk_bytes = per_edge * E_chunk
+    achieved = chunk_bytes / (corr_ms * 1e-3) / 1e9
     line = {
         "metric": METRIC, "value": E_total / (mean_ms * 1e-3), "unit": "edge-iterations/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": True,
@@ -527,6 +536,10 @@ def run_batch(args, rank, world, local_rank):
                    "parallelism": f"sequence-sharded x{world}",
                    "l2": f"inputs ({chunk * F * 10.4 / 1024:.1f} GB frame store per chunk) far larger than L2"},
         "last_chunk_corr_ms": corr_ms, "last_chunk_ba_ms": ba_ms,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": None, "kernel": "corr_tma_kernel", "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": chunk_bytes,
+                     "bytes_note": f"per-edge bytes measured on {len(sampled)} of the {len(geos)} trajectories"},
         "e2e": {"value": E_total / (e2e_ms * 1e-3), "unit": "edge-iterations/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms},
         "gpu_launches": int(launches), "clocks": clk, "wall_s_timed_region": t_wall,
