@@ -47,7 +47,8 @@ typedef enum {
 enum { PVO_HOST = 0, PVO_DEVICE = 1 };
 
 typedef struct pvo_ctx pvo_ctx;     /* device, stream, scratch arena, frame store */
-typedef struct pvo_graph pvo_graph; /* host PatchGraph (patch_graph.hpp:66-136)   */
+typedef struct pvo_graph pvo_graph;   /* host PatchGraph (patch_graph.hpp:66-136)   */
+typedef struct pvo_dgraph pvo_dgraph; /* device-resident PatchGraph (dgraph.cu)    */
 
 /* ---- library / context ------------------------------------------------- */
 int pvo_version(void);
@@ -188,6 +189,36 @@ int pvo_measure_batch(pvo_ctx* ctx, int n_edges, int n_patches, int p, const int
                       const double* centers, const uint8_t* behind, const float* patch_feats, double* delta,
                       double* weight, uint8_t* flags);
 int pvo_window_propose(pvo_ctx* ctx, double* delta, double* weight, uint8_t* flags);
+
+/* ---- device-resident patch graph ---------------------
+ * The PatchGraph operations of patch_graph.hpp:66-136 on device arrays
+ * (frames by position, patches by id, edges in key order as a CSR by patch),
+ * each a count -> scan -> scatter pass, bit-identical to pvo_graph_*.  Frames
+ * carry the frame-store slot of their pyramid, patches their descriptors
+ * ([n][2][9][C] or NULL).  pvo_window_load_dgraph flattens the active window
+ * (bundle_adjust.cpp:231-307) on the device straight into the context's
+ * resident window; pvo_dgraph_store_window writes the window's revisions
+ * (e.g. from pvo_window_propose) and/or its BA state back into the graph.   */
+int pvo_dgraph_create(pvo_ctx* ctx, const double* K, int image_w, int image_h, int patch_width, int channels,
+                      pvo_dgraph** out);
+int pvo_dgraph_destroy(pvo_dgraph* g);
+int pvo_dgraph_add_frame(pvo_dgraph* g, double timestamp, const double* pose, int frame_slot, int* out_index);
+int pvo_dgraph_add_patches(pvo_dgraph* g, int frame, int n, const double* centroids, const double* inv_depths,
+                           const float* feats, int* out_ids);
+int pvo_dgraph_connect(pvo_dgraph* g, int radius, int* n_added);
+int pvo_dgraph_remove_frame(pvo_dgraph* g, int frame);
+int pvo_dgraph_set_revisions(pvo_dgraph* g, int n, const int* patch_ids, const int* frames, const double* deltas,
+                             const double* weights);
+int pvo_dgraph_counts(pvo_dgraph* g, int* n_frames, int* n_patches, int* n_edges);
+int pvo_dgraph_edges(pvo_dgraph* g, int* kk, int* jj, double* rev, uint8_t* has_rev);
+int pvo_dgraph_frames(pvo_dgraph* g, int* indices, double* poses);
+int pvo_dgraph_patches(pvo_dgraph* g, int* ids, int* src, double* inv_depth);
+int pvo_window_load_dgraph(pvo_ctx* ctx, pvo_dgraph* g, int window, int* n_poses, int* n_patches, int* n_edges);
+int pvo_dgraph_store_window(pvo_ctx* ctx, pvo_dgraph* g, int revisions, int state);
+/* The resident window's flattened problem (any pointer may be NULL). */
+int pvo_window_problem_read(pvo_ctx* ctx, double* poses, uint8_t* fixed, int* pose_slot, int* patch_src, double* px,
+                            double* py, double* inv_depth, int* e_patch, int* e_pose, double* e_delta,
+                            double* e_weight);
 
 /* ---- batch of independent windows (config 5: sequences sharded per device) -
  * Windows are concatenated: pose/patch/edge offsets [n_windows + 1] (starting

@@ -13,6 +13,7 @@ from .api import (  # noqa: F401
     Context,
     CudaError,
     DegenerateProblem,
+    DeviceGraph,
     NormalEquations,
     Patch,
     PatchGraph,
@@ -38,6 +39,7 @@ from .api import (  # noqa: F401
     schur_solve,
     se3_exp,
     se3_log,
+    window_problem_read,
 )
 from ._capi import lib  # noqa: F401
 

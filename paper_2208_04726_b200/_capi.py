@@ -65,6 +65,20 @@ SIGNATURES = {
     "pvo_window_corr_ptr": (i32, [vp, P]),
     "pvo_measure_batch": (i32, [vp, i32, i32, i32, P, P, P, P, P, P, P, P]),
     "pvo_window_propose": (i32, [vp, P, P, P]),
+    "pvo_dgraph_create": (i32, [vp, P, i32, i32, i32, i32, C.POINTER(vp)]),
+    "pvo_dgraph_destroy": (i32, [vp]),
+    "pvo_dgraph_add_frame": (i32, [vp, f64, P, i32, P]),
+    "pvo_dgraph_add_patches": (i32, [vp, i32, i32, P, P, P, P]),
+    "pvo_dgraph_connect": (i32, [vp, i32, P]),
+    "pvo_dgraph_remove_frame": (i32, [vp, i32]),
+    "pvo_dgraph_set_revisions": (i32, [vp, i32, P, P, P, P]),
+    "pvo_dgraph_counts": (i32, [vp, P, P, P]),
+    "pvo_dgraph_edges": (i32, [vp, P, P, P, P]),
+    "pvo_dgraph_frames": (i32, [vp, P, P]),
+    "pvo_dgraph_patches": (i32, [vp, P, P, P]),
+    "pvo_window_load_dgraph": (i32, [vp, vp, i32, P, P, P]),
+    "pvo_dgraph_store_window": (i32, [vp, vp, i32, i32]),
+    "pvo_window_problem_read": (i32, [vp, P, P, P, P, P, P, P, P, P, P, P]),
     "pvo_batch_load": (i32, [vp, i32, P, P, P, P, P, P, i32, P, P, P, P, P, P, P, P, P, P, i32, i32]),
     "pvo_batch_reset": (i32, [vp]),
     "pvo_batch_iteration": (i32, [vp, i32, f64, P, i32]),

@@ -715,3 +715,102 @@ class Batch:
             out.append((poses[self.pose_off[w]:self.pose_off[w + 1]], d[self.patch_off[w]:self.patch_off[w + 1]],
                         list(norms[w, : nn[w]])))
         return out
+
+
+class DeviceGraph:
+    """PatchGraph kept on the device (pvo_dgraph_*; patch_graph.hpp:66-136): the same
+    operations and edge order as PatchGraph, plus an on-device window flatten into a
+    context's resident Window."""
+
+    def __init__(self, ctx: Context, K, image_width: int, image_height: int, channels: int = 0, patch_width: int = 3):
+        h = C.c_void_p()
+        self.ctx = ctx
+        self.K = _f64(K, (4,))
+        self.channels = channels
+        check(lib.pvo_dgraph_create(ctx.handle, _ptr(self.K), image_width, image_height, patch_width, channels,
+                                    C.byref(h)))
+        self.handle = h
+
+    def __del__(self):  # pragma: no cover
+        if getattr(self, "handle", None):
+            lib.pvo_dgraph_destroy(self.handle)
+            self.handle = None
+
+    def add_frame(self, timestamp: float, pose, frame_slot: int = 0) -> int:
+        idx = C.c_int()
+        check(lib.pvo_dgraph_add_frame(self.handle, float(timestamp), _ptr(_f64(pose, (7,))), int(frame_slot),
+                                       C.addressof(idx)))
+        return idx.value
+
+    def add_patches(self, frame: int, centroids, inverse_depths, feats=None) -> list:
+        c = _f64(centroids).reshape(-1, 2)
+        d = _f64(inverse_depths).reshape(-1)
+        f = None if feats is None else _f32(feats)
+        ids = np.empty(c.shape[0], np.int32)
+        check(lib.pvo_dgraph_add_patches(self.handle, frame, c.shape[0], _ptr(c), _ptr(d),
+                                         None if f is None else _ptr(f), _ptr(ids)))
+        return ids.tolist()
+
+    def connect(self, radius: int) -> int:
+        n = C.c_int()
+        check(lib.pvo_dgraph_connect(self.handle, radius, C.addressof(n)))
+        return n.value
+
+    def remove_frame(self, frame: int) -> None:
+        check(lib.pvo_dgraph_remove_frame(self.handle, frame))
+
+    def set_revisions(self, kk, jj, deltas, weights) -> None:
+        k, j = _i32(kk), _i32(jj)
+        check(lib.pvo_dgraph_set_revisions(self.handle, k.shape[0], _ptr(k), _ptr(j), _ptr(_f64(deltas).reshape(-1, 2)),
+                                           _ptr(_f64(weights).reshape(-1, 2))))
+
+    def counts(self):
+        a, b, c = C.c_int(), C.c_int(), C.c_int()
+        check(lib.pvo_dgraph_counts(self.handle, C.addressof(a), C.addressof(b), C.addressof(c)))
+        return a.value, b.value, c.value
+
+    def edges(self):
+        _, _, E = self.counts()
+        kk, jj = np.empty(E, np.int32), np.empty(E, np.int32)
+        rev, has = np.empty((E, 4)), np.empty(E, np.uint8)
+        check(lib.pvo_dgraph_edges(self.handle, _ptr(kk), _ptr(jj), _ptr(rev), _ptr(has)))
+        rev[has == 0] = 0.0
+        return kk, jj, rev, has.astype(bool)
+
+    def frames(self):
+        F, _, _ = self.counts()
+        idx, poses = np.empty(F, np.int32), np.empty((F, 7))
+        check(lib.pvo_dgraph_frames(self.handle, _ptr(idx), _ptr(poses)))
+        return idx, poses
+
+    def patches(self):
+        _, P, _ = self.counts()
+        ids, src, d = np.empty(P, np.int32), np.empty(P, np.int32), np.empty(P)
+        check(lib.pvo_dgraph_patches(self.handle, _ptr(ids), _ptr(src), _ptr(d)))
+        return ids, src, d
+
+    def load_window(self, window: int) -> tuple:
+        """Flatten the active window on the device into the context's resident Window;
+        returns (n_poses, n_patches, n_edges)."""
+        a, b, c = C.c_int(), C.c_int(), C.c_int()
+        check(lib.pvo_window_load_dgraph(self.ctx.handle, self.handle, window, C.addressof(a), C.addressof(b),
+                                         C.addressof(c)))
+        win = Window(self.ctx)
+        win.n_poses, win.n_patches, win.n_edges = a.value, b.value, c.value
+        self.window = win
+        return a.value, b.value, c.value
+
+    def store_window(self, revisions: bool = True, state: bool = True) -> None:
+        check(lib.pvo_dgraph_store_window(self.ctx.handle, self.handle, int(revisions), int(state)))
+
+
+def window_problem_read(ctx: Context, n_poses: int, n_patches: int, n_edges: int) -> dict:
+    """The resident window's flattened problem (pvo_window_problem_read)."""
+    out = dict(poses=np.empty((n_poses, 7)), fixed=np.empty(n_poses, np.uint8), pose_slot=np.empty(n_poses, np.int32),
+               patch_src=np.empty(n_patches, np.int32), patch_x=np.empty((n_patches, 9)),
+               patch_y=np.empty((n_patches, 9)), depth=np.empty(n_patches), e_patch=np.empty(n_edges, np.int32),
+               e_pose=np.empty(n_edges, np.int32), e_delta=np.empty((n_edges, 2)), e_weight=np.empty((n_edges, 2)))
+    k = ["poses", "fixed", "pose_slot", "patch_src", "patch_x", "patch_y", "depth", "e_patch", "e_pose", "e_delta",
+         "e_weight"]
+    check(lib.pvo_window_problem_read(ctx.handle, *[_ptr(out[n]) for n in k]))
+    return out

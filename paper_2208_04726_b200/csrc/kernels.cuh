@@ -107,6 +107,67 @@ struct MeasureParams {
 };
 cudaError_t launch_measure(const MeasureParams& p, cudaStream_t stream);
 
+// Device-resident patch graph (dgraph.cu): SoA views.
+struct DGraphView {
+    int F = 0, P = 0;
+    int* f_index = nullptr;   // [F] frame indices (ascending = position order)
+    double* f_pose = nullptr; // [F][7]
+    int* f_slot = nullptr;    // [F] frame-store slot of the frame's pyramid
+    int* p_id = nullptr;      // [P] ascending
+    int* p_src = nullptr;     // [P] source frame index
+    double* p_x = nullptr;    // [P][9]
+    double* p_y = nullptr;
+    double* p_d = nullptr;    // [P] inverse depth
+    float* p_feat = nullptr;  // [P][feat_stride] descriptors (2 levels x 9 px x C)
+    size_t feat_stride = 0;
+    int* ebeg = nullptr;      // [P+1] CSR into the edge arrays
+    int* e_frame = nullptr;   // frame index per edge (ascending inside a patch)
+    uint8_t* e_has = nullptr; // revision set
+    double* e_rev = nullptr;  // [E][4] delta x y, weight x y
+};
+// The flattened window, written straight into a context's window / BA buffers.
+struct WindowOut {
+    int n_poses = 0, n_patches = 0, n_edges = 0;
+    int* pose_frames = nullptr;
+    double* poses = nullptr;
+    uint8_t* fixed = nullptr;
+    int* pose_slot = nullptr;
+    int* free_slot = nullptr;
+    int* n_fixed_dev = nullptr;
+    int* patch_ids = nullptr;
+    int* patch_src = nullptr;
+    double* px = nullptr;
+    double* py = nullptr;
+    double* depth = nullptr;
+    int* depth_slot = nullptr;
+    int* edge_begin = nullptr;
+    float* patch_feats = nullptr;
+    int* e_patch = nullptr;
+    int* e_pose = nullptr;
+    double* e_delta = nullptr;
+    double* e_weight = nullptr;
+    int* e_graph = nullptr;   // graph edge index of each window edge
+    int* order = nullptr;     // edges sorted by frame-store slot (stable), or null
+};
+cudaError_t dg_scan(int n, const int* in, int* out, cudaStream_t s);
+cudaError_t dg_connect(const DGraphView& g, int radius, int pass, int* newlen, const int* new_ebeg, int* out_frame,
+                       uint8_t* out_has, double* out_rev, cudaStream_t s);
+cudaError_t dg_remove(const DGraphView& g, int frame, int pass, int* keep, int* newlen, const int* new_pidx,
+                      const int* new_ebeg, const DGraphView& out, cudaStream_t s);
+cudaError_t dg_set_revisions(const DGraphView& g, int n, const int* ids, const int* frames, const double* rev,
+                             int* missing, cudaStream_t s);
+cudaError_t dg_window_pass0(const DGraphView& g, int window_start, int* inc, int* nrev, cudaStream_t s);
+cudaError_t dg_window_used(const DGraphView& g, const int* inc, int* used, cudaStream_t s);
+cudaError_t dg_window_write(const DGraphView& g, int first_free, const int* inc, const int* pslot, const int* eoff,
+                            const int* used, const int* slot_of_pos, const WindowOut& w, int n_slots,
+                            cudaStream_t s);
+cudaError_t dg_window_nfixed(const DGraphView& g, int first_free, const int* used, int* n_fixed, cudaStream_t s);
+cudaError_t dg_store_revisions(const DGraphView& g, int n_edges, const int* e_graph, const double* delta,
+                               const double* weight, cudaStream_t s);
+cudaError_t dg_writeback(const DGraphView& g, int n_poses, const int* pose_frames, const uint8_t* fixed,
+                         const double* poses, int n_patches, const int* patch_ids, const double* depth,
+                         cudaStream_t s);
+
 // Device status word values (ba.cu / corr.cu) -> pvo_status on the host.
 enum DevStatus : int {
     kDevOk = 0,

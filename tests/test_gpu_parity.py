@@ -574,3 +574,127 @@ def test_window_propose_matches_oracle(ctx, c1_workload):
     dt, dq = pose_parity(poses, ref["poses"])
     assert dt.max() <= 1e-3 and dq.max() <= 1e-3
     assert np.allclose(norms, ref["residual_norms"], rtol=1e-6)
+
+
+def _random_graph_ops(rng, graphs, K, image, F_total, M, radius, removals, with_feats=0):
+    """Drive a host PatchGraph and a DeviceGraph through the same add / connect /
+    revise / remove sequence (pipeline.cpp admit + keyframe pattern)."""
+    host, dev = graphs
+    for f in range(F_total):
+        pose = orc.se3_exp(np.concatenate([rng.normal(0, 0.05, 3) + [0.1 * f, 0, 0], rng.normal(0, 0.02, 3)]))
+        a = host.add_frame(0.05 * (f + 1), pose)
+        b = dev.add_frame(0.05 * (f + 1), pose, frame_slot=f % 4)
+        assert a == b
+        cents = np.stack([rng.uniform(3, image[0] - 4, M), rng.uniform(3, image[1] - 4, M)], 1)
+        deps = rng.uniform(0.05, 1.0, M)
+        feats = rng.standard_normal((M, 2, 9, with_feats)).astype(np.float32) if with_feats else None
+        assert host.add_patches(a, cents, deps) == dev.add_patches(b, cents, deps, feats)
+        assert host.connect(radius) == dev.connect(radius)
+        kk, jj, _, _ = dev.edges()
+        sel = rng.random(len(kk)) < 0.6  # revise a random subset
+        d = rng.normal(0, 2, (sel.sum(), 2))
+        w = rng.uniform(0.05, 0.95, (sel.sum(), 2))
+        host.set_revisions(kk[sel], jj[sel], d, w)
+        dev.set_revisions(kk[sel], jj[sel], d, w)
+        if f in removals:
+            idx, _ = dev.frames()
+            victim = int(idx[len(idx) - 5])  # like Pipeline::keyframe's candidate (t - 4)
+            host.remove_frame(victim)
+            dev.remove_frame(victim)
+
+
+def _host_edges(g):
+    kk, jj, rev, has = g.edges()
+    rev = np.where(has[:, None], rev, 0.0)
+    return kk, jj, rev, has
+
+
+def test_device_graph_matches_host_graph(ctx):
+    """Device-resident graph (§8f row 3): add / connect / revise / remove sequences
+    give bit-identical edges (key order), revisions, frames and patches to the host
+    graph, and the on-device window flatten equals the host window_problem."""
+    rng = np.random.default_rng(3)
+    image = (640, 480)
+    K = [320.0, 320.0, 320.0, 240.0]
+    host = pvo.PatchGraph(K, image[0], image[1], 3)
+    dev = pvo.DeviceGraph(ctx, K, image[0], image[1], channels=0)
+    _random_graph_ops(rng, (host, dev), K, image, F_total=16, M=20, radius=5, removals={8, 11, 13})
+    hk, hj, hr, hh = _host_edges(host)
+    dk, dj, dr, dh = dev.edges()
+    assert np.array_equal(hk, dk) and np.array_equal(hj, dj) and np.array_equal(hh, dh)
+    assert np.array_equal(hr, dr)
+    hi, hp = host.frames()
+    di, dp = dev.frames()
+    assert np.array_equal(hi, di) and np.array_equal(hp, dp)
+    hid, hsrc, hd = host.patches()
+    did, dsrc, dd = dev.patches()
+    assert np.array_equal(hid, did) and np.array_equal(hsrc, dsrc) and np.array_equal(hd, dd)
+    # window flatten on the device vs the host flattening
+    ctx.frames_reserve(4, 160, 120, 40, 30, 128)
+    for window in (3, 6, 50):
+        ref = host.window_problem(window)
+        n = dev.load_window(window)
+        assert n == (len(ref["poses"]), len(ref["depth"]), len(ref["e_patch"]))
+        got = pvo.window_problem_read(ctx, *n)
+        for key in ("poses", "patch_src", "patch_x", "patch_y", "depth", "e_patch", "e_pose"):
+            assert np.array_equal(np.asarray(got[key]).reshape(np.asarray(ref[key]).shape), ref[key]), key
+        assert np.array_equal(got["fixed"].astype(bool), ref["fixed"].astype(bool))
+        assert np.array_equal(got["pose_slot"], ref["pose_frames"] % 4)
+        # revision deltas / raw weights of the window edges = the graph's revisions
+        key = {(int(a), int(b)): i for i, (a, b) in enumerate(zip(hk, hj))}
+        rows = [key[(int(ref["patch_ids"][k]), int(ref["pose_frames"][j]))] for k, j in zip(ref["e_patch"], ref["e_pose"])]
+        assert np.array_equal(got["e_delta"], hr[rows, :2]) and np.array_equal(got["e_weight"], hr[rows, 2:])
+
+
+def test_device_graph_window_loop_matches_host_path(ctx):
+    """Per-frame loop on the device graph: flatten -> corr + BA (identical to the
+    host-flattened window, bit for bit) -> write-back; propose -> revisions
+    stored into the graph's edges."""
+    w = synth.generate("c1", seed=21, frames=6, patches=24)
+    F, M = w.cfg["frames"], w.cfg["patches"]
+    _, H0, W0, D = w.level0.shape
+    _, H1, W1, _ = w.level1.shape
+    ctx.frames_reserve(F, W0, H0, W1, H1, D)
+    for f in range(F):
+        ctx.frames_upload(f, w.level0[f], w.level1[f])
+    dev = pvo.DeviceGraph(ctx, w.K, w.image[0], w.image[1], channels=D)
+    for f in range(F):
+        dev.add_frame(0.05 * f, w.poses[f], frame_slot=f)
+        ks = slice(f * M, (f + 1) * M)
+        dev.add_patches(f, w.centroids[ks], w.depth[ks], w.patch_feats[ks])
+        dev.connect(w.cfg["radius"])
+    dev.set_revisions(w.active_kk, w.active_jj, w.deltas, w.weights)
+    # host path: the host graph's window loaded from host arrays
+    g = synth.build_graph(w, pvo.PatchGraph)
+    prob = synth.window_arrays(w, g.window_problem(w.cfg["window"]))
+    win = pvo.Window(ctx)
+    win.load(prob, prob["pose_frames"], prob["patch_feats"], w.K, w.image)
+    v_host = np.empty((win.n_edges, 2, 9, 7, 7), np.float32)
+    win.iteration(2, corr_out=v_host)
+    p_host, d_host, n_host = win.read()
+    # device path
+    N, P, E = dev.load_window(w.cfg["window"])
+    assert (N, P, E) == (len(prob["poses"]), len(prob["depth"]), len(prob["e_patch"]))
+    v_dev = np.empty((E, 2, 9, 7, 7), np.float32)
+    dev.window.iteration(2, corr_out=v_dev)
+    p_dev, d_dev, n_dev = dev.window.read()
+    assert np.array_equal(v_dev, v_host)
+    assert np.array_equal(p_dev, p_host) and np.array_equal(d_dev, d_host) and n_dev == n_host
+    # write-back of the BA state into the graph (free poses, included depths)
+    dev.store_window(revisions=False, state=True)
+    idx, poses = dev.frames()
+    fixed = prob["fixed"].astype(bool)
+    for s, fr in enumerate(prob["pose_frames"]):
+        expect = p_dev[s] if not fixed[s] else w.poses[fr]
+        assert np.array_equal(poses[list(idx).index(fr)], expect)
+    ids, _, dd = dev.patches()
+    pos = {int(i): n for n, i in enumerate(ids)}
+    assert np.array_equal(dd[[pos[int(i)] for i in prob["patch_ids"]]], d_dev)
+    # propose on the device window, revisions stored into the graph
+    dev.load_window(w.cfg["window"])
+    pd, pw, _ = dev.window.propose()
+    dev.store_window(revisions=True, state=False)
+    kk, jj, rev, has = dev.edges()
+    key = {(int(a), int(b)): i for i, (a, b) in enumerate(zip(kk, jj))}
+    rows = [key[(int(prob["patch_ids"][k]), int(prob["pose_frames"][j]))] for k, j in zip(prob["e_patch"], prob["e_pose"])]
+    assert has[rows].all() and np.array_equal(rev[rows, :2], pd) and np.array_equal(rev[rows, 2:], pw)
