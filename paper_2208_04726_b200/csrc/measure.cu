@@ -6,8 +6,9 @@
 // correlate_at / correlate_at_cubic (correlation.cpp:8-35) and the
 // zero-padded bilinear / Catmull-Rom samplers (features.cpp:9-52).
 //
-// One warp per edge, lanes over channels (C <= 128: four channels per lane,
-// the centre pixel's descriptors of both levels held in registers).  Every
+// Two warps per edge (one per pyramid level, joined by a named barrier), lanes
+// over channels (C <= 128: four channels per lane, the centre pixel's
+// descriptor held in registers).  Every
 // correlation sample is the reference's per-channel FP64 formula with the
 // reference's operation order (this file is compiled with --fmad=false, so
 // every product and sum rounds like the x86-64 reference build); only the
@@ -172,10 +173,15 @@ __device__ void subpixel_peak(const Level& L, int C, G4 g, double bx, double by,
 #define PVO_MEASURE_MINB 1
 #endif
 __global__ void __launch_bounds__(256, PVO_MEASURE_MINB) measure_kernel(MeasureParams a) {
-    __shared__ double s_vals[8][2][kS * kS];
+    // two warps per edge: warp 2m runs level 0 (slice, scores, subpixel peak), warp
+    // 2m+1 level 1 (slice, subpixel peak) concurrently; they meet on a named barrier
+    __shared__ double s_vals[8][kS * kS];
+    __shared__ double s_peak1[4][2];
+    __shared__ int s_border1[4];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int e = blockIdx.x * 8 + warp;
-    if (e >= a.n_edges) return;
+    const int pair = warp >> 1, level = warp & 1;
+    const int e = blockIdx.x * 4 + pair;
+    if (e >= a.n_edges) return;  // both warps of the pair
     double cx, cy;
     bool behind;
     if (a.centers) {
@@ -196,65 +202,75 @@ __global__ void __launch_bounds__(256, PVO_MEASURE_MINB) measure_kernel(MeasureP
         flags = 4;  // flow_provider.cpp:301-302
     } else if (!isfinite(cx) || !isfinite(cy)) {
         flags = 8;
-        if (lane == 0) atomicOr(a.status, 1 << kDevBadCoords);
+        if (lane == 0 && level == 0) atomicOr(a.status, 1 << kDevBadCoords);
     } else {
         const int slot = a.e_slot ? a.e_slot[e] : a.pose_slot[a.e_pose[e]];
-        const Level L0{a.feat0 + (size_t)slot * a.h0 * a.w0 * a.channels, a.w0, a.h0};
-        const Level L1{a.feat1 + (size_t)slot * a.h1 * a.w1 * a.channels, a.w1, a.h1};
         const float* gp = a.patch_feats + (size_t)a.e_patch[e] * 2 * 9 * a.channels;
-        G4 g0, g1;
+        const Level L = level ? Level{a.feat1 + (size_t)slot * a.h1 * a.w1 * a.channels, a.w1, a.h1}
+                              : Level{a.feat0 + (size_t)slot * a.h0 * a.w0 * a.channels, a.w0, a.h0};
+        G4 g;
 #pragma unroll
         for (int k = 0; k < kCh; ++k) {
             const int c = lane + 32 * k;
-            g0.v[k] = c < a.channels ? gp[4 * a.channels + c] : 0.f;        // centre pixel, level 0
-            g1.v[k] = c < a.channels ? gp[(9 + 4) * a.channels + c] : 0.f;  // centre pixel, level 1
+            g.v[k] = c < a.channels ? gp[(9 * level + 4) * a.channels + c] : 0.f;  // centre pixel of the level
         }
-        double* v0 = s_vals[warp][0];
-        double* v1 = s_vals[warp][1];
-        const double b0x = cx / kStride, b0y = cy / kStride;
-        const double b1x = cx / (kStride * kStride), b1y = cy / (kStride * kStride);
+        double* v = s_vals[warp];
+        const double sc = level ? kStride * kStride : kStride;
+        const double bx = cx / sc, by = cy / sc;
         for (int i = 0; i < kS * kS; ++i) {
             const int alpha = i / kS, beta = i % kS;
-            const double va = corr_bilinear(L0.f, L0.W, L0.H, a.channels, g0, b0x + beta - kR, b0y + alpha - kR);
-            if (lane == 0) v0[i] = va;
+            const double va = corr_bilinear(L.f, L.W, L.H, a.channels, g, bx + beta - kR, by + alpha - kR);
+            if (lane == 0) v[i] = va;
         }
         __syncwarp();
-        // flatness / sharpness scores on the level-0 slice (flow_provider.cpp:217-250)
+        if (level == 1) {
+            // level-1 subpixel peak (flow_provider.cpp:264-265), needed unless level 0 is flat
+            double px, py;
+            bool border;
+            subpixel_peak(L, a.channels, g, bx, by, v, &px, &py, &border);
+            if (lane == 0) {
+                s_peak1[pair][0] = px;
+                s_peak1[pair][1] = py;
+                s_border1[pair] = border;
+            }
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+            return;
+        }
+        // level 0: flatness / sharpness scores on the slice (flow_provider.cpp:217-250)
         double peak = -CUDART_INF, minimum = CUDART_INF, mean = 0;
         int peak_a = 0, peak_b = 0;
         for (int i = 0; i < kS * kS; ++i) {
-            const double v = v0[i];
-            mean += v;
-            minimum = fmin(minimum, v);
-            if (v > peak) {
-                peak = v;
+            const double val = v[i];
+            mean += val;
+            minimum = fmin(minimum, val);
+            if (val > peak) {
+                peak = val;
                 peak_a = i / kS;
                 peak_b = i % kS;
             }
         }
         mean /= kS * kS;
         const double peak_to_mean = (peak - minimum) / (mean - minimum + 1e-9);
-        if (!(peak_to_mean >= 1.05)) {
-            flags = 1;  // flat: delta 0, weight 0.01
-        } else {
+        bool flat = !(peak_to_mean >= 1.05);
+        double confidence = 0.01, p0x = 0, p0y = 0;
+        bool border0 = false;
+        if (!flat) {
             double second = -CUDART_INF;
             for (int i = 0; i < kS * kS; ++i) {
                 const int alpha = i / kS, beta = i % kS;
                 if (max(abs(alpha - peak_a), abs(beta - peak_b)) <= 1) continue;
-                second = fmax(second, v0[i]);
+                second = fmax(second, v[i]);
             }
             const double score = 2.0 * (peak - 0.75) + (peak - second - 0.08);
-            double confidence = fmin(fmax(1.0 / (1.0 + exp(-12.0 * score)), 0.01), 0.99);
-            for (int i = 0; i < kS * kS; ++i) {
-                const int alpha = i / kS, beta = i % kS;
-                const double vb = corr_bilinear(L1.f, L1.W, L1.H, a.channels, g1, b1x + beta - kR, b1y + alpha - kR);
-                if (lane == 0) v1[i] = vb;
-            }
-            __syncwarp();
-            bool border0 = false, border1 = false;
-            double p0x, p0y, p1x, p1y;
-            subpixel_peak(L0, a.channels, g0, b0x, b0y, v0, &p0x, &p0y, &border0);
-            subpixel_peak(L1, a.channels, g1, b1x, b1y, v1, &p1x, &p1y, &border1);
+            confidence = fmin(fmax(1.0 / (1.0 + exp(-12.0 * score)), 0.01), 0.99);
+            subpixel_peak(L, a.channels, g, bx, by, v, &p0x, &p0y, &border0);
+        }
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+        if (flat) {
+            flags = 1;  // flat: delta 0, weight 0.01
+        } else {
+            const bool border1 = s_border1[pair];
+            const double p1x = s_peak1[pair][0], p1y = s_peak1[pair][1];
             const double e0x = kStride * p0x, e0y = kStride * p0y;
             const double e1x = kStride * kStride * p1x, e1y = kStride * kStride * p1y;
             if (border0 && border1) {
@@ -275,6 +291,7 @@ __global__ void __launch_bounds__(256, PVO_MEASURE_MINB) measure_kernel(MeasureP
             }
         }
     }
+    if (level == 1) return;
     if (lane == 0) {
         a.delta[2 * e] = dxo;
         a.delta[2 * e + 1] = dyo;
@@ -289,7 +306,7 @@ __global__ void __launch_bounds__(256, PVO_MEASURE_MINB) measure_kernel(MeasureP
 cudaError_t launch_measure(const MeasureParams& p, cudaStream_t stream) {
     if (p.n_edges <= 0) return cudaSuccess;
     if (p.channels > 32 * kCh) return cudaErrorNotSupported;
-    measure_kernel<<<(p.n_edges + 7) / 8, 256, 0, stream>>>(p);
+    measure_kernel<<<(p.n_edges + 3) / 4, 256, 0, stream>>>(p);
     return cudaGetLastError();
 }
 
