@@ -171,6 +171,8 @@ int pvo_window_load(pvo_ctx* ctx, int n_poses, const double* poses, const uint8_
 int pvo_window_set_state(pvo_ctx* ctx, const double* poses, const double* inv_depth, int memspace);
 int pvo_window_iteration(pvo_ctx* ctx, int iterations, double damping, float* corr_out, int corr_memspace);
 int pvo_window_correlate(pvo_ctx* ctx, float* corr_out, int memspace);
+/* optimize_window's iterations only (no correlation pass): propose -> BA. */
+int pvo_window_ba(pvo_ctx* ctx, int iterations, double damping);
 int pvo_window_read(pvo_ctx* ctx, double* poses, double* inv_depth, double* residual_norms, int* n_norms);
 /* Device pointer of the window's correlation volume buffer [E][2][pp][49]. */
 int pvo_window_corr_ptr(pvo_ctx* ctx, float** corr);
@@ -213,7 +215,10 @@ int pvo_dgraph_counts(pvo_dgraph* g, int* n_frames, int* n_patches, int* n_edges
 int pvo_dgraph_edges(pvo_dgraph* g, int* kk, int* jj, double* rev, uint8_t* has_rev);
 int pvo_dgraph_frames(pvo_dgraph* g, int* indices, double* poses);
 int pvo_dgraph_patches(pvo_dgraph* g, int* ids, int* src, double* inv_depth);
-int pvo_window_load_dgraph(pvo_ctx* ctx, pvo_dgraph* g, int window, int* n_poses, int* n_patches, int* n_edges);
+/* all_active: flatten every active edge (pipeline.cpp:164-181, the set propose measures) instead of the
+ * revised ones only (bundle_adjust.cpp:245).                                                           */
+int pvo_window_load_dgraph(pvo_ctx* ctx, pvo_dgraph* g, int window, int all_active, int* n_poses, int* n_patches,
+                           int* n_edges);
 int pvo_dgraph_store_window(pvo_ctx* ctx, pvo_dgraph* g, int revisions, int state);
 /* The resident window's flattened problem (any pointer may be NULL). */
 int pvo_window_problem_read(pvo_ctx* ctx, double* poses, uint8_t* fixed, int* pose_slot, int* patch_src, double* px,

@@ -61,6 +61,7 @@ SIGNATURES = {
     "pvo_window_set_state": (i32, [vp, P, P, i32]),
     "pvo_window_iteration": (i32, [vp, i32, f64, P, i32]),
     "pvo_window_correlate": (i32, [vp, P, i32]),
+    "pvo_window_ba": (i32, [vp, i32, f64]),
     "pvo_window_read": (i32, [vp, P, P, P, P]),
     "pvo_window_corr_ptr": (i32, [vp, P]),
     "pvo_measure_batch": (i32, [vp, i32, i32, i32, P, P, P, P, P, P, P, P]),
@@ -76,7 +77,7 @@ SIGNATURES = {
     "pvo_dgraph_edges": (i32, [vp, P, P, P, P]),
     "pvo_dgraph_frames": (i32, [vp, P, P]),
     "pvo_dgraph_patches": (i32, [vp, P, P, P]),
-    "pvo_window_load_dgraph": (i32, [vp, vp, i32, P, P, P]),
+    "pvo_window_load_dgraph": (i32, [vp, vp, i32, i32, P, P, P]),
     "pvo_dgraph_store_window": (i32, [vp, vp, i32, i32]),
     "pvo_window_problem_read": (i32, [vp, P, P, P, P, P, P, P, P, P, P, P]),
     "pvo_batch_load": (i32, [vp, i32, P, P, P, P, P, P, i32, P, P, P, P, P, P, P, P, P, P, i32, i32]),

@@ -639,6 +639,10 @@ class Window:
         else:
             check(lib.pvo_window_iteration(self.ctx.handle, iterations, damping, None, _capi.PVO_DEVICE))
 
+    def ba(self, iterations: int = 2, damping: float = kDefaultDamping) -> None:
+        """optimize_window's iterations only (no correlation pass)."""
+        check(lib.pvo_window_ba(self.ctx.handle, iterations, damping))
+
     def correlate(self) -> np.ndarray:
         out = np.empty((self.n_edges, 2, 9, 7, 7), np.float32)
         check(lib.pvo_window_correlate(self.ctx.handle, _ptr(out), _capi.PVO_HOST))
@@ -789,12 +793,13 @@ class DeviceGraph:
         check(lib.pvo_dgraph_patches(self.handle, _ptr(ids), _ptr(src), _ptr(d)))
         return ids, src, d
 
-    def load_window(self, window: int) -> tuple:
-        """Flatten the active window on the device into the context's resident Window;
-        returns (n_poses, n_patches, n_edges)."""
+    def load_window(self, window: int, all_active: bool = False) -> tuple:
+        """Flatten the active window on the device into the context's resident Window
+        (revised edges, as optimize_window; all_active: every active edge, the set
+        propose() measures); returns (n_poses, n_patches, n_edges)."""
         a, b, c = C.c_int(), C.c_int(), C.c_int()
-        check(lib.pvo_window_load_dgraph(self.ctx.handle, self.handle, window, C.addressof(a), C.addressof(b),
-                                         C.addressof(c)))
+        check(lib.pvo_window_load_dgraph(self.ctx.handle, self.handle, window, int(all_active), C.addressof(a),
+                                         C.addressof(b), C.addressof(c)))
         win = Window(self.ctx)
         win.n_poses, win.n_patches, win.n_edges = a.value, b.value, c.value
         self.window = win

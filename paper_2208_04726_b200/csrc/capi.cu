@@ -1214,6 +1214,20 @@ int pvo_window_iteration(pvo_ctx* ctx, int iterations, double damping, float* co
     });
 }
 
+// optimize_window's iterations on the resident window without the correlation
+// pass (the per-frame pipeline: propose -> BA, pipeline.cpp:183-198)
+int pvo_window_ba(pvo_ctx* ctx, int iterations, double damping) {
+    return guarded([&] {
+        bind(ctx);
+        Window& w = ctx->win;
+        if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
+        if (iterations < 0) fail(PVO_INVALID_ARGUMENT, "ba: negative iteration count");
+        reset_status(ctx);
+        pvo_dev::BAParams a = window_ba_params(ctx, iterations, damping);
+        launch_ba_checked(ctx, a, w.plan);
+    });
+}
+
 int pvo_window_read(pvo_ctx* ctx, double* poses, double* depth, double* residual_norms, int* n_norms) {
     return guarded([&] {
         bind(ctx);
@@ -1980,9 +1994,12 @@ int pvo_dgraph_patches(pvo_dgraph* g, int* ids, int* src, double* inv_depth) {
 // The optimize_window problem build (bundle_adjust.cpp:231-307) on the device,
 // loaded as the context's resident window (pvo_window_iteration / propose run
 // on it next).  Revision deltas + raw weights: targets are frozen on the
-// device by the BA (freeze_targets semantics).  Windows beyond 16 free poses
-// are not supported on this path yet.
-int pvo_window_load_dgraph(pvo_ctx* ctx, pvo_dgraph* g, int window, int* n_poses, int* n_patches, int* n_edges) {
+// device by the BA (freeze_targets semantics).  all_active != 0 flattens every
+// active edge (Pipeline::active_edges, pipeline.cpp:164-181: revised or not) —
+// the set propose() measures; 0 keeps the revised ones (bundle_adjust.cpp:245).
+// Windows beyond 16 free poses are not supported on this path yet.
+int pvo_window_load_dgraph(pvo_ctx* ctx, pvo_dgraph* g, int window, int all_active, int* n_poses, int* n_patches,
+                           int* n_edges) {
     return guarded([&] {
         bind(ctx);
         if (g->ctx != ctx) fail(PVO_INVALID_ARGUMENT, "window_load_dgraph: the graph belongs to another context");
@@ -2003,10 +2020,10 @@ int pvo_window_load_dgraph(pvo_ctx* ctx, pvo_dgraph* g, int window, int* n_poses
         int* slot_of_pos = ctx->s8.as<int>(F + 1);
         int* nfix = g->w_nfixed.as<int>(1);
         cuda_check(cudaMemsetAsync(used, 0, sizeof(int) * std::max(F, 1), ctx->stream), "memset");
-        cuda_check(pvo_dev::dg_window_pass0(v, window_start, inc, nrev, ctx->stream), "window");
+        cuda_check(pvo_dev::dg_window_pass0(v, window_start, all_active, inc, nrev, ctx->stream), "window");
         cuda_check(pvo_dev::dg_scan(P, inc, pslot, ctx->stream), "scan");
         cuda_check(pvo_dev::dg_scan(P, nrev, eoff, ctx->stream), "scan");
-        cuda_check(pvo_dev::dg_window_used(v, inc, used, ctx->stream), "window");
+        cuda_check(pvo_dev::dg_window_used(v, inc, all_active, used, ctx->stream), "window");
         cuda_check(pvo_dev::dg_scan(F, used, slot_of_pos, ctx->stream), "scan");
         cuda_check(pvo_dev::dg_window_nfixed(v, first_free, used, nfix, ctx->stream), "window");
         int cnt[4];
@@ -2050,7 +2067,9 @@ int pvo_window_load_dgraph(pvo_ctx* ctx, pvo_dgraph* g, int window, int* n_poses
         o.e_weight = B.e_w.as<double>(2 * (size_t)Ew);
         o.e_graph = g->w_e_graph.as<int>(Ew);
         o.order = w.order.as<int>(Ew);
-        cuda_check(pvo_dev::dg_window_write(v, first_free, inc, pslot, eoff, used, slot_of_pos, o, ctx->nf, ctx->stream),
+        o.graph_patch = g->t4.as<int>(Pw);
+        cuda_check(pvo_dev::dg_window_write(v, first_free, inc, all_active, pslot, eoff, used, slot_of_pos, o, ctx->nf,
+                                            ctx->stream),
                    "window");
         ctx->launches += 8;
         // window bookkeeping as pvo_window_load (plan fields used by the kernels)

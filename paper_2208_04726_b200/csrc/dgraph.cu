@@ -166,23 +166,23 @@ __global__ void set_rev_kernel(DGraphView g, int n, const int* ids, const int* f
 // ---- window flattening (bundle_adjust.cpp:231-307, pipeline.cpp:164-181) ----
 // pass 0: per patch, included (source position >= window_start and at least one
 // revised edge) and its revised-edge count
-__global__ void win_patch_kernel(DGraphView g, int window_start, int* inc, int* nrev) {
+__global__ void win_patch_kernel(DGraphView g, int window_start, int all, int* inc, int* nrev) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= g.P) return;
     const int s = frame_pos(g.f_index, g.F, g.p_src[k]);
     int n = 0;
     if (s >= window_start)
-        for (int i = g.ebeg[k]; i < g.ebeg[k + 1]; ++i) n += g.e_has[i];
+        for (int i = g.ebeg[k]; i < g.ebeg[k + 1]; ++i) n += all || g.e_has[i];
     inc[k] = n > 0;
     nrev[k] = n;
 }
 // referenced frames (the pose set): plain stores of 1, order-independent
-__global__ void win_used_kernel(DGraphView g, const int* inc, int* used) {
+__global__ void win_used_kernel(DGraphView g, const int* inc, int all, int* used) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= g.P || !inc[k]) return;
     used[frame_pos(g.f_index, g.F, g.p_src[k])] = 1;
     for (int i = g.ebeg[k]; i < g.ebeg[k + 1]; ++i)
-        if (g.e_has[i]) used[frame_pos(g.f_index, g.F, g.e_frame[i])] = 1;
+        if (all || g.e_has[i]) used[frame_pos(g.f_index, g.F, g.e_frame[i])] = 1;
 }
 __global__ void win_poses_kernel(DGraphView g, int first_free, const int* used, const int* slot_of_pos, WindowOut w) {
     const int pos = blockIdx.x * blockDim.x + threadIdx.x;
@@ -202,7 +202,7 @@ __global__ void win_nfixed_kernel(DGraphView g, int first_free, const int* used,
         *n_fixed = n;
     }
 }
-__global__ void win_patches_kernel(DGraphView g, const int* inc, const int* pslot, const int* eoff,
+__global__ void win_patches_kernel(DGraphView g, const int* inc, int all, const int* pslot, const int* eoff,
                                    const int* slot_of_pos, WindowOut w) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= g.P || !inc[k]) return;
@@ -217,10 +217,10 @@ __global__ void win_patches_kernel(DGraphView g, const int* inc, const int* pslo
     w.depth_slot[q] = q;  // every included patch has a free depth (bundle_adjust.cpp:123-133)
     w.edge_begin[q] = eoff[k];
     if (q == 0) w.edge_begin[w.n_patches] = eoff[g.P];
-    for (size_t c = 0; c < g.feat_stride; ++c) w.patch_feats[g.feat_stride * q + c] = g.p_feat[g.feat_stride * k + c];
+    w.graph_patch[q] = k;
     int o = eoff[k];
     for (int i = g.ebeg[k]; i < g.ebeg[k + 1]; ++i) {
-        if (!g.e_has[i]) continue;
+        if (!all && !g.e_has[i]) continue;
         w.e_patch[o] = q;
         w.e_pose[o] = slot_of_pos[frame_pos(g.f_index, g.F, g.e_frame[i])];
         w.e_delta[2 * (size_t)o] = g.e_rev[4 * (size_t)i];
@@ -231,6 +231,22 @@ __global__ void win_patches_kernel(DGraphView g, const int* inc, const int* pslo
         ++o;
     }
 }
+// the window patches' descriptors, coalesced (one float4 per thread)
+__global__ void win_feats_kernel(DGraphView g, WindowOut w) {
+    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g.feat_stride % 4 == 0) {
+        const size_t n4 = g.feat_stride / 4;
+        if (t >= (size_t)w.n_patches * n4) return;
+        const size_t q = t / n4, c = t - q * n4;
+        reinterpret_cast<float4*>(w.patch_feats)[q * n4 + c] =
+            reinterpret_cast<const float4*>(g.p_feat)[(size_t)w.graph_patch[q] * n4 + c];
+    } else {  // odd channel counts: one float per thread
+        if (t >= (size_t)w.n_patches * g.feat_stride) return;
+        const size_t q = t / g.feat_stride, c = t - q * g.feat_stride;
+        w.patch_feats[q * g.feat_stride + c] = g.p_feat[(size_t)w.graph_patch[q] * g.feat_stride + c];
+    }
+}
+
 // stable counting sort of the window edges by frame-store slot (the correlation
 // kernel's L2-friendly order), one CTA: slot-major, edge order inside a slot
 __global__ void __launch_bounds__(kScanThreads) slot_order_kernel(int E, const int* e_pose, const int* pose_slot,
@@ -323,21 +339,25 @@ cudaError_t dg_set_revisions(const DGraphView& g, int n, const int* ids, const i
     set_rev_kernel<<<blocks(n), 128, 0, s>>>(g, n, ids, frames, rev, missing);
     return cudaGetLastError();
 }
-cudaError_t dg_window_pass0(const DGraphView& g, int window_start, int* inc, int* nrev, cudaStream_t s) {
+cudaError_t dg_window_pass0(const DGraphView& g, int window_start, int all, int* inc, int* nrev, cudaStream_t s) {
     if (g.P <= 0) return cudaSuccess;
-    win_patch_kernel<<<blocks(g.P), 128, 0, s>>>(g, window_start, inc, nrev);
+    win_patch_kernel<<<blocks(g.P), 128, 0, s>>>(g, window_start, all, inc, nrev);
     return cudaGetLastError();
 }
-cudaError_t dg_window_used(const DGraphView& g, const int* inc, int* used, cudaStream_t s) {
+cudaError_t dg_window_used(const DGraphView& g, const int* inc, int all, int* used, cudaStream_t s) {
     if (g.P <= 0) return cudaSuccess;
-    win_used_kernel<<<blocks(g.P), 128, 0, s>>>(g, inc, used);
+    win_used_kernel<<<blocks(g.P), 128, 0, s>>>(g, inc, all, used);
     return cudaGetLastError();
 }
-cudaError_t dg_window_write(const DGraphView& g, int first_free, const int* inc, const int* pslot, const int* eoff,
-                            const int* used, const int* slot_of_pos, const WindowOut& w, int n_slots,
+cudaError_t dg_window_write(const DGraphView& g, int first_free, const int* inc, int all, const int* pslot,
+                            const int* eoff, const int* used, const int* slot_of_pos, const WindowOut& w, int n_slots,
                             cudaStream_t s) {
     win_poses_kernel<<<blocks(g.F), 128, 0, s>>>(g, first_free, used, slot_of_pos, w);
-    if (g.P > 0) win_patches_kernel<<<blocks(g.P), 128, 0, s>>>(g, inc, pslot, eoff, slot_of_pos, w);
+    if (g.P > 0) win_patches_kernel<<<blocks(g.P), 128, 0, s>>>(g, inc, all, pslot, eoff, slot_of_pos, w);
+    if (g.feat_stride && w.n_patches) {
+        const size_t n = (size_t)w.n_patches * (g.feat_stride % 4 == 0 ? g.feat_stride / 4 : g.feat_stride);
+        win_feats_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, w);
+    }
     if (w.order && w.n_edges > 0) slot_order_kernel<<<1, kScanThreads, 0, s>>>(w.n_edges, w.e_pose, w.pose_slot, n_slots, w.order);
     return cudaGetLastError();
 }

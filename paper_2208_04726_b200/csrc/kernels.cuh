@@ -148,6 +148,7 @@ struct WindowOut {
     double* e_weight = nullptr;
     int* e_graph = nullptr;   // graph edge index of each window edge
     int* order = nullptr;     // edges sorted by frame-store slot (stable), or null
+    int* graph_patch = nullptr;  // [n_patches] graph patch index of each window patch (scratch)
 };
 cudaError_t dg_scan(int n, const int* in, int* out, cudaStream_t s);
 cudaError_t dg_connect(const DGraphView& g, int radius, int pass, int* newlen, const int* new_ebeg, int* out_frame,
@@ -156,10 +157,10 @@ cudaError_t dg_remove(const DGraphView& g, int frame, int pass, int* keep, int* 
                       const int* new_ebeg, const DGraphView& out, cudaStream_t s);
 cudaError_t dg_set_revisions(const DGraphView& g, int n, const int* ids, const int* frames, const double* rev,
                              int* missing, cudaStream_t s);
-cudaError_t dg_window_pass0(const DGraphView& g, int window_start, int* inc, int* nrev, cudaStream_t s);
-cudaError_t dg_window_used(const DGraphView& g, const int* inc, int* used, cudaStream_t s);
-cudaError_t dg_window_write(const DGraphView& g, int first_free, const int* inc, const int* pslot, const int* eoff,
-                            const int* used, const int* slot_of_pos, const WindowOut& w, int n_slots,
+cudaError_t dg_window_pass0(const DGraphView& g, int window_start, int all, int* inc, int* nrev, cudaStream_t s);
+cudaError_t dg_window_used(const DGraphView& g, const int* inc, int all, int* used, cudaStream_t s);
+cudaError_t dg_window_write(const DGraphView& g, int first_free, const int* inc, int all, const int* pslot,
+                            const int* eoff, const int* used, const int* slot_of_pos, const WindowOut& w, int n_slots,
                             cudaStream_t s);
 cudaError_t dg_window_nfixed(const DGraphView& g, int first_free, const int* used, int* n_fixed, cudaStream_t s);
 cudaError_t dg_store_revisions(const DGraphView& g, int n_edges, const int* e_graph, const double* delta,

@@ -1,0 +1,73 @@
+"""Per-frame DPVO update entirely on the device (SURVEY.md §8f rows 1 + 3):
+new frame pyramid -> device graph (add frame / patches, connect) -> on-device
+window flatten -> propose (flow-provider measurement at the current state) ->
+revisions into the graph -> optimize_window (2 GN iterations) -> write-back.
+
+usage: python tools/pipeline_loop.py [frames=30] [config=c2]
+Prints the mean per-frame device time of each stage over the second half of
+the sequence (CUDA events on the context stream) and the host wall time."""
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import paper_2208_04726_b200 as pvo  # noqa: E402
+from paper_2208_04726_b200 import synth  # noqa: E402
+
+n_frames = int(sys.argv[1]) if len(sys.argv) > 1 else 30
+cfg = sys.argv[2] if len(sys.argv) > 2 else "c2"
+w = synth.generate(cfg, seed=5, frames=n_frames)
+F, M = w.cfg["frames"], w.cfg["patches"]
+_, H0, W0, D = w.level0.shape
+_, H1, W1, _ = w.level1.shape
+ctx = pvo.Context(0)
+stream = torch.cuda.Stream()
+ctx.set_stream(stream.cuda_stream)
+NS = 32  # frame-store ring: the window plus every frame its edges still reach
+ctx.frames_reserve(NS, W0, H0, W1, H1, D)
+dev = pvo.DeviceGraph(ctx, w.K, w.image[0], w.image[1], channels=D)
+l0 = [torch.from_numpy(w.level0[f]).pin_memory() for f in range(F)]
+l1 = [torch.from_numpy(w.level1[f]).pin_memory() for f in range(F)]
+stages = ["frame H2D + Gram", "graph add + connect", "flatten", "propose", "BA (2 it.)", "store"]
+acc = {s: [] for s in stages}
+walls, edges = [], []
+with torch.cuda.stream(stream):
+    for f in range(F):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)]
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ev[0].record(stream)
+        ctx.frames_upload(f % NS, l0[f].numpy(), l1[f].numpy())
+        ev[1].record(stream)
+        idx = dev.add_frame(0.05 * (f + 1), w.poses[f], frame_slot=f % NS)
+        ks = slice(f * M, (f + 1) * M)
+        dev.add_patches(idx, w.centroids[ks], w.depth[ks], w.patch_feats[ks])
+        dev.connect(w.cfg["radius"])
+        ev[2].record(stream)
+        # every active edge (pipeline.cpp:164-181); after propose all of them are revised,
+        # so this window is also optimize_window's problem (bundle_adjust.cpp:245)
+        n = dev.load_window(w.cfg["window"], all_active=True)
+        ev[3].record(stream)
+        dev.window.propose(read_back=False)
+        ev[4].record(stream)
+        dev.window.ba(2)
+        ev[5].record(stream)
+        dev.store_window(revisions=True, state=True)
+        ev[6].record(stream)
+        ev[6].synchronize()
+        walls.append(time.perf_counter() - t0)
+        edges.append(n[2])
+        if f >= F // 2:
+            for i, s in enumerate(stages):
+                acc[s].append(ev[i].elapsed_time(ev[i + 1]))
+print(f"{cfg}: {F} frames, {M} patches/frame, window {w.cfg['window']}, radius {w.cfg['radius']}; "
+      f"active edges at the end {edges[-1]}")
+tot = 0.0
+for s in stages:
+    m = float(np.mean(acc[s]))
+    tot += m
+    print(f"  {s:22s} {m:8.3f} ms")
+print(f"  {'device total':22s} {tot:8.3f} ms   host wall per frame {1e3 * np.mean(walls[F // 2:]):.3f} ms")
