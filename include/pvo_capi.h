@@ -212,6 +212,9 @@ int pvo_dgraph_remove_frame(pvo_dgraph* g, int frame);
 int pvo_dgraph_set_revisions(pvo_dgraph* g, int n, const int* patch_ids, const int* frames, const double* deltas,
                              const double* weights);
 int pvo_dgraph_counts(pvo_dgraph* g, int* n_frames, int* n_patches, int* n_edges);
+/* Pipeline::keyframe (pipeline.cpp:208-245) on the device graph: removes keyframe t-4 when the mean
+ * reprojected displacement t-5 -> t-3 is below threshold_px; removed = frame index or -1.          */
+int pvo_dgraph_keyframe(pvo_dgraph* g, double threshold_px, int* removed, double* mean_flow, int* n_used);
 int pvo_dgraph_edges(pvo_dgraph* g, int* kk, int* jj, double* rev, uint8_t* has_rev);
 int pvo_dgraph_frames(pvo_dgraph* g, int* indices, double* poses);
 int pvo_dgraph_patches(pvo_dgraph* g, int* ids, int* src, double* inv_depth);

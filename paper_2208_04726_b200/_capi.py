@@ -74,6 +74,7 @@ SIGNATURES = {
     "pvo_dgraph_remove_frame": (i32, [vp, i32]),
     "pvo_dgraph_set_revisions": (i32, [vp, i32, P, P, P, P]),
     "pvo_dgraph_counts": (i32, [vp, P, P, P]),
+    "pvo_dgraph_keyframe": (i32, [vp, f64, P, P, P]),
     "pvo_dgraph_edges": (i32, [vp, P, P, P, P]),
     "pvo_dgraph_frames": (i32, [vp, P, P]),
     "pvo_dgraph_patches": (i32, [vp, P, P, P]),

@@ -768,6 +768,12 @@ class DeviceGraph:
         check(lib.pvo_dgraph_set_revisions(self.handle, k.shape[0], _ptr(k), _ptr(j), _ptr(_f64(deltas).reshape(-1, 2)),
                                            _ptr(_f64(weights).reshape(-1, 2))))
 
+    def keyframe(self, threshold_px: float):
+        """Pipeline::keyframe (pipeline.cpp:208-245) -> (removed frame or -1, mean flow, patches used)."""
+        r, m, n = C.c_int(), C.c_double(), C.c_int()
+        check(lib.pvo_dgraph_keyframe(self.handle, float(threshold_px), C.addressof(r), C.addressof(m), C.addressof(n)))
+        return r.value, m.value, n.value
+
     def counts(self):
         a, b, c = C.c_int(), C.c_int(), C.c_int()
         check(lib.pvo_dgraph_counts(self.handle, C.addressof(a), C.addressof(b), C.addressof(c)))

@@ -1991,6 +1991,39 @@ int pvo_dgraph_patches(pvo_dgraph* g, int* ids, int* src, double* inv_depth) {
     });
 }
 
+// Pipeline::keyframe (pipeline.cpp:208-245): with >= 6 frames, the mean
+// reprojected displacement between keyframes t-5 and t-3 over the patches
+// seen in both; below threshold_px the candidate t-4 is removed.  removed =
+// the removed frame index or -1; mean_flow / n_used report the statistic.
+int pvo_dgraph_keyframe(pvo_dgraph* g, double threshold_px, int* removed, double* mean_flow, int* n_used) {
+    return guarded([&] {
+        pvo_ctx* ctx = g->ctx;
+        bind(ctx);
+        if (removed) *removed = -1;
+        if (mean_flow) *mean_flow = 0.0;
+        if (n_used) *n_used = 0;
+        const int F = static_cast<int>(g->f_index.size());
+        if (F < 6) return;  // need keyframes t-5 .. t
+        const int frame_a = g->f_index[F - 6], frame_b = g->f_index[F - 4], candidate = g->f_index[F - 5];
+        double* flow = g->t4.as<double>(std::max(g->P, 1));
+        int* ok = g->t0.as<int>(std::max(g->P, 1));
+        double* out = ctx->s6.as<double>(2);
+        cuda_check(pvo_dev::dg_keyframe_flow(g->view(g->cur), frame_a, frame_b, g->K, flow, ok, out, ctx->stream),
+                   "keyframe");
+        double h[2];
+        download(ctx, h, out, 2);
+        sync(ctx);
+        if (mean_flow) *mean_flow = h[0];
+        if (n_used) *n_used = static_cast<int>(h[1]);
+        if (h[1] == 0) return;
+        if (h[0] < threshold_px) {
+            const int st = pvo_dgraph_remove_frame(g, candidate);
+            if (st != PVO_OK) fail(st, std::string("keyframe: ") + pvo_last_error());
+            if (removed) *removed = candidate;
+        }
+    });
+}
+
 // The optimize_window problem build (bundle_adjust.cpp:231-307) on the device,
 // loaded as the context's resident window (pvo_window_iteration / propose run
 // on it next).  Revision deltas + raw weights: targets are frozen on the

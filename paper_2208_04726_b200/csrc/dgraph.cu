@@ -20,6 +20,7 @@
 
 #include <cstdint>
 
+#include "ba_common.cuh"
 #include "kernels.cuh"
 
 namespace pvo_dev {
@@ -313,6 +314,47 @@ __global__ void store_rev_kernel(DGraphView g, int n_edges, const int* e_graph, 
     g.e_rev[4 * (size_t)i + 3] = weight[2 * (size_t)e + 1];
 }
 
+// Pipeline::keyframe's flow test (pipeline.cpp:208-245), per patch: both edges
+// (patch, frame_a) and (patch, frame_b) present and neither reprojection behind
+// the camera -> |center_b - center_a|
+__global__ void keyframe_flow_kernel(DGraphView g, int frame_a, int frame_b, Cam K, double* flow, int* ok) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= g.P) return;
+    bool ha = false, hb = false;
+    for (int i = g.ebeg[k]; i < g.ebeg[k + 1]; ++i) {
+        ha = ha || g.e_frame[i] == frame_a;
+        hb = hb || g.e_frame[i] == frame_b;
+    }
+    ok[k] = 0;
+    if (!ha || !hb) return;
+    const int ps = frame_pos(g.f_index, g.F, g.p_src[k]);
+    const int pa = frame_pos(g.f_index, g.F, frame_a), pb = frame_pos(g.f_index, g.F, frame_b);
+    const SE3 src = se3_load(g.f_pose + 7 * (size_t)ps);
+    double ua, va, ub, vb;
+    bool ba, bb;
+    reproject_center(src, se3_load(g.f_pose + 7 * (size_t)pa), K, g.p_x + 9 * (size_t)k, g.p_y + 9 * (size_t)k, g.p_d[k],
+                     &ua, &va, &ba);
+    reproject_center(src, se3_load(g.f_pose + 7 * (size_t)pb), K, g.p_x + 9 * (size_t)k, g.p_y + 9 * (size_t)k, g.p_d[k],
+                     &ub, &vb, &bb);
+    if (ba || bb) return;
+    const double dx = ub - ua, dy = vb - va;
+    flow[k] = sqrt(dx * dx + dy * dy);
+    ok[k] = 1;
+}
+// the mean in the reference's (patch id) order: one thread, sequential sum
+__global__ void keyframe_mean_kernel(int P, const double* flow, const int* ok, double* out) {
+    if (threadIdx.x || blockIdx.x) return;
+    double sum = 0;
+    int count = 0;
+    for (int k = 0; k < P; ++k)
+        if (ok[k]) {
+            sum += flow[k];
+            ++count;
+        }
+    out[0] = count ? sum / count : 0.0;
+    out[1] = count;
+}
+
 int blocks(int n) { return n > 0 ? (n + 127) / 128 : 1; }
 
 }  // namespace
@@ -369,6 +411,12 @@ cudaError_t dg_store_revisions(const DGraphView& g, int n_edges, const int* e_gr
                                const double* weight, cudaStream_t s) {
     if (n_edges <= 0) return cudaSuccess;
     store_rev_kernel<<<blocks(n_edges), 128, 0, s>>>(g, n_edges, e_graph, delta, weight);
+    return cudaGetLastError();
+}
+cudaError_t dg_keyframe_flow(const DGraphView& g, int frame_a, int frame_b, const double* K, double* flow, int* ok,
+                             double* out, cudaStream_t s) {
+    if (g.P > 0) keyframe_flow_kernel<<<blocks(g.P), 128, 0, s>>>(g, frame_a, frame_b, Cam{K[0], K[1], K[2], K[3]}, flow, ok);
+    keyframe_mean_kernel<<<1, 32, 0, s>>>(g.P, flow, ok, out);
     return cudaGetLastError();
 }
 cudaError_t dg_writeback(const DGraphView& g, int n_poses, const int* pose_frames, const uint8_t* fixed,

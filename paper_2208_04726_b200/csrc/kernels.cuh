@@ -165,6 +165,9 @@ cudaError_t dg_window_write(const DGraphView& g, int first_free, const int* inc,
 cudaError_t dg_window_nfixed(const DGraphView& g, int first_free, const int* used, int* n_fixed, cudaStream_t s);
 cudaError_t dg_store_revisions(const DGraphView& g, int n_edges, const int* e_graph, const double* delta,
                                const double* weight, cudaStream_t s);
+// K: host intrinsics (passed by value to the kernel)
+cudaError_t dg_keyframe_flow(const DGraphView& g, int frame_a, int frame_b, const double* K, double* flow, int* ok,
+                             double* out, cudaStream_t s);
 cudaError_t dg_writeback(const DGraphView& g, int n_poses, const int* pose_frames, const uint8_t* fixed,
                          const double* poses, int n_patches, const int* patch_ids, const double* depth,
                          cudaStream_t s);

@@ -698,3 +698,65 @@ def test_device_graph_window_loop_matches_host_path(ctx):
     key = {(int(a), int(b)): i for i, (a, b) in enumerate(zip(kk, jj))}
     rows = [key[(int(prob["patch_ids"][k]), int(prob["pose_frames"][j]))] for k, j in zip(prob["e_patch"], prob["e_pose"])]
     assert has[rows].all() and np.array_equal(rev[rows, :2], pd) and np.array_equal(rev[rows, 2:], pw)
+
+
+def test_device_graph_keyframe_matches_pipeline_rule(ctx):
+    """Pipeline::keyframe (pipeline.cpp:208-245) on the device graph: the flow
+    statistic over patches seen in keyframes t-5 and t-3 (reproject_patch with
+    the behind-camera skip) matches a direct evaluation, and removals keep the
+    device graph identical to the host graph."""
+    rng = np.random.default_rng(9)
+    image = (640, 480)
+    K = np.array([320.0, 320.0, 320.0, 240.0])
+    host = pvo.PatchGraph(K, image[0], image[1], 3)
+    dev = pvo.DeviceGraph(ctx, K, image[0], image[1], channels=0)
+    cents = {}
+    removed_any = 0
+    for f in range(14):
+        pose = orc.se3_exp(np.concatenate([rng.normal(0, 0.05, 3) + [0.1 * f, 0, 0], rng.normal(0, 0.02, 3)]))
+        a = host.add_frame(0.05 * (f + 1), pose)
+        dev.add_frame(0.05 * (f + 1), pose)
+        c = np.stack([rng.uniform(3, image[0] - 4, 12), rng.uniform(3, image[1] - 4, 12)], 1)
+        d = rng.uniform(0.05, 1.0, 12)
+        ids = host.add_patches(a, c, d)
+        assert dev.add_patches(a, c, d) == ids
+        for i, pid in enumerate(ids):
+            cents[pid] = c[i]
+        host.connect(6)
+        dev.connect(6)
+        # expected statistic from the host graph
+        fidx, fposes = host.frames()
+        F = len(fidx)
+        thr = 1e9 if f % 2 == 0 else 0.0
+        removed, mean, used = dev.keyframe(thr)
+        if F < 6:
+            assert removed == -1 and used == 0
+            continue
+        fa, fb, cand = int(fidx[F - 6]), int(fidx[F - 4]), int(fidx[F - 5])
+        kk, jj, _, _ = host.edges()
+        es = set(zip(kk.tolist(), jj.tolist()))
+        pids, psrc, pdep = host.patches()
+        pose_of = {int(i): fposes[n] for n, i in enumerate(fidx)}
+        tot, cnt = 0.0, 0
+        for pid, src, dep in zip(pids, psrc, pdep):
+            if (int(pid), fa) not in es or (int(pid), fb) not in es:
+                continue
+            gx, gy = np.meshgrid(np.arange(3) - 1.0, np.arange(3) - 1.0)
+            px, py = cents[int(pid)][0] + gx.ravel(), cents[int(pid)][1] + gy.ravel()
+            ca, ba = orc.reproject_patch(pose_of[int(src)], pose_of[fa], K, px, py, dep)
+            cb, bb = orc.reproject_patch(pose_of[int(src)], pose_of[fb], K, px, py, dep)
+            if ba or bb:
+                continue
+            tot += np.hypot(*(cb[4] - ca[4]))
+            cnt += 1
+        assert used == cnt
+        if cnt:
+            assert abs(mean - tot / cnt) <= 1e-9 * max(1.0, abs(tot / cnt))
+            if tot / cnt < thr:
+                assert removed == cand
+                host.remove_frame(cand)
+                removed_any += 1
+        hk, hj, _, _ = host.edges()
+        dk, dj, _, _ = dev.edges()
+        assert np.array_equal(hk, dk) and np.array_equal(hj, dj)
+    assert removed_any >= 2
