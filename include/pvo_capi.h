@@ -177,6 +177,19 @@ int pvo_window_read(pvo_ctx* ctx, double* poses, double* inv_depth, double* resi
 /* Device pointer of the window's correlation volume buffer [E][2][pp][49]. */
 int pvo_window_corr_ptr(pvo_ctx* ctx, float** corr);
 
+/* ---- feature extraction (features.cpp:55-235) ---------
+ * pvo_frames_extract: extract_features (pool 4x4, whiten, lift 5x5 -> 25 * bc
+ * unit descriptors; level 1 from the 4x4-pooled base grid) of an image
+ * [ih][iw] into frame-store slot `slot` (+ Gram terms), bit-identical to the
+ * reference's CPU arithmetic.  The store must be reserved with C = 25 * bc and
+ * levels (iw/4, ih/4), (iw/16, ih/16).  pvo_crop_patches:
+ * crop_patch_features at the 3x3 grids of n centroids -> out [n][2][9][C].  */
+int pvo_frames_extract(pvo_ctx* ctx, int slot, const float* image, int image_w, int image_h, int base_channels,
+                       int memspace);
+int pvo_crop_patches(pvo_ctx* ctx, int slot, int n, const double* centroids, float* out, int memspace);
+/* A slot's pyramid back to the host (either pointer may be NULL). */
+int pvo_frames_download(pvo_ctx* ctx, int slot, float* level0, float* level1);
+
 /* ---- correlation flow provider (flow_provider.cpp:150-312) --
  * pvo_measure_batch: CorrelationFlowProvider::measure per edge against the
  * frame store: centers [E][2] = reproject_patch(...).points[centre], behind

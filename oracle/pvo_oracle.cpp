@@ -13,6 +13,8 @@
 //   camera.cpp:15-108         Patch::make, reproject_patch, reprojection_jacobians
 //   features.cpp:9-52         FeatureGrid::sample_zero_padded / sample_cubic
 //   correlation.cpp:8-71      correlate_at, correlate
+//   features.cpp:55-235      feature pyramid extraction (pool, whiten, lift) and
+//                             crop_patch_features
 //   flow_provider.cpp:150-287 CorrelationFlowProvider::measure (parabola_refine,
 //                             subpixel_peak) and propose's per-edge part (:289-314)
 //   patch_graph.cpp:27-173    PatchGraph (std::map keyed, same iteration order)
@@ -1493,6 +1495,127 @@ int orc_measure_batch(int n_edges, const int* e_patch, const int* e_frame, const
         for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
         work(0);
         for (auto& th : pool) th.join();
+    });
+}
+
+// ---- feature extraction (features.cpp:55-235) ----
+// image [ih][iw] float; level0 [ih/4][iw/4][25 bc], level1 [ih/16][iw/16][25 bc]
+int orc_extract_features(const float* image, int iw, int ih, int bc, float* level0, float* level1) {
+    return guard([&] {
+        if (bc != 1 && bc != 3) throw std::invalid_argument("features: base channel count must be 1 or 3");
+        if (iw < 12 || ih < 12) throw std::invalid_argument("features: image too small");
+        const int w = iw / 4, h = ih / 4;
+        std::vector<float> raw((size_t)w * h), rough((size_t)w * h), res((size_t)w * h), base((size_t)w * h * bc);
+        // pool_image: float sums over 4x4 blocks (features.cpp:55-71)
+        for (int y = 0; y < h; ++y)
+            for (int x = 0; x < w; ++x) {
+                float sum = 0;
+                for (int dy = 0; dy < 4; ++dy)
+                    for (int dx = 0; dx < 4; ++dx) sum += image[(size_t)(4 * y + dy) * iw + 4 * x + dx];
+                raw[(size_t)y * w + x] = sum / 16.0f;
+            }
+        auto clipped = [&](int x, int y, int r, auto&& f) {
+            for (int dy = -r; dy <= r; ++dy)
+                for (int dx = -r; dx <= r; ++dx) {
+                    const int xi = x + dx, yi = y + dy;
+                    if (xi < 0 || yi < 0 || xi >= w || yi >= h) continue;
+                    f(xi, yi, dx, dy);
+                }
+        };
+        // residual against the clipped 5x5 mean (features.cpp:105-121)
+        for (int y = 0; y < h; ++y)
+            for (int x = 0; x < w; ++x) {
+                double sum = 0;
+                int count = 0;
+                clipped(x, y, 2, [&](int xi, int yi, int, int) {
+                    sum += raw[(size_t)yi * w + xi];
+                    ++count;
+                });
+                rough[(size_t)y * w + x] = raw[(size_t)y * w + x] - static_cast<float>(sum / count);
+            }
+        // 3x3 binomial smoothing (features.cpp:123-141)
+        const double kern[3] = {1, 2, 1};
+        for (int y = 0; y < h; ++y)
+            for (int x = 0; x < w; ++x) {
+                double sum = 0, wt = 0;
+                clipped(x, y, 1, [&](int xi, int yi, int dx, int dy) {
+                    const double k = kern[dx + 1] * kern[dy + 1];
+                    sum += k * rough[(size_t)yi * w + xi];
+                    wt += k;
+                });
+                res[(size_t)y * w + x] = static_cast<float>(sum / wt);
+            }
+        // local-RMS normalisation (features.cpp:143-160)
+        for (int y = 0; y < h; ++y)
+            for (int x = 0; x < w; ++x) {
+                double sum_sq = 0;
+                int count = 0;
+                clipped(x, y, 2, [&](int xi, int yi, int, int) {
+                    const float r = res[(size_t)yi * w + xi];
+                    sum_sq += r * r;
+                    ++count;
+                });
+                const double rms = std::sqrt(sum_sq / count);
+                base[((size_t)y * w + x) * bc] = rms > 1e-6 ? res[(size_t)y * w + x] / static_cast<float>(rms) : 0.0f;
+            }
+        if (bc == 3) {  // central-difference gradients (features.cpp:162-173)
+            auto g0 = [&](int x, int y) { return base[((size_t)y * w + x) * 3]; };
+            for (int y = 0; y < h; ++y)
+                for (int x = 0; x < w; ++x) {
+                    base[((size_t)y * w + x) * 3 + 1] = 0.5f * (g0(std::min(x + 1, w - 1), y) - g0(std::max(x - 1, 0), y));
+                    base[((size_t)y * w + x) * 3 + 2] = 0.5f * (g0(x, std::min(y + 1, h - 1)) - g0(x, std::max(y - 1, 0)));
+                }
+        }
+        // lift_neighborhood (features.cpp:177-200)
+        auto lift = [&](const std::vector<float>& g, int gw, int gh, float* out) {
+            const int C = 25 * bc;
+            for (int y = 0; y < gh; ++y)
+                for (int x = 0; x < gw; ++x) {
+                    float* o = out + ((size_t)y * gw + x) * C;
+                    int ch = 0;
+                    for (int dy = -2; dy <= 2; ++dy)
+                        for (int dx = -2; dx <= 2; ++dx) {
+                            const int xi = x + dx, yi = y + dy;
+                            const bool in = xi >= 0 && yi >= 0 && xi < gw && yi < gh;
+                            for (int c = 0; c < bc; ++c) o[ch++] = in ? g[((size_t)yi * gw + xi) * bc + c] : 0.0f;
+                        }
+                    double nsq = 0;
+                    for (int c = 0; c < C; ++c) nsq += o[c] * o[c];
+                    if (nsq > 1e-12) {
+                        const float inv = static_cast<float>(1.0 / std::sqrt(nsq));
+                        for (int c = 0; c < C; ++c) o[c] *= inv;
+                    }
+                }
+        };
+        lift(base, w, h, level0);
+        // level 1: pool_features of the base grid, lifted (features.cpp:73-89, :226-231)
+        const int w1 = w / 4, h1 = h / 4;
+        std::vector<float> pooled((size_t)w1 * h1 * bc);
+        for (int y = 0; y < h1; ++y)
+            for (int x = 0; x < w1; ++x)
+                for (int c = 0; c < bc; ++c) {
+                    float sum = 0;
+                    for (int dy = 0; dy < 4; ++dy)
+                        for (int dx = 0; dx < 4; ++dx) sum += base[((size_t)(4 * y + dy) * w + 4 * x + dx) * bc + c];
+                    pooled[((size_t)y * w1 + x) * bc + c] = sum / 16.0f;
+                }
+        lift(pooled, w1, h1, level1);
+    });
+}
+
+// crop_patch_features (features.cpp:204-224): out [n][2][9][C]
+int orc_crop_patches(int n, const double* px, const double* py, const float* l0, int w0, int h0, const float* l1,
+                     int w1, int h1, int C, float* out) {
+    return guard([&] {
+        const GridView grids[2] = {GridView{l0, w0, h0, C}, GridView{l1, w1, h1, C}};
+        for (int p = 0; p < n; ++p)
+            for (int level = 0; level < 2; ++level) {
+                const double stride = level == 0 ? kFeatureStride : kFeatureStride * kFeatureStride;
+                for (int k = 0; k < 9; ++k)
+                    for (int c = 0; c < C; ++c)
+                        out[(((size_t)p * 2 + level) * 9 + k) * C + c] = static_cast<float>(
+                            grids[level].sample_cubic(px[9 * (size_t)p + k] / stride, py[9 * (size_t)p + k] / stride, c));
+            }
     });
 }
 

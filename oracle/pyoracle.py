@@ -370,3 +370,25 @@ def ldlt_solve(a, rhs):
     ok = I()
     check(lib.orc_ldlt_solve(I(n), _p(a), _p(_f64(rhs).ravel()), _p(x), C.byref(ok)))
     return x, bool(ok.value)
+
+
+def extract_features(image, base_channels=1):
+    """extract_features (features.cpp:55-235): -> (level0 [H/4, W/4, 25 bc], level1 [H/16, W/16, 25 bc])."""
+    img = np.ascontiguousarray(image, np.float32)
+    ih, iw = img.shape
+    C = 25 * base_channels
+    l0 = np.empty((ih // 4, iw // 4, C), np.float32)
+    l1 = np.empty((ih // 16, iw // 16, C), np.float32)
+    check(lib.orc_extract_features(_p(img), I(iw), I(ih), I(base_channels), _p(l0), _p(l1)))
+    return l0, l1
+
+
+def crop_patches(px, py, level0, level1):
+    """crop_patch_features (features.cpp:204-224) for n patches: -> [n, 2, 9, C]."""
+    x, y = _f64(px).reshape(-1, 9), _f64(py).reshape(-1, 9)
+    l0, l1 = np.ascontiguousarray(level0, np.float32), np.ascontiguousarray(level1, np.float32)
+    C = l0.shape[2]
+    out = np.empty((x.shape[0], 2, 9, C), np.float32)
+    check(lib.orc_crop_patches(I(x.shape[0]), _p(x), _p(y), _p(l0), I(l0.shape[1]), I(l0.shape[0]), _p(l1),
+                               I(l1.shape[1]), I(l1.shape[0]), I(C), _p(out)))
+    return out

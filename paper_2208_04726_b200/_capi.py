@@ -64,6 +64,9 @@ SIGNATURES = {
     "pvo_window_ba": (i32, [vp, i32, f64]),
     "pvo_window_read": (i32, [vp, P, P, P, P]),
     "pvo_window_corr_ptr": (i32, [vp, P]),
+    "pvo_frames_extract": (i32, [vp, i32, P, i32, i32, i32, i32]),
+    "pvo_crop_patches": (i32, [vp, i32, i32, P, P, i32]),
+    "pvo_frames_download": (i32, [vp, i32, P, P]),
     "pvo_measure_batch": (i32, [vp, i32, i32, i32, P, P, P, P, P, P, P, P]),
     "pvo_window_propose": (i32, [vp, P, P, P]),
     "pvo_dgraph_create": (i32, [vp, P, i32, i32, i32, i32, C.POINTER(vp)]),

@@ -151,6 +151,25 @@ class Context:
     def frames_refresh(self, slot: int) -> None:
         check(lib.pvo_frames_refresh(self.handle, slot))
 
+    def frames_extract(self, slot: int, image, base_channels: int = 1) -> None:
+        """extract_features (features.cpp:55-235) of an image [H][W] into a store slot."""
+        img = _f32(image)
+        check(lib.pvo_frames_extract(self.handle, slot, _ptr(img), img.shape[1], img.shape[0], base_channels,
+                                     _capi.PVO_HOST))
+
+    def frames_download(self, slot: int):
+        w0, h0, w1, h1, C = self.frame_shape
+        l0, l1 = np.empty((h0, w0, C), np.float32), np.empty((h1, w1, C), np.float32)
+        check(lib.pvo_frames_download(self.handle, slot, _ptr(l0), _ptr(l1)))
+        return l0, l1
+
+    def crop_patches(self, slot: int, centroids) -> np.ndarray:
+        """crop_patch_features (features.cpp:204-224) at n centroids -> [n, 2, 9, C]."""
+        c = _f64(centroids).reshape(-1, 2)
+        out = np.empty((c.shape[0], 2, 9, self.frame_shape[4]), np.float32)
+        check(lib.pvo_crop_patches(self.handle, slot, c.shape[0], _ptr(c), _ptr(out), _capi.PVO_HOST))
+        return out
+
     def frames_device_ptrs(self) -> tuple[int, int]:
         a, b = C.c_void_p(), C.c_void_p()
         check(lib.pvo_frames_device_ptrs(self.handle, C.addressof(a), C.addressof(b)))

@@ -1249,6 +1249,76 @@ int pvo_window_read(pvo_ctx* ctx, double* poses, double* depth, double* residual
     });
 }
 
+// ---- feature extraction (features.cpp:55-235) -----------
+// The frame's pyramid from its image, on the device, into frame-store `slot`
+// (+ its Gram terms).  The store must have been reserved with C = 25 * bc and
+// level sizes (iw/4, ih/4), (iw/16, ih/16).
+int pvo_frames_extract(pvo_ctx* ctx, int slot, const float* image, int iw, int ih, int base_channels, int memspace) {
+    return guarded([&] {
+        bind(ctx);
+        if (base_channels != 1 && base_channels != 3) fail(PVO_INVALID_ARGUMENT, "features: base channel count must be 1 or 3");
+        if (iw < 12 || ih < 12) fail(PVO_INVALID_ARGUMENT, "features: image too small");
+        if (slot < 0 || slot >= ctx->nf) fail(PVO_OUT_OF_RANGE, "frames: slot out of range");
+        if (ctx->C != 25 * base_channels || ctx->w0 != iw / 4 || ctx->h0 != ih / 4 || ctx->w1 != iw / 16 ||
+            ctx->h1 != ih / 16)
+            fail(PVO_INVALID_ARGUMENT, "frames_extract: frame store shape does not match the image / channels");
+        const float* dimg = memspace == PVO_DEVICE ? image : upload(ctx, ctx->s0, image, (size_t)iw * ih);
+        float* scratch = ctx->s1.as<float>(pvo_dev::extract_scratch_floats(iw, ih, base_channels));
+        const size_t c0 = (size_t)ctx->w0 * ctx->h0, c1 = (size_t)ctx->w1 * ctx->h1;
+        float* f0 = static_cast<float*>(ctx->feat0.p) + (size_t)slot * c0 * ctx->C;
+        float* f1 = static_cast<float*>(ctx->feat1.p) + (size_t)slot * c1 * ctx->C;
+        cuda_check(pvo_dev::launch_extract_features(dimg, iw, ih, base_channels, scratch, f0, f1, ctx->stream),
+                   "feature extraction");
+        ctx->launches += base_channels == 3 ? 8 : 7;
+        float* g0 = static_cast<float*>(ctx->gram0.p) + (size_t)slot * pvo_dev::gram_stride(ctx->w0) * ctx->h0 * 8;
+        float* g1 = static_cast<float*>(ctx->gram1.p) + (size_t)slot * pvo_dev::gram_stride(ctx->w1) * ctx->h1 * 8;
+        compute_gram(ctx, f0, g0, f1, g1, ctx->w0, ctx->h0, ctx->w1, ctx->h1, ctx->C);
+        if (memspace != PVO_DEVICE) sync(ctx);
+    });
+}
+
+// A slot's pyramid back to the host (level0 [H0][W0][C], level1 [H1][W1][C]).
+int pvo_frames_download(pvo_ctx* ctx, int slot, float* level0, float* level1) {
+    return guarded([&] {
+        bind(ctx);
+        if (slot < 0 || slot >= ctx->nf) fail(PVO_OUT_OF_RANGE, "frames: slot out of range");
+        const size_t c0 = (size_t)ctx->w0 * ctx->h0 * ctx->C, c1 = (size_t)ctx->w1 * ctx->h1 * ctx->C;
+        if (level0) download(ctx, level0, static_cast<const float*>(ctx->feat0.p) + (size_t)slot * c0, c0);
+        if (level1) download(ctx, level1, static_cast<const float*>(ctx->feat1.p) + (size_t)slot * c1, c1);
+        sync(ctx);
+    });
+}
+
+// crop_patch_features (features.cpp:204-224) of n patches from frame-store slot
+// `slot`: centroids [n][2] -> the 3x3 grid (Patch::make) -> out [n][2][9][C].
+int pvo_crop_patches(pvo_ctx* ctx, int slot, int n, const double* centroids, float* out, int memspace) {
+    return guarded([&] {
+        bind(ctx);
+        if (slot < 0 || slot >= ctx->nf) fail(PVO_OUT_OF_RANGE, "frames: slot out of range");
+        if (n <= 0) return;
+        std::vector<double> px(9 * (size_t)n), py(9 * (size_t)n);
+        for (int k = 0; k < n; ++k)
+            for (int row = 0; row < 3; ++row)
+                for (int col = 0; col < 3; ++col) {
+                    px[9 * (size_t)k + 3 * row + col] = centroids[2 * k] + col - 1.0;
+                    py[9 * (size_t)k + 3 * row + col] = centroids[2 * k + 1] + row - 1.0;
+                }
+        const double* dx = upload(ctx, ctx->s2, px.data(), px.size());
+        const double* dy = upload(ctx, ctx->s3, py.data(), py.size());
+        const size_t c0 = (size_t)ctx->w0 * ctx->h0, c1 = (size_t)ctx->w1 * ctx->h1;
+        const float* f0 = static_cast<const float*>(ctx->feat0.p) + (size_t)slot * c0 * ctx->C;
+        const float* f1 = static_cast<const float*>(ctx->feat1.p) + (size_t)slot * c1 * ctx->C;
+        const size_t total = (size_t)n * 2 * 9 * ctx->C;
+        float* dout = memspace == PVO_DEVICE ? out : ctx->s4.as<float>(total);
+        cuda_check(pvo_dev::launch_crop_patches(n, dx, dy, f0, ctx->w0, ctx->h0, f1, ctx->w1, ctx->h1, ctx->C, dout,
+                                                ctx->stream),
+                   "crop");
+        ctx->launches += 1;
+        if (memspace != PVO_DEVICE) download(ctx, out, dout, total);
+        sync(ctx);
+    });
+}
+
 // ---- flow-provider measurement (flow_provider.cpp:150-312) -------------------
 int pvo_measure_batch(pvo_ctx* ctx, int n_edges, int n_patches, int p, const int* e_patch, const int* e_slot,
                       const double* centers, const uint8_t* behind, const float* patch_feats, double* delta,

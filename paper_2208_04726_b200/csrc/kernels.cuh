@@ -172,6 +172,13 @@ cudaError_t dg_writeback(const DGraphView& g, int n_poses, const int* pose_frame
                          const double* poses, int n_patches, const int* patch_ids, const double* depth,
                          cudaStream_t s);
 
+// Feature pyramid extraction + patch crop (features.cu; features.cpp:55-235).
+cudaError_t launch_extract_features(const float* image, int iw, int ih, int base_channels, float* scratch,
+                                    float* level0, float* level1, cudaStream_t s);
+size_t extract_scratch_floats(int iw, int ih, int base_channels);
+cudaError_t launch_crop_patches(int n, const double* px, const double* py, const float* l0, int w0, int h0,
+                                const float* l1, int w1, int h1, int C, float* out, cudaStream_t s);
+
 // Device status word values (ba.cu / corr.cu) -> pvo_status on the host.
 enum DevStatus : int {
     kDevOk = 0,

@@ -760,3 +760,31 @@ def test_device_graph_keyframe_matches_pipeline_rule(ctx):
         dk, dj, _, _ = dev.edges()
         assert np.array_equal(hk, dk) and np.array_equal(hj, dj)
     assert removed_any >= 2
+
+
+@pytest.mark.parametrize("bc", [1, 3])
+def test_feature_extraction_matches_oracle(ctx, bc):
+    """extract_features + crop_patch_features (features.cpp:55-235) on the device:
+    bit-identical to the CPU restatement (both round like the reference)."""
+    from tests.test_oracle_pins import _smooth_image
+
+    rng = np.random.default_rng(40 + bc)
+    img = _smooth_image(rng, 480, 640)
+    C = 25 * bc
+    ctx.frames_reserve(2, 160, 120, 40, 30, C)
+    ctx.frames_extract(1, img, base_channels=bc)
+    l0, l1 = ctx.frames_download(1)
+    r0, r1 = orc.extract_features(img, base_channels=bc)
+    assert np.array_equal(l0, r0) and np.array_equal(l1, r1)
+    cents = np.stack([rng.uniform(3, 636, 40), rng.uniform(3, 476, 40)], 1)
+    got = ctx.crop_patches(1, cents)
+    gx, gy = np.meshgrid(np.arange(3) - 1.0, np.arange(3) - 1.0)
+    ref = orc.crop_patches(cents[:, :1] + gx.ravel()[None], cents[:, 1:] + gy.ravel()[None], r0, r1)
+    assert np.array_equal(got, ref)
+    # the 25-d pyramid feeds the generic correlation path: self-match peaks at the centre
+    if bc == 1:
+        coords = np.stack([cents[:8, :1] + gx.ravel()[None], cents[:8, 1:] + gy.ravel()[None]], -1)
+        out = pvo.correlate_batch(np.arange(8), np.ones(8, np.int32), coords, got[:8], ctx=ctx)
+        ref_c = orc.correlate_batch(np.arange(8), np.ones(8, np.int32), coords, got[:8],
+                                    np.stack([r0, r0]), np.stack([r1, r1]))
+        assert corr_violations(out, ref_c, _gnorm_for_batch(got[:8], np.arange(8))) == 0

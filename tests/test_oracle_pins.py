@@ -600,3 +600,67 @@ def test_measure_behind_camera_default_revision():  # flow_provider.cpp:301-302
     d, w, fl = orc.measure_batch([0], [0], np.zeros((1, 2)), np.array([1], np.uint8),
                                  np.ones((1, 2, 9, 4), np.float32), l0[None], _level1(l0)[None])
     assert fl[0] == 4 and np.allclose(d, 0) and np.allclose(w, 0.01)
+
+
+# ---------------------------------------------------------------- feature extraction
+# extract_features / whiten / lift / crop (features.cpp:55-235), SURVEY.md §8f row 2;
+# ported from test_features.cpp:38-142 on smooth random images.
+def _smooth_image(rng, h, w, blur=4):
+    img = rng.standard_normal((h + 2 * blur, w + 2 * blur))
+    k = np.exp(-0.5 * (np.arange(-2 * blur, 2 * blur + 1) / blur) ** 2)
+    k /= k.sum()
+    img = np.apply_along_axis(lambda r: np.convolve(r, k, "same"), 1, img)
+    img = np.apply_along_axis(lambda c: np.convolve(c, k, "same"), 0, img)
+    return img[blur:-blur, blur:-blur].astype(np.float32)
+
+
+def test_constant_image_gives_zero_features():  # test_features.cpp:38-44
+    l0, l1 = orc.extract_features(np.full((64, 64), 0.37, np.float32))
+    assert l0.shape == (16, 16, 25) and l1.shape == (4, 4, 25)
+    assert np.abs(l0).max() == 0 and np.abs(l1).max() == 0
+
+
+def test_levels_pool_and_unit_descriptors():  # test_features.cpp:46-87, :126-142
+    l0, l1 = orc.extract_features(_smooth_image(np.random.default_rng(5), 128, 128))
+    assert l0.shape == (32, 32, 25) and l1.shape == (8, 8, 25)
+    n0 = (l0.astype(np.float64) ** 2).sum(-1)
+    n1 = (l1.astype(np.float64) ** 2).sum(-1)
+    assert np.allclose(n0, 1.0, atol=1e-5) and np.allclose(n1, 1.0, atol=1e-5)
+
+
+def test_level0_correlation_peaks_at_integer_shift():  # test_features.cpp:89-116
+    rng = np.random.default_rng(9)
+    big = _smooth_image(rng, 176, 176)
+    a = np.ascontiguousarray(big[8:168, 8:168])
+    sx, sy = 2, -1  # whole level-0 cells (4 px)
+    b = np.ascontiguousarray(big[8 - 4 * sy:168 - 4 * sy, 8 - 4 * sx:168 - 4 * sx])
+    fa, _ = orc.extract_features(a)
+    fb, _ = orc.extract_features(b)
+    best, arg = -1e30, None
+    for dy in range(-4, 5):
+        for dx in range(-4, 5):
+            dot = (fa[8:-8, 8:-8, 12].astype(np.float64) * fb[8 + dy:fb.shape[0] - 8 + dy, 8 + dx:fb.shape[1] - 8 + dx, 12]).sum()
+            if dot > best:
+                best, arg = dot, (dx, dy)
+    assert arg == (sx, sy)
+
+
+def test_gradient_channels_appended():  # test_features.cpp:118-124
+    l0, _ = orc.extract_features(_smooth_image(np.random.default_rng(11), 96, 96), base_channels=3)
+    assert l0.shape[2] == 75
+    d = l0[5, 5].reshape(5, 5, 3)  # (dy, dx, c) stacking, one normalisation per descriptor
+    assert np.isclose(d[2, 2, 1], 0.5 * (d[2, 3, 0] - d[2, 1, 0]), atol=1e-6)
+
+
+def test_crop_matches_sampler_definition():  # features.cpp:204-224 with sample_cubic (:23-52)
+    rng = np.random.default_rng(12)
+    l0, l1 = orc.extract_features(_smooth_image(rng, 96, 96))
+    cents = np.array([[30.3, 41.7], [50.0, 20.25]])
+    gx, gy = np.meshgrid(np.arange(3) - 1.0, np.arange(3) - 1.0)
+    px = cents[:, :1] + gx.ravel()[None]
+    py = cents[:, 1:] + gy.ravel()[None]
+    out = orc.crop_patches(px, py, l0, l1)
+    from paper_2208_04726_b200 import synth
+
+    ref0 = synth.crop_cubic(l0, px[1] / 4.0, py[1] / 4.0)
+    assert np.allclose(out[1, 0], ref0, atol=1e-6)

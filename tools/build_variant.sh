@@ -3,8 +3,8 @@
 set -e
 name=$1; shift
 out=build/variants/$name; mkdir -p $out
-for s in corr corr_tma ba ba_large measure capi; do
-  extra=""; [ $s = measure ] && extra="--fmad=false"
+for s in corr corr_tma ba ba_large measure dgraph features capi; do
+  extra=""; { [ $s = measure ] || [ $s = features ]; } && extra="--fmad=false"
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo --expt-relaxed-constexpr -Xcompiler -fPIC -I include $extra "$@" -c paper_2208_04726_b200/csrc/$s.cu -o $out/$s.o &
 done
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC -I include -c paper_2208_04726_b200/csrc/graph.cpp -o $out/graph.o &
