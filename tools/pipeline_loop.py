@@ -3,9 +3,12 @@ new frame pyramid -> device graph (add frame / patches, connect) -> on-device
 window flatten -> propose (flow-provider measurement at the current state) ->
 revisions into the graph -> optimize_window (2 GN iterations) -> write-back.
 
-usage: python tools/pipeline_loop.py [frames=30] [config=c2]
+usage: python tools/pipeline_loop.py [frames=30] [config=c2] [images]
 Prints the mean per-frame device time of each stage over the second half of
-the sequence (CUDA events on the context stream) and the host wall time."""
+the sequence (CUDA events on the context stream) and the host wall time.
+With "images" the frames arrive as 480x640 images and the reference's own
+extractor runs on the device (features.cu: 25-d descriptors, patches cropped
+from the new pyramid) — image in, poses out, only the image crossing PCIe."""
 import sys
 import time
 from pathlib import Path
@@ -19,19 +22,28 @@ from paper_2208_04726_b200 import synth  # noqa: E402
 
 n_frames = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 cfg = sys.argv[2] if len(sys.argv) > 2 else "c2"
-w = synth.generate(cfg, seed=5, frames=n_frames)
+images = len(sys.argv) > 3 and sys.argv[3] == "images"
+w = synth.generate(cfg, seed=5, frames=n_frames, features=not images)
 F, M = w.cfg["frames"], w.cfg["patches"]
-_, H0, W0, D = w.level0.shape
-_, H1, W1, _ = w.level1.shape
+if images:  # smooth random images; the device extracts the 25-d reference pyramid
+    rng = np.random.default_rng(1)
+    from tests.test_oracle_pins import _smooth_image
+
+    imgs = [torch.from_numpy(_smooth_image(rng, w.image[1], w.image[0])).pin_memory() for _ in range(F)]
+    W0, H0, W1, H1, D = w.image[0] // 4, w.image[1] // 4, w.image[0] // 16, w.image[1] // 16, 25
+else:
+    _, H0, W0, D = w.level0.shape
+    _, H1, W1, _ = w.level1.shape
 ctx = pvo.Context(0)
 stream = torch.cuda.Stream()
 ctx.set_stream(stream.cuda_stream)
 NS = 32  # frame-store ring: the window plus every frame its edges still reach
 ctx.frames_reserve(NS, W0, H0, W1, H1, D)
 dev = pvo.DeviceGraph(ctx, w.K, w.image[0], w.image[1], channels=D)
-l0 = [torch.from_numpy(w.level0[f]).pin_memory() for f in range(F)]
-l1 = [torch.from_numpy(w.level1[f]).pin_memory() for f in range(F)]
-stages = ["frame H2D + Gram", "graph add + connect", "flatten", "propose", "BA (2 it.)", "store"]
+if not images:
+    l0 = [torch.from_numpy(w.level0[f]).pin_memory() for f in range(F)]
+    l1 = [torch.from_numpy(w.level1[f]).pin_memory() for f in range(F)]
+stages = ["frame (H2D/extract+Gram)", "graph add + connect", "flatten", "propose", "BA (2 it.)", "store"]
 acc = {s: [] for s in stages}
 walls, edges = [], []
 with torch.cuda.stream(stream):
@@ -40,11 +52,16 @@ with torch.cuda.stream(stream):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         ev[0].record(stream)
-        ctx.frames_upload(f % NS, l0[f].numpy(), l1[f].numpy())
+        ks = slice(f * M, (f + 1) * M)
+        if images:
+            ctx.frames_extract(f % NS, imgs[f].numpy(), base_channels=1)
+            feats = ctx.crop_patches(f % NS, w.centroids[ks])
+        else:
+            ctx.frames_upload(f % NS, l0[f].numpy(), l1[f].numpy())
+            feats = w.patch_feats[ks]
         ev[1].record(stream)
         idx = dev.add_frame(0.05 * (f + 1), w.poses[f], frame_slot=f % NS)
-        ks = slice(f * M, (f + 1) * M)
-        dev.add_patches(idx, w.centroids[ks], w.depth[ks], w.patch_feats[ks])
+        dev.add_patches(idx, w.centroids[ks], w.depth[ks], feats)
         dev.connect(w.cfg["radius"])
         ev[2].record(stream)
         # every active edge (pipeline.cpp:164-181); after propose all of them are revised,
@@ -63,7 +80,8 @@ with torch.cuda.stream(stream):
         if f >= F // 2:
             for i, s in enumerate(stages):
                 acc[s].append(ev[i].elapsed_time(ev[i + 1]))
-print(f"{cfg}: {F} frames, {M} patches/frame, window {w.cfg['window']}, radius {w.cfg['radius']}; "
+print(f"{cfg}{' (images, 25-d device features)' if images else ''}: {F} frames, {M} patches/frame, "
+      f"window {w.cfg['window']}, radius {w.cfg['radius']}; "
       f"active edges at the end {edges[-1]}")
 tot = 0.0
 for s in stages:
