@@ -132,10 +132,20 @@ PVO_HD SE3 se3_exp(const double xi[6]) {
         b = 1.0 / 6.0;
     } else {
         const double half = 0.5 * theta;
-        const double s = sin(half) / theta;
-        q = {s * ox, s * oy, s * oz, cos(half)};
-        a = (1.0 - cos(theta)) / theta2;
-        b = (theta - sin(theta)) / (theta2 * theta);
+        double sh, ch, st, ct;
+#if defined(__CUDA_ARCH__)
+        sincos(half, &sh, &ch);  // one argument reduction per angle (same values as sin / cos)
+        sincos(theta, &st, &ct);
+#else
+        sh = sin(half);
+        ch = cos(half);
+        st = sin(theta);
+        ct = cos(theta);
+#endif
+        const double s = sh / theta;
+        q = {s * ox, s * oy, s * oz, ch};
+        a = (1.0 - ct) / theta2;
+        b = (theta - st) / (theta2 * theta);
     }
     // W = skew(omega); W^2 entries
     const double w[9] = {0, -oz, oy, oz, 0, -ox, -oy, ox, 0};
