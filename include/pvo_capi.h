@@ -241,6 +241,17 @@ int pvo_window_problem_read(pvo_ctx* ctx, double* poses, uint8_t* fixed, int* po
                             double* py, double* inv_depth, int* e_patch, int* e_pose, double* e_delta,
                             double* e_weight);
 
+/* ---- simulator oracle provider (flow_provider.cpp:34-93)
+ * pvo_window_oracle_propose: revisions for every edge of the resident window
+ * from the scene's ground truth (gt_poses [N][7] per window pose slot,
+ * gt_inv_depth [P] per window patch), Gaussian noise and an exact outlier
+ * fraction, drawn from a context-owned mt19937_64 (pvo_oracle_seed) in the
+ * reference's order; they replace the window's deltas / weights.  Outputs may
+ * be NULL.                                                                   */
+int pvo_oracle_seed(pvo_ctx* ctx, uint64_t seed);
+int pvo_window_oracle_propose(pvo_ctx* ctx, const double* gt_poses, const double* gt_inv_depth, double flow_sigma,
+                              double outlier_fraction, double* delta, double* weight);
+
 /* ---- batch of independent windows (config 5: sequences sharded per device) -
  * Windows are concatenated: pose/patch/edge offsets [n_windows + 1] (starting
  * at 0); inside a window every index is window-local (as pvo_window_load);

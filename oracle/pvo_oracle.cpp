@@ -15,6 +15,7 @@
 //   correlation.cpp:8-71      correlate_at, correlate
 //   features.cpp:55-235      feature pyramid extraction (pool, whiten, lift) and
 //                             crop_patch_features
+//   flow_provider.cpp:34-93   OracleFlowProvider::propose (simulator revisions)
 //   flow_provider.cpp:150-287 CorrelationFlowProvider::measure (parabola_refine,
 //                             subpixel_peak) and propose's per-edge part (:289-314)
 //   patch_graph.cpp:27-173    PatchGraph (std::map keyed, same iteration order)
@@ -44,6 +45,7 @@
 #include <limits>
 #include <map>
 #include <optional>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -1495,6 +1497,77 @@ int orc_measure_batch(int n_edges, const int* e_patch, const int* e_frame, const
         for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
         work(0);
         for (auto& th : pool) th.join();
+    });
+}
+
+// ---- OracleFlowProvider::propose (flow_provider.cpp:34-93) on a flattened window ----
+// gt_poses [N][7] (scene poses of the window's pose slots), gt_d [P] (scene inverse
+// depth at each patch centre, flow_provider.cpp:24), the RNG a mt19937_64 seeded
+// once per call.  Out: delta [E][2], weight [E][2].
+namespace {
+struct OracleV2 {  // two-argument construction: the same argument evaluation order as Vec2(a(), b())
+    double x, y;
+    OracleV2(double a, double b) : x(a), y(b) {}
+};
+}  // namespace
+int orc_oracle_propose(int n_poses, const double* poses, const double* gt_poses, int n_patches, const int* src,
+                       const double* px, const double* py, const double* depth, const double* gt_d, int n_edges,
+                       const int* e_patch, const int* e_pose, const double* K, double flow_sigma,
+                       double outlier_fraction, uint64_t seed, double* delta, double* weight) {
+    return guard([&] {
+        (void)n_poses;
+        (void)n_patches;
+        const Intrinsics Kc = load_K(K);
+        std::mt19937_64 rng(seed);
+        std::normal_distribution<double> gauss(0.0, flow_sigma);
+        std::uniform_real_distribution<double> uniform(-32.0, 32.0);
+        const double sigma2 = flow_sigma * flow_sigma;
+        const double w = std::clamp(1.0 / (1.0 + sigma2), 0.01, 0.99);
+        constexpr double kMaxRevisionPx = 64.0;  // flow_provider.hpp:47
+        for (int e = 0; e < n_edges; ++e) {
+            const int k = e_patch[e], i = src[k], j = e_pose[e];
+            Patch cur;
+            cur.x.assign(px + 9 * (size_t)k, px + 9 * (size_t)k + 9);
+            cur.y.assign(py + 9 * (size_t)k, py + 9 * (size_t)k + 9);
+            cur.width = 3;
+            cur.inverse_depth = depth[k];
+            // ground-truth reprojection of the patch centre (flow_provider.cpp:52-55)
+            const Patch probe = make_patch(0, cur.center(), 1, gt_d[k]);
+            const PatchReprojection gt =
+                reproject_patch(load_pose(gt_poses + 7 * i), load_pose(gt_poses + 7 * j), Kc, probe);
+            const PatchReprojection now = reproject_patch(load_pose(poses + 7 * i), load_pose(poses + 7 * j), Kc, cur);
+            double dx = 0, dy = 0, wx = 0.01, wy = 0.01;
+            if (!(gt.behind_camera || now.behind_camera)) {
+                dx = gt.points[0].x - now.points[4].x;
+                dy = gt.points[0].y - now.points[4].y;
+                if (flow_sigma > 0) {
+                    const OracleV2 n(gauss(rng), gauss(rng));
+                    dx += n.x;
+                    dy += n.y;
+                }
+                const bool in_range = std::abs(dx) <= kMaxRevisionPx && std::abs(dy) <= kMaxRevisionPx;
+                dx = std::clamp(dx, -kMaxRevisionPx, kMaxRevisionPx);
+                dy = std::clamp(dy, -kMaxRevisionPx, kMaxRevisionPx);
+                wx = wy = in_range ? w : 0.01;
+            }
+            delta[2 * e] = dx;
+            delta[2 * e + 1] = dy;
+            weight[2 * e] = wx;
+            weight[2 * e + 1] = wy;
+        }
+        const size_t num_outliers = static_cast<size_t>(outlier_fraction * static_cast<double>(n_edges));
+        if (num_outliers > 0) {
+            std::vector<size_t> index(n_edges);
+            for (size_t i = 0; i < index.size(); ++i) index[i] = i;
+            std::shuffle(index.begin(), index.end(), rng);
+            for (size_t i = 0; i < num_outliers; ++i) {
+                const OracleV2 u(uniform(rng), uniform(rng));
+                delta[2 * index[i]] = u.x;
+                delta[2 * index[i] + 1] = u.y;
+                weight[2 * index[i]] = 0.01;
+                weight[2 * index[i] + 1] = 0.01;
+            }
+        }
     });
 }
 

@@ -392,3 +392,15 @@ def crop_patches(px, py, level0, level1):
     check(lib.orc_crop_patches(I(x.shape[0]), _p(x), _p(y), _p(l0), I(l0.shape[1]), I(l0.shape[0]), _p(l1),
                                I(l1.shape[1]), I(l1.shape[0]), I(C), _p(out)))
     return out
+
+
+def oracle_propose(pr, gt_poses, gt_d, K, flow_sigma=0.0, outlier_fraction=0.0, seed=0):
+    """OracleFlowProvider::propose (flow_provider.cpp:34-93) on a flattened window:
+    -> delta [E, 2], weight [E, 2] (one mt19937_64 seeded per call)."""
+    poses, fixed, src, px, py, d, ep, eo, et, ew = _prob_args(pr)
+    E = len(ep)
+    dl, wt = np.empty((E, 2)), np.empty((E, 2))
+    check(lib.orc_oracle_propose(I(len(poses)), _p(poses), _p(_f64(gt_poses)), I(len(d)), _p(src), _p(px), _p(py),
+                                 _p(d), _p(_f64(gt_d)), I(E), _p(ep), _p(eo), _p(_f64(K, (4,))), D(flow_sigma),
+                                 D(outlier_fraction), C.c_uint64(seed), _p(dl), _p(wt)))
+    return dl, wt

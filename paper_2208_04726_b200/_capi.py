@@ -84,6 +84,8 @@ SIGNATURES = {
     "pvo_window_load_dgraph": (i32, [vp, vp, i32, i32, P, P, P]),
     "pvo_dgraph_store_window": (i32, [vp, vp, i32, i32]),
     "pvo_window_problem_read": (i32, [vp, P, P, P, P, P, P, P, P, P, P, P]),
+    "pvo_oracle_seed": (i32, [vp, C.c_uint64]),
+    "pvo_window_oracle_propose": (i32, [vp, P, P, f64, f64, P, P]),
     "pvo_batch_load": (i32, [vp, i32, P, P, P, P, P, P, i32, P, P, P, P, P, P, P, P, P, P, i32, i32]),
     "pvo_batch_reset": (i32, [vp]),
     "pvo_batch_iteration": (i32, [vp, i32, f64, P, i32]),

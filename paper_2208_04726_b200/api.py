@@ -684,6 +684,19 @@ class Window:
         check(lib.pvo_window_propose(self.ctx.handle, _ptr(d), _ptr(w), _ptr(fl)))
         return d, w, fl
 
+    def oracle_propose(self, gt_poses, gt_inv_depth, flow_sigma: float = 0.0, outlier_fraction: float = 0.0,
+                       seed=None):
+        """OracleFlowProvider::propose (flow_provider.cpp:34-93) over the window's edges;
+        the revisions become the window's deltas / weights.  seed re-seeds the
+        context's provider RNG first (else the stream continues)."""
+        if seed is not None:
+            check(lib.pvo_oracle_seed(self.ctx.handle, int(seed)))
+        d, w = np.empty((self.n_edges, 2)), np.empty((self.n_edges, 2))
+        check(lib.pvo_window_oracle_propose(self.ctx.handle, _ptr(_f64(gt_poses).reshape(-1, 7)),
+                                            _ptr(_f64(gt_inv_depth)), float(flow_sigma), float(outlier_fraction),
+                                            _ptr(d), _ptr(w)))
+        return d, w
+
     def corr_device_ptr(self) -> int:
         p = C.c_void_p()
         check(lib.pvo_window_corr_ptr(self.ctx.handle, C.addressof(p)))

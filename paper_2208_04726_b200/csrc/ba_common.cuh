@@ -41,6 +41,22 @@ __device__ inline void reproject_center(const SE3& pi, const SE3& pj, const Cam&
     *behind = b;
 }
 
+// reproject_patch of a 1x1 patch at (cx, cy) with inverse depth d (the oracle
+// provider's probe, flow_provider.cpp:52-55): the bitwise-equal shortcut, else
+// the pixel's reprojection and its own behind flag
+__device__ inline void reproject_center_probe(const SE3& pi, const SE3& pj, const Cam& K, double cx, double cy,
+                                              double d, double* cu, double* cv, bool* behind) {
+    if (se3_equal(pi, pj)) {
+        *cu = cx;
+        *cv = cy;
+        *behind = false;
+        return;
+    }
+    const Relative rel = relative_pose(pi, pj);
+    const double qz = reproject_point(rel, K, d, cx, cy, cu, cv);
+    *behind = qz <= kDepthEpsilon;
+}
+
 // Per-pose rotation matrix + translation, so that a relative pose is a 3x3
 // product instead of two quaternion normalisations per edge:
 //   T_j T_i^-1 = (R_j R_i^T, t_j - R_j R_i^T t_i)   (camera.cpp:59-61)

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -174,7 +175,8 @@ struct pvo_ctx {
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_corr = nullptr, ev_copy = nullptr;
     bool timing_pending = false;
-    bool tracing = false;  // record BA phase clocks (pvo_ctx_set_tracing)
+    bool tracing = false;
+    std::mt19937_64 oracle_rng{0};  // the oracle provider's RNG (flow_provider.cpp:10, rng_(noise.seed))  // record BA phase clocks (pvo_ctx_set_tracing)
 };
 
 namespace {
@@ -1403,6 +1405,92 @@ int pvo_window_propose(pvo_ctx* ctx, double* delta_out, double* weight_out, uint
         if (weight_out) download(ctx, weight_out, m.weight, (size_t)w.n_edges * 2);
         if (flags_out) download(ctx, flags_out, m.flags, w.n_edges);
         if (delta_out || weight_out || flags_out) sync(ctx);
+    });
+}
+
+// ---- OracleFlowProvider::propose (flow_provider.cpp:34-93) ---------------------
+namespace {
+struct V2Args {  // built as V2Args(a(), b()): the reference's Vec2(gauss(rng_), gauss(rng_)) evaluation order
+    double x, y;
+    V2Args(double a, double b) : x(a), y(b) {}
+};
+}  // namespace
+
+int pvo_oracle_seed(pvo_ctx* ctx, uint64_t seed) {
+    return guarded([&] { ctx->oracle_rng.seed(seed); });
+}
+
+// Simulator revisions for every edge of the resident window: ground truth
+// (scene poses of the window's pose slots gt_poses [N][7], scene inverse depth
+// gt_inv_depth [P]) minus the current reprojection, + N(0, sigma^2) noise,
+// clamped to +-64 px, exactly floor(fraction * E) uniform outliers — the RNG
+// stream is the reference's (a context-owned mt19937_64 that persists across
+// calls, like the provider's member; the draws are consumed on the host in
+// the reference's order between two device passes).  The revisions replace
+// the window's deltas / weights (as pvo_window_propose).
+int pvo_window_oracle_propose(pvo_ctx* ctx, const double* gt_poses, const double* gt_inv_depth, double flow_sigma,
+                              double outlier_fraction, double* delta_out, double* weight_out) {
+    return guarded([&] {
+        bind(ctx);
+        Window& w = ctx->win;
+        if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
+        BABuffers& B = ctx->ba;
+        const int E = w.n_edges;
+        pvo_dev::OracleParams o;
+        o.n_edges = E;
+        o.e_patch = static_cast<const int*>(B.e_patch.p);
+        o.e_pose = static_cast<const int*>(B.e_pose.p);
+        o.patch_src = static_cast<const int*>(B.patch_src.p);
+        o.patch_x = static_cast<const double*>(B.px.p);
+        o.patch_y = static_cast<const double*>(B.py.p);
+        o.depth = static_cast<const double*>(B.depth.p);
+        o.poses = static_cast<const double*>(B.poses.p);
+        o.K = static_cast<const double*>(B.K.p);
+        o.gt_poses = upload(ctx, ctx->s0, gt_poses, 7 * (size_t)w.n_poses);
+        o.gt_depth = upload(ctx, ctx->s1, gt_inv_depth, w.n_patches);
+        o.flow_sigma = flow_sigma;
+        o.weight_in_range = std::clamp(1.0 / (1.0 + flow_sigma * flow_sigma), 0.01, 0.99);
+        o.behind = ctx->s5.as<uint8_t>(std::max(E, 1));
+        o.delta = static_cast<double*>(B.e_in.p);
+        o.weight = static_cast<double*>(B.e_w.p);
+        cuda_check(pvo_dev::launch_oracle_propose(o, 0, ctx->stream), "oracle propose");
+        std::vector<uint8_t> behind(E);
+        download(ctx, behind.data(), o.behind, E);
+        sync(ctx);
+        // host: the RNG stream in the reference's order
+        std::normal_distribution<double> gauss(0.0, flow_sigma);
+        std::uniform_real_distribution<double> uniform(-32.0, 32.0);
+        std::vector<double> noise(2 * (size_t)E, 0.0), odelta;
+        std::vector<uint8_t> omask;
+        if (flow_sigma > 0)
+            for (int e = 0; e < E; ++e)
+                if (!behind[e]) {
+                    const V2Args n(gauss(ctx->oracle_rng), gauss(ctx->oracle_rng));
+                    noise[2 * e] = n.x;
+                    noise[2 * e + 1] = n.y;
+                }
+        const size_t num_outliers = static_cast<size_t>(outlier_fraction * static_cast<double>(E));
+        if (num_outliers > 0) {
+            std::vector<size_t> index(E);
+            for (size_t i = 0; i < index.size(); ++i) index[i] = i;
+            std::shuffle(index.begin(), index.end(), ctx->oracle_rng);
+            omask.assign(E, 0);
+            odelta.assign(2 * (size_t)E, 0.0);
+            for (size_t i = 0; i < num_outliers; ++i) {
+                const V2Args u(uniform(ctx->oracle_rng), uniform(ctx->oracle_rng));
+                omask[index[i]] = 1;
+                odelta[2 * index[i]] = u.x;
+                odelta[2 * index[i] + 1] = u.y;
+            }
+            o.outlier = upload(ctx, ctx->s6, omask.data(), omask.size());
+            o.outlier_delta = upload(ctx, ctx->s7, odelta.data(), odelta.size());
+        }
+        if (flow_sigma > 0) o.noise = upload(ctx, ctx->s8, noise.data(), noise.size());
+        cuda_check(pvo_dev::launch_oracle_propose(o, 1, ctx->stream), "oracle propose");
+        ctx->launches += 2;
+        if (delta_out) download(ctx, delta_out, o.delta, 2 * (size_t)E);
+        if (weight_out) download(ctx, weight_out, o.weight, 2 * (size_t)E);
+        sync(ctx);
     });
 }
 

@@ -107,6 +107,30 @@ struct MeasureParams {
 };
 cudaError_t launch_measure(const MeasureParams& p, cudaStream_t stream);
 
+// OracleFlowProvider::propose on the resident window (measure.cu): two passes
+// around the host-side RNG draws (the reference's sequential mt19937_64 stream).
+struct OracleParams {
+    int n_edges = 0;
+    const int* e_patch = nullptr;
+    const int* e_pose = nullptr;
+    const int* patch_src = nullptr;
+    const double* patch_x = nullptr;
+    const double* patch_y = nullptr;
+    const double* depth = nullptr;
+    const double* poses = nullptr;
+    const double* gt_poses = nullptr;   // [N][7] scene poses of the window's pose slots
+    const double* gt_depth = nullptr;   // [P] scene inverse depth at each patch centre
+    const double* K = nullptr;
+    double flow_sigma = 0.0, weight_in_range = 0.99;
+    const double* noise = nullptr;      // [E][2] gauss draws (non-behind edges), pass 1
+    const uint8_t* outlier = nullptr;   // [E] or null
+    const double* outlier_delta = nullptr;
+    uint8_t* behind = nullptr;          // [E] pass 0 output
+    double* delta = nullptr;            // [E][2]
+    double* weight = nullptr;           // [E][2]
+};
+cudaError_t launch_oracle_propose(const OracleParams& p, int pass, cudaStream_t stream);
+
 // Device-resident patch graph (dgraph.cu): SoA views.
 struct DGraphView {
     int F = 0, P = 0;

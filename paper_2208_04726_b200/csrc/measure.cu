@@ -301,7 +301,61 @@ __global__ void __launch_bounds__(256, PVO_MEASURE_MINB) measure_kernel(MeasureP
     }
 }
 
+// ---- OracleFlowProvider::propose (flow_provider.cpp:34-93), simulator revisions ----
+// pass 0: ground-truth reprojection of each edge's patch centre (a 1x1 probe at
+// the centre with the scene inverse depth, between the scene poses) and the
+// current-state centre; behind flag of either.  pass 1: noise, clamp, weights.
+__global__ void oracle_propose_kernel(OracleParams a, int pass) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= a.n_edges) return;
+    if (pass == 0) {
+        const int k = a.e_patch[e], i = a.patch_src[k], j = a.e_pose[e];
+        const Cam K{a.K[0], a.K[1], a.K[2], a.K[3]};
+        const double cxp = a.patch_x[9 * (size_t)k + 4], cyp = a.patch_y[9 * (size_t)k + 4];
+        const SE3 gi = se3_load(a.gt_poses + 7 * i), gj = se3_load(a.gt_poses + 7 * j);
+        double gu, gv;
+        bool gb;
+        reproject_center_probe(gi, gj, K, cxp, cyp, a.gt_depth[k], &gu, &gv, &gb);
+        double cu, cv;
+        bool cb;
+        reproject_center(se3_load(a.poses + 7 * i), se3_load(a.poses + 7 * j), K, a.patch_x + 9 * (size_t)k,
+                         a.patch_y + 9 * (size_t)k, a.depth[k], &cu, &cv, &cb);
+        a.behind[e] = gb || cb;
+        a.delta[2 * e] = gu - cu;
+        a.delta[2 * e + 1] = gv - cv;
+        return;
+    }
+    double dx = 0, dy = 0, w = 0.01;
+    if (!a.behind[e]) {
+        dx = a.delta[2 * e];
+        dy = a.delta[2 * e + 1];
+        if (a.flow_sigma > 0) {
+            dx += a.noise[2 * e];
+            dy += a.noise[2 * e + 1];
+        }
+        const bool in_range = fabs(dx) <= 64.0 && fabs(dy) <= 64.0;  // kMaxRevisionPx (flow_provider.hpp:47)
+        dx = fmin(fmax(dx, -64.0), 64.0);
+        dy = fmin(fmax(dy, -64.0), 64.0);
+        w = in_range ? a.weight_in_range : 0.01;
+    }
+    if (a.outlier && a.outlier[e]) {
+        dx = a.outlier_delta[2 * e];
+        dy = a.outlier_delta[2 * e + 1];
+        w = 0.01;
+    }
+    a.delta[2 * e] = dx;
+    a.delta[2 * e + 1] = dy;
+    a.weight[2 * e] = w;
+    a.weight[2 * e + 1] = w;
+}
+
 }  // namespace
+
+cudaError_t launch_oracle_propose(const OracleParams& p, int pass, cudaStream_t stream) {
+    if (p.n_edges <= 0) return cudaSuccess;
+    oracle_propose_kernel<<<(p.n_edges + 127) / 128, 128, 0, stream>>>(p, pass);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_measure(const MeasureParams& p, cudaStream_t stream) {
     if (p.n_edges <= 0) return cudaSuccess;

@@ -788,3 +788,37 @@ def test_feature_extraction_matches_oracle(ctx, bc):
         ref_c = orc.correlate_batch(np.arange(8), np.ones(8, np.int32), coords, got[:8],
                                     np.stack([r0, r0]), np.stack([r1, r1]))
         assert corr_violations(out, ref_c, _gnorm_for_batch(got[:8], np.arange(8))) == 0
+
+
+def test_oracle_provider_matches_oracle(ctx, c1_workload):
+    """OracleFlowProvider::propose (flow_provider.cpp:34-93) on the resident window:
+    ground-truth reprojection on the device, the reference's mt19937_64 draws on
+    the host — bit-identical to the restatement for the same seed; the revisions
+    become the window's deltas / weights."""
+    w = c1_workload
+    F = w.cfg["frames"]
+    ctx.frames_reserve(F, w.level0.shape[2], w.level0.shape[1], w.level1.shape[2], w.level1.shape[1], 128)
+    for f in range(F):
+        ctx.frames_upload(f, w.level0[f], w.level1[f])
+    g = synth.build_graph(w, pvo.PatchGraph)
+    prob = synth.window_arrays(w, g.window_problem(w.cfg["window"]))
+    gtp, gtd = w.gt_poses[prob["pose_frames"]], w.gt_depth[prob["patch_ids"]]
+    win = pvo.Window(ctx)
+    win.load(prob, prob["pose_frames"], prob["patch_feats"], w.K, w.image)
+    for sigma, frac, seed in ((0.0, 0.0, 0), (0.5, 0.0, 7), (1.5, 0.1, 3), (0.0, 0.25, 5)):
+        d, wt = win.oracle_propose(gtp, gtd, sigma, frac, seed=seed)
+        rd, rw = orc.oracle_propose(prob, gtp, gtd, w.K, flow_sigma=sigma, outlier_fraction=frac, seed=seed)
+        assert np.array_equal(d, rd) and np.array_equal(wt, rw), (sigma, frac)
+        assert int(np.sum(wt[:, 0] == 0.01)) >= int(frac * len(d))
+    # the provider's RNG persists across calls (a member, flow_provider.cpp:10): new draws
+    d1, _ = win.oracle_propose(gtp, gtd, 0.5, 0.05, seed=9)
+    d2, _ = win.oracle_propose(gtp, gtd, 0.5, 0.05)
+    assert not np.array_equal(d1, d2)
+    # the revisions replace the window's measurements (deltas / raw weights)
+    rd, rw = orc.oracle_propose(prob, gtp, gtd, w.K, flow_sigma=0.5, outlier_fraction=0.05, seed=9)
+    win.oracle_propose(gtp, gtd, 0.5, 0.05, seed=9)
+    res = pvo.window_problem_read(ctx, len(prob["poses"]), len(prob["depth"]), win.n_edges)
+    assert np.array_equal(res["e_delta"], rd) and np.array_equal(res["e_weight"], rw)
+    win.ba(2)
+    p_dev, d_dev, _ = win.read()
+    assert np.all(np.isfinite(p_dev)) and np.all(np.isfinite(d_dev))

@@ -664,3 +664,52 @@ def test_crop_matches_sampler_definition():  # features.cpp:204-224 with sample_
 
     ref0 = synth.crop_cubic(l0, px[1] / 4.0, py[1] / 4.0)
     assert np.allclose(out[1, 0], ref0, atol=1e-6)
+
+
+# ---------------------------------------------------------------- oracle provider (flow_provider.cpp:34-93)
+def _gt_window(seed, frames, patches, radius):
+    """graph_at_ground_truth (sim_fixtures.hpp) on a synth scene, flattened over
+    every frame: the problem plus the scene poses / inverse depths per slot."""
+    from paper_2208_04726_b200 import synth
+
+    w = synth.generate("c1", seed=seed, features=False, frames=frames, patches=patches)
+    g = orc.PatchGraph(w.K, w.image[0], w.image[1])
+    for f in range(frames):
+        g.add_frame(0.05 * f, w.gt_poses[f])
+        ks = slice(f * patches, (f + 1) * patches)
+        g.add_patches(f, w.centroids[ks], w.gt_depth[ks])
+        g.connect(radius)
+    kk, jj, _, _ = g.edges()
+    for k, j in zip(kk, jj):  # the flattening takes edges with a revision
+        g.set_revision((int(k), int(j)), (0.0, 0.0), (0.5, 0.5))
+    prob = g.window_problem(frames)
+    return w, prob, w.gt_poses[prob["pose_frames"]], w.gt_depth[prob["patch_ids"]]
+
+
+def test_oracle_revisions_vanish_at_ground_truth():  # test_features.cpp:344-367
+    w, prob, gtp, gtd = _gt_window(77, 8, 16, 4)
+    delta, weight = orc.oracle_propose(prob, gtp, gtd, w.K)
+    assert len(delta) == len(prob["e_patch"]) > 0
+    assert np.all(np.linalg.norm(delta, axis=1) < 1e-9)
+    assert np.allclose(weight, 0.99)
+
+
+def test_oracle_outlier_fraction_exact():  # test_features.cpp:369-394
+    w, prob, gtp, gtd = _gt_window(78, 6, 20, 4)
+    E = len(prob["e_patch"])
+    delta, weight = orc.oracle_propose(prob, gtp, gtd, w.K, outlier_fraction=0.1, seed=3)
+    assert int(np.sum(np.isclose(weight[:, 0], 0.01))) == int(0.1 * E)
+    # the outliers are uniform in [-32, 32); the rest stay at the ground truth
+    out = np.isclose(weight[:, 0], 0.01)
+    assert np.all(np.abs(delta[out]) <= 32.0) and np.all(np.linalg.norm(delta[~out], axis=1) < 1e-9)
+
+
+def test_oracle_noise_statistics():  # flow_provider.cpp:56-66: N(0, sigma^2) per axis, weight 1/(1+sigma^2)
+    w, prob, gtp, gtd = _gt_window(79, 10, 48, 4)
+    sigma = 0.8
+    delta, weight = orc.oracle_propose(prob, gtp, gtd, w.K, flow_sigma=sigma, seed=11)
+    assert np.allclose(weight, 1.0 / (1.0 + sigma * sigma))
+    assert abs(delta.std() - sigma) < 0.05 and abs(delta.mean()) < 0.05
+    again, _ = orc.oracle_propose(prob, gtp, gtd, w.K, flow_sigma=sigma, seed=11)
+    other, _ = orc.oracle_propose(prob, gtp, gtd, w.K, flow_sigma=sigma, seed=12)
+    assert np.array_equal(delta, again) and not np.array_equal(delta, other)
