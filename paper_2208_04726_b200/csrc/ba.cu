@@ -466,21 +466,23 @@ __device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Lay
                 v[6 * si + lane] += vs[lane];
                 bvec[6 * si + lane] += bs[lane];
             }
-            // target-pose -> edge chains
+            // target-pose -> edge chains (sj >= 0: an active edge with its own free
+            // target block; the lanes' slots arrive by shuffle, no global re-reads)
             int* p2e = wi + 4;
             int* nxt = wi + 4 + kMaxFree;
-            if (lane == 0) {
-                for (int i = 0; i < kMaxFree; ++i) p2e[i] = -1;
-                for (int l = ne - 1; l >= 0; --l) {
-                    const int sjl = a.pose_free_slot[a.e_pose[eb + l]];
-                    const double* R = rec + l * kRec;
-                    const bool act = !(R[kW] == 0.0 && R[kW + 1] == 0.0);
+            for (int i = lane; i < kMaxFree; i += 32) p2e[i] = -1;
+            __syncwarp();
+            for (int l = ne - 1; l >= 0; --l) {
+                const int sjl = __shfl_sync(0xffffffffu, sj, l);
+                if (lane == 0) {
                     nxt[l] = -1;
-                    if (!poses_frozen && act && sjl >= 0 && sjl != si) {
+                    if (sjl >= 0) {
                         nxt[l] = p2e[sjl];
                         p2e[sjl] = l;
                     }
                 }
+            }
+            if (lane == 0) {
                 wi[0] = si;
                 wi[1] = ne;
                 wi[2] = dslot;

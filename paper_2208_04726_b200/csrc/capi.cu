@@ -175,8 +175,9 @@ struct pvo_ctx {
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_corr = nullptr, ev_copy = nullptr;
     bool timing_pending = false;
-    bool tracing = false;
-    std::mt19937_64 oracle_rng{0};  // the oracle provider's RNG (flow_provider.cpp:10, rng_(noise.seed))  // record BA phase clocks (pvo_ctx_set_tracing)
+    bool tracing = false;  // record BA phase clocks (pvo_ctx_set_tracing)
+    std::mt19937_64 oracle_rng{0};  // the oracle provider's RNG (flow_provider.cpp:10, rng_(noise.seed))
+    int* d_corr_ctl = nullptr;      // correlation tile queue: [extra count, queue head, warps done, -]
 };
 
 namespace {
@@ -492,13 +493,12 @@ void run_corr(pvo_ctx* ctx, pvo_dev::CorrTmaParams t) {
         t.w1 = ctx->w1;
         t.h1 = ctx->h1;
         t.coords = ctx->c_coords.as<double>((size_t)t.n_edges * 18);
-        t.meta = ctx->c_meta.as<int>((size_t)t.n_edges * 2 * pvo_dev::kCorrMetaInts);
-        const int grid = pvo_dev::corr_tma_grid(t.n_edges, ctx->num_sms);
-        t.extra_cap = pvo_dev::corr_tma_extra_cap(t.n_edges, grid);
-        t.extra = ctx->c_over.as<int>((size_t)grid * t.extra_cap * pvo_dev::kCorrMetaInts);
+        t.list_cap = pvo_dev::corr_tma_list_cap(t.n_edges);
+        t.meta = ctx->c_meta.as<int>((size_t)t.list_cap * pvo_dev::kCorrMetaInts);
+        t.ctl = ctx->d_corr_ctl;
         t.status = ctx->d_status;
         cuda_check(pvo_dev::launch_corr_tma(t, ctx->maps, ctx->num_sms, ctx->stream), "corr_tma kernel");
-        ctx->launches += 1;
+        ctx->launches += 2;  // tile preparation + correlation
         return;
     }
     pvo_dev::CorrParams cp;
@@ -630,6 +630,8 @@ int pvo_ctx_create(int device, pvo_ctx** out) {
         cuda_check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
         ctx->own_stream = true;
         cuda_check(cudaMalloc(&ctx->d_status, sizeof(int)), "cudaMalloc");
+        cuda_check(cudaMalloc(&ctx->d_corr_ctl, 4 * sizeof(int)), "cudaMalloc");
+        cuda_check(cudaMemset(ctx->d_corr_ctl, 0, 4 * sizeof(int)), "cudaMemset");  // kept zero between launches
         for (auto& e : ctx->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
         cuda_check(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
         cuda_check(cudaEventCreateWithFlags(&ctx->ev_corr, cudaEventDisableTiming), "cudaEventCreate");
@@ -646,11 +648,13 @@ int pvo_ctx_destroy(pvo_ctx* ctx) {
         DevBuf* bufs[] = {&ctx->feat0, &ctx->feat1, &ctx->gram0, &ctx->gram1, &ctx->s0, &ctx->s1, &ctx->s2,
                           &ctx->s3,    &ctx->s4,    &ctx->s5,    &ctx->s6,    &ctx->s7, &ctx->s8,
                           &ctx->win.pose_slot, &ctx->win.patch_feats, &ctx->win.corr, &ctx->win.init_poses,
-                          &ctx->win.init_depth, &ctx->win.order, &ctx->win.flags};
+                          &ctx->win.init_depth, &ctx->win.order, &ctx->win.flags, &ctx->c_coords, &ctx->c_meta,
+                          &ctx->c_over, &ctx->c_order};
         for (DevBuf* b : bufs) b->release();
         ctx->ba.release();
         ctx->bat.release();
         if (ctx->d_status) cudaFree(ctx->d_status);
+        if (ctx->d_corr_ctl) cudaFree(ctx->d_corr_ctl);
         for (auto& e : ctx->ev)
             if (e) cudaEventDestroy(e);
         if (ctx->copy_stream) {

@@ -7,29 +7,32 @@
 //     pixels; the 729 dots <g_p, f_cell> of a tile are owned by ONE warp (lane
 //     owns 3 cells x 9 pixels, lanes 27..31 idle), so a tile needs no block
 //     barrier and no cross-warp reduction;
-//   * persistent CTAs (one per SM, 8 warps), each walking its share of the
-//     edges in target-frame order so the frames being read stay in L2; warps
-//     grab tiles dynamically from a CTA counter;
+//   * a preparation launch (corr_prep_kernel) reprojects every patch pixel
+//     (FP64) and turns each (edge, level) into tile records: one per box-sized
+//     pixel group (tiles whose pixel windows do not fit one 9x9 box — strong
+//     zoom / wide spread — are split; each sub-tile writes only its member
+//     pixels), appended to ONE global tile list in processing (target-frame)
+//     order; tiles whose every tap is zero padding are zero-filled there and
+//     never reach the correlation kernel;
+//   * persistent correlation CTAs (one per SM, 8 warps) whose warps take tiles
+//     from the global list with one atomic claim kept in flight per warp (the
+//     frames being read stay in L2; no per-CTA static shares, so no tail from
+//     unequal shares); the last warp to finish resets the queue words;
 //   * every warp runs its own 3-stage TMA ring over 16-channel chunks: per
 //     chunk a 4-D tensor copy of the tile [81 cells][16 ch] (64B-swizzled, so
 //     the 8-lane phases of a 128-bit shared load hit 8 distinct bank groups;
 //     out-of-image cells are zero-filled by TMA, which IS the reference's zero
 //     padding, features.cpp:15-17) and a 2-D copy of the patch descriptors
-//     [9 px][16 ch]; the first chunk of a tile also brings the tile's planar
-//     Gram records [5][9][12] and its 9 reprojected pixels.  The warp's elected
-//     lane refills a stage as soon as the warp has consumed it;
+//     [9 px][16 ch]; the tile's planar Gram records [5][9][12] and its 9
+//     reprojected pixels arrive in a single header buffer on their own
+//     barrier, issued when the previous tile's epilogue is done.  The warp's
+//     elected lane refills a stage as soon as the warp has consumed it;
 //   * FP32 FMA dot products in fixed channel order (deterministic); output
 //     recombination in FP32 with the bilinear weights' fractional parts taken
 //     exactly in FP64 (x - floor(x)) as the reference does; coalesced stores.
 //   * tiles whose 9 pixel windows share one 8x8 cell window ("narrow": ~half
 //     of all tiles, most level-1 tiles) run a 2-cells-per-lane variant (64
 //     cells over 32 lanes) instead of 3 cells over 27 lanes: 1/3 fewer FMAs.
-// (edge, level) tiles whose pixel windows do not fit one 9x9 box (strong
-// zoom / wide spread) are split into pixel groups that each fit a box: the
-// first group takes the tile's slot, the others are appended to a per-CTA
-// extra list that the CTA's warps drain after their regular tiles (each
-// sub-tile writes only its member pixels).  Tiles whose every tap is zero
-// padding are zero-filled directly.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -43,7 +46,17 @@ namespace pvo_dev {
 
 namespace {
 
-constexpr int kWarps = 8;
+#ifndef CORR_WARPS
+#define CORR_WARPS 8
+#endif
+#ifndef CORR_STAGES
+#define CORR_STAGES 3
+#endif
+#ifndef CORR_JIT_G
+#define CORR_JIT_G 0
+#endif
+constexpr int kWarps = CORR_WARPS;  // A/B knobs (tools/build_variant.sh): 12 warps x 2 stages and
+                                    // just-in-time descriptor loads measured equal (r1f)
 constexpr int kThreads = 32 * kWarps;
 constexpr int kD = 128;
 constexpr int kBox = 9;
@@ -52,7 +65,7 @@ constexpr int kPix = 9;
 constexpr int kOut = kPix * 49;
 constexpr int kChunkCh = 16;                           // channels per pipeline chunk (64 B rows)
 constexpr int kChunks = kD / kChunkCh;                 // 8
-constexpr int kStages = 3;                             // per-warp ring depth
+constexpr int kStages = CORR_STAGES;                   // per-warp ring depth
 constexpr int kChunkTileBytes = kCells * kChunkCh * 4;  // 5184: [81][16] f32, 64B swizzle
 constexpr int kChunkGOff = 5248;                        // 128-aligned
 constexpr int kChunkGBytes = kPix * kChunkCh * 4;       // 576: [9][16] f32
@@ -64,21 +77,21 @@ constexpr int kCoordBytes = kPix * 2 * 8;               // 144
 constexpr int kHeaderBytes = 2304;
 constexpr uint32_t kChunkTx = kChunkTileBytes + kChunkGBytes;
 constexpr uint32_t kHeaderTx = kGramBytes + kCoordBytes;
-constexpr int kHeaderOff = kStages * kStageBytes;        // 18432, 2 tile headers
-constexpr int kDotsOff = kHeaderOff + 2 * kHeaderBytes;  // 23040: [9][81] f32
-constexpr int kPixOff = kDotsOff + 2944;                 // 25984: per-tile pixel table (ax, ay, floors)
-constexpr int kMetaOff = kPixOff + 640;                  // 26624: 2 tile records
-constexpr int kWarpBytes = 27648;
+constexpr int kHeaderOff = kStages * kStageBytes;        // the tile header (own barrier)
+constexpr int kDotsOff = kHeaderOff + kHeaderBytes;      // [9][81] f32
+constexpr int kPixOff = kDotsOff + 2944;                 // per-tile pixel table (ax, ay, floors)
+constexpr int kMetaOff = kPixOff + 640;                  // 2 tile records
+constexpr int kWarpBytes = (kMetaOff + 64 + 1023) / 1024 * 1024;
 constexpr int kSmemBytes = kWarps * kWarpBytes + 1024;   // + alignment slack
 static_assert(kChunkGOff >= kChunkTileBytes && kChunkGOff + kChunkGBytes <= kStageBytes, "stage");
 static_assert(kGramBytes + kCoordBytes <= kHeaderBytes, "header");
 static_assert(kMetaOff + 64 <= kWarpBytes && kWarpBytes % 1024 == 0, "warp region");
 static_assert(kCorrMetaInts == 8, "tile record");
 
-// tile record kinds (TileRec.code bits 0..1); bit 2: narrow (8x8 window);
-// bits 8..16: far-pixel mask (zero-filled by this record); bits 17..25: member
-// pixels (outputs written by this record)
-constexpr int kKindTma = 0, kKindZero = 2, kKindBad = 3;
+// tile record code: bit 2: narrow (8x8 window); bits 8..16: far-pixel mask
+// (zero-filled by this record); bits 17..25: member pixels (outputs written by
+// this record)
+constexpr int kKindTma = 0;
 constexpr int kNarrow = 4;
 constexpr int kPixMask = (1 << kPix) - 1;
 
@@ -158,6 +171,119 @@ __device__ __forceinline__ int clamp_floor(double b, int extent) {
     return (int)floor(fmin(fmax(b, -16.0), (double)extent + 16.0));
 }
 
+// ---- tile preparation (a launch before the correlation) ----
+// Block of 128 threads per kPrepEdges processing positions: one thread per (edge,
+// pixel) reprojects the patch pixel (FP64, camera.cpp:47-71), then one thread per
+// (edge, level) builds the tile record(s) — one per box-sized pixel group — and
+// the block appends them to the global tile list in one atomic; tiles whose
+// every tap is zero padding are zero-filled here and never enter the list.
+constexpr int kPrepEdges = 14;
+constexpr int kPrepTiles = 2 * kPrepEdges;
+__global__ void __launch_bounds__(128) corr_prep_kernel(CorrTmaParams a) {
+    __shared__ double s_xy[kPrepEdges * kPix * 2];
+    __shared__ int4 s_rec[kPrepTiles * kPix * 2];  // <= 9 pixel groups per tile
+    __shared__ int s_zero[kPrepTiles];
+    __shared__ int s_nrec, s_nzero, s_base;
+    const int t = threadIdx.x;
+    const int base = blockIdx.x * kPrepEdges;
+    if (t == 0) {
+        s_nrec = 0;
+        s_nzero = 0;
+    }
+    if (t < kPrepEdges * kPix) {
+        const int pos = base + t / kPix, pix = t % kPix;
+        if (pos < a.n_edges) {
+            const int e = a.order ? a.order[pos] : pos;
+            double xy[2];
+            edge_pixel(a, e, pix, xy);
+            s_xy[2 * t] = xy[0];
+            s_xy[2 * t + 1] = xy[1];
+            a.coords[(size_t)e * 18 + 2 * pix] = xy[0];
+            a.coords[(size_t)e * 18 + 2 * pix + 1] = xy[1];
+        }
+    }
+    __syncthreads();
+    const int pos = base + (t >> 1), level = t & 1;
+    if (t < kPrepTiles && pos < a.n_edges) {
+        const int e = a.order ? a.order[pos] : pos;
+        const double* xy = s_xy + (t >> 1) * kPix * 2;
+        const double inv_scale = level ? 1.0 / 16.0 : 1.0 / 4.0;  // 1 / kFeatureStride^(level+1) (features.hpp:46)
+        const int W = level ? a.w1 : a.w0, H = level ? a.h1 : a.h0;
+        int fxs[kPix], fys[kPix];
+        bool finite = true;
+        int far = 0;  // pixels whose whole 8x8 tap window lies outside the grid: all 49 outputs are 0
+#pragma unroll
+        for (int p = 0; p < kPix; ++p) {
+            const double x = xy[2 * p], y = xy[2 * p + 1];
+            finite = finite && isfinite(x) && isfinite(y);
+            fxs[p] = clamp_floor(x * inv_scale, W);  // x / 4 or x / 16, exact
+            fys[p] = clamp_floor(y * inv_scale, H);
+            if (fxs[p] + 4 < 0 || fxs[p] - 3 >= W || fys[p] + 4 < 0 || fys[p] - 3 >= H) far |= 1 << p;
+        }
+        const int fslot = a.e_slot ? a.e_slot[e] : a.pose_slot[a.e_pose[e]];
+        const int grow = (a.e_patch[e] * 2 + level) * kPix;
+        if (!finite) {
+            atomicOr(a.status, 1 << kDevBadCoords);  // correlation.cpp:43-45
+        } else if (far == kPixMask) {              // every tap of every pixel is zero padding
+            s_zero[atomicAdd(&s_nzero, 1)] = e * 2 + level;
+        } else {
+            // Pixel groups that each fit one 9x9 box: a box at origin (X0, Y0) holds the
+            // 8x8 window of pixel q iff fx_q - 3 in {X0, X0+1} and fy_q - 3 in {Y0, Y0+1}.
+            // Greedy: seed = lowest remaining pixel; of the 4 boxes containing its window
+            // take the one covering most remaining pixels.  Group 0 (usually the whole
+            // tile) also zero-fills the far pixels.
+            int rest = kPixMask & ~far;
+            bool first = true;
+            while (rest) {
+                const int p0 = __ffs(rest) - 1;
+                int best = 0, bx = 0, by = 0;
+#pragma unroll
+                for (int cand = 0; cand < 4; ++cand) {
+                    const int X0 = fxs[p0] - 3 - (cand & 1), Y0 = fys[p0] - 3 - (cand >> 1);
+                    int m = 0;
+#pragma unroll
+                    for (int q = 0; q < kPix; ++q) {
+                        const int dx = fxs[q] - 3 - X0, dy = fys[q] - 3 - Y0;
+                        if (((rest >> q) & 1) && (unsigned)dx <= 1u && (unsigned)dy <= 1u) m |= 1 << q;
+                    }
+                    if (__popc(m) > __popc(best)) {
+                        best = m;
+                        bx = X0;
+                        by = Y0;
+                    }
+                }
+                // narrow: every member's window is the same 8x8 block -> origin = that block
+                int xl = 1 << 30, xh = -(1 << 30), yl = 1 << 30, yh = -(1 << 30);
+#pragma unroll
+                for (int q = 0; q < kPix; ++q)
+                    if ((best >> q) & 1) {
+                        xl = min(xl, fxs[q]);
+                        xh = max(xh, fxs[q]);
+                        yl = min(yl, fys[q]);
+                        yh = max(yh, fys[q]);
+                    }
+                int code = kKindTma | (best << 17) | (first ? far << 8 : 0);
+                if (xl == xh && yl == yh) {
+                    code |= kNarrow;
+                    bx = xl - 3;
+                    by = yl - 3;
+                }
+                const int i = atomicAdd(&s_nrec, 1);
+                s_rec[2 * i] = make_int4(bx, by, code, fslot);
+                s_rec[2 * i + 1] = make_int4(grow, e, level, 0);
+                first = false;
+                rest &= ~best;
+            }
+        }
+    }
+    __syncthreads();
+    if (t == 0) s_base = atomicAdd(a.ctl, s_nrec);  // < list capacity: at most 9 records per tile
+    __syncthreads();
+    int4* list = reinterpret_cast<int4*>(a.meta) + 2 * (size_t)s_base;
+    for (int i = t; i < 2 * s_nrec; i += 128) list[i] = s_rec[i];
+    for (int i = t; i < s_nzero * kOut; i += 128) a.out[(size_t)s_zero[i / kOut] * kOut + i % kOut] = 0.f;
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     corr_tma_kernel(const __grid_constant__ CUtensorMap feat0, const __grid_constant__ CUtensorMap feat1,
                     const __grid_constant__ CUtensorMap gram0, const __grid_constant__ CUtensorMap gram1,
@@ -166,134 +292,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     // 1024-aligned base, derived by offset so the compiler keeps the shared address space
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     __shared__ __align__(8) uint64_t full[kWarps * kStages];
-    __shared__ int s_next, s_nextra;
+    __shared__ __align__(8) uint64_t hfull[kWarps];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int G = gridDim.x, b = blockIdx.x;
-    const int my_edges = a.n_edges > b ? (a.n_edges - 1 - b) / G + 1 : 0;
-    const int n_tiles = 2 * my_edges;
-
-    // ---- prologue (all warps): coordinates and tile records of this CTA's edges ----
-    if (tid == 0) s_nextra = 0;
-    for (int i = tid; i < my_edges * kPix; i += kThreads) {
-        const int pos = b + (i / kPix) * G;
-        const int e = a.order ? a.order[pos] : pos;
-        const int pix = i % kPix;
-        double xy[2];
-        edge_pixel(a, e, pix, xy);
-        a.coords[(size_t)e * 18 + 2 * pix] = xy[0];
-        a.coords[(size_t)e * 18 + 2 * pix + 1] = xy[1];
-    }
-    // the tile headers re-read these coordinates with bulk (async-proxy) copies
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    __syncthreads();
-    for (int i = tid; i < n_tiles; i += kThreads) {
-        const int pos = b + (i >> 1) * G;
-        const int e = a.order ? a.order[pos] : pos;
-        const int level = i & 1;
-        const double inv_scale = level ? 1.0 / 16.0 : 1.0 / 4.0;  // 1 / kFeatureStride^(level+1) (features.hpp:46)
-        const int W = level ? a.w1 : a.w0, H = level ? a.h1 : a.h0;
-        int fxs[kPix], fys[kPix];
-        bool finite = true;
-        int far = 0;  // pixels whose whole 8x8 tap window lies outside the grid: all 49 outputs are 0
-#pragma unroll
-        for (int p = 0; p < kPix; ++p) {
-            const double x = a.coords[(size_t)e * 18 + 2 * p], y = a.coords[(size_t)e * 18 + 2 * p + 1];
-            finite = finite && isfinite(x) && isfinite(y);
-            fxs[p] = clamp_floor(x * inv_scale, W);  // x / 4 or x / 16, exact
-            fys[p] = clamp_floor(y * inv_scale, H);
-            if (fxs[p] + 4 < 0 || fxs[p] - 3 >= W || fys[p] + 4 < 0 || fys[p] - 3 >= H) far |= 1 << p;
-        }
-        const int fslot = a.e_slot ? a.e_slot[e] : a.pose_slot[a.e_pose[e]];
-        const int grow = (a.e_patch[e] * 2 + level) * kPix;
-        int4* rec = reinterpret_cast<int4*>(a.meta) + 2 * ((size_t)2 * pos + level);
-        if (!finite) {
-            atomicOr(a.status, 1 << kDevBadCoords);  // correlation.cpp:43-45
-            rec[0] = make_int4(0, 0, kKindBad, fslot);
-            rec[1] = make_int4(grow, e, level, 0);
-            continue;
-        }
-        if (far == kPixMask) {  // every tap of every pixel is zero padding
-            rec[0] = make_int4(0, 0, kKindZero | (far << 8), fslot);
-            rec[1] = make_int4(grow, e, level, 0);
-            continue;
-        }
-        // Pixel groups that each fit one 9x9 box: a box at origin (X0, Y0) holds the
-        // 8x8 window of pixel q iff fx_q - 3 in {X0, X0+1} and fy_q - 3 in {Y0, Y0+1}.
-        // Greedy: seed = lowest remaining pixel; of the 4 boxes containing its window
-        // take the one covering most remaining pixels.  Group 0 (usually the whole
-        // tile) takes the tile's slot and also zero-fills the far pixels.
-        int rest = kPixMask & ~far;
-        bool first = true;
-        while (rest) {
-            const int p0 = __ffs(rest) - 1;
-            int best = 0, bx = 0, by = 0;
-#pragma unroll
-            for (int cand = 0; cand < 4; ++cand) {
-                const int X0 = fxs[p0] - 3 - (cand & 1), Y0 = fys[p0] - 3 - (cand >> 1);
-                int m = 0;
-#pragma unroll
-                for (int q = 0; q < kPix; ++q) {
-                    const int dx = fxs[q] - 3 - X0, dy = fys[q] - 3 - Y0;
-                    if (((rest >> q) & 1) && (unsigned)dx <= 1u && (unsigned)dy <= 1u) m |= 1 << q;
-                }
-                if (__popc(m) > __popc(best)) {
-                    best = m;
-                    bx = X0;
-                    by = Y0;
-                }
-            }
-            // narrow: every member's window is the same 8x8 block -> origin = that block
-            int xl = 1 << 30, xh = -(1 << 30), yl = 1 << 30, yh = -(1 << 30);
-#pragma unroll
-            for (int q = 0; q < kPix; ++q)
-                if ((best >> q) & 1) {
-                    xl = min(xl, fxs[q]);
-                    xh = max(xh, fxs[q]);
-                    yl = min(yl, fys[q]);
-                    yh = max(yh, fys[q]);
-                }
-            int code = kKindTma | (best << 17);
-            if (xl == xh && yl == yh) {
-                code |= kNarrow;
-                bx = xl - 3;
-                by = yl - 3;
-            }
-            if (first) {
-                rec[0] = make_int4(bx, by, code | (far << 8), fslot);
-                rec[1] = make_int4(grow, e, level, 0);
-                first = false;
-            } else {
-                const int x = atomicAdd(&s_nextra, 1);
-                int4* xr = reinterpret_cast<int4*>(a.extra) + 2 * ((size_t)b * a.extra_cap + x);
-                xr[0] = make_int4(bx, by, code, fslot);
-                xr[1] = make_int4(grow, e, level, 0);
-            }
-            rest &= ~best;
-        }
-    }
+    // one global tile queue over the processing positions (target-frame order:
+    // the frames in flight stay in L2), then the extra sub-tiles
+    const int n_all = min(__ldcg(a.ctl), a.list_cap);
     if (tid < kWarps * kStages) mbar_init(&full[tid], 1);
-    if (tid == 0) s_next = 0;
+    if (tid < kWarps) mbar_init(&hfull[tid], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
-    const int n_all = n_tiles + s_nextra;  // regular tiles, then this CTA's extra sub-tiles
 
     // ================= per-warp pipeline =================
     unsigned char* wb = smem + warp * kWarpBytes;
     const uint32_t wbu = smem_u32(wb);                    // shared-window addresses, computed once
     const uint32_t baru = smem_u32(full + warp * kStages);  // stage s barrier: baru + 8 * s
+    const uint32_t hbaru = smem_u32(hfull + warp);          // header barrier
 
-    // issue cursor (warp-uniform): pending tile + its record, current tile, chunk
+    // issue cursor (warp-uniform): pending tile + its record, current tile, chunk.
+    // Tiles come from the global queue; lane 0 keeps one claim in flight so the
+    // atomic's latency hides behind a whole tile.
     int pend = 0;
+    int claim = 0;
+    if (lane == 0) claim = atomicAdd(a.ctl + 1, 1);
     int4 pr0 = make_int4(0, 0, 0, 0), pr1 = make_int4(0, 0, 0, 0);
     auto grab = [&]() {
-        int t = 0;
-        if (lane == 0) t = atomicAdd(&s_next, 1);
-        pend = __shfl_sync(0xffffffffu, t, 0);
+        pend = __shfl_sync(0xffffffffu, claim, 0);
         if (pend < n_all) {
-            const int4* src = pend < n_tiles
-                                  ? reinterpret_cast<const int4*>(a.meta) + 2 * ((size_t)2 * (b + (pend >> 1) * G) + (pend & 1))
-                                  : reinterpret_cast<const int4*>(a.extra) + 2 * ((size_t)b * a.extra_cap + (pend - n_tiles));
+            if (lane == 0) claim = atomicAdd(a.ctl + 1, 1);
+            const int4* src = reinterpret_cast<const int4*>(a.meta) + 2 * (size_t)pend;
             pr0 = __ldcg(src);
             pr1 = __ldcg(src + 1);
         }
@@ -305,41 +332,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     int is = 0, hi = 0;    // next stage to fill, tiles issued
     auto issue_one = [&]() {
         if (idone) return;
-        while (ichunk == kChunks) {  // advance to the next tile that needs the pipeline
+        if (ichunk == kChunks) {  // advance to the next tile of the list
             if (pend >= n_all) {
                 idone = true;
                 return;
             }
-            const int4 r0 = pr0, r1 = pr1;
+            ir0 = pr0;
+            ir1 = pr1;
+            ichunk = 0;
             grab();
-            const int kind = r0.z & 3;
-            if (kind == kKindTma) {
-                ir0 = r0;
-                ir1 = r1;
-                ichunk = 0;
-            } else if (kind == kKindZero) {
-                float* out = a.out + ((size_t)r1.y * 2 + r1.z) * kOut;
-                for (int o = lane; o < kOut; o += 32) out[o] = 0.f;
-            }
         }
         if (lane == 0) {
             const int level = ir1.z;
             const uint32_t bar = baru + 8 * is;
             const uint32_t st = wbu + is * kStageBytes;
             if (ichunk == 0) {
-                const int hb = hi & 1;
-                int4* rec = reinterpret_cast<int4*>(wb + kMetaOff + 32 * hb);
+                int4* rec = reinterpret_cast<int4*>(wb + kMetaOff + 32 * (hi & 1));
                 rec[0] = ir0;
                 rec[1] = ir1;
-                const uint32_t hd = wbu + kHeaderOff + hb * kHeaderBytes;
-                mbar_expect_tx(bar, kChunkTx + kHeaderTx);
-                // TMA needs a 16-byte aligned start in the innermost (x) dimension: start at
-                // floor4(x0); the 12-wide box still covers x0 .. x0 + 8
-                tma_load_4d(hd, level ? &gram1 : &gram0, ir0.x & ~3, ir0.y, 0, ir0.w, bar);
-                bulk_load(hd + kGramBytes, a.coords + (size_t)ir1.y * 18, kCoordBytes, bar);
-            } else {
-                mbar_expect_tx(bar, kChunkTx);
             }
+            mbar_expect_tx(bar, kChunkTx);
             tma_load_4d(st, level ? &feat1 : &feat0, ichunk * kChunkCh, ir0.x, ir0.y, ir0.w, bar);
             tma_load_2d(st + kChunkGOff, &patch, ichunk * kChunkCh, ir1.x, bar);
         }
@@ -347,8 +359,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++ichunk;
         is = is == kStages - 1 ? 0 : is + 1;
     };
+    // the tile header (Gram records + reprojected pixels) of tile hc, into the
+    // warp's single header buffer: issued once the previous tile's epilogue is done
+    auto issue_header = [&](int hc) {
+        if (lane == 0) {
+            const int4 r0 = *reinterpret_cast<const int4*>(wb + kMetaOff + 32 * (hc & 1));
+            const int4 r1 = *reinterpret_cast<const int4*>(wb + kMetaOff + 32 * (hc & 1) + 16);
+            const uint32_t hd = wbu + kHeaderOff;
+            mbar_expect_tx(hbaru, kHeaderTx);
+            // TMA needs a 16-byte aligned start in the innermost (x) dimension: start at
+            // floor4(x0); the 12-wide box still covers x0 .. x0 + 8
+            tma_load_4d(hd, r1.z ? &gram1 : &gram0, r0.x & ~3, r0.y, 0, r0.w, hbaru);
+            bulk_load(hd + kGramBytes, a.coords + (size_t)r1.y * 18, kCoordBytes, hbaru);
+        }
+    };
     for (int k = 0; k < kStages; ++k) issue_one();
     __syncwarp();
+    if (hi > 0) issue_header(0);
 
     float* dots = reinterpret_cast<float*>(wb + kDotsOff);
     int cs = 0;          // stage being consumed
@@ -380,10 +407,29 @@ __global__ void __launch_bounds__(kThreads, 1)
             float2 part[NC][kPix];
 #pragma unroll
             for (int u = 0; u < kChunkCh / 4; ++u) {
-                float4 v[NC], gv[kPix];
+#if CORR_JIT_G
+                float4 v[NC];
 #pragma unroll
                 for (int k = 0; k < NC; ++k) {
                     // 64B swizzle: 16-byte unit u of row r lives at unit u ^ ((r >> 1) & 3)
+                    const int sw = (roff[k] >> 7) & 3;
+                    v[k] = *reinterpret_cast<const float4*>(st + roff[k] + ((u ^ sw) << 4));
+                }
+                // pixel descriptors loaded as used (few live registers)
+#pragma unroll
+                for (int p = 0; p < kPix; ++p) {
+                    const float4 gv = *reinterpret_cast<const float4*>(g + p * kChunkCh + 4 * u);
+#pragma unroll
+                    for (int k = 0; k < NC; ++k) {
+                        const float2 va = make_float2(v[k].x, v[k].y), ga = make_float2(gv.x, gv.y);
+                        part[k][p] = u == 0 ? __fmul2_rn(va, ga) : __ffma2_rn(va, ga, part[k][p]);
+                        part[k][p] = __ffma2_rn(make_float2(v[k].z, v[k].w), make_float2(gv.z, gv.w), part[k][p]);
+                    }
+                }
+#else
+                float4 v[NC], gv[kPix];
+#pragma unroll
+                for (int k = 0; k < NC; ++k) {
                     const int sw = (roff[k] >> 7) & 3;
                     v[k] = *reinterpret_cast<const float4*>(st + roff[k] + ((u ^ sw) << 4));
                 }
@@ -401,6 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int p = 0; p < kPix; ++p)
                         part[k][p] = __ffma2_rn(make_float2(v[k].z, v[k].w), make_float2(gv[p].z, gv[p].w), part[k][p]);
+#endif
             }
 #pragma unroll
             for (int k = 0; k < NC; ++k)
@@ -430,7 +477,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tile_dots(std::integral_constant<int, 3>{});
 
         // ---- epilogue ----
-        const unsigned char* hd = wb + kHeaderOff + hb * kHeaderBytes;
+        mbar_wait(hbaru, hc & 1);
+        const unsigned char* hd = wb + kHeaderOff;
         const float* gram = reinterpret_cast<const float*>(hd) + (r0.x & 3);  // box starts at floor4(x0)
         const double* tc = reinterpret_cast<const double*>(hd + kGramBytes);
         const int e = r1.y, level = r1.z, far = (r0.z >> 8) & kPixMask, member = (r0.z >> 17) & kPixMask;
@@ -504,7 +552,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 nA = nB;
             }
         }
-        __syncwarp();  // dots are rewritten by the next tile
+        __syncwarp();  // dots and the header are rewritten by the next tile
+        if (hc + 1 < hi) issue_header(hc + 1);
+    }
+    // the last warp to finish leaves the queue words zero for the next launch
+    if (lane == 0) {
+        __threadfence();
+        if (atomicAdd(a.ctl + 2, 1) == (int)gridDim.x * kWarps - 1) {
+            a.ctl[0] = 0;
+            a.ctl[1] = 0;
+            a.ctl[2] = 0;
+        }
     }
 }
 
@@ -512,15 +570,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 int corr_tma_smem_bytes() { return kSmemBytes; }
 int corr_tma_grid(int n_edges, int num_sms) { return n_edges < num_sms ? n_edges : num_sms; }
-// worst case: every pixel of every tile in its own box -> 8 extra sub-tiles per tile
-int corr_tma_extra_cap(int n_edges, int grid) { return grid > 0 ? 2 * (kPix - 1) * ((n_edges + grid - 1) / grid) : 0; }
+// worst case: every pixel of every tile in its own box -> 9 records per tile
+int corr_tma_list_cap(int n_edges) { return 2 * kPix * n_edges; }
 
 cudaError_t launch_corr_tma(const CorrTmaParams& p, const CUtensorMap* maps, int num_sms, cudaStream_t stream) {
     if (p.n_edges <= 0) return cudaSuccess;
     cudaError_t err = cudaFuncSetAttribute(corr_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     if (err != cudaSuccess) return err;
     const int grid = corr_tma_grid(p.n_edges, num_sms);
-    if (p.extra_cap < corr_tma_extra_cap(p.n_edges, grid)) return cudaErrorInvalidValue;
+    if (p.list_cap < corr_tma_list_cap(p.n_edges) || !p.ctl) return cudaErrorInvalidValue;
+    corr_prep_kernel<<<(p.n_edges + kPrepEdges - 1) / kPrepEdges, 128, 0, stream>>>(p);
     corr_tma_kernel<<<grid, kThreads, kSmemBytes, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], p);
     return cudaGetLastError();
 }

@@ -58,9 +58,9 @@ struct CorrTmaParams {
     int n_patches = 0;
     float* out = nullptr;
     double* coords = nullptr;     // scratch [E][9][2]
-    int* meta = nullptr;          // scratch [E][2][8] tile records, in processing-position order
-    int* extra = nullptr;         // scratch [grid][extra_cap][8]: extra sub-tile records per CTA
-    int extra_cap = 0;            // records per CTA (>= 8 per regular tile of the CTA)
+    int* meta = nullptr;          // scratch [list_cap][8]: the tile list (one record per box-sized pixel group)
+    int list_cap = 0;             // >= 9 records per (edge, level) tile
+    int* ctl = nullptr;           // [list length, queue head, warps done, -], zero between launches
     int* status = nullptr;
 };
 int corr_tma_smem_bytes();
@@ -71,7 +71,7 @@ int corr_tma_smem_bytes();
 constexpr int kCorrMetaInts = 8;
 // maps: feat0, feat1, gram0, gram1, patch
 int corr_tma_grid(int n_edges, int num_sms);
-int corr_tma_extra_cap(int n_edges, int grid);
+int corr_tma_list_cap(int n_edges);
 cudaError_t launch_corr_tma(const CorrTmaParams& p, const CUtensorMap* maps, int num_sms, cudaStream_t stream);
 // Gram records of a level: planes [8][H][gram_stride(W)], rows padded to a 16-byte
 // multiple (TMA global strides must be 16-byte multiples); pad cells stay zero.
