@@ -148,8 +148,13 @@ __device__ __forceinline__ T* at(unsigned char* smem, int off) {
 // ---------------------------------------------------------------------------
 constexpr int kBlk = 8;
 
+#ifndef SOLVE_PROBE_BEGIN  // phase clocks for tools/micro_solve.cu
+#define SOLVE_PROBE_BEGIN
+#define SOLVE_PROBE(i)
+#endif
 __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, const Layout& L, double* x_out) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    SOLVE_PROBE_BEGIN
     const int ld = np + 1;                    // row stride: row np carries the right-hand side
     double* A = at<double>(smem, L.A);        // [(np+1)][(np+1)] lower triangle (+ rhs row)
     double* x = at<double>(smem, L.x);        // staged system (upper triangle + rhs), then x
@@ -206,70 +211,85 @@ __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, c
         }
     }
     __syncthreads();
+    SOLVE_PROBE(0)
 
-    for (int K0 = 0; K0 < np; K0 += kBlk) {
-        const int bsz = min(kBlk, np - K0);
-        // (1) diagonal block on warp 0: lane i < bsz holds row K0+i of the block
-        if (warp == 0) {
-            double row[kBlk];
+    // (1) diagonal block on warp 0: lane i < bsz holds row K0+i of the block
+    auto diag = [&](int K0, int bsz) {
+        double row[kBlk];
 #pragma unroll
-            for (int j = 0; j < kBlk; ++j) row[j] = (lane < bsz && j <= lane) ? A[(K0 + lane) * ld + K0 + j] : 0.0;
-            bool fail = false, zero = false;
+        for (int j = 0; j < kBlk; ++j) row[j] = (lane < bsz && j <= lane) ? A[(K0 + lane) * ld + K0 + j] : 0.0;
+        bool fail = false, zero = false;
 #pragma unroll
-            for (int kk = 0; kk < kBlk; ++kk) {
-                if (kk < bsz) {
-                    const double dk = __shfl_sync(0xffffffffu, row[kk], kk);
-                    const bool valid = fabs(dk) > 0.0;
-                    if (K0 + kk == 0 && !valid) zero = true;  // Eigen: all-zero diagonal
-                    const double inv = valid ? 1.0 / dk : 0.0;
-                    if (lane == 0) dinv[K0 + kk] = inv;
-                    const double ci = row[kk];  // unscaled column entry of this lane's row
-                    const bool below = lane > kk && lane < bsz;
-                    if (below && !valid && ci != 0.0) fail = true;
-                    const double li = below ? (valid ? ci * inv : ci) : row[kk];
+        for (int kk = 0; kk < kBlk; ++kk) {
+            if (kk < bsz) {
+                const double dk = __shfl_sync(0xffffffffu, row[kk], kk);
+                const bool valid = fabs(dk) > 0.0;
+                if (K0 + kk == 0 && !valid) zero = true;  // Eigen: all-zero diagonal
+                const double inv = valid ? __drcp_rn(dk) : 0.0;  // = 1.0 / dk (both correctly rounded)
+                if (lane == 0) dinv[K0 + kk] = inv;
+                const double ci = row[kk];  // unscaled column entry of this lane's row
+                const bool below = lane > kk && lane < bsz;
+                if (below && !valid && ci != 0.0) fail = true;
+                const double li = below ? (valid ? ci * inv : ci) : row[kk];
 #pragma unroll
-                    for (int j = kk + 1; j < kBlk; ++j) {
-                        const double cj = __shfl_sync(0xffffffffu, ci, j);  // column entry of row K0+j
-                        if (below && j <= lane && valid) row[j] -= ci * (cj * inv);
-                    }
-                    row[kk] = li;
+                for (int j = kk + 1; j < kBlk; ++j) {
+                    const double cj = __shfl_sync(0xffffffffu, ci, j);  // column entry of row K0+j
+                    if (below && j <= lane && valid) row[j] -= ci * (cj * inv);
                 }
+                row[kk] = li;
             }
-            if (lane < bsz) {
-#pragma unroll
-                for (int j = 0; j < kBlk; ++j)
-                    if (j <= lane) A[(K0 + lane) * ld + K0 + j] = row[j];
-            }
-            if (__any_sync(0xffffffffu, fail) && lane == 0) s_fail = 1;
-            if (zero && lane == 0) s_zero = 1;
         }
-        __syncthreads();
-        if (s_zero) break;
-        // (2) panel rows i >= K0+bsz (the rhs row np included): forward elimination
-        for (int i = K0 + bsz + tid; i <= np; i += kThreads) {
-            double seg[kBlk];
-#pragma unroll
-            for (int j = 0; j < kBlk; ++j) seg[j] = j < bsz ? A[i * ld + K0 + j] : 0.0;
-#pragma unroll
-            for (int kk = 0; kk < kBlk; ++kk) {
-                if (kk < bsz) {
-                    const double c = seg[kk];
-                    const double inv = dinv[K0 + kk];
-#pragma unroll
-                    for (int j = kk + 1; j < kBlk; ++j)
-                        if (j < bsz) seg[j] -= c * A[(K0 + j) * ld + K0 + kk];  // L of the diagonal block
-                    const double lv = inv != 0.0 ? c * inv : c;
-                    if (inv == 0.0 && c != 0.0 && i < np) s_fail = 1;
-                    seg[kk] = lv;
-                    LT[kk * ld + i] = lv;
-                    WD[i * kBlk + kk] = c;  // = l * d (the unscaled column entry)
-                }
-            }
+        if (lane < bsz) {
 #pragma unroll
             for (int j = 0; j < kBlk; ++j)
-                if (j < bsz) A[i * ld + K0 + j] = seg[j];
+                if (j <= lane) A[(K0 + lane) * ld + K0 + j] = row[j];
+        }
+        if (__any_sync(0xffffffffu, fail) && lane == 0) s_fail = 1;
+        if (zero && lane == 0) s_zero = 1;
+    };
+    for (int K0 = 0; K0 < np; K0 += kBlk) {
+        const int bsz = min(kBlk, np - K0);
+        if (warp == 0) diag(K0, bsz);
+        __syncthreads();
+        SOLVE_PROBE(1)
+        if (s_zero) break;
+        // (2) panel rows i >= K0+bsz (the rhs row np included): forward elimination,
+        // the diagonal block's L and reciprocal pivots preloaded (broadcast loads),
+        // the row's 8 entries eliminated in registers, then stored
+        if (K0 + bsz + tid <= np) {
+            double Ld[kBlk][kBlk], inv[kBlk];
+#pragma unroll
+            for (int kk = 0; kk < kBlk; ++kk) {
+                inv[kk] = kk < bsz ? dinv[K0 + kk] : 0.0;
+#pragma unroll
+                for (int j = kk + 1; j < kBlk; ++j) Ld[j][kk] = j < bsz ? A[(K0 + j) * ld + K0 + kk] : 0.0;
+            }
+            for (int i = K0 + bsz + tid; i <= np; i += kThreads) {
+                double seg[kBlk], cs[kBlk];
+#pragma unroll
+                for (int j = 0; j < kBlk; ++j) seg[j] = j < bsz ? A[i * ld + K0 + j] : 0.0;
+                bool bad = false;
+#pragma unroll
+                for (int kk = 0; kk < kBlk; ++kk) {
+                    const double c = seg[kk];
+#pragma unroll
+                    for (int j = kk + 1; j < kBlk; ++j) seg[j] -= c * Ld[j][kk];
+                    cs[kk] = c;
+                    if (kk < bsz && inv[kk] == 0.0 && c != 0.0) bad = true;
+                    seg[kk] = inv[kk] != 0.0 ? c * inv[kk] : c;
+                }
+                if (bad && i < np) s_fail = 1;
+#pragma unroll
+                for (int kk = 0; kk < kBlk; ++kk)
+                    if (kk < bsz) {
+                        LT[kk * ld + i] = seg[kk];
+                        WD[i * kBlk + kk] = cs[kk];  // = l * d (the unscaled column entry)
+                        A[i * ld + K0 + kk] = seg[kk];
+                    }
+            }
         }
         __syncthreads();
+        SOLVE_PROBE(2)
         // (3) trailing update A[i][j] -= sum_kk (L D)_i,kk L_j,kk for K0+bsz <= j <= i (j < np)
         for (int i = K0 + bsz + warp; i <= np; i += kWarps) {
             double w[kBlk];
@@ -284,6 +304,7 @@ __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, c
             }
         }
         __syncthreads();
+        SOLVE_PROBE(3)
     }
     if (s_fail) return false;
     if (s_zero) {
@@ -294,29 +315,27 @@ __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, c
     // z = D^-1 L^-1 P b sits in row np (pseudo-inverse of D: |d| <= DBL_MIN -> 0)
     for (int i = tid; i < np; i += kThreads) x[i] = fabs(A[i * ld + i]) > DBL_MIN ? A[np * ld + i] : 0.0;
     __syncthreads();
-    // blocked backward substitution L^T x = z, last block first
-    for (int K0 = ((np - 1) / kBlk) * kBlk; K0 >= 0; K0 -= kBlk) {
-        const int bsz = min(kBlk, np - K0);
-        // x_K -= L_{J,K}^T x_J over the solved rows J below the block: warp c owns column K0+c
-        if (warp < bsz) {
-            const int c = K0 + warp;
-            double s = 0.0;
-            for (int j = K0 + bsz + lane; j < np; j += 32) s += A[j * ld + c] * x[j];
-            s = warp_sum(s);
-            if (lane == 0) od[warp] = x[c] - s;
+    // backward substitution L^T x = z on warp 0, column-oriented: lane l keeps
+    // z_l, z_{l+32}, z_{l+64} in registers; once x_i = z_i is final it is
+    // broadcast and every z_j (j < i) takes its L_ij x_i term (no barriers)
+    if (warp == 0) {
+        double z0 = lane < np ? x[lane] : 0.0, z1 = lane + 32 < np ? x[lane + 32] : 0.0;
+        double z2 = lane + 64 < np ? x[lane + 64] : 0.0;
+        for (int i = np - 1; i >= 0; --i) {
+            const int sl = i >> 5;
+            const double own = sl == 0 ? z0 : sl == 1 ? z1 : z2;
+            const double xi = __shfl_sync(0xffffffffu, own, i & 31);
+            const double* Li = A + i * ld;
+            if (lane < i) z0 -= Li[lane] * xi;
+            if (lane + 32 < i) z1 -= Li[lane + 32] * xi;
+            if (lane + 64 < i) z2 -= Li[lane + 64] * xi;
         }
-        __syncthreads();
-        // unit upper-triangular solve inside the block (warp 0, lane c holds x_c)
-        if (warp == 0) {
-            double xc = lane < bsz ? od[lane] : 0.0;
-            for (int cc = bsz - 1; cc >= 0; --cc) {
-                const double xv = __shfl_sync(0xffffffffu, xc, cc);
-                if (lane < cc) xc -= A[(K0 + cc) * ld + K0 + lane] * xv;
-            }
-            if (lane < bsz) x[K0 + lane] = xc;
-        }
-        __syncthreads();
+        if (lane < np) x[lane] = z0;
+        if (lane + 32 < np) x[lane + 32] = z1;
+        if (lane + 64 < np) x[lane + 64] = z2;
     }
+    __syncthreads();
+    SOLVE_PROBE(4)
     for (int i = tid; i < np; i += kThreads) x_out[perm[i]] = x[i];
     __syncthreads();
     return true;

@@ -6,6 +6,7 @@ __device__ long long g_ph[8];
 #define SOLVE_PROBE(i) if (threadIdx.x == 0) { const long long _t = clock64(); g_ph[i] += _t - _pt; _pt = _t; }
 #include "../paper_2208_04726_b200/csrc/ba.cu"
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 namespace pvo_dev {
 namespace {
@@ -22,10 +23,18 @@ __global__ void micro(const double* sys, int np, double* x, long long* t) {
         printf("  stage+perm %lld diag %lld panel %lld trailing %lld backsub %lld\n", g_ph[0], g_ph[1], g_ph[2], g_ph[3], g_ph[4]);
     }
 }
+// the same solve repeated (enough warp-state samples for an ncu source view)
+__global__ void micro_loop(const double* sys, int np, double* x, int reps) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Layout L = make_layout(np, 0);
+    for (int r = 0; r < reps; ++r) ldlt_solve_cta(sys, np, smem, L, x);
+}
 }  // namespace
 }  // namespace pvo_dev
-int main() {
+int main(int argc, char** argv) {
+    const int loop_np = argc > 1 ? atoi(argv[1]) : 0;  // profiling mode: micro_solve <np> <reps>
     for (int np : {42, 60, 96}) {
+        if (loop_np && np != loop_np) continue;
         const int nent = np * (np + 1) / 2;
         std::vector<double> h(nent + np), A((size_t)np * np), b(np);
         int e = 0;
@@ -45,6 +54,11 @@ int main() {
         const pvo_dev::Layout L = pvo_dev::make_layout(np, 0);
         cudaFuncSetAttribute(pvo_dev::micro, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
         long long t[2];
+        if (loop_np) {
+            cudaFuncSetAttribute(pvo_dev::micro_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
+            pvo_dev::micro_loop<<<1, 256, L.total>>>(dsys, np, dx, argc > 2 ? atoi(argv[2]) : 200);
+            cudaDeviceSynchronize();
+        }
         for (int rep = 0; rep < 3; ++rep) {
             pvo_dev::micro<<<1, 256, L.total>>>(dsys, np, dx, dt);
             cudaMemcpy(t, dt, sizeof(t), cudaMemcpyDeviceToHost);
