@@ -540,23 +540,23 @@ __device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Lay
                 const double* scw = at<double>(smem, L.scal) + w * kScal;
                 const int* p2e = wiw + 4;
                 const int* nxt = wiw + 4 + kMaxFree;
+                // one code path for every block pair (few divergent lanes): the
+                // edges of the (A, B) term are those targeting the non-source block
+                // (at most one per pose), read as Gs for the source side, Jt else
                 double val = 0.0;
-                if (A == si && B == si) {
+                const bool sa = A == si, sb = B == si;
+                if (sa && sb) {
                     val = scw[4 + 6 * ra + rb];
-                } else if (A == si) {
-                    for (int l = p2e[B]; l >= 0; l = nxt[l]) {
+                } else if (sa || sb || A == B) {
+                    const int oa = (sa ? kGs : kJt) + ra, ob = (sb ? kGs : kJt) + rb;
+                    int l = p2e[sa ? B : A];
+                    if (l >= 0) {  // the (patch, pose) edge; a chain only for repeated edges
                         const double* R = recw + l * kRec;
-                        val += (R[kGs + ra] * R[kW]) * R[kJt + rb] + (R[kGs + 6 + ra] * R[kW + 1]) * R[kJt + 6 + rb];
-                    }
-                } else if (B == si) {
-                    for (int l = p2e[A]; l >= 0; l = nxt[l]) {
-                        const double* R = recw + l * kRec;
-                        val += (R[kJt + ra] * R[kW]) * R[kGs + rb] + (R[kJt + 6 + ra] * R[kW + 1]) * R[kGs + 6 + rb];
-                    }
-                } else if (A == B) {
-                    for (int l = p2e[A]; l >= 0; l = nxt[l]) {
-                        const double* R = recw + l * kRec;
-                        val += (R[kJt + ra] * R[kW]) * R[kJt + rb] + (R[kJt + 6 + ra] * R[kW + 1]) * R[kJt + 6 + rb];
+                        val = (R[oa] * R[kW]) * R[ob] + (R[oa + 6] * R[kW + 1]) * R[ob + 6];
+                        for (l = nxt[l]; l >= 0; l = nxt[l]) {
+                            const double* Rn = recw + l * kRec;
+                            val += (Rn[oa] * Rn[kW]) * Rn[ob] + (Rn[oa + 6] * Rn[kW + 1]) * Rn[ob + 6];
+                        }
                     }
                 }
                 if (dfree) val -= (vw[ia] * scw[2]) * vw[ib];
