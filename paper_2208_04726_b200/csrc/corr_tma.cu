@@ -172,14 +172,18 @@ __device__ __forceinline__ int clamp_floor(double b, int extent) {
 }
 
 // ---- tile preparation (a launch before the correlation) ----
-// Block of 128 threads per kPrepEdges processing positions: one thread per (edge,
+// Block of kPrepThreads threads per kPrepEdges processing positions: one thread per (edge,
 // pixel) reprojects the patch pixel (FP64, camera.cpp:47-71), then one thread per
 // (edge, level) builds the tile record(s) — one per box-sized pixel group — and
 // the block appends them to the global tile list in one atomic; tiles whose
 // every tap is zero padding are zero-filled here and never enter the list.
-constexpr int kPrepEdges = 14;
+#ifndef CORR_PREP_THREADS
+#define CORR_PREP_THREADS 128
+#endif
+constexpr int kPrepThreads = CORR_PREP_THREADS;
+constexpr int kPrepEdges = kPrepThreads / kPix;  // 14 at 128 threads
 constexpr int kPrepTiles = 2 * kPrepEdges;
-__global__ void __launch_bounds__(128) corr_prep_kernel(CorrTmaParams a) {
+__global__ void __launch_bounds__(kPrepThreads) corr_prep_kernel(CorrTmaParams a) {
     __shared__ double s_xy[kPrepEdges * kPix * 2];
     __shared__ int4 s_rec[kPrepTiles * kPix * 2];  // <= 9 pixel groups per tile
     __shared__ int s_zero[kPrepTiles];
@@ -280,8 +284,11 @@ __global__ void __launch_bounds__(128) corr_prep_kernel(CorrTmaParams a) {
     if (t == 0) s_base = atomicAdd(a.ctl, s_nrec);  // < list capacity: at most 9 records per tile
     __syncthreads();
     int4* list = reinterpret_cast<int4*>(a.meta) + 2 * (size_t)s_base;
-    for (int i = t; i < 2 * s_nrec; i += 128) list[i] = s_rec[i];
-    for (int i = t; i < s_nzero * kOut; i += 128) a.out[(size_t)s_zero[i / kOut] * kOut + i % kOut] = 0.f;
+    for (int i = t; i < 2 * s_nrec; i += kPrepThreads) list[i] = s_rec[i];
+    for (int z = t >> 5; z < s_nzero; z += kPrepThreads / 32) {  // a warp per zero tile, coalesced
+        float* o = a.out + (size_t)s_zero[z] * kOut;
+        for (int i = t & 31; i < kOut; i += 32) o[i] = 0.f;
+    }
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -579,7 +586,7 @@ cudaError_t launch_corr_tma(const CorrTmaParams& p, const CUtensorMap* maps, int
     if (err != cudaSuccess) return err;
     const int grid = corr_tma_grid(p.n_edges, num_sms);
     if (p.list_cap < corr_tma_list_cap(p.n_edges) || !p.ctl) return cudaErrorInvalidValue;
-    corr_prep_kernel<<<(p.n_edges + kPrepEdges - 1) / kPrepEdges, 128, 0, stream>>>(p);
+    corr_prep_kernel<<<(p.n_edges + kPrepEdges - 1) / kPrepEdges, kPrepThreads, 0, stream>>>(p);
     corr_tma_kernel<<<grid, kThreads, kSmemBytes, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], p);
     return cudaGetLastError();
 }
