@@ -822,3 +822,84 @@ def test_oracle_provider_matches_oracle(ctx, c1_workload):
     win.ba(2)
     p_dev, d_dev, _ = win.read()
     assert np.all(np.isfinite(p_dev)) and np.all(np.isfinite(d_dev))
+
+
+def test_empty_inputs_follow_the_reference(ctx):
+    """Empty inputs: an edge-less correlate / measure batch is a no-op;
+    gauss_newton_step on an edge-less problem throws invalid_argument
+    (bundle_adjust.cpp:119-120); optimize_window on a graph without revisions
+    returns the no-op solution (bundle_adjust.cpp:254-257), like the oracle."""
+    w = synth.generate("c1", seed=3, frames=4, patches=8)
+    F = w.cfg["frames"]
+    _, H0, W0, D = w.level0.shape
+    _, H1, W1, _ = w.level1.shape
+    ctx.frames_reserve(F, W0, H0, W1, H1, D)
+    for f in range(F):
+        ctx.frames_upload(f, w.level0[f], w.level1[f])
+    pf = w.patch_feats[:8]
+    out = pvo.correlate_batch(np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros((0, 9, 2)), pf, ctx=ctx)
+    assert out.shape == (0, 2, 9, 7, 7)
+    d, wt, fl = pvo.measure_batch(np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros((0, 2)), pf, ctx=ctx)
+    assert len(d) == len(wt) == len(fl) == 0
+    pr = pvo.BAProblem(w.poses[:2], np.array([True, False]), np.zeros(0, np.int32), np.zeros((0, 9)),
+                       np.zeros((0, 9)), np.zeros(0), np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros((0, 2)),
+                       np.zeros((0, 2)), w.K)
+    with pytest.raises(ValueError, match="at least one edge"):
+        pvo.gauss_newton_step(pr, ctx=ctx)
+    # a graph whose edges carry no revision: optimize_window is a no-op on both sides
+    g = pvo.PatchGraph(w.K, w.image[0], w.image[1], 3)
+    o = orc.PatchGraph(w.K, w.image[0], w.image[1])
+    M = w.cfg["patches"]
+    for f in range(F):
+        for gg in (g, o):
+            gg.add_frame(0.05 * f, w.poses[f])
+            gg.add_patches(f, w.centroids[f * M:(f + 1) * M], w.depth[f * M:(f + 1) * M])
+            gg.connect(w.cfg["radius"])
+    sol = pvo.optimize_window(g, pvo.WindowOptions(window=10, iterations=2), ctx=ctx)
+    ref_norms, ref_ne = o.optimize_window(window=10, iterations=2)
+    assert sol.num_edges == ref_ne == 0 and sol.residual_norms == ref_norms == []
+    _, poses = g.frames()
+    assert np.array_equal(poses, w.poses[:F])
+
+
+def test_window_c2_full_size_sampled_parity_and_determinism(ctx):
+    """Config 2 at full size (16,800 edges): the correlation of a random 500-edge
+    sample against the oracle, the BA result against the oracle, and bitwise
+    identical reruns (size-independent properties at the benchmark size)."""
+    w = synth.generate("c2")
+    F = w.cfg["frames"]
+    ctx.frames_reserve(F, w.level0.shape[2], w.level0.shape[1], w.level1.shape[2], w.level1.shape[1], 128)
+    for f in range(F):
+        ctx.frames_upload(f, w.level0[f], w.level1[f])
+    g = synth.build_graph(w, pvo.PatchGraph)
+    prob = synth.window_arrays(w, g.window_problem(w.cfg["window"]))
+    win = pvo.Window(ctx)
+    win.load(prob, prob["pose_frames"], prob["patch_feats"], w.K, w.image)
+    E = win.n_edges
+    assert E == 16800
+    vols = []
+    for _ in range(2):
+        win.reset()
+        vol = np.empty((E, 2, 9, 7, 7), np.float32)
+        win.iteration(2, corr_out=vol)
+        vols.append((vol, *win.read()))
+    assert np.array_equal(vols[0][0], vols[1][0])
+    assert np.array_equal(vols[0][1], vols[1][1]) and np.array_equal(vols[0][2], vols[1][2])
+    vol, p_dev, d_dev, _ = vols[0]
+    # correlation at the loaded state, sampled edges
+    rng = np.random.default_rng(2)
+    sel = np.sort(rng.choice(E, 500, replace=False))
+    coords = np.empty((len(sel), 9, 2))
+    for n, e in enumerate(sel):
+        k = prob["e_patch"][e]
+        coords[n], _ = orc.reproject_patch(prob["poses"][prob["patch_src"][k]], prob["poses"][prob["e_pose"][e]],
+                                           w.K, prob["patch_x"][k], prob["patch_y"][k], prob["depth"][k])
+    slots = prob["pose_frames"][prob["e_pose"][sel]]
+    ref = orc.correlate_batch(prob["e_patch"][sel], slots, coords, prob["patch_feats"], w.level0, w.level1,
+                              threads=THREADS)
+    gn = _gnorm_for_batch(prob["patch_feats"], prob["e_patch"][sel])
+    assert corr_violations(vol[sel], ref, gn) == 0
+    # optimize_window's iterations on the frozen revisions: the oracle's BA
+    ref_ba = orc.ba_window(g.window_problem(w.cfg["window"]), w.K, iterations=2)
+    dt, dq = pose_parity(p_dev, ref_ba["poses"])
+    assert dt.max() <= 1e-3 and dq.max() <= 1e-3
