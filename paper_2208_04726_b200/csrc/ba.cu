@@ -702,13 +702,15 @@ __device__ void ba_window_body(const BAParams& a, bool batched) {
     {
         unsigned* abt = at<unsigned>(smem, L.ab);
         const int nent = nent_of(np_full);
+        auto row_base = [&](int r) { return r * np_full - r * (r - 1) / 2; };
         for (int ent = tid; ent < nent; ent += kThreads) {
-            int ia = 0, rowlen = np_full, base = 0;
-            while (ent >= base + rowlen) {
-                base += rowlen;
-                --rowlen;
-                ++ia;
-            }
+            // row of a packed upper-triangle entry: closed form, then an exact fix-up
+            const float q = (float)(2 * np_full + 1);
+            int ia = (int)((q - sqrtf(q * q - 8.0f * (float)ent)) * 0.5f);
+            ia = max(0, min(ia, np_full - 1));
+            while (ia > 0 && row_base(ia) > ent) --ia;
+            while (ia + 1 < np_full && row_base(ia + 1) <= ent) ++ia;
+            const int base = row_base(ia);
             const int ib = ia + ent - base;
             abt[ent] = (unsigned)ia | ((unsigned)ib << 8) | ((unsigned)(ia / 6) << 16) | ((unsigned)(ib / 6) << 24);
         }
