@@ -532,10 +532,17 @@ void run_corr(pvo_ctx* ctx, pvo_dev::CorrTmaParams t) {
 
 // Stable order of edges by frame-store slot (L2 locality of the TMA kernel).
 std::vector<int> slot_order(int n, const int* slot_of_edge) {
+    // stable counting sort by frame slot (= std::stable_sort by slot, O(n))
+    int lo = 0, hi = -1;
+    for (int e = 0; e < n; ++e) {
+        lo = e == 0 ? slot_of_edge[e] : std::min(lo, slot_of_edge[e]);
+        hi = e == 0 ? slot_of_edge[e] : std::max(hi, slot_of_edge[e]);
+    }
     std::vector<int> order(n);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int a, int b) { return slot_of_edge[a] < slot_of_edge[b]; });
+    std::vector<int> start((size_t)std::max(hi - lo + 2, 1), 0);
+    for (int e = 0; e < n; ++e) ++start[slot_of_edge[e] - lo + 1];
+    for (size_t i = 1; i < start.size(); ++i) start[i] += start[i - 1];
+    for (int e = 0; e < n; ++e) order[start[slot_of_edge[e] - lo]++] = e;
     return order;
 }
 
