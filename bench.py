@@ -583,7 +583,7 @@ def run_e2e(args, w, prob, ctx, stream, win):
         one()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    n = max(1, min(args.steps, 20))
+    n = max(1, min(args.steps, 50))
     for _ in range(n):
         one()
     torch.cuda.synchronize()

@@ -198,6 +198,18 @@ void download(pvo_ctx* ctx, T* host, const T* dev, size_t count) {
     if (count) cuda_check(cudaMemcpyAsync(host, dev, count * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
 }
 void sync(pvo_ctx* ctx) { cuda_check(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize"); }
+// Page-locked (or registered) host memory: an async copy from it is still in
+// flight when the call returns, so calls that read such caller buffers sync
+// before returning (pageable sources are staged by the copy itself).
+bool host_pinned(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
 
 void reset_status(pvo_ctx* ctx) {
     cuda_check(cudaMemsetAsync(ctx->d_status, 0, sizeof(int), ctx->stream), "status reset");
@@ -1905,8 +1917,8 @@ int pvo_dgraph_add_frame(pvo_dgraph* g, double ts, const double* pose, int frame
         g->f_index.push_back(idx);
         g->f_slot.push_back(frame_slot);
         g->f_ts.push_back(ts);
-        dg_upload_frames(g, nullptr);
-        sync(ctx);
+        dg_upload_frames(g, nullptr);  // stream-ordered; pageable sources are staged before return
+        if (host_pinned(pose)) sync(ctx);
         if (out_index) *out_index = idx;
     });
 }
@@ -1958,8 +1970,8 @@ int pvo_dgraph_add_patches(pvo_dgraph* g, int frame, int n, const double* centro
         // the new patches have no edges yet: ebeg[P0+1 .. P0+n] = E
         std::vector<int> eb(n, g->E);
         h2d(g->ebeg[b], eb.data(), 4 * (size_t)(P0 + 1), 4 * (size_t)n);
-        g->P = P0 + n;
-        sync(ctx);
+        g->P = P0 + n;  // stream-ordered; the pageable temporaries were staged by the copies
+        if (host_pinned(depths) || host_pinned(feats)) sync(ctx);
     });
 }
 
@@ -2001,7 +2013,6 @@ int pvo_dgraph_connect(pvo_dgraph* g, int radius, int* n_added) {
         if (n_added) *n_added = E2 - g->E;
         g->E = E2;
         g->cur = nb;
-        sync(ctx);
     });
 }
 
