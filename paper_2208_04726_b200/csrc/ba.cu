@@ -165,8 +165,15 @@ __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, c
     int* perm = at<int>(smem, L.perm);
     __shared__ int s_fail, s_zero;
     const int nent = nent_of(np);
-    // stage the reduced system with coalesced loads
-    for (int i = tid; i < nent + np; i += kThreads) x[i] = sys[i];
+    // stage the reduced system with coalesced loads, 8 in flight per thread
+    for (int i0 = tid; i0 < nent + np; i0 += 8 * kThreads) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = i0 + u * kThreads < nent + np ? sys[i0 + u * kThreads] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (i0 + u * kThreads < nent + np) x[i0 + u * kThreads] = v[u];
+    }
     if (tid == 0) {
         s_fail = 0;
         s_zero = 0;
@@ -621,33 +628,49 @@ __device__ void phase_update(const BAParams& a, unsigned char* smem, const Layou
     double* wr = at<double>(smem, L.wr);
     double wr_sum = 0, wr_w = 0;
     for (int k = k0 + warp; k < k1; k += kWarps) {
-        double dnew = a.depth[k];
-        if (a.depth_slot[k] >= 0) {
+        // every global input of the patch and of the lane's edge is loaded up
+        // front (independent loads in flight together), then used
+        const int dslot = a.depth_slot[k];
+        const double d0 = a.depth[k];
+        const int eb = a.patch_edge_begin[k], ne = a.patch_edge_begin[k + 1] - eb;
+        const int src = a.patch_src[k];
+        const double ph = a.patch_h[k], pbd = a.patch_bd[k];
+        double pv[kMaxNp / 32];
+#pragma unroll
+        for (int u = 0; u < kMaxNp / 32; ++u) {
+            const int i = lane + 32 * u;
+            pv[u] = i < np ? a.patch_v[(size_t)k * np + i] : 0.0;
+        }
+        const int e = eb + lane;
+        const bool has_edge = lane < ne;  // <= 32 edges per patch (kMaxEdges)
+        const int tgt = has_edge ? a.e_pose[e] : 0;
+        const double t0 = has_edge ? a.e_target[2 * e] : 0.0, t1 = has_edge ? a.e_target[2 * e + 1] : 0.0;
+        const double w0 = has_edge ? a.e_weight[2 * e] : 0.0, w1 = has_edge ? a.e_weight[2 * e + 1] : 0.0;
+        double dnew = d0;
+        if (dslot >= 0) {
             double dot = 0.0;
-            for (int i = lane; i < np; i += 32) dot += a.patch_v[(size_t)k * np + i] * delta[i];
+#pragma unroll
+            for (int u = 0; u < kMaxNp / 32; ++u)
+                if (lane + 32 * u < np) dot += pv[u] * delta[lane + 32 * u];
             dot = warp_sum(dot);
-            const double inv_h = 1.0 / a.patch_h[k];
-            const double dd = inv_h * (a.patch_bd[k] - dot);  // bundle_adjust.cpp:88-89
+            const double inv_h = 1.0 / ph;
+            const double dd = inv_h * (pbd - dot);  // bundle_adjust.cpp:88-89
             if (!isfinite(dd) && lane == 0) set_status(status, kDevNonFiniteDepth);
             dnew = fmax(0.0, dnew + dd);  // bundle_adjust.cpp:211
         }
         if (lane == 0) a.cand_depth[k] = dnew;
-        const int eb = a.patch_edge_begin[k], ne = a.patch_edge_begin[k + 1] - eb;
-        const int src = a.patch_src[k];
         const SE3 pi = se3_load(cand + 7 * src);
         double ws = 0, ww = 0;
-        for (int l = lane; l < ne; l += 32) {
-            const int e = eb + l;
-            const int tgt = a.e_pose[e];
+        if (has_edge) {
             const SE3 pj = se3_load(cand + 7 * tgt);
             double cu, cv;
             bool behind;
             const Relative rel = rel_from_mats(cmats + 12 * src, cmats + 12 * tgt);
             center_behind(se3_equal(pi, pj), rel, K, a.patch_x + 9 * (size_t)k, a.patch_y + 9 * (size_t)k, dnew, &cu,
                           &cv, &behind);
-            const double rx = cu - a.e_target[2 * e], ry = cv - a.e_target[2 * e + 1];
-            const double wx = behind ? 0.0 : a.e_weight[2 * e];
-            const double wy = behind ? 0.0 : a.e_weight[2 * e + 1];
+            const double rx = cu - t0, ry = cv - t1;
+            const double wx = behind ? 0.0 : w0;
+            const double wy = behind ? 0.0 : w1;
             ws += wx * rx * rx + wy * ry * ry;
             ww += wx + wy;
         }
@@ -749,8 +772,19 @@ __device__ void ba_window_body(const BAParams& a, bool batched) {
                 const unsigned* abt = at<unsigned>(smem, L.ab);
                 const int lane = tid & 31;
                 for (int ent = (b * kThreads + tid) >> 5; ent < nent + np; ent += (G * kThreads) >> 5) {
+                    // the lane's CTA partials: all loads in flight first (G <= 160),
+                    // then summed in CTA order (the same order as a plain loop)
+                    double v[5];
+#pragma unroll
+                    for (int u = 0; u < 5; ++u) {
+                        const int c = lane + 32 * u;
+                        v[u] = c < G ? partials[(size_t)c * pstride + ent] : 0.0;
+                    }
                     double acc = 0.0;
-                    for (int c = lane; c < G; c += 32) acc += partials[(size_t)c * pstride + ent];
+#pragma unroll
+                    for (int u = 0; u < 5; ++u)
+                        if (lane + 32 * u < G) acc += v[u];
+                    for (int c = lane + 160; c < G; c += 32) acc += partials[(size_t)c * pstride + ent];
                     acc = warp_sum(acc);
                     if (lane == 0) {
                         if (ent < nent) {
@@ -805,7 +839,19 @@ __device__ void ba_window_body(const BAParams& a, bool batched) {
             double* s_res = at<double>(smem, L.flags);
             if (tid < 32) {
                 double q[4] = {0, 0, 0, 0};
-                for (int c = tid; c < G; c += 32) {
+                double v[5][4];  // loads first, then the sums in CTA order
+#pragma unroll
+                for (int r = 0; r < 5; ++r) {
+                    const int c = tid + 32 * r;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) v[r][u] = c < G ? partials[(size_t)c * pstride + nent + np + u] : 0.0;
+                }
+#pragma unroll
+                for (int r = 0; r < 5; ++r)
+                    if (tid + 32 * r < G)
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) q[u] += v[r][u];
+                for (int c = tid + 160; c < G; c += 32) {
                     const double* pt = partials + (size_t)c * pstride + nent + np;
 #pragma unroll
                     for (int u = 0; u < 4; ++u) q[u] += pt[u];
