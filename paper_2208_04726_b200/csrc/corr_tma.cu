@@ -190,6 +190,9 @@ __global__ void __launch_bounds__(kPrepThreads) corr_prep_kernel(CorrTmaParams a
     __shared__ int s_nrec, s_nzero, s_base;
     const int t = threadIdx.x;
     const int base = blockIdx.x * kPrepEdges;
+    // the correlation launch that follows is a programmatic dependent: its CTAs
+    // may set up as SMs free up and wait (griddepcontrol.wait) for this grid
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (t == 0) {
         s_nrec = 0;
         s_nzero = 0;
@@ -302,13 +305,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     __shared__ __align__(8) uint64_t hfull[kWarps];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // one global tile queue over the processing positions (target-frame order:
-    // the frames in flight stay in L2), then the extra sub-tiles
-    const int n_all = min(__ldcg(a.ctl), a.list_cap);
     if (tid < kWarps * kStages) mbar_init(&full[tid], 1);
     if (tid < kWarps) mbar_init(&hfull[tid], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // launched as a programmatic dependent of the preparation grid: its tile
+    // list, coordinates and zero fills are complete and visible after this
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
+    // one global tile list in processing order (target-frame sorted: the frames
+    // in flight stay in L2)
+    const int n_all = min(__ldcg(a.ctl), a.list_cap);
 
     // ================= per-warp pipeline =================
     unsigned char* wb = smem + warp * kWarpBytes;
@@ -587,7 +593,18 @@ cudaError_t launch_corr_tma(const CorrTmaParams& p, const CUtensorMap* maps, int
     const int grid = corr_tma_grid(p.n_edges, num_sms);
     if (p.list_cap < corr_tma_list_cap(p.n_edges) || !p.ctl) return cudaErrorInvalidValue;
     corr_prep_kernel<<<(p.n_edges + kPrepEdges - 1) / kPrepEdges, kPrepThreads, 0, stream>>>(p);
-    corr_tma_kernel<<<grid, kThreads, kSmemBytes, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], p);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    err = cudaLaunchKernelEx(&cfg, corr_tma_kernel, maps[0], maps[1], maps[2], maps[3], maps[4], p);
+    if (err != cudaSuccess) return err;
     return cudaGetLastError();
 }
 
