@@ -420,12 +420,10 @@ void ensure_p3(int p) {
 
 void compute_gram(pvo_ctx* ctx, const float* f0, float* g0, const float* f1, float* g1, int w0, int h0, int w1,
                   int h1, int C) {
-    if (w0 * h0 > 0) {
-        cuda_check(pvo_dev::launch_gram(f0, g0, w0, h0, C, ctx->num_sms, ctx->stream), "gram kernel");
-        ctx->launches += 1;
-    }
-    if (w1 * h1 > 0) {
-        cuda_check(pvo_dev::launch_gram(f1, g1, w1, h1, C, ctx->num_sms, ctx->stream), "gram kernel");
+    if (w0 * h0 + w1 * h1 > 0) {
+        cuda_check(pvo_dev::launch_gram(f0, g0, w0, h0, f1, g1, std::max(w1, 0), std::max(h1, 0), C, ctx->num_sms,
+                                        ctx->stream),
+                   "gram kernel");
         ctx->launches += 1;
     }
 }

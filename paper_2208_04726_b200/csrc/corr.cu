@@ -302,14 +302,25 @@ __global__ void __launch_bounds__(kThreads) corr_kernel(CorrParams a) {
     }  // item loop
 }
 
-// Gram terms of one pyramid level of one frame.  One warp per cell.
-__global__ void gram_kernel(const float* __restrict__ feat, float* __restrict__ gram, int W, int H, int D) {
-    const int Wp = gram_stride(W);
+// Gram terms of both pyramid levels of one frame in one launch (cells of level
+// 0, then of level 1).  One warp per cell.
+struct GramLevel {
+    const float* feat;
+    float* gram;
+    int W, H;
+};
+__global__ void gram_kernel(GramLevel l0, GramLevel l1, int D) {
     const int warps_per_block = blockDim.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int ncell = W * H;
-    for (int cell = blockIdx.x * warps_per_block + (threadIdx.x >> 5); cell < ncell;
-         cell += gridDim.x * warps_per_block) {
+    const int n0 = l0.W * l0.H, ncell = n0 + l1.W * l1.H;
+    for (int all = blockIdx.x * warps_per_block + (threadIdx.x >> 5); all < ncell;
+         all += gridDim.x * warps_per_block) {
+        const bool lv1 = all >= n0;
+        const GramLevel& L = lv1 ? l1 : l0;
+        const int cell = lv1 ? all - n0 : all;
+        const int W = L.W, H = L.H, Wp = gram_stride(W);
+        const float* feat = L.feat;
+        float* gram = L.gram;
         const int y = cell / W, x = cell - (cell / W) * W;
         const float* f = feat + (size_t)cell * D;
         const bool hr = x + 1 < W, hd = y + 1 < H;
@@ -317,6 +328,18 @@ __global__ void gram_kernel(const float* __restrict__ feat, float* __restrict__ 
         const float* fd = hd ? f + (size_t)W * D : nullptr;
         const float* fdr = (hr && hd) ? f + (size_t)(W + 1) * D : nullptr;
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
+        if (D == 128) {  // one 16-byte load per lane and neighbour, all in flight together
+            const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 v = reinterpret_cast<const float4*>(f)[lane];
+            const float4 r = hr ? reinterpret_cast<const float4*>(fr)[lane] : zero;
+            const float4 d = hd ? reinterpret_cast<const float4*>(fd)[lane] : zero;
+            const float4 dr = (hr && hd) ? reinterpret_cast<const float4*>(fdr)[lane] : zero;
+            s0 = fmaf(v.w, v.w, fmaf(v.z, v.z, fmaf(v.y, v.y, v.x * v.x)));
+            s1 = fmaf(v.w, r.w, fmaf(v.z, r.z, fmaf(v.y, r.y, v.x * r.x)));
+            s2 = fmaf(v.w, d.w, fmaf(v.z, d.z, fmaf(v.y, d.y, v.x * d.x)));
+            s3 = fmaf(v.w, dr.w, fmaf(v.z, dr.z, fmaf(v.y, dr.y, v.x * dr.x)));
+            s4 = fmaf(r.w, d.w, fmaf(r.z, d.z, fmaf(r.y, d.y, r.x * d.x)));
+        } else
         for (int c = lane; c < D; c += 32) {
             const float v = f[c];
             const float r = hr ? fr[c] : 0.f;
@@ -361,14 +384,15 @@ cudaError_t launch_corr(const CorrParams& p, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_gram(const float* feat, float* gram, int W, int H, int D, int num_sms, cudaStream_t stream) {
+cudaError_t launch_gram(const float* feat0, float* gram0, int W0, int H0, const float* feat1, float* gram1, int W1,
+                        int H1, int D, int num_sms, cudaStream_t stream) {
     const int threads = 256;
-    const int cells = W * H;
+    const int cells = W0 * H0 + W1 * H1;
+    if (cells <= 0) return cudaSuccess;
     int blocks = (cells + 7) / 8;
     const int cap = num_sms * 16;
     if (blocks > cap) blocks = cap;
-    if (blocks < 1) blocks = 1;
-    gram_kernel<<<blocks, threads, 0, stream>>>(feat, gram, W, H, D);
+    gram_kernel<<<blocks, threads, 0, stream>>>(GramLevel{feat0, gram0, W0, H0}, GramLevel{feat1, gram1, W1, H1}, D);
     return cudaGetLastError();
 }
 

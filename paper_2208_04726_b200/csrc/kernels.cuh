@@ -76,7 +76,9 @@ cudaError_t launch_corr_tma(const CorrTmaParams& p, const CUtensorMap* maps, int
 // Gram records of a level: planes [8][H][gram_stride(W)], rows padded to a 16-byte
 // multiple (TMA global strides must be 16-byte multiples); pad cells stay zero.
 __host__ __device__ inline int gram_stride(int W) { return (W + 3) & ~3; }
-cudaError_t launch_gram(const float* feat, float* gram, int W, int H, int D, int num_sms, cudaStream_t stream);
+// both levels of a frame in one launch (a level with W * H == 0 is skipped)
+cudaError_t launch_gram(const float* feat0, float* gram0, int W0, int H0, const float* feat1, float* gram1, int W1,
+                        int H1, int D, int num_sms, cudaStream_t stream);
 
 // Flow-provider measurement per edge (measure.cu): CorrelationFlowProvider::
 // measure + propose's per-edge part (flow_provider.cpp:150-312), FP64.
