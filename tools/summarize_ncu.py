@@ -46,10 +46,15 @@ M = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", 
      "smsp__inst_executed.sum", "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
      "sm__warps_active.avg.pct_of_peak_sustained_active", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
 lines = [f"# ncu summary ({tag})", "", "## Launch list (own kernels, `--metrics gpu__time_duration.sum`, cold/serialised)", "",
-         "| kernel | launches | mean us | share |", "|---|---|---|---|"]
+         "`bench.py` also times the flow provider's `propose` once per run (its `propose_ms` field): `measure_kernel`",
+         "is listed but is not part of the benchmark step (Gram + tile preparation + correlation + BA); the step",
+         "share column excludes it.", "",
+         "| kernel | launches | mean us | share | step share |", "|---|---|---|---|---|"]
 tot = sum(sum(v) for v in per.values())
+step_tot = sum(sum(v) for k, v in per.items() if k != "measure_kernel")
 for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
-    lines.append(f"| {k} | {len(v)} | {sum(v) / len(v) / 1000:.1f} | {100 * sum(v) / tot:.1f}% |")
+    ss = "—" if k == "measure_kernel" else f"{100 * sum(v) / step_tot:.1f}%"
+    lines.append(f"| {k} | {len(v)} | {sum(v) / len(v) / 1000:.1f} | {100 * sum(v) / tot:.1f}% | {ss} |")
 traffic = None
 names = sorted(f.name[len(tag) + 1:-len(".ncu-rep")] for f in src.glob(f"{tag}_*_full.ncu-rep"))
 traffic_by_cfg = {}
