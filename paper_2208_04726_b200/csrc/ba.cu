@@ -386,29 +386,34 @@ __device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Lay
         double* bvec = v + np;
         double* sc = at<double>(smem, L.scal) + warp * kScal;
         if (k < k1) {
+            // global inputs of the patch and of the lane's edge, all issued before
+            // the first shared-memory store (which would otherwise order them)
             const int eb = a.patch_edge_begin[k], ne = a.patch_edge_begin[k + 1] - eb;
             const int src = a.patch_src[k];
-            const int si = poses_frozen ? -1 : a.pose_free_slot[src];
             const int dslot = a.depth_slot[k];
             const double d = a.depth[k];
             const double* px = a.patch_x + 9 * (size_t)k;
             const double* py = a.patch_y + 9 * (size_t)k;
+            const bool has_edge = lane < ne;
+            const int e = eb + lane;
+            const int tgt = has_edge ? a.e_pose[e] : 0;
+            const double et0 = has_edge ? a.e_target[2 * e] : 0.0, et1 = has_edge ? a.e_target[2 * e + 1] : 0.0;
+            const double ew0 = has_edge ? a.e_weight[2 * e] : 0.0, ew1 = has_edge ? a.e_weight[2 * e + 1] : 0.0;
+            const double px4 = px[4], py4 = py[4];
+            const int si = poses_frozen ? -1 : a.pose_free_slot[src];
+            int sj = (has_edge && !poses_frozen) ? a.pose_free_slot[tgt] : -1;
             for (int i = lane; i < 2 * np; i += 32) v[i] = 0.0;
             double h = 0, bd = 0, vs[6] = {0, 0, 0, 0, 0, 0}, bs[6] = {0, 0, 0, 0, 0, 0};
-            int sj = -1;
             double wrs = 0, wrw = 0;
-            if (lane < ne) {
-                const int e = eb + lane;
-                const int tgt = a.e_pose[e];
-                sj = poses_frozen ? -1 : a.pose_free_slot[tgt];
+            if (has_edge) {
                 const SE3 pi = se3_load(poses + 7 * src);
                 const SE3 pj = se3_load(poses + 7 * tgt);
                 const Relative rel = rel_from_mats(mats + 12 * src, mats + 12 * tgt);
-                const CenterJac J = center_jacobians(rel, K, d, px[4], py[4]);
-                const double r0 = J.cu - a.e_target[2 * e], r1 = J.cv - a.e_target[2 * e + 1];
+                const CenterJac J = center_jacobians(rel, K, d, px4, py4);
+                const double r0 = J.cu - et0, r1 = J.cv - et1;
                 if (!isfinite(r0) || !isfinite(r1)) set_status(status, kDevNonFiniteResidual);
-                double w0 = J.behind ? 0.0 : a.e_weight[2 * e];
-                double w1 = J.behind ? 0.0 : a.e_weight[2 * e + 1];
+                double w0 = J.behind ? 0.0 : ew0;
+                double w1 = J.behind ? 0.0 : ew1;
                 const bool active = !(w0 == 0.0 && w1 == 0.0);  // bundle_adjust.cpp:151
                 if (!active) {
                     w0 = 0.0;
@@ -443,9 +448,9 @@ __device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Lay
                 double cu, cv;
                 bool behind;
                 center_behind(se3_equal(pi, pj), rel, K, px, py, d, &cu, &cv, &behind);
-                const double rx = cu - a.e_target[2 * e], ry = cv - a.e_target[2 * e + 1];
-                const double wx = behind ? 0.0 : a.e_weight[2 * e];
-                const double wy = behind ? 0.0 : a.e_weight[2 * e + 1];
+                const double rx = cu - et0, ry = cv - et1;
+                const double wx = behind ? 0.0 : ew0;
+                const double wy = behind ? 0.0 : ew1;
                 wrs = wx * rx * rx + wy * ry * ry;
                 wrw = wx + wy;
             }
