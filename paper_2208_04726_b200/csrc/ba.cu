@@ -76,6 +76,8 @@ struct Layout {
 };
 
 constexpr int kBlkL = 8;  // LDL^T block size (see ldlt_solve_cta)
+// per-warp ints: si, ne, depth slot, patch | p2e[kMaxFree] | nxt[kMaxEdges] | targets[kMaxFree], count
+constexpr int kWarpInts = 4 + kMaxFree + kMaxEdges + kMaxFree + 1;
 constexpr int kScal = 40;  // per-warp scalars: h, bd, inv_h, pad, then the 6x6 source block
 
 __host__ __device__ inline Layout make_layout(int np_full, int n_poses) {
@@ -110,7 +112,7 @@ __host__ __device__ inline Layout make_layout(int np_full, int n_poses) {
     L.wr = a;
     a += 8 * kWarps * 4;
     L.ints = a;
-    a += 4 * kWarps * (4 + kMaxFree + kMaxEdges);
+    a += 4 * kWarps * kWarpInts;
     int s = off;
     L.A = s;
     s += 8 * (np_full + 1) * (np_full + 1);  // + the rhs row
@@ -358,7 +360,7 @@ __device__ void phase_freeze(const BAParams& a, const double* poses, int k0, int
 
 // Per-warp int block: [0]=si [1]=ne [2]=dslot [3]=k, [4..4+16)=p2e, then next[32]
 __device__ inline int* warp_ints(unsigned char* smem, const Layout& L, int w) {
-    return at<int>(smem, L.ints) + w * (4 + kMaxFree + kMaxEdges);
+    return at<int>(smem, L.ints) + w * kWarpInts;
 }
 
 // ---------------------------------------------------------------------------
@@ -514,6 +516,11 @@ __device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Lay
                 }
             }
             if (lane == 0) {
+                int* tl = nxt + kMaxEdges;  // the free target poses with an edge chain
+                int ntl = 0;
+                for (int t = 0; t < kMaxFree; ++t)
+                    if (p2e[t] >= 0) tl[ntl++] = t;
+                tl[kMaxFree] = ntl;
                 wi[0] = si;
                 wi[1] = ne;
                 wi[2] = dslot;
@@ -533,48 +540,99 @@ __device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Lay
         if (a.phase_clocks && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0 && batch == k0) a.phase_clocks[15 * 8 + 0] = clock64();
 
         // ---- ordered accumulation of the batch into the CTA system ----
-        // entry-major: each thread keeps its entry in a register across the batch's
-        // patches (decoded once; the patches' independent lookups overlap), adding
-        // them in patch order exactly as a patch-major loop would
+        // (i) the patches' block terms, patch by patch in order: within a patch
+        // every entry of S is touched at most once (the (s,s) block, and per
+        // free target t with an edge chain the (s,t) and (t,t) blocks), so the
+        // whole CTA works on one patch at a time
         int nw = 0;
         while (nw < kWarps && warp_ints(smem, L, nw)[1] >= 0) ++nw;
-        for (int ent = tid; ent < nent; ent += kThreads) {
-            const unsigned ab = abt[ent];  // ia | ib << 8 | A << 16 | B << 24
-            const int ia = ab & 0xff, ib = (ab >> 8) & 0xff, A = (ab >> 16) & 0xff, B = ab >> 24;
-            const int ra = ia - 6 * A, rb = ib - 6 * B;
-            double sacc = S[ent];
-            for (int w = 0; w < nw; ++w) {
-                const int* wiw = warp_ints(smem, L, w);
-                const int si = wiw[0];
-                const bool dfree = wiw[2] >= 0;
-                const double* recw = at<double>(smem, L.rec) + (size_t)w * kMaxEdges * kRec;
-                const double* vw = at<double>(smem, L.vb) + (size_t)w * 2 * np;
-                const double* scw = at<double>(smem, L.scal) + w * kScal;
-                const int* p2e = wiw + 4;
-                const int* nxt = wiw + 4 + kMaxFree;
-                // one code path for every block pair (few divergent lanes): the
-                // edges of the (A, B) term are those targeting the non-source block
-                // (at most one per pose), read as Gs for the source side, Jt else
+        auto ut6 = [](int u, int& r, int& c) {  // u-th entry of a 6x6 upper triangle, row-major
+            r = 0;
+            while (u >= 6 - r) {
+                u -= 6 - r;
+                ++r;
+            }
+            c = r + u;
+        };
+        auto packed = [&](int i, int j) { return i * np - i * (i - 1) / 2 + (j - i); };  // i <= j
+        for (int w = 0; w < nw; ++w) {
+            const int* wiw = warp_ints(smem, L, w);
+            const int si = wiw[0];
+            const int* p2e = wiw + 4;
+            const int* nxt = p2e + kMaxFree;
+            const int* tl = nxt + kMaxEdges;
+            const int ntl = tl[kMaxFree];
+            const double* recw = at<double>(smem, L.rec) + (size_t)w * kMaxEdges * kRec;
+            const double* scw = at<double>(smem, L.scal) + w * kScal;
+            const int nss = si >= 0 ? 21 : 0, per_t = si >= 0 ? 57 : 21;
+            const int nitems = nss + ntl * per_t;
+            for (int it = tid; it < nitems; it += kThreads) {
+                int A, B, ra, rb;
                 double val = 0.0;
-                const bool sa = A == si, sb = B == si;
-                if (sa && sb) {
+                if (it < nss) {
+                    ut6(it, ra, rb);
+                    A = B = si;
                     val = scw[4 + 6 * ra + rb];
-                } else if (sa || sb || A == B) {
-                    const int oa = (sa ? kGs : kJt) + ra, ob = (sb ? kGs : kJt) + rb;
-                    int l = p2e[sa ? B : A];
-                    if (l >= 0) {  // the (patch, pose) edge; a chain only for repeated edges
+                } else {
+                    const int j = it - nss, t = tl[j / per_t], r = j - (j / per_t) * per_t;
+                    int oa, ob;
+                    if (si >= 0 && r < 36) {  // (s, t): Gs on the source side, Jt on the target side
+                        ra = r / 6;
+                        rb = r - 6 * ra;
+                        A = si < t ? si : t;
+                        B = si < t ? t : si;
+                        oa = (si < t ? kGs : kJt) + ra;
+                        ob = (si < t ? kJt : kGs) + rb;
+                    } else {  // (t, t)
+                        ut6(si >= 0 ? r - 36 : r, ra, rb);
+                        A = B = t;
+                        oa = kJt + ra;
+                        ob = kJt + rb;
+                    }
+                    for (int l = p2e[t]; l >= 0; l = nxt[l]) {  // one edge unless an edge repeats
                         const double* R = recw + l * kRec;
-                        val = (R[oa] * R[kW]) * R[ob] + (R[oa + 6] * R[kW + 1]) * R[ob + 6];
-                        for (l = nxt[l]; l >= 0; l = nxt[l]) {
-                            const double* Rn = recw + l * kRec;
-                            val += (Rn[oa] * Rn[kW]) * Rn[ob] + (Rn[oa + 6] * Rn[kW + 1]) * Rn[ob + 6];
-                        }
+                        val += (R[oa] * R[kW]) * R[ob] + (R[oa + 6] * R[kW + 1]) * R[ob + 6];
                     }
                 }
-                if (dfree) val -= (vw[ia] * scw[2]) * vw[ib];
-                sacc += val;
+                S[packed(6 * A + ra, 6 * B + rb)] += val;
             }
-            S[ent] = sacc;
+            __syncthreads();
+        }
+        // (ii) the depth-Schur terms of all the batch's patches, S -= sum_w (v_w / h_w) v_w^T,
+        // on 4x4 register tiles of the upper triangle
+        {
+            const int nt4 = (np + 3) >> 2;
+            for (int t = tid; t < nt4 * (nt4 + 1) / 2; t += kThreads) {
+                int ti = 0, u = t;
+                while (u >= nt4 - ti) {
+                    u -= nt4 - ti;
+                    ++ti;
+                }
+                const int tj = ti + u, i0 = 4 * ti, j0 = 4 * tj;
+                double acc[4][4] = {};
+                for (int w = 0; w < nw; ++w) {
+                    if (warp_ints(smem, L, w)[2] < 0) continue;  // depth fixed: no Schur term
+                    const double* vw = at<double>(smem, L.vb) + (size_t)w * 2 * np;
+                    const double hinv = at<double>(smem, L.scal)[w * kScal + 2];
+                    double vi[4], vj[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        vi[q] = i0 + q < np ? vw[i0 + q] * hinv : 0.0;
+                        vj[q] = j0 + q < np ? vw[j0 + q] : 0.0;
+                    }
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) acc[r][c] += vi[r] * vj[c];
+                }
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int i = i0 + r, j = j0 + c;
+                        if (i < np && j < np && i <= j) S[packed(i, j)] -= acc[r][c];
+                    }
+            }
         }
         for (int i = tid; i < np; i += kThreads) {
             double racc = rhs[i];
