@@ -177,7 +177,19 @@ struct pvo_ctx {
     bool timing_pending = false;
     bool tracing = false;  // record BA phase clocks (pvo_ctx_set_tracing)
     std::mt19937_64 oracle_rng{0};  // the oracle provider's RNG (flow_provider.cpp:10, rng_(noise.seed))
-    int* d_corr_ctl = nullptr;      // correlation tile queue: [extra count, queue head, warps done, -]
+    int* d_corr_ctl = nullptr;      // correlation tile queue: [list length, queue head, warps done, -]
+    void* h_stage = nullptr;        // page-locked staging for small read-backs (async copies, one sync)
+    size_t h_stage_cap = 0;
+    void* stage(size_t bytes) {
+        if (bytes > h_stage_cap) {
+            if (h_stage) cudaFreeHost(h_stage);
+            h_stage = nullptr;
+            h_stage_cap = 0;
+            cuda_check(cudaMallocHost(&h_stage, bytes), "cudaMallocHost");
+            h_stage_cap = bytes;
+        }
+        return h_stage;
+    }
 };
 
 namespace {
@@ -293,14 +305,21 @@ pvo_dev::BAParams stage_problem(pvo_ctx* ctx, const HostProblem& pr, const Plan&
     a.n_edges = pr.n_edges;
     a.n_free_poses = pl.n_free_poses;
     a.n_free_depths = pl.n_free_depths;
+    // the plan's host vectors go through the context's page-locked staging (async
+    // copies; every caller synchronises before it returns)
+    const size_t nfs = pl.free_slot.size(), nds = pl.depth_slot.size(), neb = pl.edge_begin.size();
+    int* stg = static_cast<int*>(ctx->stage(sizeof(int) * (nfs + nds + neb)));
+    std::memcpy(stg, pl.free_slot.data(), sizeof(int) * nfs);
+    std::memcpy(stg + nfs, pl.depth_slot.data(), sizeof(int) * nds);
+    std::memcpy(stg + nfs + nds, pl.edge_begin.data(), sizeof(int) * neb);
     a.poses = upload(ctx, B.poses, pr.poses, (size_t)pr.n_poses * 7);
-    a.pose_free_slot = upload(ctx, B.free_slot, pl.free_slot.data(), pl.free_slot.size());
+    a.pose_free_slot = upload(ctx, B.free_slot, static_cast<const int*>(stg), nfs);
     a.patch_src = upload(ctx, B.patch_src, pr.src, pr.n_patches);
     a.patch_x = upload(ctx, B.px, pr.px, (size_t)pr.n_patches * pp);
     a.patch_y = upload(ctx, B.py, pr.py, (size_t)pr.n_patches * pp);
     a.depth = upload(ctx, B.depth, pr.depth, pr.n_patches);
-    a.depth_slot = upload(ctx, B.depth_slot, pl.depth_slot.data(), pl.depth_slot.size());
-    a.patch_edge_begin = upload(ctx, B.edge_begin, pl.edge_begin.data(), pl.edge_begin.size());
+    a.depth_slot = upload(ctx, B.depth_slot, static_cast<const int*>(stg + nfs), nds);
+    a.patch_edge_begin = upload(ctx, B.edge_begin, static_cast<const int*>(stg + nfs + nds), neb);
     if (pl.sorted) {
         a.e_patch = upload(ctx, B.e_patch, pr.e_patch, pr.n_edges);
         a.e_pose = upload(ctx, B.e_pose, pr.e_pose, pr.n_edges);
@@ -672,6 +691,7 @@ int pvo_ctx_destroy(pvo_ctx* ctx) {
         ctx->bat.release();
         if (ctx->d_status) cudaFree(ctx->d_status);
         if (ctx->d_corr_ctl) cudaFree(ctx->d_corr_ctl);
+        if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
         for (auto& e : ctx->ev)
             if (e) cudaEventDestroy(e);
         if (ctx->copy_stream) {
@@ -1085,6 +1105,11 @@ int pvo_window_load(pvo_ctx* ctx, int n_poses, const double* poses, const uint8_
         for (int i = 0; i < n_poses; ++i)
             if (pose_slot[i] < 0 || pose_slot[i] >= ctx->nf) fail(PVO_OUT_OF_RANGE, "window_load: bad frame slot");
         Window& w = ctx->win;
+        // the inputs are valid: the resident window is replaced from here on (a
+        // failure below leaves no window loaded).  The patch descriptors (the bulk
+        // of the bytes) go first, so the transfer runs under the planning below.
+        w.loaded = false;
+        upload(ctx, w.patch_feats, patch_feats, (size_t)n_patches * 2 * 9 * ctx->C);
         w.plan = make_plan(pr, false);
         if (!w.plan.sorted) fail(PVO_INVALID_ARGUMENT, "window_load: edges must be grouped by patch (reference order)");
         w.shape = pr;
@@ -1099,7 +1124,6 @@ int pvo_window_load(pvo_ctx* ctx, int n_poses, const double* poses, const uint8_
             const std::vector<int> order = slot_order(n_edges, eslot.data());
             upload(ctx, w.order, order.data(), order.size());  // pageable source: staged before return
         }
-        upload(ctx, w.patch_feats, patch_feats, (size_t)n_patches * 2 * 9 * ctx->C);
         upload(ctx, w.init_poses, poses, (size_t)n_poses * 7);
         upload(ctx, w.init_depth, depth, n_patches);
         upload(ctx, ctx->ba.K, K, 4);
@@ -1256,18 +1280,26 @@ int pvo_window_read(pvo_ctx* ctx, double* poses, double* depth, double* residual
         bind(ctx);
         Window& w = ctx->win;
         if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
-        const int status = read_status(ctx);
+        // status, state and norms: async copies into page-locked staging, one sync
+        const size_t norms_cap = ctx->ba.norms.cap / sizeof(double);
+        const size_t np7 = (size_t)w.n_poses * 7, nd = w.n_patches;
+        double* st = static_cast<double*>(ctx->stage(sizeof(double) * (2 + np7 + nd + norms_cap)));
+        int* st_i = reinterpret_cast<int*>(st);  // [status, n_norms]
+        double* st_p = st + 2;
+        double* st_d = st_p + np7;
+        double* st_n = st_d + nd;
+        download(ctx, st_i, ctx->d_status, 1);
+        download(ctx, st_i + 1, static_cast<int*>(ctx->ba.n_norms.p), 1);
+        if (poses) download(ctx, st_p, static_cast<double*>(ctx->ba.poses.p), np7);
+        if (depth) download(ctx, st_d, static_cast<double*>(ctx->ba.depth.p), nd);
+        if (residual_norms && norms_cap) download(ctx, st_n, static_cast<double*>(ctx->ba.norms.p), norms_cap);
+        sync(ctx);
+        const int status = st_i[0], n = st_i[1];
         if (status & (1 << pvo_dev::kDevBadCoords)) fail(PVO_INVALID_ARGUMENT, "correlate: non-finite reprojection");
         raise_ba_status(status);
-        if (poses) download(ctx, poses, static_cast<double*>(ctx->ba.poses.p), (size_t)w.n_poses * 7);
-        if (depth) download(ctx, depth, static_cast<double*>(ctx->ba.depth.p), w.n_patches);
-        int n = 0;
-        download(ctx, &n, static_cast<int*>(ctx->ba.n_norms.p), 1);
-        sync(ctx);
-        if (residual_norms && n > 0) {
-            download(ctx, residual_norms, static_cast<double*>(ctx->ba.norms.p), n);
-            sync(ctx);
-        }
+        if (poses) std::memcpy(poses, st_p, sizeof(double) * np7);
+        if (depth) std::memcpy(depth, st_d, sizeof(double) * nd);
+        if (residual_norms && n > 0) std::memcpy(residual_norms, st_n, sizeof(double) * std::min<size_t>(n, norms_cap));
         if (n_norms) *n_norms = n;
     });
 }

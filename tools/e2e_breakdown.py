@@ -1,4 +1,4 @@
-"""Host-timed breakdown of one e2e step (bench.run_e2e) on config 2."""
+"""Host-timed breakdown of one e2e step (bench.run_e2e's calls, pinned host buffers) on config 2."""
 import sys
 import time
 from pathlib import Path
@@ -16,27 +16,26 @@ l0 = torch.from_numpy(w.level0[-1]).pin_memory()
 l1 = torch.from_numpy(w.level1[-1]).pin_memory()
 vol = torch.empty((E, 2, 9, 7, 7), dtype=torch.float32).pin_memory()
 vol_np = vol.numpy()
-acc = np.zeros(5)
-for it in range(25):
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
+hp = dict(prob)
+for k in ("poses", "fixed", "pose_frames", "patch_src", "patch_x", "patch_y", "depth", "patch_feats", "e_patch",
+          "e_pose", "e_delta", "e_weight"):
+    hp[k] = torch.from_numpy(np.ascontiguousarray(prob[k])).pin_memory().numpy()
+names = ["frames_upload", "window load", "iteration + volume D2H", "read"]
+acc = np.zeros(len(names))
+n = 40
+for it in range(n + 5):
+    t = [time.perf_counter()]
     ctx.frames_upload(F - 1, l0.numpy(), l1.numpy())
     ctx.synchronize()
-    t1 = time.perf_counter()
-    win.load(prob, prob["pose_frames"], prob["patch_feats"], w.K, w.image)
-    t2 = time.perf_counter()
-    win.iteration(2)
-    ctx.synchronize()
-    t3 = time.perf_counter()
-    win.correlate  # noqa: B018
-    ok = win.corr_device_ptr()
-    torch.cuda.synchronize()
-    t4 = time.perf_counter()
+    t.append(time.perf_counter())
+    win.load(hp, hp["pose_frames"], hp["patch_feats"], w.K, w.image)
+    t.append(time.perf_counter())
     win.iteration(2, corr_out=vol_np)
+    ctx.synchronize()
+    t.append(time.perf_counter())
     win.read()
-    t5 = time.perf_counter()
+    t.append(time.perf_counter())
     if it >= 5:
-        acc += [t1 - t0, t2 - t1, t3 - t2, t4 - t3, t5 - t4]
-acc /= 20
-print("ms: frame H2D %.3f | window load %.3f | iteration (device only) %.3f | - %.3f | iteration + vol D2H + read %.3f"
-      % tuple(acc * 1e3))
+        acc += np.diff(t)
+acc /= n
+print(" | ".join(f"{a}: {b * 1e3:.3f} ms" for a, b in zip(names, acc)), f"| total {acc.sum() * 1e3:.3f} ms")
