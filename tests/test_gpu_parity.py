@@ -903,3 +903,49 @@ def test_window_c2_full_size_sampled_parity_and_determinism(ctx):
     ref_ba = orc.ba_window(g.window_problem(w.cfg["window"]), w.K, iterations=2)
     dt, dq = pose_parity(p_dev, ref_ba["poses"])
     assert dt.max() <= 1e-3 and dq.max() <= 1e-3
+
+
+def test_graph_replay_equals_eager(ctx, c1_workload):
+    """The benchmark replays the step (Gram refresh + corr + 2 GN iterations)
+    from a captured CUDA graph: the replay must reproduce the eager launches
+    bit for bit (volume, poses, depths, residual norms)."""
+    import torch
+
+    w = c1_workload
+    F = w.cfg["frames"]
+    ctx.frames_reserve(F, w.level0.shape[2], w.level0.shape[1], w.level1.shape[2], w.level1.shape[1], 128)
+    for f in range(F):
+        ctx.frames_upload(f, w.level0[f], w.level1[f])
+    g = synth.build_graph(w, pvo.PatchGraph)
+    prob = synth.window_arrays(w, g.window_problem(w.cfg["window"]))
+    win = pvo.Window(ctx)
+    win.load(prob, prob["pose_frames"], prob["patch_feats"], w.K, w.image)
+    stream = torch.cuda.Stream()
+    ctx.set_stream(stream.cuda_stream)
+    vol = torch.empty((win.n_edges, 2, 9, 7, 7), dtype=torch.float32, device="cuda")
+    try:
+        def step():
+            ctx.frames_refresh(F - 1)
+            win.iteration(2, corr_device_ptr=vol.data_ptr())
+
+        with torch.cuda.stream(stream):
+            win.reset()
+            step()
+        torch.cuda.synchronize()
+        ref = (vol.cpu().numpy().copy(), *win.read())
+        graph = torch.cuda.CUDAGraph()
+        win.reset()
+        with torch.cuda.graph(graph, stream=stream, capture_error_mode="relaxed"):
+            step()
+        torch.cuda.synchronize()
+        vol.zero_()
+        with torch.cuda.stream(stream):
+            win.reset()
+            graph.replay()
+        torch.cuda.synchronize()
+        got = (vol.cpu().numpy(), *win.read())
+        assert np.array_equal(got[0], ref[0])
+        assert np.array_equal(got[1], ref[1]) and np.array_equal(got[2], ref[2])
+        assert np.array_equal(np.asarray(got[3]), np.asarray(ref[3]))
+    finally:
+        ctx.set_stream(None)
