@@ -162,7 +162,7 @@ struct pvo_ctx {
     DevBuf s0, s1, s2, s3, s4, s5, s6, s7, s8;
     // TMA descriptors of the frame store (feat0, feat1, gram0, gram1) and the
     // production correlation kernel's scratch
-    CUtensorMap maps[5];  // feat0, feat1, gram0, gram1, patch descriptors (per call)
+    CUtensorMap maps[7];  // feat0, feat1, gram0, gram1, patch descriptors (per call), feat0/feat1 8x8 boxes
     bool maps_ok = false;
     const void* patch_map_base = nullptr;
     int patch_map_rows = 0;
@@ -491,11 +491,13 @@ void encode_frame_maps(pvo_ctx* ctx) {
     const uint64_t f1[4] = {128, (uint64_t)ctx->w1, (uint64_t)ctx->h1, (uint64_t)ctx->nf};
     const uint64_t g0[4] = {(uint64_t)pvo_dev::gram_stride(ctx->w0), (uint64_t)ctx->h0, 8, (uint64_t)ctx->nf};
     const uint64_t g1[4] = {(uint64_t)pvo_dev::gram_stride(ctx->w1), (uint64_t)ctx->h1, 8, (uint64_t)ctx->nf};
-    const uint32_t fbox[4] = {16, 9, 9, 1}, gbox[4] = {12, 9, 5, 1};
+    const uint32_t fbox[4] = {16, 9, 9, 1}, gbox[4] = {12, 9, 5, 1}, nbox[4] = {16, 8, 8, 1};
     ctx->maps_ok = encode_map(&ctx->maps[0], 4, ctx->feat0.p, f0, fbox, CU_TENSOR_MAP_SWIZZLE_64B) &&
                    encode_map(&ctx->maps[1], 4, ctx->feat1.p, f1, fbox, CU_TENSOR_MAP_SWIZZLE_64B) &&
                    encode_map(&ctx->maps[2], 4, ctx->gram0.p, g0, gbox, CU_TENSOR_MAP_SWIZZLE_NONE) &&
-                   encode_map(&ctx->maps[3], 4, ctx->gram1.p, g1, gbox, CU_TENSOR_MAP_SWIZZLE_NONE);
+                   encode_map(&ctx->maps[3], 4, ctx->gram1.p, g1, gbox, CU_TENSOR_MAP_SWIZZLE_NONE) &&
+                   encode_map(&ctx->maps[5], 4, ctx->feat0.p, f0, nbox, CU_TENSOR_MAP_SWIZZLE_64B) &&
+                   encode_map(&ctx->maps[6], 4, ctx->feat1.p, f1, nbox, CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
 // Descriptor of the patch-descriptor array [P * 2 * 9][128] (cached per base).

@@ -76,6 +76,7 @@ constexpr int kGramBytes = 5 * kGramPlane * 4;          // 2160: [5][9][12]
 constexpr int kCoordBytes = kPix * 2 * 8;               // 144
 constexpr int kHeaderBytes = 2304;
 constexpr uint32_t kChunkTx = kChunkTileBytes + kChunkGBytes;
+constexpr uint32_t kChunkTxNarrow = 64 * kChunkCh * 4 + kChunkGBytes;  // narrow tiles: an 8x8 box
 constexpr uint32_t kHeaderTx = kGramBytes + kCoordBytes;
 constexpr int kHeaderOff = kStages * kStageBytes;        // the tile header (own barrier)
 constexpr int kDotsOff = kHeaderOff + kHeaderBytes;      // [9][81] f32
@@ -297,7 +298,8 @@ __global__ void __launch_bounds__(kPrepThreads) corr_prep_kernel(CorrTmaParams a
 __global__ void __launch_bounds__(kThreads, 1)
     corr_tma_kernel(const __grid_constant__ CUtensorMap feat0, const __grid_constant__ CUtensorMap feat1,
                     const __grid_constant__ CUtensorMap gram0, const __grid_constant__ CUtensorMap gram1,
-                    const __grid_constant__ CUtensorMap patch, CorrTmaParams a) {
+                    const __grid_constant__ CUtensorMap patch, const __grid_constant__ CUtensorMap feat0n,
+                    const __grid_constant__ CUtensorMap feat1n, CorrTmaParams a) {
     extern __shared__ unsigned char smem_raw[];
     // 1024-aligned base, derived by offset so the compiler keeps the shared address space
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -364,8 +366,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 rec[0] = ir0;
                 rec[1] = ir1;
             }
-            mbar_expect_tx(bar, kChunkTx);
-            tma_load_4d(st, level ? &feat1 : &feat0, ichunk * kChunkCh, ir0.x, ir0.y, ir0.w, bar);
+            const bool narrow = ir0.z & kNarrow;  // 8x8 box: the 64 cells the narrow variant reads
+            mbar_expect_tx(bar, narrow ? kChunkTxNarrow : kChunkTx);
+            tma_load_4d(st, narrow ? (level ? &feat1n : &feat0n) : (level ? &feat1 : &feat0), ichunk * kChunkCh,
+                        ir0.x, ir0.y, ir0.w, bar);
             tma_load_2d(st + kChunkGOff, &patch, ichunk * kChunkCh, ir1.x, bar);
         }
         if (ichunk == 0) ++hi;
@@ -399,11 +403,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     // of the 8x8 window at the box origin.  Results go to dots[p][box row].
     auto tile_dots = [&](auto nc_tag) {
         constexpr int NC = decltype(nc_tag)::value;
-        int roff[NC];
+        int roff[NC], soff[NC];  // dots index (9-wide box rows) x 64; stage row offset (8-wide when narrow)
 #pragma unroll
         for (int k = 0; k < NC; ++k) {
             const int r = NC == 3 ? lane + 27 * k : ((lane >> 3) + 4 * k) * kBox + (lane & 7);
+            const int rs = NC == 3 ? r : ((lane >> 3) + 4 * k) * 8 + (lane & 7);
             roff[k] = r * 64;
+            soff[k] = rs * 64;
         }
         // (even, odd)-channel sums per (cell, pixel): packed FP32x2 FMAs (FFMA2)
         float2 acc[NC][kPix];
@@ -425,8 +431,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int k = 0; k < NC; ++k) {
                     // 64B swizzle: 16-byte unit u of row r lives at unit u ^ ((r >> 1) & 3)
-                    const int sw = (roff[k] >> 7) & 3;
-                    v[k] = *reinterpret_cast<const float4*>(st + roff[k] + ((u ^ sw) << 4));
+                    const int sw = (soff[k] >> 7) & 3;
+                    v[k] = *reinterpret_cast<const float4*>(st + soff[k] + ((u ^ sw) << 4));
                 }
                 // pixel descriptors loaded as used (few live registers)
 #pragma unroll
@@ -443,8 +449,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float4 v[NC], gv[kPix];
 #pragma unroll
                 for (int k = 0; k < NC; ++k) {
-                    const int sw = (roff[k] >> 7) & 3;
-                    v[k] = *reinterpret_cast<const float4*>(st + roff[k] + ((u ^ sw) << 4));
+                    const int sw = (soff[k] >> 7) & 3;
+                    v[k] = *reinterpret_cast<const float4*>(st + soff[k] + ((u ^ sw) << 4));
                 }
 #pragma unroll
                 for (int p = 0; p < kPix; ++p) gv[p] = *reinterpret_cast<const float4*>(g + p * kChunkCh + 4 * u);
@@ -603,7 +609,7 @@ cudaError_t launch_corr_tma(const CorrTmaParams& p, const CUtensorMap* maps, int
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    err = cudaLaunchKernelEx(&cfg, corr_tma_kernel, maps[0], maps[1], maps[2], maps[3], maps[4], p);
+    err = cudaLaunchKernelEx(&cfg, corr_tma_kernel, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], p);
     if (err != cudaSuccess) return err;
     return cudaGetLastError();
 }

@@ -69,7 +69,7 @@ int corr_tma_smem_bytes();
 //   gram{0,1}: [slot][8 planes][H][gram_stride(W)] f32 (planes 0..4 used), box {12, 9, 5, 1}
 //   patch:     [P * 2 * 9][128] f32, box {16 ch, 9 rows}
 constexpr int kCorrMetaInts = 8;
-// maps: feat0, feat1, gram0, gram1, patch
+// maps: feat0, feat1, gram0, gram1, patch, feat0 / feat1 with an 8x8 box (narrow tiles)
 int corr_tma_grid(int n_edges, int num_sms);
 int corr_tma_list_cap(int n_edges);
 cudaError_t launch_corr_tma(const CorrTmaParams& p, const CUtensorMap* maps, int num_sms, cudaStream_t stream);
