@@ -299,19 +299,28 @@ def run_ours(args, rank, world, local_rank):
     # (same kernels, same arguments; the window is fixed, as within one frame of
     # the reference's loop): removes the host launch gaps between the kernels
     eager_step, graph, per_step_launches = step, None, 0
+    split_step = eager_step
     if not args.no_graph:
         try:
             win.reset()
             l0 = ctx.kernel_launches
+            # the timed graph carries no timing events (event nodes add device time)
+            ctx.set_timing(False)
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=stream, capture_error_mode="relaxed"):
                 eager_step()
             per_step_launches = ctx.kernel_launches - l0
+            ctx.set_timing(True)
+            # a second capture with the library's corr | BA events, for the split pass
+            split_graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(split_graph, stream=stream, capture_error_mode="relaxed"):
+                eager_step()
             torch.cuda.synchronize()
-            step = graph.replay
+            step, split_step = graph.replay, split_graph.replay
         except Exception as ex:  # capture unsupported here: time the eager launches
             print(f"bench: CUDA graph capture failed ({type(ex).__name__}: {ex}); eager steps", file=sys.stderr)
-            graph, step = None, eager_step
+            ctx.set_timing(True)
+            graph, step, split_step = None, eager_step, eager_step
             torch.cuda.synchronize()
         with torch.cuda.stream(stream):
             for _ in range(args.warmup):
@@ -345,13 +354,15 @@ def run_ours(args, rank, world, local_rank):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     mean_ms = float(np.mean(step_ms))
     # the step's split (correlation incl. tile preparation | BA) from the library's
-    # per-iteration events, read back after each of a few more flushed steps
+    # per-iteration events (captured into the graph as event nodes, so a replay
+    # records them with no host launch latency inside), read back after each of a
+    # few more flushed steps
     kt = []
     with torch.cuda.stream(stream):
         for i in range(min(args.steps, 50)):
             flush.zero_()
             win.reset()
-            eager_step()
+            split_step()
             kt.append(ctx.last_timing())
     corr_ms = float(np.mean([k[0] for k in kt]))
     ba_ms = float(np.mean([k[1] for k in kt]))

@@ -65,6 +65,9 @@ int64_t pvo_ctx_kernel_launches(pvo_ctx* ctx);
  * (per attempt, up to 16 attempts x 8 stamps: assemble start/end, reduce
  * start/end, solve start, update start/end, after the last barrier). */
 int pvo_ctx_set_tracing(pvo_ctx* ctx, int on);
+/* per-iteration timing events (pvo_ctx_last_timing), on by default; recorded as
+ * external event nodes under stream capture (a replayed graph records them) */
+int pvo_ctx_set_timing(pvo_ctx* ctx, int on);
 int pvo_ctx_ba_phase_cycles(pvo_ctx* ctx, long long* out128);
 /* Gauss-Newton attempts of the last BA run (divergence-guard retries included). */
 int pvo_ctx_ba_attempts(pvo_ctx* ctx, int* attempts);

@@ -38,6 +38,7 @@ SIGNATURES = {
     "pvo_ctx_last_timing": (i32, [vp, P, P]),
     "pvo_ctx_ba_attempts": (i32, [vp, P]),
     "pvo_ctx_set_tracing": (i32, [vp, i32]),
+    "pvo_ctx_set_timing": (i32, [vp, i32]),
     "pvo_ctx_ba_phase_cycles": (i32, [vp, P]),
     "pvo_se3_exp": (i32, [P, P]),
     "pvo_se3_log": (i32, [P, P]),

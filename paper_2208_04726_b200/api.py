@@ -120,6 +120,10 @@ class Context:
         check(lib.pvo_ctx_ba_attempts(self.handle, C.addressof(n)))
         return n.value
 
+    def set_timing(self, on: bool = True) -> None:
+        """Per-iteration timing events (last_timing); on by default."""
+        check(lib.pvo_ctx_set_timing(self.handle, int(bool(on))))
+
     def set_tracing(self, on: bool = True) -> None:
         check(lib.pvo_ctx_set_tracing(self.handle, int(bool(on))))
 

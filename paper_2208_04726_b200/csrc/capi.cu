@@ -176,6 +176,7 @@ struct pvo_ctx {
     cudaEvent_t ev_corr = nullptr, ev_copy = nullptr;
     bool timing_pending = false;
     bool tracing = false;  // record BA phase clocks (pvo_ctx_set_tracing)
+    bool timing = true;    // record the per-iteration timing events (pvo_ctx_set_timing)
     std::mt19937_64 oracle_rng{0};  // the oracle provider's RNG (flow_provider.cpp:10, rng_(noise.seed))
     int* d_corr_ctl = nullptr;      // correlation tile queue: [list length, queue head, warps done, -]
     void* h_stage = nullptr;        // page-locked staging for small read-backs (async copies, one sync)
@@ -210,6 +211,16 @@ void download(pvo_ctx* ctx, T* host, const T* dev, size_t count) {
     if (count) cuda_check(cudaMemcpyAsync(host, dev, count * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
 }
 void sync(pvo_ctx* ctx) { cuda_check(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize"); }
+// The per-iteration timing events (pvo_ctx_last_timing).  Under stream capture
+// they are recorded as external event nodes, so a graph replay records them too.
+void record_timing(pvo_ctx* ctx, int i) {
+    if (!ctx->timing) return;
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    cuda_check(cudaStreamIsCapturing(ctx->stream, &st), "cudaStreamIsCapturing");
+    cuda_check(cudaEventRecordWithFlags(ctx->ev[i], ctx->stream,
+                                        st == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0),
+               "event");
+}
 // Page-locked (or registered) host memory: an async copy from it is still in
 // flight when the call returns, so calls that read such caller buffers sync
 // before returning (pageable sources are staged by the copy itself).
@@ -733,6 +744,14 @@ int pvo_ctx_synchronize(pvo_ctx* ctx) {
 
 int64_t pvo_ctx_kernel_launches(pvo_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
+int pvo_ctx_set_timing(pvo_ctx* ctx, int on) {
+    return guarded([&] {
+        bind(ctx);
+        ctx->timing = on != 0;
+        if (!ctx->timing) ctx->timing_pending = false;
+    });
+}
+
 int pvo_ctx_set_tracing(pvo_ctx* ctx, int on) {
     return guarded([&] {
         bind(ctx);
@@ -1243,9 +1262,9 @@ int pvo_window_iteration(pvo_ctx* ctx, int iterations, double damping, float* co
         if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
         if (iterations < 0) fail(PVO_INVALID_ARGUMENT, "ba: negative iteration count");
         reset_status(ctx);
-        cuda_check(cudaEventRecord(ctx->ev[0], ctx->stream), "event");
+        record_timing(ctx, 0);
         run_corr(ctx, window_corr_params(ctx, corr_memspace == PVO_DEVICE ? corr_out : nullptr));
-        cuda_check(cudaEventRecord(ctx->ev[1], ctx->stream), "event");
+        record_timing(ctx, 1);
         const bool readback = corr_out && corr_memspace != PVO_DEVICE;
         if (readback) {  // the volume's D2H runs on the copy stream, under the BA kernels
             cuda_check(cudaEventRecord(ctx->ev_corr, ctx->stream), "event");
@@ -1257,8 +1276,8 @@ int pvo_window_iteration(pvo_ctx* ctx, int iterations, double damping, float* co
         }
         pvo_dev::BAParams a = window_ba_params(ctx, iterations, damping);
         launch_ba_checked(ctx, a, w.plan);
-        cuda_check(cudaEventRecord(ctx->ev[2], ctx->stream), "event");
-        ctx->timing_pending = true;
+        record_timing(ctx, 2);
+        ctx->timing_pending = ctx->timing;
         if (readback) cuda_check(cudaStreamWaitEvent(ctx->stream, ctx->ev_copy, 0), "stream wait");
     });
 }
@@ -1740,7 +1759,7 @@ int pvo_batch_iteration(pvo_ctx* ctx, int iterations, double damping, float* cor
         cuda_check(cudaMemsetAsync(B.status.p, 0, sizeof(int) * B.n_windows, ctx->stream), "memset");
         cuda_check(cudaMemsetAsync(B.status2.p, 0, sizeof(int) * 2 * B.n_windows, ctx->stream), "memset");
         cuda_check(cudaMemsetAsync(B.n_norms.p, 0, sizeof(int) * B.n_windows, ctx->stream), "memset");
-        cuda_check(cudaEventRecord(ctx->ev[0], ctx->stream), "event");
+        record_timing(ctx, 0);
         pvo_dev::CorrTmaParams cp;
         cp.n_edges = B.n_edges;
         cp.order = static_cast<const int*>(B.order.p);
@@ -1758,13 +1777,13 @@ int pvo_batch_iteration(pvo_ctx* ctx, int iterations, double damping, float* cor
         float* vol = corr_memspace == PVO_DEVICE && corr_out ? corr_out : static_cast<float*>(B.corr.p);
         cp.out = vol;
         run_corr(ctx, cp);
-        cuda_check(cudaEventRecord(ctx->ev[1], ctx->stream), "event");
+        record_timing(ctx, 1);
         cuda_check(pvo_dev::launch_ba_batch(static_cast<const pvo_dev::BAParams*>(B.params.p), B.n_windows,
                                             B.max_free, B.max_poses, ctx->stream),
                    "ba batch kernel");
         ctx->launches += 1;
-        cuda_check(cudaEventRecord(ctx->ev[2], ctx->stream), "event");
-        ctx->timing_pending = true;
+        record_timing(ctx, 2);
+        ctx->timing_pending = ctx->timing;
         if (corr_out && corr_memspace != PVO_DEVICE) download(ctx, corr_out, vol, (size_t)B.n_edges * 2 * 9 * 49);
     });
 }
