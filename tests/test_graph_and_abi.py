@@ -246,3 +246,43 @@ int main() {
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0, (out.returncode, out.stdout, out.stderr)
     assert out.stdout.startswith("ok 2 edges")
+
+
+def test_add_patches_grid_and_radius_one_connect():  # test_patch_graph.cpp:38-51, :63-76
+    rng = np.random.default_rng(2)
+    for g in _both():
+        g.add_frame(0.0, I7)
+        g.add_frame(0.1, I7)
+        c0 = rng.uniform(8, 248, (4, 2))
+        c1 = rng.uniform(8, 248, (4, 2))
+        g.add_patches(0, c0, [0.1] * 4)
+        g.add_patches(1, c1, [0.1] * 4)
+        g.connect(1)
+        kk, jj, _, _ = g.edges()
+        ids, src, d = g.patches()
+        src_of = {int(i): int(s) for i, s in zip(ids, src)}
+        assert len(kk) == 8 and len(set(int(k) for k in kk)) == 8  # one edge per patch
+        assert all(src_of[int(k)] == int(j) for k, j in zip(kk, jj))  # ... onto its source frame
+        assert np.all(d == 0.1)  # one shared inverse depth per patch grid
+
+
+def test_removing_a_middle_frame_keeps_the_graph_consistent():  # test_patch_graph.cpp:110-140 (graph part)
+    rng = np.random.default_rng(4)
+    a, b = _both()
+    for f in range(5):
+        pose = random_pose(rng, 0.2, 0.2)
+        c = rng.uniform(8, 248, (3, 2))
+        for g in (a, b):
+            g.add_frame(0.1 * f, pose)
+            g.add_patches(f, c, [0.2] * 3)
+            g.connect(3)
+    for g in (a, b):
+        g.remove_frame(1)
+        idx, _ = g.frames()
+        assert 1 not in set(int(i) for i in idx)
+        kk, jj, _, _ = g.edges()
+        ids, src, _ = g.patches()
+        assert 1 not in set(int(j) for j in jj) and 1 not in set(int(s) for s in src)
+        assert set(int(k) for k in kk) <= set(int(i) for i in ids)
+        assert set(int(j) for j in jj) <= set(int(i) for i in idx)
+    _same_edges(a, b)

@@ -713,3 +713,24 @@ def test_oracle_noise_statistics():  # flow_provider.cpp:56-66: N(0, sigma^2) pe
     again, _ = orc.oracle_propose(prob, gtp, gtd, w.K, flow_sigma=sigma, seed=11)
     other, _ = orc.oracle_propose(prob, gtp, gtd, w.K, flow_sigma=sigma, seed=12)
     assert np.array_equal(delta, again) and not np.array_equal(delta, other)
+
+
+def test_extra_consistent_anchor_leaves_minimizer_unchanged():  # test_bundle_adjust.cpp:334-367
+    """Two fixed poses with a baseline pin the gauge (scale included): fixing a
+    third, consistent pose (window 5 instead of 6 of 8 frames) must not move the
+    minimizer of optimize_window(4 iterations)."""
+    def solve(window):
+        w, g, _ = _gt_graph(103, 8, 48, 8, (5, 1e-3), window)  # frames 3..7 perturbed
+        g.optimize_window(window=window, iterations=4)
+        return g.frames()[1]
+
+    two, three = solve(6), solve(5)
+    for a, b in zip(two, three):
+        d, ang = orc.pose_distance(a, b)
+        assert d < 1e-6 and ang < 1e-6
+
+
+def test_damping_constant():  # test_bundle_adjust.cpp:130-133
+    from paper_2208_04726_b200 import api
+
+    assert api.kDefaultDamping == 1e-4 and api.BAProblem.__dataclass_fields__["damping"].default == 1e-4
