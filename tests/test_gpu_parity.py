@@ -949,3 +949,19 @@ def test_graph_replay_equals_eager(ctx, c1_workload):
         assert np.array_equal(np.asarray(got[3]), np.asarray(ref[3]))
     finally:
         ctx.set_stream(None)
+
+
+def test_extra_consistent_anchor_on_the_device(ctx):  # test_bundle_adjust.cpp:334-367
+    """The consistent-anchor property through the product graph and the device
+    BA (optimize_window, 4 iterations): window 5 vs 6 of 8 frames, same minimizer."""
+    from tests.test_oracle_pins import _gt_graph
+
+    def solve(window):
+        w, g, _ = _gt_graph(103, 8, 48, 8, (5, 1e-3), window, graph_cls=pvo.PatchGraph)
+        pvo.optimize_window(g, pvo.WindowOptions(window=window, iterations=4), ctx=ctx)
+        return g.frames()[1]
+
+    two, three = solve(6), solve(5)
+    for a, b in zip(two, three):
+        d, ang = orc.pose_distance(a, b)
+        assert d < 1e-6 and ang < 1e-6

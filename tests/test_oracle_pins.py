@@ -441,7 +441,7 @@ def test_behind_camera_edges_not_fatal():  # test_bundle_adjust.cpp:408-417
     g.optimize_window(window=3)
 
 
-def _gt_graph(seed, frames, patches, radius, noise, window, weight=0.9):
+def _gt_graph(seed, frames, patches, radius, noise, window, weight=0.9, graph_cls=None):
     """graph_at_ground_truth + set_oracle_revisions analogue on a synth workload
     (sim_fixtures.hpp:13-85): exact GT-pointing deltas, uniform weight."""
     from paper_2208_04726_b200 import synth
@@ -449,7 +449,7 @@ def _gt_graph(seed, frames, patches, radius, noise, window, weight=0.9):
     w = synth.generate("c1", seed=seed, features=False, frames=frames, patches=patches)
     w.cfg["radius"] = radius
     w.cfg["window"] = window
-    g = orc.PatchGraph(w.K, w.image[0], w.image[1])
+    g = (graph_cls or orc.PatchGraph)(w.K, w.image[0], w.image[1])
     rng = np.random.default_rng(seed)
     for f in range(frames):
         g.add_frame(0.05 * f, w.gt_poses[f])
