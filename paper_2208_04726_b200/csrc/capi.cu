@@ -119,6 +119,11 @@ struct Window {
     Plan plan;
     HostProblem shape;  // sizes, K, image size (pointers unused)
     DevBuf pose_slot, patch_feats, corr, init_poses, init_depth, order, flags;
+    // host-loaded windows: the processing order of each half of the edge range
+    // (edges [0, half) then [half, E)), so a host read-back of the volume can
+    // start on the first half while the second is correlated (0: no split)
+    DevBuf order_half;
+    int half = 0;
 };
 
 // Batch of independent windows (config 5: many sequences per device).  All
@@ -173,7 +178,7 @@ struct pvo_ctx {
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     // copy stream: device->host read-back of the correlation volume overlaps the BA kernels
     cudaStream_t copy_stream = nullptr;
-    cudaEvent_t ev_corr = nullptr, ev_copy = nullptr;
+    cudaEvent_t ev_corr = nullptr, ev_copy = nullptr, ev_corr2 = nullptr;
     bool timing_pending = false;
     bool tracing = false;  // record BA phase clocks (pvo_ctx_set_tracing)
     bool timing = true;    // record the per-iteration timing events (pvo_ctx_set_timing)
@@ -527,14 +532,14 @@ bool encode_patch_map(pvo_ctx* ctx, const float* base, int n_patches) {
 // Correlation of a batch of edges against the frame store: the TMA kernel for
 // D = 128 (it splits wide tiles into sub-tiles itself), or the generic kernel
 // for other channel counts.  `t` carries the inputs; scratch is filled in here.
-void run_corr(pvo_ctx* ctx, pvo_dev::CorrTmaParams t) {
+void run_corr(pvo_ctx* ctx, pvo_dev::CorrTmaParams t, int index_edges = 0) {
     if (t.n_edges <= 0) return;
     if (ctx->maps_ok && encode_patch_map(ctx, t.patch_feats, t.n_patches)) {
         t.w0 = ctx->w0;
         t.h0 = ctx->h0;
         t.w1 = ctx->w1;
         t.h1 = ctx->h1;
-        t.coords = ctx->c_coords.as<double>((size_t)t.n_edges * 18);
+        t.coords = ctx->c_coords.as<double>((size_t)std::max(t.n_edges, index_edges) * 18);  // indexed by edge
         t.list_cap = pvo_dev::corr_tma_list_cap(t.n_edges);
         t.meta = ctx->c_meta.as<int>((size_t)t.list_cap * pvo_dev::kCorrMetaInts);
         t.ctl = ctx->d_corr_ctl;
@@ -684,6 +689,7 @@ int pvo_ctx_create(int device, pvo_ctx** out) {
         for (auto& e : ctx->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
         cuda_check(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
         cuda_check(cudaEventCreateWithFlags(&ctx->ev_corr, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventCreateWithFlags(&ctx->ev_corr2, cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming), "cudaEventCreate");
         *out = ctx;
     });
@@ -712,6 +718,7 @@ int pvo_ctx_destroy(pvo_ctx* ctx) {
             cudaStreamDestroy(ctx->copy_stream);
         }
         if (ctx->ev_corr) cudaEventDestroy(ctx->ev_corr);
+        if (ctx->ev_corr2) cudaEventDestroy(ctx->ev_corr2);
         if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
         if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
         delete ctx;
@@ -1144,6 +1151,13 @@ int pvo_window_load(pvo_ctx* ctx, int n_poses, const double* poses, const uint8_
             for (int e = 0; e < n_edges; ++e) eslot[e] = pose_slot[e_pose[e]];
             const std::vector<int> order = slot_order(n_edges, eslot.data());
             upload(ctx, w.order, order.data(), order.size());  // pageable source: staged before return
+            w.half = n_edges >= 4096 ? n_edges / 2 : 0;
+            if (w.half) {
+                std::vector<int> oh = slot_order(w.half, eslot.data());
+                const std::vector<int> o2 = slot_order(n_edges - w.half, eslot.data() + w.half);
+                for (int v : o2) oh.push_back(v + w.half);
+                upload(ctx, w.order_half, oh.data(), oh.size());
+            }
         }
         upload(ctx, w.init_poses, poses, (size_t)n_poses * 7);
         upload(ctx, w.init_depth, depth, n_patches);
@@ -1263,10 +1277,38 @@ int pvo_window_iteration(pvo_ctx* ctx, int iterations, double damping, float* co
         if (iterations < 0) fail(PVO_INVALID_ARGUMENT, "ba: negative iteration count");
         reset_status(ctx);
         record_timing(ctx, 0);
-        run_corr(ctx, window_corr_params(ctx, corr_memspace == PVO_DEVICE ? corr_out : nullptr));
-        record_timing(ctx, 1);
         const bool readback = corr_out && corr_memspace != PVO_DEVICE;
-        if (readback) {  // the volume's D2H runs on the copy stream, under the BA kernels
+        const size_t vol_edge = (size_t)2 * 9 * 49;
+        if (readback && w.half > 0 && ctx->maps_ok) {
+            // two launches over the halves of the edge range: the first half's
+            // read-back runs on the copy stream while the second is correlated
+            const int* oh = static_cast<const int*>(w.order_half.p);
+            pvo_dev::CorrTmaParams c1 = window_corr_params(ctx, nullptr), c2 = c1;
+            c1.n_edges = w.half;
+            c1.order = oh;
+            c2.n_edges = w.n_edges - w.half;
+            c2.order = oh + w.half;
+            run_corr(ctx, c1, w.n_edges);
+            cuda_check(cudaEventRecord(ctx->ev_corr, ctx->stream), "event");
+            run_corr(ctx, c2, w.n_edges);
+            record_timing(ctx, 1);
+            cuda_check(cudaEventRecord(ctx->ev_corr2, ctx->stream), "event");
+            float* vol = static_cast<float*>(w.corr.p);
+            cuda_check(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_corr, 0), "stream wait");
+            cuda_check(cudaMemcpyAsync(corr_out, vol, sizeof(float) * w.half * vol_edge, cudaMemcpyDeviceToHost,
+                                       ctx->copy_stream),
+                       "D2H");
+            cuda_check(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_corr2, 0), "stream wait");
+            cuda_check(cudaMemcpyAsync(corr_out + (size_t)w.half * vol_edge, vol + (size_t)w.half * vol_edge,
+                                       sizeof(float) * (size_t)(w.n_edges - w.half) * vol_edge, cudaMemcpyDeviceToHost,
+                                       ctx->copy_stream),
+                       "D2H");
+            cuda_check(cudaEventRecord(ctx->ev_copy, ctx->copy_stream), "event");
+        } else {
+            run_corr(ctx, window_corr_params(ctx, corr_memspace == PVO_DEVICE ? corr_out : nullptr));
+            record_timing(ctx, 1);
+        }
+        if (readback && !(w.half > 0 && ctx->maps_ok)) {  // the volume's D2H runs on the copy stream, under BA
             cuda_check(cudaEventRecord(ctx->ev_corr, ctx->stream), "event");
             cuda_check(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_corr, 0), "stream wait");
             cuda_check(cudaMemcpyAsync(corr_out, w.corr.p, sizeof(float) * (size_t)w.n_edges * 2 * 9 * 49,
@@ -2273,6 +2315,7 @@ int pvo_window_load_dgraph(pvo_ctx* ctx, pvo_dgraph* g, int window, int all_acti
             fail(PVO_INVALID_ARGUMENT, "window_load_dgraph: descriptor channels differ from the frame store");
         Window& w = ctx->win;
         w.loaded = false;
+        w.half = 0;  // the processing order is built on the device: no split read-back
         const int F = static_cast<int>(g->f_index.size()), P = g->P;
         const int window_start = std::max(F - window, 0), first_free = std::max(F - window, 1);
         pvo_dev::DGraphView v = g->view(g->cur);
