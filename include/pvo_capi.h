@@ -176,6 +176,9 @@ int pvo_window_iteration(pvo_ctx* ctx, int iterations, double damping, float* co
 int pvo_window_correlate(pvo_ctx* ctx, float* corr_out, int memspace);
 /* optimize_window's iterations only (no correlation pass): propose -> BA. */
 int pvo_window_ba(pvo_ctx* ctx, int iterations, double damping);
+/* residual_norms must hold iterations + 2 doubles of the last call; iteration
+ * counts above PVO_MAX_WINDOW_ITERATIONS are rejected (INVALID_ARGUMENT). */
+#define PVO_MAX_WINDOW_ITERATIONS 128
 int pvo_window_read(pvo_ctx* ctx, double* poses, double* inv_depth, double* residual_norms, int* n_norms);
 /* Device pointer of the window's correlation volume buffer [E][2][pp][49]. */
 int pvo_window_corr_ptr(pvo_ctx* ctx, float** corr);

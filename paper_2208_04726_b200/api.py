@@ -79,6 +79,21 @@ def _ptr(a: Optional[np.ndarray]):
     return None if a is None else a.ctypes
 
 
+# pvo_capi.h PVO_MAX_WINDOW_ITERATIONS: the window path's norms hold iterations + 2
+MAX_WINDOW_ITERATIONS = 128
+
+
+def _check_corr_out(corr_out, n_edges: int) -> None:
+    """A host volume the C side DMAs n_edges * 2 * 9 * 49 floats into."""
+    if corr_out is None:
+        return
+    if not isinstance(corr_out, np.ndarray) or corr_out.dtype != np.float32 or not corr_out.flags.c_contiguous \
+            or not corr_out.flags.writeable:
+        raise ValueError("corr_out: need a writeable C-contiguous float32 array")
+    if corr_out.size < n_edges * 2 * 9 * 49:
+        raise ValueError(f"corr_out: {corr_out.size} floats < {n_edges} edges x 882")
+
+
 # ---------------------------------------------------------------------------
 # context
 # ---------------------------------------------------------------------------
@@ -655,6 +670,7 @@ class Window:
 
     def iteration(self, iterations: int = 2, damping: float = kDefaultDamping, corr_out=None,
                   corr_device_ptr: int | None = None) -> None:
+        _check_corr_out(corr_out, self.n_edges)
         if corr_device_ptr is not None:
             check(lib.pvo_window_iteration(self.ctx.handle, iterations, damping, corr_device_ptr, _capi.PVO_DEVICE))
         elif corr_out is not None:
@@ -673,7 +689,7 @@ class Window:
 
     def read(self):
         poses, d = np.empty((self.n_poses, 7)), np.empty(self.n_patches)
-        norms = np.empty(130)
+        norms = np.empty(MAX_WINDOW_ITERATIONS + 2)
         nn = C.c_int()
         check(lib.pvo_window_read(self.ctx.handle, _ptr(poses), _ptr(d), _ptr(norms), C.addressof(nn)))
         return poses, d, list(norms[: nn.value])
@@ -738,6 +754,7 @@ class Batch:
         check(lib.pvo_batch_reset(self.ctx.handle))
 
     def iteration(self, iterations: int = 2, damping: float = kDefaultDamping, corr_out=None) -> None:
+        _check_corr_out(corr_out, self.n_edges)
         if corr_out is not None:
             check(lib.pvo_batch_iteration(self.ctx.handle, iterations, damping, _ptr(corr_out), _capi.PVO_HOST))
         else:

@@ -703,7 +703,7 @@ int pvo_ctx_destroy(pvo_ctx* ctx) {
         DevBuf* bufs[] = {&ctx->feat0, &ctx->feat1, &ctx->gram0, &ctx->gram1, &ctx->s0, &ctx->s1, &ctx->s2,
                           &ctx->s3,    &ctx->s4,    &ctx->s5,    &ctx->s6,    &ctx->s7, &ctx->s8,
                           &ctx->win.pose_slot, &ctx->win.patch_feats, &ctx->win.corr, &ctx->win.init_poses,
-                          &ctx->win.init_depth, &ctx->win.order, &ctx->win.flags, &ctx->c_coords, &ctx->c_meta,
+                          &ctx->win.init_depth, &ctx->win.order, &ctx->win.order_half, &ctx->win.flags, &ctx->c_coords, &ctx->c_meta,
                           &ctx->c_over, &ctx->c_order};
         for (DevBuf* b : bufs) b->release();
         ctx->ba.release();
@@ -1275,11 +1275,15 @@ int pvo_window_iteration(pvo_ctx* ctx, int iterations, double damping, float* co
         Window& w = ctx->win;
         if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
         if (iterations < 0) fail(PVO_INVALID_ARGUMENT, "ba: negative iteration count");
+        if (iterations > PVO_MAX_WINDOW_ITERATIONS) fail(PVO_INVALID_ARGUMENT, "ba: too many iterations");
         reset_status(ctx);
         record_timing(ctx, 0);
         const bool readback = corr_out && corr_memspace != PVO_DEVICE;
         const size_t vol_edge = (size_t)2 * 9 * 49;
-        if (readback && w.half > 0 && ctx->maps_ok) {
+        // the split needs the TMA path (the generic kernel has no edge order)
+        const bool split = readback && w.half > 0 && ctx->maps_ok &&
+                           encode_patch_map(ctx, static_cast<const float*>(w.patch_feats.p), w.n_patches);
+        if (split) {
             // two launches over the halves of the edge range: the first half's
             // read-back runs on the copy stream while the second is correlated
             const int* oh = static_cast<const int*>(w.order_half.p);
@@ -1308,7 +1312,7 @@ int pvo_window_iteration(pvo_ctx* ctx, int iterations, double damping, float* co
             run_corr(ctx, window_corr_params(ctx, corr_memspace == PVO_DEVICE ? corr_out : nullptr));
             record_timing(ctx, 1);
         }
-        if (readback && !(w.half > 0 && ctx->maps_ok)) {  // the volume's D2H runs on the copy stream, under BA
+        if (readback && !split) {  // the volume's D2H runs on the copy stream, under BA
             cuda_check(cudaEventRecord(ctx->ev_corr, ctx->stream), "event");
             cuda_check(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_corr, 0), "stream wait");
             cuda_check(cudaMemcpyAsync(corr_out, w.corr.p, sizeof(float) * (size_t)w.n_edges * 2 * 9 * 49,
@@ -1332,6 +1336,7 @@ int pvo_window_ba(pvo_ctx* ctx, int iterations, double damping) {
         Window& w = ctx->win;
         if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
         if (iterations < 0) fail(PVO_INVALID_ARGUMENT, "ba: negative iteration count");
+        if (iterations > PVO_MAX_WINDOW_ITERATIONS) fail(PVO_INVALID_ARGUMENT, "ba: too many iterations");
         reset_status(ctx);
         pvo_dev::BAParams a = window_ba_params(ctx, iterations, damping);
         launch_ba_checked(ctx, a, w.plan);
@@ -1362,7 +1367,8 @@ int pvo_window_read(pvo_ctx* ctx, double* poses, double* depth, double* residual
         raise_ba_status(status);
         if (poses) std::memcpy(poses, st_p, sizeof(double) * np7);
         if (depth) std::memcpy(depth, st_d, sizeof(double) * nd);
-        if (residual_norms && n > 0) std::memcpy(residual_norms, st_n, sizeof(double) * std::min<size_t>(n, norms_cap));
+        const size_t n_copy = std::min<size_t>(std::min<size_t>(n, norms_cap), PVO_MAX_WINDOW_ITERATIONS + 2);
+        if (residual_norms && n > 0) std::memcpy(residual_norms, st_n, sizeof(double) * n_copy);
         if (n_norms) *n_norms = n;
     });
 }
