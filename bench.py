@@ -131,7 +131,7 @@ def corr_bytes_per_edge(prob, K, level_shapes, D=128):
     level the union of in-bounds integer cells touched by the 3x3x7x7 bilinear
     taps x D x 4 B, + 2 x 9 x D x 4 B of patch features + 3,528 B of output."""
     import oracle.pyoracle as orc  # noqa: F401  (not used: coords come from the numpy generator)
-    from paper_2208_04726_b200 import synth
+    import pvo_synth as synth
 
     E = len(prob["e_patch"])
     total = 0.0
@@ -174,7 +174,7 @@ def setup(config: str, seed: int, device: int):
     import torch
 
     import paper_2208_04726_b200 as pvo
-    from paper_2208_04726_b200 import synth
+    import pvo_synth as synth
 
     w = synth.generate(config, seed=seed)
     g = synth.build_graph(w, pvo.PatchGraph)
@@ -199,7 +199,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     import oracle.pyoracle as orc
-    from paper_2208_04726_b200 import synth
+    import pvo_synth as synth
 
     # c5 (a batch of c2 sequences): the CPU path's per-edge cost is the c2 window's
     w = synth.generate("c2" if args.config == "c5" else args.config, seed=0)
@@ -251,7 +251,7 @@ def cpu_baseline(w, prob, sample_edges=600):
     """Oracle timed on the host: corr single-threaded on a bounded sample (the
     reference is single-threaded) + full optimize_window(2)."""
     import oracle.pyoracle as orc
-    from paper_2208_04726_b200 import synth
+    import pvo_synth as synth
 
     E = len(prob["e_patch"])
     sample = min(E, sample_edges)
@@ -446,7 +446,7 @@ def run_batch(args, rank, world, local_rank):
     import torch
 
     import paper_2208_04726_b200 as pvo
-    from paper_2208_04726_b200 import synth
+    import pvo_synth as synth
     from paper_2208_04726_b200.dist import gather_poses, max_over_ranks
 
     torch.cuda.set_device(local_rank)

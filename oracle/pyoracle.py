@@ -1,19 +1,25 @@
-"""ctypes binding of the CPU oracle (oracle/liboracle_pvo.so).
+"""ctypes binding of the CPU oracle.
 
 TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and the
-cpu-baseline leg of bench.py, never by the product package.  The oracle is the
-CPU restatement of the reference (oracle/pvo_oracle.cpp); the functions here
-mirror the product's Python API so parity tests read side by side.
+cpu-baseline leg of bench.py, never by the product package.  Two backends
+with one flat orc_* C surface: the reference's OWN sources compiled by
+oracle/ref_build.py (oracle/_ref/libpvo_ref.so, preferred when present) and
+the restatement oracle/pvo_oracle.cpp (always built; it covers the one entry
+the reference exposes only through its simulator, orc_oracle_propose).  The
+functions here mirror the product's Python API so parity tests read side by
+side.
 """
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
 
 HERE = Path(__file__).resolve().parent
-LIB_PATH = HERE / "liboracle_pvo.so"
+LIB_PATH = HERE / "liboracle_pvo.so"  # the restatement (oracle/pvo_oracle.cpp)
+REF_LIB_PATH = HERE / "_ref" / "libpvo_ref.so"  # the reference itself (oracle/ref_build.py)
 
 STATUS_EXC = {1: ValueError, 2: RuntimeError, 3: ArithmeticError, 4: IndexError, 5: RuntimeError}
 
@@ -25,10 +31,10 @@ class OracleDegenerate(RuntimeError):
 STATUS_EXC[2] = OracleDegenerate
 
 
-def _load():
-    if not LIB_PATH.exists():
-        raise OSError(f"{LIB_PATH} missing")
-    lib = C.CDLL(str(LIB_PATH))
+def _load(path: Path):
+    if not path.exists():
+        raise OSError(f"{path} missing")
+    lib = C.CDLL(str(path))
     lib.orc_last_error.restype = C.c_char_p
     lib.orc_graph_create.restype = C.c_void_p
     lib.orc_graph_create.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
@@ -38,13 +44,77 @@ def _load():
 
 
 try:
-    lib = _load()
+    lib_restated = _load(LIB_PATH)
 except Exception:  # pragma: no cover - build on demand from the repo root
     import subprocess
     import sys
 
     subprocess.run([sys.executable, str(HERE / "build.py")], check=True)
-    lib = _load()
+    lib_restated = _load(LIB_PATH)
+
+
+class _Dispatch:
+    """Each orc_* entry from the reference build when it exports it (every
+    entry but the simulator-bound orc_oracle_propose), else the restatement.
+    Error messages come from whichever library ran the last call."""
+
+    def __init__(self, ref, restated):
+        self._ref, self._restated, self._last = ref, restated, restated
+
+    def __getattr__(self, name):
+        if name == "orc_last_error":
+            return self._last.orc_last_error
+        try:
+            fn, src = getattr(self._ref, name), self._ref
+        except AttributeError:
+            fn, src = getattr(self._restated, name), self._restated
+
+        def call(*args):
+            self._last = src
+            return fn(*args)
+
+        call.restype = fn.restype
+        return call
+
+    def source(self, name: str) -> str:
+        try:
+            getattr(self._ref, name)
+            return "reference"
+        except AttributeError:
+            return "restatement"
+
+
+# PVO_ORACLE=restated|ref|auto (default auto: the reference build when present)
+_MODE = os.environ.get("PVO_ORACLE", "auto")
+lib_ref = None
+if _MODE in ("auto", "ref") and REF_LIB_PATH.exists():
+    lib_ref = _load(REF_LIB_PATH)
+elif _MODE == "ref":
+    raise OSError(f"PVO_ORACLE=ref but {REF_LIB_PATH} is missing (python oracle/ref_build.py)")
+lib = _Dispatch(lib_ref, lib_restated) if lib_ref is not None else lib_restated
+BACKEND = "reference (oracle/_ref/libpvo_ref.so)" if lib_ref is not None else "restatement (oracle/liboracle_pvo.so)"
+
+
+class using:
+    """with using("restated"|"reference"): run the oracle calls on one backend."""
+
+    def __init__(self, which: str):
+        if which not in ("restated", "reference"):
+            raise ValueError(which)
+        if which == "reference" and lib_ref is None:
+            raise OSError(f"{REF_LIB_PATH} missing (python oracle/ref_build.py)")
+        self.which = which
+
+    def __enter__(self):
+        global lib
+        self._saved = lib
+        lib = lib_restated if self.which == "restated" else _Dispatch(lib_ref, lib_restated)
+        return self
+
+    def __exit__(self, *exc):
+        global lib
+        lib = self._saved
+        return False
 
 
 def check(status: int) -> None:

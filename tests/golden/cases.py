@@ -15,7 +15,7 @@ import hashlib
 
 import numpy as np
 
-from paper_2208_04726_b200 import synth
+import pvo_synth as synth
 
 
 def digest(*arrays) -> str:

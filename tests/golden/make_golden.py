@@ -1,4 +1,9 @@
-"""Regenerate tests/golden/golden_v1.npz from the CPU restatement (see cases.py).
+"""Regenerate the golden fixtures (see cases.py):
+
+* golden_ref_v1.npz - outputs of the REFERENCE's own code (oracle/_ref,
+  built from /root/reference/proj/src by oracle/ref_build.py): the golden
+  vectors the GPU suite checks the product against;
+* golden_v1.npz     - the same cases through the restatement (oracle drift check).
 
     python tests/golden/make_golden.py
 """
@@ -37,6 +42,10 @@ def build() -> dict:
 
 
 if __name__ == "__main__":
-    path = Path(__file__).resolve().parent / "golden_v1.npz"
-    np.savez_compressed(path, **build())
-    print(path, path.stat().st_size, "bytes")
+    here = Path(__file__).resolve().parent
+    with orc.using("restated"):
+        np.savez_compressed(here / "golden_v1.npz", **build())
+    with orc.using("reference"):
+        np.savez_compressed(here / "golden_ref_v1.npz", **build())
+    for name in ("golden_v1.npz", "golden_ref_v1.npz"):
+        print(here / name, (here / name).stat().st_size, "bytes")

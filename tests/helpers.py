@@ -33,6 +33,6 @@ def pose_parity(a, b):
 
 def smooth_features(rng, H, W, D):
     """Blurred, unit-norm random feature grid (the synth generator's recipe)."""
-    from paper_2208_04726_b200 import synth
+    import pvo_synth as synth
 
     return synth.make_level0(rng, 1, H, W, D)[0]

@@ -1,7 +1,10 @@
-"""Golden regression fixtures (tests/golden/): the CPU restatement must reproduce
-them bit for bit (CPU suite), and the B200 path must match them within the
-parity tolerances without the oracle in the loop (GPU suite).  See
-tests/golden/cases.py for what the fixtures are and are not."""
+"""Golden fixtures (tests/golden/).  golden_ref_v1.npz holds the REFERENCE's
+own outputs (its sources compiled into oracle/_ref by oracle/ref_build.py);
+golden_v1.npz the restatement's.  CPU suite: each backend reproduces its file
+bit for bit, and the restatement agrees with the reference (bit-exact
+correlation / measurement / features, 1e-8 BA).  GPU suite: the B200 path
+matches the reference's golden outputs within the parity tolerances, without
+any oracle in the loop.  See tests/golden/cases.py for the cases."""
 from pathlib import Path
 
 import numpy as np
@@ -10,10 +13,17 @@ import pytest
 from tests.golden import cases
 
 GOLDEN = Path(__file__).resolve().parent / "golden" / "golden_v1.npz"
+GOLDEN_REF = Path(__file__).resolve().parent / "golden" / "golden_ref_v1.npz"
+EXACT = ["corr_out", "measure_delta", "measure_weight", "measure_flags", "feat_level0", "feat_level1", "feat_crops"]
 
 
 @pytest.fixture(scope="module")
 def golden():
+    return np.load(GOLDEN_REF)
+
+
+@pytest.fixture(scope="module")
+def golden_restated():
     return np.load(GOLDEN)
 
 
@@ -26,12 +36,34 @@ def test_golden_inputs_are_stable(golden):
     assert str(golden["feat_inputs_sha"]) == cases.digest(*f.values())
 
 
-def test_oracle_reproduces_golden(golden):
+def test_oracle_reproduces_golden(golden_restated):
+    import oracle.pyoracle as orc
     from tests.golden.make_golden import build
 
-    fresh = build()
+    with orc.using("restated"):
+        fresh = build()
+    for k in golden_restated.files:
+        assert np.array_equal(fresh[k], golden_restated[k]), k
+
+
+def test_reference_reproduces_golden(golden):
+    import oracle.pyoracle as orc
+    from tests.golden.make_golden import build
+
+    if orc.lib_ref is None:
+        pytest.skip("oracle/_ref not built (no /root/reference here)")
+    with orc.using("reference"):
+        fresh = build()
     for k in golden.files:
         assert np.array_equal(fresh[k], golden[k]), k
+
+
+def test_restatement_pinned_to_reference(golden, golden_restated):
+    for k in EXACT:
+        assert np.array_equal(golden[k], golden_restated[k]), k
+    for k in ["ba_poses", "ba_depth", "ba_norms"]:
+        ref, res = golden[k], golden_restated[k]
+        assert np.abs(ref - res).max() <= 1e-8 * max(1.0, np.abs(ref).max()), k
 
 
 @pytest.mark.gpu

@@ -12,7 +12,7 @@ import pytest
 
 import oracle.pyoracle as orc
 import paper_2208_04726_b200 as pvo
-from paper_2208_04726_b200 import synth
+import pvo_synth as synth
 from tests.helpers import pose_parity, random_pose, random_twist, smooth_features
 
 pytestmark = pytest.mark.gpu

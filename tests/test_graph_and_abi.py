@@ -8,7 +8,8 @@ import numpy as np
 import pytest
 
 import oracle.pyoracle as orc
-from paper_2208_04726_b200 import PatchGraph, synth
+from paper_2208_04726_b200 import PatchGraph
+import pvo_synth as synth
 from paper_2208_04726_b200 import api as pvo
 from paper_2208_04726_b200._capi import SIGNATURES, lib
 from tests.helpers import random_pose

@@ -34,7 +34,9 @@ def _free_port():
 def _worker(rank, world, port, q):
     import torch.distributed as dist
 
-    from paper_2208_04726_b200 import PatchGraph, synth
+    from paper_2208_04726_b200 import PatchGraph
+
+    import pvo_synth as synth
     from paper_2208_04726_b200.dist import gather_poses, max_over_ranks, shard
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -71,7 +73,8 @@ def test_gloo_two_ranks_shard_and_gather():
     assert t0 == t1 == [2.0, 2.0]  # MAX over ranks
     assert g0 == g1  # every rank sees the same gathered list
     # the gathered block of each rank equals an independent single-process run
-    from paper_2208_04726_b200 import PatchGraph, synth
+    from paper_2208_04726_b200 import PatchGraph
+    import pvo_synth as synth
 
     for rank, seqs in ((0, s0), (1, s1)):
         ref = []

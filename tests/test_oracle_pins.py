@@ -176,7 +176,7 @@ def test_gauge_invariance():  # test_camera.cpp:182-195
 # ---------------------------------------------------------------- correlation (test_features.cpp:144-245)
 def _pyramid(seed, H=64, W=64, D=25):
     rng = np.random.default_rng(seed)
-    from paper_2208_04726_b200 import synth
+    import pvo_synth as synth
 
     l0 = smooth_features(rng, H, W, D)
     l1 = synth.make_level1(l0[None])[0]
@@ -184,7 +184,7 @@ def _pyramid(seed, H=64, W=64, D=25):
 
 
 def _crop(l0, l1, centroid):
-    from paper_2208_04726_b200 import synth
+    import pvo_synth as synth
 
     x, y = orc.patch_make(centroid, 3, 1.0)
     return (synth.crop_cubic(l0, x / 4.0, y / 4.0), synth.crop_cubic(l1, x / 16.0, y / 16.0)), np.stack([x, y], 1)
@@ -444,7 +444,7 @@ def test_behind_camera_edges_not_fatal():  # test_bundle_adjust.cpp:408-417
 def _gt_graph(seed, frames, patches, radius, noise, window, weight=0.9, graph_cls=None):
     """graph_at_ground_truth + set_oracle_revisions analogue on a synth workload
     (sim_fixtures.hpp:13-85): exact GT-pointing deltas, uniform weight."""
-    from paper_2208_04726_b200 import synth
+    import pvo_synth as synth
 
     w = synth.generate("c1", seed=seed, features=False, frames=frames, patches=patches)
     w.cfg["radius"] = radius
@@ -515,7 +515,7 @@ def _measure_one(g_patch, lvl0, lvl1, center):
 
 
 def _crop_patch(lvl0, lvl1, centroid):
-    from paper_2208_04726_b200 import synth
+    import pvo_synth as synth
 
     px, py = _patch_grid(centroid)  # Patch::make grid (camera.cpp:15-38)
     g0 = synth.crop_cubic(lvl0, px / 4.0, py / 4.0)
@@ -529,7 +529,7 @@ def _patch_grid(centroid):
 
 
 def _smooth_grid(rng, H, W, D, passes=3):
-    from paper_2208_04726_b200 import synth
+    import pvo_synth as synth
 
     g = synth.make_level0(rng, 1, H, W, D)[0]
     for _ in range(passes - 1):  # extra blur passes: a smoother field for subpixel accuracy
@@ -542,7 +542,7 @@ def _smooth_grid(rng, H, W, D, passes=3):
 
 
 def _level1(g):
-    from paper_2208_04726_b200 import synth
+    import pvo_synth as synth
 
     return synth.make_level1(g[None])[0]
 
@@ -660,7 +660,7 @@ def test_crop_matches_sampler_definition():  # features.cpp:204-224 with sample_
     px = cents[:, :1] + gx.ravel()[None]
     py = cents[:, 1:] + gy.ravel()[None]
     out = orc.crop_patches(px, py, l0, l1)
-    from paper_2208_04726_b200 import synth
+    import pvo_synth as synth
 
     ref0 = synth.crop_cubic(l0, px[1] / 4.0, py[1] / 4.0)
     assert np.allclose(out[1, 0], ref0, atol=1e-6)
@@ -670,7 +670,7 @@ def test_crop_matches_sampler_definition():  # features.cpp:204-224 with sample_
 def _gt_window(seed, frames, patches, radius):
     """graph_at_ground_truth (sim_fixtures.hpp) on a synth scene, flattened over
     every frame: the problem plus the scene poses / inverse depths per slot."""
-    from paper_2208_04726_b200 import synth
+    import pvo_synth as synth
 
     w = synth.generate("c1", seed=seed, features=False, frames=frames, patches=patches)
     g = orc.PatchGraph(w.K, w.image[0], w.image[1])

@@ -18,7 +18,7 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import paper_2208_04726_b200 as pvo  # noqa: E402
-from paper_2208_04726_b200 import synth  # noqa: E402
+import pvo_synth as synth  # noqa: E402
 
 n_frames = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 cfg = sys.argv[2] if len(sys.argv) > 2 else "c2"
