@@ -828,6 +828,24 @@ Matrix<S, R1, C2> operator*(const MBase<A, S, R1, C1>& a, const MBase<B, S, R2, 
     out.resize(a.rows(), b.cols());
     const Desc<S> x = a.desc(), y = b.desc(), o = out.desc();
     const Index n = x.c;
+    if (n >= 16 && o.r * o.c >= 64) {
+        // large operands: contiguous copies (rows of a, columns of b), same
+        // sequential inner sums, so the result is identical to the loop below
+        std::vector<S> ar(static_cast<size_t>(x.r * n)), bc(static_cast<size_t>(y.c * n));
+        for (Index i = 0; i < x.r; ++i)
+            for (Index k = 0; k < n; ++k) ar[i * n + k] = x.at(i, k);
+        for (Index j = 0; j < y.c; ++j)
+            for (Index k = 0; k < n; ++k) bc[j * n + k] = y.at(k, j);
+        for (Index j = 0; j < o.c; ++j)
+            for (Index i = 0; i < o.r; ++i) {
+                const S* ap = &ar[i * n];
+                const S* bp = &bc[j * n];
+                S s = ap[0] * bp[0];
+                for (Index k = 1; k < n; ++k) s += ap[k] * bp[k];
+                o.at(i, j) = s;
+            }
+        return out;
+    }
     for (Index j = 0; j < o.c; ++j)
         for (Index i = 0; i < o.r; ++i) {
             S s = n ? x.at(i, 0) * y.at(0, j) : S(0);

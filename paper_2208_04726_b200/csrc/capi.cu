@@ -539,6 +539,8 @@ void run_corr(pvo_ctx* ctx, pvo_dev::CorrTmaParams t, int index_edges = 0) {
         t.h0 = ctx->h0;
         t.w1 = ctx->w1;
         t.h1 = ctx->h1;
+        t.feat0 = static_cast<const float*>(ctx->feat0.p);
+        t.feat1 = static_cast<const float*>(ctx->feat1.p);
         t.coords = ctx->c_coords.as<double>((size_t)std::max(t.n_edges, index_edges) * 18);  // indexed by edge
         t.list_cap = pvo_dev::corr_tma_list_cap(t.n_edges);
         t.meta = ctx->c_meta.as<int>((size_t)t.list_cap * pvo_dev::kCorrMetaInts);

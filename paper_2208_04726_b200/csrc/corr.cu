@@ -27,6 +27,7 @@
 
 #include <cstdint>
 
+#include "corr_exact.cuh"
 #include "geometry.cuh"
 #include "kernels.cuh"
 
@@ -293,8 +294,14 @@ __global__ void __launch_bounds__(kThreads) corr_kernel(CorrParams a) {
                             w11 * w11 * (double)g11[0];
                 n2 += 2.0 * (w00 * w10 * (double)g00[1] + w01 * w11 * (double)g01[1] + w00 * w01 * (double)g00[2] +
                              w10 * w11 * (double)g10[2] + w00 * w11 * (double)g00[3] + w10 * w01 * (double)g00[4]);
-                const double c = n2 > 1e-12 ? dot / sqrt(n2) : 0.0;  // correlation.cpp:22
-                out[(size_t)p * 49 + ab] = (float)c;
+                const double m = w00 * (double)g00[0] + w10 * (double)g10[0] + w01 * (double)g01[0] +
+                                 w11 * (double)g11[0];  // >= ||f(x)||^2 (Cauchy-Schwarz)
+                float c;
+                if (corr_needs_exact((float)n2, (float)m))  // cancelling taps: the reference's way
+                    c = corr_exact_thread(pfeat + (size_t)p * D, fbase, W, H, D, xs, ys);
+                else
+                    c = n2 > 1e-12 ? (float)(dot / sqrt(n2)) : 0.f;  // correlation.cpp:22
+                out[(size_t)p * 49 + ab] = c;
             }
             __syncthreads();
         }

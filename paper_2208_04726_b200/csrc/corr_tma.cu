@@ -39,6 +39,7 @@
 #include <cstdint>
 #include <type_traits>
 
+#include "corr_exact.cuh"
 #include "geometry.cuh"
 #include "kernels.cuh"
 
@@ -531,6 +532,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
         float* out = a.out + ((size_t)e * 2 + level) * kOut;
+        unsigned exact = 0;  // outputs to re-evaluate directly: bit 7 * (col >= 32) + alpha
 #pragma unroll 1
         for (int col = lane; col < kPix * 7; col += 32) {
             const int p = (col * 37) >> 8, beta = col - 7 * p;  // col / 7 for col < 63
@@ -549,9 +551,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float* d = dots + p * kCells + cy * kBox + cx;
             const float* G = gram + cy * kGramW + cx;
             const float qa = bx0 * bx0, qb = ax * ax, qc = 2.f * ax * bx0, qd = ax * bx0;
-            // row terms of row y: <g, fx(y)>, |fx(y)|^2
+            // row terms of row y: <g, fx(y)>, |fx(y)|^2, and sum_x w_x |f(y, x)|^2
             float dA = fmaf(ax, d[1], bx0 * d[0]);
             float nA = fmaf(qc, G[kGramPlane], fmaf(qb, G[1], qa * G[0]));
+            float mA = fmaf(ax, G[1], bx0 * G[0]);
+            const int ebit = col >= 32 ? 7 : 0;
 #pragma unroll
             for (int alpha = 0; alpha < 7; ++alpha) {
                 const float* dn = d + (alpha + 1) * kBox;
@@ -566,9 +570,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float by0 = 1.f - ay;
                 const float dot = fmaf(ay, dB, by0 * dA);
                 const float n2 = fmaf(2.f * ay * by0, cr, fmaf(ay * ay, nB, by0 * by0 * nA));
+                const float mB = fmaf(ax, Gn[1], bx0 * Gn[0]);
+                if (corr_needs_exact(n2, fmaf(ay, mB, by0 * mA))) exact |= 1u << (ebit + alpha);
                 o[alpha * 7] = n2 > 1e-12f ? dot * rsqrt_approx(n2) : 0.f;  // correlation.cpp:22
                 dA = dB;
                 nA = nB;
+                mA = mB;
+            }
+        }
+        // cancelling taps: the warp re-evaluates those outputs the reference's way
+        // (corr_exact.cuh); rare on real features, so the common path stays FP32
+        unsigned todo = __ballot_sync(0xffffffffu, exact != 0);
+        while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            unsigned m = __shfl_sync(0xffffffffu, exact, src);
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                const int col = src + (b >= 7 ? 32 : 0), alpha = b >= 7 ? b - 7 : b;
+                const int p = (col * 37) >> 8, beta = col - 7 * p;
+                const double x = tc[2 * p] * inv_scale + (double)(beta - 3);
+                const double y = tc[2 * p + 1] * inv_scale + (double)(alpha - 3);
+                const float* fr = (level ? a.feat1 : a.feat0) + (size_t)r0.w * W * H * kD;
+                const float v = corr_exact_warp(a.patch_feats + (size_t)(r1.x + p) * kD, fr, W, H, kD, x, y);
+                if (lane == 0) out[p * 49 + alpha * 7 + beta] = v;
             }
         }
         __syncwarp();  // dots and the header are rewritten by the next tile

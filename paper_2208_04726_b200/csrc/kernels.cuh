@@ -56,6 +56,8 @@ struct CorrTmaParams {
     int w0 = 0, h0 = 0, w1 = 0, h1 = 0;
     const float* patch_feats = nullptr;  // [P][2][9][128]
     int n_patches = 0;
+    const float* feat0 = nullptr;        // frame store [slot][H][W][128] (direct re-evaluation
+    const float* feat1 = nullptr;        // of outputs whose bilinear taps cancel, corr_exact.cuh)
     float* out = nullptr;
     double* coords = nullptr;     // scratch [E][9][2]
     int* meta = nullptr;          // scratch [list_cap][8]: the tile list (one record per box-sized pixel group)
