@@ -39,6 +39,7 @@
 // ============================================================================
 #include <algorithm>
 #include <cfloat>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -1955,4 +1956,61 @@ int orc_ldlt_solve(int n, const double* a, const double* rhs, double* x, int* ok
     });
 }
 
+// ---- timing entries for bench.py's CPU legs (test infrastructure) ----
+// The per-iteration correlation work of the reference's pipeline over a flat
+// window: for every edge reproject_patch (camera.cpp:47-71) then correlate
+// (correlation.cpp:37-71), edges split over `threads` host threads.  Inputs are
+// staged before the clock starts (the pipeline keeps patches, descriptors and
+// pyramids resident); *seconds = wall time of the edge loop only.
+int orc_bench_corr(int n_poses, const double* poses, int n_patches, int p, const int* src, const double* px,
+                   const double* py, const double* depth, int n_edges, const int* e_patch, const int* e_pose,
+                   const int* e_frame, const double* K, int channels, const float* patch_feats,
+                   const float* frames0, int w0, int h0, const float* frames1, int w1, int h1, int threads,
+                   double* seconds) {
+    return guard([&] {
+        std::vector<Pose> P;
+        for (int i = 0; i < n_poses; ++i) P.push_back(load_pose(poses + 7 * i));
+        std::vector<Patch> pt;
+        for (int k = 0; k < n_patches; ++k) pt.push_back(load_patch(p, px + k * p * p, py + k * p * p, depth[k], src[k]));
+        const Intrinsics Kc = load_K(K);
+        const size_t pp = static_cast<size_t>(p) * p;
+        const size_t f0 = static_cast<size_t>(w0) * h0 * channels, f1 = static_cast<size_t>(w1) * h1 * channels;
+        std::vector<float> out(static_cast<size_t>(n_edges) * 2 * pp * kCorrSize * kCorrSize);
+        const int nt = threads > 0 ? threads : 1;
+        const auto t0 = std::chrono::steady_clock::now();
+        auto work = [&](int t) {
+            for (int e = t; e < n_edges; e += nt) {
+                const Patch& patch = pt[e_patch[e]];
+                const PatchReprojection r = reproject_patch(P[patch.source_frame], P[e_pose[e]], Kc, patch);
+                std::vector<double> c(2 * pp);
+                for (size_t k = 0; k < pp; ++k) c[2 * k] = r.points[k].x, c[2 * k + 1] = r.points[k].y;
+                const float* g = patch_feats + static_cast<size_t>(e_patch[e]) * 2 * pp * channels;
+                correlate(p, channels, g, g + pp * channels, GridView{frames0 + e_frame[e] * f0, w0, h0, channels},
+                          GridView{frames1 + e_frame[e] * f1, w1, h1, channels}, c.data(),
+                          out.data() + static_cast<size_t>(e) * 2 * pp * kCorrSize * kCorrSize);
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+        work(0);
+        for (auto& th : pool) th.join();
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+// optimize_window (bundle_adjust.cpp:225-375) on a copy of the graph; *seconds
+// = the call alone (the copy is made before the clock starts).
+int orc_bench_optimize_window(void* g, int window, int iterations, double damping, double* seconds) {
+    return guard([&] {
+        PatchGraph copy = *static_cast<PatchGraph*>(g);
+        WindowOptions opt;
+        opt.window = window;
+        opt.iterations = iterations;
+        opt.damping = damping;
+        const auto t0 = std::chrono::steady_clock::now();
+        optimize_window(copy, opt);
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
 }  // extern "C"
+

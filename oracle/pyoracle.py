@@ -474,3 +474,26 @@ def oracle_propose(pr, gt_poses, gt_d, K, flow_sigma=0.0, outlier_fraction=0.0, 
                                  _p(d), _p(_f64(gt_d)), I(E), _p(ep), _p(eo), _p(_f64(K, (4,))), D(flow_sigma),
                                  D(outlier_fraction), C.c_uint64(seed), _p(dl), _p(wt)))
     return dl, wt
+
+
+# ---- timing helpers for bench.py's CPU legs (wall seconds measured in C++) ----
+def bench_corr(pr, K, e_frame, patch_feats, frames0, frames1, threads=1):
+    """reproject_patch + correlate over every edge of a flat window; -> seconds."""
+    poses, fixed, src, px, py, d, ep, eo, et, ew = _prob_args(pr)
+    ef = np.ascontiguousarray(e_frame, np.int32)
+    pf = np.ascontiguousarray(patch_feats, np.float32)
+    f0 = np.ascontiguousarray(frames0, np.float32)
+    f1 = np.ascontiguousarray(frames1, np.float32)
+    sec = D()
+    check(lib.orc_bench_corr(I(len(poses)), _p(poses), I(len(d)), I(3), _p(src), _p(px), _p(py), _p(d), I(len(ep)),
+                             _p(ep), _p(eo), _p(ef), _p(_f64(K, (4,))), I(pf.shape[-1]), _p(pf), _p(f0),
+                             I(f0.shape[2]), I(f0.shape[1]), _p(f1), I(f1.shape[2]), I(f1.shape[1]), I(threads),
+                             C.byref(sec)))
+    return sec.value
+
+
+def bench_optimize_window(graph, window=10, iterations=2, damping=1e-4):
+    """optimize_window on a copy of the graph; -> seconds of the call."""
+    sec = D()
+    check(lib.orc_bench_optimize_window(graph._h, I(window), I(iterations), D(damping), C.byref(sec)))
+    return sec.value

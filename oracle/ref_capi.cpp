@@ -16,6 +16,7 @@
 // Pipeline::active_edges (pipeline.cpp:164-181), a Pipeline member.
 // Poses cross the surface as 7 raw doubles and are reloaded bit for bit
 // (see load_pose).
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -680,4 +681,63 @@ int orc_ldlt_solve(int n, const double* a, const double* rhs, double* x, int* ok
     });
 }
 
+// ---- timing entries for bench.py's CPU legs (the reference's own code) ----
+// Per-iteration correlation work of the reference pipeline over a flat window:
+// for every edge reproject_patch (camera.cpp:47-71) then correlate
+// (correlation.cpp:37-71), edges split over `threads` host threads (the
+// reference itself is single-threaded; edges are independent).  Patches,
+// PatchFeatures and FeaturePyramids are staged before the clock starts, as the
+// pipeline keeps them resident (flow_provider.hpp:108-112).
+int orc_bench_corr(int n_poses, const double* poses, int n_patches, int p, const int* src, const double* px,
+                   const double* py, const double* depth, int n_edges, const int* e_patch, const int* e_pose,
+                   const int* e_frame, const double* K, int channels, const float* patch_feats,
+                   const float* frames0, int w0, int h0, const float* frames1, int w1, int h1, int threads,
+                   double* seconds) {
+    return guard([&] {
+        std::vector<Pose> P;
+        for (int i = 0; i < n_poses; ++i) P.push_back(load_pose(poses + 7 * i));
+        std::vector<Patch> pt;
+        std::vector<PatchFeatures> pf;
+        const size_t pp = static_cast<size_t>(p) * p;
+        for (int k = 0; k < n_patches; ++k) {
+            pt.push_back(load_patch(p, px + k * p * p, py + k * p * p, depth[k], src[k]));
+            const float* g = patch_feats + static_cast<size_t>(k) * 2 * pp * channels;
+            pf.push_back(load_feats(p, channels, g, g + pp * channels));
+        }
+        const Intrinsics Kc = load_K(K);
+        FrameCache cache{frames0, frames1, w0, h0, w1, h1, channels, {}};
+        for (int e = 0; e < n_edges; ++e) cache.at(e_frame[e]);
+        std::vector<CorrelationGrid> out(static_cast<size_t>(n_edges));
+        const int nt = threads > 0 ? threads : 1;
+        const auto t0 = std::chrono::steady_clock::now();
+        auto work = [&](int t) {
+            for (int e = t; e < n_edges; e += nt) {
+                const Patch& patch = pt[e_patch[e]];
+                const PatchReprojection r = reproject_patch(P[patch.source_frame], P[e_pose[e]], Kc, patch);
+                out[e] = correlate(pf[e_patch[e]], cache.at(e_frame[e]), r.points);
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+        work(0);
+        for (auto& th : pool) th.join();
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+// optimize_window (bundle_adjust.cpp:225-375) on a copy of the graph; *seconds
+// = the call alone (the copy is made before the clock starts).
+int orc_bench_optimize_window(void* g, int window, int iterations, double damping, double* seconds) {
+    return guard([&] {
+        PatchGraph copy = G(g);
+        WindowOptions opt;
+        opt.window = window;
+        opt.iterations = iterations;
+        opt.damping = damping;
+        const auto t0 = std::chrono::steady_clock::now();
+        optimize_window(copy, opt);
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
 }  // extern "C"
+

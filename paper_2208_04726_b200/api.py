@@ -753,9 +753,14 @@ class Batch:
     def reset(self) -> None:
         check(lib.pvo_batch_reset(self.ctx.handle))
 
-    def iteration(self, iterations: int = 2, damping: float = kDefaultDamping, corr_out=None) -> None:
+    def iteration(self, iterations: int = 2, damping: float = kDefaultDamping, corr_out=None,
+                  corr_device_ptr: int | None = None) -> None:
+        """corr_out: host volume [E, 2, 9, 7, 7]; corr_device_ptr: a device buffer of
+        the same size (e.g. a torch tensor's data_ptr()) that receives the volume."""
         _check_corr_out(corr_out, self.n_edges)
-        if corr_out is not None:
+        if corr_device_ptr is not None:
+            check(lib.pvo_batch_iteration(self.ctx.handle, iterations, damping, corr_device_ptr, _capi.PVO_DEVICE))
+        elif corr_out is not None:
             check(lib.pvo_batch_iteration(self.ctx.handle, iterations, damping, _ptr(corr_out), _capi.PVO_HOST))
         else:
             check(lib.pvo_batch_iteration(self.ctx.handle, iterations, damping, None, _capi.PVO_DEVICE))
