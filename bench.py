@@ -13,8 +13,13 @@ gather of poses and stats after the timed region).
 Metric: corr+BA edge-iterations/s = E / t_step (whole job: sum over ranks of E
 divided by the max-over-ranks step time).
 
---impl reference times the reference CPU path (the oracle restatement,
-oracle/, because the reference itself cannot be built here) on the host cores.
+--impl reference times the reference's own CPU implementation of the path on
+the host cores: its sources compiled unmodified into oracle/_ref by
+oracle/ref_build.py (the restatement oracle/pvo_oracle.cpp only if that build
+is absent), every edge of the window per step, reproject_patch + correlate
+split over all host threads and the reference's single-threaded
+optimize_window.  Without torchrun, --gpus N > 1 relaunches itself under
+torch.distributed.run (one rank per GPU, 127.0.0.1 rendezvous).
 """
 from __future__ import annotations
 
@@ -170,6 +175,35 @@ def corr_bytes_per_edge(prob, K, level_shapes, D=128):
     return total, per
 
 
+L2_NOTE = "GPU arm: L2 flushed between steps (256 MiB write, outside the timed events); CPU arm: n/a"
+
+
+def workload_config(name: str, w, E: int, world: int) -> dict:
+    """The `config` object of the JSON line, identical in both arms."""
+    return {"workload": name, "desc": w.cfg["desc"], "edges_per_gpu": E, "window": w.cfg["window"],
+            "radius": w.cfg["radius"], "patches_per_frame": w.cfg["patches"], "channels": 128,
+            "ba_iterations": 2, "sequences": world, "parallelism": f"sequence-sharded x{world}", "l2": L2_NOTE}
+
+
+def batch_config(n_seq_total: int, world: int, chunk: int, n_chunks: int, E_chunk: int, distinct: int,
+                 frames: int) -> dict:
+    return {"workload": "c5", "desc": "batch of independent sequences at the DPVO default window, sharded by "
+            "sequence", "sequences_total": n_seq_total, "sequences_per_gpu": n_seq_total // world, "chunk": chunk,
+            "chunks_per_gpu": n_chunks, "edges_per_gpu": E_chunk * n_chunks, "distinct_trajectories_per_gpu": distinct,
+            "frames_per_sequence": frames, "parallelism": f"sequence-sharded x{world}",
+            "l2": f"inputs ({chunk * frames * 10.4 / 1024:.1f} GB frame store per chunk) far larger than L2"}
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def setup(config: str, seed: int, device: int):
     import torch
 
@@ -195,82 +229,111 @@ def setup(config: str, seed: int, device: int):
 
 
 # ---------------------------------------------------------------- reference arm
+def _ref_inputs(config: str):
+    import oracle.pyoracle as orc
+    import pvo_synth as synth
+
+    w = synth.generate("c2" if config == "c5" else config, seed=0)
+    og = synth.build_graph(w, orc.PatchGraph)
+    prob = og.window_problem(w.cfg["window"])
+    pf = w.patch_feats[prob["patch_ids"]]
+    frames = prob["pose_frames"][prob["e_pose"]]
+    return w, og, prob, pf, frames
+
+
+def _ref_step(orc, w, og, prob, pf, frames, threads, edges=None):
+    """One iteration of the reference's per-frame hot path over the window:
+    reproject_patch + correlate for every edge (or the given edge slice), then
+    optimize_window(2 iterations).  Seconds (corr, BA), measured in C++."""
+    sub = prob
+    if edges is not None:
+        sub = dict(prob)
+        for k in ("e_patch", "e_pose", "e_target", "e_weight"):
+            sub[k] = prob[k][edges]
+    t_corr = orc.bench_corr(sub, w.K, frames if edges is None else frames[edges], pf, w.level0, w.level1,
+                            threads=threads)
+    t_ba = orc.bench_optimize_window(og, window=w.cfg["window"], iterations=2)
+    return t_corr, t_ba
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
     import oracle.pyoracle as orc
-    import pvo_synth as synth
 
-    # c5 (a batch of c2 sequences): the CPU path's per-edge cost is the c2 window's
-    w = synth.generate("c2" if args.config == "c5" else args.config, seed=0)
-    og = synth.build_graph(w, orc.PatchGraph)
-    prob = og.window_problem(w.cfg["window"])
+    w, og, prob, pf, frames = _ref_inputs(args.config)
     E = len(prob["e_patch"])
     threads = os.cpu_count() or 1
-    sample = min(E, args.ref_edges)
-    coords = np.empty((sample, 9, 2))
-    for e in range(sample):
-        k = prob["e_patch"][e]
-        coords[e], _ = orc.reproject_patch(prob["poses"][prob["patch_src"][k]], prob["poses"][prob["e_pose"][e]],
-                                           w.K, prob["patch_x"][k], prob["patch_y"][k], prob["depth"][k])
-    pf = w.patch_feats[prob["patch_ids"]]
-    slots = prob["pose_frames"][prob["e_pose"][:sample]]
-
-    def one_step():
-        t0 = time.perf_counter()
-        orc.correlate_batch(prob["e_patch"][:sample], slots, coords, pf, w.level0, w.level1, threads=threads)
-        t1 = time.perf_counter()
-        # the iteration loop of optimize_window on the flattened window (dense H,
-        # Schur, Eigen-LDLT restatement, guard): bundle_adjust.cpp:309-366
-        orc.ba_window(prob, w.K, iterations=2)
-        t2 = time.perf_counter()
-        return (t1 - t0) / sample * E, t2 - t1
-
-    for _ in range(args.warmup):
-        one_step()
-    times = [one_step() for _ in range(args.steps)]
-    step_s = float(np.mean([a + b for a, b in times]))
+    kind = "reference" if orc.lib_ref is not None else "port"
+    # every step is the whole window unless K steps of it would not finish in a
+    # few minutes: then each step takes the next contiguous slice of the edges
+    # (the slices cycle through all edges) and the full BA
+    probe_c, probe_b = _ref_step(orc, w, og, prob, pf, frames, threads)
+    budget_s = 240.0
+    n_slices = max(1, int(np.ceil((args.steps + args.warmup) * (probe_c + probe_b) / budget_s)))
+    bounds = np.linspace(0, E, n_slices + 1).astype(int)
+    times = []
+    for i in range(args.warmup + args.steps):
+        sl = i % n_slices
+        edges = None if n_slices == 1 else np.arange(bounds[sl], bounds[sl + 1])
+        tc, tb = _ref_step(orc, w, og, prob, pf, frames, threads, edges)
+        if i >= args.warmup:
+            n_e = E if edges is None else len(edges)
+            times.append((tc / n_e, tb))
+    per_edge_corr = float(np.mean([a for a, _ in times]))
+    t_ba = float(np.mean([b for _, b in times]))
+    if args.config == "c5":
+        # a batch of independent sequences: one sequence per host core, so the
+        # single-threaded BA of each sequence overlaps the others'
+        step_s = per_edge_corr * E + t_ba / threads
+        how = (f"c5 = independent c2 sequences over {threads} host threads: corr of every edge of a c2 window "
+               f"split over the threads, BA time / {threads} (one sequence per core)")
+    else:
+        step_s = per_edge_corr * E + t_ba
+        how = (f"reproject_patch + correlate over every edge of the {args.config} window on {threads} threads, "
+               f"then the reference's single-threaded optimize_window(2)")
+    if n_slices > 1:
+        how += f"; each step one of {n_slices} contiguous edge slices (cycling through all {E} edges)"
     value = E / step_s
+    if args.config == "c5":  # the GPU arm's batch layout (run_batch), for an identical config
+        n_seq = args.sequences // world
+        chunk = min(n_seq, args.chunk)
+        cfg = batch_config(n_seq * world, world, chunk, -(-n_seq // chunk), E * chunk, min(args.distinct, chunk),
+                           w.cfg["frames"])
+    else:
+        cfg = workload_config(args.config, w, E, world)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "edge-iterations/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "edge-iterations/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
-        "config": {"workload": args.config, "edges": E, "window": w.cfg["window"], "radius": w.cfg["radius"],
-                   "patches_per_frame": w.cfg["patches"], "channels": 128},
-        "cpu_baseline": {"value": value, "unit": "edge-iterations/s", "cores": threads, "kind": "port",
-                         "sample": f"correlate() over the first {sample} of {E} edges on {threads} threads "
-                                   f"(extrapolated to all edges) + full optimize_window(2 iterations, dense H, "
-                                   f"single-threaded as in the reference); oracle/pvo_oracle.cpp -O3"},
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64 (f32 feature storage)", "data": "synthetic",
+        "config": cfg,
+        "cpu_baseline": {"value": value, "unit": "edge-iterations/s", "cores": threads, "kind": kind,
+                         "cpu": cpu_model(), "sample": how,
+                         "build": "oracle/_ref: /root/reference/proj/src compiled unmodified, -O3 -DNDEBUG"
+                         if kind == "reference" else "oracle/pvo_oracle.cpp -O3 -DNDEBUG (restatement)"},
         "e2e": {"value": value, "unit": "edge-iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "corr_ms": float(np.mean([a for a, _ in times])) * 1e3, "ba_ms": float(np.mean([b for _, b in times])) * 1e3,
+        "corr_ms": per_edge_corr * E * 1e3, "ba_ms": t_ba * 1e3,
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(w, prob, sample_edges=600):
-    """Oracle timed on the host: corr single-threaded on a bounded sample (the
-    reference is single-threaded) + full optimize_window(2)."""
+def cpu_baseline(w, prob):
+    """The reference's CPU path on ONE host core over the whole window (no
+    extrapolation): reproject_patch + correlate for every edge, then
+    optimize_window(2) on the same graph."""
     import oracle.pyoracle as orc
     import pvo_synth as synth
 
-    E = len(prob["e_patch"])
-    sample = min(E, sample_edges)
-    coords = np.empty((sample, 9, 2))
-    for e in range(sample):
-        k = prob["e_patch"][e]
-        coords[e], _ = orc.reproject_patch(prob["poses"][prob["patch_src"][k]], prob["poses"][prob["e_pose"][e]],
-                                           w.K, prob["patch_x"][k], prob["patch_y"][k], prob["depth"][k])
-    slots = prob["pose_frames"][prob["e_pose"][:sample]]
-    t0 = time.perf_counter()
-    orc.correlate_batch(prob["e_patch"][:sample], slots, coords, prob["patch_feats"], w.level0, w.level1, threads=1)
-    t_corr = (time.perf_counter() - t0) / sample * E
     og = synth.build_graph(w, orc.PatchGraph)
-    t0 = time.perf_counter()
-    og.optimize_window(window=w.cfg["window"], iterations=2)
-    t_ba = time.perf_counter() - t0
-    return {"value": E / (t_corr + t_ba), "unit": "edge-iterations/s", "cores": 1, "kind": "port",
-            "sample": f"correlate() on {sample}/{E} edges (1 thread, extrapolated) + optimize_window(2) in full; "
-                      f"corr {t_corr * 1e3:.0f} ms + BA {t_ba * 1e3:.0f} ms per iteration"}
+    frames = prob["pose_frames"][prob["e_pose"]]
+    E = len(prob["e_patch"])
+    t_corr = orc.bench_corr(prob, w.K, frames, prob["patch_feats"], w.level0, w.level1, threads=1)
+    t_ba = orc.bench_optimize_window(og, window=w.cfg["window"], iterations=2)
+    kind = "reference" if orc.lib_ref is not None else "port"
+    return {"value": E / (t_corr + t_ba), "unit": "edge-iterations/s", "cores": 1, "kind": kind,
+            "cpu": cpu_model(),
+            "sample": f"one full iteration on 1 core: reproject_patch + correlate over all {E} edges "
+                      f"({t_corr * 1e3:.0f} ms) + optimize_window(2) ({t_ba * 1e3:.0f} ms)"}
 
 
 # ---------------------------------------------------------------- our arm
@@ -412,11 +475,8 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": "edge-iterations/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32 corr (f64 coords/weights), f64 BA", "data": "synthetic",
-        "config": {"workload": args.config, "desc": w.cfg["desc"], "edges_per_gpu": E, "window": w.cfg["window"],
-                   "radius": w.cfg["radius"], "patches_per_frame": w.cfg["patches"], "channels": 128,
-                   "ba_iterations": 2, "sequences": world, "parallelism": f"sequence-sharded x{world}",
-                   "l2": "flushed between steps (256 MiB write, outside the timed events)",
-                   "state": "window state restored before every step (outside the timed events)",
+        "config": workload_config(args.config, w, E, world),
+        "timing": {"state": "window state restored before every step (outside the timed events)",
                    "launch": "CUDA graph of the step's launches, replayed" if graph is not None else "eager launches"},
         "corr_ms": corr_ms_max, "ba_ms": ba_ms_max, "propose_ms": float(np.mean(prop_ms)),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
@@ -578,12 +638,7 @@ def run_batch(args, rank, world, local_rank):
         "metric": METRIC, "value": E_total / (mean_ms * 1e-3), "unit": "edge-iterations/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 corr (f64 coords/weights), f64 BA", "data": "synthetic",
-        "config": {"workload": "c5", "desc": "batch of independent sequences at the DPVO default window, "
-                   "sharded by sequence", "sequences_total": n_seq * world, "sequences_per_gpu": n_seq,
-                   "chunk": chunk, "chunks_per_gpu": n_chunks, "edges_per_gpu": E_chunk * n_chunks,
-                   "distinct_trajectories_per_gpu": len(geos), "frames_per_sequence": F,
-                   "parallelism": f"sequence-sharded x{world}",
-                   "l2": f"inputs ({chunk * F * 10.4 / 1024:.1f} GB frame store per chunk) far larger than L2"},
+        "config": batch_config(n_seq * world, world, chunk, n_chunks, E_chunk, len(geos), F),
         "last_chunk_corr_ms": corr_ms, "last_chunk_ba_ms": ba_ms,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": None, "kernel": "corr_tma_kernel", "peak_kind": peak_kind,
@@ -640,6 +695,19 @@ def run_e2e(args, w, prob, ctx, stream, win):
     return {"ms": ms, "h2d": int(h2d), "d2h": int(d2h)}
 
 
+def relaunch(n: int) -> None:
+    """`python bench.py --gpus N` without torchrun: run this script under
+    torch.distributed.run with N ranks (one per GPU, rendezvous on 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -650,13 +718,16 @@ def main():
     ap.add_argument("--sequences", type=int, default=1024, help="c5: sequences in the whole job")
     ap.add_argument("--chunk", type=int, default=256, help="c5: sequences per device launch")
     ap.add_argument("--distinct", type=int, default=32, help="c5: distinct trajectories per rank")
-    ap.add_argument("--ref-edges", type=int, default=256)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a captured step")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        relaunch(args.gpus)  # does not return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" in os.environ and args.gpus != world:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
