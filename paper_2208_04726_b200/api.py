@@ -159,6 +159,9 @@ class Context:
         self.frame_shape = (w0, h0, w1, h1, channels)
 
     def frames_upload(self, slot: int, level0, level1, device: bool = False) -> None:
+        """Copy a pyramid into a frame-store slot (+ its Gram terms).  device=True:
+        torch tensors / device pointers, read in order on the context's stream
+        (set_stream) — the producer must have finished or run on that stream."""
         if device:  # torch tensors / raw device pointers
             p0 = level0 if isinstance(level0, int) else level0.data_ptr()
             p1 = level1 if isinstance(level1, int) else level1.data_ptr()

@@ -34,7 +34,8 @@ NVCC_FLAGS = [
     "-I",
     str(ROOT / "include"),
 ]
-SOURCES = ["corr.cu", "corr_tma.cu", "ba.cu", "ba_large.cu", "measure.cu", "dgraph.cu", "features.cu", "capi.cu", "graph.cpp"]
+SOURCES = ["corr.cu", "corr_tma.cu", "ba.cu", "ba_large.cu", "measure.cu", "dgraph.cu", "features.cu", "capi_core.cu", "capi_window.cu",
+           "capi_provider.cu", "capi_batch.cu", "capi_dgraph.cu", "graph.cpp"]
 # per-file extra flags: the provider measurement rounds every product / sum like the
 # x86-64 reference build (no FMA contraction), so its discrete decisions agree
 EXTRA = {"measure.cu": ["--fmad=false"], "features.cu": ["--fmad=false"]}

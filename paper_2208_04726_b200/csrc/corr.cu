@@ -290,14 +290,13 @@ __global__ void __launch_bounds__(kThreads) corr_kernel(CorrParams a) {
                 const float* g01 = s_gram + 5 * (c00 + TW);
                 const float* g11 = s_gram + 5 * (c00 + TW + 1);
                 // Gram record: [0]=|f|^2 [1]=<f,f_right> [2]=<f,f_down> [3]=<f,f_diag> [4]=<f_right,f_down>
-                double n2 = w00 * w00 * (double)g00[0] + w10 * w10 * (double)g10[0] + w01 * w01 * (double)g01[0] +
-                            w11 * w11 * (double)g11[0];
+                const double diag = w00 * w00 * (double)g00[0] + w10 * w10 * (double)g10[0] +
+                                    w01 * w01 * (double)g01[0] + w11 * w11 * (double)g11[0];
+                double n2 = diag;
                 n2 += 2.0 * (w00 * w10 * (double)g00[1] + w01 * w11 * (double)g01[1] + w00 * w01 * (double)g00[2] +
                              w10 * w11 * (double)g10[2] + w00 * w11 * (double)g00[3] + w10 * w01 * (double)g00[4]);
-                const double m = w00 * (double)g00[0] + w10 * (double)g10[0] + w01 * (double)g01[0] +
-                                 w11 * (double)g11[0];  // >= ||f(x)||^2 (Cauchy-Schwarz)
                 float c;
-                if (corr_needs_exact((float)n2, (float)m))  // cancelling taps: the reference's way
+                if (corr_needs_exact((float)n2, (float)diag))  // cancelling taps: the reference's way
                     c = corr_exact_thread(pfeat + (size_t)p * D, fbase, W, H, D, xs, ys);
                 else
                     c = n2 > 1e-12 ? (float)(dot / sqrt(n2)) : 0.f;  // correlation.cpp:22

@@ -6,27 +6,29 @@
 // bilinear taps cancel (anti-correlated neighbour cells) the sampled
 // descriptor's norm ||f(x)||^2 = sum_t sum_t' w_t w_t' <f_t, f_t'> is a small
 // difference of large terms and loses its relative accuracy.  The kernels
-// detect that case — n2 < kCancelRatio * sum_t w_t |f_t|^2 (an upper bound of
-// ||f(x)||^2 by Cauchy-Schwarz, bilinear weights summing to 1), or n2 within
-// 2 % of the 1e-12 threshold — and recompute the output here exactly as
+// detect that case — n2 below half of its diagonal part
+// sum_t w_t^2 |f_t|^2, i.e. the cross terms <f_t, f_t'> cancel most of it
+// (orthogonal taps give n2 = diagonal, positively correlated ones more, a
+// sample over the zero padding keeps only diagonal terms), or n2 within 2 %
+// of the 1e-12 threshold — and recompute the output here exactly as
 // correlation.cpp:8-23 does: every channel sampled by the zero-padded
 // bilinear sampler (features.cpp:9-21) in FP64, dot and squared norm
-// accumulated in FP64.  On smooth or independent features the ratio stays
-// >= 1/4, so the fallback only runs on genuinely cancelling inputs.
+// accumulated in FP64.  (sum_t w_t |f_t|)^2 <= 4 * diagonal, so every output
+// whose norm is below 1/8 of the aligned-taps norm is re-evaluated.
 #pragma once
 
 #include <cuda_runtime.h>
 
 namespace pvo_dev {
 
-// n2 below this fraction of sum_t w_t |f_t|^2: recompute directly
-constexpr float kCancelRatio = 1.0f / 8.0f;
+// n2 below this fraction of its diagonal part: recompute directly
+constexpr float kCancelRatio = 0.5f;
 
-__device__ __forceinline__ bool corr_needs_exact(float n2, float m) {
+__device__ __forceinline__ bool corr_needs_exact(float n2, float diag) {
 #ifdef PVO_CORR_NO_EXACT  // A/B knob (tools/build_variant.sh): the Gram form alone
     return false;
 #else
-    return n2 < kCancelRatio * m || (n2 > 0.98e-12f && n2 < 1.02e-12f);
+    return n2 < kCancelRatio * diag || (n2 > 0.98e-12f && n2 < 1.02e-12f);
 #endif
 }
 
@@ -59,6 +61,9 @@ __device__ inline void corr_exact_partial(const float* g, const float* grid, int
 }
 
 __device__ __forceinline__ float corr_exact_finish(double dot, double n2) {
+#ifdef PVO_CORR_EXACT_SENTINEL  // debug knob: mark re-evaluated outputs
+    return __int_as_float(0x7fc00001);
+#endif
     return n2 > 1e-12 ? (float)(dot / sqrt(n2)) : 0.f;  // correlation.cpp:22
 }
 

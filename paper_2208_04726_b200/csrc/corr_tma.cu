@@ -551,10 +551,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float* d = dots + p * kCells + cy * kBox + cx;
             const float* G = gram + cy * kGramW + cx;
             const float qa = bx0 * bx0, qb = ax * ax, qc = 2.f * ax * bx0, qd = ax * bx0;
-            // row terms of row y: <g, fx(y)>, |fx(y)|^2, and sum_x w_x |f(y, x)|^2
+            // row terms of row y: <g, fx(y)>, |fx(y)|^2 and its diagonal part
+            // sum_x w_x^2 |f(y, x)|^2 (the cancellation check's scale)
             float dA = fmaf(ax, d[1], bx0 * d[0]);
-            float nA = fmaf(qc, G[kGramPlane], fmaf(qb, G[1], qa * G[0]));
-            float mA = fmaf(ax, G[1], bx0 * G[0]);
+            float sA = fmaf(qb, G[1], qa * G[0]);
+            float nA = fmaf(qc, G[kGramPlane], sA);
             const int ebit = col >= 32 ? 7 : 0;
 #pragma unroll
             for (int alpha = 0; alpha < 7; ++alpha) {
@@ -562,20 +563,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float* Gn = G + (alpha + 1) * kGramW;
                 const float* Gc = G + alpha * kGramW;
                 const float dB = fmaf(ax, dn[1], bx0 * dn[0]);
-                const float nB = fmaf(qc, Gn[kGramPlane], fmaf(qb, Gn[1], qa * Gn[0]));
+                const float sB = fmaf(qb, Gn[1], qa * Gn[0]);
+                const float nB = fmaf(qc, Gn[kGramPlane], sB);
                 // <fx(y), fx(y+1)> = (1-ax)^2 down[x] + ax^2 down[x+1] + ax(1-ax) (diag[x] + anti[x])
                 const float cr = fmaf(qd, Gc[3 * kGramPlane] + Gc[4 * kGramPlane],
                                       fmaf(qb, Gc[2 * kGramPlane + 1], qa * Gc[2 * kGramPlane]));
                 const float ay = s_ay[p * 7 + alpha];
                 const float by0 = 1.f - ay;
                 const float dot = fmaf(ay, dB, by0 * dA);
-                const float n2 = fmaf(2.f * ay * by0, cr, fmaf(ay * ay, nB, by0 * by0 * nA));
-                const float mB = fmaf(ax, Gn[1], bx0 * Gn[0]);
-                if (corr_needs_exact(n2, fmaf(ay, mB, by0 * mA))) exact |= 1u << (ebit + alpha);
-                o[alpha * 7] = n2 > 1e-12f ? dot * rsqrt_approx(n2) : 0.f;  // correlation.cpp:22
+                const float wa = by0 * by0, wb = ay * ay;
+                const float n2 = fmaf(2.f * ay * by0, cr, fmaf(wb, nB, wa * nA));
+                if (corr_needs_exact(n2, fmaf(wb, sB, wa * sA)))
+                    exact |= 1u << (ebit + alpha);  // written once, by the re-evaluation below
+                else
+                    o[alpha * 7] = n2 > 1e-12f ? dot * rsqrt_approx(n2) : 0.f;  // correlation.cpp:22
                 dA = dB;
                 nA = nB;
-                mA = mB;
+                sA = sB;
             }
         }
         // cancelling taps: the warp re-evaluates those outputs the reference's way

@@ -102,6 +102,7 @@ def test_c5_chunk(ctx):
         l0 /= l0.norm(dim=-1, keepdim=True)
         l1 = (l0.view(k, H1, 4, W1, 4, 128).mean(dim=(2, 4)))
         l1 = (l1 / l1.norm(dim=-1, keepdim=True).clamp_min(1e-12)).contiguous()
+        torch.cuda.synchronize()  # device uploads are ordered on the context's stream, not torch's
         for j in range(k):
             ctx.frames_upload(s0 + j, l0[j], l1[j], device=True)
         torch.cuda.synchronize()

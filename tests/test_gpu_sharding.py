@@ -47,6 +47,7 @@ def _sequence(sid, ctx, slot0):
     l0 /= l0.norm(dim=-1, keepdim=True)
     l1 = l0.view(F, H0 // 4, 4, W0 // 4, 4, 128).mean(dim=(2, 4))
     l1 = (l1 / l1.norm(dim=-1, keepdim=True).clamp_min(1e-12)).contiguous()
+    torch.cuda.synchronize()  # device uploads are ordered on the context's stream, not torch's
     for f in range(F):
         ctx.frames_upload(slot0 + f, l0[f], l1[f], device=True)
     torch.cuda.synchronize()
@@ -71,10 +72,12 @@ def _run_block(seqs):
             K, image = w.K, w.image
         bat = pvo.Batch(ctx)
         bat.load(probs, slots, feats, K, image)
-        vol = torch.empty((bat.n_edges, 2, 9, 7, 7), dtype=torch.float32, device="cuda")
+        # NaN-filled: an output the kernels never write would show up (and differ between processes)
+        vol = torch.full((bat.n_edges, 2, 9, 7, 7), float("nan"), dtype=torch.float32, device="cuda")
         bat.iteration(2, corr_device_ptr=vol.data_ptr())
         res = bat.read()
         vols = [vol[bat.edge_off[i]:bat.edge_off[i + 1]].cpu().numpy() for i in range(len(seqs))]
+        assert not any(np.isnan(v).any() for v in vols), "unwritten correlation outputs"
         return [(r[0], r[1], np.asarray(r[2]), v) for r, v in zip(res, vols)]
     finally:
         ctx.close()
@@ -126,5 +129,5 @@ def test_sequence_results_bit_identical_across_shardings():
         got = _sharded(world)
         assert sorted(got) == list(range(N_SEQ))
         for sid in range(N_SEQ):
-            for a, b in zip(got[sid], ref[sid]):
-                assert a == b, (world, sid)  # poses, depths, norms, correlation volume bytes
+            for name, a, b in zip(("poses", "depths", "norms", "volume"), got[sid], ref[sid]):
+                assert a == b, (world, sid, name)
