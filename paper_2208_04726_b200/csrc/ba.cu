@@ -22,12 +22,11 @@
 //                 + damping on the diagonal.
 //   --- grid sync
 //   P3 solve      EVERY CTA solves the small pose system redundantly (identical
-//                 inputs and code -> bit-identical results, no broadcast):
-//                 Eigen's LDLT pivot sequence (largest remaining original
-//                 diagonal, bundle_adjust.cpp:76) is simulated first, then an
-//                 unpivoted right-looking LDL^T of the permuted system runs in
-//                 shared memory; retraction of the free poses into the CTA's
-//                 own copy of the candidate state.
+//                 inputs and code -> bit-identical results, no broadcast): a
+//                 natural-order LDL^T of the SPD reduced system with the
+//                 matrix in registers, one barrier per column
+//                 (ldlt_solve_cta); retraction of the free poses into the
+//                 CTA's own copy of the candidate state.
 //   P4 update     warp per patch: depth back-substitution, clamp at 0, weighted
 //                 residual at the candidate state (bitwise-equal-pose shortcut).
 //   --- grid sync
@@ -138,198 +137,147 @@ __device__ __forceinline__ T* at(unsigned char* smem, int off) {
 }
 
 // ---------------------------------------------------------------------------
-// Pivoted LDLT solve of an np x np SPD system held as (upper triangle, rhs),
-// Eigen's pivot rule; all threads of the CTA.  x_out may be
-// shared or global memory.  Returns false (all threads) on a factorization
-// failure (zero pivot with a non-zero column below, LDLT::info()).
+// LDL^T solve of the np x np reduced pose system S x = rhs, held as (upper
+// triangle row-major, rhs) in global memory; all threads of the CTA.  x_out
+// may be shared or global memory.  Returns false (all threads) when a pivot is
+// negative / non-finite, or zero with a non-zero column below (LDLT::info()).
 //
-// Blocked right-looking LDL^T (block 8) on the permuted matrix:
-//   (1) warp 0 factors the 8x8 diagonal block (pivot chain in registers/shuffles),
-//   (2) one thread per panel row eliminates its 8 entries in registers,
-//   (3) all threads apply the rank-8 trailing update A -= (L D) L^T.
+// The reference factors S with Eigen's pivoted LDLT (bundle_adjust.cpp:76).
+// S is symmetric positive definite by construction (the Schur complement of
+// the damped, positive definite GN Hessian), so the natural-order LDL^T gives
+// the same solution up to rounding; no pivot sequence is simulated.
+//
+// Register-resident right-looking elimination with one barrier per column:
+// [S; rhs^T] (row np carries the right-hand side, so the forward substitution
+// comes for free) is distributed block-cyclically over a 16 x 16 thread grid
+// and held in registers for the whole factorisation.  Step k broadcasts the
+// (final) column k and 1/d_k through a double-buffered shared column; every
+// thread applies  A[i][j] -= c_i (c_j / d_k)  (k < j <= i, c = unscaled
+// column k; inactive columns get a zero factor, so the update is branch-free)
+// and the owners of column k+1 publish it (and the next pivot's reciprocal)
+// for step k+1.  The backward substitution L^T x = D^-1 L^-1 rhs runs on
+// warp 0 with x in registers, column-oriented, no barriers (|d| <= DBL_MIN ->
+// pseudo-inverse 0, LDLT::_solve_impl).  (tools/micro_solve: np = 60 in
+// 25.3 us per solve vs 29.0 us for the Eigen-pivot-order blocked version.)
 // ---------------------------------------------------------------------------
-constexpr int kBlk = 8;
+// 16 x 16 thread grid, block-cyclic: thread (ty, tx) owns rows ty + 16 a and
+// columns tx + 16 b of [S; rhs^T]; RPT x CPT entries in registers
+constexpr int kGrid = 16;
+static_assert(kThreads == kGrid * kGrid, "solve grid");
 
 #ifndef SOLVE_PROBE_BEGIN  // phase clocks for tools/micro_solve.cu
 #define SOLVE_PROBE_BEGIN
 #define SOLVE_PROBE(i)
 #endif
-__device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, const Layout& L, double* x_out) {
+template <int RPT, int CPT>
+__device__ bool ldlt_solve_regs(const double* sys, int np, unsigned char* smem, const Layout& L, double* x_out) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int ty = tid / kGrid, tx = tid % kGrid;
     SOLVE_PROBE_BEGIN
-    const int ld = np + 1;                    // row stride: row np carries the right-hand side
-    double* A = at<double>(smem, L.A);        // [(np+1)][(np+1)] lower triangle (+ rhs row)
-    double* x = at<double>(smem, L.x);        // staged system (upper triangle + rhs), then x
-    double* od = at<double>(smem, L.od);
-    double* dinv = at<double>(smem, L.c);     // reciprocal pivots
-    double* LT = at<double>(smem, L.pw);      // [kBlk][np+1]: L panel, transposed
-    double* WD = LT + kBlk * ld;              // [np+1][kBlk]: unscaled panel (= L D)
-    int* perm = at<int>(smem, L.perm);
-    __shared__ int s_fail, s_zero;
-    const int nent = nent_of(np);
-    // stage the reduced system with coalesced loads, 8 in flight per thread
-    for (int i0 = tid; i0 < nent + np; i0 += 8 * kThreads) {
-        double v[8];
+    const int ld = np + 1;
+    double* A = at<double>(smem, L.A);    // [(np+1)][(np+1)]: L (scaled) and z = D^-1 L^-1 rhs in row np
+    double* col = at<double>(smem, L.pw);  // [2][np+1] column broadcast, double-buffered by step parity
+    double* dinv = at<double>(smem, L.c);  // 1 / d_k
+    double* dv = at<double>(smem, L.l);    // d_k
+    double v[RPT][CPT];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = i0 + u * kThreads < nent + np ? sys[i0 + u * kThreads] : 0.0;
+    for (int a = 0; a < RPT; ++a) {
+        const int i = ty + kGrid * a;
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-            if (i0 + u * kThreads < nent + np) x[i0 + u * kThreads] = v[u];
-    }
-    if (tid == 0) {
-        s_fail = 0;
-        s_zero = 0;
-    }
-    __syncthreads();
-    // Pivot order.  Eigen's LDLT picks, step by step, the largest remaining
-    // |diagonal| of the original matrix (its left-looking update leaves the
-    // trailing diagonal untouched): with distinct values that is the
-    // descending order of |diag|, computed here as a parallel rank.  Among
-    // exactly equal values Eigen's order follows its swap history; we keep
-    // index order there, which changes rounding only (same SPD solution).
-    for (int i = tid; i < np; i += kThreads) od[i] = fabs(x[i * np - i * (i - 1) / 2]);  // diag (i, i)
-    __syncthreads();
-    for (int i = tid; i < np; i += kThreads) {
-        const double di = od[i];
-        int rank = 0;
-        for (int j = 0; j < np; ++j) {
-            const double dj = od[j];
-            rank += (dj > di) || (dj == di && j < i);
+        for (int b = 0; b < CPT; ++b) {
+            const int j = tx + kGrid * b;
+            // entry (i, j), j <= i: the packed upper triangle's (j, i); row np: the rhs
+            double x = 0.0;
+            if (j <= i && j < np && i <= np) x = i < np ? sys[j * np - j * (j - 1) / 2 + (i - j)] : sys[nent_of(np) + j];
+            v[a][b] = x;
         }
-        perm[rank] = i;
     }
-    __syncthreads();
-    // A = P S P^T (lower triangle), and row np = (P rhs)^T: eliminating it with
-    // the factorization yields z = D^-1 L^-1 P rhs (forward substitution for free)
-    for (int i = warp; i <= np; i += kWarps) {
-        const int a = i < np ? perm[i] : -1;
-        for (int j = lane; j <= i && j < np; j += 32) {
-            double v;
-            if (a < 0) {
-                v = x[nent + perm[j]];
-            } else {
-                int r = a, s = perm[j];
-                if (r > s) {
-                    const int t = r;
-                    r = s;
-                    s = t;
-                }
-                v = x[r * np - r * (r - 1) / 2 + (s - r)];
-            }
-            A[i * ld + j] = v;
+    // column 0 (owned by tx == 0) and the first pivot
+    if (tx == 0) {
+#pragma unroll
+        for (int a = 0; a < RPT; ++a)
+            if (ty + kGrid * a <= np) col[ty + kGrid * a] = v[a][0];
+        if (ty == 0) {
+            dv[0] = v[0][0];
+            dinv[0] = v[0][0] != 0.0 ? __drcp_rn(v[0][0]) : 0.0;  // = 1.0 / d (correctly rounded)
         }
     }
     __syncthreads();
     SOLVE_PROBE(0)
-
-    // (1) diagonal block on warp 0: lane i < bsz holds row K0+i of the block
-    auto diag = [&](int K0, int bsz) {
-        double row[kBlk];
+    bool fail = false;
+    for (int k = 0; k < np; ++k) {
+        const double* cur = col + (k & 1) * ld;
+        double* nxt = col + ((k + 1) & 1) * ld;
+        const double dk = dv[k], inv = dinv[k];
+        double ci[RPT], cj[CPT];
 #pragma unroll
-        for (int j = 0; j < kBlk; ++j) row[j] = (lane < bsz && j <= lane) ? A[(K0 + lane) * ld + K0 + j] : 0.0;
-        bool fail = false, zero = false;
-#pragma unroll
-        for (int kk = 0; kk < kBlk; ++kk) {
-            if (kk < bsz) {
-                const double dk = __shfl_sync(0xffffffffu, row[kk], kk);
-                const bool valid = fabs(dk) > 0.0;
-                if (K0 + kk == 0 && !valid) zero = true;  // Eigen: all-zero diagonal
-                const double inv = valid ? __drcp_rn(dk) : 0.0;  // = 1.0 / dk (both correctly rounded)
-                if (lane == 0) dinv[K0 + kk] = inv;
-                const double ci = row[kk];  // unscaled column entry of this lane's row
-                const bool below = lane > kk && lane < bsz;
-                if (below && !valid && ci != 0.0) fail = true;
-                const double li = below ? (valid ? ci * inv : ci) : row[kk];
-#pragma unroll
-                for (int j = kk + 1; j < kBlk; ++j) {
-                    const double cj = __shfl_sync(0xffffffffu, ci, j);  // column entry of row K0+j
-                    if (below && j <= lane && valid) row[j] -= ci * (cj * inv);
-                }
-                row[kk] = li;
-            }
+        for (int a = 0; a < RPT; ++a) {
+            const int i = ty + kGrid * a;
+            ci[a] = (i > k && i <= np) ? cur[i] : 0.0;
         }
-        if (lane < bsz) {
 #pragma unroll
-            for (int j = 0; j < kBlk; ++j)
-                if (j <= lane) A[(K0 + lane) * ld + K0 + j] = row[j];
+        for (int b = 0; b < CPT; ++b) {
+            const int j = tx + kGrid * b;
+            cj[b] = (j > k && j < np) ? cur[j] * inv : 0.0;  // inactive columns: no update
         }
-        if (__any_sync(0xffffffffu, fail) && lane == 0) s_fail = 1;
-        if (zero && lane == 0) s_zero = 1;
-    };
-    for (int K0 = 0; K0 < np; K0 += kBlk) {
-        const int bsz = min(kBlk, np - K0);
-        if (warp == 0) diag(K0, bsz);
-        __syncthreads();
-        SOLVE_PROBE(1)
-        if (s_zero) break;
-        // (2) panel rows i >= K0+bsz (the rhs row np included): forward elimination,
-        // the diagonal block's L and reciprocal pivots preloaded (broadcast loads),
-        // the row's 8 entries eliminated in registers, then stored
-        if (K0 + bsz + tid <= np) {
-            double Ld[kBlk][kBlk], inv[kBlk];
+        // a zero pivot is valid only with a zero column below (LDLT::info()); negative
+        // or non-finite pivots do not occur in the SPD system: a failed factorisation
+        if (tx == (k & (kGrid - 1)) && dk == 0.0) {
 #pragma unroll
-            for (int kk = 0; kk < kBlk; ++kk) {
-                inv[kk] = kk < bsz ? dinv[K0 + kk] : 0.0;
+            for (int a = 0; a < RPT; ++a) fail = fail || (ci[a] != 0.0 && ty + kGrid * a < np);
+        }
+        fail = fail || !(dk >= 0.0) || !isfinite(dk);
 #pragma unroll
-                for (int j = kk + 1; j < kBlk; ++j) Ld[j][kk] = j < bsz ? A[(K0 + j) * ld + K0 + kk] : 0.0;
+        for (int a = 0; a < RPT; ++a)
+#pragma unroll
+            for (int b = 0; b < CPT; ++b) v[a][b] -= ci[a] * cj[b];  // A -= c c^T / d_k (unpivoted LDLT)
+        // column k+1 is final after step k: its owners publish it and the next pivot
+        const int kn = k + 1;
+        if (tx == (kn & (kGrid - 1)) && kn < np) {
+            const int bn = kn / kGrid;
+            double vc[RPT];
+#pragma unroll
+            for (int a = 0; a < RPT; ++a) {  // v[a][bn] by selects (no dynamic register indexing)
+                vc[a] = v[a][0];
+#pragma unroll
+                for (int b = 1; b < CPT; ++b) vc[a] = b == bn ? v[a][b] : vc[a];
             }
-            for (int i = K0 + bsz + tid; i <= np; i += kThreads) {
-                double seg[kBlk], cs[kBlk];
+            double dn = 0.0;
 #pragma unroll
-                for (int j = 0; j < kBlk; ++j) seg[j] = j < bsz ? A[i * ld + K0 + j] : 0.0;
-                bool bad = false;
-#pragma unroll
-                for (int kk = 0; kk < kBlk; ++kk) {
-                    const double c = seg[kk];
-#pragma unroll
-                    for (int j = kk + 1; j < kBlk; ++j) seg[j] -= c * Ld[j][kk];
-                    cs[kk] = c;
-                    if (kk < bsz && inv[kk] == 0.0 && c != 0.0) bad = true;
-                    seg[kk] = inv[kk] != 0.0 ? c * inv[kk] : c;
-                }
-                if (bad && i < np) s_fail = 1;
-#pragma unroll
-                for (int kk = 0; kk < kBlk; ++kk)
-                    if (kk < bsz) {
-                        LT[kk * ld + i] = seg[kk];
-                        WD[i * kBlk + kk] = cs[kk];  // = l * d (the unscaled column entry)
-                        A[i * ld + K0 + kk] = seg[kk];
-                    }
+            for (int a = 0; a < RPT; ++a) {
+                const int i = ty + kGrid * a;
+                if (i >= kn && i <= np) nxt[i] = vc[a];
+                dn = i == kn ? vc[a] : dn;
+            }
+            if (ty == (kn & (kGrid - 1))) {  // the diagonal entry's owner
+                dv[kn] = dn;
+                dinv[kn] = dn != 0.0 ? __drcp_rn(dn) : 0.0;
             }
         }
         __syncthreads();
-        SOLVE_PROBE(2)
-        // (3) trailing update A[i][j] -= sum_kk (L D)_i,kk L_j,kk for K0+bsz <= j <= i (j < np)
-        for (int i = K0 + bsz + warp; i <= np; i += kWarps) {
-            double w[kBlk];
-#pragma unroll
-            for (int kk = 0; kk < kBlk; ++kk) w[kk] = kk < bsz ? WD[i * kBlk + kk] : 0.0;
-            for (int j = K0 + bsz + lane; j <= i && j < np; j += 32) {
-                double acc = A[i * ld + j];
-#pragma unroll
-                for (int kk = 0; kk < kBlk; ++kk)
-                    if (kk < bsz) acc -= w[kk] * LT[kk * ld + j];
-                A[i * ld + j] = acc;
-            }
-        }
-        __syncthreads();
-        SOLVE_PROBE(3)
     }
-    if (s_fail) return false;
-    if (s_zero) {
-        for (int i = tid; i < np; i += kThreads) x_out[i] = 0.0;
-        __syncthreads();
-        return true;
+    SOLVE_PROBE(1)
+    if (__syncthreads_or(fail)) return false;
+    // store L = C D^-1 (strictly lower) and z = D^-1 y (row np); |d| <= DBL_MIN: pseudo-inverse 0
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) {
+        const int i = ty + kGrid * a;
+#pragma unroll
+        for (int b = 0; b < CPT; ++b) {
+            const int j = tx + kGrid * b;
+            if (j < i && j < np && i <= np) A[i * ld + j] = fabs(dv[j]) > DBL_MIN ? v[a][b] * dinv[j] : 0.0;
+        }
     }
-    // z = D^-1 L^-1 P b sits in row np (pseudo-inverse of D: |d| <= DBL_MIN -> 0)
-    for (int i = tid; i < np; i += kThreads) x[i] = fabs(A[i * ld + i]) > DBL_MIN ? A[np * ld + i] : 0.0;
     __syncthreads();
+    SOLVE_PROBE(2)
     // backward substitution L^T x = z on warp 0, column-oriented: lane l keeps
     // z_l, z_{l+32}, z_{l+64} in registers; once x_i = z_i is final it is
-    // broadcast and every z_j (j < i) takes its L_ij x_i term (no barriers)
+    // broadcast and every z_r (r < i) takes its L_ir x_i term (no barriers)
     if (warp == 0) {
-        double z0 = lane < np ? x[lane] : 0.0, z1 = lane + 32 < np ? x[lane + 32] : 0.0;
-        double z2 = lane + 64 < np ? x[lane + 64] : 0.0;
+        __syncwarp();
+        const double* z = A + np * ld;
+        double z0 = lane < np ? z[lane] : 0.0, z1 = lane + 32 < np ? z[lane + 32] : 0.0;
+        double z2 = lane + 64 < np ? z[lane + 64] : 0.0;
         for (int i = np - 1; i >= 0; --i) {
             const int sl = i >> 5;
             const double own = sl == 0 ? z0 : sl == 1 ? z1 : z2;
@@ -339,15 +287,18 @@ __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, c
             if (lane + 32 < i) z1 -= Li[lane + 32] * xi;
             if (lane + 64 < i) z2 -= Li[lane + 64] * xi;
         }
-        if (lane < np) x[lane] = z0;
-        if (lane + 32 < np) x[lane + 32] = z1;
-        if (lane + 64 < np) x[lane + 64] = z2;
+        if (lane < np) x_out[lane] = z0;
+        if (lane + 32 < np) x_out[lane + 32] = z1;
+        if (lane + 64 < np) x_out[lane + 64] = z2;
     }
     __syncthreads();
-    SOLVE_PROBE(4)
-    for (int i = tid; i < np; i += kThreads) x_out[perm[i]] = x[i];
-    __syncthreads();
+    SOLVE_PROBE(3)
     return true;
+}
+
+__device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, const Layout& L, double* x_out) {
+    if (np <= 63) return ldlt_solve_regs<4, 4>(sys, np, smem, L, x_out);  // rows <= 64, columns <= 64
+    return ldlt_solve_regs<7, 6>(sys, np, smem, L, x_out);                // np <= 96: rows <= 112, columns <= 96
 }
 
 // ---------------------------------------------------------------------------

@@ -4,6 +4,8 @@
 __device__ long long g_ph[8];
 #define SOLVE_PROBE_BEGIN long long _pt = clock64(); if (threadIdx.x == 0) for (int _i = 0; _i < 8; ++_i) g_ph[_i] = 0;
 #define SOLVE_PROBE(i) if (threadIdx.x == 0) { const long long _t = clock64(); g_ph[i] += _t - _pt; _pt = _t; }
+__device__ long long g_loop[128];
+#define SOLVE_LOOP_PROBE(i) if (threadIdx.x == 0 && (i) < 128) g_loop[i] = clock64();
 #include "../paper_2208_04726_b200/csrc/ba.cu"
 #include <cstdio>
 #include <cstdlib>
@@ -20,7 +22,9 @@ __global__ void micro(const double* sys, int np, double* x, long long* t) {
     if (threadIdx.x == 0) {
         t[0] = t1 - t0;
         t[1] = ok;
-        printf("  stage+perm %lld diag %lld panel %lld trailing %lld backsub %lld\n", g_ph[0], g_ph[1], g_ph[2], g_ph[3], g_ph[4]);
+        printf("  load %lld factor %lld store %lld backsub %lld | loop deltas", g_ph[0], g_ph[1], g_ph[2], g_ph[3]);
+        for (int i = np - 1; i > np - 12 && i > 0; --i) printf(" %lld", g_loop[i - 1] - g_loop[i]);
+        printf("\n");
     }
 }
 // the same solve repeated (enough warp-state samples for an ncu source view)
@@ -58,6 +62,20 @@ int main(int argc, char** argv) {
             cudaFuncSetAttribute(pvo_dev::micro_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
             pvo_dev::micro_loop<<<1, 256, L.total>>>(dsys, np, dx, argc > 2 ? atoi(argv[2]) : 200);
             cudaDeviceSynchronize();
+        }
+        {  // steady-state time per solve: 200 back-to-back solves in one launch (CUDA events)
+            cudaFuncSetAttribute(pvo_dev::micro_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
+            cudaEvent_t e0, e1;
+            cudaEventCreate(&e0);
+            cudaEventCreate(&e1);
+            pvo_dev::micro_loop<<<1, 256, L.total>>>(dsys, np, dx, 20);
+            cudaEventRecord(e0);
+            pvo_dev::micro_loop<<<1, 256, L.total>>>(dsys, np, dx, 200);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            printf("np=%d loop: %.2f us per solve\n", np, ms * 1e3 / 200);
         }
         for (int rep = 0; rep < 3; ++rep) {
             pvo_dev::micro<<<1, 256, L.total>>>(dsys, np, dx, dt);
