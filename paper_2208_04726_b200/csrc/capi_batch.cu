@@ -194,6 +194,8 @@ int pvo_batch_iteration(pvo_ctx* ctx, int iterations, double damping, float* cor
         cuda_check(cudaMemsetAsync(B.status.p, 0, sizeof(int) * B.n_windows, ctx->stream), "memset");
         cuda_check(cudaMemsetAsync(B.status2.p, 0, sizeof(int) * 2 * B.n_windows, ctx->stream), "memset");
         cuda_check(cudaMemsetAsync(B.n_norms.p, 0, sizeof(int) * B.n_windows, ctx->stream), "memset");
+        cuda_check(cudaMemsetAsync(B.norms.p, 0, sizeof(double) * B.n_windows * Batch::kNormStride, ctx->stream),
+                   "memset");
         record_timing(ctx, 0);
         pvo_dev::CorrTmaParams cp;
         cp.n_edges = B.n_edges;

@@ -49,6 +49,9 @@ struct pvo_dgraph {
             if (bytes <= d.cap) return;
             DevBuf n;
             n.get(std::max(bytes, 2 * d.cap));
+            // zero the new allocation first: the copy below moves the old capacity, whose
+            // tail past the live entries was never written (compute-sanitizer initcheck)
+            cuda_check(cudaMemsetAsync(n.p, 0, n.cap, ctx->stream), "grow");
             if (d.p) cuda_check(cudaMemcpyAsync(n.p, d.p, d.cap, cudaMemcpyDeviceToDevice, ctx->stream), "grow");
             cuda_check(cudaStreamSynchronize(ctx->stream), "grow");
             d.release();

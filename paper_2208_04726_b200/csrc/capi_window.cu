@@ -210,6 +210,8 @@ int pvo_window_iteration(pvo_ctx* ctx, int iterations, double damping, float* co
             cuda_check(cudaEventRecord(ctx->ev_copy, ctx->copy_stream), "event");
         }
         pvo_dev::BAParams a = window_ba_params(ctx, iterations, damping);
+        // the read-back copies the whole norms buffer: no uninitialised tail
+        cuda_check(cudaMemsetAsync(a.residual_norms, 0, ctx->ba.norms.cap, ctx->stream), "memset");
         launch_ba_checked(ctx, a, w.plan);
         record_timing(ctx, 2);
         ctx->timing_pending = ctx->timing;
@@ -228,6 +230,8 @@ int pvo_window_ba(pvo_ctx* ctx, int iterations, double damping) {
         if (iterations > PVO_MAX_WINDOW_ITERATIONS) fail(PVO_INVALID_ARGUMENT, "ba: too many iterations");
         reset_status(ctx);
         pvo_dev::BAParams a = window_ba_params(ctx, iterations, damping);
+        // the read-back copies the whole norms buffer: no uninitialised tail
+        cuda_check(cudaMemsetAsync(a.residual_norms, 0, ctx->ba.norms.cap, ctx->stream), "memset");
         launch_ba_checked(ctx, a, w.plan);
     });
 }

@@ -198,12 +198,17 @@ __global__ void __launch_bounds__(256, PVO_MEASURE_MINB) measure_kernel(MeasureP
     }
     double dxo = 0, dyo = 0, wgt = 0.01;
     int flags = 0;
+    const bool valid = !behind && isfinite(cx) && isfinite(cy);
     if (behind) {
         flags = 4;  // flow_provider.cpp:301-302
-    } else if (!isfinite(cx) || !isfinite(cy)) {
+    } else if (!valid) {
         flags = 8;
         if (lane == 0 && level == 0) atomicOr(a.status, 1 << kDevBadCoords);
-    } else {
+    }
+    // level-0 results carried across the pair's barrier
+    bool flat = true, border0 = false;
+    double confidence = 0.01, p0x = 0, p0y = 0;
+    if (valid) {
         const int slot = a.e_slot ? a.e_slot[e] : a.pose_slot[a.e_pose[e]];
         const float* gp = a.patch_feats + (size_t)a.e_patch[e] * 2 * 9 * a.channels;
         const Level L = level ? Level{a.feat1 + (size_t)slot * a.h1 * a.w1 * a.channels, a.w1, a.h1}
@@ -233,39 +238,41 @@ __global__ void __launch_bounds__(256, PVO_MEASURE_MINB) measure_kernel(MeasureP
                 s_peak1[pair][1] = py;
                 s_border1[pair] = border;
             }
-            asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
-            return;
-        }
-        // level 0: flatness / sharpness scores on the slice (flow_provider.cpp:217-250)
-        double peak = -CUDART_INF, minimum = CUDART_INF, mean = 0;
-        int peak_a = 0, peak_b = 0;
-        for (int i = 0; i < kS * kS; ++i) {
-            const double val = v[i];
-            mean += val;
-            minimum = fmin(minimum, val);
-            if (val > peak) {
-                peak = val;
-                peak_a = i / kS;
-                peak_b = i % kS;
-            }
-        }
-        mean /= kS * kS;
-        const double peak_to_mean = (peak - minimum) / (mean - minimum + 1e-9);
-        bool flat = !(peak_to_mean >= 1.05);
-        double confidence = 0.01, p0x = 0, p0y = 0;
-        bool border0 = false;
-        if (!flat) {
-            double second = -CUDART_INF;
+        } else {
+            // level 0: flatness / sharpness scores on the slice (flow_provider.cpp:217-250)
+            double peak = -CUDART_INF, minimum = CUDART_INF, mean = 0;
+            int peak_a = 0, peak_b = 0;
             for (int i = 0; i < kS * kS; ++i) {
-                const int alpha = i / kS, beta = i % kS;
-                if (max(abs(alpha - peak_a), abs(beta - peak_b)) <= 1) continue;
-                second = fmax(second, v[i]);
+                const double val = v[i];
+                mean += val;
+                minimum = fmin(minimum, val);
+                if (val > peak) {
+                    peak = val;
+                    peak_a = i / kS;
+                    peak_b = i % kS;
+                }
             }
-            const double score = 2.0 * (peak - 0.75) + (peak - second - 0.08);
-            confidence = fmin(fmax(1.0 / (1.0 + exp(-12.0 * score)), 0.01), 0.99);
-            subpixel_peak(L, a.channels, g, bx, by, v, &p0x, &p0y, &border0);
+            mean /= kS * kS;
+            const double peak_to_mean = (peak - minimum) / (mean - minimum + 1e-9);
+            flat = !(peak_to_mean >= 1.05);
+            if (!flat) {
+                double second = -CUDART_INF;
+                for (int i = 0; i < kS * kS; ++i) {
+                    const int alpha = i / kS, beta = i % kS;
+                    if (max(abs(alpha - peak_a), abs(beta - peak_b)) <= 1) continue;
+                    second = fmax(second, v[i]);
+                }
+                const double score = 2.0 * (peak - 0.75) + (peak - second - 0.08);
+                confidence = fmin(fmax(1.0 / (1.0 + exp(-12.0 * score)), 0.01), 0.99);
+                subpixel_peak(L, a.channels, g, bx, by, v, &p0x, &p0y, &border0);
+            }
         }
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+    }
+    // the pair meets on its named barrier at one program point, unconditionally (also
+    // for behind / non-finite edges), each warp converged: bar.sync counts threads
+    __syncwarp();
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+    if (valid && level == 0) {
         if (flat) {
             flags = 1;  // flat: delta 0, weight 0.01
         } else {
