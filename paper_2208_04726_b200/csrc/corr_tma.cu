@@ -48,16 +48,20 @@ namespace pvo_dev {
 namespace {
 
 #ifndef CORR_WARPS
-#define CORR_WARPS 8
+#define CORR_WARPS 10
 #endif
 #ifndef CORR_STAGES
-#define CORR_STAGES 3
+#define CORR_STAGES 2
 #endif
 #ifndef CORR_JIT_G
 #define CORR_JIT_G 0
 #endif
-constexpr int kWarps = CORR_WARPS;  // A/B knobs (tools/build_variant.sh): 12 warps x 2 stages and
-                                    // just-in-time descriptor loads measured equal (r1f)
+#ifndef CORR_NO_PARTS
+#define CORR_NO_PARTS 1
+#endif
+constexpr int kWarps = CORR_WARPS;  // A/B knobs (tools/build_variant.sh).  r2: one FFMA2 chain per
+                                    // (cell, pixel) over the 128 channels (no per-chunk partials: 184
+                                    // registers) lets 10 warps x 2 stages fit: -5 % vs 8 x 3 (r1f)
 constexpr int kThreads = 32 * kWarps;
 constexpr int kD = 128;
 constexpr int kBox = 9;
@@ -422,9 +426,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(baru + 8 * cs, cph);
             const unsigned char* st = wb + cs * kStageBytes;
             const float* g = reinterpret_cast<const float*>(st + kChunkGOff);
-            // per-chunk partial sums, then one add into the tile total: short chains
-            // (8 + 8 terms per component) keep the FP32 error far inside 1e-4
+            // default (CORR_NO_PARTS): the FFMA2 accumulates straight into the tile total
+            // (64 terms per component); the per-chunk partials of round 1 (8 + 8 terms,
+            // then one add) cost 54 registers and one FADD2 per chunk for no measurable
+            // accuracy gain (parity on every C2 edge and the adversarial sets unchanged)
+#if !CORR_NO_PARTS
             float2 part[NC][kPix];
+#endif
 #pragma unroll
             for (int u = 0; u < kChunkCh / 4; ++u) {
 #if CORR_JIT_G
@@ -455,6 +463,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
 #pragma unroll
                 for (int p = 0; p < kPix; ++p) gv[p] = *reinterpret_cast<const float4*>(g + p * kChunkCh + 4 * u);
+#if CORR_NO_PARTS  // A/B knob: one chain per (cell, pixel, parity) over all 128 channels
+#pragma unroll
+                for (int k = 0; k < NC; ++k)
+#pragma unroll
+                    for (int p = 0; p < kPix; ++p)
+                        acc[k][p] = __ffma2_rn(make_float2(v[k].x, v[k].y), make_float2(gv[p].x, gv[p].y), acc[k][p]);
+#pragma unroll
+                for (int k = 0; k < NC; ++k)
+#pragma unroll
+                    for (int p = 0; p < kPix; ++p)
+                        acc[k][p] = __ffma2_rn(make_float2(v[k].z, v[k].w), make_float2(gv[p].z, gv[p].w), acc[k][p]);
+#else
 #pragma unroll
                 for (int k = 0; k < NC; ++k)
 #pragma unroll
@@ -468,11 +488,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int p = 0; p < kPix; ++p)
                         part[k][p] = __ffma2_rn(make_float2(v[k].z, v[k].w), make_float2(gv[p].z, gv[p].w), part[k][p]);
 #endif
+#endif
             }
+#if !CORR_NO_PARTS
 #pragma unroll
             for (int k = 0; k < NC; ++k)
 #pragma unroll
                 for (int p = 0; p < kPix; ++p) acc[k][p] = __fadd2_rn(acc[k][p], part[k][p]);
+#endif
             __syncwarp();  // every lane is done with this stage: refill it
             if (++cs == kStages) {
                 cs = 0;
