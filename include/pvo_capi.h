@@ -14,7 +14,8 @@
  *             world -> camera, Eigen coefficient order (se3.hpp:38-61).
  *   K         4 doubles: fx, fy, cx, cy (camera.hpp:10-23).
  *   patch     p*p x-coordinates and p*p y-coordinates, row-major
- *             (camera.hpp:29-38); the GPU kernels require p == 3.
+ *             (camera.hpp:29-38); camera ops and pvo_correlate take any p,
+ *             the batched correlation / BA kernels require p == 3.
  *   features  HWC fp32, data[(y*W + x)*C + c]  (features.hpp:14-36).
  *   corr out  [2][p*p][7][7] fp32 per edge, index ((v*p+u)*7+alpha)*7+beta
  *             (correlation.hpp:17-26).
@@ -96,11 +97,27 @@ int pvo_reprojection_jacobians(pvo_ctx* ctx, int n, int p, const double* poses_i
 
 /* ---- correlation (correlation.hpp:33-44) ----------------------------------
  * pvo_correlate: one patch against one host pyramid (the reference signature,
- * correlation.cpp:37-71).  feats0/feats1: [p*p][C]; coords [p*p][2].
+ * correlation.cpp:37-71).  feats0/feats1: [p*p][C]; coords [p*p][2].  Any
+ * patch width p (p = 3 runs the production Gram-form kernel, others the
+ * direct FP64 form); the pyramid is cached on the device (below).
  * Throws (returns) INVALID_ARGUMENT on non-finite coordinates.            */
 int pvo_correlate(pvo_ctx* ctx, int p, int channels, const float* feats0, const float* feats1,
                   const float* level0, int w0, int h0, const float* level1, int w1, int h1,
                   const double* coords, float* out);
+/* correlate_at / correlate_at_cubic (correlation.hpp:37-44, correlation.cpp:8-35)
+ * at n free level-space points: features [n][C] (one query descriptor per
+ * point), xy [n][2], against ONE host grid [h][w][C]; cubic != 0 selects the
+ * Catmull-Rom sampler (features.cpp:23-52).  out [n] FP64.                 */
+int pvo_correlate_points(pvo_ctx* ctx, int n, int channels, const float* features, const float* grid, int w,
+                         int h, const double* xy, int cubic, double* out);
+/* The host grids passed to pvo_correlate / pvo_correlate_points stay on the
+ * device, keyed by address + shape + a sampled-content fingerprint (LRU within
+ * PVO_GRID_CACHE_MB, default 4096): a provider-owned pyramid is uploaded once,
+ * not on every call.  Grids must not be modified in place while cached
+ * (the reference never does: pyramids are built once per frame); clear the
+ * cache if they are.                                                         */
+int pvo_grid_cache_stats(pvo_ctx* ctx, int64_t* hits, int64_t* misses, int* entries, int64_t* bytes);
+int pvo_grid_cache_clear(pvo_ctx* ctx);
 
 /* Frame store: device-resident pyramids for n_frames slots, plus the per-cell
  * Gram terms the normalised correlation needs (computed at upload).

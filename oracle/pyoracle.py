@@ -265,6 +265,15 @@ def correlate_at(feature, grid, x, y):
     return out.value
 
 
+def correlate_at_cubic(feature, grid, x, y):
+    f = np.ascontiguousarray(feature, np.float32)
+    g = np.ascontiguousarray(grid, np.float32)
+    out = D()
+    check(lib.orc_correlate_at_cubic(_p(f), I(f.shape[0]), _p(g), I(g.shape[1]), I(g.shape[0]), D(x), D(y),
+                                     C.byref(out)))
+    return out.value
+
+
 def sample_zero_padded(grid, x, y, c):
     g = np.ascontiguousarray(grid, np.float32)
     out = D()

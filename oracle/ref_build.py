@@ -13,6 +13,14 @@ travels to the GPU box with the snapshot):
 * pvo_ref_tests   - the reference's own unit tests (proj/tests/test_*.cpp,
                     doctest suites se3 camera patch_graph bundle_adjust
                     features simulator trajectory pipeline) linked against it.
+* pvo_dropin_tests - the SAME reference tests linked against the product's
+                    drop-in operator layer instead: the reference's sources
+                    minus camera.cpp / correlation.cpp / bundle_adjust.cpp,
+                    plus paper_2208_04726_b200/dropin/*.cpp (the reference's
+                    declared operators implemented over the C-ABI) and
+                    libpvo_b200.so.  Run on the GPU box by tests/test_dropin.py:
+                    the reference's own test cases exercise the sm_100a
+                    kernels through the reference's C++ signatures.
 
 The reference's CMake build itself is not run (it needs cmake + system
 Eigen/libpng/vendor trees); this script is the committed recipe instead.
@@ -42,6 +50,11 @@ FLAGS = ["g++", "-std=c++20", "-O3", "-DNDEBUG", "-fPIC", "-pthread", "-w", "-I"
 
 LIB = OUT / "libpvo_ref.so"
 TESTS = OUT / "pvo_ref_tests"
+DROPIN_TESTS = OUT / "pvo_dropin_tests"
+PKG = ROOT / "paper_2208_04726_b200"
+DROPIN = PKG / "dropin"
+# reference translation units the drop-in layer replaces
+DROPIN_REPLACES = {"camera", "correlation", "bundle_adjust"}
 
 
 def available() -> bool:
@@ -83,7 +96,32 @@ def build(force: bool = False) -> Path | None:
         tmp = TESTS.with_suffix(".tmp")
         subprocess.run(FLAGS + [*map(str, test_objs), *map(str, lib_objs), "-o", str(tmp)], check=True)
         os.replace(tmp, TESTS)
+    build_dropin(objs[: len(LIB_SOURCES)], test_objs, force)
     return LIB
+
+
+def build_dropin(lib_objs: list[Path], test_objs: list[Path], force: bool = False) -> Path | None:
+    """Link the reference's tests against the drop-in layer + libpvo_b200.so."""
+    so = PKG / "libpvo_b200.so"
+    if not so.exists():
+        return None
+    extra = ["-I", str(ROOT / "include"), "-I", str(DROPIN)]
+    jobs = [(src, OBJ / f"{src.stem}.o", extra) for src in sorted(DROPIN.glob("*.cpp"))]
+    deps_newest = max(p.stat().st_mtime for p in DROPIN.glob("*.hpp"))
+    for src, obj, ex in jobs:
+        if obj.exists() and obj.stat().st_mtime < deps_newest:
+            obj.unlink()
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex_:
+        drop_objs = list(ex_.map(lambda j: _compile(*j), jobs))
+    kept = [o for o in lib_objs if o.stem not in DROPIN_REPLACES]
+    newest = max(o.stat().st_mtime for o in drop_objs + kept + test_objs + [so])
+    if force or not DROPIN_TESTS.exists() or DROPIN_TESTS.stat().st_mtime < newest:
+        tmp = DROPIN_TESTS.with_suffix(".tmp")
+        rpath = "-Wl,-rpath,$ORIGIN/../../paper_2208_04726_b200"
+        subprocess.run(FLAGS + [*map(str, test_objs), *map(str, kept), *map(str, drop_objs), "-L", str(PKG),
+                                "-lpvo_b200", rpath, "-o", str(tmp)], check=True)
+        os.replace(tmp, DROPIN_TESTS)
+    return DROPIN_TESTS
 
 
 if __name__ == "__main__":

@@ -25,7 +25,11 @@ from .api import (  # noqa: F401
     build_target,
     compose,
     correlate,
+    correlate_at,
+    correlate_at_cubic,
     correlate_batch,
+    correlate_points,
+    grid_cache_stats,
     default_context,
     gauss_newton_step,
     inverse,

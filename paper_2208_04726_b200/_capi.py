@@ -48,6 +48,9 @@ SIGNATURES = {
     "pvo_reproject_patches": (i32, [vp, i32, i32, P, P, P, P, P, P, P, P]),
     "pvo_reprojection_jacobians": (i32, [vp, i32, i32, P, P, P, P, P, P, P, P]),
     "pvo_correlate": (i32, [vp, i32, i32, P, P, P, i32, i32, P, i32, i32, P, P]),
+    "pvo_correlate_points": (i32, [vp, i32, i32, P, P, i32, i32, P, i32, P]),
+    "pvo_grid_cache_stats": (i32, [vp, P, P, P, P]),
+    "pvo_grid_cache_clear": (i32, [vp]),
     "pvo_frames_reserve": (i32, [vp, i32, i32, i32, i32, i32, i32]),
     "pvo_frames_upload": (i32, [vp, i32, P, P, i32]),
     "pvo_frames_refresh": (i32, [vp, i32]),

@@ -366,6 +366,38 @@ def correlate(patch_features, pyramid, reprojection, ctx: Optional[Context] = No
     return out
 
 
+def correlate_points(features, grid, xy, cubic: bool = False, ctx: Optional[Context] = None) -> np.ndarray:
+    """correlate_at / correlate_at_cubic (correlation.cpp:8-35) at n level-space
+    points: features [n, C], grid [H, W, C], xy [n, 2] -> [n] float64."""
+    f = _f32(features)
+    g = _f32(grid)
+    q = _f64(xy).reshape(-1, 2)
+    n = q.shape[0]
+    if g.ndim != 3 or f.reshape(n, -1).shape[1] != g.shape[2]:
+        raise ValueError("correlate_at: channel count mismatch")
+    out = np.empty(n, np.float64)
+    check(lib.pvo_correlate_points(_ctx(ctx).handle, n, g.shape[2], _ptr(f), _ptr(g), g.shape[1], g.shape[0], _ptr(q),
+                                   1 if cubic else 0, _ptr(out)))
+    return out
+
+
+def correlate_at(feature, grid, x: float, y: float, ctx: Optional[Context] = None) -> float:
+    """correlate_at (correlation.cpp:8-23) of one descriptor at one position."""
+    return float(correlate_points(np.asarray(feature)[None], grid, [[x, y]], False, ctx)[0])
+
+
+def correlate_at_cubic(feature, grid, x: float, y: float, ctx: Optional[Context] = None) -> float:
+    """correlate_at_cubic (correlation.cpp:25-35) of one descriptor at one position."""
+    return float(correlate_points(np.asarray(feature)[None], grid, [[x, y]], True, ctx)[0])
+
+
+def grid_cache_stats(ctx: Optional[Context] = None) -> dict:
+    """Device grid cache of the reference-signature correlation calls."""
+    v = [C.c_int64(), C.c_int64(), C.c_int(), C.c_int64()]
+    check(lib.pvo_grid_cache_stats(_ctx(ctx).handle, *[C.addressof(x) for x in v]))
+    return {"hits": v[0].value, "misses": v[1].value, "entries": v[2].value, "bytes": v[3].value}
+
+
 def correlate_batch(e_patch, e_slot, coords, patch_feats, ctx: Optional[Context] = None) -> np.ndarray:
     """Batched correlate over the context's frame store: out [E, 2, 9, 7, 7]."""
     c = _ctx(ctx)

@@ -148,6 +148,22 @@ struct Batch {
     }
 };
 
+// A host feature grid mirrored on the device (the reference-signature calls
+// pvo_correlate / pvo_correlate_points take host FeatureGrids).  Keyed by the
+// host address, shape and a fingerprint of sampled contents: the reference's
+// providers build each pyramid once and never modify it (flow_provider.cpp
+// add_frame), so a pyramid is uploaded (and its Gram terms derived) once
+// instead of on every call.  LRU within a byte budget (PVO_GRID_CACHE_MB).
+struct GridEntry {
+    const void* host = nullptr;
+    int w = 0, h = 0, C = 0;
+    uint64_t fp = 0;
+    DevBuf feat, gram;
+    bool has_gram = false;
+    uint64_t tick = 0;
+    size_t bytes = 0;
+};
+
 struct pvo_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -177,6 +193,10 @@ struct pvo_ctx {
     bool timing_pending = false;
     bool tracing = false;  // record BA phase clocks (pvo_ctx_set_tracing)
     bool timing = true;    // record the per-iteration timing events (pvo_ctx_set_timing)
+    std::vector<GridEntry*> grids;  // host-grid cache (GridEntry above)
+    uint64_t grid_tick = 0;
+    size_t grid_bytes = 0;
+    int64_t grid_hits = 0, grid_misses = 0;
     std::mt19937_64 oracle_rng{0};  // the oracle provider's RNG (flow_provider.cpp:10, rng_(noise.seed))
     int* d_corr_ctl = nullptr;      // correlation tile queue: [list length, queue head, warps done, -]
     void* h_stage = nullptr;        // page-locked staging for small read-backs (async copies, one sync)
@@ -572,6 +592,82 @@ inline void run_corr(pvo_ctx* ctx, pvo_dev::CorrTmaParams t, int index_edges = 0
     cp.status = ctx->d_status;
     cuda_check(pvo_dev::launch_corr(cp, ctx->stream), "corr kernel");
     ctx->launches += 1;
+}
+
+// Fingerprint of a host grid: its size and 256 evenly spaced samples.
+inline uint64_t grid_fingerprint(const float* data, size_t n) {
+    uint64_t h = 1469598103934665603ull ^ n;
+    if (!n) return h;
+    const size_t samples = std::min<size_t>(n, 256);
+    for (size_t i = 0; i < samples; ++i) {
+        uint32_t bits;
+        std::memcpy(&bits, data + (samples == 1 ? 0 : i * (n - 1) / (samples - 1)), 4);
+        h = (h ^ bits) * 1099511628211ull;
+    }
+    return h;
+}
+
+inline void grid_cache_clear(pvo_ctx* ctx) {
+    for (GridEntry* e : ctx->grids) {
+        e->feat.release();
+        e->gram.release();
+        delete e;
+    }
+    ctx->grids.clear();
+    ctx->grid_bytes = 0;
+}
+
+// The device copy of host grid [h][w][C] (uploaded on a miss; Gram terms
+// derived when `gram` is asked for).  Stream-ordered: the caller syncs before
+// the host buffer may change.
+inline GridEntry* cached_grid(pvo_ctx* ctx, const float* host, int w, int h, int C, bool gram) {
+    const size_t n = (size_t)std::max(w, 0) * std::max(h, 0) * C;
+    const uint64_t fp = grid_fingerprint(host, n);
+    GridEntry* hit = nullptr;
+    for (GridEntry* e : ctx->grids)
+        if (e->host == host && e->w == w && e->h == h && e->C == C && e->fp == fp) hit = e;
+    if (hit) {
+        ++ctx->grid_hits;
+    } else {
+        ++ctx->grid_misses;
+        const size_t bytes = sizeof(float) * (n + (size_t)std::max(pvo_dev::gram_stride(w) * h, 1) * 8);
+        const char* mb = std::getenv("PVO_GRID_CACHE_MB");
+        const size_t cap = (size_t)(mb ? std::max(1L, std::atol(mb)) : 4096L) << 20;
+        while (ctx->grid_bytes + bytes > cap) {  // evict least recently used (never the one this call just used)
+            auto lru = std::min_element(ctx->grids.begin(), ctx->grids.end(),
+                                        [](const GridEntry* a, const GridEntry* b) { return a->tick < b->tick; });
+            if (lru == ctx->grids.end() || (*lru)->tick == ctx->grid_tick) break;
+            ctx->grid_bytes -= (*lru)->bytes;
+            cuda_check(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");  // in-flight readers
+            (*lru)->feat.release();
+            (*lru)->gram.release();
+            delete *lru;
+            ctx->grids.erase(lru);
+        }
+        hit = new GridEntry;
+        hit->host = host;
+        hit->w = w;
+        hit->h = h;
+        hit->C = C;
+        hit->fp = fp;
+        hit->bytes = bytes;
+        ctx->grids.push_back(hit);
+        ctx->grid_bytes += bytes;
+        upload(ctx, hit->feat, host, n);
+    }
+    hit->tick = ++ctx->grid_tick;
+    if (gram && !hit->has_gram) {
+        float* g = hit->gram.as<float>((size_t)std::max(pvo_dev::gram_stride(w) * h, 1) * 8);
+        cuda_check(cudaMemsetAsync(g, 0, hit->gram.cap, ctx->stream), "memset");
+        if (n) {
+            cuda_check(pvo_dev::launch_gram(static_cast<const float*>(hit->feat.p), g, w, h, nullptr, nullptr, 0, 0, C,
+                                            ctx->num_sms, ctx->stream),
+                       "gram kernel");
+            ctx->launches += 1;
+        }
+        hit->has_gram = true;
+    }
+    return hit;
 }
 
 // Stable order of edges by frame-store slot (L2 locality of the TMA kernel).

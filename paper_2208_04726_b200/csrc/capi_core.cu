@@ -123,6 +123,7 @@ int pvo_ctx_destroy(pvo_ctx* ctx) {
         for (DevBuf* b : bufs) b->release();
         ctx->ba.release();
         ctx->bat.release();
+        grid_cache_clear(ctx);
         if (ctx->d_status) cudaFree(ctx->d_status);
         if (ctx->d_corr_ctl) cudaFree(ctx->d_corr_ctl);
         if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
@@ -289,24 +290,32 @@ int pvo_correlate(pvo_ctx* ctx, int p, int C, const float* feats0, const float* 
                   int h0, const float* level1, int w1, int h1, const double* coords, float* out) {
     return guarded([&] {
         bind(ctx);
-        ensure_p3(p);
-        if (C < 1 || w0 < 0 || h0 < 0 || w1 < 0 || h1 < 0) fail(PVO_INVALID_ARGUMENT, "correlate: bad sizes");
-        for (int k = 0; k < p * p; ++k)
+        if (p < 1 || C < 1 || w0 < 0 || h0 < 0 || w1 < 0 || h1 < 0) fail(PVO_INVALID_ARGUMENT, "correlate: bad sizes");
+        const int pp = p * p;
+        for (int k = 0; k < pp; ++k)
             if (!finite2(coords + 2 * k)) fail(PVO_INVALID_ARGUMENT, "correlate: non-finite reprojection");
-        const size_t n0 = (size_t)w0 * h0 * C, n1 = (size_t)w1 * h1 * C;
-        float* f0 = upload(ctx, ctx->s0, level0, n0);
-        float* f1 = upload(ctx, ctx->s1, level1, n1);
-        float* g0 = ctx->s2.as<float>((size_t)pvo_dev::gram_stride(w0) * h0 * 8);
-        float* g1 = ctx->s3.as<float>((size_t)std::max(pvo_dev::gram_stride(w1) * h1, 1) * 8);
-        compute_gram(ctx, f0, g0, f1, g1, w0, h0, w1, h1, C);
-        float* pf = ctx->s4.as<float>((size_t)2 * 9 * C);
-        cuda_check(cudaMemcpyAsync(pf, feats0, sizeof(float) * 9 * C, cudaMemcpyHostToDevice, ctx->stream), "H2D");
-        cuda_check(cudaMemcpyAsync(pf + 9 * C, feats1, sizeof(float) * 9 * C, cudaMemcpyHostToDevice, ctx->stream),
+        // the pyramid stays on the device between calls (grid cache); Gram terms only for the 3x3 kernel
+        GridEntry* g0 = cached_grid(ctx, level0, w0, h0, C, p == 3);
+        GridEntry* g1 = cached_grid(ctx, level1, w1, h1, C, p == 3);
+        const float* f0 = static_cast<const float*>(g0->feat.p);
+        const float* f1 = static_cast<const float*>(g1->feat.p);
+        float* pf = ctx->s4.as<float>((size_t)2 * pp * C);
+        cuda_check(cudaMemcpyAsync(pf, feats0, sizeof(float) * pp * C, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+        cuda_check(cudaMemcpyAsync(pf + (size_t)pp * C, feats1, sizeof(float) * pp * C, cudaMemcpyHostToDevice,
+                                   ctx->stream),
                    "H2D");
-        double* dc = upload(ctx, ctx->s5, coords, 18);
+        double* dc = upload(ctx, ctx->s5, coords, (size_t)2 * pp);
+        float* dout = ctx->s7.as<float>((size_t)2 * pp * 49);
+        if (p != 3) {  // any other width: the direct FP64 form of correlation.cpp:8-71
+            cuda_check(pvo_dev::launch_corr_direct(pp, C, pf, dc, f0, w0, h0, f1, w1, h1, dout, ctx->stream),
+                       "corr_direct kernel");
+            ctx->launches += 1;
+            download(ctx, out, dout, (size_t)2 * pp * 49);
+            sync(ctx);
+            return;
+        }
         int zero = 0;
         int* idx = upload(ctx, ctx->s6, &zero, 1);
-        float* dout = ctx->s7.as<float>(2 * 9 * 49);
         reset_status(ctx);
         pvo_dev::CorrParams cp;
         cp.n_edges = 1;
@@ -316,8 +325,8 @@ int pvo_correlate(pvo_ctx* ctx, int p, int C, const float* feats0, const float* 
         cp.coords = dc;
         cp.feat0 = f0;
         cp.feat1 = f1;
-        cp.gram0 = g0;
-        cp.gram1 = g1;
+        cp.gram0 = static_cast<const float*>(g0->gram.p);
+        cp.gram1 = static_cast<const float*>(g1->gram.p);
         cp.w0 = w0;
         cp.h0 = h0;
         cp.w1 = w1;
@@ -329,6 +338,48 @@ int pvo_correlate(pvo_ctx* ctx, int p, int C, const float* feats0, const float* 
         ctx->launches += 1;
         download(ctx, out, dout, 2 * 9 * 49);
         if (read_status(ctx)) fail(PVO_INVALID_ARGUMENT, "correlate: non-finite reprojection");
+    });
+}
+
+int pvo_correlate_points(pvo_ctx* ctx, int n, int C, const float* features, const float* grid, int w, int h,
+                         const double* xy, int cubic, double* out) {
+    return guarded([&] {
+        bind(ctx);
+        if (n < 0 || C < 1 || w < 0 || h < 0) fail(PVO_INVALID_ARGUMENT, "correlate_at: bad sizes");
+        if (n == 0) return;
+        GridEntry* g = cached_grid(ctx, grid, w, h, C, false);
+        pvo_dev::PointsParams a;
+        a.n = n;
+        a.channels = C;
+        a.cubic = cubic ? 1 : 0;
+        a.features = upload(ctx, ctx->s0, features, (size_t)n * C);
+        a.xy = upload(ctx, ctx->s1, xy, (size_t)n * 2);
+        a.grid = static_cast<const float*>(g->feat.p);
+        a.W = w;
+        a.H = h;
+        a.out = ctx->s2.as<double>(n);
+        cuda_check(pvo_dev::launch_points(a, ctx->stream), "points kernel");
+        ctx->launches += 1;
+        download(ctx, out, a.out, n);
+        sync(ctx);
+    });
+}
+
+int pvo_grid_cache_stats(pvo_ctx* ctx, int64_t* hits, int64_t* misses, int* entries, int64_t* bytes) {
+    return guarded([&] {
+        if (!ctx) fail(PVO_INVALID_ARGUMENT, "null context");
+        if (hits) *hits = ctx->grid_hits;
+        if (misses) *misses = ctx->grid_misses;
+        if (entries) *entries = (int)ctx->grids.size();
+        if (bytes) *bytes = (int64_t)ctx->grid_bytes;
+    });
+}
+
+int pvo_grid_cache_clear(pvo_ctx* ctx) {
+    return guarded([&] {
+        bind(ctx);
+        sync(ctx);
+        grid_cache_clear(ctx);
     });
 }
 

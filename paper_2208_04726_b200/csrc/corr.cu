@@ -377,6 +377,23 @@ __global__ void gram_kernel(GramLevel l0, GramLevel l1, int D) {
     }
 }
 
+// correlate() for one patch of any width (correlation.cpp:37-71): block (pixel,
+// level), a warp per output over the 49 offsets, evaluated directly.
+__global__ void corr_direct_kernel(int pp, int C, const float* feats, const double* coords, const float* f0, int w0,
+                                   int h0, const float* f1, int w1, int h1, float* out) {
+    const int pix = blockIdx.x, level = blockIdx.y;
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const float* g = feats + ((size_t)level * pp + pix) * C;
+    const double scale = level == 0 ? 4.0 : 16.0;  // kFeatureStride, kFeatureStride^2 (correlation.cpp:51)
+    const double bx = coords[2 * pix] / scale, by = coords[2 * pix + 1] / scale;
+    for (int o = warp; o < 49; o += nw) {
+        const int alpha = o / 7, beta = o - 7 * alpha;
+        const float r = level == 0 ? corr_exact_warp(g, f0, w0, h0, C, bx + (beta - 3), by + (alpha - 3))
+                                   : corr_exact_warp(g, f1, w1, h1, C, bx + (beta - 3), by + (alpha - 3));
+        if ((threadIdx.x & 31) == 0) out[((size_t)level * pp + pix) * 49 + o] = r;
+    }
+}
+
 }  // namespace
 
 int corr_smem_bytes(int channels) { return corr_layout(channels).total_bytes; }
@@ -387,6 +404,13 @@ cudaError_t launch_corr(const CorrParams& p, cudaStream_t stream) {
     cudaError_t err = cudaFuncSetAttribute(corr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
     corr_kernel<<<p.n_edges, kThreads, smem, stream>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_corr_direct(int pp, int C, const float* feats, const double* coords, const float* f0, int w0,
+                               int h0, const float* f1, int w1, int h1, float* out, cudaStream_t stream) {
+    if (pp <= 0) return cudaSuccess;
+    corr_direct_kernel<<<dim3(pp, 2), 256, 0, stream>>>(pp, C, feats, coords, f0, w0, h0, f1, w1, h1, out);
     return cudaGetLastError();
 }
 

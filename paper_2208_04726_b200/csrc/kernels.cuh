@@ -37,6 +37,11 @@ struct CorrParams {
 
 int corr_smem_bytes(int channels);
 cudaError_t launch_corr(const CorrParams& p, cudaStream_t stream);
+// correlate() of ONE patch of any width p (pp = p * p pixels) evaluated
+// directly as the reference does (FP64 samples and sums, corr_exact.cuh):
+// feats [2][pp][C], coords [pp][2] -> out [2][pp][49].
+cudaError_t launch_corr_direct(int pp, int channels, const float* feats, const double* coords, const float* f0,
+                               int w0, int h0, const float* f1, int w1, int h1, float* out, cudaStream_t stream);
 
 // K2 production path (corr_tma.cu): D = 128, TMA pipeline, persistent CTAs.
 struct CorrTmaParams {
@@ -110,6 +115,18 @@ struct MeasureParams {
     int* status = nullptr;
 };
 cudaError_t launch_measure(const MeasureParams& p, cudaStream_t stream);
+
+// correlate_at / correlate_at_cubic at n free level-space points against one
+// grid (measure.cu), FP64 like the reference (correlation.cpp:8-35).
+struct PointsParams {
+    int n = 0, channels = 0, cubic = 0;
+    const float* features = nullptr;  // [n][C]
+    const double* xy = nullptr;       // [n][2]
+    const float* grid = nullptr;      // [H][W][C]
+    int W = 0, H = 0;
+    double* out = nullptr;            // [n]
+};
+cudaError_t launch_points(const PointsParams& p, cudaStream_t stream);
 
 // OracleFlowProvider::propose on the resident window (measure.cu): two passes
 // around the host-side RNG draws (the reference's sequential mt19937_64 stream).

@@ -356,11 +356,76 @@ __global__ void oracle_propose_kernel(OracleParams a, int pass) {
     a.weight[2 * e + 1] = w;
 }
 
+
+// ---- correlate_at / correlate_at_cubic at free points (correlation.cpp:8-35) ----
+// One warp per query point, lanes over channels c = lane, lane + 32, ... (any C);
+// each channel's sample is the reference's per-channel expression
+// (features.cpp:9-52; this file is compiled with --fmad=false), the channel
+// sums a fixed warp tree.  Non-finite or out-of-int-range positions sample only
+// padding (the reference's int conversion of such a floor lands outside the
+// grid): the result is 0.
+__global__ void points_kernel(PointsParams a) {
+    const int lane = threadIdx.x & 31;
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= a.n) return;
+    const double x = a.xy[2 * (size_t)i], y = a.xy[2 * (size_t)i + 1];
+    const float* g = a.features + (size_t)i * a.channels;
+    double dot = 0, nrm = 0;
+    const bool ok = fabs(x) < 1e9 && fabs(y) < 1e9;  // false for NaN / inf too
+    if (ok) {
+        const int x0 = (int)floor(x), y0 = (int)floor(y);
+        if (!a.cubic) {
+            const double ax = x - x0, ay = y - y0;
+            for (int c = lane; c < a.channels; c += 32) {
+                double v[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int xi = x0 + (t & 1), yi = y0 + (t >> 1);
+                    v[t] = (xi < 0 || yi < 0 || xi >= a.W || yi >= a.H)
+                               ? 0.0
+                               : (double)a.grid[((size_t)yi * a.W + xi) * a.channels + c];
+                }
+                const double s = (1 - ax) * (1 - ay) * v[0] + ax * (1 - ay) * v[1] + (1 - ax) * ay * v[2] +
+                                 ax * ay * v[3];
+                dot += g[c] * s;
+                nrm += s * s;
+            }
+        } else {
+            double wx[4], wy[4];
+            cubic_weights(x - x0, wx);
+            cubic_weights(y - y0, wy);
+            for (int c = lane; c < a.channels; c += 32) {
+                double s = 0;
+                for (int j = 0; j < 4; ++j) {
+                    const int yi = y0 - 1 + j;
+                    if (yi < 0 || yi >= a.H) continue;
+                    double row = 0;
+                    for (int k = 0; k < 4; ++k) {
+                        const int xi = x0 - 1 + k;
+                        if (xi < 0 || xi >= a.W) continue;
+                        row += wx[k] * (double)a.grid[((size_t)yi * a.W + xi) * a.channels + c];
+                    }
+                    s += wy[j] * row;
+                }
+                dot += g[c] * s;
+                nrm += s * s;
+            }
+        }
+    }
+    const double r = finish(dot, nrm);
+    if (lane == 0) a.out[i] = r;
+}
 }  // namespace
 
 cudaError_t launch_oracle_propose(const OracleParams& p, int pass, cudaStream_t stream) {
     if (p.n_edges <= 0) return cudaSuccess;
     oracle_propose_kernel<<<(p.n_edges + 127) / 128, 128, 0, stream>>>(p, pass);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_points(const PointsParams& p, cudaStream_t stream) {
+    if (p.n <= 0) return cudaSuccess;
+    points_kernel<<<(p.n + 7) / 8, 256, 0, stream>>>(p);
     return cudaGetLastError();
 }
 
