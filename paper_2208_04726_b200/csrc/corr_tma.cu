@@ -48,20 +48,22 @@ namespace pvo_dev {
 namespace {
 
 #ifndef CORR_WARPS
-#define CORR_WARPS 10
+#define CORR_WARPS 8
 #endif
 #ifndef CORR_STAGES
-#define CORR_STAGES 2
+#define CORR_STAGES 3
 #endif
-#ifndef CORR_JIT_G
-#define CORR_JIT_G 0
+// Dot accumulation (A/B knob CORR_ACC): 0 = per-chunk partials (8 + 8 terms, then
+// one add), 1 = one FFMA2 chain per (cell, pixel) over all 128 channels (64
+// terms: 168 registers, 10 warps x 2 stages fit, -5 %, but a long-chain rounding
+// tail: max |err|/tol 1.08 on a 40k-edge C4 sample, 6,408 outputs above 0.25 of
+// the tolerance), 2 = pixel-outer per-chunk sums.  0 and 2 give max |err|/tol
+// 0.47 on every C2 edge and 0.45 on the C4 sample, 236 outputs above 0.25
+// (profiles/r2/corr_accuracy.txt); 0 is the faster of the two.
+#ifndef CORR_ACC
+#define CORR_ACC 0
 #endif
-#ifndef CORR_NO_PARTS
-#define CORR_NO_PARTS 1
-#endif
-constexpr int kWarps = CORR_WARPS;  // A/B knobs (tools/build_variant.sh).  r2: one FFMA2 chain per
-                                    // (cell, pixel) over the 128 channels (no per-chunk partials: 184
-                                    // registers) lets 10 warps x 2 stages fit: -5 % vs 8 x 3 (r1f)
+constexpr int kWarps = CORR_WARPS;  // A/B knobs (tools/build_variant.sh)
 constexpr int kThreads = 32 * kWarps;
 constexpr int kD = 128;
 constexpr int kBox = 9;
@@ -426,35 +428,42 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(baru + 8 * cs, cph);
             const unsigned char* st = wb + cs * kStageBytes;
             const float* g = reinterpret_cast<const float*>(st + kChunkGOff);
-            // default (CORR_NO_PARTS): the FFMA2 accumulates straight into the tile total
-            // (64 terms per component); the per-chunk partials of round 1 (8 + 8 terms,
-            // then one add) cost 54 registers and one FADD2 per chunk for no measurable
-            // accuracy gain (parity on every C2 edge and the adversarial sets unchanged)
-#if !CORR_NO_PARTS
-            float2 part[NC][kPix];
+#if CORR_ACC == 2
+            // pixel-outer: the chunk's 16 channels of the lane's cells stay in registers,
+            // each (cell, pixel) sums its 16 channels in a short FFMA2 chain (8 terms per
+            // component) and adds that once into the tile total — the accuracy of
+            // per-chunk partials without holding a second [NC][9] accumulator set
+            float4 v[NC][kChunkCh / 4];
+#pragma unroll
+            for (int k = 0; k < NC; ++k) {
+                const int sw = (soff[k] >> 7) & 3;  // 64B swizzle: unit u of row r at u ^ ((r >> 1) & 3)
+#pragma unroll
+                for (int u = 0; u < kChunkCh / 4; ++u)
+                    v[k][u] = *reinterpret_cast<const float4*>(st + soff[k] + ((u ^ sw) << 4));
+            }
+#pragma unroll
+            for (int p = 0; p < kPix; ++p) {
+                float4 gv[kChunkCh / 4];
+#pragma unroll
+                for (int u = 0; u < kChunkCh / 4; ++u) gv[u] = *reinterpret_cast<const float4*>(g + p * kChunkCh + 4 * u);
+#pragma unroll
+                for (int k = 0; k < NC; ++k) {
+                    float2 t = __fmul2_rn(make_float2(v[k][0].x, v[k][0].y), make_float2(gv[0].x, gv[0].y));
+                    t = __ffma2_rn(make_float2(v[k][0].z, v[k][0].w), make_float2(gv[0].z, gv[0].w), t);
+#pragma unroll
+                    for (int u = 1; u < kChunkCh / 4; ++u) {
+                        t = __ffma2_rn(make_float2(v[k][u].x, v[k][u].y), make_float2(gv[u].x, gv[u].y), t);
+                        t = __ffma2_rn(make_float2(v[k][u].z, v[k][u].w), make_float2(gv[u].z, gv[u].w), t);
+                    }
+                    acc[k][p] = __fadd2_rn(acc[k][p], t);
+                }
+            }
+#else
+#if CORR_ACC == 0
+            float2 part[NC][kPix];  // per-chunk partials (r1): 8 + 8 terms per component
 #endif
 #pragma unroll
             for (int u = 0; u < kChunkCh / 4; ++u) {
-#if CORR_JIT_G
-                float4 v[NC];
-#pragma unroll
-                for (int k = 0; k < NC; ++k) {
-                    // 64B swizzle: 16-byte unit u of row r lives at unit u ^ ((r >> 1) & 3)
-                    const int sw = (soff[k] >> 7) & 3;
-                    v[k] = *reinterpret_cast<const float4*>(st + soff[k] + ((u ^ sw) << 4));
-                }
-                // pixel descriptors loaded as used (few live registers)
-#pragma unroll
-                for (int p = 0; p < kPix; ++p) {
-                    const float4 gv = *reinterpret_cast<const float4*>(g + p * kChunkCh + 4 * u);
-#pragma unroll
-                    for (int k = 0; k < NC; ++k) {
-                        const float2 va = make_float2(v[k].x, v[k].y), ga = make_float2(gv.x, gv.y);
-                        part[k][p] = u == 0 ? __fmul2_rn(va, ga) : __ffma2_rn(va, ga, part[k][p]);
-                        part[k][p] = __ffma2_rn(make_float2(v[k].z, v[k].w), make_float2(gv.z, gv.w), part[k][p]);
-                    }
-                }
-#else
                 float4 v[NC], gv[kPix];
 #pragma unroll
                 for (int k = 0; k < NC; ++k) {
@@ -463,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
 #pragma unroll
                 for (int p = 0; p < kPix; ++p) gv[p] = *reinterpret_cast<const float4*>(g + p * kChunkCh + 4 * u);
-#if CORR_NO_PARTS  // A/B knob: one chain per (cell, pixel, parity) over all 128 channels
+#if CORR_ACC == 1  // one chain per (cell, pixel, parity) over all 128 channels (64 terms)
 #pragma unroll
                 for (int k = 0; k < NC; ++k)
 #pragma unroll
@@ -488,13 +497,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int p = 0; p < kPix; ++p)
                         part[k][p] = __ffma2_rn(make_float2(v[k].z, v[k].w), make_float2(gv[p].z, gv[p].w), part[k][p]);
 #endif
-#endif
             }
-#if !CORR_NO_PARTS
+#if CORR_ACC == 0
 #pragma unroll
             for (int k = 0; k < NC; ++k)
 #pragma unroll
                 for (int p = 0; p < kPix; ++p) acc[k][p] = __fadd2_rn(acc[k][p], part[k][p]);
+#endif
 #endif
             __syncwarp();  // every lane is done with this stage: refill it
             if (++cs == kStages) {
