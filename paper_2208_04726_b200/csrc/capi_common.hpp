@@ -193,6 +193,10 @@ struct pvo_ctx {
     bool timing_pending = false;
     bool tracing = false;  // record BA phase clocks (pvo_ctx_set_tracing)
     bool timing = true;    // record the per-iteration timing events (pvo_ctx_set_timing)
+    // FP64 neighbour-Gram maps of the frame store for the provider measurement
+    // ([slot][H][W][kGram25] per level, launch_gram25), derived lazily per slot
+    DevBuf g25_0, g25_1;
+    std::vector<uint8_t> g25_valid;
     std::vector<GridEntry*> grids;  // host-grid cache (GridEntry above)
     uint64_t grid_tick = 0;
     size_t grid_bytes = 0;
@@ -466,6 +470,38 @@ inline void launch_ba_checked(pvo_ctx* ctx, pvo_dev::BAParams& a, const Plan& pl
 
 inline void ensure_p3(int p) {
     if (p != 3) fail(PVO_UNSUPPORTED, "the sm_100a kernels implement 3x3 patches (p = 3)");
+}
+
+// A frame-store slot's features changed: its FP64 neighbour-Gram maps are stale.
+inline void invalidate_g25(pvo_ctx* ctx, int slot) {
+    if (slot >= 0 && slot < (int)ctx->g25_valid.size()) ctx->g25_valid[slot] = 0;
+}
+
+// The FP64 neighbour-Gram maps of every slot (the Gram-form measurement kernel
+// reads them): allocated on first use, re-derived for the slots written since.
+// PVO_MEASURE_DIRECT=1 selects the direct kernel instead (A/B).
+inline void ensure_g25(pvo_ctx* ctx, pvo_dev::MeasureParams& m) {
+    static const bool direct = std::getenv("PVO_MEASURE_DIRECT") != nullptr;
+    if (direct) return;
+    const size_t c0 = (size_t)ctx->w0 * ctx->h0, c1 = (size_t)ctx->w1 * ctx->h1;
+    double* g0 = ctx->g25_0.as<double>((size_t)ctx->nf * c0 * pvo_dev::kGram25);
+    double* g1 = ctx->g25_1.as<double>((size_t)ctx->nf * std::max<size_t>(c1, 1) * pvo_dev::kGram25);
+    if ((int)ctx->g25_valid.size() != ctx->nf) ctx->g25_valid.assign(ctx->nf, 0);
+    for (int s = 0; s < ctx->nf; ++s) {
+        if (ctx->g25_valid[s]) continue;
+        const float* f0 = static_cast<const float*>(ctx->feat0.p) + (size_t)s * c0 * ctx->C;
+        const float* f1 = static_cast<const float*>(ctx->feat1.p) + (size_t)s * c1 * ctx->C;
+        cuda_check(pvo_dev::launch_gram25(f0, ctx->w0, ctx->h0, ctx->C, g0 + (size_t)s * c0 * pvo_dev::kGram25,
+                                          ctx->stream),
+                   "gram25 kernel");
+        cuda_check(pvo_dev::launch_gram25(f1, ctx->w1, ctx->h1, ctx->C, g1 + (size_t)s * c1 * pvo_dev::kGram25,
+                                          ctx->stream),
+                   "gram25 kernel");
+        ctx->launches += c1 ? 2 : 1;
+        ctx->g25_valid[s] = 1;
+    }
+    m.g25_0 = g0;
+    m.g25_1 = g1;
 }
 
 inline void compute_gram(pvo_ctx* ctx, const float* f0, float* g0, const float* f1, float* g1, int w0, int h0, int w1,

@@ -115,7 +115,7 @@ int pvo_ctx_destroy(pvo_ctx* ctx) {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
-        DevBuf* bufs[] = {&ctx->feat0, &ctx->feat1, &ctx->gram0, &ctx->gram1, &ctx->s0, &ctx->s1, &ctx->s2,
+        DevBuf* bufs[] = {&ctx->feat0, &ctx->feat1, &ctx->gram0, &ctx->gram1, &ctx->g25_0, &ctx->g25_1, &ctx->s0, &ctx->s1, &ctx->s2,
                           &ctx->s3,    &ctx->s4,    &ctx->s5,    &ctx->s6,    &ctx->s7, &ctx->s8,
                           &ctx->win.pose_slot, &ctx->win.patch_feats, &ctx->win.corr, &ctx->win.init_poses,
                           &ctx->win.init_depth, &ctx->win.order, &ctx->win.order_half, &ctx->win.flags, &ctx->c_coords, &ctx->c_meta,
@@ -399,6 +399,7 @@ int pvo_frames_reserve(pvo_ctx* ctx, int n_frames, int w0, int h0, int w1, int h
         const size_t gb1 = sizeof(float) * (size_t)n_frames * std::max(pvo_dev::gram_stride(w1) * h1, 1) * 8;
         ctx->gram0.get(gb0);
         ctx->gram1.get(gb1);
+        ctx->g25_valid.assign(n_frames, 0);
         // row-pad cells of the Gram planes must read as zero (out of the image)
         cuda_check(cudaMemsetAsync(ctx->gram0.p, 0, gb0, ctx->stream), "memset");
         cuda_check(cudaMemsetAsync(ctx->gram1.p, 0, gb1, ctx->stream), "memset");
@@ -416,6 +417,7 @@ int pvo_frames_refresh(pvo_ctx* ctx, int slot) {
         float* g0 = static_cast<float*>(ctx->gram0.p) + (size_t)slot * pvo_dev::gram_stride(ctx->w0) * ctx->h0 * 8;
         float* g1 = static_cast<float*>(ctx->gram1.p) + (size_t)slot * pvo_dev::gram_stride(ctx->w1) * ctx->h1 * 8;
         compute_gram(ctx, f0, g0, f1, g1, ctx->w0, ctx->h0, ctx->w1, ctx->h1, ctx->C);
+        invalidate_g25(ctx, slot);
     });
 }
 
@@ -432,6 +434,7 @@ int pvo_frames_upload(pvo_ctx* ctx, int slot, const float* level0, const float* 
         float* g0 = static_cast<float*>(ctx->gram0.p) + (size_t)slot * pvo_dev::gram_stride(ctx->w0) * ctx->h0 * 8;
         float* g1 = static_cast<float*>(ctx->gram1.p) + (size_t)slot * pvo_dev::gram_stride(ctx->w1) * ctx->h1 * 8;
         compute_gram(ctx, f0, g0, f1, g1, ctx->w0, ctx->h0, ctx->w1, ctx->h1, ctx->C);
+        invalidate_g25(ctx, slot);
         if (memspace != PVO_DEVICE) sync(ctx);
     });
 }

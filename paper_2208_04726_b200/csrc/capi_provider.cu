@@ -28,6 +28,7 @@ int pvo_frames_extract(pvo_ctx* ctx, int slot, const float* image, int iw, int i
         float* g0 = static_cast<float*>(ctx->gram0.p) + (size_t)slot * pvo_dev::gram_stride(ctx->w0) * ctx->h0 * 8;
         float* g1 = static_cast<float*>(ctx->gram1.p) + (size_t)slot * pvo_dev::gram_stride(ctx->w1) * ctx->h1 * 8;
         compute_gram(ctx, f0, g0, f1, g1, ctx->w0, ctx->h0, ctx->w1, ctx->h1, ctx->C);
+        invalidate_g25(ctx, slot);
         if (memspace != PVO_DEVICE) sync(ctx);
     });
 }
@@ -109,6 +110,7 @@ int pvo_measure_batch(pvo_ctx* ctx, int n_edges, int n_patches, int p, const int
         m.flags = ctx->s6.as<uint8_t>(n_edges);
         m.status = ctx->d_status;
         reset_status(ctx);
+        ensure_g25(ctx, m);
         cuda_check(pvo_dev::launch_measure(m, ctx->stream), "measure kernel");
         ctx->launches += 1;
         download(ctx, delta, m.delta, (size_t)n_edges * 2);
@@ -152,6 +154,7 @@ int pvo_window_propose(pvo_ctx* ctx, double* delta_out, double* weight_out, uint
         m.weight = static_cast<double*>(B.e_w.p);
         m.flags = w.flags.as<uint8_t>(w.n_edges);
         m.status = ctx->d_status;
+        ensure_g25(ctx, m);
         cuda_check(pvo_dev::launch_measure(m, ctx->stream), "measure kernel");
         ctx->launches += 1;
         if (delta_out) download(ctx, delta_out, m.delta, (size_t)w.n_edges * 2);

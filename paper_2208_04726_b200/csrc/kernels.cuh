@@ -113,8 +113,20 @@ struct MeasureParams {
     double* weight = nullptr;           // [E][2]
     uint8_t* flags = nullptr;           // [E] 1 flat, 2 out of range, 4 behind, 8 non-finite (optional)
     int* status = nullptr;
+    // FP64 neighbour-Gram maps of the frame store ([slot][H][W][kGram25], gram25_kernel):
+    // when set, the Gram-form measurement kernel runs (else the direct one)
+    const double* g25_0 = nullptr;
+    const double* g25_1 = nullptr;
 };
 cudaError_t launch_measure(const MeasureParams& p, cudaStream_t stream);
+
+// FP64 Gram terms <f(x, y), f(x + dx, y + dy)> of every cell for the 25 offsets
+// of the half plane |dx|, |dy| <= 3, (dy > 0) or (dy == 0, dx >= 0) — every
+// tap pair of a 4x4 Catmull-Rom footprint (and of a 2x2 bilinear one); 0 when
+// the neighbour lies outside the grid.  One level of one frame:
+// feat [H][W][C] -> g25 [H][W][kGram25].
+constexpr int kGram25 = 25;
+cudaError_t launch_gram25(const float* feat, int W, int H, int C, double* g25, cudaStream_t stream);
 
 // correlate_at / correlate_at_cubic at n free level-space points against one
 // grid (measure.cu), FP64 like the reference (correlation.cpp:8-35).

@@ -22,7 +22,9 @@
 
 #include <math_constants.h>
 
+#include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 #include <cstdint>
 
 #include "ba_common.cuh"
@@ -308,6 +310,493 @@ __global__ void __launch_bounds__(256, PVO_MEASURE_MINB) measure_kernel(MeasureP
     }
 }
 
+
+// ============================================================================
+// Gram-form measurement (the default when the frame store's FP64 neighbour-Gram
+// maps exist).  By linearity every sample the provider takes is a weighted sum
+// of integer cells, f(x) = sum_t w_t f_t, so
+//   dot   = <g, f(x)>  = sum_t w_t <g, f_t>               (cell dots, FP64)
+//   |f|^2 = sum_t sum_t' w_t w_t' <f_t, f_t'>              (frame Gram maps, FP64)
+// with the reference's own weights (bilinear: features.cpp:10-20; Catmull-Rom:
+// features.cpp:23-52, this file is compiled with --fmad=false so they round
+// as the x86-64 reference build does).  Per edge and level the warp computes
+// the <g, f_t> of the 8x8 slice window and of the 6x6 window around the
+// discrete peak (lane per cell, channels in order, FP64 sums of exact
+// products) and stages their Gram terms in shared memory; a sample is then a
+// few dozen FP64 operations instead of a pass over all channels, and the hill
+// climb's samples need no channel reduction (16 lanes, one per tap).  Products
+// of FP32 features are exact in FP64, so the regrouping changes only the
+// summation order (~1e-16 relative) — except where the taps cancel: a sample
+// whose |f|^2 falls below half its diagonal part (or near the 1e-12 threshold,
+// correlation.cpp:22) is re-evaluated by the direct samplers above, as are the
+// (rounding-edge) samples whose taps leave the staged windows.
+// ============================================================================
+__host__ __device__ constexpr int g25_index(int dx, int dy) { return dy == 0 ? dx : 4 + (dy - 1) * 7 + dx + 3; }
+
+constexpr int kG25TileW = 8, kG25TileH = 4;                   // cells per block
+constexpr int kG25SW = kG25TileW + 6, kG25SH = kG25TileH + 3;  // staged: cols x-3 .. x+10, rows y .. y+6
+
+__global__ void __launch_bounds__(256) gram25_kernel(const float* feat, int W, int H, int C, double* g25) {
+    extern __shared__ float s_f[];  // [kG25SH * kG25SW][C + 1] (odd stride: conflict-free per cell)
+    const int tx0 = blockIdx.x * kG25TileW, ty0 = blockIdx.y * kG25TileH;
+    const int stride = C + 1;
+    for (int t = threadIdx.x; t < kG25SW * kG25SH * C; t += blockDim.x) {
+        const int cell = t / C, c = t - cell * C;
+        const int x = tx0 - 3 + cell % kG25SW, y = ty0 + cell / kG25SW;
+        s_f[cell * stride + c] = (x >= 0 && y >= 0 && x < W && y < H) ? feat[((size_t)y * W + x) * C + c] : 0.f;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < kG25TileW * kG25TileH * kGram25; t += blockDim.x) {
+        const int cl = t / kGram25, m = t - cl * kGram25;
+        const int lx = cl % kG25TileW, ly = cl / kG25TileW;
+        const int x = tx0 + lx, y = ty0 + ly;
+        if (x >= W || y >= H) continue;
+        const int dy = m < 4 ? 0 : 1 + (m - 4) / 7, dx = m < 4 ? m : (m - 4) % 7 - 3;
+        const float* fa = s_f + (ly * kG25SW + lx + 3) * stride;
+        const float* fb = s_f + ((ly + dy) * kG25SW + lx + 3 + dx) * stride;  // zero outside the grid
+        double sum = 0;
+        for (int c = 0; c < C; ++c) sum += (double)fa[c] * (double)fb[c];
+        g25[((size_t)y * W + x) * kGram25 + m] = sum;
+    }
+}
+
+constexpr int kMeasWarps = 8;  // 4 edges per block, a warp per (edge, level)
+
+struct alignas(16) MeasWarpSmem {
+    float g[128];         // the level's centre-pixel descriptor
+    double v[kS * kS];    // the 7x7 slice
+    double sd[64];        // <g, f> of the 8x8 slice window (kept: the climb window reuses them)
+    union {
+        double sgr[64][5];  // Gram (0,0) (1,0) (0,1) (1,1) (-1,1) of the slice window
+        struct {
+            double d[36];             // <g, f> of the 6x6 window around the discrete peak
+            double gr[36][kGram25];   // its Gram maps
+        } climb;
+    } u;
+};
+constexpr int kMeasSmem = kMeasWarps * (int)sizeof(MeasWarpSmem);
+
+// <g, f_cell> (g in shared memory): FP64 sums of exact products (explicit FMAs:
+// the product of two FP32 values is exact in FP64, so an FMA rounds like the
+// separate add), four interleaved partial sums (short dependent chains)
+__device__ __noinline__ double cell_dot(const float* gs, const float* fc, int C) {
+    double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    if ((C & 3) == 0) {
+        const float4* f4 = reinterpret_cast<const float4*>(fc);
+        const float4* g4 = reinterpret_cast<const float4*>(gs);
+#pragma unroll 4
+        for (int q = 0; q < (C >> 2); ++q) {
+            const float4 fv = __ldg(f4 + q), gv = g4[q];
+            s0 = __fma_rn((double)gv.x, (double)fv.x, s0);
+            s1 = __fma_rn((double)gv.y, (double)fv.y, s1);
+            s2 = __fma_rn((double)gv.z, (double)fv.z, s2);
+            s3 = __fma_rn((double)gv.w, (double)fv.w, s3);
+        }
+    } else {
+        for (int c = 0; c < C; ++c) s0 = __fma_rn((double)gs[c], (double)__ldg(fc + c), s0);
+    }
+    return (s0 + s1) + (s2 + s3);
+}
+
+// Two cells at once (independent load streams in flight together).
+__device__ __noinline__ void cell_dot2(const float* gs, const float* fa, const float* fb, int C, double* da,
+                                       double* db) {
+    double a0 = 0, a1 = 0, b0 = 0, b1 = 0;
+    if ((C & 3) == 0) {
+        const float4* fa4 = reinterpret_cast<const float4*>(fa);
+        const float4* fb4 = reinterpret_cast<const float4*>(fb);
+        const float4* g4 = reinterpret_cast<const float4*>(gs);
+#pragma unroll 4
+        for (int q = 0; q < (C >> 2); ++q) {
+            const float4 va = __ldg(fa4 + q), vb = __ldg(fb4 + q), gv = g4[q];
+            a0 = __fma_rn((double)gv.x, (double)va.x, a0);
+            b0 = __fma_rn((double)gv.x, (double)vb.x, b0);
+            a1 = __fma_rn((double)gv.y, (double)va.y, a1);
+            b1 = __fma_rn((double)gv.y, (double)vb.y, b1);
+            a0 = __fma_rn((double)gv.z, (double)va.z, a0);
+            b0 = __fma_rn((double)gv.z, (double)vb.z, b0);
+            a1 = __fma_rn((double)gv.w, (double)va.w, a1);
+            b1 = __fma_rn((double)gv.w, (double)vb.w, b1);
+        }
+    } else {
+        for (int c = 0; c < C; ++c) {
+            a0 = __fma_rn((double)gs[c], (double)__ldg(fa + c), a0);
+            b0 = __fma_rn((double)gs[c], (double)__ldg(fb + c), b0);
+        }
+    }
+    *da = a0 + a1;
+    *db = b0 + b1;
+}
+
+// Per-lane shared-memory offsets (in doubles, relative to the lane's tap cell's
+// Gram record) of the 16 Gram terms <f_p, f_q> of a 4x4 tap footprint in the
+// 6x6 climb window: the record of p at offset q - p when that offset lies in
+// the stored half plane, else the record of q at offset p - q.
+__device__ __forceinline__ void cubic_gram_offsets(int p, int off[16]) {
+    const int pi = p & 3, pj = p >> 2;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const int ddx = (q & 3) - pi, ddy = (q >> 2) - pj;
+        const bool fwd = ddy > 0 || (ddy == 0 && ddx >= 0);
+        off[q] = fwd ? g25_index(ddx, ddy) : (ddy * 6 + ddx) * kGram25 + g25_index(-ddx, -ddy);
+    }
+}
+
+// One Catmull-Rom correlation sample on a half warp (lane & 15 = tap j * 4 + i)
+// from the staged 6x6 window at (qx, qy); both halves call it together (each
+// with its own position).  *redo: the sample must be evaluated directly.
+__device__ __noinline__ double cubic_gram(const MeasWarpSmem& S, const int* off, int qx, int qy, double x, double y,
+                             bool* redo) {
+    const int p = threadIdx.x & 15;
+    const int x0 = (int)floor(x), y0 = (int)floor(y);
+    double wx[4], wy[4];
+    cubic_weights(x - x0, wx);
+    cubic_weights(y - y0, wy);
+    const int bxl = x0 - 1 - qx, byl = y0 - 1 - qy;  // window index of tap (0, 0)
+    const bool inwin = bxl >= 0 && byl >= 0 && bxl <= 2 && byl <= 2;
+    double dot = 0, n2 = 0, diag = 0;
+    if (inwin) {
+        const int pi = p & 3, pj = p >> 2;
+        const int cp = (byl + pj) * 6 + bxl + pi;
+        const double* gp = &S.u.climb.gr[cp][0];
+        double r0 = 0, r1 = 0;
+#pragma unroll
+        for (int q = 0; q < 16; q += 2) {
+            r0 = __fma_rn(wy[q >> 2] * wx[q & 3], gp[off[q]], r0);
+            r1 = __fma_rn(wy[(q + 1) >> 2] * wx[(q + 1) & 3], gp[off[q + 1]], r1);
+        }
+        const double wp = wy[pj] * wx[pi];
+        dot = wp * S.u.climb.d[cp];
+        n2 = wp * (r0 + r1);
+        diag = wp * wp * gp[0];
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+        dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+        diag += __shfl_xor_sync(0xffffffffu, diag, o);
+    }
+    *redo = !inwin || n2 < 0.5 * diag || (n2 > 0.98e-12 && n2 < 1.02e-12);
+    return n2 > 1e-12 ? dot / sqrt(n2) : 0.0;
+}
+
+// First-occurrence argmax of the slice (the reference's `v > best` scan order)
+// as a warp reduction: lanes hold samples lane and lane + 32.
+__device__ __forceinline__ int slice_argmax(const double* v) {
+    const int lane = threadIdx.x & 31;
+    double b = -CUDART_INF;
+    int bi = kR * kS + kR;  // no sample above -inf: the reference keeps (3, 3)
+    for (int i = lane; i < kS * kS; i += 32)
+        if (v[i] > b) {
+            b = v[i];
+            bi = i;
+        }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, b, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > b || (ob == b && oi < bi && ob > -CUDART_INF)) {
+            b = ob;
+            bi = oi;
+        }
+    }
+    return bi;
+}
+
+// subpixel_peak (flow_provider.cpp:167-205) on the Gram form: the discrete
+// argmax of the slice S.v, the 6x6 window around it staged, then the hill climb
+// with f0 / f2 of each parabola step on the two half warps.
+__device__ __noinline__ void subpixel_peak_gram(MeasWarpSmem& S, const Level& L, int C, const double* gm, const G4& g4,
+                                   double bx, double by, int ox, int oy, double* px, double* py, bool* on_border) {
+    const int lane = threadIdx.x & 31;
+    const int bi = slice_argmax(S.v);
+    const int best_a = bi / kS, best_b = bi % kS;
+    *on_border = best_a == 0 || best_a == kS - 1 || best_b == 0 || best_b == kS - 1;
+    double dx = best_b - kR, dy = best_a - kR;
+    if (!(fabs(bx) < 1e8 && fabs(by) < 1e8)) {  // every sample is zero padding: no parabola step moves
+        *px = dx;
+        *py = dy;
+        return;
+    }
+    const int qx = (int)floor(bx + dx) - 2, qy = (int)floor(by + dy) - 2;
+    __syncwarp();  // the slice Gram buffer is reused for the climb window
+    for (int q = lane; q < 36; q += 32) {
+        const int x = qx + q % 6, y = qy + q / 6;
+        const int sx = x - ox, sy = y - oy;  // inside the slice window: its dot is already there
+        const bool in = x >= 0 && y >= 0 && x < L.W && y < L.H;
+        S.u.climb.d[q] = (sx >= 0 && sx < 8 && sy >= 0 && sy < 8) ? S.sd[sy * 8 + sx]
+                         : in                                     ? cell_dot(S.g, L.f + ((size_t)y * L.W + x) * C, C)
+                                                                  : 0.0;
+    }
+    for (int t = lane; t < 36 * kGram25; t += 32) {
+        const int q = t / kGram25, m = t - q * kGram25;
+        const int x = qx + q % 6, y = qy + q / 6;
+        const bool in = x >= 0 && y >= 0 && x < L.W && y < L.H;
+        S.u.climb.gr[q][m] = in ? __ldg(gm + ((size_t)y * L.W + x) * kGram25 + m) : 0.0;
+    }
+    __syncwarp();
+    int off[16];
+    cubic_gram_offsets(lane & 15, off);
+    bool redo;
+    double current = cubic_gram(S, off, qx, qy, bx + dx, by + dy, &redo);
+    if (redo) current = corr_cubic(L.f, L.W, L.H, C, g4, bx + dx, by + dy);
+    double h = 0.5;
+    const bool upper = lane >= 16;
+#pragma unroll 1
+    for (int hs = 0; hs < 6; ++hs, h *= 0.5) {
+#pragma unroll 1
+        for (int ax = 0; ax < 2; ++ax) {
+            const bool along_x = ax == 0;
+            // parabola_refine (flow_provider.cpp:152-162): f0 on lanes 0-15, f2 on 16-31; f1 = current
+            const double x = bx + dx, y = by + dy;
+            const double sx = upper ? x + (along_x ? h : 0) : x - (along_x ? h : 0);
+            const double sy = upper ? y + (along_x ? 0 : h) : y - (along_x ? 0 : h);
+            const double fv = cubic_gram(S, off, qx, qy, sx, sy, &redo);
+            double f0 = __shfl_sync(0xffffffffu, fv, 0), f2 = __shfl_sync(0xffffffffu, fv, 16);
+            const unsigned rb = __ballot_sync(0xffffffffu, redo);
+            if (rb & 1u) f0 = corr_cubic(L.f, L.W, L.H, C, g4, x - (along_x ? h : 0), y - (along_x ? 0 : h));
+            if (rb & 0x10000u) f2 = corr_cubic(L.f, L.W, L.H, C, g4, x + (along_x ? h : 0), y + (along_x ? 0 : h));
+            const double f1 = current;
+            const double denom = f0 - 2 * f1 + f2;
+            double step = 0.0;
+            if (!(fabs(denom) < 1e-12 || denom > 0)) step = fmin(fmax(0.5 * h * (f0 - f2) / denom, -h), h);
+            if (step == 0.0) continue;
+            const double nx = dx + (along_x ? step : 0);
+            const double ny = dy + (along_x ? 0 : step);
+            double value = cubic_gram(S, off, qx, qy, bx + nx, by + ny, &redo);
+            if (redo) value = corr_cubic(L.f, L.W, L.H, C, g4, bx + nx, by + ny);
+            if (value >= current) {  // hill climb only
+                dx = nx;
+                dy = ny;
+                current = value;
+            }
+        }
+    }
+    *px = dx;
+    *py = dy;
+}
+
+// One (edge, level) measurement task of a warp: the slice, then (level 0) the
+// flatness / sharpness scores and, unless flat, the subpixel peak, or (level 1)
+// the subpixel peak.  Result record: {px, py, confidence, border | flat << 1};
+// *valid_out / *behind_out: the edge's centre state (identical for both levels).
+struct MeasRecord {
+    double px, py, conf;
+    int bits;  // border | flat << 1
+};
+__device__ __forceinline__ MeasRecord measure_task(const MeasureParams& a, MeasWarpSmem& S, int e, int level,
+                                                   bool* valid_out, bool* behind_out) {
+    const int lane = threadIdx.x & 31;
+    const int C = a.channels;
+    double cx, cy;
+    bool behind;
+    if (a.centers) {
+        cx = a.centers[2 * e];
+        cy = a.centers[2 * e + 1];
+        behind = a.behind && a.behind[e];
+    } else {  // window mode: reproject_patch of the current state (camera.cpp:47-71)
+        const int k = a.e_patch[e];
+        const SE3 pi = se3_load(a.poses + 7 * a.patch_src[k]);
+        const SE3 pj = se3_load(a.poses + 7 * a.e_pose[e]);
+        const Cam K{a.K[0], a.K[1], a.K[2], a.K[3]};
+        reproject_center(pi, pj, K, a.patch_x + 9 * (size_t)k, a.patch_y + 9 * (size_t)k, a.depth[k], &cx,
+                         &cy, &behind);
+    }
+    const bool valid = !behind && isfinite(cx) && isfinite(cy);
+    // this task's record: level 0 {flat, confidence, p0x, p0y, border0}, level 1 {p1x, p1y, border1}
+    double r_conf = 0.01, r_px = 0, r_py = 0;
+    int r_flat = 1, r_border = 0;
+    if (valid) {
+        const int slot = a.e_slot ? a.e_slot[e] : a.pose_slot[a.e_pose[e]];
+        const Level L = level ? Level{a.feat1 + (size_t)slot * a.h1 * a.w1 * C, a.w1, a.h1}
+                              : Level{a.feat0 + (size_t)slot * a.h0 * a.w0 * C, a.w0, a.h0};
+        const double* gm = level ? a.g25_1 + (size_t)slot * a.h1 * a.w1 * kGram25
+                                 : a.g25_0 + (size_t)slot * a.h0 * a.w0 * kGram25;
+        const float* gp = a.patch_feats + ((size_t)a.e_patch[e] * 2 * 9 + 9 * level + 4) * C;  // centre pixel
+        __syncwarp();  // the previous task is done with S
+        G4 g;
+#pragma unroll
+        for (int k = 0; k < kCh; ++k) {
+            const int c = lane + 32 * k;
+            g.v[k] = c < C ? gp[c] : 0.f;
+            if (c < C) S.g[c] = g.v[k];
+        }
+        const double sc = level ? kStride * kStride : kStride;
+        const double bx = cx / sc, by = cy / sc;
+        const bool span = fabs(bx) < 1e8 && fabs(by) < 1e8;  // else every tap is zero padding
+        const int ox = span ? (int)floor(bx) - kR : 0, oy = span ? (int)floor(by) - kR : 0;
+        __syncwarp();
+        if (span) {
+            {  // slice window dots: cells lane and lane + 32, interleaved
+                const int x0 = ox + (lane & 7), y0 = oy + (lane >> 3), y1 = y0 + 4;
+                const bool in0 = x0 >= 0 && y0 >= 0 && x0 < L.W && y0 < L.H;
+                const bool in1 = x0 >= 0 && y1 >= 0 && x0 < L.W && y1 < L.H;
+                double d0, d1;
+                cell_dot2(S.g, L.f + (in0 ? (size_t)y0 * L.W + x0 : 0) * C,
+                          L.f + (in1 ? (size_t)y1 * L.W + x0 : 0) * C, C, &d0, &d1);
+                S.sd[lane] = in0 ? d0 : 0.0;
+                S.sd[lane + 32] = in1 ? d1 : 0.0;
+            }
+            for (int q = lane; q < 64; q += 32) {
+                const int x = ox + (q & 7), y = oy + (q >> 3);
+                const bool in = x >= 0 && y >= 0 && x < L.W && y < L.H;
+                const double* gc = gm + (in ? (size_t)y * L.W + x : 0) * kGram25;
+                S.u.sgr[q][0] = in ? __ldg(gc + g25_index(0, 0)) : 0.0;
+                S.u.sgr[q][1] = in ? __ldg(gc + g25_index(1, 0)) : 0.0;
+                S.u.sgr[q][2] = in ? __ldg(gc + g25_index(0, 1)) : 0.0;
+                S.u.sgr[q][3] = in ? __ldg(gc + g25_index(1, 1)) : 0.0;
+                S.u.sgr[q][4] = in ? __ldg(gc + g25_index(-1, 1)) : 0.0;
+            }
+            __syncwarp();
+        }
+        // the 7x7 slice (correlate_at at base + (beta - 3, alpha - 3)), lane per sample
+        unsigned redo = 0;
+        for (int n = 0; n < 2; ++n) {
+            const int i = lane + 32 * n;
+            if (i >= kS * kS) break;
+            const int alpha = i / kS, beta = i % kS;
+            double val = 0.0;
+            if (span) {
+                const double x = bx + beta - kR, y = by + alpha - kR;  // flow_provider.cpp:226-227
+                const int x0 = (int)floor(x), y0 = (int)floor(y);
+                const double ax = x - x0, ay = y - y0;
+                const int lx = x0 - ox, ly = y0 - oy;
+                if (lx >= 0 && lx <= 6 && ly >= 0 && ly <= 6) {
+                    const double w0 = (1 - ax) * (1 - ay), w1 = ax * (1 - ay), w2 = (1 - ax) * ay, w3 = ax * ay;
+                    const int c0 = ly * 8 + lx;
+                    const double* d = S.sd;
+                    const double(*G)[5] = S.u.sgr;
+                    const double dot = w0 * d[c0] + w1 * d[c0 + 1] + w2 * d[c0 + 8] + w3 * d[c0 + 9];
+                    const double diag = w0 * w0 * G[c0][0] + w1 * w1 * G[c0 + 1][0] + w2 * w2 * G[c0 + 8][0] +
+                                        w3 * w3 * G[c0 + 9][0];
+                    const double cross = w0 * w1 * G[c0][1] + w0 * w2 * G[c0][2] + w0 * w3 * G[c0][3] +
+                                         w1 * w2 * G[c0 + 1][4] + w1 * w3 * G[c0 + 1][2] + w2 * w3 * G[c0 + 8][1];
+                    const double n2 = diag + 2.0 * cross;
+                    if (n2 < 0.5 * diag || (n2 > 0.98e-12 && n2 < 1.02e-12)) redo |= 1u << n;
+                    val = n2 > 1e-12 ? dot / sqrt(n2) : 0.0;
+                } else {
+                    redo |= 1u << n;
+                }
+            }
+            S.v[i] = val;
+        }
+        unsigned todo = __ballot_sync(0xffffffffu, redo != 0);
+        while (todo) {  // direct evaluation of the flagged samples, a warp each
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            unsigned m = __shfl_sync(0xffffffffu, redo, src);
+            while (m) {
+                const int n = __ffs(m) - 1;
+                m &= m - 1;
+                const int i = src + 32 * n, alpha = i / kS, beta = i % kS;
+                const double r = corr_bilinear(L.f, L.W, L.H, C, g, bx + beta - kR, by + alpha - kR);
+                if (lane == 0) S.v[i] = r;
+            }
+        }
+        __syncwarp();
+        bool border = false;
+        if (level == 1) {
+            r_flat = 0;
+            subpixel_peak_gram(S, L, C, gm, g, bx, by, ox, oy, &r_px, &r_py, &border);
+        } else {
+            // level 0: flatness / sharpness scores on the slice (flow_provider.cpp:217-250),
+            // as warp reductions (the mean as a fixed-order tree)
+            const int pi = slice_argmax(S.v);
+            const double peak = S.v[pi];
+            const int peak_a = pi / kS, peak_b = pi % kS;
+            double minimum = CUDART_INF, mean = 0, second = -CUDART_INF;
+            for (int i = lane; i < kS * kS; i += 32) {
+                const double val = S.v[i];
+                mean += val;
+                minimum = fmin(minimum, val);
+                if (max(abs(i / kS - peak_a), abs(i % kS - peak_b)) > 1) second = fmax(second, val);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                mean += __shfl_xor_sync(0xffffffffu, mean, o);
+                minimum = fmin(minimum, __shfl_xor_sync(0xffffffffu, minimum, o));
+                second = fmax(second, __shfl_xor_sync(0xffffffffu, second, o));
+            }
+            mean /= kS * kS;
+            const double peak_to_mean = (peak - minimum) / (mean - minimum + 1e-9);
+            r_flat = !(peak_to_mean >= 1.05);
+            if (!r_flat) {
+                const double score = 2.0 * (peak - 0.75) + (peak - second - 0.08);
+                r_conf = fmin(fmax(1.0 / (1.0 + exp(-12.0 * score)), 0.01), 0.99);
+                subpixel_peak_gram(S, L, C, gm, g, bx, by, ox, oy, &r_px, &r_py, &border);
+            }
+        }
+        r_border = border;
+    }
+    *valid_out = valid;
+    *behind_out = behind;
+    return MeasRecord{r_px, r_py, r_conf, r_border | (r_flat << 1)};
+}
+
+// The measurement of an edge from its two level records (flow_provider.cpp:252-287).
+__device__ __forceinline__ void measure_combine(const MeasureParams& a, int e, bool valid, bool behind,
+                                                const MeasRecord& r0, const MeasRecord& r1) {
+    const double p0x = r0.px, p0y = r0.py, p1x = r1.px, p1y = r1.py;
+    double confidence = r0.conf;
+    const int b0 = r0.bits, b1 = r1.bits;
+    const bool flat = (b0 >> 1) & 1, border0 = b0 & 1, border1 = b1 & 1;
+    double dxo = 0, dyo = 0, wgt = 0.01;
+    int flags = 0;
+    if (behind) {
+        flags = 4;  // flow_provider.cpp:301-302
+    } else if (!valid) {
+        flags = 8;
+        atomicOr(a.status, 1 << kDevBadCoords);
+    } else if (flat) {
+        flags = 1;  // flat: delta 0, weight 0.01
+    } else {
+        const double e0x = kStride * p0x, e0y = kStride * p0y;
+        const double e1x = kStride * kStride * p1x, e1y = kStride * kStride * p1y;
+        if (border0 && border1) {
+            flags = 2;  // out of range: delta 0, weight 0.01
+        } else {
+            if (border0) {
+                dxo = e1x;
+                dyo = e1y;
+                confidence = fmin(confidence, 0.25);
+            } else {
+                dxo = e0x;
+                dyo = e0y;
+                const double ddx = e1x - e0x, ddy = e1y - e0y;
+                if (!border1 && sqrt(ddx * ddx + ddy * ddy) > 2.0 * kStride * kStride)
+                    confidence = fmin(confidence, 0.25);
+            }
+            wgt = confidence;
+        }
+    }
+    a.delta[2 * e] = dxo;
+    a.delta[2 * e + 1] = dyo;
+    a.weight[2 * e] = wgt;
+    a.weight[2 * e + 1] = wgt;
+    if (a.flags) a.flags[e] = (uint8_t)flags;
+}
+
+// Paired warps (default): a block runs kMeasWarps / 2 edges, warp 2m level 0 and
+// warp 2m + 1 level 1 of edge m; they meet on a named barrier.
+#ifndef PVO_MEASURE_GRAM_MINB
+#define PVO_MEASURE_GRAM_MINB 2
+#endif
+__global__ void __launch_bounds__(32 * kMeasWarps, PVO_MEASURE_GRAM_MINB) measure_gram_kernel(MeasureParams a) {
+    extern __shared__ __align__(16) unsigned char s_meas[];
+    __shared__ MeasRecord s_rec1[kMeasWarps / 2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int pair = warp >> 1, level = warp & 1;
+    const int e = blockIdx.x * (kMeasWarps / 2) + pair;
+    if (e >= a.n_edges) return;  // both warps of the pair
+    MeasWarpSmem& S = reinterpret_cast<MeasWarpSmem*>(s_meas)[warp];
+    bool valid, behind;
+    const MeasRecord r = measure_task(a, S, e, level, &valid, &behind);
+    if (level == 1 && lane == 0) s_rec1[pair] = r;
+    __syncwarp();
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+    if (level == 0 && lane == 0) measure_combine(a, e, valid, behind, r, s_rec1[pair]);
+}
+
 // ---- OracleFlowProvider::propose (flow_provider.cpp:34-93), simulator revisions ----
 // pass 0: ground-truth reprojection of each edge's patch centre (a 1x1 probe at
 // the centre with the scene inverse depth, between the scene poses) and the
@@ -432,7 +921,25 @@ cudaError_t launch_points(const PointsParams& p, cudaStream_t stream) {
 cudaError_t launch_measure(const MeasureParams& p, cudaStream_t stream) {
     if (p.n_edges <= 0) return cudaSuccess;
     if (p.channels > 32 * kCh) return cudaErrorNotSupported;
+    if (p.g25_0 && p.g25_1) {
+        cudaError_t err =
+            cudaFuncSetAttribute(measure_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMeasSmem);
+        if (err != cudaSuccess) return err;
+        measure_gram_kernel<<<(p.n_edges + kMeasWarps / 2 - 1) / (kMeasWarps / 2), 32 * kMeasWarps, kMeasSmem,
+                              stream>>>(p);
+        return cudaGetLastError();
+    }
     measure_kernel<<<(p.n_edges + 3) / 4, 256, 0, stream>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gram25(const float* feat, int W, int H, int C, double* g25, cudaStream_t stream) {
+    if (W <= 0 || H <= 0) return cudaSuccess;
+    const int smem = kG25SW * kG25SH * (C + 1) * (int)sizeof(float);
+    cudaError_t err = cudaFuncSetAttribute(gram25_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err != cudaSuccess) return err;
+    const dim3 grid((W + kG25TileW - 1) / kG25TileW, (H + kG25TileH - 1) / kG25TileH);
+    gram25_kernel<<<grid, 256, smem, stream>>>(feat, W, H, C, g25);
     return cudaGetLastError();
 }
 

@@ -103,3 +103,51 @@ def test_corr_adversarial_inputs(ctx, kind, D):
     if kind == "stripes":
         assert np.count_nonzero(ref == 0.0) > 0  # the exactly cancelling samples were exercised
         assert np.all(out[ref == 0.0] == 0.0)
+
+
+@pytest.mark.parametrize("kind", ["unsmoothed", "checker", "stripes", "tiny", "dead"])
+def test_measure_adversarial_inputs(ctx, kind):
+    """The provider measurement (flow_provider.cpp:209-287) on the same inputs:
+    the Gram-form kernel's slice and hill-climb samples cancel here too and go
+    through the direct re-evaluation; flags must equal the reference's and the
+    deltas / weights agree to 1e-6 px / 1e-9.
+
+    "stripes" (f(x + 1) = -f(x)) and "dead" (40 % all-zero cells) make the
+    7x7 slice full of EXACT ties; the reference resolves them by scan order
+    (flow_provider.cpp:173-180, :230-234) and the last-ulp differences of any
+    regrouped channel sum (the Gram form here; the warp-tree sums of the
+    direct kernel, PVO_MEASURE_DIRECT=1, disagree on as many edges) pick other
+    equal maxima, which then steer the hill climb elsewhere.  For those two
+    inputs the test bounds the disagreeing edges instead (<= 10 %, flags
+    <= 2 %)."""
+    rng = np.random.default_rng(abs(hash(("measure", kind))) % 2**32)
+    F, D = 3, 128
+    l0 = np.stack([_grid(kind, rng, H0, W0, D) for _ in range(F)]).astype(np.float32)
+    l1 = np.stack([_grid(kind, rng, H0 // 4 + 1, W0 // 4, D) for _ in range(F)]).astype(np.float32)
+    n = 200
+    coords = np.concatenate([_coords(rng, n // 2, True), _coords(rng, n - n // 2, False)])
+    feats = _unit(rng.standard_normal((n, 2, 9, D))).astype(np.float32)
+    for i in range(0, n, 2):
+        f = i % F
+        feats[i, 0] = synth.crop_cubic(l0[f], coords[i, :, 0] / 4, coords[i, :, 1] / 4)
+        feats[i, 1] = synth.crop_cubic(l1[f], coords[i, :, 0] / 16, coords[i, :, 1] / 16)
+    if kind == "tiny":
+        feats *= np.float32(3.0)
+    e_patch = np.arange(n, dtype=np.int32)
+    e_frame = (np.arange(n) % F).astype(np.int32)
+    centers = coords[:, 4]
+    ctx.frames_reserve(F, W0, H0, l1.shape[2], l1.shape[1], D)
+    for f in range(F):
+        ctx.frames_upload(f, l0[f], l1[f])
+    d, w, fl = pvo.measure_batch(e_patch, e_frame, centers, feats, ctx=ctx)
+    rd, rw, rfl = orc.measure_batch(e_patch, e_frame, centers, None, feats, l0, l1, threads=THREADS)
+    flips = int((fl != rfl).sum())
+    off = int(((np.abs(d - rd).max(1) > 1e-6) | (np.abs(w - rw).max(1) > 1e-9)).sum())
+    bad = np.nonzero((np.abs(d - rd).max(1) > 1e-6) | (np.abs(w - rw).max(1) > 1e-9) | (fl != rfl))[0]
+    print(f"{kind}: flat {int((rfl & 1).sum())}, out-of-range {int((rfl & 2).sum())}, flips {flips}, off {off}")
+    for i in bad[:8]:
+        print(f"  edge {i}: gpu d {d[i]} w {w[i][0]:.6g} fl {fl[i]} | ref d {rd[i]} w {rw[i][0]:.6g} fl {rfl[i]}")
+    if kind in ("stripes", "dead"):
+        assert flips <= 0.02 * n and len(bad) <= 0.10 * n, (flips, off)
+    else:
+        assert flips == 0 and off <= 1, (flips, off)
