@@ -443,6 +443,7 @@ def run_ours(args, rank, world, local_rank):
             e1.synchronize()
             if i:
                 prop_ms.append(e0.elapsed_time(e1))
+    prop_replayed = ctx.measure_replayed  # edges re-measured exactly (near-tie decisions)
     win.load(prob, prob["pose_frames"], prob["patch_feats"], w.K, w.image)  # restore the revisions
 
     # max over ranks (the job's clock)
@@ -478,7 +479,7 @@ def run_ours(args, rank, world, local_rank):
         "config": workload_config(args.config, w, E, world),
         "timing": {"state": "window state restored before every step (outside the timed events)",
                    "launch": "CUDA graph of the step's launches, replayed" if graph is not None else "eager launches"},
-        "corr_ms": corr_ms_max, "ba_ms": ba_ms_max, "propose_ms": float(np.mean(prop_ms)),
+        "corr_ms": corr_ms_max, "ba_ms": ba_ms_max, "propose_ms": float(np.mean(prop_ms)), "propose_replayed_edges": prop_replayed,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "kernel": "corr_tma_kernel", "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": total_b},

@@ -227,6 +227,11 @@ int pvo_measure_batch(pvo_ctx* ctx, int n_edges, int n_patches, int p, const int
                       const double* centers, const uint8_t* behind, const float* patch_feats, double* delta,
                       double* weight, uint8_t* flags);
 int pvo_window_propose(pvo_ctx* ctx, double* delta, double* weight, uint8_t* flags);
+/* Edges of the last measurement whose Gram-form decisions lay within the
+ * rounding margin of a flip (tied argmax, hill-climb comparison, parabola
+ * denominator, flatness / level-consistency threshold) and were measured again
+ * with the reference's exact per-channel arithmetic (synchronises).         */
+int pvo_measure_replayed(pvo_ctx* ctx, int* count);
 
 /* ---- device-resident patch graph ---------------------
  * The PatchGraph operations of patch_graph.hpp:66-136 on device arrays

@@ -73,6 +73,7 @@ SIGNATURES = {
     "pvo_frames_download": (i32, [vp, i32, P, P]),
     "pvo_measure_batch": (i32, [vp, i32, i32, i32, P, P, P, P, P, P, P, P]),
     "pvo_window_propose": (i32, [vp, P, P, P]),
+    "pvo_measure_replayed": (i32, [vp, P]),
     "pvo_dgraph_create": (i32, [vp, P, i32, i32, i32, i32, C.POINTER(vp)]),
     "pvo_dgraph_destroy": (i32, [vp]),
     "pvo_dgraph_add_frame": (i32, [vp, f64, P, i32, P]),

@@ -135,6 +135,14 @@ class Context:
         check(lib.pvo_ctx_ba_attempts(self.handle, C.addressof(n)))
         return n.value
 
+    @property
+    def measure_replayed(self) -> int:
+        """Edges of the last provider measurement re-run with the reference's exact
+        arithmetic because a decision lay within the rounding margin (synchronises)."""
+        n = C.c_int()
+        check(lib.pvo_measure_replayed(self.handle, C.addressof(n)))
+        return n.value
+
     def set_timing(self, on: bool = True) -> None:
         """Per-iteration timing events (last_timing); on by default."""
         check(lib.pvo_ctx_set_timing(self.handle, int(bool(on))))

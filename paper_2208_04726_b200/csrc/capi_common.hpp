@@ -197,6 +197,7 @@ struct pvo_ctx {
     // ([slot][H][W][kGram25] per level, launch_gram25), derived lazily per slot
     DevBuf g25_0, g25_1;
     std::vector<uint8_t> g25_valid;
+    DevBuf replay;  // the measurement's exact-replay list (kept zeroed by the kernels)
     std::vector<GridEntry*> grids;  // host-grid cache (GridEntry above)
     uint64_t grid_tick = 0;
     size_t grid_bytes = 0;
@@ -502,6 +503,14 @@ inline void ensure_g25(pvo_ctx* ctx, pvo_dev::MeasureParams& m) {
     }
     m.g25_0 = g0;
     m.g25_1 = g1;
+    const size_t need = ((size_t)m.n_edges + 3) * sizeof(int);
+    if (ctx->replay.cap < need) {  // (re)allocated: zero it once; the kernels leave it zero
+        ctx->replay.get(need);
+        cuda_check(cudaMemsetAsync(ctx->replay.p, 0, ctx->replay.cap, ctx->stream), "memset");
+    }
+    m.replay_done = static_cast<int*>(ctx->replay.p);  // [done, stat, count, edges...]
+    m.replay_stat = m.replay_done + 1;
+    m.replay = m.replay_done + 2;
 }
 
 inline void compute_gram(pvo_ctx* ctx, const float* f0, float* g0, const float* f1, float* g1, int w0, int h0, int w1,

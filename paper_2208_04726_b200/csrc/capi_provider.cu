@@ -112,7 +112,7 @@ int pvo_measure_batch(pvo_ctx* ctx, int n_edges, int n_patches, int p, const int
         reset_status(ctx);
         ensure_g25(ctx, m);
         cuda_check(pvo_dev::launch_measure(m, ctx->stream), "measure kernel");
-        ctx->launches += 1;
+        ctx->launches += m.g25_0 ? 2 : 1;  // Gram-form kernel + exact replay
         download(ctx, delta, m.delta, (size_t)n_edges * 2);
         download(ctx, weight, m.weight, (size_t)n_edges * 2);
         if (flags) download(ctx, flags, m.flags, n_edges);
@@ -156,11 +156,24 @@ int pvo_window_propose(pvo_ctx* ctx, double* delta_out, double* weight_out, uint
         m.status = ctx->d_status;
         ensure_g25(ctx, m);
         cuda_check(pvo_dev::launch_measure(m, ctx->stream), "measure kernel");
-        ctx->launches += 1;
+        ctx->launches += m.g25_0 ? 2 : 1;  // Gram-form kernel + exact replay
         if (delta_out) download(ctx, delta_out, m.delta, (size_t)w.n_edges * 2);
         if (weight_out) download(ctx, weight_out, m.weight, (size_t)w.n_edges * 2);
         if (flags_out) download(ctx, flags_out, m.flags, w.n_edges);
         if (delta_out || weight_out || flags_out) sync(ctx);
+    });
+}
+
+int pvo_measure_replayed(pvo_ctx* ctx, int* count) {
+    return guarded([&] {
+        bind(ctx);
+        if (!count) fail(PVO_INVALID_ARGUMENT, "measure_replayed: null output");
+        *count = 0;
+        if (ctx->replay.cap < 3 * sizeof(int)) return;
+        cuda_check(cudaMemcpyAsync(count, static_cast<int*>(ctx->replay.p) + 1, sizeof(int), cudaMemcpyDeviceToHost,
+                                   ctx->stream),
+                   "replay count");
+        sync(ctx);
     });
 }
 

@@ -117,6 +117,11 @@ struct MeasureParams {
     // when set, the Gram-form measurement kernel runs (else the direct one)
     const double* g25_0 = nullptr;
     const double* g25_1 = nullptr;
+    // exact replay list of the Gram-form kernel ([0] count, [1 ..] edges; zero on
+    // entry, left zero) and its completion counter; required with g25_0 / g25_1
+    int* replay = nullptr;
+    int* replay_done = nullptr;
+    int* replay_stat = nullptr;  // receives the replayed-edge count of the call
 };
 cudaError_t launch_measure(const MeasureParams& p, cudaStream_t stream);
 

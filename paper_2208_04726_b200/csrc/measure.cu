@@ -28,6 +28,7 @@
 #include <cstdint>
 
 #include "ba_common.cuh"
+#include "corr_exact.cuh"
 #include "kernels.cuh"
 
 namespace pvo_dev {
@@ -55,9 +56,45 @@ __device__ __forceinline__ double finish(double dot, double nrm) {
     return nrm > 1e-12 ? dot / sqrt(nrm) : 0.0;
 }
 
+// The same epilogue bit for bit as the reference: the per-channel products
+// g_c v_c and v_c^2 (each rounded once, as `dot += feature[c] * v` rounds them)
+// are staged in the warp's scratch xs[2][128] and summed in channel order
+// c = 0, 1, ... by lanes 0 (dot) and 1 (norm) — the sequential loop of
+// correlation.cpp:18-21.  Used by the exact replay of near-tie edges.
+__device__ __noinline__ double finish_seq(const G4& g, const double* v, int C, double* xs) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < kCh; ++k) {
+        const int c = lane + 32 * k;
+        if (c < C) {
+            xs[c] = (double)g.v[k] * v[k];
+            xs[128 + c] = v[k] * v[k];
+        }
+    }
+    __syncwarp();
+    double s = 0;
+    if (lane < 2) {
+        const double* p = xs + 128 * lane;
+        int c = 0;
+        for (; c + 16 <= C; c += 16) {  // loads batched ahead of the dependent adds
+            double t[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) t[k] = p[c + k];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) s += t[k];
+        }
+        for (; c < C; ++c) s += p[c];
+    }
+    const double dot = __shfl_sync(0xffffffffu, s, 0), nrm = __shfl_sync(0xffffffffu, s, 1);
+    __syncwarp();  // xs is rewritten by the next sample
+    return nrm > 1e-12 ? dot / sqrt(nrm) : 0.0;
+}
+
 // correlate_at (correlation.cpp:8-23) with sample_zero_padded (features.cpp:9-21).
 // Not inlined: one copy of the sampler keeps the kernel inside the instruction cache.
-__device__ __noinline__ double corr_bilinear(const float* f, int W, int H, int C, G4 g, double x, double y) {
+// xs: null -> warp-tree channel sum; else the reference's sequential sum (finish_seq)
+__device__ __noinline__ double corr_bilinear(const float* f, int W, int H, int C, G4 g, double x, double y,
+                                             double* xs = nullptr) {
     const int lane = threadIdx.x & 31;
     const int x0 = (int)floor(x), y0 = (int)floor(y);
     const double ax = x - x0, ay = y - y0;
@@ -74,6 +111,7 @@ __device__ __noinline__ double corr_bilinear(const float* f, int W, int H, int C
             v[k] = t == 0 ? w[0] * val : v[k] + w[t] * val;
         }
     }
+    if (xs) return finish_seq(g, v, C, xs);
     double dot = 0, nrm = 0;
 #pragma unroll
     for (int k = 0; k < kCh; ++k) {
@@ -90,33 +128,113 @@ __device__ __forceinline__ void cubic_weights(double t, double w[4]) {  // featu
     w[3] = (0.5 * t - 0.5) * t * t;
 }
 
-// correlate_at_cubic (correlation.cpp:25-35) with sample_cubic (features.cpp:23-52):
-// taps outer (one address per tap, four channel loads at immediate offsets),
-// the per-channel operation order unchanged.
-__device__ __noinline__ double corr_cubic(const float* f, int W, int H, int C, G4 g, double x, double y) {
+// A square window of n x n cells of one level staged in the warp's shared
+// memory for the exact replay ([cell][C + 1] floats: an odd stride, so lanes on
+// distinct cells or on consecutive channels hit distinct banks); cells outside
+// the grid hold 0, the reference's zero padding (features.cpp:15-17).
+struct SmemWin {
+    float* s = nullptr;
+    int x0 = 0, y0 = 0, n = 0, stride = 0;
+    __device__ bool holds(int x, int y, int span) const {  // cells x .. x + span - 1 (same in y)
+        return s && x >= x0 && y >= y0 && x + span <= x0 + n && y + span <= y0 + n;
+    }
+    __device__ const float* cell(int x, int y) const { return s + ((y - y0) * n + (x - x0)) * stride; }
+};
+
+__device__ void stage_window(SmemWin& w, const Level& L, int C, int x0, int y0, int n) {
+    const int lane = threadIdx.x & 31;
+    __syncwarp();  // the previous window's readers are done
+    w.x0 = x0;
+    w.y0 = y0;
+    w.n = n;
+    w.stride = C + 1;
+    const int cells = n * n;
+    constexpr int kBatch = 16;  // cells whose loads are all in flight before any store
+    for (int q0 = 0; q0 < cells; q0 += kBatch) {
+        float r[kBatch][kCh];
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            const int q = q0 + j, x = x0 + q % n, y = y0 + q / n;
+            const bool in = q < cells && x >= 0 && y >= 0 && x < L.W && y < L.H;
+            const float* src = L.f + (in ? (size_t)y * L.W + x : 0) * C;
+#pragma unroll
+            for (int k = 0; k < kCh; ++k) r[j][k] = (in && lane + 32 * k < C) ? __ldg(src + lane + 32 * k) : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j)
+#pragma unroll
+            for (int k = 0; k < kCh; ++k)
+                if (q0 + j < cells && lane + 32 * k < C) w.s[(q0 + j) * w.stride + lane + 32 * k] = r[j][k];
+    }
+    __syncwarp();
+}
+
+// correlate_at_cubic (correlation.cpp:25-35) with sample_cubic (features.cpp:23-52).
+// kPreload (the exact replay, which has the registers): all 16 taps' channel
+// loads are issued first — from the staged window when it holds the footprint —
+// then the reference's per-channel operation order; out-of-grid taps read as 0,
+// and adding their zero term where the reference skips it (features.cpp:40-47)
+// leaves every sum bit-identical (x + 0 == x; +0 + -0 == +0).  Otherwise taps
+// outer with one address per tap (few registers: the Gram-form kernel's rare
+// direct re-evaluations must not make its hill climb spill).
+template <bool kPreload>
+__device__ __noinline__ double corr_cubic_t(const float* f, int W, int H, int C, G4 g, double x, double y,
+                                            double* xs, const SmemWin* win) {
     const int lane = threadIdx.x & 31;
     const int x0 = (int)floor(x), y0 = (int)floor(y);
     double wx[4], wy[4];
     cubic_weights(x - x0, wx);
     cubic_weights(y - y0, wy);
     double v[kCh] = {0, 0, 0, 0};
+    if constexpr (kPreload) {
+        float val[16][kCh];
+        if (win && win->holds(x0 - 1, y0 - 1, 4)) {  // the 4 x 4 footprint is staged (zeros outside the grid)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int yi = y0 - 1 + j;
-        if (yi < 0 || yi >= H) continue;
-        double row[kCh] = {0, 0, 0, 0};
+            for (int t = 0; t < 16; ++t) {
+                const float* p = win->cell(x0 - 1 + (t & 3), y0 - 1 + (t >> 2)) + lane;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int xi = x0 - 1 + i;
-            if (xi < 0 || xi >= W) continue;
-            const float* p = f + ((size_t)yi * W + xi) * C + lane;
+                for (int k = 0; k < kCh; ++k) val[t][k] = lane + 32 * k < C ? p[32 * k] : 0.f;
+            }
+        } else {
 #pragma unroll
-            for (int k = 0; k < kCh; ++k)
-                if (lane + 32 * k < C) row[k] += wx[i] * (double)__ldg(p + 32 * k);
+            for (int t = 0; t < 16; ++t) {
+                const int xi = x0 - 1 + (t & 3), yi = y0 - 1 + (t >> 2);
+                const bool in = xi >= 0 && xi < W && yi >= 0 && yi < H;
+                const float* p = f + (in ? (size_t)yi * W + xi : 0) * C + lane;
+#pragma unroll
+                for (int k = 0; k < kCh; ++k) val[t][k] = (in && lane + 32 * k < C) ? __ldg(p + 32 * k) : 0.f;
+            }
         }
 #pragma unroll
-        for (int k = 0; k < kCh; ++k) v[k] += wy[j] * row[k];
+        for (int j = 0; j < 4; ++j) {
+            double row[kCh] = {0, 0, 0, 0};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int k = 0; k < kCh; ++k) row[k] += wx[i] * (double)val[4 * j + i][k];
+#pragma unroll
+            for (int k = 0; k < kCh; ++k) v[k] += wy[j] * row[k];
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int yi = y0 - 1 + j;
+            if (yi < 0 || yi >= H) continue;
+            double row[kCh] = {0, 0, 0, 0};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int xi = x0 - 1 + i;
+                if (xi < 0 || xi >= W) continue;
+                const float* p = f + ((size_t)yi * W + xi) * C + lane;
+#pragma unroll
+                for (int k = 0; k < kCh; ++k)
+                    if (lane + 32 * k < C) row[k] += wx[i] * (double)__ldg(p + 32 * k);
+            }
+#pragma unroll
+            for (int k = 0; k < kCh; ++k) v[k] += wy[j] * row[k];
+        }
     }
+    if (xs) return finish_seq(g, v, C, xs);
     double dot = 0, nrm = 0;
 #pragma unroll
     for (int k = 0; k < kCh; ++k) {
@@ -125,11 +243,20 @@ __device__ __noinline__ double corr_cubic(const float* f, int W, int H, int C, G
     }
     return finish(dot, nrm);
 }
+__device__ __forceinline__ double corr_cubic(const float* f, int W, int H, int C, G4 g, double x, double y,
+                                            double* xs = nullptr) {
+    return corr_cubic_t<false>(f, W, H, C, g, x, y, xs, nullptr);
+}
+__device__ __forceinline__ double corr_cubic_exact(const float* f, int W, int H, int C, G4 g, double x, double y,
+                                                  double* xs, const SmemWin* win) {
+    return win ? corr_cubic_t<true>(f, W, H, C, g, x, y, xs, win) : corr_cubic_t<false>(f, W, H, C, g, x, y, xs, win);
+}
 
 // subpixel_peak (flow_provider.cpp:167-205) from the 7x7 slice `vals` (already
 // evaluated at base + (beta - 3, alpha - 3)); returns the offset in cells
 __device__ void subpixel_peak(const Level& L, int C, G4 g, double bx, double by,
-                              const double* vals, double* ox, double* oy, bool* on_border) {
+                              const double* vals, double* ox, double* oy, bool* on_border, double* xs,
+                              SmemWin* win) {
     int best_a = kR, best_b = kR;
     double best = -CUDART_INF;
     for (int alpha = 0; alpha < kS; ++alpha)
@@ -143,23 +270,29 @@ __device__ void subpixel_peak(const Level& L, int C, G4 g, double bx, double by,
         }
     *on_border = best_a == 0 || best_a == kS - 1 || best_b == 0 || best_b == kS - 1;
     double dx = best_b - kR, dy = best_a - kR;
-    double current = corr_cubic(L.f, L.W, L.H, C, g, bx + dx, by + dy);
+    // every climb sample lies within 1 cell of the discrete peak (sum of steps < 1): its
+    // Catmull-Rom footprint is inside the 6 x 6 window at floor(peak) - 2
+    if (win && fabs(bx) < 1e8 && fabs(by) < 1e8)
+        stage_window(*win, L, C, (int)floor(bx + dx) - 2, (int)floor(by + dy) - 2, 6);
+    double current = corr_cubic_exact(L.f, L.W, L.H, C, g, bx + dx, by + dy, xs, win);
     double h = 0.5;
     for (int hs = 0; hs < 6; ++hs, h *= 0.5) {
         for (int ax = 0; ax < 2; ++ax) {
             const bool along_x = ax == 0;
             // parabola_refine (flow_provider.cpp:152-162); f1 = the current value
             const double x = bx + dx, y = by + dy;
-            const double f0 = corr_cubic(L.f, L.W, L.H, C, g, x - (along_x ? h : 0), y - (along_x ? 0 : h));
+            const double f0 =
+                corr_cubic_exact(L.f, L.W, L.H, C, g, x - (along_x ? h : 0), y - (along_x ? 0 : h), xs, win);
             const double f1 = current;
-            const double f2 = corr_cubic(L.f, L.W, L.H, C, g, x + (along_x ? h : 0), y + (along_x ? 0 : h));
+            const double f2 =
+                corr_cubic_exact(L.f, L.W, L.H, C, g, x + (along_x ? h : 0), y + (along_x ? 0 : h), xs, win);
             const double denom = f0 - 2 * f1 + f2;
             double step = 0.0;
             if (!(fabs(denom) < 1e-12 || denom > 0)) step = fmin(fmax(0.5 * h * (f0 - f2) / denom, -h), h);
             if (step == 0.0) continue;
             const double nx = dx + (along_x ? step : 0);
             const double ny = dy + (along_x ? 0 : step);
-            const double value = corr_cubic(L.f, L.W, L.H, C, g, bx + nx, by + ny);
+            const double value = corr_cubic_exact(L.f, L.W, L.H, C, g, bx + nx, by + ny, xs, win);
             if (value >= current) {  // hill climb only
                 dx = nx;
                 dy = ny;
@@ -171,19 +304,17 @@ __device__ void subpixel_peak(const Level& L, int C, G4 g, double bx, double by,
     *oy = dy;
 }
 
-#ifndef PVO_MEASURE_MINB
-#define PVO_MEASURE_MINB 1
-#endif
-__global__ void __launch_bounds__(256, PVO_MEASURE_MINB) measure_kernel(MeasureParams a) {
-    // two warps per edge: warp 2m runs level 0 (slice, scores, subpixel peak), warp
-    // 2m+1 level 1 (slice, subpixel peak) concurrently; they meet on a named barrier
-    __shared__ double s_vals[8][kS * kS];
-    __shared__ double s_peak1[4][2];
-    __shared__ int s_border1[4];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int pair = warp >> 1, level = warp & 1;
-    const int e = blockIdx.x * 4 + pair;
-    if (e >= a.n_edges) return;  // both warps of the pair
+// The direct measurement of edge e by a warp pair (warp `level` of the pair):
+// every sample through the per-channel samplers above.  xs: null -> warp-tree
+// channel sums (the PVO_MEASURE_DIRECT A/B kernel); else the warp's [2][128]
+// scratch -> the reference's sequential channel sums, so every sample, and
+// with it every decision, is bit-identical to the reference (the exact replay
+// of near-tie edges, measure_exact_kernel).  vals: the warp's 7x7 slice;
+// peak1 / border1: the pair's level-1 result; bar: the pair's named barrier.
+__device__ __forceinline__ void measure_direct_edge(const MeasureParams& a, int e, int level, double* vals,
+                                                    double* peak1, int* border1, int bar, double* xs,
+                                                    float* win_buf) {
+    const int lane = threadIdx.x & 31;
     double cx, cy;
     bool behind;
     if (a.centers) {
@@ -221,24 +352,55 @@ __global__ void __launch_bounds__(256, PVO_MEASURE_MINB) measure_kernel(MeasureP
             const int c = lane + 32 * k;
             g.v[k] = c < a.channels ? gp[(9 * level + 4) * a.channels + c] : 0.f;  // centre pixel of the level
         }
-        double* v = s_vals[warp];
+        double* v = vals;
         const double sc = level ? kStride * kStride : kStride;
         const double bx = cx / sc, by = cy / sc;
-        for (int i = 0; i < kS * kS; ++i) {
-            const int alpha = i / kS, beta = i % kS;
-            const double va = corr_bilinear(L.f, L.W, L.H, a.channels, g, bx + beta - kR, by + alpha - kR);
-            if (lane == 0) v[i] = va;
+        SmemWin win;
+        win.s = win_buf;
+        if (xs) {  // exact: a lane per slice sample, the reference's sequential channel loop
+            const float* gc = gp + (9 * level + 4) * a.channels;
+            const bool span = fabs(bx) < 1e8 && fabs(by) < 1e8;
+            if (span && win.s)  // the 8 x 8 cells the 7 x 7 bilinear samples touch
+                stage_window(win, L, a.channels, (int)floor(bx) - kR, (int)floor(by) - kR, 8);
+            for (int i = lane; i < kS * kS; i += 32) {
+                const int alpha = i / kS, beta = i % kS;
+                const double x = bx + beta - kR, y = by + alpha - kR;
+                double dot = 0, n2 = 0;
+                const int x0 = span ? (int)floor(x) : 0, y0 = span ? (int)floor(y) : 0;
+                if (span && win.s && win.holds(x0, y0, 2)) {
+                    // features.cpp:9-21 per channel (window zeros = out-of-grid taps), sums in order
+                    const double ax = x - x0, ay = y - y0;
+                    const float *p00 = win.cell(x0, y0), *p10 = win.cell(x0 + 1, y0);
+                    const float *p01 = win.cell(x0, y0 + 1), *p11 = win.cell(x0 + 1, y0 + 1);
+#pragma unroll 8
+                    for (int c = 0; c < a.channels; ++c) {
+                        const double vv = (1 - ax) * (1 - ay) * (double)p00[c] + ax * (1 - ay) * (double)p10[c] +
+                                          (1 - ax) * ay * (double)p01[c] + ax * ay * (double)p11[c];
+                        dot += (double)__ldg(gc + c) * vv;
+                        n2 += vv * vv;
+                    }
+                } else {
+                    corr_exact_partial(gc, L.f, L.W, L.H, a.channels, x, y, 0, 1, dot, n2);
+                }
+                v[i] = n2 > 1e-12 ? dot / sqrt(n2) : 0.0;  // correlation.cpp:22
+            }
+        } else {
+            for (int i = 0; i < kS * kS; ++i) {
+                const int alpha = i / kS, beta = i % kS;
+                const double va = corr_bilinear(L.f, L.W, L.H, a.channels, g, bx + beta - kR, by + alpha - kR);
+                if (lane == 0) v[i] = va;
+            }
         }
         __syncwarp();
         if (level == 1) {
             // level-1 subpixel peak (flow_provider.cpp:264-265), needed unless level 0 is flat
             double px, py;
             bool border;
-            subpixel_peak(L, a.channels, g, bx, by, v, &px, &py, &border);
+            subpixel_peak(L, a.channels, g, bx, by, v, &px, &py, &border, xs, win.s ? &win : nullptr);
             if (lane == 0) {
-                s_peak1[pair][0] = px;
-                s_peak1[pair][1] = py;
-                s_border1[pair] = border;
+                peak1[0] = px;
+                peak1[1] = py;
+                *border1 = border;
             }
         } else {
             // level 0: flatness / sharpness scores on the slice (flow_provider.cpp:217-250)
@@ -266,23 +428,23 @@ __global__ void __launch_bounds__(256, PVO_MEASURE_MINB) measure_kernel(MeasureP
                 }
                 const double score = 2.0 * (peak - 0.75) + (peak - second - 0.08);
                 confidence = fmin(fmax(1.0 / (1.0 + exp(-12.0 * score)), 0.01), 0.99);
-                subpixel_peak(L, a.channels, g, bx, by, v, &p0x, &p0y, &border0);
+                subpixel_peak(L, a.channels, g, bx, by, v, &p0x, &p0y, &border0, xs, win.s ? &win : nullptr);
             }
         }
     }
     // the pair meets on its named barrier at one program point, unconditionally (also
     // for behind / non-finite edges), each warp converged: bar.sync counts threads
     __syncwarp();
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+    asm volatile("bar.sync %0, 64;" ::"r"(bar) : "memory");
     if (valid && level == 0) {
         if (flat) {
             flags = 1;  // flat: delta 0, weight 0.01
         } else {
-            const bool border1 = s_border1[pair];
-            const double p1x = s_peak1[pair][0], p1y = s_peak1[pair][1];
+            const bool b1 = *border1;
+            const double p1x = peak1[0], p1y = peak1[1];
             const double e0x = kStride * p0x, e0y = kStride * p0y;
             const double e1x = kStride * kStride * p1x, e1y = kStride * kStride * p1y;
-            if (border0 && border1) {
+            if (border0 && b1) {
                 flags = 2;  // out of range: delta 0, weight 0.01
             } else {
                 if (border0) {
@@ -293,7 +455,7 @@ __global__ void __launch_bounds__(256, PVO_MEASURE_MINB) measure_kernel(MeasureP
                     dxo = e0x;
                     dyo = e0y;
                     const double ddx = e1x - e0x, ddy = e1y - e0y;
-                    if (!border1 && sqrt(ddx * ddx + ddy * ddy) > 2.0 * kStride * kStride)
+                    if (!b1 && sqrt(ddx * ddx + ddy * ddy) > 2.0 * kStride * kStride)
                         confidence = fmin(confidence, 0.25);
                 }
                 wgt = confidence;
@@ -310,6 +472,57 @@ __global__ void __launch_bounds__(256, PVO_MEASURE_MINB) measure_kernel(MeasureP
     }
 }
 
+#ifndef PVO_MEASURE_MINB
+#define PVO_MEASURE_MINB 1
+#endif
+// The direct kernel (PVO_MEASURE_DIRECT=1; A/B): four edges per block.
+__global__ void __launch_bounds__(256, PVO_MEASURE_MINB) measure_kernel(MeasureParams a) {
+    __shared__ double s_vals[8][kS * kS];
+    __shared__ double s_peak1[4][2];
+    __shared__ int s_border1[4];
+    const int warp = threadIdx.x >> 5;
+    const int pair = warp >> 1, level = warp & 1;
+    const int e = blockIdx.x * 4 + pair;
+    if (e >= a.n_edges) return;  // both warps of the pair
+    measure_direct_edge(a, e, level, s_vals[warp], s_peak1[pair], &s_border1[pair], 1 + pair, nullptr, nullptr);
+}
+
+// Exact replay: the edges the Gram-form kernel found within a rounding margin of
+// one of the reference's discrete decisions (a tied argmax, a hill-climb
+// comparison, a parabola denominator or the flatness / level-consistency
+// thresholds; measure_gram_kernel) are measured again, a warp pair per edge,
+// with every sample bit-identical to the reference.  The list is
+// replay[0] = count, replay[1 ..] = edges; it is left zeroed for the next call.
+constexpr int kExactBlocks = 296;
+constexpr int kExactWinFloats = 64 * 129;  // an 8 x 8 window at C <= 128
+constexpr int kExactSmem = 2 * kExactWinFloats * (int)sizeof(float);
+__global__ void __launch_bounds__(64) measure_exact_kernel(MeasureParams a) {
+    __shared__ double s_vals[2][kS * kS];
+    __shared__ double s_xs[2][2 * 128];
+    __shared__ double s_peak1[2];
+    __shared__ int s_border1;
+    extern __shared__ float s_win[];  // [2][kExactWinFloats]
+    const int warp = threadIdx.x >> 5;
+    const int n = min(__ldcg(a.replay), a.n_edges);
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        measure_direct_edge(a, __ldcg(a.replay + 1 + i), warp, s_vals[warp], s_peak1, &s_border1, 1, s_xs[warp],
+                            s_win + warp * kExactWinFloats);
+        __syncthreads();  // s_peak1 / s_border1 are rewritten by the next edge
+    }
+    // the last block to finish leaves the count zero for the next launch
+    __shared__ bool s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(a.replay_done, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        if (a.replay_stat) *a.replay_stat = a.replay[0];
+        a.replay[0] = 0;
+        *a.replay_done = 0;
+    }
+}
 
 // ============================================================================
 // Gram-form measurement (the default when the frame store's FP64 neighbour-Gram
@@ -366,6 +579,7 @@ struct alignas(16) MeasWarpSmem {
     float g[128];         // the level's centre-pixel descriptor
     double v[kS * kS];    // the 7x7 slice
     double sd[64];        // <g, f> of the 8x8 slice window (kept: the climb window reuses them)
+    double xs[256];       // finish_seq scratch (exact re-evaluation of near-tie comparisons)
     union {
         double sgr[64][5];  // Gram (0,0) (1,0) (0,1) (1,1) (-1,1) of the slice window
         struct {
@@ -480,9 +694,36 @@ __device__ __noinline__ double cubic_gram(const MeasWarpSmem& S, const int* off,
     return n2 > 1e-12 ? dot / sqrt(n2) : 0.0;
 }
 
+// Rounding margin of the Gram-form samples for the discrete decisions: a sample
+// is a cosine against g (|value| <= |g|) whose regrouped FP64 sums differ from
+// the reference's sequential ones by ~1e-16 |g|; any decision closer than
+// kTieRel |g| to flipping sends the edge to the exact replay.
+constexpr double kTieRel = 1e-12;
+constexpr double kTieExactRel = 1e-14;  // residual margin after an exact re-evaluation of both sides
+// near-tie reasons (bit mask)
+constexpr int kTieArgmax = 1, kTieFlat = 2, kTieDenom = 4, kTieStep = 8, kTieClimb = 16, kTieDist = 32;
+
+// Two Catmull-Rom samples with the reference's exact arithmetic (kept out of
+// line: the Gram-form climb's registers stay free of the direct sampler's).
+__device__ __noinline__ void resolve_exact(const Level& L, int C, const G4& g4, double xa, double ya, double xb,
+                                           double yb, double* xs, double* va, double* vb) {
+    *va = corr_cubic(L.f, L.W, L.H, C, g4, xa, ya, xs);
+    *vb = corr_cubic(L.f, L.W, L.H, C, g4, xb, yb, xs);
+}
+
+// Every tap of the Catmull-Rom sample at (x, y) lies outside the grid (the
+// sample is an exact zero in the reference and here).
+__device__ __forceinline__ bool cubic_pad(double x, double y, int W, int H) {
+    const double xf = floor(x), yf = floor(y);
+    return xf + 2 < 0 || xf - 1 >= W || yf + 2 < 0 || yf - 1 >= H;
+}
+
 // First-occurrence argmax of the slice (the reference's `v > best` scan order)
-// as a warp reduction: lanes hold samples lane and lane + 32.
-__device__ __forceinline__ int slice_argmax(const double* v) {
+// as a warp reduction: lanes hold samples lane and lane + 32.  *tie: another
+// sample lies within eps of the maximum (the reference's choice depends on
+// rounding there).
+__device__ __forceinline__ int slice_argmax(const double* v, double eps = -1.0, int* tie = nullptr,
+                                            const unsigned* pad = nullptr) {
     const int lane = threadIdx.x & 31;
     double b = -CUDART_INF;
     int bi = kR * kS + kR;  // no sample above -inf: the reference keeps (3, 3)
@@ -500,6 +741,15 @@ __device__ __forceinline__ int slice_argmax(const double* v) {
             bi = oi;
         }
     }
+    if (tie) {
+        // exact zeros of padding-only samples are exact in the reference too: two
+        // of them never tie by rounding (pad: bit n of lane l = sample l + 32 n)
+        const bool bpad = pad && ((__shfl_sync(0xffffffffu, pad[0], bi & 31) >> (bi >> 5)) & 1);
+        bool near = false;
+        for (int i = lane, n = 0; i < kS * kS; i += 32, ++n)
+            near |= i != bi && v[i] >= b - eps && !(bpad && ((pad[0] >> n) & 1));
+        if (__any_sync(0xffffffffu, near)) *tie |= kTieArgmax;
+    }
     return bi;
 }
 
@@ -507,9 +757,10 @@ __device__ __forceinline__ int slice_argmax(const double* v) {
 // argmax of the slice S.v, the 6x6 window around it staged, then the hill climb
 // with f0 / f2 of each parabola step on the two half warps.
 __device__ __noinline__ void subpixel_peak_gram(MeasWarpSmem& S, const Level& L, int C, const double* gm, const G4& g4,
-                                   double bx, double by, int ox, int oy, double* px, double* py, bool* on_border) {
+                                   double bx, double by, int ox, int oy, double* px, double* py, bool* on_border,
+                                   double eps, int* tie, const unsigned* pad) {
     const int lane = threadIdx.x & 31;
-    const int bi = slice_argmax(S.v);
+    const int bi = slice_argmax(S.v, eps, tie, pad);
     const int best_a = bi / kS, best_b = bi % kS;
     *on_border = best_a == 0 || best_a == kS - 1 || best_b == 0 || best_b == kS - 1;
     double dx = best_b - kR, dy = best_a - kR;
@@ -540,6 +791,7 @@ __device__ __noinline__ void subpixel_peak_gram(MeasWarpSmem& S, const Level& L,
     bool redo;
     double current = cubic_gram(S, off, qx, qy, bx + dx, by + dy, &redo);
     if (redo) current = corr_cubic(L.f, L.W, L.H, C, g4, bx + dx, by + dy);
+    bool cur_pad = cubic_pad(bx + dx, by + dy, L.W, L.H);
     double h = 0.5;
     const bool upper = lane >= 16;
 #pragma unroll 1
@@ -558,17 +810,37 @@ __device__ __noinline__ void subpixel_peak_gram(MeasWarpSmem& S, const Level& L,
             if (rb & 0x10000u) f2 = corr_cubic(L.f, L.W, L.H, C, g4, x + (along_x ? h : 0), y + (along_x ? 0 : h));
             const double f1 = current;
             const double denom = f0 - 2 * f1 + f2;
+            // near-flips of parabola_refine's tests (denominator sign / 1e-12 floor, step == 0)
+            // (padding-only samples are exact zeros in the reference too: no rounding ties)
+            const bool p0 = cubic_pad(x - (along_x ? h : 0), y - (along_x ? 0 : h), L.W, L.H);
+            const bool p2 = cubic_pad(x + (along_x ? h : 0), y + (along_x ? 0 : h), L.W, L.H);
+            if (!(p0 && p2 && cur_pad) && (fabs(denom) <= 4 * eps || fabs(fabs(denom) - 1e-12) <= 4 * eps))
+                *tie |= kTieDenom;
             double step = 0.0;
-            if (!(fabs(denom) < 1e-12 || denom > 0)) step = fmin(fmax(0.5 * h * (f0 - f2) / denom, -h), h);
+            if (!(fabs(denom) < 1e-12 || denom > 0)) {
+                step = fmin(fmax(0.5 * h * (f0 - f2) / denom, -h), h);
+                if (!(p0 && p2) && fabs(f0 - f2) <= 2 * eps) *tie |= kTieStep;
+            }
             if (step == 0.0) continue;
             const double nx = dx + (along_x ? step : 0);
             const double ny = dy + (along_x ? 0 : step);
             double value = cubic_gram(S, off, qx, qy, bx + nx, by + ny, &redo);
             if (redo) value = corr_cubic(L.f, L.W, L.H, C, g4, bx + nx, by + ny);
+            const bool vpad = cubic_pad(bx + nx, by + ny, L.W, L.H);
+            if (!(vpad && cur_pad) && fabs(value - current) <= 2 * eps) {
+                // the comparison is within the Gram form's rounding margin: evaluate both
+                // samples with the reference's exact arithmetic (per-channel samplers,
+                // sequential channel sums) at these positions, which differ from the
+                // reference's by the ~1e-16 rounding of earlier steps; only a remaining
+                // gap below kTieExactRel |g| (a true tie) needs the full exact replay
+                resolve_exact(L, C, g4, bx + nx, by + ny, bx + dx, by + dy, S.xs, &value, &current);
+                if (fabs(value - current) <= kTieExactRel / kTieRel * eps) *tie |= kTieClimb;
+            }
             if (value >= current) {  // hill climb only
                 dx = nx;
                 dy = ny;
                 current = value;
+                cur_pad = vpad;
             }
         }
     }
@@ -578,11 +850,12 @@ __device__ __noinline__ void subpixel_peak_gram(MeasWarpSmem& S, const Level& L,
 
 // One (edge, level) measurement task of a warp: the slice, then (level 0) the
 // flatness / sharpness scores and, unless flat, the subpixel peak, or (level 1)
-// the subpixel peak.  Result record: {px, py, confidence, border | flat << 1};
+// the subpixel peak.  Result record: {px, py, confidence, border | flat << 1 |
+// tie << 2 (a decision within the rounding margin: replay exactly)};
 // *valid_out / *behind_out: the edge's centre state (identical for both levels).
 struct MeasRecord {
     double px, py, conf;
-    int bits;  // border | flat << 1
+    int bits;  // border | flat << 1 | tie reasons << 2
 };
 __device__ __forceinline__ MeasRecord measure_task(const MeasureParams& a, MeasWarpSmem& S, int e, int level,
                                                    bool* valid_out, bool* behind_out) {
@@ -621,6 +894,10 @@ __device__ __forceinline__ MeasRecord measure_task(const MeasureParams& a, MeasW
             g.v[k] = c < C ? gp[c] : 0.f;
             if (c < C) S.g[c] = g.v[k];
         }
+        double gn2 = 0;
+#pragma unroll
+        for (int k = 0; k < kCh; ++k) gn2 += (double)g.v[k] * g.v[k];
+        const double eps = kTieRel * sqrt(warp_sum(gn2));
         const double sc = level ? kStride * kStride : kStride;
         const double bx = cx / sc, by = cy / sc;
         const bool span = fabs(bx) < 1e8 && fabs(by) < 1e8;  // else every tap is zero padding
@@ -650,7 +927,7 @@ __device__ __forceinline__ MeasRecord measure_task(const MeasureParams& a, MeasW
             __syncwarp();
         }
         // the 7x7 slice (correlate_at at base + (beta - 3, alpha - 3)), lane per sample
-        unsigned redo = 0;
+        unsigned redo = 0, pad = 0;  // pad: padding-only samples (exact zeros, as in the reference)
         for (int n = 0; n < 2; ++n) {
             const int i = lane + 32 * n;
             if (i >= kS * kS) break;
@@ -659,6 +936,7 @@ __device__ __forceinline__ MeasRecord measure_task(const MeasureParams& a, MeasW
             if (span) {
                 const double x = bx + beta - kR, y = by + alpha - kR;  // flow_provider.cpp:226-227
                 const int x0 = (int)floor(x), y0 = (int)floor(y);
+                if (x0 + 1 < 0 || x0 >= L.W || y0 + 1 < 0 || y0 >= L.H) pad |= 1u << n;
                 const double ax = x - x0, ay = y - y0;
                 const int lx = x0 - ox, ly = y0 - oy;
                 if (lx >= 0 && lx <= 6 && ly >= 0 && ly <= 6) {
@@ -695,13 +973,15 @@ __device__ __forceinline__ MeasRecord measure_task(const MeasureParams& a, MeasW
         }
         __syncwarp();
         bool border = false;
+        int tie = 0;  // reasons (all-padding slices, !span, are decided exactly: no ties there)
         if (level == 1) {
             r_flat = 0;
-            subpixel_peak_gram(S, L, C, gm, g, bx, by, ox, oy, &r_px, &r_py, &border);
+            subpixel_peak_gram(S, L, C, gm, g, bx, by, ox, oy, &r_px, &r_py, &border, eps, &tie, &pad);
         } else {
             // level 0: flatness / sharpness scores on the slice (flow_provider.cpp:217-250),
             // as warp reductions (the mean as a fixed-order tree)
-            const int pi = slice_argmax(S.v);
+            int targ = 0;  // (the argmax matters only when the slice is not flat)
+            const int pi = slice_argmax(S.v, eps, &targ, &pad);
             const double peak = S.v[pi];
             const int peak_a = pi / kS, peak_b = pi % kS;
             double minimum = CUDART_INF, mean = 0, second = -CUDART_INF;
@@ -720,13 +1000,17 @@ __device__ __forceinline__ MeasRecord measure_task(const MeasureParams& a, MeasW
             mean /= kS * kS;
             const double peak_to_mean = (peak - minimum) / (mean - minimum + 1e-9);
             r_flat = !(peak_to_mean >= 1.05);
+            // the flatness threshold within the propagated rounding margin of peak, min, mean
+            if (fabs(peak_to_mean - 1.05) <= 8 * eps * (1 + fabs(peak_to_mean)) / (mean - minimum + 1e-9))
+                tie |= kTieFlat;
             if (!r_flat) {
+                tie |= targ;
                 const double score = 2.0 * (peak - 0.75) + (peak - second - 0.08);
                 r_conf = fmin(fmax(1.0 / (1.0 + exp(-12.0 * score)), 0.01), 0.99);
-                subpixel_peak_gram(S, L, C, gm, g, bx, by, ox, oy, &r_px, &r_py, &border);
+                subpixel_peak_gram(S, L, C, gm, g, bx, by, ox, oy, &r_px, &r_py, &border, eps, &tie, &pad);
             }
         }
-        r_border = border;
+        r_border = border | (span ? tie << 2 : 0);
     }
     *valid_out = valid;
     *behind_out = behind;
@@ -740,6 +1024,8 @@ __device__ __forceinline__ void measure_combine(const MeasureParams& a, int e, b
     double confidence = r0.conf;
     const int b0 = r0.bits, b1 = r1.bits;
     const bool flat = (b0 >> 1) & 1, border0 = b0 & 1, border1 = b1 & 1;
+    // near-tie decisions: level 0's always count, level 1's only when its peak is used
+    int tie = valid ? (b0 >> 2) | (flat ? 0 : b1 >> 2) : 0;
     double dxo = 0, dyo = 0, wgt = 0.01;
     int flags = 0;
     if (behind) {
@@ -763,12 +1049,17 @@ __device__ __forceinline__ void measure_combine(const MeasureParams& a, int e, b
                 dxo = e0x;
                 dyo = e0y;
                 const double ddx = e1x - e0x, ddy = e1y - e0y;
-                if (!border1 && sqrt(ddx * ddx + ddy * ddy) > 2.0 * kStride * kStride)
-                    confidence = fmin(confidence, 0.25);
+                const double dist = sqrt(ddx * ddx + ddy * ddy);
+                if (!border1 && dist > 2.0 * kStride * kStride) confidence = fmin(confidence, 0.25);
+                if (!border1 && fabs(dist - 2.0 * kStride * kStride) <= 1e-9) tie |= kTieDist;
             }
             wgt = confidence;
         }
     }
+    if (tie) a.replay[1 + atomicAdd(a.replay, 1)] = e;  // measure_exact_kernel rewrites this edge
+#ifdef PVO_MEASURE_TIE_STATS  // debug variant (tools/measure_ties.py): flags = 128 | reasons, no replay
+    if (tie) flags = 128 | tie;
+#endif
     a.delta[2 * e] = dxo;
     a.delta[2 * e + 1] = dyo;
     a.weight[2 * e] = wgt;
@@ -925,8 +1216,16 @@ cudaError_t launch_measure(const MeasureParams& p, cudaStream_t stream) {
         cudaError_t err =
             cudaFuncSetAttribute(measure_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMeasSmem);
         if (err != cudaSuccess) return err;
+        if (!p.replay || !p.replay_done) return cudaErrorInvalidValue;
         measure_gram_kernel<<<(p.n_edges + kMeasWarps / 2 - 1) / (kMeasWarps / 2), 32 * kMeasWarps, kMeasSmem,
                               stream>>>(p);
+        err = cudaGetLastError();
+        if (err != cudaSuccess) return err;
+#ifndef PVO_MEASURE_TIE_STATS
+        err = cudaFuncSetAttribute(measure_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kExactSmem);
+        if (err != cudaSuccess) return err;
+        measure_exact_kernel<<<kExactBlocks, 64, kExactSmem, stream>>>(p);
+#endif
         return cudaGetLastError();
     }
     measure_kernel<<<(p.n_edges + 3) / 4, 256, 0, stream>>>(p);
