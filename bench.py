@@ -131,10 +131,13 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- workload
-def corr_bytes_per_edge(prob, K, level_shapes, D=128):
+def corr_bytes_per_edge(prob, K, level_shapes, D=128, with_fma=False):
     """Algorithmic bytes of the correlation per edge: for each
     level the union of in-bounds integer cells touched by the 3x3x7x7 bilinear
-    taps x D x 4 B, + 2 x 9 x D x 4 B of patch features + 3,528 B of output."""
+    taps x D x 4 B, + 2 x 9 x D x 4 B of patch features + 3,528 B of output.
+    with_fma: also the algorithmic contraction, sum over (edge, level, pixel) of
+    (in-grid cells of the pixel's 8x8 tap window) x D FMAs — the dot products
+    every bilinear tap is a weighted sum of (DESIGN.md §3 K2)."""
     import oracle.pyoracle as orc  # noqa: F401  (not used: coords come from the numpy generator)
     import pvo_synth as synth
 
@@ -142,6 +145,7 @@ def corr_bytes_per_edge(prob, K, level_shapes, D=128):
     total = 0.0
     poses, src = prob["poses"], prob["patch_src"]
     per = np.empty(E)
+    fma = [0]
     rel_cache = {}
     for e in range(E):
         k = prob["e_patch"][e]
@@ -164,6 +168,9 @@ def corr_bytes_per_edge(prob, K, level_shapes, D=128):
             fx, fy = np.floor(u / s).astype(int), np.floor(v / s).astype(int)
             cells = set()
             for p in range(9):
+                nx = max(0, min(W, fx[p] + 5) - max(0, fx[p] - 3))
+                ny = max(0, min(H, fy[p] + 5) - max(0, fy[p] - 3))
+                fma[0] += nx * ny * D  # <g_p, f_cell> over the pixel's in-grid 8x8 tap cells
                 for yy in range(fy[p] - 3, fy[p] + 5):
                     if 0 <= yy < H:
                         for xx in range(fx[p] - 3, fx[p] + 5):
@@ -172,7 +179,20 @@ def corr_bytes_per_edge(prob, K, level_shapes, D=128):
             b += len(cells) * D * 4
         per[e] = b
         total += b
+    if with_fma:
+        return total, per, fma[0]
     return total, per
+
+
+def fp32_roofline(total_fma, corr_ms, clk):
+    """The correlation's compute roofline: algorithmic FMAs (corr_bytes_per_edge
+    with_fma) x 2 FLOP over the measured prep + corr time, against the FP32 CUDA-core
+    peak of the clock it ran at (148 SMs x 128 FMA/clk x 2 FLOP)."""
+    mhz = (clk or {}).get("sm_max_mhz") or 1965.0
+    peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
+    ach = 2.0 * total_fma / (corr_ms * 1e-3) / 1e12
+    return {"achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+            "algorithmic_fma_per_launch": float(total_fma), "peak_kind": "148 SMs x 128 FP32 FMA/clk at sm_max_mhz"}
 
 
 L2_NOTE = "GPU arm: L2 flushed between steps (256 MiB write, outside the timed events); CPU arm: n/a"
@@ -464,12 +484,16 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         return
     hbm, peak_kind = load_peaks()
-    total_b, _ = corr_bytes_per_edge(prob, w.K, [w.level0.shape[1:3], w.level1.shape[1:3]])
+    total_b, _, total_fma = corr_bytes_per_edge(prob, w.K, [w.level0.shape[1:3], w.level1.shape[1:3]],
+                                                 with_fma=True)
     achieved = total_b / (corr_ms * 1e-3) / 1e9
     prof = ROOT / "profiles" / "corr_traffic.json"
-    traffic = None
+    traffic, counters = None, None
     if prof.exists():
-        traffic = json.loads(prof.read_text()).get(args.config)
+        pj = json.loads(prof.read_text())
+        traffic = pj.get(args.config)
+        counters = pj.get("counters", {}).get(args.config)
+    fp32 = fp32_roofline(total_fma, corr_ms, clk)
     cpu = cpu_baseline(w, prob) if (world == 1 and not args.no_cpu) else None
     value = E * world / (mean_ms * 1e-3)
     line = {
@@ -482,7 +506,9 @@ def run_ours(args, rank, world, local_rank):
         "corr_ms": corr_ms_max, "ba_ms": ba_ms_max, "propose_ms": float(np.mean(prop_ms)), "propose_replayed_edges": prop_replayed,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "kernel": "corr_tma_kernel", "peak_kind": peak_kind,
-                     "algorithmic_bytes_per_launch": total_b},
+                     "algorithmic_bytes_per_launch": total_b, "fp32": fp32, "ncu": counters,
+                     "note": "achieved = algorithmic gather bytes / (prep + corr time); the kernel is bound by FP32 "
+                             "FMA issue + shared-memory wavefronts, not DRAM (see fp32 and ncu)"},
         "e2e": {"value": E * world / (e2e["ms"] * 1e-3), "unit": "edge-iterations/s",
                 "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"], "ms_per_step": e2e["ms"]},
         "gpu_launches": int(launches),

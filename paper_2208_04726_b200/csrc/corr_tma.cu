@@ -148,6 +148,19 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
                  "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
                  : "memory");
 }
+// Correlation-volume stores: written once, never re-read by the kernels, so they
+// stream past L2 (evict-first) instead of displacing the frames and patch
+// descriptors the tiles in flight read (A/B knob CORR_STCS).
+#ifndef CORR_STCS
+#define CORR_STCS 1
+#endif
+__device__ __forceinline__ void store_out(float* p, float v) {
+#if CORR_STCS
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
+}
 __device__ __forceinline__ float rsqrt_approx(float x) {
     float r;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -298,7 +311,7 @@ __global__ void __launch_bounds__(kPrepThreads) corr_prep_kernel(CorrTmaParams a
     for (int i = t; i < 2 * s_nrec; i += kPrepThreads) list[i] = s_rec[i];
     for (int z = t >> 5; z < s_nzero; z += kPrepThreads / 32) {  // a warp per zero tile, coalesced
         float* o = a.out + (size_t)s_zero[z] * kOut;
-        for (int i = t & 31; i < kOut; i += 32) o[i] = 0.f;
+        for (int i = t & 31; i < kOut; i += 32) store_out(o + i, 0.f);
     }
 }
 
@@ -572,7 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (!((member >> p) & 1)) {
                 if ((far >> p) & 1) {  // every tap of this pixel is zero padding
 #pragma unroll
-                    for (int alpha = 0; alpha < 7; ++alpha) o[alpha * 7] = 0.f;
+                    for (int alpha = 0; alpha < 7; ++alpha) store_out(o + alpha * 7, 0.f);
                 }
                 continue;  // else: another sub-tile of this (edge, level) writes it
             }
@@ -608,7 +621,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (corr_needs_exact(n2, fmaf(wb, sB, wa * sA)))
                     exact |= 1u << (ebit + alpha);  // written once, by the re-evaluation below
                 else
-                    o[alpha * 7] = n2 > 1e-12f ? dot * rsqrt_approx(n2) : 0.f;  // correlation.cpp:22
+                    store_out(o + alpha * 7, n2 > 1e-12f ? dot * rsqrt_approx(n2) : 0.f);  // correlation.cpp:22
                 dA = dB;
                 nA = nB;
                 sA = sB;
@@ -630,7 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const double y = tc[2 * p + 1] * inv_scale + (double)(alpha - 3);
                 const float* fr = (level ? a.feat1 : a.feat0) + (size_t)r0.w * W * H * kD;
                 const float v = corr_exact_warp(a.patch_feats + (size_t)(r1.x + p) * kD, fr, W, H, kD, x, y);
-                if (lane == 0) out[p * 49 + alpha * 7 + beta] = v;
+                if (lane == 0) store_out(out + p * 49 + alpha * 7 + beta, v);
             }
         }
         __syncwarp();  // dots and the header are rewritten by the next tile

@@ -40,6 +40,27 @@ def raw(rep, names):
     return {n: vv[hh.index(n)] for n in names if n in hh}
 
 
+COUNTERS = {"dram_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+            "lts_pct": "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+            "fma_pipe_pct": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_elapsed",
+            "sm_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+            "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",
+            "smem_wavefronts_pct": "l1tex__data_pipe_lsu_wavefronts_mem_shared.avg.pct_of_peak_sustained_elapsed",
+            "kernel_us": "gpu__time_duration.sum"}
+
+
+def corr_counters(rep, tag):
+    """The correlation kernel's ncu utilisation counters (one --set full launch),
+    as bench.py reports them under roofline.ncu."""
+    d = raw(rep, list(COUNTERS.values()))
+    out = {k: float(d[v].replace(",", "")) for k, v in COUNTERS.items() if v in d}
+    if "kernel_us" in out:
+        out["kernel_us"] /= 1000.0  # base unit ns
+    out["source"] = f"profiles/{tag}_ncu_summary.md ({Path(rep).name})"
+    return out
+
+
 M = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
      "sm__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
      "lts__throughput.avg.pct_of_peak_sustained_elapsed", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_elapsed",
@@ -58,6 +79,7 @@ for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
 traffic = None
 names = sorted(f.name[len(tag) + 1:-len(".ncu-rep")] for f in src.glob(f"{tag}_*_full.ncu-rep"))
 traffic_by_cfg = {}
+counters_by_cfg = {}
 for name in names:
     rep = src / f"{tag}_{name}.ncu-rep"
     if not rep.exists():
@@ -78,9 +100,11 @@ for name in names:
         traffic = mb(vv[hh.index("dram__bytes_read.sum")]) + mb(vv[hh.index("dram__bytes_write.sum")])
         cfg = name.split("_")[1] if name.count("_") >= 2 else "c2"
         traffic_by_cfg[cfg] = traffic
+        counters_by_cfg[cfg] = corr_counters(rep, tag)
 (out_dir / f"{tag}_ncu_summary.md").write_text("\n".join(lines) + "\n")
 if traffic_by_cfg:
     traffic_by_cfg["source"] = f"{tag}_corr*_full.ncu-rep (dram__bytes_read.sum + dram__bytes_write.sum, one launch)"
+    traffic_by_cfg["counters"] = counters_by_cfg
     (out_dir / "corr_traffic.json").write_text(json.dumps(traffic_by_cfg) + "\n")
 print("\n".join(lines))
 print("traffic", traffic)
