@@ -37,6 +37,9 @@ int pvo_batch_load(pvo_ctx* ctx, int n_windows, const int* pose_off, const int* 
         std::vector<int> n_free(n_windows), n_free_d(n_windows);
         B.max_free = 0;
         B.max_poses = 0;
+        B.large_idx.clear();
+        B.large_plans.clear();
+        int max_free_large = 0;
         for (int w = 0; w < n_windows; ++w) {
             const int po = pose_off[w], ko = patch_off[w], eo = edge_off[w];
             HostProblem pr{pose_off[w + 1] - po, poses + 7 * (size_t)po, fixed + po, patch_off[w + 1] - ko, p,
@@ -47,9 +50,8 @@ int pvo_batch_load(pvo_ctx* ctx, int n_windows, const int* pose_off, const int* 
             pr.image_w = image_w;
             pr.image_h = image_h;
             validate(pr);
-            const Plan pl = make_plan(pr, false);
+            Plan pl = make_plan(pr, false);
             if (!pl.sorted) fail(PVO_INVALID_ARGUMENT, "batch_load: edges must be grouped by patch (reference order)");
-            if (pl.large) fail(PVO_UNSUPPORTED, "batch_load: a window beyond 16 free poses / 128 poses");
             std::copy(pl.free_slot.begin(), pl.free_slot.end(), free_slot.begin() + po);
             std::copy(pl.depth_slot.begin(), pl.depth_slot.end(), depth_slot.begin() + ko);
             std::copy(pl.edge_begin.begin(), pl.edge_begin.end(), edge_begin.begin() + ko + w);
@@ -61,12 +63,22 @@ int pvo_batch_load(pvo_ctx* ctx, int n_windows, const int* pose_off, const int* 
             n_free[w] = pl.n_free_poses;
             n_free_d[w] = pl.n_free_depths;
             const int np = 6 * pl.n_free_poses;
+            if (pl.large) {  // its own plan and scratch (Batch::lb); no batched-kernel buffers
+                v_off[w + 1] = v_off[w];
+                part_off[w + 1] = part_off[w];
+                sys_off[w + 1] = sys_off[w];
+                max_free_large = std::max(max_free_large, pl.n_free_poses);
+                B.large_idx.push_back(w);
+                B.large_plans.push_back(std::move(pl));
+                continue;
+            }
             v_off[w + 1] = v_off[w] + (size_t)pr.n_patches * std::max(np, 1);
             part_off[w + 1] = part_off[w] + pvo_dev::ba_partials_doubles(pl.n_free_poses, 1);
             sys_off[w + 1] = sys_off[w] + (size_t)np * (np + 1) / 2 + np + 1;
             B.max_free = std::max(B.max_free, pl.n_free_poses);
             B.max_poses = std::max(B.max_poses, pr.n_poses);
         }
+        B.n_small = n_windows - (int)B.large_idx.size();
         // device arrays
         upload(ctx, B.poses, poses, (size_t)NP * 7);
         upload(ctx, B.init_poses, poses, (size_t)NP * 7);
@@ -143,12 +155,20 @@ int pvo_batch_load(pvo_ctx* ctx, int n_windows, const int* pose_off, const int* 
             a.patch_bd = patch_bd + ko;
             a.partials = partials + part_off[w];
             a.system = system + sys_off[w];
-            a.delta = delta + (size_t)w * std::max(6 * B.max_free, 1);
+            a.delta = delta + (size_t)w * std::max(6 * B.max_free, 1);  // (large windows: Batch::lb.delta)
             a.residual_norms = norms + (size_t)w * Batch::kNormStride;
             a.n_norms = n_norms + w;
             a.status = status + w;
             a.status2 = status2 + 2 * w;
             a.attempts = attempts + w;
+        }
+        if (!B.large_idx.empty()) B.lb.delta.as<double>((size_t)6 * max_free_large);
+        for (size_t i = 0; i < B.large_idx.size(); ++i) {  // the large path's per-window buffers
+            pvo_dev::BAParams& a = B.hparams[B.large_idx[i]];
+            a.partials = nullptr;
+            a.system = nullptr;
+            a.patch_v = nullptr;
+            a.delta = static_cast<double*>(B.lb.delta.p);
         }
         B.iterations = -1;
         sync(ctx);
@@ -165,7 +185,18 @@ void batch_params(pvo_ctx* ctx, int iterations, double damping) {
         a.iterations = iterations;
         a.damping = damping;
     }
-    upload(ctx, B.params, B.hparams.data(), B.hparams.size());
+    // the batched kernel's windows: every window that is not on the large path
+    std::vector<pvo_dev::BAParams>& small = B.small_params;  // kept: the H2D copy reads it
+    small.clear();
+    size_t li = 0;
+    for (int w = 0; w < B.n_windows; ++w) {
+        if (li < B.large_idx.size() && B.large_idx[li] == w) {
+            ++li;
+            continue;
+        }
+        small.push_back(B.hparams[w]);
+    }
+    if (!small.empty()) upload(ctx, B.params, small.data(), small.size());
     B.iterations = iterations;
     B.damping = damping;
 }
@@ -215,10 +246,22 @@ int pvo_batch_iteration(pvo_ctx* ctx, int iterations, double damping, float* cor
         cp.out = vol;
         run_corr(ctx, cp);
         record_timing(ctx, 1);
-        cuda_check(pvo_dev::launch_ba_batch(static_cast<const pvo_dev::BAParams*>(B.params.p), B.n_windows,
-                                            B.max_free, B.max_poses, ctx->stream),
-                   "ba batch kernel");
-        ctx->launches += 1;
+        if (B.n_small > 0) {
+            cuda_check(pvo_dev::launch_ba_batch(static_cast<const pvo_dev::BAParams*>(B.params.p), B.n_small,
+                                                B.max_free, B.max_poses, ctx->stream),
+                       "ba batch kernel");
+            ctx->launches += 1;
+        }
+        for (size_t i = 0; i < B.large_idx.size(); ++i) {  // stream-ordered, sharing Batch::lb
+            const Plan& pl = B.large_plans[i];
+            upload(ctx, B.lb.g_begin, pl.g_begin.data(), pl.g_begin.size());
+            upload(ctx, B.lb.g_lo, pl.g_lo.data(), pl.g_lo.size());
+            upload(ctx, B.lb.g_nl, pl.g_nl.data(), pl.g_nl.size());
+            upload(ctx, B.lb.g_off, pl.g_off.data(), pl.g_off.size());
+            upload(ctx, B.lb.patch_group, pl.patch_group.data(), pl.patch_group.size());
+            pvo_dev::BAParams a = B.hparams[B.large_idx[i]];
+            launch_ba_checked(ctx, a, pl, &B.lb);
+        }
         record_timing(ctx, 2);
         ctx->timing_pending = ctx->timing;
         if (corr_out && corr_memspace != PVO_DEVICE) download(ctx, corr_out, vol, (size_t)B.n_edges * 2 * 9 * 49);

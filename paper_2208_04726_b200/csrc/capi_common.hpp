@@ -137,7 +137,15 @@ struct Batch {
         e_weight, cand_poses, cand_depth, patch_v, patch_h, patch_bd, partials, system, delta, norms, n_norms,
         status2, attempts, status, K, g_e_patch, g_e_pose, g_src, pose_slot, order, patch_feats, corr, params,
         init_poses, init_depth;
+    // windows beyond 16 free poses / 128 poses: run one after another on the large-window
+    // BA (ba_large.cu) with their own plans; the other windows share the batched kernel
+    std::vector<int> large_idx;
+    std::vector<Plan> large_plans;
+    std::vector<pvo_dev::BAParams> small_params;
+    int n_small = 0;
+    BABuffers lb;  // the large windows' group arrays and scratch
     void release() {
+        lb.release();
         DevBuf* all[] = {&poses,     &free_slot, &src,        &px,        &py,         &depth,     &depth_slot,
                          &edge_begin, &e_patch,  &e_pose,     &e_in,      &e_w,        &e_target,  &e_weight,
                          &cand_poses, &cand_depth, &patch_v,  &patch_h,   &patch_bd,   &partials,  &system,
@@ -414,8 +422,9 @@ inline pvo_dev::BAParams stage_problem(pvo_ctx* ctx, const HostProblem& pr, cons
 }
 
 // Large-window parameter block over the context's buffers (groups uploaded by stage_problem).
-inline pvo_dev::BALargeParams large_params(pvo_ctx* ctx, const pvo_dev::BAParams& a, const Plan& pl) {
-    BABuffers& B = ctx->ba;
+inline pvo_dev::BALargeParams large_params(pvo_ctx* ctx, const pvo_dev::BAParams& a, const Plan& pl,
+                                           BABuffers* bufs = nullptr) {
+    BABuffers& B = bufs ? *bufs : ctx->ba;
     pvo_dev::BALargeParams p;
     p.a = a;
     const int np = 6 * pl.n_free_poses;
@@ -440,12 +449,13 @@ inline pvo_dev::BALargeParams large_params(pvo_ctx* ctx, const pvo_dev::BAParams
     return p;
 }
 
-inline void launch_ba_checked(pvo_ctx* ctx, pvo_dev::BAParams& a, const Plan& pl) {
+// bufs: the large path's group arrays / scratch (default: the resident window's)
+inline void launch_ba_checked(pvo_ctx* ctx, pvo_dev::BAParams& a, const Plan& pl, BABuffers* bufs = nullptr) {
     cuda_check(cudaMemsetAsync(a.n_norms, 0, sizeof(int), ctx->stream), "memset");
     if (pl.large) {
         if (a.gn_step_mode) fail(PVO_UNSUPPORTED, "gauss_newton_step: pose systems beyond 16 free poses");
         cuda_check(cudaMemsetAsync(a.attempts, 0, sizeof(int), ctx->stream), "memset");
-        pvo_dev::BALargeParams p = large_params(ctx, a, pl);
+        pvo_dev::BALargeParams p = large_params(ctx, a, pl, bufs);
         const char* dump = std::getenv("PVO_BA_LARGE_DUMP");
         const int np = 6 * pl.n_free_poses;
         if (dump) p.dbg_A = ctx->ba.dbg_h.as<double>((size_t)(np + 1) * (np + 1));

@@ -445,7 +445,8 @@ int pvo_dgraph_keyframe(pvo_dgraph* g, double threshold_px, int* removed, double
 // device by the BA (freeze_targets semantics).  all_active != 0 flattens every
 // active edge (Pipeline::active_edges, pipeline.cpp:164-181: revised or not) —
 // the set propose() measures; 0 keeps the revised ones (bundle_adjust.cpp:245).
-// Windows beyond 16 free poses are not supported on this path yet.
+// Windows beyond 16 free poses / 128 poses run on the large-window BA (its patch-group
+// plan is built on the host from the device-flattened structure: one read-back).
 int pvo_window_load_dgraph(pvo_ctx* ctx, pvo_dgraph* g, int window, int all_active, int* n_poses, int* n_patches,
                            int* n_edges) {
     return guarded([&] {
@@ -487,8 +488,9 @@ int pvo_window_load_dgraph(pvo_ctx* ctx, pvo_dgraph* g, int window, int all_acti
         if (n_edges) *n_edges = Ew;
         g->window_from_graph = false;
         if (Pw == 0) return;  // nothing to optimise
-        if (N - nfixed > pvo_dev::ba_max_free_poses() || N > pvo_dev::ba_max_poses())
-            fail(PVO_UNSUPPORTED, "window_load_dgraph: windows beyond 16 free poses / 128 poses");
+        // windows beyond 16 free poses / 128 poses run on the multi-kernel large-window BA,
+        // whose patch-group plan is built on the host from the flattened structure below
+        const bool large = N - nfixed > pvo_dev::ba_max_free_poses() || N > pvo_dev::ba_max_poses();
         BABuffers& B = ctx->ba;
         pvo_dev::WindowOut o;
         o.n_poses = N;
@@ -528,6 +530,34 @@ int pvo_window_load_dgraph(pvo_ctx* ctx, pvo_dgraph* g, int window, int all_acti
         w.plan = Plan{};
         w.plan.n_free_poses = N - nfixed;
         w.plan.n_free_depths = Pw;
+        if (large) {
+            // the large path's plan (plan_groups): patch runs by source pose, their free-pose
+            // windows — from the device-flattened patch sources, edge CSR, edge poses and
+            // free slots (edges are patch-contiguous: identity permutation)
+            std::vector<int> src(Pw), ep(Ew);
+            w.plan.edge_begin.resize(Pw + 1);
+            w.plan.free_slot.resize(N);
+            download(ctx, src.data(), o.patch_src, Pw);
+            download(ctx, w.plan.edge_begin.data(), o.edge_begin, Pw + 1);
+            download(ctx, ep.data(), o.e_pose, Ew);
+            download(ctx, w.plan.free_slot.data(), o.free_slot, N);
+            sync(ctx);
+            w.plan.perm.resize(Ew);
+            for (int e = 0; e < Ew; ++e) w.plan.perm[e] = e;
+            HostProblem pr;
+            pr.n_poses = N;
+            pr.n_patches = Pw;
+            pr.n_edges = Ew;
+            pr.src = src.data();
+            pr.e_pose = ep.data();
+            w.plan.large = true;
+            plan_groups(pr, w.plan);
+            upload(ctx, B.g_begin, w.plan.g_begin.data(), w.plan.g_begin.size());
+            upload(ctx, B.g_lo, w.plan.g_lo.data(), w.plan.g_lo.size());
+            upload(ctx, B.g_nl, w.plan.g_nl.data(), w.plan.g_nl.size());
+            upload(ctx, B.g_off, w.plan.g_off.data(), w.plan.g_off.size());
+            upload(ctx, B.patch_group, w.plan.patch_group.data(), w.plan.patch_group.size());
+        }
         w.shape = HostProblem{};
         std::memcpy(w.shape.K, g->K, sizeof(g->K));
         w.shape.image_w = g->w;

@@ -495,6 +495,53 @@ def test_batch_of_windows_matches_single_windows_and_oracle(ctx):
         assert np.array_equal(p1, p2) and np.array_equal(d1, d2) and n1 == n2
 
 
+def test_batch_with_a_large_window(ctx):
+    """A batch mixing windows of <= 16 free poses (the batched kernel, a CTA per
+    window) with one of 19 free poses (run after them on the large-window BA with
+    its own patch-group plan): the large window equals the single-window large
+    path bit for bit, every window matches the oracle within the BA tolerance,
+    and reruns are bit-identical."""
+    ws = [synth.generate("c1", seed=31, frames=6, patches=24), synth.generate("c1", seed=32, frames=22, patches=10),
+          synth.generate("c1", seed=33, frames=6, patches=24)]
+    windows = [ws[0].cfg["window"], 20, ws[2].cfg["window"]]
+    _, H0, W0, D = ws[0].level0.shape
+    _, H1, W1, _ = ws[0].level1.shape
+    nF = [w.cfg["frames"] for w in ws]
+    base = np.concatenate([[0], np.cumsum(nF)])
+    ctx.frames_reserve(int(base[-1]), W0, H0, W1, H1, D)
+    probs, slots, wps = [], [], []
+    for i, w in enumerate(ws):
+        for f in range(nF[i]):
+            ctx.frames_upload(int(base[i]) + f, w.level0[f], w.level1[f])
+        g = synth.build_graph(w, pvo.PatchGraph)
+        wp = g.window_problem(windows[i])
+        wps.append(wp)
+        prob = synth.window_arrays(w, wp)
+        probs.append(prob)
+        slots.append(prob["pose_frames"] + int(base[i]))
+    assert int((~probs[1]["fixed"].astype(bool)).sum()) > 16
+    bat = pvo.Batch(ctx)
+    bat.load(probs, slots, [p["patch_feats"] for p in probs], ws[0].K, ws[0].image)
+    bat.iteration(2)
+    res = bat.read()
+    for i, (w, prob) in enumerate(zip(ws, probs)):
+        win = pvo.Window(ctx)
+        win.load(prob, slots[i], prob["patch_feats"], w.K, w.image)
+        win.iteration(2)
+        p1, d1, n1 = win.read()
+        poses, depth, norms = res[i]
+        if i == 1:  # the large window runs the same kernels as the single-window large path
+            assert np.array_equal(poses, p1) and np.array_equal(depth, d1) and np.array_equal(norms, n1)
+        rb = orc.ba_window(wps[i], w.K, iterations=2)
+        dt, dq = pose_parity(poses, rb["poses"])
+        assert dt.max() <= 1e-3 and dq.max() <= 1e-3
+        assert len(norms) == len(rb["residual_norms"]) and np.allclose(norms, rb["residual_norms"], rtol=1e-6)
+    bat.reset()
+    bat.iteration(2)
+    for (p1, d1, n1), (p2, d2, n2) in zip(res, bat.read()):
+        assert np.array_equal(p1, p2) and np.array_equal(d1, d2) and np.array_equal(n1, n2)
+
+
 def _measure_report(name, d, w, fl, rd, rw, rfl):
     dd = np.abs(d - rd).max(1)
     dw = np.abs(w - rw).max(1)
@@ -698,6 +745,45 @@ def test_device_graph_window_loop_matches_host_path(ctx):
     key = {(int(a), int(b)): i for i, (a, b) in enumerate(zip(kk, jj))}
     rows = [key[(int(prob["patch_ids"][k]), int(prob["pose_frames"][j]))] for k, j in zip(prob["e_patch"], prob["e_pose"])]
     assert has[rows].all() and np.array_equal(rev[rows, :2], pd) and np.array_equal(rev[rows, 2:], pw)
+
+
+def test_device_graph_large_window_matches_host_path(ctx):
+    """A device-graph window beyond 16 free poses (20-frame window: 19 free poses,
+    a 114-dim pose system) runs on the large-window BA with a patch-group plan
+    built from the device-flattened structure; it equals the host-flattened
+    window's run bit for bit (same plan, same kernels) and the oracle within
+    the BA tolerance."""
+    w = synth.generate("c1", seed=5, frames=22, patches=10)
+    F, M = w.cfg["frames"], w.cfg["patches"]
+    window = 20
+    _, H0, W0, D = w.level0.shape
+    _, H1, W1, _ = w.level1.shape
+    ctx.frames_reserve(F, W0, H0, W1, H1, D)
+    for f in range(F):
+        ctx.frames_upload(f, w.level0[f], w.level1[f])
+    dev = pvo.DeviceGraph(ctx, w.K, w.image[0], w.image[1], channels=D)
+    for f in range(F):
+        dev.add_frame(0.05 * f, w.poses[f], frame_slot=f)
+        ks = slice(f * M, (f + 1) * M)
+        dev.add_patches(f, w.centroids[ks], w.depth[ks], w.patch_feats[ks])
+        dev.connect(w.cfg["radius"])
+    dev.set_revisions(w.active_kk, w.active_jj, w.deltas, w.weights)
+    g = synth.build_graph(w, pvo.PatchGraph)
+    wp = g.window_problem(window)
+    assert int((~wp["fixed"].astype(bool)).sum()) > 16
+    prob = synth.window_arrays(w, wp)
+    win = pvo.Window(ctx)
+    win.load(prob, prob["pose_frames"], prob["patch_feats"], w.K, w.image)
+    win.iteration(2)
+    p_host, d_host, n_host = win.read()
+    N, P, E = dev.load_window(window)
+    assert (N, P, E) == (len(prob["poses"]), len(prob["depth"]), len(prob["e_patch"]))
+    dev.window.iteration(2)
+    p_dev, d_dev, n_dev = dev.window.read()
+    assert np.array_equal(p_dev, p_host) and np.array_equal(d_dev, d_host) and n_dev == n_host
+    rb = orc.ba_window(wp, w.K, iterations=2)
+    assert np.abs(p_dev[:, 4:] - rb["poses"][:, 4:]).max() <= 1e-3
+    assert np.abs(d_dev - rb["depth"]).max() <= 1e-3 * max(1.0, np.abs(rb["depth"]).max())
 
 
 def test_device_graph_keyframe_matches_pipeline_rule(ctx):
