@@ -389,6 +389,15 @@ class PatchGraph:
 
 
 # ---- bundle adjustment on flat problems ----
+def _patch_width(px):
+    """p of a [P, p*p] patch-pixel array (Patch::make's row-major grid)."""
+    pp = px.shape[1] if px.ndim == 2 and px.shape[0] else 9
+    p = int(round(pp ** 0.5))
+    if p * p != pp:
+        raise ValueError("patch pixel arrays must hold p*p entries per patch")
+    return p
+
+
 def _prob_args(pr):
     poses = _f64(pr["poses"]).reshape(-1, 7)
     fixed = np.ascontiguousarray(pr["fixed"], np.uint8)
@@ -410,7 +419,7 @@ def gauss_newton_step(pr, K, damping=1e-4, depth_free=None, debug=False):
     nd = Pn if dfree is None else int(dfree.sum())
     n = 6 * nf + nd
     dh, db = (np.empty((n, n)), np.empty(n)) if debug else (None, None)
-    check(lib.orc_gauss_newton_step(I(N), _p(poses), _p(fixed), I(Pn), I(3), _p(src), _p(px), _p(py), _p(d),
+    check(lib.orc_gauss_newton_step(I(N), _p(poses), _p(fixed), I(Pn), I(_patch_width(px)), _p(src), _p(px), _p(py), _p(d),
                                     _p(dfree), I(E), _p(ep), _p(eo), _p(et), _p(ew), _p(_f64(K, (4,))), D(damping),
                                     _p(out_p), _p(out_d), _p(norms), _p(dh), _p(db), C.byref(nfp), C.byref(nfd)))
     res = dict(poses=out_p, depth=out_d, residual_norms=list(norms))
@@ -425,7 +434,7 @@ def ba_window(pr, K, damping=1e-4, iterations=2, structure_only=0):
     N, Pn, E = len(poses), len(d), len(ep)
     out_p, out_d, norms = np.empty((N, 7)), np.empty(Pn), np.empty(iterations + 2)
     nn = I()
-    check(lib.orc_ba_window(I(N), _p(poses), _p(fixed), I(Pn), I(3), _p(src), _p(px), _p(py), _p(d), I(E), _p(ep),
+    check(lib.orc_ba_window(I(N), _p(poses), _p(fixed), I(Pn), I(_patch_width(px)), _p(src), _p(px), _p(py), _p(d), I(E), _p(ep),
                             _p(eo), _p(et), _p(ew), _p(_f64(K, (4,))), D(damping), I(iterations), I(structure_only),
                             _p(out_p), _p(out_d), _p(norms), C.byref(nn)))
     return dict(poses=out_p, depth=out_d, residual_norms=list(norms[: nn.value]))

@@ -12,8 +12,41 @@ void set_last_error(const std::string& msg) { g_last_error = msg; }
 
 namespace pvo_host {
 
-void run_ba(pvo_ctx* ctx, const HostProblem& pr, const BARun& run) {
+// Patches of any odd width p on the 3 x 3 kernels: the bundle adjustment reads a
+// patch only through (a) its centre pixel p*p/2 — the Jacobian centre
+// Patch::center(), the frozen-target and WRMS centre PatchReprojection::center()
+// (camera.cpp:34-44, camera.hpp:49), one and the same pixel for odd p — and
+// (b) the behind-camera test "any pixel with q_z <= eps" (camera.cpp:47-71).  q_z
+// is affine in the pixel coordinates and the patch grid is axis-aligned, so its
+// minimum over the p x p grid is attained at one of the 4 corners: the 3 x 3
+// stand-in {first, centre, last column} x {first, centre, last row} carries
+// exactly the pixels the reference's decisions depend on.  (Even widths use the
+// pixel mean as the Jacobian centre but pixel p*p/2 for targets: unsupported.)
+static HostProblem as_3x3(const HostProblem& pr, std::vector<double>& px9, std::vector<double>& py9) {
+    if (pr.p < 1) fail(PVO_INVALID_ARGUMENT, "patch: width must be >= 1");
+    if (pr.p == 3) return pr;
+    if (pr.p % 2 == 0) fail(PVO_UNSUPPORTED, "ba: even patch widths (the Jacobian centre is not a pixel)");
+    const int p = pr.p, cols[3] = {0, p / 2, p - 1};
+    px9.resize((size_t)pr.n_patches * 9);
+    py9.resize((size_t)pr.n_patches * 9);
+    for (int k = 0; k < pr.n_patches; ++k)
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) {
+                const size_t src = (size_t)k * p * p + (size_t)cols[r] * p + cols[c];
+                px9[(size_t)k * 9 + 3 * r + c] = pr.px[src];
+                py9[(size_t)k * 9 + 3 * r + c] = pr.py[src];
+            }
+    HostProblem q = pr;
+    q.p = 3;
+    q.px = px9.data();
+    q.py = py9.data();
+    return q;
+}
+
+void run_ba(pvo_ctx* ctx, const HostProblem& pr_in, const BARun& run) {
     bind(ctx);
+    std::vector<double> px9, py9;
+    const HostProblem pr = as_3x3(pr_in, px9, py9);
     validate(pr);
     if (run.gn_step_mode && pr.n_edges == 0) fail(PVO_INVALID_ARGUMENT, "ba: need at least one edge");
     const Plan pl = make_plan(pr, false);

@@ -284,10 +284,10 @@ def generate(name: str = "c2", seed: int | None = None, channels: int = CHANNELS
                     delta, weight, lvl0, lvl1, pfeat)
 
 
-def build_graph(w: Workload, graph_cls, with_revisions: bool = True):
+def build_graph(w: Workload, graph_cls, with_revisions: bool = True, patch_width: int = 3):
     """Build a PatchGraph (product or oracle class) the way Pipeline::admit does."""
     F, M = w.cfg["frames"], w.cfg["patches"]
-    g = graph_cls(w.K, w.image[0], w.image[1], 3)
+    g = graph_cls(w.K, w.image[0], w.image[1], patch_width)
     for f in range(F):
         idx = g.add_frame(0.05 * f, w.poses[f])
         assert idx == f
