@@ -791,7 +791,6 @@ __device__ __noinline__ void subpixel_peak_gram(MeasWarpSmem& S, const Level& L,
     bool redo;
     double current = cubic_gram(S, off, qx, qy, bx + dx, by + dy, &redo);
     if (redo) current = corr_cubic(L.f, L.W, L.H, C, g4, bx + dx, by + dy);
-    bool cur_pad = cubic_pad(bx + dx, by + dy, L.W, L.H);
     double h = 0.5;
     const bool upper = lane >= 16;
 #pragma unroll 1
@@ -812,22 +811,24 @@ __device__ __noinline__ void subpixel_peak_gram(MeasWarpSmem& S, const Level& L,
             const double denom = f0 - 2 * f1 + f2;
             // near-flips of parabola_refine's tests (denominator sign / 1e-12 floor, step == 0)
             // (padding-only samples are exact zeros in the reference too: no rounding ties)
-            const bool p0 = cubic_pad(x - (along_x ? h : 0), y - (along_x ? 0 : h), L.W, L.H);
-            const bool p2 = cubic_pad(x + (along_x ? h : 0), y + (along_x ? 0 : h), L.W, L.H);
-            if (!(p0 && p2 && cur_pad) && (fabs(denom) <= 4 * eps || fabs(fabs(denom) - 1e-12) <= 4 * eps))
+            if ((fabs(denom) <= 4 * eps || fabs(fabs(denom) - 1e-12) <= 4 * eps) &&
+                !(cubic_pad(x - (along_x ? h : 0), y - (along_x ? 0 : h), L.W, L.H) &&
+                  cubic_pad(x + (along_x ? h : 0), y + (along_x ? 0 : h), L.W, L.H) && cubic_pad(x, y, L.W, L.H)))
                 *tie |= kTieDenom;
             double step = 0.0;
             if (!(fabs(denom) < 1e-12 || denom > 0)) {
                 step = fmin(fmax(0.5 * h * (f0 - f2) / denom, -h), h);
-                if (!(p0 && p2) && fabs(f0 - f2) <= 2 * eps) *tie |= kTieStep;
+                if (fabs(f0 - f2) <= 2 * eps && !(cubic_pad(x - (along_x ? h : 0), y - (along_x ? 0 : h), L.W, L.H) &&
+                                                   cubic_pad(x + (along_x ? h : 0), y + (along_x ? 0 : h), L.W, L.H)))
+                    *tie |= kTieStep;
             }
             if (step == 0.0) continue;
             const double nx = dx + (along_x ? step : 0);
             const double ny = dy + (along_x ? 0 : step);
             double value = cubic_gram(S, off, qx, qy, bx + nx, by + ny, &redo);
             if (redo) value = corr_cubic(L.f, L.W, L.H, C, g4, bx + nx, by + ny);
-            const bool vpad = cubic_pad(bx + nx, by + ny, L.W, L.H);
-            if (!(vpad && cur_pad) && fabs(value - current) <= 2 * eps) {
+            if (fabs(value - current) <= 2 * eps &&
+                !(cubic_pad(bx + nx, by + ny, L.W, L.H) && cubic_pad(bx + dx, by + dy, L.W, L.H))) {
                 // the comparison is within the Gram form's rounding margin: evaluate both
                 // samples with the reference's exact arithmetic (per-channel samplers,
                 // sequential channel sums) at these positions, which differ from the
@@ -840,7 +841,6 @@ __device__ __noinline__ void subpixel_peak_gram(MeasWarpSmem& S, const Level& L,
                 dx = nx;
                 dy = ny;
                 current = value;
-                cur_pad = vpad;
             }
         }
     }
@@ -1072,6 +1072,9 @@ __device__ __forceinline__ void measure_combine(const MeasureParams& a, int e, b
 #ifndef PVO_MEASURE_GRAM_MINB
 #define PVO_MEASURE_GRAM_MINB 2
 #endif
+// A block runs kMeasWarps / 2 edges: warp 2m level 0 and warp 2m + 1 level 1 of edge
+// m, meeting on a named barrier.  (A persistent grid of warp pairs taking edges from a
+// queue ran 15 % slower: profiles/r2/measure_ab.txt.)
 __global__ void __launch_bounds__(32 * kMeasWarps, PVO_MEASURE_GRAM_MINB) measure_gram_kernel(MeasureParams a) {
     extern __shared__ __align__(16) unsigned char s_meas[];
     __shared__ MeasRecord s_rec1[kMeasWarps / 2];

@@ -22,3 +22,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:corr
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:corr_tma_kernel -s 2 -c 1 -o $o/${tag}_corr_c4_full \
   python bench.py --no-cpu --config c4 --steps 5 --warmup 3 > /dev/null 2>&1
 ls $o | grep $tag
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:measure_gram_kernel -s 1 -c 1 -o $o/${tag}_measure_full \
+  python tools/prof_measure.py c2 2 > /dev/null 2>&1
