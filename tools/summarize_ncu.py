@@ -14,7 +14,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
-out_dir = ROOT / "profiles"
+out_dir = ROOT / "profiles" / (tag[:2] if tag.startswith("r2") else "")
 out_dir.mkdir(exist_ok=True)
 src = ROOT / "gpurun_out"
 
@@ -57,7 +57,7 @@ def corr_counters(rep, tag):
     out = {k: float(d[v].replace(",", "")) for k, v in COUNTERS.items() if v in d}
     if "kernel_us" in out:
         out["kernel_us"] /= 1000.0  # base unit ns
-    out["source"] = f"profiles/{tag}_ncu_summary.md ({Path(rep).name})"
+    out["source"] = f"{out_dir.relative_to(ROOT)}/{tag}_ncu_summary.md ({Path(rep).name})"
     return out
 
 
@@ -67,14 +67,15 @@ M = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", 
      "smsp__inst_executed.sum", "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
      "sm__warps_active.avg.pct_of_peak_sustained_active", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
 lines = [f"# ncu summary ({tag})", "", "## Launch list (own kernels, `--metrics gpu__time_duration.sum`, cold/serialised)", "",
-         "`bench.py` also times the flow provider's `propose` once per run (its `propose_ms` field): `measure_kernel`",
-         "is listed but is not part of the benchmark step (Gram + tile preparation + correlation + BA); the step",
-         "share column excludes it.", "",
+         "`bench.py` also times the flow provider's `propose` once per run (its `propose_ms` field): its kernels",
+         "(`measure_gram_kernel`, `measure_exact_kernel`, the per-slot `gram25_kernel` maps) are listed but are not",
+         "part of the benchmark step (Gram + tile preparation + correlation + BA); the step share column excludes them.", "",
          "| kernel | launches | mean us | share | step share |", "|---|---|---|---|---|"]
 tot = sum(sum(v) for v in per.values())
-step_tot = sum(sum(v) for k, v in per.items() if k != "measure_kernel")
+NOT_STEP = ("measure_kernel", "measure_gram_kernel", "measure_exact_kernel", "gram25_kernel")  # propose(), not the step
+step_tot = sum(sum(v) for k, v in per.items() if k not in NOT_STEP)
 for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
-    ss = "—" if k == "measure_kernel" else f"{100 * sum(v) / step_tot:.1f}%"
+    ss = "—" if k in NOT_STEP else f"{100 * sum(v) / step_tot:.1f}%"
     lines.append(f"| {k} | {len(v)} | {sum(v) / len(v) / 1000:.1f} | {100 * sum(v) / tot:.1f}% | {ss} |")
 traffic = None
 names = sorted(f.name[len(tag) + 1:-len(".ncu-rep")] for f in src.glob(f"{tag}_*_full.ncu-rep"))
@@ -105,6 +106,6 @@ for name in names:
 if traffic_by_cfg:
     traffic_by_cfg["source"] = f"{tag}_corr*_full.ncu-rep (dram__bytes_read.sum + dram__bytes_write.sum, one launch)"
     traffic_by_cfg["counters"] = counters_by_cfg
-    (out_dir / "corr_traffic.json").write_text(json.dumps(traffic_by_cfg) + "\n")
+    (ROOT / "profiles" / "corr_traffic.json").write_text(json.dumps(traffic_by_cfg) + "\n")
 print("\n".join(lines))
 print("traffic", traffic)
