@@ -958,6 +958,7 @@ __device__ __forceinline__ MeasRecord measure_task(const MeasureParams& a, MeasW
             }
             S.v[i] = val;
         }
+        __syncwarp();  // the owners' writes of S.v are ordered before lane 0 rewrites flagged samples
         unsigned todo = __ballot_sync(0xffffffffu, redo != 0);
         while (todo) {  // direct evaluation of the flagged samples, a warp each
             const int src = __ffs(todo) - 1;

@@ -7,7 +7,9 @@ Covers: gram_kernel, corr_prep_kernel + corr_tma_kernel (D = 128, with the
 cancellation fallback triggered), corr_kernel (D = 25), ba_kernel (window,
 guard), bal_* (large window: 20 free poses), ba_batch_kernel, the device
 graph (connect / flatten / keyframe / remove), measure + oracle propose,
-feature extraction + crop.  Prints 'sanitize cases ok'."""
+feature extraction + crop, the measurement's exact replay on tied slices, a
+batch holding a window beyond 16 free poses, odd patch widths.  Prints
+'sanitize cases ok'."""
 import sys
 from pathlib import Path
 
@@ -85,6 +87,37 @@ for f in range(10):
         dg.store_window(revisions=False, state=True)
     if f >= 6:
         dg.keyframe(1e9)
+# --- provider measurement on exact ties (stripes): the exact replay kernel runs --
+Hs, Ws, Ds = 30, 40, 128
+rng = np.random.default_rng(9)
+row = rng.standard_normal((Hs, 1, Ds))
+row /= np.linalg.norm(row, axis=-1, keepdims=True)
+stripes = (row * np.where(np.arange(Ws) % 2 == 0, 1.0, -1.0)[None, :, None]).astype(np.float32)
+l1s = stripes[: Hs // 4 + 1, : Ws // 4].copy()
+ctx.frames_reserve(1, Ws, Hs, Ws // 4, Hs // 4 + 1, Ds)
+ctx.frames_upload(0, stripes, l1s)
+ns = 24
+cs = np.stack([rng.uniform(8, 4 * Ws - 8, ns), rng.uniform(8, 4 * Hs - 8, ns)], 1)
+fs = rng.standard_normal((ns, 2, 9, Ds)).astype(np.float32)
+pvo.measure_batch(np.arange(ns, dtype=np.int32), np.zeros(ns, np.int32), cs, fs, ctx=ctx)
+assert ctx.measure_replayed > 0
+# --- batch with a window beyond 16 free poses (batched kernel + bal_* chain) ---
+wb = synth.generate("c1", seed=8, frames=22, patches=8)
+ctx.frames_reserve(22 + F, W0, H0, W1, H1, D)
+for f in range(22):
+    ctx.frames_upload(f, wb.level0[f], wb.level1[f])
+for f in range(F):
+    ctx.frames_upload(22 + f, w.level0[f], w.level1[f])
+pbig = synth.window_arrays(wb, synth.build_graph(wb, pvo.PatchGraph).window_problem(20))
+bat2 = pvo.Batch(ctx)
+bat2.load([pbig, prob], [pbig["pose_frames"], prob["pose_frames"] + 22], [pbig["patch_feats"], prob["patch_feats"]],
+          w.K, w.image)
+bat2.iteration(2)
+bat2.read()
+# --- odd patch widths through the 3x3 stand-in ----------------------------------
+g5 = synth.build_graph(synth.generate("c1", seed=10, frames=6, patches=8, features=False), pvo.PatchGraph,
+                       patch_width=5)
+pvo.optimize_window(g5, pvo.WindowOptions(window=6), ctx=ctx)
 ctx.synchronize()
 ctx.close()
 print("sanitize cases ok")
