@@ -70,7 +70,7 @@ __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 struct Layout {
     int ab, pose, cand, rmat, rmatc, delta, flags, uni;
     int S, rhs, rec, vb, scal, wr, ints;  // assembly
-    int A, x, od, perm, c, l, pw;         // solve
+    int A, x, od, perm, c, l, pw, blk;    // solve
     int total;
 };
 
@@ -127,6 +127,9 @@ __host__ __device__ inline Layout make_layout(int np_full, int n_poses) {
     s += 8 * 16 * (np_full + 1);  // blocked LDL^T panel buffers (L^T panel, L D panel)
     L.perm = s;
     s += 4 * np_full;
+    s = align16(s);
+    L.blk = s;  // 6-column blocked LDL^T: raw panel [6][112], W and L panels [112][6]
+    s += 8 * 3 * 6 * 112;
     L.total = align16(a > s ? a : s);
     return L;
 }
@@ -296,7 +299,215 @@ __device__ bool ldlt_solve_regs(const double* sys, int np, unsigned char* smem, 
     return true;
 }
 
+// 1 / d in FP64: the MUFU estimate + two Newton steps (full precision, not the
+// correctly rounded __drcp_rn: a shorter dependency chain on the pivot path;
+// every thread computes the same value, so CTAs stay bit-identical)
+__device__ __forceinline__ double rcp_nr(double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
+}
+
+// Blocked variant: 6 columns (one pose) per step, two barriers per step instead of
+// six.  The matrix stays register-resident and block-cyclic as above.  Step K
+// (columns k0 .. k0+5): the owners have published the block's raw columns (rows
+// >= k0) to a panel; every row thread i >= k0 + 6 (the rhs row np included)
+// factors the 6 x 6 diagonal block redundantly in registers (LDL^T, natural order)
+// and solves its row, W_i = A_iK L_KK^-T and L_iK = W_i D_K^-1, writing L_iK
+// (final) into A and W_i / L_iK into the panels; after a barrier every thread
+// applies the block's rank-6 update A_ij -= L_iK . W_jK to its entries and the
+// owners of the next block publish it.  The same factorisation as the unblocked
+// loop up to the regrouping of each block's six updates.
+template <int RPT, int CPT>
+__device__ bool ldlt_solve_blk6(const double* sys, int np, unsigned char* smem, const Layout& L, double* x_out) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int ty = tid / kGrid, tx = tid % kGrid;
+    SOLVE_PROBE_BEGIN
+    const int ld = np + 1;
+    constexpr int kR = kGrid * RPT;  // rows held (>= np + 1)
+    double* A = at<double>(smem, L.A);
+    double* dinv = at<double>(smem, L.c);
+    double* dv = at<double>(smem, L.l);
+    double* P = at<double>(smem, L.blk);  // [6][kR] raw panel columns
+    double* Wp = P + 6 * kR;              // [kR][6] W rows
+    double* Lp = Wp + 6 * kR;             // [kR][6] L rows
+    int* s_fail = at<int>(smem, L.perm);
+    double v[RPT][CPT];
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) {
+        const int i = ty + kGrid * a;
+#pragma unroll
+        for (int b = 0; b < CPT; ++b) {
+            const int j = tx + kGrid * b;
+            double x = 0.0;
+            if (j <= i && j < np && i <= np) x = i < np ? sys[j * np - j * (j - 1) / 2 + (i - j)] : sys[nent_of(np) + j];
+            v[a][b] = x;
+        }
+    }
+    if (tid == 0) *s_fail = 0;
+    // the first block's raw columns
+#pragma unroll
+    for (int b = 0; b < CPT; ++b) {
+        const int j = tx + kGrid * b;
+        if (j < 6 && j < np) {
+#pragma unroll
+            for (int a = 0; a < RPT; ++a) {
+                const int i = ty + kGrid * a;
+                if (i >= 0 && i <= np) P[j * kR + i] = v[a][b];
+            }
+        }
+    }
+    __syncthreads();
+    SOLVE_PROBE(0)
+    for (int k0 = 0; k0 < np; k0 += 6) {
+        const int kn = k0 + 6;
+        // ---- panel: row threads ----
+        const int i = k0 + tid;
+        if (i <= np) {
+            // diagonal block LDL^T in registers: l[r][m] (r > m), d[m]
+            double a6[6][6], d[6], id[6];
+#pragma unroll
+            for (int r = 0; r < 6; ++r)
+#pragma unroll
+                for (int m = 0; m <= r; ++m) a6[r][m] = P[m * kR + k0 + r];
+#pragma unroll
+            for (int m = 0; m < 6; ++m) {
+                double dm = a6[m][m];
+#pragma unroll
+                for (int q = 0; q < m; ++q) dm -= a6[m][q] * (a6[m][q] * d[q]);
+                d[m] = dm;
+                id[m] = dm != 0.0 ? rcp_nr(dm) : 0.0;
+#pragma unroll
+                for (int r = m + 1; r < 6; ++r) {
+                    double s = a6[r][m];
+#pragma unroll
+                    for (int q = 0; q < m; ++q) s -= a6[r][q] * (a6[m][q] * d[q]);
+                    a6[r][m] = s * id[m];  // l_rm
+                }
+            }
+            if (i < kn) {  // a diagonal-block row: its L entries and pivot are final
+#pragma unroll
+                for (int rr = 0; rr < 6; ++rr) {  // rr == tid (static register indices)
+                    if (rr != tid) continue;
+#pragma unroll
+                    for (int m = 0; m < rr; ++m) A[i * ld + k0 + m] = fabs(d[m]) > DBL_MIN ? a6[rr][m] : 0.0;
+                    dv[i] = d[rr];
+                    dinv[i] = id[rr];
+                    bool bad = !(d[rr] >= 0.0) || !isfinite(d[rr]);
+                    // zero pivot: valid only with a zero column below (LDLT::info())
+#pragma unroll
+                    for (int q = rr + 1; q < 6; ++q) bad = bad || (d[rr] == 0.0 && a6[q][rr] != 0.0);
+                    if (bad) *s_fail = 1;
+                }
+            } else {  // a panel row (or the rhs row): W_i = A_iK L_KK^-T, L_iK = W_i D^-1
+                double w[6];
+#pragma unroll
+                for (int q = 0; q < 6; ++q) {
+                    double s = P[q * kR + i];
+#pragma unroll
+                    for (int m = 0; m < q; ++m) s -= w[m] * a6[q][m];
+                    w[q] = s;
+                }
+                const int r = i - kn;
+                bool bad = false;
+#pragma unroll
+                for (int q = 0; q < 6; ++q) {
+                    const double lq = fabs(d[q]) > DBL_MIN ? w[q] * id[q] : 0.0;
+                    bad = bad || (d[q] == 0.0 && w[q] != 0.0 && i < np);
+                    Wp[r * 6 + q] = w[q];
+                    Lp[r * 6 + q] = lq;
+                    A[i * ld + k0 + q] = lq;
+                }
+                if (bad) *s_fail = 1;
+            }
+        }
+        __syncthreads();
+        if (kn >= np) break;
+        // ---- trailing update A_ij -= L_iK . W_jK for i, j >= k0 + 6 ----
+        double lr[RPT][6], wc[CPT][6];
+#pragma unroll
+        for (int a = 0; a < RPT; ++a) {  // 16-byte loads: a row is 48 B
+            const int ia = ty + kGrid * a - kn;
+            const bool in = ia >= 0 && ia <= np - kn;
+            const double2* src = reinterpret_cast<const double2*>(Lp + (in ? ia : 0) * 6);
+#pragma unroll
+            for (int h = 0; h < 3; ++h) {
+                const double2 t = in ? src[h] : make_double2(0.0, 0.0);
+                lr[a][2 * h] = t.x;
+                lr[a][2 * h + 1] = t.y;
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < CPT; ++b) {
+            const int jb = tx + kGrid * b - kn;
+            const bool in = jb >= 0 && jb < np - kn;
+            const double2* src = reinterpret_cast<const double2*>(Wp + (in ? jb : 0) * 6);
+#pragma unroll
+            for (int h = 0; h < 3; ++h) {
+                const double2 t = in ? src[h] : make_double2(0.0, 0.0);
+                wc[b][2 * h] = t.x;
+                wc[b][2 * h + 1] = t.y;
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < RPT; ++a)
+#pragma unroll
+            for (int b = 0; b < CPT; ++b) {
+                double s = v[a][b];
+#pragma unroll
+                for (int q = 0; q < 6; ++q) s -= lr[a][q] * wc[b][q];
+                v[a][b] = s;
+            }
+        // the next block's raw columns kn .. kn+5 (rows >= kn)
+#pragma unroll
+        for (int b = 0; b < CPT; ++b) {
+            const int j = tx + kGrid * b;
+            if (j >= kn && j < kn + 6 && j < np) {
+#pragma unroll
+                for (int a = 0; a < RPT; ++a) {
+                    const int ii = ty + kGrid * a;
+                    if (ii >= kn && ii <= np) P[(j - kn) * kR + ii] = v[a][b];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    SOLVE_PROBE(1)
+    if (*((volatile int*)s_fail)) return false;  // uniform: read after the loop's last barrier
+    SOLVE_PROBE(2)
+    if (warp == 0) {
+        __syncwarp();
+        const double* z = A + np * ld;
+        double z0 = lane < np ? z[lane] : 0.0, z1 = lane + 32 < np ? z[lane + 32] : 0.0;
+        double z2 = lane + 64 < np ? z[lane + 64] : 0.0;
+        for (int i = np - 1; i >= 0; --i) {
+            const int sl = i >> 5;
+            const double own = sl == 0 ? z0 : sl == 1 ? z1 : z2;
+            const double xi = __shfl_sync(0xffffffffu, own, i & 31);
+            const double* Li = A + i * ld;
+            if (lane < i) z0 -= Li[lane] * xi;
+            if (lane + 32 < i) z1 -= Li[lane + 32] * xi;
+            if (lane + 64 < i) z2 -= Li[lane + 64] * xi;
+        }
+        if (lane < np) x_out[lane] = z0;
+        if (lane + 32 < np) x_out[lane + 32] = z1;
+        if (lane + 64 < np) x_out[lane + 64] = z2;
+    }
+    __syncthreads();
+    SOLVE_PROBE(3)
+    return true;
+}
+
 __device__ bool ldlt_solve_cta(const double* sys, int np, unsigned char* smem, const Layout& L, double* x_out) {
+#ifndef PVO_LDLT_SCALAR
+    if (np % 6 == 0) {  // pose systems: 6 columns per pose
+        if (np <= 63) return ldlt_solve_blk6<4, 4>(sys, np, smem, L, x_out);
+        return ldlt_solve_blk6<7, 6>(sys, np, smem, L, x_out);
+    }
+#endif
     if (np <= 63) return ldlt_solve_regs<4, 4>(sys, np, smem, L, x_out);  // rows <= 64, columns <= 64
     return ldlt_solve_regs<7, 6>(sys, np, smem, L, x_out);                // np <= 96: rows <= 112, columns <= 96
 }
