@@ -63,6 +63,10 @@ namespace {
 #ifndef CORR_ACC
 #define CORR_ACC 0
 #endif
+#ifndef CORR_CLAIM
+#define CORR_CLAIM 1
+#endif
+constexpr int kClaim = CORR_CLAIM;  // tiles per queue claim
 constexpr int kWarps = CORR_WARPS;  // A/B knobs (tools/build_variant.sh)
 constexpr int kThreads = 32 * kWarps;
 constexpr int kD = 128;
@@ -347,14 +351,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     // issue cursor (warp-uniform): pending tile + its record, current tile, chunk.
     // Tiles come from the global queue; lane 0 keeps one claim in flight so the
     // atomic's latency hides behind a whole tile.
+    // CORR_CLAIM consecutive tiles per atomic (A/B knob), the next claim kept in flight
     int pend = 0;
     int claim = 0;
-    if (lane == 0) claim = atomicAdd(a.ctl + 1, 1);
+    int cl_next = 0, cl_left = 0;  // warp-uniform: next tile of the current claim, tiles left in it
+    if (lane == 0) claim = atomicAdd(a.ctl + 1, kClaim);
     int4 pr0 = make_int4(0, 0, 0, 0), pr1 = make_int4(0, 0, 0, 0);
     auto grab = [&]() {
-        pend = __shfl_sync(0xffffffffu, claim, 0);
+        if (cl_left == 0) {
+            cl_next = __shfl_sync(0xffffffffu, claim, 0);
+            cl_left = kClaim;
+            if (cl_next < n_all && lane == 0) claim = atomicAdd(a.ctl + 1, kClaim);
+        }
+        pend = cl_next++;
+        --cl_left;
         if (pend < n_all) {
-            if (lane == 0) claim = atomicAdd(a.ctl + 1, 1);
             const int4* src = reinterpret_cast<const int4*>(a.meta) + 2 * (size_t)pend;
             pr0 = __ldcg(src);
             pr1 = __ldcg(src + 1);
