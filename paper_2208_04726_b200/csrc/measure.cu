@@ -573,7 +573,10 @@ __global__ void __launch_bounds__(256) gram25_kernel(const float* feat, int W, i
     }
 }
 
-constexpr int kMeasWarps = 8;  // 4 edges per block, a warp per (edge, level)
+#ifndef PVO_MEASURE_WARPS
+#define PVO_MEASURE_WARPS 8
+#endif
+constexpr int kMeasWarps = PVO_MEASURE_WARPS;  // kMeasWarps / 2 edges per block, a warp per (edge, level)
 
 struct alignas(16) MeasWarpSmem {
     float g[128];         // the level's centre-pixel descriptor
