@@ -760,12 +760,10 @@ __device__ __forceinline__ int slice_argmax(const double* v, double eps = -1.0, 
 // argmax of the slice S.v, the 6x6 window around it staged, then the hill climb
 // with f0 / f2 of each parabola step on the two half warps.
 __device__ __noinline__ void subpixel_peak_gram(MeasWarpSmem& S, const Level& L, int C, const double* gm, const G4& g4,
-                                   double bx, double by, int ox, int oy, double* px, double* py, bool* on_border,
-                                   double eps, int* tie, const unsigned* pad) {
+                                   double bx, double by, int ox, int oy, int bi, double* px, double* py, double eps,
+                                   int* tie) {
     const int lane = threadIdx.x & 31;
-    const int bi = slice_argmax(S.v, eps, tie, pad);
-    const int best_a = bi / kS, best_b = bi % kS;
-    *on_border = best_a == 0 || best_a == kS - 1 || best_b == 0 || best_b == kS - 1;
+    const int best_a = bi / kS, best_b = bi % kS;  // the slice argmax (measure_task)
     double dx = best_b - kR, dy = best_a - kR;
     if (!(fabs(bx) < 1e8 && fabs(by) < 1e8)) {  // every sample is zero padding: no parabola step moves
         *px = dx;
@@ -860,8 +858,15 @@ struct MeasRecord {
     double px, py, conf;
     int bits;  // border | flat << 1 | tie reasons << 2
 };
+// Two phases around the pair's mid barrier (id `bar_mid`, both warps reach it
+// unconditionally): (A) slice, argmax and border flag, and on level 0 the
+// flatness / sharpness scores; the pair exchanges {border, flat} through `xchg`
+// ([2] ints); (B) the hill climbs — skipped when their results are discarded:
+// a flat slice (flow_provider.cpp:236-240 returns before any subpixel peak) or
+// both argmaxes on the border (out of range, :266-270), as in the reference's
+// outputs (it evaluates and drops the out-of-range climbs).
 __device__ __forceinline__ MeasRecord measure_task(const MeasureParams& a, MeasWarpSmem& S, int e, int level,
-                                                   bool* valid_out, bool* behind_out) {
+                                                   bool* valid_out, bool* behind_out, int* xchg, int bar_mid) {
     const int lane = threadIdx.x & 31;
     const int C = a.channels;
     double cx, cy;
@@ -882,15 +887,21 @@ __device__ __forceinline__ MeasRecord measure_task(const MeasureParams& a, MeasW
     // this task's record: level 0 {flat, confidence, p0x, p0y, border0}, level 1 {p1x, p1y, border1}
     double r_conf = 0.01, r_px = 0, r_py = 0;
     int r_flat = 1, r_border = 0;
+    // phase-A results the climb needs (defined for valid edges)
+    Level L{nullptr, 0, 0};
+    const double* gm = nullptr;
+    G4 g;
+    double eps = 0.0, bx = 0.0, by = 0.0;
+    int ox = 0, oy = 0, bi = kR * kS + kR, tie = 0;
+    unsigned pad = 0;
+    bool span = false, border = false;
     if (valid) {
         const int slot = a.e_slot ? a.e_slot[e] : a.pose_slot[a.e_pose[e]];
-        const Level L = level ? Level{a.feat1 + (size_t)slot * a.h1 * a.w1 * C, a.w1, a.h1}
-                              : Level{a.feat0 + (size_t)slot * a.h0 * a.w0 * C, a.w0, a.h0};
-        const double* gm = level ? a.g25_1 + (size_t)slot * a.h1 * a.w1 * kGram25
-                                 : a.g25_0 + (size_t)slot * a.h0 * a.w0 * kGram25;
+        L = level ? Level{a.feat1 + (size_t)slot * a.h1 * a.w1 * C, a.w1, a.h1}
+                  : Level{a.feat0 + (size_t)slot * a.h0 * a.w0 * C, a.w0, a.h0};
+        gm = level ? a.g25_1 + (size_t)slot * a.h1 * a.w1 * kGram25 : a.g25_0 + (size_t)slot * a.h0 * a.w0 * kGram25;
         const float* gp = a.patch_feats + ((size_t)a.e_patch[e] * 2 * 9 + 9 * level + 4) * C;  // centre pixel
         __syncwarp();  // the previous task is done with S
-        G4 g;
 #pragma unroll
         for (int k = 0; k < kCh; ++k) {
             const int c = lane + 32 * k;
@@ -900,11 +911,13 @@ __device__ __forceinline__ MeasRecord measure_task(const MeasureParams& a, MeasW
         double gn2 = 0;
 #pragma unroll
         for (int k = 0; k < kCh; ++k) gn2 += (double)g.v[k] * g.v[k];
-        const double eps = kTieRel * sqrt(warp_sum(gn2));
+        eps = kTieRel * sqrt(warp_sum(gn2));
         const double sc = level ? kStride * kStride : kStride;
-        const double bx = cx / sc, by = cy / sc;
-        const bool span = fabs(bx) < 1e8 && fabs(by) < 1e8;  // else every tap is zero padding
-        const int ox = span ? (int)floor(bx) - kR : 0, oy = span ? (int)floor(by) - kR : 0;
+        bx = cx / sc;
+        by = cy / sc;
+        span = fabs(bx) < 1e8 && fabs(by) < 1e8;  // else every tap is zero padding
+        ox = span ? (int)floor(bx) - kR : 0;
+        oy = span ? (int)floor(by) - kR : 0;
         __syncwarp();
         if (span) {
             {  // slice window dots: cells lane and lane + 32, interleaved
@@ -930,7 +943,7 @@ __device__ __forceinline__ MeasRecord measure_task(const MeasureParams& a, MeasW
             __syncwarp();
         }
         // the 7x7 slice (correlate_at at base + (beta - 3, alpha - 3)), lane per sample
-        unsigned redo = 0, pad = 0;  // pad: padding-only samples (exact zeros, as in the reference)
+        unsigned redo = 0;  // pad: padding-only samples (exact zeros, as in the reference)
         for (int n = 0; n < 2; ++n) {
             const int i = lane + 32 * n;
             if (i >= kS * kS) break;
@@ -976,24 +989,25 @@ __device__ __forceinline__ MeasRecord measure_task(const MeasureParams& a, MeasW
             }
         }
         __syncwarp();
-        bool border = false;
-        int tie = 0;  // reasons (all-padding slices, !span, are decided exactly: no ties there)
+        // argmax (the reference's first maximum) and border flag; a near-tied argmax
+        // matters for level 1 (its peak and border) and, unless flat, for level 0
+        int targ = 0;
+        bi = slice_argmax(S.v, eps, &targ, &pad);
+        const int best_a = bi / kS, best_b = bi % kS;
+        border = best_a == 0 || best_a == kS - 1 || best_b == 0 || best_b == kS - 1;
         if (level == 1) {
             r_flat = 0;
-            subpixel_peak_gram(S, L, C, gm, g, bx, by, ox, oy, &r_px, &r_py, &border, eps, &tie, &pad);
+            tie = targ;
         } else {
             // level 0: flatness / sharpness scores on the slice (flow_provider.cpp:217-250),
             // as warp reductions (the mean as a fixed-order tree)
-            int targ = 0;  // (the argmax matters only when the slice is not flat)
-            const int pi = slice_argmax(S.v, eps, &targ, &pad);
-            const double peak = S.v[pi];
-            const int peak_a = pi / kS, peak_b = pi % kS;
+            const double peak = S.v[bi];
             double minimum = CUDART_INF, mean = 0, second = -CUDART_INF;
             for (int i = lane; i < kS * kS; i += 32) {
                 const double val = S.v[i];
                 mean += val;
                 minimum = fmin(minimum, val);
-                if (max(abs(i / kS - peak_a), abs(i % kS - peak_b)) > 1) second = fmax(second, val);
+                if (max(abs(i / kS - best_a), abs(i % kS - best_b)) > 1) second = fmax(second, val);
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
@@ -1011,11 +1025,21 @@ __device__ __forceinline__ MeasRecord measure_task(const MeasureParams& a, MeasW
                 tie |= targ;
                 const double score = 2.0 * (peak - 0.75) + (peak - second - 0.08);
                 r_conf = fmin(fmax(1.0 / (1.0 + exp(-12.0 * score)), 0.01), 0.99);
-                subpixel_peak_gram(S, L, C, gm, g, bx, by, ox, oy, &r_px, &r_py, &border, eps, &tie, &pad);
             }
         }
-        r_border = border | (span ? tie << 2 : 0);
     }
+    // ---- the pair exchanges {border, flat}; the climbs run only where they are used ----
+    if (lane == 0) xchg[level] = valid ? (int)border | (level == 0 ? r_flat << 1 : 0) : 3;
+    __syncwarp();
+    asm volatile("bar.sync %0, 64;" ::"r"(bar_mid) : "memory");
+    const int x0 = xchg[0], x1 = xchg[1];
+    const bool climb = valid && span && !((x0 >> 1) & 1) && !((x0 & 1) && (x1 & 1));
+    if (climb) subpixel_peak_gram(S, L, C, gm, g, bx, by, ox, oy, bi, &r_px, &r_py, eps, &tie);
+    else if (valid) {  // no climb: the discrete peak (the reference's starting point)
+        r_px = bi % kS - kR;
+        r_py = bi / kS - kR;
+    }
+    if (valid) r_border = border | (span ? tie << 2 : 0);
     *valid_out = valid;
     *behind_out = behind;
     return MeasRecord{r_px, r_py, r_conf, r_border | (r_flat << 1)};
@@ -1087,8 +1111,9 @@ __global__ void __launch_bounds__(32 * kMeasWarps, PVO_MEASURE_GRAM_MINB) measur
     const int e = blockIdx.x * (kMeasWarps / 2) + pair;
     if (e >= a.n_edges) return;  // both warps of the pair
     MeasWarpSmem& S = reinterpret_cast<MeasWarpSmem*>(s_meas)[warp];
+    __shared__ int s_x[kMeasWarps / 2][2];
     bool valid, behind;
-    const MeasRecord r = measure_task(a, S, e, level, &valid, &behind);
+    const MeasRecord r = measure_task(a, S, e, level, &valid, &behind, s_x[pair], 1 + kMeasWarps / 2 + pair);
     if (level == 1 && lane == 0) s_rec1[pair] = r;
     __syncwarp();
     asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
