@@ -593,6 +593,10 @@ struct alignas(16) MeasWarpSmem {
 };
 constexpr int kMeasSmem = kMeasWarps * (int)sizeof(MeasWarpSmem);
 
+#ifndef PVO_CELL_DOT_UNROLL
+#define PVO_CELL_DOT_UNROLL 4
+#endif
+constexpr int kCellDotUnroll = PVO_CELL_DOT_UNROLL;  // channel quads per batch of loads in flight (A/B knob)
 // <g, f_cell> (g in shared memory): FP64 sums of exact products (explicit FMAs:
 // the product of two FP32 values is exact in FP64, so an FMA rounds like the
 // separate add), four interleaved partial sums (short dependent chains)
@@ -601,7 +605,7 @@ __device__ __noinline__ double cell_dot(const float* gs, const float* fc, int C)
     if ((C & 3) == 0) {
         const float4* f4 = reinterpret_cast<const float4*>(fc);
         const float4* g4 = reinterpret_cast<const float4*>(gs);
-#pragma unroll 4
+#pragma unroll(kCellDotUnroll)
         for (int q = 0; q < (C >> 2); ++q) {
             const float4 fv = __ldg(f4 + q), gv = g4[q];
             s0 = __fma_rn((double)gv.x, (double)fv.x, s0);
@@ -623,7 +627,7 @@ __device__ __noinline__ void cell_dot2(const float* gs, const float* fa, const f
         const float4* fa4 = reinterpret_cast<const float4*>(fa);
         const float4* fb4 = reinterpret_cast<const float4*>(fb);
         const float4* g4 = reinterpret_cast<const float4*>(gs);
-#pragma unroll 4
+#pragma unroll(kCellDotUnroll)
         for (int q = 0; q < (C >> 2); ++q) {
             const float4 va = __ldg(fa4 + q), vb = __ldg(fb4 + q), gv = g4[q];
             a0 = __fma_rn((double)gv.x, (double)va.x, a0);
