@@ -83,9 +83,14 @@ with torch.cuda.stream(stream):
 print(f"{cfg}{' (images, 25-d device features)' if images else ''}: {F} frames, {M} patches/frame, "
       f"window {w.cfg['window']}, radius {w.cfg['radius']}; "
       f"active edges at the end {edges[-1]}")
-tot = 0.0
+# mean and median per stage: graph admission and flatten read small counts back
+# (new edge count to size the next pass, window sizes), so their event-timed
+# stages include host scheduling latency, which a shared host makes spiky
+tot, totm = 0.0, 0.0
 for s in stages:
-    m = float(np.mean(acc[s]))
+    m, md = float(np.mean(acc[s])), float(np.median(acc[s]))
     tot += m
-    print(f"  {s:22s} {m:8.3f} ms")
-print(f"  {'device total':22s} {tot:8.3f} ms   host wall per frame {1e3 * np.mean(walls[F // 2:]):.3f} ms")
+    totm += md
+    print(f"  {s:22s} {m:8.3f} ms   (median {md:.3f}, max {float(np.max(acc[s])):.3f})")
+print(f"  {'device total':22s} {tot:8.3f} ms   (median {totm:.3f})   host wall per frame "
+      f"{1e3 * np.mean(walls[F // 2:]):.3f} ms")
