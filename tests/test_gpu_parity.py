@@ -542,6 +542,32 @@ def test_batch_with_a_large_window(ctx):
         assert np.array_equal(p1, p2) and np.array_equal(d1, d2) and np.array_equal(n1, n2)
 
 
+def test_batch_of_only_large_windows(ctx):
+    """A batch whose every window is beyond 16 free poses: no batched-kernel launch,
+    each window on the large-window BA; results equal the single-window large path."""
+    ws = [synth.generate("c1", seed=s, frames=22, patches=8) for s in (41, 42)]
+    _, H0, W0, D = ws[0].level0.shape
+    _, H1, W1, _ = ws[0].level1.shape
+    ctx.frames_reserve(44, W0, H0, W1, H1, D)
+    probs, slots = [], []
+    for i, w in enumerate(ws):
+        for f in range(22):
+            ctx.frames_upload(22 * i + f, w.level0[f], w.level1[f])
+        prob = synth.window_arrays(w, synth.build_graph(w, pvo.PatchGraph).window_problem(20))
+        probs.append(prob)
+        slots.append(prob["pose_frames"] + 22 * i)
+    bat = pvo.Batch(ctx)
+    bat.load(probs, slots, [p["patch_feats"] for p in probs], ws[0].K, ws[0].image)
+    bat.iteration(2)
+    res = bat.read()
+    for i, (w, prob) in enumerate(zip(ws, probs)):
+        win = pvo.Window(ctx)
+        win.load(prob, slots[i], prob["patch_feats"], w.K, w.image)
+        win.iteration(2)
+        p1, d1, n1 = win.read()
+        assert np.array_equal(res[i][0], p1) and np.array_equal(res[i][1], d1) and np.array_equal(res[i][2], n1)
+
+
 def _measure_report(name, d, w, fl, rd, rw, rfl):
     dd = np.abs(d - rd).max(1)
     dw = np.abs(w - rw).max(1)
