@@ -553,10 +553,24 @@ __global__ void __launch_bounds__(256) gram25_kernel(const float* feat, int W, i
     extern __shared__ float s_f[];  // [kG25SH * kG25SW][C + 1] (odd stride: conflict-free per cell)
     const int tx0 = blockIdx.x * kG25TileW, ty0 = blockIdx.y * kG25TileH;
     const int stride = C + 1;
-    for (int t = threadIdx.x; t < kG25SW * kG25SH * C; t += blockDim.x) {
-        const int cell = t / C, c = t - cell * C;
-        const int x = tx0 - 3 + cell % kG25SW, y = ty0 + cell / kG25SW;
-        s_f[cell * stride + c] = (x >= 0 && y >= 0 && x < W && y < H) ? feat[((size_t)y * W + x) * C + c] : 0.f;
+    // staged in batches: every thread's loads of a batch are in flight before its stores
+    constexpr int kStageBatch = 8;
+    const int total = kG25SW * kG25SH * C;
+    for (int t0 = threadIdx.x; t0 < total; t0 += kStageBatch * blockDim.x) {
+        float r[kStageBatch];
+#pragma unroll
+        for (int b = 0; b < kStageBatch; ++b) {
+            const int t = t0 + b * blockDim.x;
+            const int cell = t / C, c = t - cell * C;
+            const int x = tx0 - 3 + cell % kG25SW, y = ty0 + cell / kG25SW;
+            r[b] = (t < total && x >= 0 && y >= 0 && x < W && y < H) ? __ldg(feat + ((size_t)y * W + x) * C + c) : 0.f;
+        }
+#pragma unroll
+        for (int b = 0; b < kStageBatch; ++b) {
+            const int t = t0 + b * blockDim.x;
+            const int cell = t / C, c = t - cell * C;
+            if (t < total) s_f[cell * stride + c] = r[b];
+        }
     }
     __syncthreads();
     for (int t = threadIdx.x; t < kG25TileW * kG25TileH * kGram25; t += blockDim.x) {
@@ -567,9 +581,18 @@ __global__ void __launch_bounds__(256) gram25_kernel(const float* feat, int W, i
         const int dy = m < 4 ? 0 : 1 + (m - 4) / 7, dx = m < 4 ? m : (m - 4) % 7 - 3;
         const float* fa = s_f + (ly * kG25SW + lx + 3) * stride;
         const float* fb = s_f + ((ly + dy) * kG25SW + lx + 3 + dx) * stride;  // zero outside the grid
-        double sum = 0;
-        for (int c = 0; c < C; ++c) sum += (double)fa[c] * (double)fb[c];
-        g25[((size_t)y * W + x) * kGram25 + m] = sum;
+        // FP64 sums of exact products (an FP32 x FP32 product is exact in FP64, so the
+        // FMA rounds like the separate add), four interleaved chains
+        double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+        int c = 0;
+        for (; c + 4 <= C; c += 4) {
+            s0 = __fma_rn((double)fa[c], (double)fb[c], s0);
+            s1 = __fma_rn((double)fa[c + 1], (double)fb[c + 1], s1);
+            s2 = __fma_rn((double)fa[c + 2], (double)fb[c + 2], s2);
+            s3 = __fma_rn((double)fa[c + 3], (double)fb[c + 3], s3);
+        }
+        for (; c < C; ++c) s0 = __fma_rn((double)fa[c], (double)fb[c], s0);
+        g25[((size_t)y * W + x) * kGram25 + m] = (s0 + s1) + (s2 + s3);
     }
 }
 
