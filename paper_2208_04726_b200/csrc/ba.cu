@@ -646,16 +646,36 @@ __device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Lay
                 bs[c] = warp_sum(bs[c]);
             }
             __syncwarp();
-            // per-edge target blocks (disjoint unless a target repeats: serialise)
-            for (int l = 0; l < ne; ++l) {
-                const int sjl = __shfl_sync(0xffffffffu, sj, l);
-                if (sjl >= 0 && lane < 6) {
-                    const double* R = rec + l * kRec;
-                    const double g0 = R[kJt + lane] * R[kW], g1 = R[kJt + 6 + lane] * R[kW + 1];
-                    v[6 * sjl + lane] += g0 * R[kJd] + g1 * R[kJd + 1];
-                    bvec[6 * sjl + lane] += -(g0 * R[kR] + g1 * R[kR + 1]);
+            // per-edge target blocks: with distinct targets (one edge per (patch, frame):
+            // every window problem) each lane adds its own edge's block at once; a
+            // repeated target (possible in a flat problem) serialises in edge order
+            const bool has_t = sj >= 0;
+            const unsigned same = __match_any_sync(0xffffffffu, sj);  // every lane (no short-circuit)
+            const unsigned with_t = __ballot_sync(0xffffffffu, has_t);
+            const bool dup = has_t && __popc(same & with_t) > 1;
+            const bool distinct = !__any_sync(0xffffffffu, dup);
+            if (distinct) {
+                if (has_t) {
+                    const double* R = rec + lane * kRec;
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) {
+                        const double g0 = R[kJt + c] * R[kW], g1 = R[kJt + 6 + c] * R[kW + 1];
+                        v[6 * sj + c] += g0 * R[kJd] + g1 * R[kJd + 1];
+                        bvec[6 * sj + c] += -(g0 * R[kR] + g1 * R[kR + 1]);
+                    }
                 }
                 __syncwarp();
+            } else {
+                for (int l = 0; l < ne; ++l) {
+                    const int sjl = __shfl_sync(0xffffffffu, sj, l);
+                    if (sjl >= 0 && lane < 6) {
+                        const double* R = rec + l * kRec;
+                        const double g0 = R[kJt + lane] * R[kW], g1 = R[kJt + 6 + lane] * R[kW + 1];
+                        v[6 * sjl + lane] += g0 * R[kJd] + g1 * R[kJd + 1];
+                        bvec[6 * sjl + lane] += -(g0 * R[kR] + g1 * R[kR + 1]);
+                    }
+                    __syncwarp();
+                }
             }
             if (si >= 0 && lane < 6) {
                 v[6 * si + lane] += vs[lane];
@@ -667,22 +687,30 @@ __device__ void phase_assemble(const BAParams& a, unsigned char* smem, const Lay
             int* nxt = wi + 4 + kMaxFree;
             for (int i = lane; i < kMaxFree; i += 32) p2e[i] = -1;
             __syncwarp();
-            for (int l = ne - 1; l >= 0; --l) {
-                const int sjl = __shfl_sync(0xffffffffu, sj, l);
-                if (lane == 0) {
-                    nxt[l] = -1;
-                    if (sjl >= 0) {
-                        nxt[l] = p2e[sjl];
-                        p2e[sjl] = l;
+            if (distinct) {  // one-edge chains: every lane sets its own
+                if (lane < ne) nxt[lane] = -1;
+                if (has_t) p2e[sj] = lane;
+            } else {
+                for (int l = ne - 1; l >= 0; --l) {
+                    const int sjl = __shfl_sync(0xffffffffu, sj, l);
+                    if (lane == 0) {
+                        nxt[l] = -1;
+                        if (sjl >= 0) {
+                            nxt[l] = p2e[sjl];
+                            p2e[sjl] = l;
+                        }
                     }
                 }
             }
+            __syncwarp();
+            {  // the free target poses with an edge chain, ascending (a ballot compaction)
+                int* tl = nxt + kMaxEdges;
+                const bool used = lane < kMaxFree && p2e[lane < kMaxFree ? lane : 0] >= 0;
+                const unsigned um = __ballot_sync(0xffffffffu, used);
+                if (used) tl[__popc(um & ((1u << lane) - 1))] = lane;
+                if (lane == 0) tl[kMaxFree] = __popc(um);
+            }
             if (lane == 0) {
-                int* tl = nxt + kMaxEdges;  // the free target poses with an edge chain
-                int ntl = 0;
-                for (int t = 0; t < kMaxFree; ++t)
-                    if (p2e[t] >= 0) tl[ntl++] = t;
-                tl[kMaxFree] = ntl;
                 wi[0] = si;
                 wi[1] = ne;
                 wi[2] = dslot;
