@@ -9,7 +9,7 @@ int pvo_batch_load(pvo_ctx* ctx, int n_windows, const int* pose_off, const int* 
                    const double* px, const double* py, const double* depth, const float* patch_feats,
                    const int* e_patch, const int* e_pose, const double* e_delta, const double* e_weight,
                    const double* K, int image_w, int image_h) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (ctx->nf == 0) fail(PVO_INVALID_ARGUMENT, "batch_load: frame store is empty (pvo_frames_reserve)");
         if (n_windows < 1) fail(PVO_INVALID_ARGUMENT, "batch_load: no windows");
@@ -203,7 +203,7 @@ void batch_params(pvo_ctx* ctx, int iterations, double damping) {
 }  // namespace
 
 int pvo_batch_reset(pvo_ctx* ctx) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         Batch& B = ctx->bat;
         if (!B.loaded) fail(PVO_INVALID_ARGUMENT, "batch: nothing loaded");
@@ -215,7 +215,7 @@ int pvo_batch_reset(pvo_ctx* ctx) {
 }
 
 int pvo_batch_iteration(pvo_ctx* ctx, int iterations, double damping, float* corr_out, int corr_memspace) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         Batch& B = ctx->bat;
         if (!B.loaded) fail(PVO_INVALID_ARGUMENT, "batch: nothing loaded");
@@ -247,6 +247,7 @@ int pvo_batch_iteration(pvo_ctx* ctx, int iterations, double damping, float* cor
         run_corr(ctx, cp);
         record_timing(ctx, 1);
         if (B.n_small > 0) {
+            NvtxRange range("ba_batch");
             cuda_check(pvo_dev::launch_ba_batch(static_cast<const pvo_dev::BAParams*>(B.params.p), B.n_small,
                                                 B.max_free, B.max_poses, ctx->stream),
                        "ba batch kernel");
@@ -269,7 +270,7 @@ int pvo_batch_iteration(pvo_ctx* ctx, int iterations, double damping, float* cor
 }
 
 int pvo_batch_read(pvo_ctx* ctx, double* poses, double* inv_depth, double* residual_norms, int* n_norms) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         Batch& B = ctx->bat;
         if (!B.loaded) fail(PVO_INVALID_ARGUMENT, "batch: nothing loaded");

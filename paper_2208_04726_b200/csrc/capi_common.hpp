@@ -451,6 +451,7 @@ inline pvo_dev::BALargeParams large_params(pvo_ctx* ctx, const pvo_dev::BAParams
 
 // bufs: the large path's group arrays / scratch (default: the resident window's)
 inline void launch_ba_checked(pvo_ctx* ctx, pvo_dev::BAParams& a, const Plan& pl, BABuffers* bufs = nullptr) {
+    NvtxRange range(pl.large ? "ba_large" : "ba");
     cuda_check(cudaMemsetAsync(a.n_norms, 0, sizeof(int), ctx->stream), "memset");
     if (pl.large) {
         if (a.gn_step_mode) fail(PVO_UNSUPPORTED, "gauss_newton_step: pose systems beyond 16 free poses");
@@ -604,6 +605,7 @@ inline bool encode_patch_map(pvo_ctx* ctx, const float* base, int n_patches) {
 // for other channel counts.  `t` carries the inputs; scratch is filled in here.
 inline void run_corr(pvo_ctx* ctx, pvo_dev::CorrTmaParams t, int index_edges = 0) {
     if (t.n_edges <= 0) return;
+    NvtxRange range("corr");
     if (ctx->maps_ok && encode_patch_map(ctx, t.patch_feats, t.n_patches)) {
         t.w0 = ctx->w0;
         t.h0 = ctx->h0;

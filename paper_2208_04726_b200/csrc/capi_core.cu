@@ -114,7 +114,7 @@ const char* pvo_status_string(int status) {
 }
 
 int pvo_ctx_create(int device, pvo_ctx** out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!out) fail(PVO_INVALID_ARGUMENT, "null output");
         *out = nullptr;
         int n = 0;
@@ -144,7 +144,7 @@ int pvo_ctx_create(int device, pvo_ctx** out) {
 }
 
 int pvo_ctx_destroy(pvo_ctx* ctx) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
@@ -175,7 +175,7 @@ int pvo_ctx_destroy(pvo_ctx* ctx) {
 }
 
 int pvo_ctx_set_stream(pvo_ctx* ctx, void* stream) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (ctx->own_stream) {
             cudaStreamSynchronize(ctx->stream);
@@ -192,7 +192,7 @@ int pvo_ctx_set_stream(pvo_ctx* ctx, void* stream) {
 }
 
 int pvo_ctx_synchronize(pvo_ctx* ctx) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         sync(ctx);
     });
@@ -201,7 +201,7 @@ int pvo_ctx_synchronize(pvo_ctx* ctx) {
 int64_t pvo_ctx_kernel_launches(pvo_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
 int pvo_ctx_set_timing(pvo_ctx* ctx, int on) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         ctx->timing = on != 0;
         if (!ctx->timing) ctx->timing_pending = false;
@@ -209,7 +209,7 @@ int pvo_ctx_set_timing(pvo_ctx* ctx, int on) {
 }
 
 int pvo_ctx_set_tracing(pvo_ctx* ctx, int on) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         ctx->tracing = on != 0;
         if (ctx->tracing) {
@@ -220,7 +220,7 @@ int pvo_ctx_set_tracing(pvo_ctx* ctx, int on) {
 }
 
 int pvo_ctx_ba_phase_cycles(pvo_ctx* ctx, long long* out128) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (!ctx->tracing) fail(PVO_INVALID_ARGUMENT, "tracing is off (pvo_ctx_set_tracing)");
         download(ctx, out128, static_cast<const long long*>(ctx->ba.clocks.p), 128);
@@ -229,7 +229,7 @@ int pvo_ctx_ba_phase_cycles(pvo_ctx* ctx, long long* out128) {
 }
 
 int pvo_ctx_ba_attempts(pvo_ctx* ctx, int* attempts) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         *attempts = 0;
         if (ctx->ba.attempts.p) {
@@ -240,7 +240,7 @@ int pvo_ctx_ba_attempts(pvo_ctx* ctx, int* attempts) {
 }
 
 int pvo_ctx_last_timing(pvo_ctx* ctx, double* corr_ms, double* ba_ms) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (!ctx->timing_pending) fail(PVO_INVALID_ARGUMENT, "no timed iteration recorded");
         cuda_check(cudaEventSynchronize(ctx->ev[2]), "cudaEventSynchronize");
@@ -254,27 +254,27 @@ int pvo_ctx_last_timing(pvo_ctx* ctx, double* corr_ms, double* ba_ms) {
 
 // ---- SE(3) host utilities ------------------------------------------------
 int pvo_se3_exp(const double* xi, double* out) {
-    return guarded([&] { pvo_dev::se3_store(pvo_dev::se3_exp(xi), out); });
+    return guarded(__func__, [&] { pvo_dev::se3_store(pvo_dev::se3_exp(xi), out); });
 }
 int pvo_se3_log(const double* pose, double* xi) {
-    return guarded([&] { se3_log_host(pose, xi); });
+    return guarded(__func__, [&] { se3_log_host(pose, xi); });
 }
 int pvo_se3_compose(const double* a, const double* b, double* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         pvo_dev::se3_store(pvo_dev::se3_compose(pvo_dev::se3_load(a), pvo_dev::se3_load(b)), out);
     });
 }
 int pvo_se3_inverse(const double* a, double* out) {
-    return guarded([&] { pvo_dev::se3_store(pvo_dev::se3_inverse(pvo_dev::se3_load(a)), out); });
+    return guarded(__func__, [&] { pvo_dev::se3_store(pvo_dev::se3_inverse(pvo_dev::se3_load(a)), out); });
 }
 int pvo_se3_retract(const double* a, const double* xi, double* out) {
-    return guarded([&] { pvo_dev::se3_store(pvo_dev::se3_retract(pvo_dev::se3_load(a), xi), out); });
+    return guarded(__func__, [&] { pvo_dev::se3_store(pvo_dev::se3_retract(pvo_dev::se3_load(a), xi), out); });
 }
 
 // ---- camera ----------------------------------------------------------------
 int pvo_reproject_patches(pvo_ctx* ctx, int n, int p, const double* pi, const double* pj, const double* K,
                           const double* x, const double* y, const double* d, double* out_xy, uint8_t* behind) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (n < 0 || p < 1) fail(PVO_INVALID_ARGUMENT, "reproject: bad sizes");
         if (n == 0) return;
@@ -297,7 +297,7 @@ int pvo_reproject_patches(pvo_ctx* ctx, int n, int p, const double* pi, const do
 
 int pvo_reprojection_jacobians(pvo_ctx* ctx, int n, int p, const double* pi, const double* pj, const double* K,
                                const double* x, const double* y, const double* d, double* out, uint8_t* behind) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (n < 0 || p < 1) fail(PVO_INVALID_ARGUMENT, "jacobians: bad sizes");
         if (n == 0) return;
@@ -321,7 +321,7 @@ int pvo_reprojection_jacobians(pvo_ctx* ctx, int n, int p, const double* pi, con
 // ---- correlation -------------------------------------------------------------
 int pvo_correlate(pvo_ctx* ctx, int p, int C, const float* feats0, const float* feats1, const float* level0, int w0,
                   int h0, const float* level1, int w1, int h1, const double* coords, float* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (p < 1 || C < 1 || w0 < 0 || h0 < 0 || w1 < 0 || h1 < 0) fail(PVO_INVALID_ARGUMENT, "correlate: bad sizes");
         const int pp = p * p;
@@ -376,7 +376,7 @@ int pvo_correlate(pvo_ctx* ctx, int p, int C, const float* feats0, const float* 
 
 int pvo_correlate_points(pvo_ctx* ctx, int n, int C, const float* features, const float* grid, int w, int h,
                          const double* xy, int cubic, double* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (n < 0 || C < 1 || w < 0 || h < 0) fail(PVO_INVALID_ARGUMENT, "correlate_at: bad sizes");
         if (n == 0) return;
@@ -399,7 +399,7 @@ int pvo_correlate_points(pvo_ctx* ctx, int n, int C, const float* features, cons
 }
 
 int pvo_grid_cache_stats(pvo_ctx* ctx, int64_t* hits, int64_t* misses, int* entries, int64_t* bytes) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!ctx) fail(PVO_INVALID_ARGUMENT, "null context");
         if (hits) *hits = ctx->grid_hits;
         if (misses) *misses = ctx->grid_misses;
@@ -409,7 +409,7 @@ int pvo_grid_cache_stats(pvo_ctx* ctx, int64_t* hits, int64_t* misses, int* entr
 }
 
 int pvo_grid_cache_clear(pvo_ctx* ctx) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         sync(ctx);
         grid_cache_clear(ctx);
@@ -417,7 +417,7 @@ int pvo_grid_cache_clear(pvo_ctx* ctx) {
 }
 
 int pvo_frames_reserve(pvo_ctx* ctx, int n_frames, int w0, int h0, int w1, int h1, int C) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (n_frames < 1 || w0 < 1 || h0 < 1 || w1 < 0 || h1 < 0 || C < 1) fail(PVO_INVALID_ARGUMENT, "frames: bad sizes");
         ctx->nf = n_frames;
@@ -441,7 +441,7 @@ int pvo_frames_reserve(pvo_ctx* ctx, int n_frames, int w0, int h0, int w1, int h
 }
 
 int pvo_frames_refresh(pvo_ctx* ctx, int slot) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (slot < 0 || slot >= ctx->nf) fail(PVO_OUT_OF_RANGE, "frames: slot out of range");
         const size_t c0 = (size_t)ctx->w0 * ctx->h0, c1 = (size_t)ctx->w1 * ctx->h1;
@@ -455,7 +455,7 @@ int pvo_frames_refresh(pvo_ctx* ctx, int slot) {
 }
 
 int pvo_frames_upload(pvo_ctx* ctx, int slot, const float* level0, const float* level1, int memspace) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (slot < 0 || slot >= ctx->nf) fail(PVO_OUT_OF_RANGE, "frames: slot out of range");
         const size_t c0 = (size_t)ctx->w0 * ctx->h0, c1 = (size_t)ctx->w1 * ctx->h1;
@@ -473,7 +473,7 @@ int pvo_frames_upload(pvo_ctx* ctx, int slot, const float* level0, const float* 
 }
 
 int pvo_frames_device_ptrs(pvo_ctx* ctx, float** level0, float** level1) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (level0) *level0 = static_cast<float*>(ctx->feat0.p);
         if (level1) *level1 = static_cast<float*>(ctx->feat1.p);
@@ -482,7 +482,7 @@ int pvo_frames_device_ptrs(pvo_ctx* ctx, float** level0, float** level1) {
 
 int pvo_correlate_batch(pvo_ctx* ctx, int n_edges, int n_patches, int p, const int* e_patch, const int* e_slot,
                         const double* coords, const float* patch_feats, float* out, int memspace) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         ensure_p3(p);
         if (ctx->nf == 0) fail(PVO_INVALID_ARGUMENT, "correlate_batch: frame store is empty (pvo_frames_reserve)");
@@ -542,7 +542,7 @@ int pvo_gauss_newton_step(pvo_ctx* ctx, int n_poses, const double* poses, const 
                           const double* e_target, const double* e_weight, const double* K, double damping,
                           double* out_poses, double* out_depth, double* residual_norms, double* debug_h,
                           double* debug_b, int* n_free_poses, int* n_free_depths) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         HostProblem pr{n_poses, poses, fixed, n_patches, p, src, px, py, depth, depth_free, n_edges,
                        e_patch, e_pose, e_target, e_weight};
         std::memcpy(pr.K, K, sizeof(pr.K));
@@ -563,7 +563,7 @@ int pvo_gauss_newton_step(pvo_ctx* ctx, int n_poses, const double* poses, const 
 
 int pvo_schur_solve(pvo_ctx* ctx, int np, int nd, const double* hpp, const double* hpd, const double* hdd,
                     const double* bp, const double* bd, double* dp, double* dd) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (np < 0 || nd < 0) fail(PVO_INVALID_ARGUMENT, "schur: bad sizes");
         for (int k = 0; k < nd; ++k)
@@ -593,7 +593,7 @@ int pvo_ba_window(pvo_ctx* ctx, int n_poses, const double* poses, const uint8_t*
                   const int* e_patch, const int* e_pose, const double* e_target, const double* e_weight,
                   const double* K, int image_w, int image_h, int freeze_targets, double damping, int iterations,
                   int structure_only, double* out_poses, double* out_depth, double* residual_norms, int* n_norms) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (iterations < 0 || structure_only < 0) fail(PVO_INVALID_ARGUMENT, "ba: negative iteration count");
         HostProblem pr{n_poses, poses, fixed, n_patches, p, src, px, py, depth, nullptr, n_edges,
                        e_patch, e_pose, e_target, e_weight};

@@ -89,7 +89,7 @@ struct pvo_dgraph {
 extern "C" {
 
 int pvo_dgraph_create(pvo_ctx* ctx, const double* K, int w, int h, int p, int channels, pvo_dgraph** out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (!out) fail(PVO_INVALID_ARGUMENT, "null output");
         ensure_p3(p);
@@ -128,7 +128,7 @@ void dg_upload_frames(pvo_dgraph* g, const std::vector<double>* poses_host) {
 
 // patch_graph.cpp:27-34 (+ the frame-store slot holding the frame's pyramid)
 int pvo_dgraph_add_frame(pvo_dgraph* g, double ts, const double* pose, int frame_slot, int* out_index) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         pvo_ctx* ctx = g->ctx;
         bind(ctx);
         if (!g->f_ts.empty() && ts <= g->f_ts.back()) {
@@ -161,7 +161,7 @@ int pvo_dgraph_add_frame(pvo_dgraph* g, double ts, const double* pose, int frame
 // patch_graph.cpp:36-60 + Patch::make (camera.cpp:15-32); feats [n][2][9][C] or NULL
 int pvo_dgraph_add_patches(pvo_dgraph* g, int frame, int n, const double* centroids, const double* depths,
                            const float* feats, int* out_ids) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         pvo_ctx* ctx = g->ctx;
         bind(ctx);
         g->position(frame);
@@ -212,7 +212,7 @@ int pvo_dgraph_add_patches(pvo_dgraph* g, int frame, int n, const double* centro
 
 // patch_graph.cpp:62-85
 int pvo_dgraph_connect(pvo_dgraph* g, int radius, int* n_added) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         pvo_ctx* ctx = g->ctx;
         bind(ctx);
         if (radius < 1) fail(PVO_INVALID_ARGUMENT, "patch graph: radius must be >= 1");
@@ -253,7 +253,7 @@ int pvo_dgraph_connect(pvo_dgraph* g, int radius, int* n_added) {
 
 // patch_graph.cpp:87-128
 int pvo_dgraph_remove_frame(pvo_dgraph* g, int frame) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         pvo_ctx* ctx = g->ctx;
         bind(ctx);
         const int pos = g->position(frame);
@@ -324,7 +324,7 @@ int pvo_dgraph_remove_frame(pvo_dgraph* g, int frame) {
 // patch_graph.cpp:153-164 for n keys (host arrays)
 int pvo_dgraph_set_revisions(pvo_dgraph* g, int n, const int* patch_ids, const int* frames, const double* deltas,
                              const double* weights) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         pvo_ctx* ctx = g->ctx;
         bind(ctx);
         if (n <= 0) return;
@@ -356,7 +356,7 @@ int pvo_dgraph_set_revisions(pvo_dgraph* g, int n, const int* patch_ids, const i
 }
 
 int pvo_dgraph_counts(pvo_dgraph* g, int* n_frames, int* n_patches, int* n_edges) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (n_frames) *n_frames = static_cast<int>(g->f_index.size());
         if (n_patches) *n_patches = g->P;
         if (n_edges) *n_edges = g->E;
@@ -365,7 +365,7 @@ int pvo_dgraph_counts(pvo_dgraph* g, int* n_frames, int* n_patches, int* n_edges
 
 // edges in key order (kk = patch id, jj = frame), rev [E][4], has_rev [E] (host copies)
 int pvo_dgraph_edges(pvo_dgraph* g, int* kk, int* jj, double* rev, uint8_t* has_rev) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         pvo_ctx* ctx = g->ctx;
         bind(ctx);
         const int b = g->cur, P = g->P, E = g->E;
@@ -383,7 +383,7 @@ int pvo_dgraph_edges(pvo_dgraph* g, int* kk, int* jj, double* rev, uint8_t* has_
 }
 
 int pvo_dgraph_frames(pvo_dgraph* g, int* indices, double* poses) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(g->ctx);
         const size_t F = g->f_index.size();
         if (indices) std::copy(g->f_index.begin(), g->f_index.end(), indices);
@@ -395,7 +395,7 @@ int pvo_dgraph_frames(pvo_dgraph* g, int* indices, double* poses) {
 }
 
 int pvo_dgraph_patches(pvo_dgraph* g, int* ids, int* src, double* inv_depth) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         pvo_ctx* ctx = g->ctx;
         bind(ctx);
         const int b = g->cur;
@@ -411,7 +411,7 @@ int pvo_dgraph_patches(pvo_dgraph* g, int* ids, int* src, double* inv_depth) {
 // seen in both; below threshold_px the candidate t-4 is removed.  removed =
 // the removed frame index or -1; mean_flow / n_used report the statistic.
 int pvo_dgraph_keyframe(pvo_dgraph* g, double threshold_px, int* removed, double* mean_flow, int* n_used) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         pvo_ctx* ctx = g->ctx;
         bind(ctx);
         if (removed) *removed = -1;
@@ -449,7 +449,7 @@ int pvo_dgraph_keyframe(pvo_dgraph* g, double threshold_px, int* removed, double
 // plan is built on the host from the device-flattened structure: one read-back).
 int pvo_window_load_dgraph(pvo_ctx* ctx, pvo_dgraph* g, int window, int all_active, int* n_poses, int* n_patches,
                            int* n_edges) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (g->ctx != ctx) fail(PVO_INVALID_ARGUMENT, "window_load_dgraph: the graph belongs to another context");
         if (window < 1) fail(PVO_INVALID_ARGUMENT, "ba: window must be >= 1");
@@ -591,7 +591,7 @@ int pvo_window_load_dgraph(pvo_ctx* ctx, pvo_dgraph* g, int window, int all_acti
 // graph's edges (has_rev set), and its BA state (free poses, every included
 // depth) back into the graph (bundle_adjust.cpp:368-373).
 int pvo_dgraph_store_window(pvo_ctx* ctx, pvo_dgraph* g, int revisions, int state) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (!g->window_from_graph || !ctx->win.loaded) fail(PVO_INVALID_ARGUMENT, "dgraph: no window loaded from this graph");
         pvo_dev::DGraphView v = g->view(g->cur);

@@ -9,7 +9,7 @@ extern "C" {
 // (+ its Gram terms).  The store must have been reserved with C = 25 * bc and
 // level sizes (iw/4, ih/4), (iw/16, ih/16).
 int pvo_frames_extract(pvo_ctx* ctx, int slot, const float* image, int iw, int ih, int base_channels, int memspace) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (base_channels != 1 && base_channels != 3) fail(PVO_INVALID_ARGUMENT, "features: base channel count must be 1 or 3");
         if (iw < 12 || ih < 12) fail(PVO_INVALID_ARGUMENT, "features: image too small");
@@ -35,7 +35,7 @@ int pvo_frames_extract(pvo_ctx* ctx, int slot, const float* image, int iw, int i
 
 // A slot's pyramid back to the host (level0 [H0][W0][C], level1 [H1][W1][C]).
 int pvo_frames_download(pvo_ctx* ctx, int slot, float* level0, float* level1) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (slot < 0 || slot >= ctx->nf) fail(PVO_OUT_OF_RANGE, "frames: slot out of range");
         const size_t c0 = (size_t)ctx->w0 * ctx->h0 * ctx->C, c1 = (size_t)ctx->w1 * ctx->h1 * ctx->C;
@@ -48,7 +48,7 @@ int pvo_frames_download(pvo_ctx* ctx, int slot, float* level0, float* level1) {
 // crop_patch_features (features.cpp:204-224) of n patches from frame-store slot
 // `slot`: centroids [n][2] -> the 3x3 grid (Patch::make) -> out [n][2][9][C].
 int pvo_crop_patches(pvo_ctx* ctx, int slot, int n, const double* centroids, float* out, int memspace) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (slot < 0 || slot >= ctx->nf) fail(PVO_OUT_OF_RANGE, "frames: slot out of range");
         if (n <= 0) return;
@@ -79,7 +79,7 @@ int pvo_crop_patches(pvo_ctx* ctx, int slot, int n, const double* centroids, flo
 int pvo_measure_batch(pvo_ctx* ctx, int n_edges, int n_patches, int p, const int* e_patch, const int* e_slot,
                       const double* centers, const uint8_t* behind, const float* patch_feats, double* delta,
                       double* weight, uint8_t* flags) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         ensure_p3(p);
         if (ctx->nf == 0) fail(PVO_INVALID_ARGUMENT, "measure_batch: frame store is empty (pvo_frames_reserve)");
@@ -125,7 +125,7 @@ int pvo_measure_batch(pvo_ctx* ctx, int n_edges, int n_patches, int p, const int
 // edge revisions, which the next pvo_window_iteration freezes into targets
 // (pipeline.cpp:183-198: propose -> set_revision -> optimize_window).
 int pvo_window_propose(pvo_ctx* ctx, double* delta_out, double* weight_out, uint8_t* flags_out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         Window& w = ctx->win;
         if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
@@ -165,7 +165,7 @@ int pvo_window_propose(pvo_ctx* ctx, double* delta_out, double* weight_out, uint
 }
 
 int pvo_measure_replayed(pvo_ctx* ctx, int* count) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (!count) fail(PVO_INVALID_ARGUMENT, "measure_replayed: null output");
         *count = 0;
@@ -186,7 +186,7 @@ struct V2Args {  // built as V2Args(a(), b()): the reference's Vec2(gauss(rng_),
 }  // namespace
 
 int pvo_oracle_seed(pvo_ctx* ctx, uint64_t seed) {
-    return guarded([&] { ctx->oracle_rng.seed(seed); });
+    return guarded(__func__, [&] { ctx->oracle_rng.seed(seed); });
 }
 
 // Simulator revisions for every edge of the resident window: ground truth
@@ -199,7 +199,7 @@ int pvo_oracle_seed(pvo_ctx* ctx, uint64_t seed) {
 // the window's deltas / weights (as pvo_window_propose).
 int pvo_window_oracle_propose(pvo_ctx* ctx, const double* gt_poses, const double* gt_inv_depth, double flow_sigma,
                               double outlier_fraction, double* delta_out, double* weight_out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         Window& w = ctx->win;
         if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");

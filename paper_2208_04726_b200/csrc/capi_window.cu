@@ -9,7 +9,7 @@ int pvo_window_load(pvo_ctx* ctx, int n_poses, const double* poses, const uint8_
                     const float* patch_feats, int n_edges, const int* e_patch, const int* e_pose,
                     const double* e_delta, const double* e_weight, const double* K, int image_w, int image_h,
                     int memspace) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (memspace != PVO_HOST) fail(PVO_INVALID_ARGUMENT, "window_load: host arrays expected");
         if (ctx->nf == 0) fail(PVO_INVALID_ARGUMENT, "window_load: frame store is empty (pvo_frames_reserve)");
@@ -58,7 +58,7 @@ int pvo_window_load(pvo_ctx* ctx, int n_poses, const double* poses, const uint8_
 }
 
 int pvo_window_set_state(pvo_ctx* ctx, const double* poses, const double* depth, int memspace) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         Window& w = ctx->win;
         if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
@@ -145,7 +145,7 @@ pvo_dev::BAParams window_ba_params(pvo_ctx* ctx, int iterations, double damping)
 }  // namespace
 
 int pvo_window_correlate(pvo_ctx* ctx, float* out, int memspace) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         Window& w = ctx->win;
         if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
@@ -159,7 +159,7 @@ int pvo_window_correlate(pvo_ctx* ctx, float* out, int memspace) {
 }
 
 int pvo_window_iteration(pvo_ctx* ctx, int iterations, double damping, float* corr_out, int corr_memspace) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         Window& w = ctx->win;
         if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
@@ -222,7 +222,7 @@ int pvo_window_iteration(pvo_ctx* ctx, int iterations, double damping, float* co
 // optimize_window's iterations on the resident window without the correlation
 // pass (the per-frame pipeline: propose -> BA, pipeline.cpp:183-198)
 int pvo_window_ba(pvo_ctx* ctx, int iterations, double damping) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         Window& w = ctx->win;
         if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
@@ -237,7 +237,7 @@ int pvo_window_ba(pvo_ctx* ctx, int iterations, double damping) {
 }
 
 int pvo_window_read(pvo_ctx* ctx, double* poses, double* depth, double* residual_norms, int* n_norms) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         Window& w = ctx->win;
         if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
@@ -268,7 +268,7 @@ int pvo_window_read(pvo_ctx* ctx, double* poses, double* depth, double* residual
 
 int pvo_window_problem_read(pvo_ctx* ctx, double* poses, uint8_t* fixed, int* pose_slot, int* patch_src, double* px,
                             double* py, double* depth, int* e_patch, int* e_pose, double* e_delta, double* e_weight) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         Window& w = ctx->win;
         if (!w.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
@@ -295,7 +295,7 @@ int pvo_window_problem_read(pvo_ctx* ctx, double* poses, uint8_t* fixed, int* po
 }
 
 int pvo_window_corr_ptr(pvo_ctx* ctx, float** corr) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bind(ctx);
         if (!ctx->win.loaded) fail(PVO_INVALID_ARGUMENT, "window: nothing loaded");
         *corr = static_cast<float*>(ctx->win.corr.p);

@@ -225,7 +225,7 @@ void se3_log_host(const double* pose, double* xi) {
 extern "C" {
 
 int pvo_graph_create(const double* K, int w, int h, int p, pvo_graph** out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!out) fail(PVO_INVALID_ARGUMENT, "null output");
         if (p < 1) fail(PVO_INVALID_ARGUMENT, "patch graph: patch width must be >= 1");
         if (K[0] <= 0 || K[1] <= 0) fail(PVO_INVALID_ARGUMENT, "intrinsics: focal lengths must be positive");
@@ -245,7 +245,7 @@ int pvo_graph_destroy(pvo_graph* g) {
 
 // patch_graph.cpp:27-34
 int pvo_graph_add_frame(pvo_graph* g, double ts, const double* pose, int* out_index) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!g->frames.empty() && ts <= g->frames.back().ts) {
             fail(PVO_INVALID_ARGUMENT, "patch graph: timestamp must exceed the last frame's");
         }
@@ -260,7 +260,7 @@ int pvo_graph_add_frame(pvo_graph* g, double ts, const double* pose, int* out_in
 
 // patch_graph.cpp:36-60 + Patch::make (camera.cpp:15-32)
 int pvo_graph_add_patches(pvo_graph* g, int frame, int n, const double* centroids, const double* depths, int* out_ids) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         bool found = false;
         for (const FrameRec& f : g->frames) found = found || f.index == frame;
         if (!found) fail(PVO_INVALID_ARGUMENT, "patch graph: no frame " + std::to_string(frame));
@@ -294,7 +294,7 @@ int pvo_graph_add_patches(pvo_graph* g, int frame, int n, const double* centroid
 
 // patch_graph.cpp:62-85: edge iff |pos(src) - pos(j)| <= r - 1.
 int pvo_graph_connect(pvo_graph* g, int radius, int* n_added) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (radius < 1) fail(PVO_INVALID_ARGUMENT, "patch graph: radius must be >= 1");
         int added = 0;
         const int F = static_cast<int>(g->frames.size());
@@ -324,7 +324,7 @@ int pvo_graph_connect(pvo_graph* g, int radius, int* n_added) {
 
 // patch_graph.cpp:87-128
 int pvo_graph_remove_frame(pvo_graph* g, int frame) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         int pos = -1;
         for (size_t i = 0; i < g->frames.size(); ++i)
             if (g->frames[i].index == frame) pos = static_cast<int>(i);
@@ -358,7 +358,7 @@ int pvo_graph_remove_frame(pvo_graph* g, int frame) {
 
 // patch_graph.cpp:153-164
 int pvo_graph_set_revision(pvo_graph* g, int patch_id, int frame, const double* delta, const double* weight) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         EdgeRec* hit = nullptr;
         for (PatchRec& pt : g->patches) {
             if (pt.id != patch_id) continue;
@@ -381,10 +381,10 @@ int pvo_graph_set_revision(pvo_graph* g, int patch_id, int frame, const double* 
 }
 
 int pvo_graph_set_pose(pvo_graph* g, int frame, const double* pose) {
-    return guarded([&] { std::memcpy(g->frames[g->position(frame)].pose, pose, 7 * sizeof(double)); });
+    return guarded(__func__, [&] { std::memcpy(g->frames[g->position(frame)].pose, pose, 7 * sizeof(double)); });
 }
 int pvo_graph_set_inverse_depth(pvo_graph* g, int patch_id, double d) {
-    return guarded([&] { g->patch(patch_id).d = d; });
+    return guarded(__func__, [&] { g->patch(patch_id).d = d; });
 }
 int pvo_graph_num_frames(pvo_graph* g) { return static_cast<int>(g->frames.size()); }
 int pvo_graph_num_patches(pvo_graph* g) { return static_cast<int>(g->patches.size()); }
@@ -395,7 +395,7 @@ int pvo_graph_num_edges(pvo_graph* g) {
 }
 
 int pvo_graph_edges(pvo_graph* g, int* kk, int* jj, double* rev, uint8_t* has_rev) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         size_t i = 0;
         for (const PatchRec& pt : g->patches) {
             for (const EdgeRec& e : pt.edges) {
@@ -415,7 +415,7 @@ int pvo_graph_edges(pvo_graph* g, int* kk, int* jj, double* rev, uint8_t* has_re
 }
 
 int pvo_graph_frames(pvo_graph* g, int* indices, double* poses) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         for (size_t i = 0; i < g->frames.size(); ++i) {
             indices[i] = g->frames[i].index;
             if (poses) std::memcpy(poses + 7 * i, g->frames[i].pose, 7 * sizeof(double));
@@ -424,7 +424,7 @@ int pvo_graph_frames(pvo_graph* g, int* indices, double* poses) {
 }
 
 int pvo_graph_patches(pvo_graph* g, int* ids, int* src, double* depth) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         for (size_t i = 0; i < g->patches.size(); ++i) {
             ids[i] = g->patches[i].id;
             if (src) src[i] = g->patches[i].src;
@@ -435,7 +435,7 @@ int pvo_graph_patches(pvo_graph* g, int* ids, int* src, double* depth) {
 
 // Pipeline::active_edges (pipeline.cpp:164-181)
 int pvo_graph_active_edges(pvo_graph* g, int window, int* kk, int* jj, int* n) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         int oldest = 0;
         if (!g->frames.empty() && window > 0) {
             const int F = static_cast<int>(g->frames.size());
@@ -458,7 +458,7 @@ int pvo_graph_active_edges(pvo_graph* g, int window, int* kk, int* jj, int* n) {
 
 // build_target (bundle_adjust.cpp:47-60)
 int pvo_graph_build_target(pvo_graph* g, int patch_id, int frame, double* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         const EdgeRec* hit = nullptr;
         const PatchRec* owner = nullptr;
         for (const PatchRec& pt : g->patches) {
@@ -482,7 +482,7 @@ int pvo_graph_build_target(pvo_graph* g, int patch_id, int frame, double* out) {
 int pvo_graph_window_problem(pvo_graph* g, int window, int* n_poses, int* n_patches, int* n_edges, int* pose_frames,
                              double* poses, uint8_t* fixed, int* patch_ids, int* patch_src, double* px, double* py,
                              double* depth, int* e_patch, int* e_pose, double* e_target, double* e_weight) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         Flat f;
         if (!flatten(g, window, f)) {
             *n_poses = *n_patches = *n_edges = 0;
@@ -512,7 +512,7 @@ int pvo_graph_window_problem(pvo_graph* g, int window, int* n_poses, int* n_patc
 // every included depth (:368-373).
 int pvo_optimize_window(pvo_ctx* ctx, pvo_graph* g, int window, int iterations, int structure_only, double damping,
                         double* residual_norms, int* n_norms, int* num_edges) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         Flat f;
         if (n_norms) *n_norms = 0;
         if (num_edges) *num_edges = 0;

@@ -2,10 +2,12 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/pvo_capi.h"
@@ -36,6 +38,35 @@ int guarded(F&& f) {
         set_last_error(e.what());
         return PVO_INVALID_ARGUMENT;
     }
+}
+
+// NVTX range in the "pvo" domain (nvtx3 is header-only; without a profiler
+// attached a push/pop is a null-pointer check).  Every C-ABI entry point
+// opens one named after itself; the launch helpers nest "corr" / "ba" /
+// "measure" / ... inside it, so an nsys / ncu --nvtx timeline shows the
+// reference-facing call and the kernels it issued.
+inline nvtxDomainHandle_t nvtx_domain() {
+    static const nvtxDomainHandle_t d = nvtxDomainCreateA("pvo");
+    return d;
+}
+struct NvtxRange {
+    explicit NvtxRange(const char* name) {
+        nvtxEventAttributes_t ev{};
+        ev.version = NVTX_VERSION;
+        ev.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+        ev.messageType = NVTX_MESSAGE_TYPE_ASCII;
+        ev.message.ascii = name;
+        nvtxDomainRangePushEx(nvtx_domain(), &ev);
+    }
+    ~NvtxRange() { nvtxDomainRangePop(nvtx_domain()); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
+template <typename F>
+int guarded(const char* entry, F&& f) {
+    NvtxRange range(entry);
+    return guarded(std::forward<F>(f));
 }
 
 inline void cuda_check(cudaError_t err, const char* what) {
