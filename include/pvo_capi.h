@@ -245,6 +245,10 @@ int pvo_measure_replayed(pvo_ctx* ctx, int* count);
 int pvo_dgraph_create(pvo_ctx* ctx, const double* K, int image_w, int image_h, int patch_width, int channels,
                       pvo_dgraph** out);
 int pvo_dgraph_destroy(pvo_dgraph* g);
+// Capacity hint (no reference counterpart: the reference's std::vectors grow on
+// the host): size the graph's device buffers for `patches` / `edges` / `frames`
+// so a per-frame loop does not allocate inside a frame; growth past it is automatic.
+int pvo_dgraph_reserve(pvo_dgraph* g, int patches, int edges, int frames);
 int pvo_dgraph_add_frame(pvo_dgraph* g, double timestamp, const double* pose, int frame_slot, int* out_index);
 int pvo_dgraph_add_patches(pvo_dgraph* g, int frame, int n, const double* centroids, const double* inv_depths,
                            const float* feats, int* out_ids);

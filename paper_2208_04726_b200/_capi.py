@@ -76,6 +76,7 @@ SIGNATURES = {
     "pvo_measure_replayed": (i32, [vp, P]),
     "pvo_dgraph_create": (i32, [vp, P, i32, i32, i32, i32, C.POINTER(vp)]),
     "pvo_dgraph_destroy": (i32, [vp]),
+    "pvo_dgraph_reserve": (i32, [vp, i32, i32, i32]),
     "pvo_dgraph_add_frame": (i32, [vp, f64, P, i32, P]),
     "pvo_dgraph_add_patches": (i32, [vp, i32, i32, P, P, P, P]),
     "pvo_dgraph_connect": (i32, [vp, i32, P]),

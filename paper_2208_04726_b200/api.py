@@ -841,6 +841,11 @@ class DeviceGraph:
             lib.pvo_dgraph_destroy(self.handle)
             self.handle = None
 
+    def reserve(self, patches: int, edges: int, frames: int) -> None:
+        """Capacity hint: size the device buffers up front so a per-frame loop does
+        not allocate inside a frame (growth past the hint stays automatic)."""
+        check(lib.pvo_dgraph_reserve(self.handle, int(patches), int(edges), int(frames)))
+
     def add_frame(self, timestamp: float, pose, frame_slot: int = 0) -> int:
         idx = C.c_int()
         check(lib.pvo_dgraph_add_frame(self.handle, float(timestamp), _ptr(_f64(pose, (7,))), int(frame_slot),

@@ -473,9 +473,12 @@ __global__ void __launch_bounds__(kST, 1) bal_solve_kernel(BALargeParams P) {
             for (int kk = 0; kk < kB; ++kk) {
                 if (kk < kb) {
                     const double c = seg[kk];
+                    // fixed trip count: with j = kk + 1 .. the outer loop stayed rolled
+                    // and seg[] went to local memory (STACK 304 B, 600 LDL/STL); columns
+                    // j >= kb are never stored, so they need no guard
 #pragma unroll
-                    for (int j = kk + 1; j < kB; ++j)
-                        if (j < kb) seg[j] -= c * Dg[j * (kB + 1) + kk];
+                    for (int j = 0; j < kB; ++j)
+                        if (j > kk) seg[j] -= c * Dg[j * (kB + 1) + kk];
                     const double inv = dinv[kk];
                     if (inv == 0.0 && c != 0.0 && i < np) fail = true;
                     Wp[kk * pr_cap + t] = c;

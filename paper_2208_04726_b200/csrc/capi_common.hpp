@@ -216,11 +216,19 @@ struct pvo_ctx {
     size_t h_stage_cap = 0;
     void* stage(size_t bytes) {
         if (bytes > h_stage_cap) {
+            // same headroom policy as DevBuf::get: page-locking is the costliest allocation
+            if (h_stage_cap)
+                bytes = std::max(bytes, std::min(h_stage_cap + h_stage_cap / 2, bytes + (size_t(256) << 20)));
+            const auto t0 = std::chrono::steady_clock::now();
             if (h_stage) cudaFreeHost(h_stage);
             h_stage = nullptr;
+            const size_t old = h_stage_cap;
             h_stage_cap = 0;
             cuda_check(cudaMallocHost(&h_stage, bytes), "cudaMallocHost");
             h_stage_cap = bytes;
+            if (pvo_host::DevBuf::trace_alloc())
+                std::fprintf(stderr, "[pvo alloc] pinned staging %zu -> %zu bytes, %.3f ms\n", old, bytes,
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
         }
         return h_stage;
     }

@@ -43,21 +43,22 @@ struct pvo_dgraph {
         v.e_rev = static_cast<double*>(e_rev[b].p);
         return v;
     }
+    // grow d to at least `bytes` (doubling), preserving its contents
+    void grow(DevBuf& d, size_t bytes) {
+        if (bytes <= d.cap) return;
+        DevBuf n;
+        n.get(std::max(bytes, 2 * d.cap));
+        // zero the new allocation first: the copy below moves the old capacity, whose
+        // tail past the live entries was never written (compute-sanitizer initcheck)
+        cuda_check(cudaMemsetAsync(n.p, 0, n.cap, ctx->stream), "grow");
+        if (d.p) cuda_check(cudaMemcpyAsync(n.p, d.p, d.cap, cudaMemcpyDeviceToDevice, ctx->stream), "grow");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "grow");
+        d.release();
+        d = n;
+        n.p = nullptr;
+    }
     // grow buffer set b to hold np patches / ne edges, preserving contents
     void reserve(int b, int np, int ne) {
-        auto grow = [&](DevBuf& d, size_t bytes) {
-            if (bytes <= d.cap) return;
-            DevBuf n;
-            n.get(std::max(bytes, 2 * d.cap));
-            // zero the new allocation first: the copy below moves the old capacity, whose
-            // tail past the live entries was never written (compute-sanitizer initcheck)
-            cuda_check(cudaMemsetAsync(n.p, 0, n.cap, ctx->stream), "grow");
-            if (d.p) cuda_check(cudaMemcpyAsync(n.p, d.p, d.cap, cudaMemcpyDeviceToDevice, ctx->stream), "grow");
-            cuda_check(cudaStreamSynchronize(ctx->stream), "grow");
-            d.release();
-            d = n;
-            n.p = nullptr;
-        };
         grow(p_id[b], 4 * (size_t)std::max(np, 1));
         grow(p_src[b], 4 * (size_t)std::max(np, 1));
         grow(p_x[b], 8 * 9 * (size_t)std::max(np, 1));
@@ -104,6 +105,36 @@ int pvo_dgraph_create(pvo_ctx* ctx, const double* K, int w, int h, int p, int ch
         g->reserve(0, 64, 64);
         cuda_check(cudaMemsetAsync(g->ebeg[0].p, 0, sizeof(int), ctx->stream), "memset");
         *out = g;
+    });
+}
+
+// Capacity hint: size every graph buffer (both buffer sets, the frame arrays and
+// the pass scratch) for `patches` patches, `edges` edges and `frames` frames up
+// front, so a long-running per-frame loop never allocates inside a frame (a
+// cudaMalloc can stall the host for milliseconds, and cudaFree synchronises the
+// device).  Growth past the hint stays automatic.
+int pvo_dgraph_reserve(pvo_dgraph* g, int patches, int edges, int frames) {
+    return guarded(__func__, [&] {
+        if (!g) fail(PVO_INVALID_ARGUMENT, "null graph");
+        pvo_ctx* ctx = g->ctx;
+        bind(ctx);
+        if (patches < 0 || edges < 0 || frames < 0) fail(PVO_INVALID_ARGUMENT, "dgraph reserve: negative capacity");
+        for (int b = 0; b < 2; ++b) g->reserve(b, std::max(patches, g->P), std::max(edges, g->E));
+        const size_t F = std::max<size_t>((size_t)frames, g->f_index.size()) + 1;
+        g->grow(g->f_pose_d, 8 * 7 * F);
+        g->grow(g->f_idx_d, 4 * F);
+        g->grow(g->f_slot_d, 4 * F);
+        const size_t P1 = (size_t)std::max(patches, g->P) + 1;
+        DevBuf* scratch[] = {&g->t0, &g->t1, &g->t2, &g->t3};
+        for (DevBuf* t : scratch) t->get(4 * P1);
+        g->t4.get(std::max(8 * P1, 8 * 7 * F));
+        g->missing.get(4);
+        g->w_nfixed.get(4);
+        g->w_pose_frames.get(4 * F);
+        g->w_fixed.get(F);
+        g->w_patch_ids.get(4 * P1);
+        g->w_e_graph.get(4 * ((size_t)std::max(edges, g->E) + 1));
+        sync(ctx);
     });
 }
 

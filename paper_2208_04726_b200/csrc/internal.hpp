@@ -4,7 +4,11 @@
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
 
+#include <algorithm>
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -81,12 +85,25 @@ struct DevBuf {
     void* get(size_t bytes) {
         if (bytes == 0) bytes = 16;
         if (bytes > cap) {
+            // a regrown buffer gets 1.5x headroom (at most +256 MiB): buffers that track a
+            // growing graph (one more frame of patches / edges per call) would otherwise be
+            // freed and reallocated on every call — cudaFree synchronises the device, and
+            // the driver's (un)mapping made the per-frame pipeline's host time spiky
+            if (cap) bytes = std::max(bytes, std::min(cap + cap / 2, bytes + (size_t(256) << 20)));
+            const auto t0 = std::chrono::steady_clock::now();
             if (p) cudaFree(p);
             p = nullptr;
             cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+            if (trace_alloc())
+                std::fprintf(stderr, "[pvo alloc] %zu -> %zu bytes, %.3f ms\n", cap, bytes,
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
             cap = bytes;
         }
         return p;
+    }
+    static bool trace_alloc() {  // PVO_TRACE_ALLOC=1: log every (re)allocation to stderr
+        static const bool on = std::getenv("PVO_TRACE_ALLOC") != nullptr;
+        return on;
     }
     template <typename T>
     T* as(size_t count) {

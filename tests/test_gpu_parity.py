@@ -719,10 +719,12 @@ def test_device_graph_matches_host_graph(ctx):
         assert np.array_equal(got["e_delta"], hr[rows, :2]) and np.array_equal(got["e_weight"], hr[rows, 2:])
 
 
-def test_device_graph_window_loop_matches_host_path(ctx):
+@pytest.mark.parametrize("reserve", [False, True])
+def test_device_graph_window_loop_matches_host_path(ctx, reserve):
     """Per-frame loop on the device graph: flatten -> corr + BA (identical to the
     host-flattened window, bit for bit) -> write-back; propose -> revisions
-    stored into the graph's edges."""
+    stored into the graph's edges.  With `reserve` the buffers are sized up front
+    (pvo_dgraph_reserve) and must not change a bit of the results."""
     w = synth.generate("c1", seed=21, frames=6, patches=24)
     F, M = w.cfg["frames"], w.cfg["patches"]
     _, H0, W0, D = w.level0.shape
@@ -731,6 +733,8 @@ def test_device_graph_window_loop_matches_host_path(ctx):
     for f in range(F):
         ctx.frames_upload(f, w.level0[f], w.level1[f])
     dev = pvo.DeviceGraph(ctx, w.K, w.image[0], w.image[1], channels=D)
+    if reserve:
+        dev.reserve(patches=F * M, edges=F * M * F, frames=F)
     for f in range(F):
         dev.add_frame(0.05 * f, w.poses[f], frame_slot=f)
         ks = slice(f * M, (f + 1) * M)

@@ -40,15 +40,19 @@ ctx.set_stream(stream.cuda_stream)
 NS = 32  # frame-store ring: the window plus every frame its edges still reach
 ctx.frames_reserve(NS, W0, H0, W1, H1, D)
 dev = pvo.DeviceGraph(ctx, w.K, w.image[0], w.image[1], channels=D)
+if "--no-reserve" not in sys.argv:  # size the graph once: no allocation inside a frame
+    dev.reserve(patches=F * M, edges=F * M * (2 * w.cfg["radius"] + 1), frames=F)
 if not images:
     l0 = [torch.from_numpy(w.level0[f]).pin_memory() for f in range(F)]
     l1 = [torch.from_numpy(w.level1[f]).pin_memory() for f in range(F)]
 stages = ["frame (H2D/extract+Gram)", "graph add + connect", "flatten", "propose", "BA (2 it.)", "store"]
 acc = {s: [] for s in stages}
-walls, edges = [], []
+walls, edges, attempts, host_ms = [], [], [], []
 with torch.cuda.stream(stream):
     for f in range(F):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)]
+        if "--spikes" in sys.argv:
+            print(f"[frame {f}]", file=sys.stderr, flush=True)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         ev[0].record(stream)
@@ -60,13 +64,16 @@ with torch.cuda.stream(stream):
             ctx.frames_upload(f % NS, l0[f].numpy(), l1[f].numpy())
             feats = w.patch_feats[ks]
         ev[1].record(stream)
+        th = [time.perf_counter()]
         idx = dev.add_frame(0.05 * (f + 1), w.poses[f], frame_slot=f % NS)
         dev.add_patches(idx, w.centroids[ks], w.depth[ks], feats)
         dev.connect(w.cfg["radius"])
+        th.append(time.perf_counter())
         ev[2].record(stream)
         # every active edge (pipeline.cpp:164-181); after propose all of them are revised,
         # so this window is also optimize_window's problem (bundle_adjust.cpp:245)
         n = dev.load_window(w.cfg["window"], all_active=True)
+        th.append(time.perf_counter())
         ev[3].record(stream)
         dev.window.propose(read_back=False)
         ev[4].record(stream)
@@ -77,6 +84,8 @@ with torch.cuda.stream(stream):
         ev[6].synchronize()
         walls.append(time.perf_counter() - t0)
         edges.append(n[2])
+        attempts.append(ctx.ba_attempts)  # GN attempts of this frame's BA (guard retries included)
+        host_ms.append((1e3 * (th[1] - th[0]), 1e3 * (th[2] - th[1])))
         if f >= F // 2:
             for i, s in enumerate(stages):
                 acc[s].append(ev[i].elapsed_time(ev[i + 1]))
@@ -92,5 +101,14 @@ for s in stages:
     tot += m
     totm += md
     print(f"  {s:22s} {m:8.3f} ms   (median {md:.3f}, max {float(np.max(acc[s])):.3f})")
+print(f"  divergence guard: {sum(attempts) - 2 * len(attempts)} retries over {2 * len(attempts)} GN iterations")
 print(f"  {'device total':22s} {tot:8.3f} ms   (median {totm:.3f})   host wall per frame "
       f"{1e3 * np.mean(walls[F // 2:]):.3f} ms")
+if "--spikes" in sys.argv:  # frames whose graph stages took > 3x the median (device events + host wall)
+    half = F // 2
+    for s_i, s in ((0, stages[1]), (1, stages[2])):
+        med = float(np.median(acc[s]))
+        for j, v in enumerate(acc[s]):
+            if v > 3 * med:
+                print(f"  spike: frame {half + j} {s}: {v:.3f} ms device-event span, "
+                      f"{host_ms[half + j][s_i]:.3f} ms host wall in the calls")
