@@ -799,19 +799,57 @@ __device__ __noinline__ void subpixel_peak_gram(MeasWarpSmem& S, const Level& L,
     }
     const int qx = (int)floor(bx + dx) - 2, qy = (int)floor(by + dy) - 2;
     __syncwarp();  // the slice Gram buffer is reused for the climb window
-    for (int q = lane; q < 36; q += 32) {
-        const int x = qx + q % 6, y = qy + q / 6;
-        const int sx = x - ox, sy = y - oy;  // inside the slice window: its dot is already there
-        const bool in = x >= 0 && y >= 0 && x < L.W && y < L.H;
-        S.u.climb.d[q] = (sx >= 0 && sx < 8 && sy >= 0 && sy < 8) ? S.sd[sy * 8 + sx]
-                         : in                                     ? cell_dot(S.g, L.f + ((size_t)y * L.W + x) * C, C)
-                                                                  : 0.0;
+    {  // cells lane and lane + 32 (lanes 0-3); dots outside the slice window computed
+       // here, a lane's two fresh cells together (one load stream pair in flight)
+        int cx[2], cy[2], kind[2];  // kind: 0 zero padding, 1 slice dot, 2 fresh dot
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int q = lane + 32 * h;
+            cx[h] = qx + q % 6;
+            cy[h] = qy + q / 6;
+            const int sx = cx[h] - ox, sy = cy[h] - oy;
+            const bool in = q < 36 && cx[h] >= 0 && cy[h] >= 0 && cx[h] < L.W && cy[h] < L.H;
+            kind[h] = !in ? 0 : (sx >= 0 && sx < 8 && sy >= 0 && sy < 8) ? 1 : 2;
+        }
+        double dv[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+            dv[h] = kind[h] == 1 ? S.sd[(cy[h] - oy) * 8 + cx[h] - ox] : 0.0;
+        const float* f0 = L.f + ((size_t)cy[0] * L.W + cx[0]) * C;
+        const float* f1 = L.f + ((size_t)cy[1] * L.W + cx[1]) * C;
+        if (kind[0] == 2 && kind[1] == 2)
+            cell_dot2(S.g, f0, f1, C, &dv[0], &dv[1]);
+        else if (kind[0] == 2)
+            dv[0] = cell_dot(S.g, f0, C);
+        else if (kind[1] == 2)
+            dv[1] = cell_dot(S.g, f1, C);
+        S.u.climb.d[lane] = dv[0];
+        if (lane < 4) S.u.climb.d[lane + 32] = dv[1];
     }
-    for (int t = lane; t < 36 * kGram25; t += 32) {
-        const int q = t / kGram25, m = t - q * kGram25;
-        const int x = qx + q % 6, y = qy + q / 6;
-        const bool in = x >= 0 && y >= 0 && x < L.W && y < L.H;
-        S.u.climb.gr[q][m] = in ? __ldg(gm + ((size_t)y * L.W + x) * kGram25 + m) : 0.0;
+    // the window's Gram records: each window row is 6 x 25 contiguous doubles of
+    // the map, 5 coalesced loads per lane; three rows (15 loads) in flight per batch
+    // (a load-store loop kept one L2 round trip per element in flight)
+    constexpr int kRowG = 6 * kGram25, kPerRow = (kRowG + 31) / 32;
+#pragma unroll 1
+    for (int r0 = 0; r0 < 6; r0 += 3) {
+        double tv[3][kPerRow];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            const int y = qy + r0 + r;
+#pragma unroll
+            for (int i = 0; i < kPerRow; ++i) {
+                const int j = lane + 32 * i, x = qx + j / kGram25;
+                const bool in = j < kRowG && x >= 0 && y >= 0 && x < L.W && y < L.H;
+                tv[r][i] = in ? __ldg(gm + ((size_t)y * L.W + qx) * kGram25 + j) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int i = 0; i < kPerRow; ++i) {
+                const int j = lane + 32 * i;
+                if (j < kRowG) (&S.u.climb.gr[(r0 + r) * 6][0])[j] = tv[r][i];
+            }
     }
     __syncwarp();
     int off[16];
@@ -957,15 +995,22 @@ __device__ __forceinline__ MeasRecord measure_task(const MeasureParams& a, MeasW
                 S.sd[lane] = in0 ? d0 : 0.0;
                 S.sd[lane + 32] = in1 ? d1 : 0.0;
             }
-            for (int q = lane; q < 64; q += 32) {
-                const int x = ox + (q & 7), y = oy + (q >> 3);
-                const bool in = x >= 0 && y >= 0 && x < L.W && y < L.H;
-                const double* gc = gm + (in ? (size_t)y * L.W + x : 0) * kGram25;
-                S.u.sgr[q][0] = in ? __ldg(gc + g25_index(0, 0)) : 0.0;
-                S.u.sgr[q][1] = in ? __ldg(gc + g25_index(1, 0)) : 0.0;
-                S.u.sgr[q][2] = in ? __ldg(gc + g25_index(0, 1)) : 0.0;
-                S.u.sgr[q][3] = in ? __ldg(gc + g25_index(1, 1)) : 0.0;
-                S.u.sgr[q][4] = in ? __ldg(gc + g25_index(-1, 1)) : 0.0;
+            {  // the slice window's Gram terms, both cells' ten loads in flight together
+                constexpr int kG5[5] = {g25_index(0, 0), g25_index(1, 0), g25_index(0, 1), g25_index(1, 1),
+                                        g25_index(-1, 1)};
+                double tv[2][5];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int q = lane + 32 * h, x = ox + (q & 7), y = oy + (q >> 3);
+                    const bool in = x >= 0 && y >= 0 && x < L.W && y < L.H;
+                    const double* gc = gm + (in ? (size_t)y * L.W + x : 0) * kGram25;
+#pragma unroll
+                    for (int m = 0; m < 5; ++m) tv[h][m] = in ? __ldg(gc + kG5[m]) : 0.0;
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int m = 0; m < 5; ++m) S.u.sgr[lane + 32 * h][m] = tv[h][m];
             }
             __syncwarp();
         }
