@@ -66,8 +66,11 @@ struct Plan {
 // pose, cut to <= 64 patches; the window of a run = the free pose slots its
 // patches touch (source + edge targets).  The reduced system's half-bandwidth
 // is the widest window - 1 (patch_graph.cpp:79 keeps edges within the radius).
+#ifndef PVO_GROUP_PATCHES
+#define PVO_GROUP_PATCHES 64
+#endif
 inline void plan_groups(const HostProblem& pr, Plan& pl) {
-    constexpr int kGroupPatches = 64;
+    constexpr int kGroupPatches = PVO_GROUP_PATCHES;  // A/B knob (assemble CTAs per run)
     pl.g_begin.assign(1, 0);
     pl.patch_group.assign(pr.n_patches, 0);
     int k = 0;
