@@ -380,6 +380,10 @@ __global__ void bal_reduce_kernel(BALargeParams P) {
 // ---------------------------------------------------------------------------
 // solve: banded blocked LDL^T + back-substitution + retraction (one CTA)
 // ---------------------------------------------------------------------------
+// A/B knob: the diagonal block factored by one warp (1) or four (4)
+#ifndef PVO_BAL_DIAG_WARPS
+#define PVO_BAL_DIAG_WARPS 4
+#endif
 __global__ void __launch_bounds__(kST, 1) bal_solve_kernel(BALargeParams P) {
     if (P.ctrl[0] || P.ctrl[2]) return;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -418,6 +422,68 @@ __global__ void __launch_bounds__(kST, 1) bal_solve_kernel(BALargeParams P) {
         const int nr = r1 - r0 + 1;
         // (1) diagonal block, warp 0: lane = row, the row in registers (loads issued
         //     together), the unscaled pivot column broadcast through shared memory
+#if PVO_BAL_DIAG_WARPS == 4
+        // (A/B variant) four warps: lane = row, warp w holds columns 8w .. 8w+7 of
+        // it; per pivot the owner warp publishes d_kk, 1/d_kk and the column into
+        // a double-buffered slot, one 128-thread named barrier, then every warp
+        // updates its columns (the same expressions as the one-warp form)
+        if (warp < 4) {
+            constexpr int kCW = kB / 4;
+            __shared__ double ccw[2][kB + 1];
+            double r[kCW];
+#pragma unroll
+            for (int c = 0; c < kCW; ++c) {
+                const int j = kCW * warp + c;
+                r[c] = (lane < kb && j <= lane) ? A[(size_t)(k0 + lane) * ld + k0 + j] : 0.0;
+            }
+            bool fail = false, zero = false;
+#pragma unroll 1
+            for (int kk = 0; kk < kb; ++kk) {
+                const int ow = kk / kCW, oc = kk - kCW * ow;
+                double* cb = ccw[kk & 1];
+                const bool below = lane > kk && lane < kb;
+                bool vk = true;  // the owner's pivot test (its column kk is written by it alone)
+                if (warp == ow) {
+                    double rk = 0.0;
+#pragma unroll
+                    for (int c = 0; c < kCW; ++c)
+                        if (c == oc) rk = r[c];
+                    const double dk = __shfl_sync(0xffffffffu, rk, kk);
+                    const bool valid = fabs(dk) > 0.0;
+                    vk = valid;
+                    if (k0 + kk == 0 && !valid) zero = true;  // Eigen: all-zero diagonal -> x = 0
+                    const double inv = valid ? 1.0 / dk : 0.0;
+                    const double ci = below ? rk : 0.0;
+                    if (below && !valid && ci != 0.0) fail = true;
+                    cb[lane] = ci;
+                    if (lane == 0) {
+                        cb[kB] = inv;
+                        dinv[kk] = inv;
+                    }
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                const double inv = cb[kB];
+                const double ci = cb[lane];
+                const double cs = ci * inv;
+#pragma unroll
+                for (int c = 0; c < kCW; ++c) {
+                    const int j = kCW * warp + c;
+                    if (below && j > kk && j <= lane) r[c] -= cs * cb[j];
+                    if (below && j == kk) r[c] = vk ? cs : ci;
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < kCW; ++c) {
+                const int j = kCW * warp + c;
+                if (lane < kb && j <= lane) {
+                    Dg[lane * (kB + 1) + j] = r[c];
+                    A[(size_t)(k0 + lane) * ld + k0 + j] = r[c];
+                }
+            }
+            if (__any_sync(0xffffffffu, fail) && lane == 0) s_fail = 1;
+            if (__any_sync(0xffffffffu, zero) && lane == 0) s_zero = 1;
+        }
+#else
         if (warp == 0) {
             double r[kB];
 #pragma unroll
@@ -455,6 +521,7 @@ __global__ void __launch_bounds__(kST, 1) bal_solve_kernel(BALargeParams P) {
             if (__any_sync(0xffffffffu, fail) && lane == 0) s_fail = 1;
             if (__any_sync(0xffffffffu, zero) && lane == 0) s_zero = 1;
         }
+#endif
         __syncthreads();
         if (pc) {
             const long long t = clock64();
